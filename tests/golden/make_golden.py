@@ -1,0 +1,142 @@
+"""Generate golden vectors from the *reference* implementation.
+
+Run in the build container (the reference is importable there, read-only):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--big]
+
+For every case the reference package ``hifde`` assembles the matrix, factors
+it (``factor_hifde`` / ``factor_hifde3x`` / ``factor_mf``, src/driver.py:201-251),
+solves seeded right-hand sides (``apply_inverse``, src/driver.py:113-129) and
+runs PCG at tol 1e-12 with its own factor (src/krylov.py:48-77).  The outputs
+are committed as small ``.npz`` fixtures; ``/root/reference`` never has to
+exist where the tests run.  Coefficient fields for the BASELINE "gauss" cases
+are built here with numpy/scipy (Gaussian noise, sigma 4h, threshold 0 --
+SURVEY.md section 8(d)) and handed to the reference's ``CoeffField`` /
+``assemble`` so the reference defines the matrix.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CASES = [
+    # name, dim, n(ref grid arg), m, eps, variant, field, seed, nrhs, store_vectors
+    ("g2d_n16_m2", 2, 16, 2, 1e-6, "hifde", "const", 0, 2, True),
+    ("g2d_n32_m4", 2, 32, 4, 1e-6, "hifde", "const", 0, 2, True),
+    ("g2d_n64_m4_hc", 2, 64, 4, 1e-9, "hifde", "median", 5, 2, True),
+    ("g2d_n64_m8_gauss", 2, 64, 8, 1e-9, "hifde", "gauss", 0, 4, True),
+    ("g2d_cfg1", 2, 128, 8, 1e-6, "hifde", "const", 0, 1, True),
+    ("g2d_n32_m4_mf", 2, 32, 4, 0.0, "mf", "const", 0, 2, True),
+    ("g2d_n32_m4_skip2", 2, 32, 4, 1e-6, "hifde", "const", 0, 1, True, 2),
+    ("g3d_n8_m2", 3, 8, 2, 1e-6, "hifde", "const", 0, 2, True),
+    ("g3d_n16_m2_x", 3, 16, 2, 1e-6, "hifde3x", "const", 0, 2, True),
+    ("g3d_n16_m4_x_hc", 3, 16, 4, 1e-3, "hifde3x", "median", 0, 2, True),
+    ("g3d_n16_m4_x_gauss", 3, 16, 4, 1e-3, "hifde3x", "gauss", 0, 2, True),
+    ("g3d_n32_m4_x", 3, 32, 4, 1e-6, "hifde3x", "const", 0, 1, False),
+]
+
+BIG_CASES = [
+    ("cfg2", 2, 512, 8, 1e-9, "hifde", "gauss", 0, 16, False),
+    ("cfg4", 3, 64, 4, 1e-6, "hifde3x", "const", 0, 16, False),
+]
+
+
+def _gauss_field(hifde, g, seed):
+    from scipy.ndimage import gaussian_filter
+    rng = np.random.default_rng(seed)
+    a = []
+    for ax in range(g.dim):
+        shape = tuple(g.n if i == ax else g.n - 1 for i in range(g.dim))
+        s = gaussian_filter(rng.standard_normal(shape), sigma=4.0, mode="reflect",
+                            truncate=4.0)
+        a.append(np.where(s <= 0.0, 1e-2, 1e2))
+    return hifde.CoeffField(tuple(a), np.zeros((g.n - 1,) * g.dim))
+
+
+def csr_digest(csr) -> str:
+    h = hashlib.sha256()
+    for arr in (csr.indptr.astype(np.int64), csr.indices.astype(np.int64),
+                csr.data.astype(np.float64)):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()
+
+
+def run_case(hifde, case):
+    name, dim, n, m, eps, variant, fld, seed, nrhs, vectors = case[:10]
+    skip = case[10] if len(case) > 10 else None
+    g = hifde.build_grid(dim, n, m)
+    if fld == "const":
+        field = hifde.constant_field(g, 1.0, 0.0)
+    elif fld == "median":
+        field = hifde.high_contrast_field(g, seed)
+    else:
+        field = _gauss_field(hifde, g, seed)
+    a = hifde.assemble(g, field)
+    csr = a.to_scipy()
+    csr.sort_indices()
+    t0 = time.perf_counter()
+    kw = {} if skip is None else {"skip_levels": skip}
+    if variant == "mf":
+        f = hifde.factor_mf(a, g)
+    elif variant == "hifde":
+        f = hifde.factor_hifde(a, g, eps, **kw)
+    else:
+        f = hifde.factor_hifde3x(a, g, eps, **kw)
+    tf = time.perf_counter() - t0
+    tags, ranks, reds = [], [], []
+    for lf in f.levels:
+        if abs(lf.level - round(lf.level)) > 1e-9:
+            tags.append(lf.level)
+            ranks.append(sum(len(r.sk) for r in lf.records))
+            reds.append(sum(len(r.rd) for r in lf.records))
+    b = np.random.default_rng(1).standard_normal((g.ndof, nrhs))
+    x = f.apply_inverse(b)
+    resid = np.linalg.norm(csr @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    xa = np.random.default_rng(2).standard_normal(g.ndof)
+    ax = csr @ xa
+    apply_err = float(np.linalg.norm(f.apply(xa) - ax) / np.linalg.norm(ax))
+    rep = hifde.pcg(csr, b[:, 0], f.apply_inverse, tol=1e-12)
+    out = dict(
+        dim=dim, n=n, m=m, eps=eps, variant=variant, field=fld, seed=seed,
+        skip_levels=-1 if skip is None else skip, nrhs=nrhs,
+        csr_sha256=csr_digest(csr), nnz=csr.nnz,
+        skel_tags=np.array(tags), skel_ranks=np.array(ranks, dtype=np.int64),
+        skel_redundant=np.array(reds, dtype=np.int64),
+        level_tags=np.array([lf.level for lf in f.levels]),
+        trace=np.array([t[1] for t in f.metrics["active_trace"]], dtype=np.int64),
+        s_top=f.metrics["s_top"], m_f_bytes=f.metrics["m_f_bytes"],
+        oneshot_resid=resid, apply_err=apply_err,
+        pcg_iters=rep.n_i, pcg_resid=rep.residual, t_f_ref=tf,
+    )
+    if vectors:
+        out["x_oneshot"] = x
+        out["u_pcg"] = rep.x
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: N={g.ndof} t_f={tf:.2f}s s_L={out['s_top']} ranks={ranks} "
+          f"resid={resid.max():.2e} pcg={rep.n_i}", flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true", help="also run configs 2 and 4")
+    ap.add_argument("--only", default=None)
+    args = ap.parse_args()
+    sys.path.insert(0, os.environ.get("HIFDE_REF_SRC", "/root/reference/pkg/src"))
+    import hifde
+    cases = CASES + (BIG_CASES if args.big else [])
+    for case in cases:
+        if args.only and case[0] != args.only:
+            continue
+        run_case(hifde, case)
+
+
+if __name__ == "__main__":
+    main()
