@@ -1,0 +1,155 @@
+/*
+ * hifde_gpu.h -- C ABI of the B200-native HIF-DE factor/solve hot path.
+ *
+ * The reference (hifde 0.1.0, /root/reference/pkg/src/hifde) is a pure-Python
+ * package with no FFI.  These entry points replace, one for one, the Python
+ * functions on its hot path; the Python shim in paper_1307_2895_b200/driver.py
+ * binds them with ctypes and keeps the reference's names and signatures:
+ *
+ *   hifde_factor   <- factor_hifde   (src/driver.py:212-225)
+ *                     factor_hifde3x (src/driver.py:228-251)
+ *                     factor_mf      (src/driver.py:201-209)
+ *   hifde_solve    <- GeneralizedLDL.apply_inverse (src/driver.py:113-129)
+ *                     and module-level apply_inverse (src/driver.py:258-259)
+ *   hifde_get_info / hifde_get_level
+ *                  <- GeneralizedLDL.metrics (src/driver.py:165-171)
+ *   hifde_free     <- (Python GC of the factor object)
+ *   hifde_last_error
+ *                  <- the exception message (FactorizationError family,
+ *                     src/dense.py:41-50; cell context as in
+ *                     src/factor_ops.py:193-200)
+ *
+ * Status codes map onto the reference's exception classes:
+ *   HIFDE_OK 0, HIFDE_INDEFINITE 1 (IndefiniteBlockError),
+ *   HIFDE_SINGULAR 2 (SingularBlockError), HIFDE_BADARG 3 (ValueError),
+ *   HIFDE_CUDA 4 (RuntimeError), HIFDE_INTERNAL 5 (AssertionError).
+ *
+ * Plain C types only: no torch or CUDA types cross this boundary (the stream
+ * is an opaque pointer to a cudaStream_t, NULL for the library's own).
+ */
+#ifndef HIFDE_GPU_H
+#define HIFDE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HIFDE_OK 0
+#define HIFDE_INDEFINITE 1
+#define HIFDE_SINGULAR 2
+#define HIFDE_BADARG 3
+#define HIFDE_CUDA 4
+#define HIFDE_INTERNAL 5
+
+/* factorization variants (the reference's "skeletonize-fronts" switch) */
+#define HIFDE_VARIANT_MF 0      /* factor_mf: elimination only, exact      */
+#define HIFDE_VARIANT_HIFDE 1   /* factor_hifde: edges (2D) / faces (3D)   */
+#define HIFDE_VARIANT_HIFDE3X 2 /* factor_hifde3x: faces + edges (3D)      */
+
+/* ordering of the groups of one skeletonization level */
+#define HIFDE_ORDER_AUTO 0      /* exact reference order when cheap        */
+#define HIFDE_ORDER_SNAPSHOT 1  /* all IDs of a level from one snapshot    */
+#define HIFDE_ORDER_EXACT 2     /* reference's sequential semantics        */
+
+typedef struct hifde_options {
+  int variant;          /* HIFDE_VARIANT_*                                  */
+  int skip_levels;      /* skeletonization skipped below this level         */
+  int spd;              /* 1: Cholesky mode (the only mode implemented)     */
+  int order_mode;       /* HIFDE_ORDER_*                                    */
+  int exact_max_batches;/* AUTO: exact order when the level needs <= this   */
+  int device;           /* CUDA device ordinal                              */
+  int input_on_device;  /* CSR arrays are device pointers                   */
+  int verify;           /* 1: check cells of each level are non-interacting */
+  double eps;           /* ID relative tolerance (0 -> exact rank)          */
+  void* stream;         /* cudaStream_t or NULL                             */
+} hifde_options_t;
+
+typedef struct hifde_factor hifde_factor_t;
+
+typedef struct hifde_info {
+  int64_t n;            /* matrix order N                                   */
+  int32_t dim;
+  int32_t nlevels;      /* number of level records (integer + fractional)   */
+  int64_t s_top;        /* size of the terminal dense block                 */
+  int64_t m_f_bytes;    /* 8 * nfloats, the reference's accounting          */
+  int64_t device_bytes; /* bytes actually held on the device by the factor  */
+  double t_f_seconds;   /* host wall time of hifde_factor                   */
+  double eps;
+  int32_t spd;
+  int32_t variant;
+} hifde_info_t;
+
+typedef struct hifde_level_info {
+  double tag;           /* level tag: l, l+1/2, l+1/3, l+2/3                */
+  int32_t kind;         /* 0 elimination, 1 skeletonization                 */
+  int32_t nbatches;     /* launches used (exact-order batches)              */
+  int64_t ngroups;      /* cells / groups                                   */
+  int64_t nskel;        /* sum |sk| (skeleton levels)                       */
+  int64_t nredundant;   /* sum |rd| (skeleton levels)                       */
+  int64_t active_after; /* active DOFs after the level (active_trace)       */
+  int64_t max_front;    /* largest |c|+|q|                                  */
+  double seconds;       /* host wall time of the level                      */
+  double gflop;         /* algorithmic FLOPs of the level     */
+  double gbytes;        /* algorithmic bytes of the level     */
+} hifde_level_info_t;
+
+/* Library version string. */
+const char* hifde_version(void);
+
+/* Number of visible CUDA devices (0 if no driver / no GPU). */
+int hifde_device_count(void);
+
+/* Fill *opt with the reference defaults for `variant`
+ * (skip_levels 0 for MF/HIFDE, 1 for HIFDE3X; spd 1; AUTO ordering). */
+void hifde_default_options(hifde_options_t* opt, int variant);
+
+/*
+ * Factor the symmetric matrix A given as full symmetric CSR
+ * (indptr[n+1] int64, indices[nnz] int32, vals[nnz] float64; what
+ * SparseSymMatrix.to_scipy() returns, src/sparse.py:105-111) on the
+ * uniform grid (dim, n_grid, m_leaf, nlevels) of GridConfig
+ * (src/discretize.py:43-74).  A is not modified.
+ */
+int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* vals,
+                 int64_t n, int dim, int n_grid, int m_leaf, int nlevels,
+                 const hifde_options_t* opt, hifde_factor_t** out);
+
+/*
+ * x = F^{-1} b for an n x nrhs block stored row-major (C order, ld = nrhs),
+ * b and x on the host (device_ptrs = 0) or the device (device_ptrs = 1).
+ * Reentrant for a finished factor; b and x may alias.
+ */
+int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n,
+                int nrhs, int device_ptrs, void* stream);
+
+int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info);
+int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info);
+
+/* Number of kernel launches issued by the last hifde_factor / hifde_solve
+ * on this thread (the bench's gpu_launches count). */
+int64_t hifde_last_launch_count(void);
+
+void hifde_free(hifde_factor_t* f);
+
+/* Thread-local message describing the last non-zero status. */
+const char* hifde_last_error(void);
+
+/*
+ * Host-only partition hook (no GPU needed): groups of `level_kind`
+ * (0 interior, 1 interface-edge, 2 interface-face) at level `ell` over the
+ * DOFs with active[i] != 0, in the reference's order
+ * (src/partition.py:68-181).  Writes the member DOFs group after group into
+ * members[] and the group offsets into offsets[ngroups+1]; returns the number
+ * of groups, or -1 if the capacities are too small.
+ */
+int64_t hifde_partition(int dim, int n_grid, int m_leaf, int ell, int level_kind,
+                        const uint8_t* active, int32_t* members, int64_t members_cap,
+                        int64_t* offsets, int64_t offsets_cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HIFDE_GPU_H */

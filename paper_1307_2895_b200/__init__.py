@@ -1,0 +1,15 @@
+"""B200-native HIF-DE factor/solve (arXiv 1307.2895) behind the reference's API.
+
+The hot path (level sweep of eliminations and ID skeletonizations, and the
+apply_inverse sweep) runs in hand-written sm_100a CUDA kernels in
+``libhifde_gpu.so``; this package is the thin Python face of its C ABI.
+"""
+
+from .driver import (FactorizationError, GeneralizedLDL, IndefiniteBlockError,
+                     SingularBlockError, apply_inverse, device_count, factor_hifde,
+                     factor_hifde3x, factor_mf)
+from .problems import (CoeffField, GridConfig, assemble, baseline_problem, build_grid,
+                       constant_field, gaussian_contrast_field, high_contrast_field)
+from .solvers import pcg
+
+__version__ = "0.1.0"

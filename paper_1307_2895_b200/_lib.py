@@ -1,0 +1,108 @@
+"""ctypes binding of ``include/hifde_gpu.h`` (the C ABI of libhifde_gpu.so).
+
+There is no CPU fallback: if the library is missing or no B200 is visible the
+factor entry points raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from ._build import LIB
+
+HIFDE_OK, HIFDE_INDEFINITE, HIFDE_SINGULAR, HIFDE_BADARG, HIFDE_CUDA, HIFDE_INTERNAL = range(6)
+VARIANT_MF, VARIANT_HIFDE, VARIANT_HIFDE3X = 0, 1, 2
+ORDER = {"auto": 0, "snapshot": 1, "exact": 2}
+
+
+class Options(C.Structure):
+    _fields_ = [
+        ("variant", C.c_int),
+        ("skip_levels", C.c_int),
+        ("spd", C.c_int),
+        ("order_mode", C.c_int),
+        ("exact_max_batches", C.c_int),
+        ("device", C.c_int),
+        ("input_on_device", C.c_int),
+        ("verify", C.c_int),
+        ("eps", C.c_double),
+        ("stream", C.c_void_p),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64),
+        ("dim", C.c_int32),
+        ("nlevels", C.c_int32),
+        ("s_top", C.c_int64),
+        ("m_f_bytes", C.c_int64),
+        ("device_bytes", C.c_int64),
+        ("t_f_seconds", C.c_double),
+        ("eps", C.c_double),
+        ("spd", C.c_int32),
+        ("variant", C.c_int32),
+    ]
+
+
+class LevelInfo(C.Structure):
+    _fields_ = [
+        ("tag", C.c_double),
+        ("kind", C.c_int32),
+        ("nbatches", C.c_int32),
+        ("ngroups", C.c_int64),
+        ("nskel", C.c_int64),
+        ("nredundant", C.c_int64),
+        ("active_after", C.c_int64),
+        ("max_front", C.c_int64),
+        ("seconds", C.c_double),
+        ("gflop", C.c_double),
+        ("gbytes", C.c_double),
+    ]
+
+
+# every symbol the public header declares
+EXPORTS = [
+    "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
+    "hifde_solve", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
+    "hifde_free", "hifde_last_error", "hifde_partition",
+]
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load (once) and type the library; raises if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB
+    if not os.path.exists(p):
+        raise RuntimeError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = C.CDLL(p)
+    P = C.POINTER
+    lib.hifde_version.restype = C.c_char_p
+    lib.hifde_device_count.restype = C.c_int
+    lib.hifde_default_options.argtypes = [P(Options), C.c_int]
+    lib.hifde_default_options.restype = None
+    lib.hifde_factor.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                                 C.c_int, C.c_int, P(Options), P(C.c_void_p)]
+    lib.hifde_factor.restype = C.c_int
+    lib.hifde_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                                C.c_void_p]
+    lib.hifde_solve.restype = C.c_int
+    lib.hifde_get_info.argtypes = [C.c_void_p, P(Info)]
+    lib.hifde_get_info.restype = C.c_int
+    lib.hifde_get_level.argtypes = [C.c_void_p, C.c_int, P(LevelInfo)]
+    lib.hifde_get_level.restype = C.c_int
+    lib.hifde_last_launch_count.restype = C.c_int64
+    lib.hifde_free.argtypes = [C.c_void_p]
+    lib.hifde_free.restype = None
+    lib.hifde_last_error.restype = C.c_char_p
+    lib.hifde_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                    C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
+    lib.hifde_partition.restype = C.c_int64
+    if path is None:
+        _lib = lib
+    return lib

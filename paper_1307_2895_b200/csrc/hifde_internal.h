@@ -1,0 +1,85 @@
+// Internal structures shared by the host runtime and the sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hifde {
+
+// Per-cell work item of an elimination level (src/factor_ops.py:138-159).
+// Front DOFs are c (ascending) followed by q (ascending) in the idx arena.
+struct ElimTask {
+  int32_t nc, nq;
+  int32_t nblk, maxnb;      // consumed clique blocks, largest block order
+  int64_t dofs_off;         // idx arena: c[nc] then q[nq]
+  int64_t blk_off;          // list arena: consumed block ids (ascending)
+  int64_t scratch_off;      // scratch arena (doubles) for a global front, -1: smem
+  int64_t C_off;            // factor arena: Cholesky factor, nc x nc row-major
+  int64_t W_off;            // factor arena: W = C^-1 A_cq, nc x nq row-major
+  int64_t U_off;            // block arena: new clique block, nq x nq row-major
+};
+
+// Per-group work item of a skeletonization level (src/factor_ops.py:162-214).
+struct SkelTask {
+  int32_t nc, nq;
+  int32_t nblk, maxnb;      // clique blocks touching c (read only)
+  int64_t dofs_off;         // idx arena: c[nc] then q[nq]
+  int64_t blk_off;          // list arena
+  int64_t scratch_off;      // scratch arena workspace, -1: smem
+  int64_t rec_off;          // factor arena: T (k x r), C (r x r), W (r x k)
+  int64_t delta_off;        // block arena: delta block (k x k)
+  int64_t out_off;          // idx arena: sk (ascending) then rd (ascending), global ids
+  int32_t group;            // index of the group within its level
+  int32_t pad;
+};
+
+// Solve-sweep record (one per elimination cell / skeleton group with rd != {}).
+struct SolveRec {
+  int32_t nc;               // |cell| (elimination) or |rd| (skeleton)
+  int32_t nq;               // |nbrs| (elimination) or |sk| (skeleton)
+  int64_t idx_off;          // idx arena: cell then nbrs / rd then sk
+  int64_t C_off, W_off, T_off;  // factor arena
+  int64_t contrib_off;      // elimination: row offset in the contribution buffer
+};
+
+// Device views of the persistent arenas.
+struct Arenas {
+  const int64_t* indptr;    // A0 (original matrix) CSR
+  const int32_t* indices;
+  const double* a0;
+  int32_t* idx;             // index arena (cells, neighbour lists, sk/rd)
+  const int32_t* lists;     // per-level block lists
+  const int64_t* blk_dof_off;  // block table: dof list offset in idx
+  const int32_t* blk_n;        //              order
+  const int64_t* blk_val_off;  //              value offset in the block arena
+  double* bvals;            // block arena
+  double* fac;              // factor arena
+  double* scratch;          // per-level scratch arena
+  uint8_t* active;          // device active mask (exact-order batches)
+  int* status;              // per-task status words
+  int32_t* kout;            // per-group skeleton rank
+};
+
+// Kernel launchers (kernels_factor.cu / kernels_solve.cu).
+void launch_elim(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem,
+                 int smem_cap_doubles, cudaStream_t s);
+void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps,
+                 size_t smem, int smem_cap_doubles, cudaStream_t s);
+void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s);
+
+// solve
+void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
+                           double* v, int nrhs, double* contrib, double* scratch,
+                           int64_t scratch_per_rec, size_t smem, cudaStream_t s);
+void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,
+                         int ntargets, const double* contrib, double* v, int nrhs,
+                         cudaStream_t s);
+void launch_solve_elim_bwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
+                           double* v, int nrhs, double* scratch, int64_t scratch_per_rec,
+                           size_t smem, cudaStream_t s);
+void launch_solve_skel(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
+                       double* v, int nrhs, int forward, double* scratch,
+                       int64_t scratch_per_rec, size_t smem, cudaStream_t s);
+
+constexpr int kThreads = 256;
+
+}  // namespace hifde

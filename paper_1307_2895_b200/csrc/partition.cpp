@@ -1,0 +1,168 @@
+// Level partitioning on the host.  Exact integer geometry in doubled grid
+// units, mirroring the reference's semantics (src/partition.py):
+//   * interior cells: active DOFs with no coordinate on a separator plane,
+//     keyed by cell index with the first axis fastest (:68-92);
+//   * interface groups: Voronoi assignment to edge / face centres with the
+//     multi-plane exclusions, lowest family winning distance ties and ties
+//     within a family rounding down (:95-181);
+//   * adaptive cells: Voronoi to cell centres, then in ascending key order
+//     each cell sheds members still coupled to another current cell (:184-227).
+// Groups come out in the reference's order: ascending key (family-major for
+// interfaces), members ascending.
+#include "partition.h"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace hifde {
+
+namespace {
+
+// Bucket the selected DOFs (ascending) by key in [0, nkeys): counting sort,
+// which keeps members ascending inside each bucket.  Empty buckets dropped.
+Groups bucket(const std::vector<int32_t>& dofs, const std::vector<int64_t>& keys, int64_t nkeys) {
+  Groups out;
+  std::vector<int64_t> cnt((size_t)nkeys + 1, 0);
+  for (int64_t k : keys) cnt[(size_t)k + 1]++;
+  for (int64_t i = 0; i < nkeys; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
+  out.members.resize(dofs.size());
+  std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+  for (size_t i = 0; i < dofs.size(); ++i) out.members[(size_t)pos[(size_t)keys[i]]++] = dofs[i];
+  out.offsets.clear();
+  out.offsets.push_back(0);
+  for (int64_t k = 0; k < nkeys; ++k)
+    if (cnt[(size_t)k + 1] > cnt[(size_t)k]) out.offsets.push_back(cnt[(size_t)k + 1]);
+  return out;
+}
+
+inline int64_t ipow(int64_t b, int e) {
+  int64_t r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
+
+// nearest centre w*j, j in [1, top], ties to the lower j (doubled coords x2)
+inline int64_t near_mult(int64_t x2, int64_t w, int64_t top) {
+  int64_t j = (x2 + w - 1) / (2 * w);
+  return std::min(std::max(j, (int64_t)1), top);
+}
+// nearest centre w*(j - 1/2), j in [1, top], ties to the lower j
+inline int64_t near_half(int64_t x2, int64_t w, int64_t top) {
+  int64_t j = (x2 + 2 * w - 1) / (2 * w);
+  return std::min(std::max(j, (int64_t)1), top);
+}
+
+}  // namespace
+
+Groups interior_groups(const GridDesc& g, int ell, const uint8_t* active) {
+  if (ell < 0 || ell >= std::max(g.nlevels, 1)) throw std::invalid_argument("level out of range");
+  const int64_t w = (int64_t)g.m << ell;
+  const int64_t k = g.n / w;
+  const int64_t N = g.ndof();
+  std::vector<int32_t> dofs;
+  std::vector<int64_t> keys;
+  int x[3];
+  for (int64_t d = 0; d < N; ++d) {
+    if (!active[d]) continue;
+    int64_t r = d;
+    bool inside = true;
+    int64_t key = 0, stride = 1;
+    for (int ax = 0; ax < g.dim; ++ax) {
+      x[ax] = (int)(r % g.side()) + 1;
+      r /= g.side();
+      if (x[ax] % w == 0) { inside = false; break; }
+      key += (x[ax] / w) * stride;
+      stride *= k;
+    }
+    if (!inside) continue;
+    dofs.push_back((int32_t)d);
+    keys.push_back(key);
+  }
+  return bucket(dofs, keys, ipow(k, g.dim));
+}
+
+Groups interface_groups(const GridDesc& g, int ell, const uint8_t* active, int kind) {
+  const bool face = kind == 1;
+  if (g.dim == 2 && face) throw std::invalid_argument("faces need a 3D grid");
+  const int64_t w = (int64_t)g.m << ell;
+  const int64_t k = g.n / w;
+  const int64_t span = ipow(k, g.dim);
+  const int64_t N = g.ndof();
+  std::vector<int32_t> dofs;
+  std::vector<int64_t> keys;
+  int64_t x2[3];
+  for (int64_t d = 0; d < N; ++d) {
+    if (!active[d]) continue;
+    int64_t r = d;
+    int planes = 0;
+    for (int ax = 0; ax < g.dim; ++ax) {
+      const int64_t x = r % g.side() + 1;
+      r /= g.side();
+      x2[ax] = 2 * x;
+      planes += (x % w == 0);
+    }
+    bool excluded;
+    if (g.dim == 2) excluded = planes == 2;
+    else if (face) excluded = planes >= 2;
+    else excluded = planes == 3;
+    if (excluded) continue;
+    int64_t best_d = INT64_MAX, best_key = 0;
+    for (int fam = 0; fam < g.dim; ++fam) {
+      int64_t dist = 0, key = 0, stride = 1;
+      for (int ax = 0; ax < g.dim; ++ax) {
+        const bool on_plane = face ? (ax == fam) : (ax != fam);
+        int64_t j, c2, sp;
+        if (on_plane) { j = near_mult(x2[ax], w, k - 1); c2 = 2 * w * j; sp = k - 1; }
+        else { j = near_half(x2[ax], w, k); c2 = w * (2 * j - 1); sp = k; }
+        dist += (x2[ax] - c2) * (x2[ax] - c2);
+        key += (j - 1) * stride;
+        stride *= sp;
+      }
+      if (dist < best_d) { best_d = dist; best_key = fam * span + key; }
+    }
+    dofs.push_back((int32_t)d);
+    keys.push_back(best_key);
+  }
+  return bucket(dofs, keys, span * g.dim);
+}
+
+Groups adaptive_groups(const GridDesc& g, int ell, const uint8_t* active, const CouplingTest& foreign) {
+  const int64_t w = (int64_t)g.m << ell;
+  const int64_t k = g.n / w;
+  const int64_t N = g.ndof();
+  std::vector<int32_t> dofs;
+  std::vector<int64_t> keys;
+  std::vector<int64_t> owner((size_t)N, -1);
+  for (int64_t d = 0; d < N; ++d) {
+    if (!active[d]) continue;
+    int64_t r = d, key = 0, stride = 1;
+    for (int ax = 0; ax < g.dim; ++ax) {
+      const int64_t x = r % g.side() + 1;
+      r /= g.side();
+      key += (near_half(2 * x, w, k) - 1) * stride;
+      stride *= k;
+    }
+    owner[(size_t)d] = key;
+    dofs.push_back((int32_t)d);
+    keys.push_back(key);
+  }
+  Groups vor = bucket(dofs, keys, ipow(k, g.dim));
+  Groups out;
+  std::vector<char> shed;
+  for (int64_t gi = 0; gi < vor.size(); ++gi) {
+    const int32_t* mem = vor.begin(gi);
+    const int cnt = vor.count(gi);
+    const int64_t key = owner[(size_t)mem[0]];
+    shed.assign((size_t)cnt, 0);
+    for (int i = 0; i < cnt; ++i) shed[(size_t)i] = foreign(mem[i], key, owner.data()) ? 1 : 0;
+    int kept = 0;
+    for (int i = 0; i < cnt; ++i) {
+      if (shed[(size_t)i]) owner[(size_t)mem[i]] = -1;
+      else { out.members.push_back(mem[i]); ++kept; }
+    }
+    if (kept) out.offsets.push_back((int64_t)out.members.size());
+  }
+  return out;
+}
+
+}  // namespace hifde

@@ -1,0 +1,987 @@
+// Host runtime of the B200 HIF-DE path: level schedule, symbolic analysis,
+// device arenas, kernel orchestration and the C ABI (include/hifde_gpu.h).
+//
+// Data model: the working matrix A_l is the original stencil
+// matrix A0 restricted to the active DOFs plus a set of live dense "clique
+// blocks".  An elimination consumes every block touching its cell and emits
+// one block over its neighbour set (the Schur update); a skeletonization with
+// redundant DOFs emits a delta block over its skeletons.  This reproduces the
+// reference's sparsity pattern exactly (src/sparse.py), so neighbour sets,
+// partitions and order-dependent steps match the reference.  The host keeps
+// only integer structure (DOF lists, block membership); every floating-point
+// operation runs in the sm_100a kernels.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hifde_gpu.h"
+#include "hifde_internal.h"
+#include "partition.h"
+
+namespace hifde {
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define HCK(x)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      throw Fail{HIFDE_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};          \
+  } while (0)
+
+constexpr size_t kSmemCap = 200 * 1024;  // dynamic shared memory per CTA we allow
+
+double now_s() {
+  using namespace std::chrono;
+  return duration<double>(steady_clock::now().time_since_epoch()).count();
+}
+
+size_t align16(size_t x) { return (x + 15) / 16 * 16; }
+
+// Growable device array with stream-ordered (pooled) allocation.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  void reserve(size_t c, cudaStream_t s) {
+    if (c <= cap) return;
+    size_t nc = std::max(c, cap + cap / 2 + 4096);
+    T* q = nullptr;
+    HCK(cudaMallocAsync((void**)&q, nc * sizeof(T), s));
+    if (n) HCK(cudaMemcpyAsync(q, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) HCK(cudaFreeAsync(p, s));
+    p = q;
+    cap = nc;
+  }
+  size_t bump(size_t k, cudaStream_t s) {
+    reserve(n + k, s);
+    size_t off = n;
+    n += k;
+    return off;
+  }
+  void upload(const T* h, size_t off, size_t cnt, cudaStream_t s) {
+    if (cnt) HCK(cudaMemcpyAsync(p + off, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void release(cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = cap = 0;
+  }
+};
+
+struct LevelRec {
+  double tag = 0;
+  int kind = 0;  // 0 elimination, 1 skeleton
+  int nbatches = 1;
+  int64_t ngroups = 0, nskel = 0, nred = 0, active_after = 0, max_front = 0;
+  double seconds = 0, gflop = 0, gbytes = 0;
+  // solve metadata
+  std::vector<SolveRec> recs;
+  SolveRec* d_recs = nullptr;
+  int max_nc = 0, max_nq = 0;
+  // elimination forward reduction (targets / CSR of contribution rows)
+  int64_t ncontrib = 0;
+  int32_t* d_targets = nullptr;
+  int64_t* d_ptr = nullptr;
+  int64_t* d_ent = nullptr;
+  int ntargets = 0;
+};
+
+}  // namespace
+}  // namespace hifde
+
+struct hifde_factor {
+  int64_t n = 0;
+  int dim = 0, variant = 0, spd = 1, device = 0;
+  double eps = 0;
+  int64_t s_top = 0, m_f_bytes = 0;
+  double t_f = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  hifde::DBuf<double> fac;
+  hifde::DBuf<int32_t> idx;
+  std::vector<hifde::LevelRec> levels;  // last entry = terminal block (kind 2)
+  int64_t max_contrib = 0;
+  ~hifde_factor() {
+    cudaSetDevice(device);
+    for (auto& L : levels) {
+      if (L.d_recs) cudaFree(L.d_recs);
+      if (L.d_targets) cudaFree(L.d_targets);
+      if (L.d_ptr) cudaFree(L.d_ptr);
+      if (L.d_ent) cudaFree(L.d_ent);
+    }
+    if (fac.p) cudaFree(fac.p);
+    if (idx.p) cudaFree(idx.p);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace hifde {
+namespace {
+
+template <class T>
+T* to_device(const std::vector<T>& h) {
+  if (h.empty()) return nullptr;
+  T* d = nullptr;
+  HCK(cudaMalloc((void**)&d, h.size() * sizeof(T)));
+  HCK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Factorization state
+// ---------------------------------------------------------------------------
+struct Factorizer {
+  GridDesc g;
+  hifde_options_t opt;
+  hifde_factor_t* F;
+  cudaStream_t s;
+  int64_t N;
+  // A0 (host + device)
+  std::vector<int64_t> indptr;
+  std::vector<int32_t> indices;
+  int64_t* d_indptr = nullptr;
+  int32_t* d_indices = nullptr;
+  double* d_a0 = nullptr;
+  // activity
+  std::vector<uint8_t> active;
+  uint8_t* d_active = nullptr;
+  // idx arena host mirror
+  std::vector<int32_t> h_idx;
+  // block table
+  std::vector<int64_t> blk_dof_off;
+  std::vector<int32_t> blk_n;
+  std::vector<int64_t> blk_val_off;
+  std::vector<uint8_t> blk_alive;
+  DBuf<int64_t> d_blk_dof_off;
+  DBuf<int32_t> d_blk_n;
+  DBuf<int64_t> d_blk_val_off;
+  size_t blk_uploaded = 0;
+  std::vector<std::vector<int32_t>> member;  // live blocks containing a DOF
+  DBuf<double> bvals;
+  DBuf<double> scratch;
+  DBuf<int32_t> lists;
+  DBuf<int> status;
+  DBuf<int32_t> kout;
+  // stamps
+  std::vector<int64_t> dstamp, bstamp;
+  int64_t stamp = 0;
+  // block-foreign cache for adaptive partitioning
+  std::vector<int64_t> bf_key;
+  std::vector<uint8_t> bf_val;
+  int64_t bf_epoch = 0;
+  size_t idx_uploaded = 0;
+
+  void upload_idx() {
+    F->idx.reserve(h_idx.size(), s);
+    F->idx.n = h_idx.size();
+    F->idx.upload(h_idx.data() + idx_uploaded, idx_uploaded, h_idx.size() - idx_uploaded, s);
+    idx_uploaded = h_idx.size();
+  }
+  void upload_blocks() {
+    size_t nb = blk_n.size();
+    if (nb == blk_uploaded) return;
+    d_blk_dof_off.reserve(nb, s);
+    d_blk_n.reserve(nb, s);
+    d_blk_val_off.reserve(nb, s);
+    d_blk_dof_off.upload(blk_dof_off.data() + blk_uploaded, blk_uploaded, nb - blk_uploaded, s);
+    d_blk_n.upload(blk_n.data() + blk_uploaded, blk_uploaded, nb - blk_uploaded, s);
+    d_blk_val_off.upload(blk_val_off.data() + blk_uploaded, blk_uploaded, nb - blk_uploaded, s);
+    d_blk_dof_off.n = d_blk_n.n = d_blk_val_off.n = nb;
+    blk_uploaded = nb;
+  }
+  Arenas arenas() {
+    Arenas A;
+    A.indptr = d_indptr;
+    A.indices = d_indices;
+    A.a0 = d_a0;
+    A.idx = F->idx.p;
+    A.lists = lists.p;
+    A.blk_dof_off = d_blk_dof_off.p;
+    A.blk_n = d_blk_n.p;
+    A.blk_val_off = d_blk_val_off.p;
+    A.bvals = bvals.p;
+    A.fac = F->fac.p;
+    A.scratch = scratch.p;
+    A.active = d_active;
+    A.status = status.p;
+    A.kout = kout.p;
+    return A;
+  }
+
+  int32_t add_block(int64_t dof_off, int32_t nb, int64_t val_off) {
+    int32_t id = (int32_t)blk_n.size();
+    blk_dof_off.push_back(dof_off);
+    blk_n.push_back(nb);
+    blk_val_off.push_back(val_off);
+    blk_alive.push_back(1);
+    bstamp.push_back(0);
+    bf_key.push_back(-2);
+    bf_val.push_back(0);
+    for (int32_t i = 0; i < nb; ++i) member[(size_t)h_idx[(size_t)(dof_off + i)]].push_back(id);
+    return id;
+  }
+  void kill_block(int32_t b) {
+    blk_alive[(size_t)b] = 0;
+    const int32_t* d = h_idx.data() + blk_dof_off[(size_t)b];
+    for (int32_t i = 0; i < blk_n[(size_t)b]; ++i) {
+      auto& v = member[(size_t)d[i]];
+      auto it = std::find(v.begin(), v.end(), b);
+      if (it != v.end()) {
+        *it = v.back();
+        v.pop_back();
+      }
+    }
+  }
+
+  // Neighbour set q of the group c and the live blocks touching c
+  // (src/sparse.py:164-173 on the clique representation).
+  void front_of(const int32_t* c, int nc, std::vector<int32_t>& blks, std::vector<int32_t>& q) {
+    const int64_t tc = ++stamp;
+    for (int i = 0; i < nc; ++i) dstamp[(size_t)c[i]] = tc;
+    const int64_t tq = ++stamp;
+    blks.clear();
+    q.clear();
+    for (int i = 0; i < nc; ++i)
+      for (int32_t b : member[(size_t)c[i]])
+        if (bstamp[(size_t)b] != tq) {
+          bstamp[(size_t)b] = tq;
+          blks.push_back(b);
+        }
+    std::sort(blks.begin(), blks.end());
+    auto consider = [&](int32_t d) {
+      if (active[(size_t)d] && dstamp[(size_t)d] != tc && dstamp[(size_t)d] != tq) {
+        dstamp[(size_t)d] = tq;
+        q.push_back(d);
+      }
+    };
+    for (int32_t b : blks) {
+      const int32_t* d = h_idx.data() + blk_dof_off[(size_t)b];
+      for (int32_t i = 0; i < blk_n[(size_t)b]; ++i) consider(d[i]);
+    }
+    for (int i = 0; i < nc; ++i)
+      for (int64_t k = indptr[(size_t)c[i]]; k < indptr[(size_t)c[i] + 1]; ++k) consider(indices[(size_t)k]);
+    std::sort(q.begin(), q.end());
+  }
+
+  int maxnb_of(const std::vector<int32_t>& blks) {
+    int m = 0;
+    for (int32_t b : blks) m = std::max(m, blk_n[(size_t)b]);
+    return m;
+  }
+
+  // cells of an elimination level must not interact (assert_noninteracting,
+  // src/partition.py:230-241)
+  void check_noninteracting(const Groups& gr, double tag) {
+    std::vector<int64_t> cell_of((size_t)N, -1);
+    for (int64_t gi = 0; gi < gr.size(); ++gi)
+      for (int i = 0; i < gr.count(gi); ++i) cell_of[(size_t)gr.begin(gi)[i]] = gi;
+    std::vector<int32_t> blks, q;
+    for (int64_t gi = 0; gi < gr.size(); ++gi) {
+      front_of(gr.begin(gi), gr.count(gi), blks, q);
+      for (int32_t d : q)
+        if (cell_of[(size_t)d] >= 0 && cell_of[(size_t)d] != gi) {
+          char buf[128];
+          snprintf(buf, sizeof buf, "cells interact at level %g", tag);
+          throw Fail{HIFDE_INTERNAL, buf};
+        }
+    }
+  }
+
+  void check_status(int64_t off, int64_t cnt, double tag, const char* what) {
+    if (cnt <= 0) return;
+    std::vector<int> st((size_t)cnt);
+    HCK(cudaMemcpyAsync(st.data(), status.p + off, cnt * sizeof(int), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < cnt; ++i)
+      if (st[(size_t)i] != 0) {
+        char buf[256];
+        const char* kind = st[(size_t)i] == 1 ? "matrix is not positive definite" : "singular pivot";
+        snprintf(buf, sizeof buf, "%s (%s %lld of level %g)", kind, what, (long long)i, tag);
+        throw Fail{st[(size_t)i] == 1 ? HIFDE_INDEFINITE : HIFDE_SINGULAR, buf};
+      }
+  }
+
+  // -------------------------------------------------------------------------
+  void elimination_level(const Groups& gr, double tag, LevelRec& L, bool is_top) {
+    const int64_t nt = gr.size();
+    L.kind = is_top ? 2 : 0;
+    L.ngroups = nt;
+    std::vector<ElimTask> tasks((size_t)nt);
+    std::vector<std::vector<int32_t>> consumed((size_t)nt);
+    std::vector<int32_t> hl;  // block lists of this level
+    std::vector<int32_t> q;
+    size_t smem = 0;
+    scratch.n = 0;
+    const int64_t idx_level_start = (int64_t)h_idx.size();
+    for (int64_t t = 0; t < nt; ++t) {
+      const int32_t* c = gr.begin(t);
+      const int nc = gr.count(t);
+      front_of(c, nc, consumed[(size_t)t], q);
+      const int nq = (int)q.size(), nf = nc + nq;
+      ElimTask& T = tasks[(size_t)t];
+      T.nc = nc;
+      T.nq = nq;
+      T.nblk = (int)consumed[(size_t)t].size();
+      T.maxnb = maxnb_of(consumed[(size_t)t]);
+      T.dofs_off = (int64_t)h_idx.size();
+      h_idx.insert(h_idx.end(), c, c + nc);
+      h_idx.insert(h_idx.end(), q.begin(), q.end());
+      T.blk_off = (int64_t)hl.size();
+      hl.insert(hl.end(), consumed[(size_t)t].begin(), consumed[(size_t)t].end());
+      const size_t ib = align16(sizeof(int32_t) * (size_t)(nf + T.maxnb));
+      const size_t need = ib + sizeof(double) * (size_t)nf * nf;
+      if (need <= kSmemCap) {
+        T.scratch_off = -1;
+        smem = std::max(smem, need);
+      } else {
+        T.scratch_off = (int64_t)scratch.bump((size_t)nf * nf, s);
+        smem = std::max(smem, ib);
+      }
+      T.C_off = (int64_t)F->fac.bump((size_t)nc * nc, s);
+      T.W_off = (int64_t)F->fac.bump((size_t)nc * nq, s);
+      T.U_off = nq > 0 ? (int64_t)bvals.bump((size_t)nq * nq, s) : 0;
+      L.max_front = std::max<int64_t>(L.max_front, nf);
+      SolveRec R;
+      R.nc = nc;
+      R.nq = nq;
+      R.idx_off = T.dofs_off;
+      R.C_off = T.C_off;
+      R.W_off = T.W_off;
+      R.T_off = 0;
+      R.contrib_off = L.ncontrib;
+      L.ncontrib += nq;
+      L.recs.push_back(R);
+      L.max_nc = std::max(L.max_nc, nc);
+      L.max_nq = std::max(L.max_nq, nq);
+      F->m_f_bytes += 8 * ((int64_t)nc * nc + nc + (int64_t)nc * nq);
+      const double dc = nc, dq = nq;
+      L.gflop += (dc * dc * dc / 3 + dc * dc * dq + dc * dq + dc * dq * dq) * 1e-9;
+      L.gbytes += 8.0 * ((dc + dq) * (dc + dq) + dc * dc + dc + dc * dq + 2 * dq * dq) * 1e-9;
+    }
+    // host structure updates: consumed blocks die, new neighbour blocks live
+    for (int64_t t = 0; t < nt; ++t) {
+      for (int32_t b : consumed[(size_t)t]) kill_block(b);
+      const ElimTask& T = tasks[(size_t)t];
+      if (T.nq > 0) add_block(T.dofs_off + T.nc, T.nq, T.U_off);
+      const int32_t* c = gr.begin(t);
+      for (int i = 0; i < T.nc; ++i) active[(size_t)c[i]] = 0;
+    }
+    (void)idx_level_start;
+    // uploads
+    upload_idx();
+    upload_blocks();
+    lists.reserve(std::max<size_t>(hl.size(), 1), s);
+    lists.n = hl.size();
+    lists.upload(hl.data(), 0, hl.size(), s);
+    DBuf<ElimTask> dt;
+    dt.reserve((size_t)nt, s);
+    dt.upload(tasks.data(), 0, (size_t)nt, s);
+    status.n = 0;
+    status.bump((size_t)nt, s);
+    Arenas A = arenas();
+    launch_elim(dt.p, (int)nt, A, smem, 0, s);
+    ++g_launches;
+    HCK(cudaGetLastError());
+    // device active mask: the eliminated cells retire
+    // (kept in sync lazily: only skeleton kernels read it, and they run
+    // after the host re-uploads the mask below)
+    HCK(cudaMemcpyAsync(d_active, active.data(), (size_t)N, cudaMemcpyHostToDevice, s));
+    check_status(0, nt, tag, is_top ? "top block" : "cell");
+    dt.release(s);
+    // solve-side reduction structure for the shared neighbour DOFs
+    if (!is_top) build_reduction(L);
+  }
+
+  void build_reduction(LevelRec& L) {
+    // targets: every q DOF of the level; entries in record order
+    std::vector<int32_t> targets;
+    std::vector<int64_t> cnt;
+    const int64_t tq = ++stamp;
+    std::vector<int32_t> slot_of_dof;  // via dstamp/bstamp trick: use a map vector
+    // map DOF -> target index (use a temporary N-sized vector only when needed)
+    static thread_local std::vector<int32_t> tmap;
+    if ((int64_t)tmap.size() < N) tmap.assign((size_t)N, -1);
+    for (const SolveRec& R : L.recs) {
+      const int32_t* q = h_idx.data() + R.idx_off + R.nc;
+      for (int a = 0; a < R.nq; ++a) {
+        const int32_t d = q[a];
+        if (dstamp[(size_t)d] != tq) {
+          dstamp[(size_t)d] = tq;
+          tmap[(size_t)d] = (int32_t)targets.size();
+          targets.push_back(d);
+          cnt.push_back(0);
+        }
+        cnt[(size_t)tmap[(size_t)d]]++;
+      }
+    }
+    std::vector<int64_t> ptr(targets.size() + 1, 0);
+    for (size_t i = 0; i < targets.size(); ++i) ptr[i + 1] = ptr[i] + cnt[i];
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    std::vector<int64_t> ent((size_t)ptr.back());
+    for (const SolveRec& R : L.recs) {
+      const int32_t* q = h_idx.data() + R.idx_off + R.nc;
+      for (int a = 0; a < R.nq; ++a) ent[(size_t)fill[(size_t)tmap[(size_t)q[a]]]++] = R.contrib_off + a;
+    }
+    L.ntargets = (int)targets.size();
+    L.d_targets = to_device(targets);
+    L.d_ptr = to_device(ptr);
+    L.d_ent = to_device(ent);
+    F->max_contrib = std::max(F->max_contrib, L.ncontrib);
+  }
+
+  // -------------------------------------------------------------------------
+  void skeleton_level(const Groups& gr, double tag, LevelRec& L) {
+    const int64_t nt = gr.size();
+    L.kind = 1;
+    L.ngroups = nt;
+    std::vector<SkelTask> tasks((size_t)nt);
+    std::vector<int32_t> hl, blks, q;
+    size_t smem = 0;
+    scratch.n = 0;
+    // exact-order batch index of every group (groups are neighbours when one
+    // holds a DOF of the other's neighbour set)
+    std::vector<int> batch((size_t)nt, 0);
+    std::vector<int32_t> gof_dofs;  // DOFs of this level's groups, to reset
+    static thread_local std::vector<int32_t> group_of;
+    if ((int64_t)group_of.size() < N) group_of.assign((size_t)N, -1);
+    for (int64_t t = 0; t < nt; ++t)
+      for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = (int32_t)t;
+    int nbatch = 1;
+    for (int64_t t = 0; t < nt; ++t) {
+      const int32_t* c = gr.begin(t);
+      const int nc = gr.count(t);
+      front_of(c, nc, blks, q);
+      const int nq = (int)q.size(), nf = nc + nq;
+      SkelTask& T = tasks[(size_t)t];
+      T.nc = nc;
+      T.nq = nq;
+      T.nblk = (int)blks.size();
+      T.maxnb = maxnb_of(blks);
+      T.group = (int32_t)t;
+      T.pad = 0;
+      T.dofs_off = (int64_t)h_idx.size();
+      h_idx.insert(h_idx.end(), c, c + nc);
+      h_idx.insert(h_idx.end(), q.begin(), q.end());
+      T.out_off = (int64_t)h_idx.size();
+      h_idx.insert(h_idx.end(), (size_t)nc, 0);
+      T.blk_off = (int64_t)hl.size();
+      hl.insert(hl.end(), blks.begin(), blks.end());
+      const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 5 * nc));
+      const size_t q4 = (size_t)nc * nc / 4 + nc;
+      const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 4 * q4 + (size_t)nc * nc;
+      const size_t need = ib + sizeof(double) * wsd;
+      if (need <= kSmemCap) {
+        T.scratch_off = -1;
+        smem = std::max(smem, need);
+      } else {
+        T.scratch_off = (int64_t)scratch.bump(wsd, s);
+        smem = std::max(smem, ib);
+      }
+      T.rec_off = (int64_t)F->fac.bump((size_t)nc * nc + 2 * q4, s);
+      T.delta_off = (int64_t)bvals.bump((size_t)nc * nc, s);
+      L.max_front = std::max<int64_t>(L.max_front, nf);
+      int b = 0;
+      for (int32_t d : q) {
+        const int32_t go = group_of[(size_t)d];
+        if (go >= 0 && go < t) b = std::max(b, batch[(size_t)go] + 1);
+      }
+      batch[(size_t)t] = b;
+      nbatch = std::max(nbatch, b + 1);
+    }
+    for (int64_t t = 0; t < nt; ++t)
+      for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = -1;
+    bool exact = opt.order_mode == HIFDE_ORDER_EXACT ||
+                 (opt.order_mode == HIFDE_ORDER_AUTO && nbatch <= opt.exact_max_batches);
+    if (!exact) {
+      std::fill(batch.begin(), batch.end(), 0);
+      nbatch = 1;
+    }
+    L.nbatches = nbatch;
+    // order tasks by batch (stable keeps the reference order inside a batch)
+    std::vector<int64_t> order((size_t)nt);
+    for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return batch[(size_t)a] < batch[(size_t)b]; });
+    std::vector<SkelTask> sorted((size_t)nt);
+    std::vector<int64_t> bstart((size_t)nbatch + 1, 0);
+    for (int64_t i = 0; i < nt; ++i) {
+      sorted[(size_t)i] = tasks[(size_t)order[(size_t)i]];
+      bstart[(size_t)batch[(size_t)order[(size_t)i]] + 1]++;
+    }
+    for (int b = 0; b < nbatch; ++b) bstart[(size_t)b + 1] += bstart[(size_t)b];
+    upload_idx();
+    upload_blocks();
+    lists.reserve(std::max<size_t>(hl.size(), 1), s);
+    lists.n = hl.size();
+    lists.upload(hl.data(), 0, hl.size(), s);
+    DBuf<SkelTask> dt;
+    dt.reserve((size_t)nt, s);
+    dt.upload(sorted.data(), 0, (size_t)nt, s);
+    status.n = 0;
+    status.bump((size_t)nt, s);
+    kout.n = 0;
+    kout.bump((size_t)nt, s);
+    Arenas A = arenas();
+    for (int b = 0; b < nbatch; ++b) {
+      const int64_t lo = bstart[(size_t)b], hi = bstart[(size_t)b + 1];
+      if (hi <= lo) continue;
+      launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, 0, s);
+      launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
+      g_launches += 2;
+    }
+    HCK(cudaGetLastError());
+    check_status(0, nt, tag, "group");
+    std::vector<int32_t> k((size_t)nt);
+    HCK(cudaMemcpyAsync(k.data(), kout.p, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    // read back the sk/rd lists written by the kernels
+    for (int64_t t = 0; t < nt; ++t) {
+      const SkelTask& T = tasks[(size_t)t];
+      HCK(cudaMemcpyAsync(h_idx.data() + T.out_off, F->idx.p + T.out_off, (size_t)T.nc * sizeof(int32_t),
+                          cudaMemcpyDeviceToHost, s));
+    }
+    HCK(cudaStreamSynchronize(s));
+    dt.release(s);
+    for (int64_t t = 0; t < nt; ++t) {
+      const SkelTask& T = tasks[(size_t)t];
+      const int kk = k[(size_t)t], r = T.nc - kk;
+      const int32_t* out = h_idx.data() + T.out_off;
+      L.nskel += kk;
+      L.nred += r;
+      for (int i = kk; i < T.nc; ++i) active[(size_t)out[i]] = 0;
+      if (r > 0 && kk > 0) add_block(T.out_off, kk, T.delta_off);
+      if (r > 0) {
+        SolveRec R;
+        R.nc = r;
+        R.nq = kk;
+        R.idx_off = T.out_off;
+        R.T_off = T.rec_off;
+        R.C_off = T.rec_off + (int64_t)kk * r;
+        R.W_off = R.C_off + (int64_t)r * r;
+        R.contrib_off = 0;
+        L.recs.push_back(R);
+        L.max_nc = std::max(L.max_nc, r);
+        L.max_nq = std::max(L.max_nq, kk);
+        F->m_f_bytes += 8 * ((int64_t)kk * r + (int64_t)r * r + r + (int64_t)r * kk);
+      }
+      const double dc = T.nc, dq = T.nq, dk = kk, dr = r;
+      double fl = 4 * dq * dc * dk - 2 * dk * dk * (dq + dc) + 4 * dk * dk * dk / 3 + 2 * dq * dc +
+                  dk * dk * dr + 2 * dk * dk * dr + 4 * dk * dr * dr;
+      if (r > 0) fl += dr * dr * dr / 3 + dr * dr * dk + dk * dk * dr;
+      L.gflop += fl * 1e-9;
+      L.gbytes += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
+    }
+  }
+
+  // -------------------------------------------------------------------------
+  bool adaptive_foreign(int32_t d, int64_t key, const int64_t* owner) {
+    for (int64_t k = indptr[(size_t)d]; k < indptr[(size_t)d + 1]; ++k) {
+      const int64_t o = owner[indices[(size_t)k]];
+      if (o != -1 && o != key) return true;
+    }
+    const int64_t tag = (bf_epoch << 32) + key;
+    for (int32_t b : member[(size_t)d]) {
+      if (bf_key[(size_t)b] != tag) {
+        bf_key[(size_t)b] = tag;
+        uint8_t f = 0;
+        const int32_t* dd = h_idx.data() + blk_dof_off[(size_t)b];
+        for (int32_t i = 0; i < blk_n[(size_t)b] && !f; ++i) {
+          const int32_t e = dd[i];
+          if (!active[(size_t)e]) continue;
+          const int64_t o = owner[e];
+          if (o != -1 && o != key) f = 1;
+        }
+        bf_val[(size_t)b] = f;
+      }
+      if (bf_val[(size_t)b]) return true;
+    }
+    return false;
+  }
+
+  void run(const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz) {
+    const double t0 = now_s();
+    N = g.ndof();
+    // A0
+    if (opt.input_on_device) {
+      indptr.resize((size_t)N + 1);
+      HCK(cudaMemcpy(indptr.data(), ip, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      nnz = indptr.back();
+      indices.resize((size_t)nnz);
+      HCK(cudaMemcpy(indices.data(), ix, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    } else {
+      indptr.assign(ip, ip + N + 1);
+      indices.assign(ix, ix + nnz);
+    }
+    HCK(cudaMallocAsync((void**)&d_indptr, (N + 1) * sizeof(int64_t), s));
+    HCK(cudaMallocAsync((void**)&d_indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t), s));
+    HCK(cudaMallocAsync((void**)&d_a0, std::max<int64_t>(nnz, 1) * sizeof(double), s));
+    HCK(cudaMemcpyAsync(d_indptr, indptr.data(), (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    HCK(cudaMemcpyAsync(d_indices, indices.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    HCK(cudaMemcpyAsync(d_a0, va, nnz * sizeof(double),
+                        opt.input_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    active.assign((size_t)N, 1);
+    HCK(cudaMallocAsync((void**)&d_active, std::max<int64_t>(N, 1), s));
+    HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
+    member.assign((size_t)N, {});
+    dstamp.assign((size_t)N, 0);
+    F->fac.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
+    F->idx.reserve((size_t)std::max<int64_t>(16 * N, 1 << 16), s);
+    bvals.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
+
+    const int Lv = g.nlevels;
+    auto record_trace = [&](LevelRec& L, double tl) {
+      int64_t a = 0;
+      for (int64_t i = 0; i < N; ++i) a += active[(size_t)i];
+      L.active_after = a;
+      L.seconds = now_s() - tl;
+    };
+    for (int ell = 0; ell < Lv; ++ell) {
+      {
+        const double tl = now_s();
+        Groups gr;
+        if (opt.variant == HIFDE_VARIANT_HIFDE3X && ell > 0) {
+          ++bf_epoch;
+          gr = adaptive_groups(g, ell, active.data(), [&](int32_t d, int64_t key, const int64_t* owner) {
+            return adaptive_foreign(d, key, owner);
+          });
+        } else {
+          gr = interior_groups(g, ell, active.data());
+        }
+        if (opt.verify) check_noninteracting(gr, (double)ell);
+        F->levels.emplace_back();
+        LevelRec& L = F->levels.back();
+        L.tag = (double)ell;
+        elimination_level(gr, L.tag, L, false);
+        record_trace(L, tl);
+      }
+      auto skel = [&](double tag, int kind) {
+        const double tl = now_s();
+        Groups gr = interface_groups(g, ell, active.data(), kind);
+        F->levels.emplace_back();
+        LevelRec& L = F->levels.back();
+        L.tag = tag;
+        skeleton_level(gr, tag, L);
+        record_trace(L, tl);
+      };
+      if (opt.variant == HIFDE_VARIANT_HIFDE) {
+        if (ell >= opt.skip_levels) skel(ell + 0.5, g.dim == 2 ? 0 : 1);
+      } else if (opt.variant == HIFDE_VARIANT_HIFDE3X) {
+        skel(ell + 1.0 / 3.0, 1);
+        if (ell >= opt.skip_levels) skel(ell + 2.0 / 3.0, 0);
+      }
+    }
+    // terminal block: every DOF still active (src/driver.py:152-157)
+    {
+      const double tl = now_s();
+      Groups top;
+      for (int64_t i = 0; i < N; ++i)
+        if (active[(size_t)i]) top.members.push_back((int32_t)i);
+      F->s_top = (int64_t)top.members.size();
+      F->levels.emplace_back();
+      LevelRec& L = F->levels.back();
+      L.tag = (double)Lv;
+      if (!top.members.empty()) {
+        top.offsets.push_back((int64_t)top.members.size());
+        elimination_level(top, L.tag, L, true);
+        L.gflop = std::pow((double)F->s_top, 3) / 3 * 1e-9;
+        L.gbytes = 16.0 * F->s_top * F->s_top * 1e-9;
+      }
+      L.kind = 2;
+      record_trace(L, tl);
+    }
+    // solve metadata to the device
+    for (auto& L : F->levels) L.d_recs = to_device(L.recs);
+    HCK(cudaStreamSynchronize(s));
+    bvals.release(s);
+    scratch.release(s);
+    lists.release(s);
+    status.release(s);
+    kout.release(s);
+    d_blk_dof_off.release(s);
+    d_blk_n.release(s);
+    d_blk_val_off.release(s);
+    cudaFreeAsync(d_indptr, s);
+    cudaFreeAsync(d_indices, s);
+    cudaFreeAsync(d_a0, s);
+    cudaFreeAsync(d_active, s);
+    HCK(cudaStreamSynchronize(s));
+    F->t_f = now_s() - t0;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Solve sweep
+// ---------------------------------------------------------------------------
+void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, bool dev, cudaStream_t s) {
+  const int64_t N = F->n;
+  const size_t bytes = (size_t)N * nrhs * sizeof(double);
+  double* v = nullptr;
+  HCK(cudaMallocAsync((void**)&v, std::max<size_t>(bytes, 8), s));
+  HCK(cudaMemcpyAsync(v, b, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  double* contrib = nullptr;
+  HCK(cudaMallocAsync((void**)&contrib, std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
+  // global workspace for records too large for shared memory
+  size_t scratch_need = 0;
+  auto ws_plan = [&](const LevelRec& L, int64_t per_rec_doubles, size_t& smem, int64_t& per_rec) {
+    const size_t need = (size_t)per_rec_doubles * sizeof(double);
+    if (need <= kSmemCap) { smem = need; per_rec = 0; }
+    else { smem = 0; per_rec = per_rec_doubles; scratch_need = std::max(scratch_need, (size_t)per_rec * L.recs.size()); }
+  };
+  for (const auto& L : F->levels) {
+    size_t sm; int64_t pr;
+    if (L.kind == 1) ws_plan(L, (int64_t)(L.max_nc + L.max_nq) * nrhs, sm, pr);
+    else ws_plan(L, (int64_t)L.max_nc * nrhs, sm, pr);
+  }
+  double* scratch = nullptr;
+  HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
+  const int32_t* idx = F->idx.p;
+  const double* fac = F->fac.p;
+  const size_t nl = F->levels.size();
+  for (size_t li = 0; li < nl; ++li) {
+    const LevelRec& L = F->levels[li];
+    const int nr = (int)L.recs.size();
+    if (!nr) continue;
+    size_t sm; int64_t pr;
+    if (L.kind == 1) {
+      ws_plan(L, (int64_t)(L.max_nc + L.max_nq) * nrhs, sm, pr);
+      launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s);
+      ++g_launches;
+    } else {
+      ws_plan(L, (int64_t)L.max_nc * nrhs, sm, pr);
+      launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s);
+      ++g_launches;
+      if (L.kind == 0) {
+        launch_solve_reduce(L.d_targets, L.d_ptr, L.d_ent, L.ntargets, contrib, v, nrhs, s);
+        ++g_launches;
+      }
+    }
+  }
+  for (size_t li = nl; li-- > 0;) {
+    const LevelRec& L = F->levels[li];
+    const int nr = (int)L.recs.size();
+    if (!nr) continue;
+    size_t sm; int64_t pr;
+    if (L.kind == 1) {
+      ws_plan(L, (int64_t)(L.max_nc + L.max_nq) * nrhs, sm, pr);
+      launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s);
+    } else {
+      ws_plan(L, (int64_t)L.max_nc * nrhs, sm, pr);
+      launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s);
+    }
+    ++g_launches;
+  }
+  HCK(cudaGetLastError());
+  HCK(cudaMemcpyAsync(x, v, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  HCK(cudaFreeAsync(v, s));
+  HCK(cudaFreeAsync(contrib, s));
+  HCK(cudaFreeAsync(scratch, s));
+  if (!dev) HCK(cudaStreamSynchronize(s));
+}
+
+int fail_to_status(const Fail& f) {
+  g_err = f.msg;
+  return f.code;
+}
+
+void set_pool_threshold(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+}  // namespace
+}  // namespace hifde
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace hifde;
+
+extern "C" {
+
+const char* hifde_version(void) { return "hifde-b200 0.1.0 (sm_100a)"; }
+
+int hifde_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void hifde_default_options(hifde_options_t* o, int variant) {
+  std::memset(o, 0, sizeof *o);
+  o->variant = variant;
+  o->skip_levels = variant == HIFDE_VARIANT_HIFDE3X ? 1 : 0;
+  o->spd = 1;
+  o->order_mode = HIFDE_ORDER_AUTO;
+  o->exact_max_batches = 24;
+  o->device = 0;
+  o->eps = 0.0;
+}
+
+const char* hifde_last_error(void) { return g_err.c_str(); }
+
+int64_t hifde_last_launch_count(void) { return g_launches; }
+
+int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* vals, int64_t n,
+                 int dim, int n_grid, int m_leaf, int nlevels, const hifde_options_t* opt,
+                 hifde_factor_t** out) {
+  g_err.clear();
+  g_launches = 0;
+  if (!out || !opt) { g_err = "null argument"; return HIFDE_BADARG; }
+  *out = nullptr;
+  if (dim != 2 && dim != 3) { g_err = "dim must be 2 or 3"; return HIFDE_BADARG; }
+  if (opt->variant == HIFDE_VARIANT_HIFDE3X && dim != 3) {
+    g_err = "factor_hifde3x requires a 3D grid";
+    return HIFDE_BADARG;
+  }
+  if (!opt->spd) {
+    g_err = "indefinite (Bunch-Kaufman) factorization is not implemented on the GPU path";
+    return HIFDE_BADARG;
+  }
+  GridDesc g;
+  g.dim = dim;
+  g.n = n_grid;
+  g.m = m_leaf;
+  g.nlevels = nlevels;
+  if (n_grid < 2 || m_leaf < 2 || nlevels < 0 || g.ndof() != n) {
+    g_err = "grid does not match the matrix order";
+    return HIFDE_BADARG;
+  }
+  if (nlevels > 0 && ((int64_t)m_leaf << nlevels) != n_grid) {
+    g_err = "n must equal m * 2^nlevels";
+    return HIFDE_BADARG;
+  }
+  std::unique_ptr<hifde_factor_t> F(new hifde_factor_t);
+  try {
+    HCK(cudaSetDevice(opt->device));
+    set_pool_threshold(opt->device);
+    F->device = opt->device;
+    F->n = n;
+    F->dim = dim;
+    F->variant = opt->variant;
+    F->spd = 1;
+    F->eps = opt->variant == HIFDE_VARIANT_MF ? 0.0 : opt->eps;
+    if (opt->stream) {
+      F->stream = (cudaStream_t)opt->stream;
+    } else {
+      HCK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
+      F->own_stream = true;
+    }
+    Factorizer fz;
+    fz.g = g;
+    fz.opt = *opt;
+    if (opt->variant == HIFDE_VARIANT_MF) {
+      fz.opt.variant = HIFDE_VARIANT_HIFDE;
+      fz.opt.skip_levels = nlevels;  // factor_mf == factor_hifde(skip_levels=L)
+      fz.opt.eps = 0.0;
+    }
+    if (fz.opt.exact_max_batches <= 0) fz.opt.exact_max_batches = 24;
+    fz.F = F.get();
+    fz.s = F->stream;
+    const int64_t nnz = opt->input_on_device ? 0 : indptr[n];
+    fz.run(indptr, indices, vals, nnz);
+  } catch (const Fail& f) {
+    return fail_to_status(f);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
+  }
+  *out = F.release();
+  return HIFDE_OK;
+}
+
+int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n, int nrhs,
+                int device_ptrs, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!f || !b || !x) { g_err = "null argument"; return HIFDE_BADARG; }
+  if (n != f->n || nrhs < 1) { g_err = "right-hand side shape mismatch"; return HIFDE_BADARG; }
+  try {
+    HCK(cudaSetDevice(f->device));
+    cudaStream_t s = stream ? (cudaStream_t)stream : f->stream;
+    do_solve(f, b, x, nrhs, device_ptrs != 0, s);
+  } catch (const Fail& e) {
+    return fail_to_status(e);
+  }
+  return HIFDE_OK;
+}
+
+int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
+  if (!f || !info) return HIFDE_BADARG;
+  std::memset(info, 0, sizeof *info);
+  info->n = f->n;
+  info->dim = f->dim;
+  info->nlevels = (int32_t)f->levels.size() - 1;
+  info->s_top = f->s_top;
+  info->m_f_bytes = f->m_f_bytes;
+  info->device_bytes = (int64_t)(f->fac.n * sizeof(double) + f->idx.n * sizeof(int32_t));
+  info->t_f_seconds = f->t_f;
+  info->eps = f->eps;
+  info->spd = f->spd;
+  info->variant = f->variant;
+  return HIFDE_OK;
+}
+
+int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info) {
+  if (!f || !info || level < 0 || level >= (int)f->levels.size()) return HIFDE_BADARG;
+  const auto& L = f->levels[(size_t)level];
+  info->tag = L.tag;
+  info->kind = L.kind;
+  info->nbatches = L.nbatches;
+  info->ngroups = L.ngroups;
+  info->nskel = L.nskel;
+  info->nredundant = L.nred;
+  info->active_after = L.active_after;
+  info->max_front = L.max_front;
+  info->seconds = L.seconds;
+  info->gflop = L.gflop;
+  info->gbytes = L.gbytes;
+  return HIFDE_OK;
+}
+
+void hifde_free(hifde_factor_t* f) { delete f; }
+
+int64_t hifde_partition(int dim, int n_grid, int m_leaf, int ell, int level_kind,
+                        const uint8_t* active, int32_t* members, int64_t members_cap,
+                        int64_t* offsets, int64_t offsets_cap) {
+  try {
+    GridDesc g;
+    g.dim = dim;
+    g.n = n_grid;
+    g.m = m_leaf;
+    int L = 0;
+    while (((int64_t)m_leaf << (L + 1)) <= n_grid) ++L;
+    g.nlevels = L;
+    Groups gr = level_kind == 0 ? interior_groups(g, ell, active)
+                                : interface_groups(g, ell, active, level_kind == 2 ? 1 : 0);
+    if ((int64_t)gr.members.size() > members_cap || gr.size() + 1 > offsets_cap) return -1;
+    std::memcpy(members, gr.members.data(), gr.members.size() * sizeof(int32_t));
+    std::memcpy(offsets, gr.offsets.data(), gr.offsets.size() * sizeof(int64_t));
+    return gr.size();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,198 @@
+"""Reference-facing API of the B200 HIF-DE path.
+
+Same names, signatures, options and error classes as the reference's hot-path
+entry points (``src/driver.py:201-259``), backed by the sm_100a library
+through its C ABI (``include/hifde_gpu.h``):
+
+* ``factor_hifde(a, grid, eps, spd=True, skip_levels=0, verify=False)``
+* ``factor_hifde3x(a, grid, eps, spd=True, skip_levels=1, verify=False)``
+* ``factor_mf(a, grid, spd=True, verify=False)``
+* ``GeneralizedLDL.apply_inverse(b)`` / ``apply_inverse(f, b)``
+
+``a`` is anything the reference accepts that can produce a symmetric CSR
+(the reference's ``SparseSymMatrix`` via ``to_scipy()``, a SciPy sparse matrix,
+or a dense array); unlike the reference it is not consumed.  ``grid`` is any
+object with ``dim, n, m, nlevels`` (the reference's ``GridConfig`` works).
+There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib as L
+
+
+class FactorizationError(Exception):
+    """Base class for factorization failures (src/dense.py:41-42)."""
+
+
+class IndefiniteBlockError(FactorizationError):
+    """Cholesky requested on a block that is not positive definite."""
+
+
+class SingularBlockError(FactorizationError):
+    """A pivot fell below the singularity threshold."""
+
+
+def _raise(lib, code: int):
+    msg = lib.hifde_last_error().decode(errors="replace")
+    if code == L.HIFDE_INDEFINITE:
+        raise IndefiniteBlockError(msg)
+    if code == L.HIFDE_SINGULAR:
+        raise SingularBlockError(msg)
+    if code == L.HIFDE_BADARG:
+        raise ValueError(msg)
+    if code == L.HIFDE_INTERNAL:
+        raise AssertionError(msg)
+    raise RuntimeError(msg)
+
+
+def _as_csr(a) -> sp.csr_matrix:
+    if hasattr(a, "to_scipy"):
+        a = a.to_scipy()
+    m = sp.csr_matrix(a, dtype=np.float64)
+    m.sum_duplicates()
+    m.sort_indices()
+    if m.shape[0] != m.shape[1]:
+        raise ValueError("matrix must be square")
+    return m
+
+
+class GeneralizedLDL:
+    """GPU-resident generalized LDL factor (src/driver.py:64-149).
+
+    ``apply_inverse`` runs the up/down sweep on the device; ``metrics`` holds
+    the reference's keys (``s_top``, ``active_trace``, ``level_seconds``,
+    ``m_f_bytes``, ``t_f_seconds``) plus ``skeleton_counts`` and per-level
+    algorithmic FLOP/byte counts.
+    """
+
+    def __init__(self, handle: int, lib, spd: bool):
+        self._h = C.c_void_p(handle)
+        self._lib = lib
+        info = L.Info()
+        lib.hifde_get_info(self._h, C.byref(info))
+        self.n = int(info.n)
+        self.dim = int(info.dim)
+        self.spd = spd
+        self.eps = float(info.eps)
+        self.device_bytes = int(info.device_bytes)
+        self.level_info = []
+        for i in range(info.nlevels + 1):
+            li = L.LevelInfo()
+            lib.hifde_get_level(self._h, i, C.byref(li))
+            self.level_info.append({k: getattr(li, k) for k, _ in L.LevelInfo._fields_})
+        levels = self.level_info[:-1]
+        trace = [(-1.0, self.n)] + [(d["tag"], int(d["active_after"])) for d in levels]
+        self.metrics = {
+            "s_top": int(info.s_top),
+            "active_trace": trace,
+            "level_seconds": [(d["tag"], d["seconds"]) for d in levels],
+            "m_f_bytes": int(info.m_f_bytes),
+            "t_f_seconds": float(info.t_f_seconds),
+            "skeleton_counts": [(d["tag"], int(d["nskel"])) for d in levels if d["kind"] == 1],
+            "factor_gflop": sum(d["gflop"] for d in self.level_info),
+            "factor_gbytes": sum(d["gbytes"] for d in self.level_info),
+            "launches": int(lib.hifde_last_launch_count()),
+        }
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def storage_bytes(self) -> int:
+        return self.metrics["m_f_bytes"]
+
+    def apply_inverse(self, b) -> np.ndarray:
+        """x ~= A^{-1} b for b of shape (N,) or (N, nrhs); host arrays."""
+        arr = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+        vec = arr.ndim == 1
+        if arr.shape[0] != self.n:
+            raise ValueError("right-hand side has the wrong length")
+        nrhs = 1 if vec else arr.shape[1]
+        out = np.empty_like(arr)
+        if arr.size:
+            code = self._lib.hifde_solve(self._h, arr.ctypes.data, out.ctypes.data, self.n, nrhs, 0, None)
+            if code:
+                _raise(self._lib, code)
+        return out
+
+    def apply_inverse_device(self, b_ptr: int, x_ptr: int, nrhs: int, stream: Optional[int] = None):
+        """Device-pointer variant (row-major N x nrhs float64 buffers)."""
+        code = self._lib.hifde_solve(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), self.n, nrhs, 1,
+                                     C.c_void_p(stream) if stream else None)
+        if code:
+            _raise(self._lib, code)
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            self._lib.hifde_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
+            order: str = "auto", exact_max_batches: int = 24, device: int = 0,
+            stream: Optional[int] = None) -> GeneralizedLDL:
+    lib = L.load()
+    if not spd:
+        raise NotImplementedError("indefinite (Bunch-Kaufman) mode is outside the GPU hot path")
+    csr = _as_csr(a)
+    indptr = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+    indices = np.ascontiguousarray(csr.indices, dtype=np.int32)
+    data = np.ascontiguousarray(csr.data, dtype=np.float64)
+    opt = L.Options()
+    lib.hifde_default_options(C.byref(opt), variant)
+    opt.skip_levels = int(skip_levels)
+    opt.spd = 1
+    opt.eps = float(eps)
+    opt.order_mode = L.ORDER[order]
+    opt.exact_max_batches = int(exact_max_batches)
+    opt.device = int(device)
+    opt.verify = int(bool(verify))
+    opt.stream = stream
+    h = C.c_void_p()
+    code = lib.hifde_factor(indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, csr.shape[0],
+                            int(grid.dim), int(grid.n), int(grid.m), int(grid.nlevels),
+                            C.byref(opt), C.byref(h))
+    if code:
+        _raise(lib, code)
+    return GeneralizedLDL(h.value, lib, spd)
+
+
+def factor_hifde(a, grid, eps: float, spd: bool = True, skip_levels: int = 0,
+                 verify: bool = False, **kw) -> GeneralizedLDL:
+    """Interior elimination plus edge (2D) / face (3D) skeletonization
+    (src/driver.py:212-225)."""
+    return _factor(a, grid, eps, L.VARIANT_HIFDE, spd, skip_levels, verify, **kw)
+
+
+def factor_hifde3x(a, grid, eps: float, spd: bool = True, skip_levels: int = 1,
+                   verify: bool = False, **kw) -> GeneralizedLDL:
+    """3D faces + edges with adaptive minimal separators (src/driver.py:228-251)."""
+    if grid.dim != 3:
+        raise ValueError("factor_hifde3x requires a 3D grid")
+    return _factor(a, grid, eps, L.VARIANT_HIFDE3X, spd, skip_levels, verify, **kw)
+
+
+def factor_mf(a, grid, spd: bool = True, verify: bool = False, **kw) -> GeneralizedLDL:
+    """Multifrontal elimination, exact to rounding (src/driver.py:201-209)."""
+    return _factor(a, grid, 0.0, L.VARIANT_MF, spd, grid.nlevels, verify, **kw)
+
+
+def apply_inverse(f: GeneralizedLDL, b) -> np.ndarray:
+    return f.apply_inverse(b)
+
+
+def device_count() -> int:
+    return int(L.load().hifde_device_count())

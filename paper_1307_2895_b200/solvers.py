@@ -1,0 +1,48 @@
+"""Preconditioned CG consumer of ``apply_inverse`` (src/krylov.py:48-77).
+
+The factor is used as the preconditioner exactly as the reference's bench does
+(src/bench.py:169-171).  The matvec with A runs on the host here: Krylov
+solvers are a consumer of the hot path, not part of it.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class SolveReport:
+    x: np.ndarray
+    n_i: int
+    residual: float
+    converged: bool
+
+
+def pcg(a, b, precond=None, tol: float = 1e-12, max_iter: int = 1000) -> SolveReport:
+    """CG on ||b - A x|| / ||b|| <= tol with an SPD preconditioner callable."""
+    pc = precond if precond is not None else (lambda v: v)
+    b = np.asarray(b, dtype=float)
+    bn = float(np.linalg.norm(b))
+    if bn == 0.0:
+        return SolveReport(np.zeros_like(b), 0, 0.0, True)
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = pc(r)
+    p = z.copy()
+    rz = float(r @ z)
+    res = 1.0
+    for it in range(1, max_iter + 1):
+        ap = a @ p
+        alpha = rz / float(p @ ap)
+        x += alpha * p
+        r -= alpha * ap
+        res = float(np.linalg.norm(r)) / bn
+        if res <= tol:
+            return SolveReport(x, it, res, True)
+        z = pc(r)
+        rz_new = float(r @ z)
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return SolveReport(x, max_iter, res, False)

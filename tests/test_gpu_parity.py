@@ -1,0 +1,163 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle on the same seeded inputs.
+
+BASELINE.json criteria, as written in the tests:
+  * factorization: ||A F^-1 x - x|| / ||x|| <= 10 x the reference's value;
+  * solution: ||u_gpu - u_ref|| / ||u_ref|| <= 10 eps on PCG-converged
+    solutions (tol 1e-12, each preconditioned by its own factor; SURVEY.md
+    appendix E shows one-shot solutions of two valid factors differ by > 10 eps);
+  * skeleton ranks: per-level sum |sk| within +-2% of the reference.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1307_2895_b200 as H
+from oracle import hifde_oracle as O
+from tests import golden_cases as G
+
+pytestmark = pytest.mark.gpu
+
+NAMES = G.golden_names()
+
+
+def _grid(gd):
+    return H.build_grid(int(gd["dim"]), int(gd["n"]), int(gd["m"]))
+
+
+def _factor(gd, csr, **kw):
+    g = _grid(gd)
+    variant = str(gd["variant"])
+    eps = float(gd["eps"])
+    skip = G.skip_levels(gd)
+    if variant == "mf":
+        return g, H.factor_mf(csr, g, **kw)
+    if variant == "hifde3x":
+        return g, H.factor_hifde3x(csr, g, eps, **({} if skip is None else {"skip_levels": skip}), **kw)
+    return g, H.factor_hifde(csr, g, eps, **({} if skip is None else {"skip_levels": skip}), **kw)
+
+
+@pytest.mark.parametrize("order", ["auto", "snapshot"])
+@pytest.mark.parametrize("name", NAMES)
+def test_gpu_matches_reference_golden(name, order):
+    gd = G.load(name)
+    _, csr = G.build_problem(gd)
+    assert G.csr_digest(csr) == str(gd["csr_sha256"])
+    g, f = _factor(gd, csr, order=order)
+    eps = float(gd["eps"])
+    tags = [t for t, _ in f.metrics["active_trace"][1:]]
+    assert np.allclose(tags, gd["level_tags"])
+    counts = [c for _, c in f.metrics["skeleton_counts"]]
+    assert G.ranks_within(counts, gd["skel_ranks"]), (counts, gd["skel_ranks"].tolist())
+    s_ref = int(gd["s_top"])
+    assert abs(f.metrics["s_top"] - s_ref) <= max(1, 0.02 * s_ref)
+    b = G.rhs(gd, g.ndof)
+    x = f.apply_inverse(b)
+    resid = np.linalg.norm(csr @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    tol = 10 * gd["oneshot_resid"] + (1e-13 if str(gd["variant"]) == "mf" else 1e-14)
+    assert np.all(resid <= tol), (resid, gd["oneshot_resid"])
+    rep = H.pcg(csr, b[:, 0], f.apply_inverse, tol=1e-12)
+    assert rep.converged
+    if "u_pcg" in gd:
+        ref = gd["u_pcg"]
+        diff = np.linalg.norm(rep.x - ref) / np.linalg.norm(ref)
+        assert diff <= max(10 * eps, 1e-10), diff
+    assert abs(rep.n_i - int(gd["pcg_iters"])) <= max(1, int(0.2 * int(gd["pcg_iters"])))
+
+
+@pytest.mark.parametrize("name", ["g2d_n32_m4", "g2d_n64_m4_hc", "g3d_n16_m4_x_hc", "g3d_n16_m2_x"])
+def test_gpu_exact_order_matches_oracle(name):
+    """In exact (reference) order the GPU's ranks equal the sequential oracle's
+    and the factors agree as operators."""
+    gd = G.load(name)
+    _, csr = G.build_problem(gd)
+    g, f = _factor(gd, csr, order="exact")
+    og = O.make_grid(int(gd["dim"]), int(gd["n"]), int(gd["m"]))
+    fo = O.factor(csr, og, float(gd["eps"]), str(gd["variant"]), G.skip_levels(gd))
+    ranks = [c for _, c in f.metrics["skeleton_counts"]]
+    ranks_o = [c for _, c in fo.skeleton_counts()]
+    assert G.ranks_within(ranks, ranks_o, rel=0.005), (ranks, ranks_o)
+    assert f.metrics["m_f_bytes"] == pytest.approx(fo.metrics["m_f_bytes"], rel=0.02)
+    b = G.rhs(gd, g.ndof)
+    x, xo = f.apply_inverse(b), fo.apply_inverse(b)
+    r = np.max(np.linalg.norm(csr @ x - b, axis=0) / np.linalg.norm(b, axis=0))
+    ro = np.max(np.linalg.norm(csr @ xo - b, axis=0) / np.linalg.norm(b, axis=0))
+    assert r <= 10 * ro + 1e-14
+
+
+def test_mf_exact_and_matches_oracle_operator():
+    g = H.build_grid(2, 32, 4)
+    a = H.assemble(g, H.high_contrast_field(g, seed=3))
+    f = H.factor_mf(a, g)
+    fo = O.factor(a, O.make_grid(2, 32, 4), 0.0, "mf")
+    b = np.random.default_rng(0).standard_normal((g.ndof, 3))
+    x = f.apply_inverse(b)
+    assert np.linalg.norm(a @ x - b) / np.linalg.norm(b) <= 1e-12
+    assert np.linalg.norm(x - fo.apply_inverse(b)) <= 1e-10 * np.linalg.norm(x)
+    assert f.metrics["s_top"] == fo.metrics["s_top"]
+
+
+def test_mf_top_separator_count():
+    """MF top block is the top-level cross, 2(n-1)-1 DOFs (tests/test_driver.py:35-40)."""
+    g = H.build_grid(2, 64, 4)
+    a = H.assemble(g, H.constant_field(g))
+    f = H.factor_mf(a, g)
+    assert f.metrics["s_top"] == 2 * (64 - 1) - 1
+    assert f.metrics["s_top"] == f.metrics["active_trace"][-1][1]
+
+
+def test_single_dof_grid():
+    g = H.GridConfig(dim=2, n=2, m=2, nlevels=0, h=0.5)
+    a = H.assemble(g, H.constant_field(g))
+    f = H.factor_mf(a, g)
+    assert f.apply_inverse(np.array([16.0]))[0] == pytest.approx(1.0)
+
+
+def test_vector_and_block_rhs_agree():
+    g = H.build_grid(2, 64, 4)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=2))
+    f = H.factor_hifde(a, g, 1e-9)
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((g.ndof, 5))
+    X = f.apply_inverse(B)
+    for j in range(5):
+        xj = f.apply_inverse(B[:, j])
+        assert np.allclose(xj, X[:, j], rtol=1e-12, atol=1e-14 * np.abs(X).max())
+    lin = f.apply_inverse(2.5 * B[:, 0] - 1.5 * B[:, 1])
+    assert np.allclose(lin, 2.5 * X[:, 0] - 1.5 * X[:, 1], atol=1e-10 * np.abs(X).max())
+    # zero right-hand side
+    assert not f.apply_inverse(np.zeros(g.ndof)).any()
+
+
+def test_indefinite_block_raises():
+    """tests/test_driver.py:214-221: a strongly negative shift makes a leaf
+    block indefinite -> IndefiniteBlockError in SPD mode."""
+    g = H.build_grid(2, 4, 2)
+    fld = H.constant_field(g)
+    fld.b[0, 0] = -1e4
+    a = H.assemble(g, fld)
+    with pytest.raises(H.IndefiniteBlockError):
+        H.factor_mf(a, g)
+
+
+def test_hifde3x_rejects_2d():
+    g = H.build_grid(2, 8, 2)
+    a = H.assemble(g, H.constant_field(g))
+    with pytest.raises(ValueError):
+        H.factor_hifde3x(a, g, 1e-6)
+
+
+def test_tiny_eps_behaves_like_mf():
+    g = H.build_grid(2, 16, 2)
+    a = H.assemble(g, H.constant_field(g))
+    f = H.factor_hifde(a, g, 1e-15)
+    b = np.random.default_rng(5).standard_normal(g.ndof)
+    x = f.apply_inverse(b)
+    assert np.linalg.norm(a @ x - b) / np.linalg.norm(b) <= 1e-12
+
+
+def test_verify_noninteracting_passes():
+    g = H.build_grid(3, 16, 4)
+    a = H.assemble(g, H.constant_field(g))
+    f = H.factor_hifde3x(a, g, 1e-6, verify=True)
+    assert f.metrics["s_top"] > 0
