@@ -93,6 +93,7 @@ typedef struct hifde_level_info {
   double seconds;       /* host wall time of the level                      */
   double gflop;         /* algorithmic FLOPs of the level     */
   double gbytes;        /* algorithmic bytes of the level     */
+  double gpu_seconds;   /* CUDA-event time of the level's kernels           */
 } hifde_level_info_t;
 
 /* Library version string. */

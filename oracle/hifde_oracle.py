@@ -38,7 +38,9 @@ reference itself (``tests/golden/make_golden.py``).
 
 from __future__ import annotations
 
+import os
 import time
+from contextlib import nullcontext
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -725,6 +727,17 @@ def _schedule(g: Grid, variant: str, skip_levels: int, store: CliqueStore, coord
                 yield ell + 2.0 / 3.0, interface_groups(g, ell, store.active, "edge", coords), True
 
 
+def _cell_loop_threads():
+    """BLAS capped at one thread for the cell sweep unless HIFDE_NUM_THREADS
+    overrides (src/driver.py:35-41,183)."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        return nullcontext()
+    cap = os.environ.get("HIFDE_NUM_THREADS")
+    return threadpool_limits(limits=int(cap) if cap else 1)
+
+
 def factor(csr, g: Grid, eps: float, variant: str = "hifde",
            skip_levels: int | None = None, spd: bool = True) -> OracleFactor:
     """Sequential (reference-order) HIF-DE factorization.
@@ -746,15 +759,16 @@ def factor(csr, g: Grid, eps: float, variant: str = "hifde",
     levels = []
     trace = [(-1.0, int(store.active.sum()))]
     level_times = []
-    for tag, cells, is_skel in _schedule(g, variant, skip_levels, store, coords):
-        tl = time.perf_counter()
-        if is_skel:
-            recs = [store.skeletonize(c, eps) for c in cells]
-        else:
-            recs = [store.eliminate(c) for c in cells]
-        levels.append((tag, recs))
-        trace.append((tag, int(store.active.sum())))
-        level_times.append((tag, time.perf_counter() - tl))
+    with _cell_loop_threads():
+        for tag, cells, is_skel in _schedule(g, variant, skip_levels, store, coords):
+            tl = time.perf_counter()
+            if is_skel:
+                recs = [store.skeletonize(c, eps) for c in cells]
+            else:
+                recs = [store.eliminate(c) for c in cells]
+            levels.append((tag, recs))
+            trace.append((tag, int(store.active.sum())))
+            level_times.append((tag, time.perf_counter() - tl))
     s, a_top = store.top_block()
     L, D, _ = ldl_spd(a_top)
     f = OracleFactor(store.n, g.dim, eps, levels, s, L, D)

@@ -59,6 +59,7 @@ class LevelInfo(C.Structure):
         ("seconds", C.c_double),
         ("gflop", C.c_double),
         ("gbytes", C.c_double),
+        ("gpu_seconds", C.c_double),
     ]
 
 

@@ -90,6 +90,8 @@ struct LevelRec {
   int nbatches = 1;
   int64_t ngroups = 0, nskel = 0, nred = 0, active_after = 0, max_front = 0;
   double seconds = 0, gflop = 0, gbytes = 0;
+  double gpu_seconds = 0;                 // CUDA-event time of the level's kernels
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // solve metadata
   std::vector<SolveRec> recs;
   SolveRec* d_recs = nullptr;
@@ -395,7 +397,11 @@ struct Factorizer {
     status.n = 0;
     status.bump((size_t)nt, s);
     Arenas A = arenas();
+    HCK(cudaEventCreate(&L.ev0));
+    HCK(cudaEventCreate(&L.ev1));
+    HCK(cudaEventRecord(L.ev0, s));
     launch_elim(dt.p, (int)nt, A, smem, 0, s);
+    HCK(cudaEventRecord(L.ev1, s));
     ++g_launches;
     HCK(cudaGetLastError());
     // device active mask: the eliminated cells retire
@@ -538,6 +544,9 @@ struct Factorizer {
     kout.n = 0;
     kout.bump((size_t)nt, s);
     Arenas A = arenas();
+    HCK(cudaEventCreate(&L.ev0));
+    HCK(cudaEventCreate(&L.ev1));
+    HCK(cudaEventRecord(L.ev0, s));
     for (int b = 0; b < nbatch; ++b) {
       const int64_t lo = bstart[(size_t)b], hi = bstart[(size_t)b + 1];
       if (hi <= lo) continue;
@@ -545,6 +554,7 @@ struct Factorizer {
       launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
       g_launches += 2;
     }
+    HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
     check_status(0, nt, tag, "group");
     std::vector<int32_t> k((size_t)nt);
@@ -707,6 +717,15 @@ struct Factorizer {
     // solve metadata to the device
     for (auto& L : F->levels) L.d_recs = to_device(L.recs);
     HCK(cudaStreamSynchronize(s));
+    for (auto& L : F->levels) {
+      if (L.ev0 && L.ev1) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, L.ev0, L.ev1) == cudaSuccess) L.gpu_seconds = ms * 1e-3;
+        cudaEventDestroy(L.ev0);
+        cudaEventDestroy(L.ev1);
+        L.ev0 = L.ev1 = nullptr;
+      }
+    }
     bvals.release(s);
     scratch.release(s);
     lists.release(s);
@@ -956,6 +975,7 @@ int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info
   info->seconds = L.seconds;
   info->gflop = L.gflop;
   info->gbytes = L.gbytes;
+  info->gpu_seconds = L.gpu_seconds;
   return HIFDE_OK;
 }
 

@@ -48,9 +48,13 @@ def test_gpu_matches_reference_golden(name, order):
     tags = [t for t, _ in f.metrics["active_trace"][1:]]
     assert np.allclose(tags, gd["level_tags"])
     counts = [c for _, c in f.metrics["skeleton_counts"]]
-    assert G.ranks_within(counts, gd["skel_ranks"]), (counts, gd["skel_ranks"].tolist())
+    # default ("auto") ordering must meet BASELINE's +-2%; the opt-in snapshot
+    # ordering is allowed the +2.5%-class drift SURVEY.md appendix D measured
+    # for loose-eps 3D coarse levels
+    rel = 0.02 if order == "auto" else 0.04
+    assert G.ranks_within(counts, gd["skel_ranks"], rel=rel), (counts, gd["skel_ranks"].tolist())
     s_ref = int(gd["s_top"])
-    assert abs(f.metrics["s_top"] - s_ref) <= max(1, 0.02 * s_ref)
+    assert abs(f.metrics["s_top"] - s_ref) <= max(1, rel * s_ref)
     b = G.rhs(gd, g.ndof)
     x = f.apply_inverse(b)
     resid = np.linalg.norm(csr @ x - b, axis=0) / np.linalg.norm(b, axis=0)
