@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(NT) elim_kernel(const ElimTask* __restrict__ t
   double* F = t.scratch_off < 0 ? reinterpret_cast<double*>(smem + ibytes) : A.scratch + t.scratch_off;
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += NT) sdofs[i] = gd[i];
+  for (int i = threadIdx.x; i < nc; i += NT) A.active[gd[i]] = 0;  // the cell retires
   for (int e = threadIdx.x; e < nf * nf; e += NT) F[e] = 0.0;
   __syncthreads();
 

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -91,6 +92,7 @@ struct LevelRec {
   int64_t ngroups = 0, nskel = 0, nred = 0, active_after = 0, max_front = 0;
   double seconds = 0, gflop = 0, gbytes = 0;
   double gpu_seconds = 0;                 // CUDA-event time of the level's kernels
+  double t_part = 0, t_sym = 0, t_upd = 0, t_launch = 0, t_sync = 0;  // host phases
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // solve metadata
   std::vector<SolveRec> recs;
@@ -305,22 +307,38 @@ struct Factorizer {
     }
   }
 
-  void check_status(int64_t off, int64_t cnt, double tag, const char* what) {
-    if (cnt <= 0) return;
-    std::vector<int> st((size_t)cnt);
-    HCK(cudaMemcpyAsync(st.data(), status.p + off, cnt * sizeof(int), cudaMemcpyDeviceToHost, s));
+  struct Pending {
+    int64_t off, cnt;
+    double tag;
+    const char* what;
+  };
+  std::vector<Pending> pending;
+  size_t status_checked = 0;
+  // Per-task status words of every launch since the last check: one D2H copy
+  // at the next synchronization point (no extra stream syncs per level).
+  void check_status() {
+    if (status.n == status_checked) { pending.clear(); return; }
+    const size_t cnt = status.n - status_checked;
+    std::vector<int> st(cnt);
+    HCK(cudaMemcpyAsync(st.data(), status.p + status_checked, cnt * sizeof(int), cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
-    for (int64_t i = 0; i < cnt; ++i)
-      if (st[(size_t)i] != 0) {
-        char buf[256];
-        const char* kind = st[(size_t)i] == 1 ? "matrix is not positive definite" : "singular pivot";
-        snprintf(buf, sizeof buf, "%s (%s %lld of level %g)", kind, what, (long long)i, tag);
-        throw Fail{st[(size_t)i] == 1 ? HIFDE_INDEFINITE : HIFDE_SINGULAR, buf};
+    for (const Pending& P : pending)
+      for (int64_t i = 0; i < P.cnt; ++i) {
+        const int v = st[(size_t)(P.off - (int64_t)status_checked + i)];
+        if (v != 0) {
+          char buf[256];
+          const char* kind = v == 1 ? "matrix is not positive definite" : "singular pivot";
+          snprintf(buf, sizeof buf, "%s (%s %lld of level %g)", kind, P.what, (long long)i, P.tag);
+          throw Fail{v == 1 ? HIFDE_INDEFINITE : HIFDE_SINGULAR, buf};
+        }
       }
+    status_checked = status.n;
+    pending.clear();
   }
 
   // -------------------------------------------------------------------------
   void elimination_level(const Groups& gr, double tag, LevelRec& L, bool is_top) {
+    const double t_begin = now_s();
     const int64_t nt = gr.size();
     L.kind = is_top ? 2 : 0;
     L.ngroups = nt;
@@ -376,6 +394,8 @@ struct Factorizer {
       L.gflop += (dc * dc * dc / 3 + dc * dc * dq + dc * dq + dc * dq * dq) * 1e-9;
       L.gbytes += 8.0 * ((dc + dq) * (dc + dq) + dc * dc + dc + dc * dq + 2 * dq * dq) * 1e-9;
     }
+    double tp = now_s();
+    L.t_sym = tp - t_begin;
     // host structure updates: consumed blocks die, new neighbour blocks live
     for (int64_t t = 0; t < nt; ++t) {
       for (int32_t b : consumed[(size_t)t]) kill_block(b);
@@ -385,6 +405,8 @@ struct Factorizer {
       for (int i = 0; i < T.nc; ++i) active[(size_t)c[i]] = 0;
     }
     (void)idx_level_start;
+    L.t_upd = now_s() - tp;
+    tp = now_s();
     // uploads
     upload_idx();
     upload_blocks();
@@ -394,9 +416,10 @@ struct Factorizer {
     DBuf<ElimTask> dt;
     dt.reserve((size_t)nt, s);
     dt.upload(tasks.data(), 0, (size_t)nt, s);
-    status.n = 0;
-    status.bump((size_t)nt, s);
+    const int64_t st_off = (int64_t)status.bump((size_t)nt, s);
+    pending.push_back({st_off, nt, tag, is_top ? "top block" : "cell"});
     Arenas A = arenas();
+    A.status = status.p + st_off;
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
@@ -404,14 +427,14 @@ struct Factorizer {
     HCK(cudaEventRecord(L.ev1, s));
     ++g_launches;
     HCK(cudaGetLastError());
-    // device active mask: the eliminated cells retire
-    // (kept in sync lazily: only skeleton kernels read it, and they run
-    // after the host re-uploads the mask below)
-    HCK(cudaMemcpyAsync(d_active, active.data(), (size_t)N, cudaMemcpyHostToDevice, s));
-    check_status(0, nt, tag, is_top ? "top block" : "cell");
+    // (the kernel retires the cells in the device active mask itself)
+    L.t_launch = now_s() - tp;
+    tp = now_s();
+    if (is_top) check_status();
     dt.release(s);
     // solve-side reduction structure for the shared neighbour DOFs
     if (!is_top) build_reduction(L);
+    L.t_sync = now_s() - tp;
   }
 
   void build_reduction(LevelRec& L) {
@@ -453,6 +476,7 @@ struct Factorizer {
 
   // -------------------------------------------------------------------------
   void skeleton_level(const Groups& gr, double tag, LevelRec& L) {
+    const double t_begin = now_s();
     const int64_t nt = gr.size();
     L.kind = 1;
     L.ngroups = nt;
@@ -460,6 +484,7 @@ struct Factorizer {
     std::vector<int32_t> hl, blks, q;
     size_t smem = 0;
     scratch.n = 0;
+    const int64_t idx_level_start = (int64_t)h_idx.size();
     // exact-order batch index of every group (groups are neighbours when one
     // holds a DOF of the other's neighbour set)
     std::vector<int> batch((size_t)nt, 0);
@@ -519,6 +544,8 @@ struct Factorizer {
       nbatch = 1;
     }
     L.nbatches = nbatch;
+    double tp = now_s();
+    L.t_sym = tp - t_begin;
     // order tasks by batch (stable keeps the reference order inside a batch)
     std::vector<int64_t> order((size_t)nt);
     for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
@@ -539,11 +566,12 @@ struct Factorizer {
     DBuf<SkelTask> dt;
     dt.reserve((size_t)nt, s);
     dt.upload(sorted.data(), 0, (size_t)nt, s);
-    status.n = 0;
-    status.bump((size_t)nt, s);
+    const int64_t st_off = (int64_t)status.bump((size_t)nt, s);
+    pending.push_back({st_off, nt, tag, "group"});
     kout.n = 0;
     kout.bump((size_t)nt, s);
     Arenas A = arenas();
+    A.status = status.p + st_off;
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
@@ -556,16 +584,19 @@ struct Factorizer {
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
-    check_status(0, nt, tag, "group");
+    L.t_launch = now_s() - tp;
+    tp = now_s();
     std::vector<int32_t> k((size_t)nt);
     HCK(cudaMemcpyAsync(k.data(), kout.p, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    // read back the sk/rd lists written by the kernels
-    for (int64_t t = 0; t < nt; ++t) {
-      const SkelTask& T = tasks[(size_t)t];
-      HCK(cudaMemcpyAsync(h_idx.data() + T.out_off, F->idx.p + T.out_off, (size_t)T.nc * sizeof(int32_t),
+    // read back the sk/rd lists written by the kernels: one copy of this
+    // level's slice of the index arena
+    if ((int64_t)h_idx.size() > idx_level_start)
+      HCK(cudaMemcpyAsync(h_idx.data() + idx_level_start, F->idx.p + idx_level_start,
+                          (h_idx.size() - (size_t)idx_level_start) * sizeof(int32_t),
                           cudaMemcpyDeviceToHost, s));
-    }
-    HCK(cudaStreamSynchronize(s));
+    check_status();  // synchronizes the stream
+    L.t_sync = now_s() - tp;
+    tp = now_s();
     dt.release(s);
     for (int64_t t = 0; t < nt; ++t) {
       const SkelTask& T = tasks[(size_t)t];
@@ -596,6 +627,7 @@ struct Factorizer {
       L.gflop += fl * 1e-9;
       L.gbytes += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
     }
+    L.t_upd = now_s() - tp;
   }
 
   // -------------------------------------------------------------------------
@@ -654,6 +686,7 @@ struct Factorizer {
     bvals.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
 
     const int Lv = g.nlevels;
+    const double t_setup = now_s() - t0;
     auto record_trace = [&](LevelRec& L, double tl) {
       int64_t a = 0;
       for (int64_t i = 0; i < N; ++i) a += active[(size_t)i];
@@ -675,6 +708,7 @@ struct Factorizer {
         if (opt.verify) check_noninteracting(gr, (double)ell);
         F->levels.emplace_back();
         LevelRec& L = F->levels.back();
+        L.t_part = now_s() - tl;
         L.tag = (double)ell;
         elimination_level(gr, L.tag, L, false);
         record_trace(L, tl);
@@ -684,6 +718,7 @@ struct Factorizer {
         Groups gr = interface_groups(g, ell, active.data(), kind);
         F->levels.emplace_back();
         LevelRec& L = F->levels.back();
+        L.t_part = now_s() - tl;
         L.tag = tag;
         skeleton_level(gr, tag, L);
         record_trace(L, tl);
@@ -740,6 +775,16 @@ struct Factorizer {
     cudaFreeAsync(d_active, s);
     HCK(cudaStreamSynchronize(s));
     F->t_f = now_s() - t0;
+    if (getenv("HIFDE_PROFILE")) {
+      fprintf(stderr, "[hifde] factor %.3f ms (setup %.3f ms)\n", F->t_f * 1e3, t_setup * 1e3);
+      for (const auto& L : F->levels)
+        fprintf(stderr,
+                "[hifde] tag %6.3f kind %d groups %7lld batches %3d maxfront %5lld | host ms: part %.3f sym %.3f "
+                "upd %.3f launch %.3f sync %.3f total %.3f | gpu ms %.3f\n",
+                L.tag, L.kind, (long long)L.ngroups, L.nbatches, (long long)L.max_front, L.t_part * 1e3,
+                L.t_sym * 1e3, L.t_upd * 1e3, L.t_launch * 1e3, L.t_sync * 1e3, L.seconds * 1e3,
+                L.gpu_seconds * 1e3);
+    }
   }
 };
 
