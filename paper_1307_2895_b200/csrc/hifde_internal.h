@@ -59,11 +59,18 @@ struct Arenas {
   int32_t* kout;            // per-group skeleton rank
 };
 
+constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA we use
+constexpr int kSchurTile = 64;                 // schur_tile_kernel tile edge
+constexpr int kTrsmPanel = 16;                 // elim_big_kernel TRSM panel width
+
 // Kernel launchers (kernels_factor.cu / kernels_solve.cu).
-void launch_elim(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem,
-                 int smem_cap_doubles, cudaStream_t s);
-void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps,
-                 size_t smem, int smem_cap_doubles, cudaStream_t s);
+void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,
+                       cudaStream_t s);
+void launch_elim_big(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, cudaStream_t s);
+void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
+                        cudaStream_t s);
+void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,
+                 cudaStream_t s);
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s);
 
 // solve

@@ -1,15 +1,23 @@
 // sm_100a kernels of the HIF-DE factorization.
 //
-// One CTA owns one cell (elimination) or one group (skeletonization).  The
-// front is assembled from the original stencil matrix A0 and the live clique
-// blocks, then factored in shared memory when
-// it fits, otherwise in an L2-resident global scratch slab.
+// Work decomposition:
+//   * elim_small_kernel  -- one CTA per cell whose whole front fits in shared
+//                           memory: assembly, Cholesky, TRSM and Schur update.
+//   * elim_big_kernel    -- one CTA per large cell: assembles the c rows of the
+//                           front and the q x q clique part, Cholesky (shared
+//                           memory when it fits) and a panelled TRSM; the
+//                           Schur update U -= W^T W is then done by
+//   * schur_tile_kernel  -- many CTAs per cell, 64 x 64 tiles on FP64 DMMA
+//                           tensor cores (mma.sync m8n8k4 f64).
+//   * skel_kernel        -- one CTA per skeletonization group: ID by
+//                           column-pivoted QR (LAPACK dlaqp2 pivoting and norm
+//                           downdating, early stop at the rank cut), congruence,
+//                           inner elimination of rd against sk, delta block.
 //
 // Reference semantics followed:
 //   elimination   src/factor_ops.py:138-159, src/dense.py:187-219
 //   skeletonize   src/factor_ops.py:162-214
-//   CPQR / ID     src/dense.py:239-264 (LAPACK dgeqp3 / dlaqp2 pivoting and
-//                 column-norm downdating, rank = first |R_jj| <= eps |R_11|)
+//   CPQR / ID     src/dense.py:239-264
 #include <cfloat>
 #include <cstdint>
 
@@ -19,8 +27,6 @@ namespace hifde {
 
 namespace {
 
-constexpr int NT = kThreads;
-constexpr int NWARP = NT / 32;
 constexpr double kSingularRtol = 1e-14;  // src/dense.py:38
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* s, int n, int32_t key) {
@@ -46,20 +52,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Block-wide sum; every thread gets the result.  red must hold NWARP doubles.
-__device__ double block_sum(double v, double* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int w = 0; w < NWARP; ++w) s += red[w];
-  return s;
-}
-
+template <int NT>
 __device__ double block_max(double v, double* red) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -68,126 +63,122 @@ __device__ double block_max(double v, double* red) {
   __syncthreads();
   double s = red[0];
 #pragma unroll
-  for (int w = 1; w < NWARP; ++w) s = fmax(s, red[w]);
+  for (int w = 1; w < NW; ++w) s = fmax(s, red[w]);
   return s;
 }
 
-// Block-wide argmax (largest value, lowest index on ties -- idamax).
-__device__ int block_argmax(double v, int idx, double* redv, int* redi) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-    if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
-  }
-  __syncthreads();
-  if (lane == 0) { redv[wid] = v; redi[wid] = idx; }
-  __syncthreads();
-  double bv = redv[0];
-  int bi = redi[0];
-#pragma unroll
-  for (int w = 1; w < NWARP; ++w) {
-    if (redv[w] > bv || (redv[w] == bv && redi[w] < bi)) { bv = redv[w]; bi = redi[w]; }
-  }
-  return bi;
-}
+__device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// In-place right-looking Cholesky of the n x n lower triangle of A (row-major,
-// leading dimension ld).  Returns HIFDE status: 1 indefinite (a pivot <= 0 or
-// NaN, dpotrf info > 0), 2 singular (min D <= 1e-14 max|diag|), 0 ok.
-__device__ int chol_inplace(double* A, int n, int ld, double* red) {
+// In-place Cholesky of the lower triangle of A (n x n, row-major, ld).
+// Right-looking with the column scaling deferred by one step, so every step
+// needs a single barrier.  Status: 1 indefinite (pivot <= 0 or NaN, dpotrf
+// info > 0), 2 singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
+template <int NT>
+__device__ int chol_1sync(double* A, int n, int ld, double* red) {
   if (n == 0) return 0;
   double sc = 0.0;
   for (int i = threadIdx.x; i < n; i += NT) sc = fmax(sc, fabs(A[(size_t)i * ld + i]));
-  double scale = block_max(sc, red);
+  double scale = block_max<NT>(sc, red);
   if (scale == 0.0) {
     double s2 = 0.0;
     for (int e = threadIdx.x; e < n * n; e += NT) {
-      int i = e / n, j = e - i * n;
+      const int i = e / n, j = e - i * n;
       if (j <= i) s2 = fmax(s2, fabs(A[(size_t)i * ld + j]));
     }
-    scale = block_max(s2, red);
+    scale = block_max<NT>(s2, red);
   }
-  double dmin = DBL_MAX;
+  double dmin = DBL_MAX, prev_piv = 0.0, prev_inv = 0.0;
   for (int k = 0; k < n; ++k) {
     __syncthreads();
     const double akk = A[(size_t)k * ld + k];
-    __syncthreads();
     if (!(akk > 0.0)) return 1;
     const double piv = sqrt(akk);
-    const double inv = 1.0 / piv;
-    dmin = fmin(dmin, piv * piv);
-    if (threadIdx.x == 0) A[(size_t)k * ld + k] = piv;
-    for (int i = k + 1 + threadIdx.x; i < n; i += NT) A[(size_t)i * ld + k] *= inv;
-    __syncthreads();
+    const double rakk = 1.0 / akk;
+    dmin = fmin(dmin, akk);
+    if (k > 0) {  // finish column k-1 (no longer read by anyone)
+      for (int i = k + threadIdx.x; i < n; i += NT) A[(size_t)i * ld + k - 1] *= prev_inv;
+      if (threadIdx.x == 0) A[(size_t)(k - 1) * ld + k - 1] = prev_piv;
+    }
     const int m = n - k - 1;
     for (int e = threadIdx.x; e < m * m; e += NT) {
       const int ii = e / m, jj = e - ii * m;
       if (jj <= ii) {
         const int i = k + 1 + ii, j = k + 1 + jj;
-        A[(size_t)i * ld + j] -= A[(size_t)i * ld + k] * A[(size_t)j * ld + k];
+        A[(size_t)i * ld + j] -= A[(size_t)i * ld + k] * (A[(size_t)j * ld + k] * rakk);
       }
     }
+    prev_piv = piv;
+    prev_inv = 1.0 / piv;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) A[(size_t)(n - 1) * ld + n - 1] = prev_piv;
   __syncthreads();
   if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;
   return 0;
 }
 
-// B (n x m, row-major, ld ldb) <- C^{-1} B with C lower (row-major, ld ldc).
-__device__ void trsm_lower(const double* C, int n, int ldc, double* B, int m, int ldb) {
+// B (n x m, row-major, ldb) <- C^{-1} B, C lower (row-major, ldc); one barrier
+// per row (row scaling deferred by one step).
+template <int NT>
+__device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, int ldb) {
+  double prev = 0.0;
   for (int i = 0; i < n; ++i) {
     __syncthreads();
-    const double cii = C[(size_t)i * ldc + i];
-    for (int j = threadIdx.x; j < m; j += NT) B[(size_t)i * ldb + j] /= cii;
-    __syncthreads();
+    const double cinv = 1.0 / C[(size_t)i * ldc + i];
+    if (i > 0)
+      for (int j = threadIdx.x; j < m; j += NT) B[(size_t)(i - 1) * ldb + j] *= prev;
     const int rows = n - i - 1;
     for (int e = threadIdx.x; e < rows * m; e += NT) {
-      const int l = i + 1 + e / m, j = e % m;
-      B[(size_t)l * ldb + j] -= C[(size_t)l * ldc + i] * B[(size_t)i * ldb + j];
+      const int l = i + 1 + e / m, j = e - (e / m) * m;
+      B[(size_t)l * ldb + j] -= C[(size_t)l * ldc + i] * (B[(size_t)i * ldb + j] * cinv);
     }
+    prev = cinv;
   }
+  __syncthreads();
+  if (n > 0)
+    for (int j = threadIdx.x; j < m; j += NT) B[(size_t)(n - 1) * ldb + j] *= prev;
   __syncthreads();
 }
 
-__device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Elimination: F = A0[c+q, c+q] (minus the q x q part of A0) + sum of consumed
-// clique blocks; C C^T = F_cc; W = C^-1 F_cq; U = F_qq - W^T W.
-// Also used for the terminal block (nq == 0).
+// Small cells: the whole front in shared memory.
+// F = A0[c+q, c] parts + sum of consumed clique blocks; C C^T = F_cc;
+// W = C^-1 F_cq; U = F_qq - W^T W.  Also the terminal block (nq == 0).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) elim_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
+template <int NT>
+__global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[NWARP];
+  __shared__ double red[NT / 32];
   const ElimTask t = tasks[blockIdx.x];
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
   int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
   int32_t* smap = sdofs + nf;
   const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(nf + t.maxnb), 16);
-  double* F = t.scratch_off < 0 ? reinterpret_cast<double*>(smem + ibytes) : A.scratch + t.scratch_off;
+  double* F = reinterpret_cast<double*>(smem + ibytes);
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += NT) sdofs[i] = gd[i];
   for (int i = threadIdx.x; i < nc; i += NT) A.active[gd[i]] = 0;  // the cell retires
   for (int e = threadIdx.x; e < nf * nf; e += NT) F[e] = 0.0;
   __syncthreads();
-
-  // original stencil couplings of the c rows (A0[c,c], A0[c,q] and mirror)
   for (int p = threadIdx.x; p < nc; p += NT) {
     const int g = sdofs[p];
     for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
       const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
       if (pj < 0) continue;
       const double v = A.a0[k];
-      F[(size_t)p * nf + pj] += v;
-      if (pj >= nc) F[(size_t)pj * nf + p] += v;
+      F[p * nf + pj] += v;
+      if (pj >= nc) F[pj * nf + p] += v;
     }
   }
   __syncthreads();
-  // consumed clique blocks, in ascending block id (deterministic extend-add)
   const int32_t* bl = A.lists + t.blk_off;
   for (int b = 0; b < t.nblk; ++b) {
     const int bid = bl[b];
@@ -199,55 +190,213 @@ __global__ void __launch_bounds__(NT) elim_kernel(const ElimTask* __restrict__ t
     for (int e = threadIdx.x; e < nb * nb; e += NT) {
       const int k = e / nb, l = e - k * nb;
       const int pk = smap[k], pl = smap[l];
-      if (pk >= 0 && pl >= 0) F[(size_t)pk * nf + pl] += bv[e];
+      if (pk >= 0 && pl >= 0) F[pk * nf + pl] += bv[e];
     }
     __syncthreads();
   }
-
-  int st = chol_inplace(F, nc, nf, red);
+  const int st = chol_1sync<NT>(F, nc, nf, red);
   if (st != 0) {
     if (threadIdx.x == 0) A.status[blockIdx.x] = st;
     return;
   }
   if (nq > 0) {
-    trsm_lower(F, nc, nf, F + nc, nq, nf);
+    trsm_1sync<NT>(F, nc, nf, F + nc, nq, nf);
     double* U = A.bvals + t.U_off;
     for (int e = threadIdx.x; e < nq * nq; e += NT) {
       const int a = e / nq, b = e - a * nq;
-      double s = F[(size_t)(nc + a) * nf + nc + b];
-      for (int k = 0; k < nc; ++k) s -= F[(size_t)k * nf + nc + a] * F[(size_t)k * nf + nc + b];
+      double s = F[(nc + a) * nf + nc + b];
+      for (int k = 0; k < nc; ++k) s -= F[k * nf + nc + a] * F[k * nf + nc + b];
       U[e] = s;
     }
     double* W = A.fac + t.W_off;
     for (int e = threadIdx.x; e < nc * nq; e += NT) {
       const int i = e / nq, j = e - i * nq;
-      W[e] = F[(size_t)i * nf + nc + j];
+      W[e] = F[i * nf + nc + j];
     }
   }
   double* C = A.fac + t.C_off;
   for (int e = threadIdx.x; e < nc * nc; e += NT) {
     const int i = e / nc, j = e - i * nc;
-    C[e] = (j <= i) ? F[(size_t)i * nf + j] : 0.0;
+    C[e] = (j <= i) ? F[i * nf + j] : 0.0;
   }
   if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
 }
 
 // ---------------------------------------------------------------------------
-// Skeletonization of one group: M = A[c+q, c] (column-major), CPQR of the q
-// rows with early stop at the rank cut, T = R11^-1 R12, congruence, inner
-// elimination of rd against sk, delta clique block -W^T W over sk.
+// Large cells, phase A (one CTA per cell): c rows of the front
+// ([F_cc | F_cq]) and the q x q clique part U; Cholesky of F_cc (shared memory
+// when it fits, otherwise in place in the record); W = C^-1 F_cq by column
+// panels staged in shared memory, written in place in the record.
 // ---------------------------------------------------------------------------
+constexpr int kPanel = kTrsmPanel;
+
+template <int NT>
+__global__ void __launch_bounds__(NT) elim_big_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[NT / 32];
+  const ElimTask t = tasks[blockIdx.x];
+  const int nc = t.nc, nq = t.nq, nf = nc + nq;
+  int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
+  int32_t* smap = sdofs + nf;
+  const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(nf + t.maxnb), 16);
+  double* panel = reinterpret_cast<double*>(smem + ibytes);         // nc x kPanel
+  const bool c_in_smem = t.scratch_off < 0;
+  double* Cg = A.fac + t.C_off;
+  double* F = c_in_smem ? panel + (size_t)nc * kPanel : Cg;          // F_cc, ld nc
+  double* W = A.fac + t.W_off;                                       // nc x nq
+  double* U = A.bvals + t.U_off;                                     // nq x nq
+  const int32_t* gd = A.idx + t.dofs_off;
+  for (int i = threadIdx.x; i < nf; i += NT) sdofs[i] = gd[i];
+  for (int i = threadIdx.x; i < nc; i += NT) A.active[gd[i]] = 0;
+  for (int e = threadIdx.x; e < nc * nc; e += NT) F[e] = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)nc * nq; e += NT) W[e] = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)nq * nq; e += NT) U[e] = 0.0;
+  __syncthreads();
+  for (int p = threadIdx.x; p < nc; p += NT) {
+    const int g = sdofs[p];
+    for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
+      const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
+      if (pj < 0) continue;
+      const double v = A.a0[k];
+      if (pj < nc) F[(size_t)p * nc + pj] += v;
+      else W[(size_t)p * nq + pj - nc] += v;
+    }
+  }
+  __syncthreads();
+  const int32_t* bl = A.lists + t.blk_off;
+  for (int b = 0; b < t.nblk; ++b) {
+    const int bid = bl[b];
+    const int nb = A.blk_n[bid];
+    const int32_t* bd = A.idx + A.blk_dof_off[bid];
+    const double* bv = A.bvals + A.blk_val_off[bid];
+    for (int k = threadIdx.x; k < nb; k += NT) smap[k] = front_pos(sdofs, nc, nq, bd[k]);
+    __syncthreads();
+    for (size_t e = threadIdx.x; e < (size_t)nb * nb; e += NT) {
+      const int k = (int)(e / nb), l = (int)(e - (size_t)k * nb);
+      const int pk = smap[k], pl = smap[l];
+      if (pk < 0 || pl < 0) continue;
+      const double v = bv[e];
+      if (pk < nc) {
+        if (pl < nc) F[(size_t)pk * nc + pl] += v;
+        else W[(size_t)pk * nq + pl - nc] += v;
+      } else if (pl >= nc) {
+        U[(size_t)(pk - nc) * nq + pl - nc] += v;
+      }
+    }
+    __syncthreads();
+  }
+  const int st = chol_1sync<NT>(F, nc, nc, red);
+  if (st != 0) {
+    if (threadIdx.x == 0) A.status[blockIdx.x] = st;
+    return;
+  }
+  // W = C^-1 F_cq, kPanel columns at a time through shared memory
+  for (int j0 = 0; j0 < nq; j0 += kPanel) {
+    const int pw = min(kPanel, nq - j0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * kPanel; e += NT) {
+      const int i = e / kPanel, j = e - i * kPanel;
+      panel[e] = j < pw ? W[(size_t)i * nq + j0 + j] : 0.0;
+    }
+    trsm_1sync<NT>(F, nc, nc, panel, kPanel, kPanel);
+    for (int e = threadIdx.x; e < nc * kPanel; e += NT) {
+      const int i = e / kPanel, j = e - i * kPanel;
+      if (j < pw) W[(size_t)i * nq + j0 + j] = panel[e];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nc * nc; e += NT) {
+    const int i = e / nc, j = e - i * nc;
+    const double v = (j <= i) ? F[e] : 0.0;
+    if (c_in_smem || j > i) Cg[e] = v;
+  }
+  if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Large cells, phase B: U[a,b] -= sum_k W[k,a] W[k,b] on 64 x 64 tiles
+// (upper-triangular tile pairs, mirrored), FP64 DMMA m8n8k4.
+// 128 threads = 2 x 2 warps, each warp a 32 x 32 sub-tile (4 x 4 MMA tiles).
+// ---------------------------------------------------------------------------
+constexpr int kTile = kSchurTile, kKc = 16, kLdS = 68;
+
+__global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restrict__ tasks,
+                                                         const int4* __restrict__ tiles, Arenas A) {
+  __shared__ double Wa[kKc][kLdS];
+  __shared__ double Wb[kKc][kLdS];
+  const int4 tl = tiles[blockIdx.x];
+  const ElimTask t = tasks[tl.x];
+  const int nc = t.nc, nq = t.nq;
+  const int a0 = tl.y * kTile, b0 = tl.z * kTile;
+  const double* W = A.fac + t.W_off;
+  double* U = A.bvals + t.U_off;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wy = wid >> 1, wx = wid & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  for (int k0 = 0; k0 < nc; k0 += kKc) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kKc * kTile; e += 128) {
+      const int kk = e / kTile, aa = e - kk * kTile;
+      const int k = k0 + kk;
+      Wa[kk][aa] = (k < nc && a0 + aa < nq) ? W[(size_t)k * nq + a0 + aa] : 0.0;
+      Wb[kk][aa] = (k < nc && b0 + aa < nq) ? W[(size_t)k * nq + b0 + aa] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kKc; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = Wa[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bf[n] = Wb[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+    }
+  }
+  const bool diag = tl.y == tl.z;
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = a0 + wy * 32 + m * 8 + (lane >> 2);
+        const int b = b0 + wx * 32 + n * 8 + 2 * (lane & 3) + h;
+        if (a >= nq || b >= nq) continue;
+        if (diag && b > a) continue;
+        const double v = U[(size_t)a * nq + b] - acc[m][n][h];
+        U[(size_t)a * nq + b] = v;
+        if (a != b) U[(size_t)b * nq + a] = v;
+      }
+}
+
+// ---------------------------------------------------------------------------
+// Skeletonization of one group.
+//   M = A[c+q, c]: A_cc (nc x nc) and Mq = A_qc (nq x nc), column-major.
+//   CPQR of Mq: per step one warp picks the pivot, swaps and builds the
+//   Householder reflector; all warps then update the trailing columns
+//   (warp per column) and downdate their norms -- two barriers per step.
+//   The Householder vectors are never needed again (only R), so they are not
+//   even scaled into place.
+// ---------------------------------------------------------------------------
+template <int NT>
 __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ tasks, Arenas A,
                                                   double eps) {
+  constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[NWARP];
-  __shared__ int redi[NWARP];
+  __shared__ double red[NW];
+  __shared__ double sh_beta, sh_tau, sh_scal;
+  __shared__ int sh_stop, sh_k;
   const SkelTask t = tasks[blockIdx.x];
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
-  const int ld = nf;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
-  // integer workspace (always shared)
   int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
   int32_t* salive = sdofs + nf;
   int32_t* smap = salive + nf;
@@ -258,15 +407,17 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   int32_t* rdo = sko + nc;
   const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(2 * nf + t.maxnb + 5 * nc), 16);
   double* ws = t.scratch_off < 0 ? reinterpret_cast<double*>(smem + ibytes) : A.scratch + t.scratch_off;
-  const size_t q4 = (size_t)nc * nc / 4 + nc;
-  double* M = ws;                                  // nf x nc, column-major
-  double* vn1 = M + (size_t)nf * nc;
+  const int ldq = nq;                                  // Mq column-major, ld nq
+  double* Acc = ws;                                    // nc x nc, row-major (symmetric)
+  double* Mq = Acc + (size_t)nc * nc;                  // nq x nc
+  double* vn1 = Mq + (size_t)nq * nc;
   double* vn2 = vn1 + nc;
-  double* Tp = vn2 + nc;                           // k x r, pivot order
-  double* Ts = Tp + q4;                            // k x r, sorted
-  double* Bsr = Ts + q4;                           // k x r
-  double* Wm = Bsr + q4;                           // r x k
-  double* Brr = Wm + q4;                           // r x r
+  double* Z = vn2 + nc;                                // post-CPQR workspace
+  const size_t q4 = (size_t)nc * nc / 4 + nc;
+  double* Ts = Z;                                      // k x r
+  double* Bsr = Ts + q4;                               // k x r
+  double* Wm = Bsr + q4;                               // r x k
+  double* Brr = Wm + q4;                               // r x r
 
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += NT) {
@@ -275,17 +426,17 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
     salive[i] = (i < nc) ? 1 : (int)A.active[g];
   }
   for (int i = threadIdx.x; i < nc; i += NT) perm[i] = i;
-  for (size_t e = threadIdx.x; e < (size_t)nf * nc; e += NT) M[e] = 0.0;
+  for (int e = threadIdx.x; e < nc * nc; e += NT) Acc[e] = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)nq * nc; e += NT) Mq[e] = 0.0;
   __syncthreads();
-
   for (int p = threadIdx.x; p < nc; p += NT) {
     const int g = sdofs[p];
     for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
       const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
       if (pj < 0 || !salive[pj]) continue;
       const double v = A.a0[k];
-      if (pj < nc) M[p + (size_t)pj * ld] += v;
-      else M[pj + (size_t)p * ld] += v;
+      if (pj < nc) Acc[p * nc + pj] += v;
+      else Mq[(pj - nc) + (size_t)p * ldq] += v;
     }
   }
   __syncthreads();
@@ -303,135 +454,143 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
     for (int e = threadIdx.x; e < nb * nb; e += NT) {
       const int k = e / nb, l = e - k * nb;
       const int pk = smap[k], pl = smap[l];
-      if (pk >= 0 && pl >= 0 && pl < nc) M[pk + (size_t)pl * ld] += bv[e];
+      if (pk < 0 || pl < 0 || pl >= nc) continue;
+      if (pk < nc) Acc[pk * nc + pl] += bv[e];
+      else Mq[(pk - nc) + (size_t)pl * ldq] += bv[e];
     }
     __syncthreads();
   }
 
-  // ---- column-pivoted QR of Mq = M[nc:, :] (dlaqp2 semantics) ----------
-  double* Mq = M + nc;
+  // ---- CPQR of Mq ------------------------------------------------------
   int nq_alive = 0;
-  for (int i = nc + threadIdx.x; i < nf; i += NT) nq_alive += salive[i];
-  nq_alive = (int)block_sum((double)nq_alive, red);
-  for (int j = wid; j < nc; j += NWARP) {
+  if (threadIdx.x == 0) {
+    for (int i = nc; i < nf; ++i) nq_alive += salive[i];
+    sh_k = nq_alive;
+  }
+  for (int j = wid; j < nc; j += NW) {
     double s = 0.0;
-    for (int r = lane; r < nq; r += 32) { const double x = Mq[r + (size_t)j * ld]; s += x * x; }
+    const double* col = Mq + (size_t)j * ldq;
+    for (int r = lane; r < nq; r += 32) s += col[r] * col[r];
     s = warp_sum(s);
     if (lane == 0) { vn1[j] = sqrt(s); vn2[j] = vn1[j]; }
   }
   __syncthreads();
+  nq_alive = sh_k;
   const int kmax = nq < nc ? nq : nc;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);  // sqrt(dlamch('E'))
-  int k = kmax;
   double thr = 0.0;
+  int k = kmax;
   for (int i = 0; i < kmax; ++i) {
-    double bv = -1.0;
-    int bi = nc;
-    for (int j = i + threadIdx.x; j < nc; j += NT) {
-      const double v = vn1[j];
-      if (v > bv || (v == bv && j < bi)) { bv = v; bi = j; }
-    }
-    const int pvt = block_argmax(bv, bi, red, redi);
-    if (i == 0 && vn1[pvt] == 0.0) { k = 0; break; }   // zero block: all redundant
-    __syncthreads();
-    if (pvt != i) {
-      for (int r = threadIdx.x; r < nq; r += NT) {
-        const double a = Mq[r + (size_t)i * ld];
-        Mq[r + (size_t)i * ld] = Mq[r + (size_t)pvt * ld];
-        Mq[r + (size_t)pvt * ld] = a;
+    if (wid == 0) {
+      // pivot: largest partial norm, lowest index on ties (idamax)
+      double bv = -1.0;
+      int bi = nc;
+      for (int j = i + lane; j < nc; j += 32) {
+        const double v = vn1[j];
+        if (v > bv) { bv = v; bi = j; }
       }
-      if (threadIdx.x == 0) {
-        const int pi = perm[i]; perm[i] = perm[pvt]; perm[pvt] = pi;
-        vn1[pvt] = vn1[i];
-        vn2[pvt] = vn2[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
       }
+      const int pvt = bi;
+      int stop = 0;
+      if (i == 0 && vn1[pvt] == 0.0) stop = 2;  // zero block: everything redundant
+      if (!stop) {
+        if (pvt != i) {
+          double* ci = Mq + (size_t)i * ldq;
+          double* cp = Mq + (size_t)pvt * ldq;
+          for (int r = lane; r < nq; r += 32) { const double x = ci[r]; ci[r] = cp[r]; cp[r] = x; }
+          if (lane == 0) {
+            const int pi = perm[i]; perm[i] = perm[pvt]; perm[pvt] = pi;
+            vn1[pvt] = vn1[i];
+            vn2[pvt] = vn2[i];
+          }
+        }
+        __syncwarp();
+        const double* ci = Mq + (size_t)i * ldq;
+        double xs = 0.0;
+        for (int r = i + 1 + lane; r < nq; r += 32) xs += ci[r] * ci[r];
+        const double xnorm = sqrt(warp_sum(xs));
+        const double alpha = ci[i];
+        double beta, tau, scal;
+        if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
+        else {
+          beta = -copysign(hypot(alpha, xnorm), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
+        const double rii = fabs(beta);
+        if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
+        if (rii <= thr) stop = 1;
+        if (lane == 0) { sh_beta = beta; sh_tau = tau; sh_scal = scal; }
+      }
+      if (lane == 0) sh_stop = stop;
     }
     __syncthreads();
-    // Householder reflector of Mq[i:, i] (dlarfg)
-    double xs = 0.0;
-    for (int r = i + 1 + threadIdx.x; r < nq; r += NT) { const double x = Mq[r + (size_t)i * ld]; xs += x * x; }
-    const double xnorm = sqrt(block_sum(xs, red));
-    const double alpha = Mq[i + (size_t)i * ld];
-    double beta, tau;
-    if (xnorm == 0.0) { beta = alpha; tau = 0.0; }
-    else { beta = -copysign(hypot(alpha, xnorm), alpha); tau = (beta - alpha) / beta; }
-    const double rii = fabs(beta);
-    if (i == 0) {
-      thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
-    }
-    if (rii <= thr) { k = i; break; }
-    __syncthreads();
-    if (xnorm != 0.0) {
-      const double scal = 1.0 / (alpha - beta);
-      for (int r = i + 1 + threadIdx.x; r < nq; r += NT) Mq[r + (size_t)i * ld] *= scal;
-    }
-    if (threadIdx.x == 0) Mq[i + (size_t)i * ld] = beta;
-    __syncthreads();
-    // apply H_i to the trailing columns and downdate their norms (warp/column)
-    for (int j = i + 1 + wid; j < nc; j += NWARP) {
-      double* col = Mq + (size_t)j * ld;
-      const double* v = Mq + (size_t)i * ld;
+    if (sh_stop) { k = sh_stop == 2 ? 0 : i; break; }
+    const double tau = sh_tau, scal = sh_scal;
+    const double* v = Mq + (size_t)i * ldq;  // v_r = scal * v[r] for r > i
+    for (int j = i + 1 + wid; j < nc; j += NW) {
+      double* col = Mq + (size_t)j * ldq;
       if (tau != 0.0) {
-        double s = (lane == 0) ? col[i] : 0.0;
+        double s = 0.0;
         for (int r = i + 1 + lane; r < nq; r += 32) s += v[r] * col[r];
-        s = warp_sum(s) * tau;
-        if (lane == 0) col[i] -= s;
-        for (int r = i + 1 + lane; r < nq; r += 32) col[r] -= s * v[r];
+        s = warp_sum(s);
+        const double w = tau * (col[i] + scal * s);
+        __syncwarp();
+        if (lane == 0) col[i] -= w;
+        const double ws2 = w * scal;
+        for (int r = i + 1 + lane; r < nq; r += 32) col[r] -= ws2 * v[r];
+        __syncwarp();
       }
-      __syncwarp();
       double nv = vn1[j];
-      int recompute = 0;
+      bool recompute = false;
       if (nv != 0.0) {
         double tmp = fabs(col[i]) / nv;
         tmp = 1.0 - tmp * tmp;
         tmp = tmp > 0.0 ? tmp : 0.0;
         const double ratio = nv / vn2[j];
-        const double tmp2 = tmp * ratio * ratio;
-        if (tmp2 <= tol3z) recompute = 1;
-        else nv = nv * sqrt(tmp);
+        if (tmp * ratio * ratio <= tol3z) recompute = true;
+        else nv *= sqrt(tmp);
       }
       if (recompute) {
         double s = 0.0;
         for (int r = i + 1 + lane; r < nq; r += 32) s += col[r] * col[r];
         s = warp_sum(s);
         nv = (i + 1 < nq) ? sqrt(s) : 0.0;
-        if (lane == 0) { vn1[j] = nv; vn2[j] = nv; }
-      } else if (lane == 0) {
-        vn1[j] = nv;
+        if (lane == 0) vn2[j] = nv;
       }
+      if (lane == 0) vn1[j] = nv;
     }
+    if (threadIdx.x == 0) Mq[i + (size_t)i * ldq] = sh_beta;  // R_ii (column i no longer read)
     __syncthreads();
   }
   __syncthreads();
   const int r = nc - k;
 
-  // T = R11^-1 R12 (back substitution, in place on Mq rows 0..k-1)
-  for (int i = k - 1; i >= 0; --i) {
-    __syncthreads();
-    const double d = Mq[i + (size_t)i * ld];
-    for (int j = threadIdx.x; j < r; j += NT) Mq[i + (size_t)(k + j) * ld] /= d;
-    __syncthreads();
-    for (int e = threadIdx.x; e < i * r; e += NT) {
-      const int l = e % i, j = e / i;
-      Mq[l + (size_t)(k + j) * ld] -= Mq[l + (size_t)i * ld] * Mq[i + (size_t)(k + j) * ld];
+  // T = R11^-1 R12 (back substitution, one thread per column of R12)
+  for (int j = threadIdx.x; j < r; j += NT) {
+    double* col = Mq + (size_t)(k + j) * ldq;
+    for (int i = k - 1; i >= 0; --i) {
+      double s = col[i];
+      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)l * ldq] * col[l];
+      col[i] = s / Mq[i + (size_t)i * ldq];
     }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < k * r; e += NT) {
-    const int a = e / r, b = e - a * r;
-    Tp[e] = Mq[a + (size_t)(k + b) * ld];
   }
   // ascending sk / rd with their pivot positions
   for (int a = threadIdx.x; a < nc; a += NT) {
-    const int v = perm[a];
+    const int pv = perm[a];
     int rank = 0;
     if (a < k) {
-      for (int b = 0; b < k; ++b) rank += perm[b] < v;
-      skl[rank] = v;
+      for (int b = 0; b < k; ++b) rank += perm[b] < pv;
+      skl[rank] = pv;
       sko[rank] = a;
     } else {
-      for (int b = k; b < nc; ++b) rank += perm[b] < v;
-      rdl[rank] = v;
+      for (int b = k; b < nc; ++b) rank += perm[b] < pv;
+      rdl[rank] = pv;
       rdo[rank] = a - k;
     }
   }
@@ -446,55 +605,52 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   }
   for (int e = threadIdx.x; e < k * r; e += NT) {
     const int a = e / r, b = e - a * r;
-    Ts[e] = Tp[(size_t)sko[a] * r + rdo[b]];
+    Ts[e] = Mq[sko[a] + (size_t)(k + rdo[b]) * ldq];
   }
   __syncthreads();
   // B_sr = A_sr - A_ss T
-#define ACC(x, y) M[(size_t)(x) + (size_t)(y) * ld]
   for (int e = threadIdx.x; e < k * r; e += NT) {
     const int a = e / r, b = e - a * r;
-    const int sa = skl[a];
-    double s = ACC(sa, rdl[b]);
-    for (int l = 0; l < k; ++l) s -= ACC(sa, skl[l]) * Ts[(size_t)l * r + b];
+    const double* arow = Acc + skl[a] * nc;
+    double s = arow[rdl[b]];
+    for (int l = 0; l < k; ++l) s -= arow[skl[l]] * Ts[l * r + b];
     Bsr[e] = s;
   }
   __syncthreads();
-  // B_rr = A_rr - A_sr^T T - T^T B_sr
+  // B_rr = A_rr - A_sr^T T - T^T B_sr  (then symmetrized)
   for (int e = threadIdx.x; e < r * r; e += NT) {
     const int a = e / r, b = e - a * r;
-    double s = ACC(rdl[a], rdl[b]);
+    double s = Acc[rdl[a] * nc + rdl[b]];
     for (int l = 0; l < k; ++l)
-      s -= ACC(skl[l], rdl[a]) * Ts[(size_t)l * r + b] + Ts[(size_t)l * r + a] * Bsr[(size_t)l * r + b];
+      s -= Acc[skl[l] * nc + rdl[a]] * Ts[l * r + b] + Ts[l * r + a] * Bsr[l * r + b];
     Brr[e] = s;
   }
-#undef ACC
   __syncthreads();
   for (int e = threadIdx.x; e < r * r; e += NT) {
     const int a = e / r, b = e - a * r;
     if (a < b) {
-      const double m = 0.5 * (Brr[e] + Brr[(size_t)b * r + a]);
+      const double m = 0.5 * (Brr[e] + Brr[b * r + a]);
       Brr[e] = m;
-      Brr[(size_t)b * r + a] = m;
+      Brr[b * r + a] = m;
     }
   }
   __syncthreads();
-  const int st = chol_inplace(Brr, r, r, red);
+  const int st = chol_1sync<NT>(Brr, r, r, red);
   if (st != 0) {
     if (threadIdx.x == 0) A.status[t.group] = st;
     return;
   }
-  // W = C^-1 B_sr^T (r x k)
   for (int e = threadIdx.x; e < r * k; e += NT) {
     const int a = e / k, b = e - a * k;
-    Wm[e] = Bsr[(size_t)b * r + a];
+    Wm[e] = Bsr[b * r + a];
   }
+  if (k > 0) trsm_1sync<NT>(Brr, r, r, Wm, k, k);
   __syncthreads();
-  if (k > 0) trsm_lower(Brr, r, r, Wm, k, k);
   double* dl = A.bvals + t.delta_off;
   for (int e = threadIdx.x; e < k * k; e += NT) {
     const int a = e / k, b = e - a * k;
     double s = 0.0;
-    for (int l = 0; l < r; ++l) s -= Wm[(size_t)l * k + a] * Wm[(size_t)l * k + b];
+    for (int l = 0; l < r; ++l) s -= Wm[l * k + a] * Wm[l * k + b];
     dl[e] = s;
   }
   double* rec = A.fac + t.rec_off;
@@ -504,8 +660,8 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
     const int a = e / r, b = e - a * r;
     C[e] = (b <= a) ? Brr[e] : 0.0;
   }
-  double* W = C + (size_t)r * r;
-  for (int e = threadIdx.x; e < r * k; e += NT) W[e] = Wm[e];
+  double* Wo = C + (size_t)r * r;
+  for (int e = threadIdx.x; e < r * k; e += NT) Wo[e] = Wm[e];
   if (threadIdx.x == 0) A.status[t.group] = 0;
 }
 
@@ -517,26 +673,52 @@ __global__ void apply_rd_kernel(const SkelTask* __restrict__ tasks, Arenas A) {
   for (int a = k + threadIdx.x; a < t.nc; a += blockDim.x) A.active[out[a]] = 0;
 }
 
-void launch_elim(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem,
-                 int /*smem_cap_doubles*/, cudaStream_t s) {
-  if (ntasks <= 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(elim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  elim_kernel<<<ntasks, NT, smem, s>>>(d_tasks, A);
+// ---------------------------------------------------------------------------
+template <class K>
+static void allow_smem(K kern) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
 }
 
-void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem,
-                 int /*smem_cap_doubles*/, cudaStream_t s) {
+void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,
+                       cudaStream_t s) {
   if (ntasks <= 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(skel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
+  static bool once = false;
+  if (!once) {
+    allow_smem(elim_small_kernel<128>);
+    allow_smem(elim_small_kernel<256>);
+    once = true;
   }
-  skel_kernel<<<ntasks, NT, smem, s>>>(d_tasks, A, eps);
+  if (nt <= 128) elim_small_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A);
+  else elim_small_kernel<256><<<ntasks, 256, smem, s>>>(d_tasks, A);
+}
+
+void launch_elim_big(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, cudaStream_t s) {
+  if (ntasks <= 0) return;
+  static bool once = false;
+  if (!once) {
+    allow_smem(elim_big_kernel<512>);
+    once = true;
+  }
+  elim_big_kernel<512><<<ntasks, 512, smem, s>>>(d_tasks, A);
+}
+
+void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
+                        cudaStream_t s) {
+  if (ntiles <= 0) return;
+  schur_tile_kernel<<<ntiles, 128, 0, s>>>(d_tasks, d_tiles, A);
+}
+
+void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,
+                 cudaStream_t s) {
+  if (ntasks <= 0) return;
+  static bool once = false;
+  if (!once) {
+    allow_smem(skel_kernel<128>);
+    allow_smem(skel_kernel<512>);
+    once = true;
+  }
+  if (nt <= 128) skel_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A, eps);
+  else skel_kernel<512><<<ntasks, 512, smem, s>>>(d_tasks, A, eps);
 }
 
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s) {

@@ -20,34 +20,45 @@ namespace {
 
 constexpr int NT = kThreads;
 
-// x (n x nrhs, row-major) <- C^{-1} x, C lower n x n row-major.
+// x (n x nrhs, row-major) <- C^{-1} x, C lower n x n row-major.  One barrier
+// per row: row i's scaling by 1/C_ii is deferred to the next step.
 __device__ void fwd_subst(const double* __restrict__ C, int n, double* x, int nrhs) {
+  double prev = 0.0;
   for (int i = 0; i < n; ++i) {
     __syncthreads();
-    const double d = C[(size_t)i * n + i];
-    for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)i * nrhs + r] /= d;
-    __syncthreads();
+    const double cinv = 1.0 / C[(size_t)i * n + i];
+    if (i > 0)
+      for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)(i - 1) * nrhs + r] *= prev;
     const int rows = n - i - 1;
     for (int e = threadIdx.x; e < rows * nrhs; e += NT) {
-      const int l = i + 1 + e / nrhs, r = e % nrhs;
-      x[(size_t)l * nrhs + r] -= C[(size_t)l * n + i] * x[(size_t)i * nrhs + r];
+      const int l = i + 1 + e / nrhs, r = e - (e / nrhs) * nrhs;
+      x[(size_t)l * nrhs + r] -= C[(size_t)l * n + i] * (x[(size_t)i * nrhs + r] * cinv);
     }
+    prev = cinv;
   }
+  __syncthreads();
+  if (n > 0)
+    for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)(n - 1) * nrhs + r] *= prev;
   __syncthreads();
 }
 
-// x <- C^{-T} x.
+// x <- C^{-T} x (same deferred-scaling scheme, bottom-up).
 __device__ void bwd_subst(const double* __restrict__ C, int n, double* x, int nrhs) {
+  double prev = 0.0;
   for (int i = n - 1; i >= 0; --i) {
     __syncthreads();
-    const double d = C[(size_t)i * n + i];
-    for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)i * nrhs + r] /= d;
-    __syncthreads();
+    const double cinv = 1.0 / C[(size_t)i * n + i];
+    if (i < n - 1)
+      for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)(i + 1) * nrhs + r] *= prev;
     for (int e = threadIdx.x; e < i * nrhs; e += NT) {
-      const int l = e / nrhs, r = e % nrhs;
-      x[(size_t)l * nrhs + r] -= C[(size_t)i * n + l] * x[(size_t)i * nrhs + r];
+      const int l = e / nrhs, r = e - l * nrhs;
+      x[(size_t)l * nrhs + r] -= C[(size_t)i * n + l] * (x[(size_t)i * nrhs + r] * cinv);
     }
+    prev = cinv;
   }
+  __syncthreads();
+  if (n > 0)
+    for (int r = threadIdx.x; r < nrhs; r += NT) x[r] *= prev;
   __syncthreads();
 }
 

@@ -45,7 +45,7 @@ struct Fail {
       throw Fail{HIFDE_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};          \
   } while (0)
 
-constexpr size_t kSmemCap = 200 * 1024;  // dynamic shared memory per CTA we allow
+constexpr size_t kSmemCap = kSmemCapBytes;
 
 double now_s() {
   using namespace std::chrono;
@@ -343,12 +343,13 @@ struct Factorizer {
     L.kind = is_top ? 2 : 0;
     L.ngroups = nt;
     std::vector<ElimTask> tasks((size_t)nt);
+    std::vector<uint8_t> is_big((size_t)nt, 0);
     std::vector<std::vector<int32_t>> consumed((size_t)nt);
     std::vector<int32_t> hl;  // block lists of this level
     std::vector<int32_t> q;
-    size_t smem = 0;
+    size_t smem_small = 0, smem_big = 0;
+    int max_small_nf = 0;
     scratch.n = 0;
-    const int64_t idx_level_start = (int64_t)h_idx.size();
     for (int64_t t = 0; t < nt; ++t) {
       const int32_t* c = gr.begin(t);
       const int nc = gr.count(t);
@@ -368,10 +369,14 @@ struct Factorizer {
       const size_t need = ib + sizeof(double) * (size_t)nf * nf;
       if (need <= kSmemCap) {
         T.scratch_off = -1;
-        smem = std::max(smem, need);
+        smem_small = std::max(smem_small, need);
+        max_small_nf = std::max(max_small_nf, nf);
       } else {
-        T.scratch_off = (int64_t)scratch.bump((size_t)nf * nf, s);
-        smem = std::max(smem, ib);
+        is_big[(size_t)t] = 1;
+        const size_t pan = sizeof(double) * (size_t)nc * kTrsmPanel;
+        const size_t with_c = ib + pan + sizeof(double) * (size_t)nc * nc;
+        if (with_c <= kSmemCap) { T.scratch_off = -1; smem_big = std::max(smem_big, with_c); }
+        else { T.scratch_off = 0; smem_big = std::max(smem_big, ib + pan); }
       }
       T.C_off = (int64_t)F->fac.bump((size_t)nc * nc, s);
       T.W_off = (int64_t)F->fac.bump((size_t)nc * nq, s);
@@ -404,34 +409,66 @@ struct Factorizer {
       const int32_t* c = gr.begin(t);
       for (int i = 0; i < T.nc; ++i) active[(size_t)c[i]] = 0;
     }
-    (void)idx_level_start;
     L.t_upd = now_s() - tp;
     tp = now_s();
+    // split into the shared-memory path and the large-front path (+ tiles)
+    std::vector<ElimTask> small, big;
+    std::vector<int4> tiles;
+    for (int64_t t = 0; t < nt; ++t) {
+      const ElimTask& T = tasks[(size_t)t];
+      if (!is_big[(size_t)t]) { small.push_back(T); continue; }
+      const int bi = (int)big.size();
+      big.push_back(T);
+      const int ntl = (T.nq + kSchurTile - 1) / kSchurTile;
+      for (int a = 0; a < ntl; ++a)
+        for (int b = a; b < ntl; ++b) tiles.push_back(make_int4(bi, a, b, 0));
+    }
     // uploads
     upload_idx();
     upload_blocks();
     lists.reserve(std::max<size_t>(hl.size(), 1), s);
     lists.n = hl.size();
     lists.upload(hl.data(), 0, hl.size(), s);
-    DBuf<ElimTask> dt;
-    dt.reserve((size_t)nt, s);
-    dt.upload(tasks.data(), 0, (size_t)nt, s);
-    const int64_t st_off = (int64_t)status.bump((size_t)nt, s);
-    pending.push_back({st_off, nt, tag, is_top ? "top block" : "cell"});
+    DBuf<ElimTask> d_small, d_big;
+    DBuf<int4> d_tiles;
+    d_small.reserve(small.size(), s);
+    d_small.upload(small.data(), 0, small.size(), s);
+    d_big.reserve(big.size(), s);
+    d_big.upload(big.data(), 0, big.size(), s);
+    d_tiles.reserve(tiles.size(), s);
+    d_tiles.upload(tiles.data(), 0, tiles.size(), s);
+    const int64_t st_small = (int64_t)status.bump(small.size(), s);
+    const int64_t st_big = (int64_t)status.bump(big.size(), s);
+    const char* what = is_top ? "top block" : "cell";
+    pending.push_back({st_small, (int64_t)small.size(), tag, what});
+    pending.push_back({st_big, (int64_t)big.size(), tag, what});
     Arenas A = arenas();
-    A.status = status.p + st_off;
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
-    launch_elim(dt.p, (int)nt, A, smem, 0, s);
+    if (!small.empty()) {
+      A.status = status.p + st_small;
+      launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= 64 ? 128 : 256, s);
+      ++g_launches;
+    }
+    if (!big.empty()) {
+      A.status = status.p + st_big;
+      launch_elim_big(d_big.p, (int)big.size(), A, smem_big, s);
+      ++g_launches;
+      if (!tiles.empty()) {
+        launch_schur_tiles(d_big.p, d_tiles.p, (int)tiles.size(), A, s);
+        ++g_launches;
+      }
+    }
     HCK(cudaEventRecord(L.ev1, s));
-    ++g_launches;
     HCK(cudaGetLastError());
-    // (the kernel retires the cells in the device active mask itself)
+    // (the kernels retire the cells in the device active mask themselves)
     L.t_launch = now_s() - tp;
     tp = now_s();
     if (is_top) check_status();
-    dt.release(s);
+    d_small.release(s);
+    d_big.release(s);
+    d_tiles.release(s);
     // solve-side reduction structure for the shared neighbour DOFs
     if (!is_top) build_reduction(L);
     L.t_sync = now_s() - tp;
@@ -483,6 +520,7 @@ struct Factorizer {
     std::vector<SkelTask> tasks((size_t)nt);
     std::vector<int32_t> hl, blks, q;
     size_t smem = 0;
+    int max_nc = 0, max_nq = 0;
     scratch.n = 0;
     const int64_t idx_level_start = (int64_t)h_idx.size();
     // exact-order batch index of every group (groups are neighbours when one
@@ -515,7 +553,9 @@ struct Factorizer {
       hl.insert(hl.end(), blks.begin(), blks.end());
       const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 5 * nc));
       const size_t q4 = (size_t)nc * nc / 4 + nc;
-      const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 4 * q4 + (size_t)nc * nc;
+      const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + (size_t)nc * nc;
+      max_nc = std::max(max_nc, nc);
+      max_nq = std::max(max_nq, nq);
       const size_t need = ib + sizeof(double) * wsd;
       if (need <= kSmemCap) {
         T.scratch_off = -1;
@@ -578,7 +618,7 @@ struct Factorizer {
     for (int b = 0; b < nbatch; ++b) {
       const int64_t lo = bstart[(size_t)b], hi = bstart[(size_t)b + 1];
       if (hi <= lo) continue;
-      launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, 0, s);
+      launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
       launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
       g_launches += 2;
     }
