@@ -45,7 +45,7 @@ def _stale() -> bool:
 def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3",
+    cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3,-fopenmp", "-lgomp",
            "-shared", "-cudart", "static", "--threads", "4",
            "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            *[os.path.join(PKG, s) for s in SOURCES]]

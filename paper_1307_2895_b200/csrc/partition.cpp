@@ -16,14 +16,29 @@
 
 namespace hifde {
 
+void Coords::build(const GridDesc& g) {
+  dim = g.dim;
+  const int64_t N = g.ndof();
+  const int s = g.side();
+  for (int ax = 0; ax < g.dim; ++ax) x[ax].resize((size_t)N);
+  int c[3] = {1, 1, 1};
+  for (int64_t d = 0; d < N; ++d) {
+    for (int ax = 0; ax < g.dim; ++ax) x[ax][(size_t)d] = (int16_t)c[ax];
+    for (int ax = 0; ax < g.dim; ++ax) {  // odometer, first axis fastest
+      if (++c[ax] <= s) break;
+      c[ax] = 1;
+    }
+  }
+}
+
 namespace {
 
 // Bucket the selected DOFs (ascending) by key in [0, nkeys): counting sort,
 // which keeps members ascending inside each bucket.  Empty buckets dropped.
-Groups bucket(const std::vector<int32_t>& dofs, const std::vector<int64_t>& keys, int64_t nkeys) {
+Groups bucket(const std::vector<int32_t>& dofs, const std::vector<int32_t>& keys, int64_t nkeys) {
   Groups out;
   std::vector<int64_t> cnt((size_t)nkeys + 1, 0);
-  for (int64_t k : keys) cnt[(size_t)k + 1]++;
+  for (int32_t k : keys) cnt[(size_t)k + 1]++;
   for (int64_t i = 0; i < nkeys; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
   out.members.resize(dofs.size());
   std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
@@ -42,62 +57,57 @@ inline int64_t ipow(int64_t b, int e) {
 }
 
 // nearest centre w*j, j in [1, top], ties to the lower j (doubled coords x2)
-inline int64_t near_mult(int64_t x2, int64_t w, int64_t top) {
-  int64_t j = (x2 + w - 1) / (2 * w);
-  return std::min(std::max(j, (int64_t)1), top);
+inline int near_mult(int x2, int w, int top) {
+  int j = (x2 + w - 1) / (2 * w);
+  return std::min(std::max(j, 1), top);
 }
 // nearest centre w*(j - 1/2), j in [1, top], ties to the lower j
-inline int64_t near_half(int64_t x2, int64_t w, int64_t top) {
-  int64_t j = (x2 + 2 * w - 1) / (2 * w);
-  return std::min(std::max(j, (int64_t)1), top);
+inline int near_half(int x2, int w, int top) {
+  int j = (x2 + 2 * w - 1) / (2 * w);
+  return std::min(std::max(j, 1), top);
 }
 
 }  // namespace
 
-Groups interior_groups(const GridDesc& g, int ell, const uint8_t* active) {
+Groups interior_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act) {
   if (ell < 0 || ell >= std::max(g.nlevels, 1)) throw std::invalid_argument("level out of range");
-  const int64_t w = (int64_t)g.m << ell;
-  const int64_t k = g.n / w;
-  const int64_t N = g.ndof();
-  std::vector<int32_t> dofs;
-  std::vector<int64_t> keys;
-  int x[3];
-  for (int64_t d = 0; d < N; ++d) {
-    if (!active[d]) continue;
-    int64_t r = d;
+  const int w = g.m << ell;
+  const int k = g.n / w;
+  std::vector<int32_t> dofs, keys;
+  dofs.reserve(act.size());
+  keys.reserve(act.size());
+  for (int32_t d : act) {
     bool inside = true;
-    int64_t key = 0, stride = 1;
+    int key = 0, stride = 1;
     for (int ax = 0; ax < g.dim; ++ax) {
-      x[ax] = (int)(r % g.side()) + 1;
-      r /= g.side();
-      if (x[ax] % w == 0) { inside = false; break; }
-      key += (x[ax] / w) * stride;
+      const int x = X.x[ax][(size_t)d];
+      const int q = x / w;
+      if (x - q * w == 0) { inside = false; break; }
+      key += q * stride;
       stride *= k;
     }
     if (!inside) continue;
-    dofs.push_back((int32_t)d);
+    dofs.push_back(d);
     keys.push_back(key);
   }
   return bucket(dofs, keys, ipow(k, g.dim));
 }
 
-Groups interface_groups(const GridDesc& g, int ell, const uint8_t* active, int kind) {
+Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
+                        int kind) {
   const bool face = kind == 1;
   if (g.dim == 2 && face) throw std::invalid_argument("faces need a 3D grid");
-  const int64_t w = (int64_t)g.m << ell;
-  const int64_t k = g.n / w;
-  const int64_t span = ipow(k, g.dim);
-  const int64_t N = g.ndof();
-  std::vector<int32_t> dofs;
-  std::vector<int64_t> keys;
-  int64_t x2[3];
-  for (int64_t d = 0; d < N; ++d) {
-    if (!active[d]) continue;
-    int64_t r = d;
+  const int w = g.m << ell;
+  const int k = g.n / w;
+  const int span = (int)ipow(k, g.dim);
+  std::vector<int32_t> dofs, keys;
+  dofs.reserve(act.size());
+  keys.reserve(act.size());
+  int x2[3];
+  for (int32_t d : act) {
     int planes = 0;
     for (int ax = 0; ax < g.dim; ++ax) {
-      const int64_t x = r % g.side() + 1;
-      r /= g.side();
+      const int x = X.x[ax][(size_t)d];
       x2[ax] = 2 * x;
       planes += (x % w == 0);
     }
@@ -106,44 +116,42 @@ Groups interface_groups(const GridDesc& g, int ell, const uint8_t* active, int k
     else if (face) excluded = planes >= 2;
     else excluded = planes == 3;
     if (excluded) continue;
-    int64_t best_d = INT64_MAX, best_key = 0;
+    int64_t best_d = INT64_MAX;
+    int best_key = 0;
     for (int fam = 0; fam < g.dim; ++fam) {
-      int64_t dist = 0, key = 0, stride = 1;
+      int64_t dist = 0;
+      int key = 0, stride = 1;
       for (int ax = 0; ax < g.dim; ++ax) {
         const bool on_plane = face ? (ax == fam) : (ax != fam);
-        int64_t j, c2, sp;
+        int j, c2, sp;
         if (on_plane) { j = near_mult(x2[ax], w, k - 1); c2 = 2 * w * j; sp = k - 1; }
         else { j = near_half(x2[ax], w, k); c2 = w * (2 * j - 1); sp = k; }
-        dist += (x2[ax] - c2) * (x2[ax] - c2);
+        dist += (int64_t)(x2[ax] - c2) * (x2[ax] - c2);
         key += (j - 1) * stride;
         stride *= sp;
       }
       if (dist < best_d) { best_d = dist; best_key = fam * span + key; }
     }
-    dofs.push_back((int32_t)d);
+    dofs.push_back(d);
     keys.push_back(best_key);
   }
-  return bucket(dofs, keys, span * g.dim);
+  return bucket(dofs, keys, (int64_t)span * g.dim);
 }
 
-Groups adaptive_groups(const GridDesc& g, int ell, const uint8_t* active, const CouplingTest& foreign) {
-  const int64_t w = (int64_t)g.m << ell;
-  const int64_t k = g.n / w;
-  const int64_t N = g.ndof();
-  std::vector<int32_t> dofs;
-  std::vector<int64_t> keys;
-  std::vector<int64_t> owner((size_t)N, -1);
-  for (int64_t d = 0; d < N; ++d) {
-    if (!active[d]) continue;
-    int64_t r = d, key = 0, stride = 1;
+Groups adaptive_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
+                       int64_t ndof, const CouplingTest& foreign) {
+  const int w = g.m << ell;
+  const int k = g.n / w;
+  std::vector<int32_t> dofs, keys;
+  std::vector<int64_t> owner((size_t)ndof, -1);
+  for (int32_t d : act) {
+    int key = 0, stride = 1;
     for (int ax = 0; ax < g.dim; ++ax) {
-      const int64_t x = r % g.side() + 1;
-      r /= g.side();
-      key += (near_half(2 * x, w, k) - 1) * stride;
+      key += (near_half(2 * X.x[ax][(size_t)d], w, k) - 1) * stride;
       stride *= k;
     }
     owner[(size_t)d] = key;
-    dofs.push_back((int32_t)d);
+    dofs.push_back(d);
     keys.push_back(key);
   }
   Groups vor = bucket(dofs, keys, ipow(k, g.dim));

@@ -14,12 +14,14 @@ struct GridDesc {
     for (int i = 0; i < dim; ++i) s *= side();
     return s;
   }
-  // 1-based grid coordinate of DOF d along axis ax (first axis fastest).
-  int coord(int64_t d, int ax) const {
-    const int64_t s = side();
-    for (int i = 0; i < ax; ++i) d /= s;
-    return (int)(d % s) + 1;
-  }
+};
+
+// 1-based integer grid coordinates of every DOF (first axis fastest),
+// precomputed once per factorization.
+struct Coords {
+  int dim = 0;
+  std::vector<int16_t> x[3];
+  void build(const GridDesc& g);
 };
 
 // Groups in CSR form: members[offsets[g] .. offsets[g+1]), ascending members.
@@ -31,16 +33,19 @@ struct Groups {
   int count(int64_t g) const { return (int)(offsets[g + 1] - offsets[g]); }
 };
 
+// `act` is the ascending list of active DOFs.
 // interior_cells (src/partition.py:68-92)
-Groups interior_groups(const GridDesc& g, int ell, const uint8_t* active);
+Groups interior_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act);
 
 // interface_cells (src/partition.py:108-181); kind: 0 = edge, 1 = face
-Groups interface_groups(const GridDesc& g, int ell, const uint8_t* active, int kind);
+Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
+                        int kind);
 
 // adaptive_interior_cells (src/partition.py:184-227).  `foreign(d, key, owner)`
 // must report whether DOF d (active, owned by cell `key`) couples to an active
 // DOF whose current owner is neither -1 nor `key`.
 using CouplingTest = std::function<bool(int32_t d, int64_t key, const int64_t* owner)>;
-Groups adaptive_groups(const GridDesc& g, int ell, const uint8_t* active, const CouplingTest& foreign);
+Groups adaptive_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
+                       int64_t ndof, const CouplingTest& foreign);
 
 }  // namespace hifde

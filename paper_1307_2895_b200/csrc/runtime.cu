@@ -26,6 +26,8 @@
 #include "hifde_internal.h"
 #include "partition.h"
 
+#include <omp.h>
+
 namespace hifde {
 
 namespace {
@@ -147,6 +149,72 @@ T* to_device(const std::vector<T>& h) {
   return d;
 }
 
+// Live clique blocks containing each DOF: up to kInline ids stored inline per
+// DOF, the rare overflow in a side table.
+struct Membership {
+  static constexpr int kInline = 8;
+  std::unique_ptr<int32_t[]> ids;
+  std::vector<uint8_t> cnt;
+  std::vector<std::vector<int32_t>> over;  // indexed by overflow slot
+  std::vector<int32_t> over_slot;          // per DOF, -1 if none
+  void init(int64_t n) {
+    ids.reset(new int32_t[(size_t)n * kInline]);
+    cnt.assign((size_t)n, 0);
+    over_slot.assign((size_t)n, -1);
+    over.clear();
+  }
+  void add(int32_t d, int32_t b) {
+    uint8_t& c = cnt[(size_t)d];
+    if (c < kInline) { ids[(size_t)d * kInline + c] = b; ++c; return; }
+    int32_t& sl = over_slot[(size_t)d];
+    if (sl < 0) { sl = (int32_t)over.size(); over.emplace_back(); }
+    over[(size_t)sl].push_back(b);
+  }
+  void remove(int32_t d, int32_t b) {
+    int32_t* v = &ids[(size_t)d * kInline];
+    uint8_t& c = cnt[(size_t)d];
+    for (int i = 0; i < c; ++i)
+      if (v[i] == b) {
+        const int32_t sl = over_slot[(size_t)d];
+        if (sl >= 0 && !over[(size_t)sl].empty()) {  // refill from the overflow
+          v[i] = over[(size_t)sl].back();
+          over[(size_t)sl].pop_back();
+        } else {
+          v[i] = v[c - 1];
+          --c;
+        }
+        return;
+      }
+    const int32_t sl = over_slot[(size_t)d];
+    if (sl >= 0) {
+      auto& o = over[(size_t)sl];
+      auto it = std::find(o.begin(), o.end(), b);
+      if (it != o.end()) { *it = o.back(); o.pop_back(); }
+    }
+  }
+  template <class Fn>
+  void for_each(int32_t d, Fn&& fn) const {
+    const int32_t* v = &ids[(size_t)d * kInline];
+    for (int i = 0; i < cnt[(size_t)d]; ++i) fn(v[i]);
+    const int32_t sl = over_slot[(size_t)d];
+    if (sl >= 0)
+      for (int32_t b : over[(size_t)sl]) fn(b);
+  }
+};
+
+// Per-thread scratch of the symbolic analysis.
+struct SymCtx {
+  std::vector<int32_t> dstamp, bstamp;
+  int32_t stamp = 0;
+  std::vector<int32_t> qbuf, bbuf;  // concatenated outputs of this thread
+};
+
+struct FrontSym {  // result of the symbolic analysis of one cell / group
+  int tid;
+  int64_t q_off, b_off;
+  int nq, nb, maxnb;
+};
+
 // ---------------------------------------------------------------------------
 // Factorization state
 // ---------------------------------------------------------------------------
@@ -156,12 +224,20 @@ struct Factorizer {
   hifde_factor_t* F;
   cudaStream_t s;
   int64_t N;
-  // A0 (host + device)
-  std::vector<int64_t> indptr;
-  std::vector<int32_t> indices;
+  // A0 (host + device); the host pattern aliases the caller's arrays when
+  // they are host arrays
+  std::vector<int64_t> indptr_own;
+  std::vector<int32_t> indices_own;
+  const int64_t* indptr = nullptr;
+  const int32_t* indices = nullptr;
+  Coords X;
+  std::vector<int32_t> act;  // ascending active DOFs
+  std::vector<SymCtx> ctx;
+  int nthreads = 1;
   int64_t* d_indptr = nullptr;
   int32_t* d_indices = nullptr;
   double* d_a0 = nullptr;
+  bool own_a0 = false;
   // activity
   std::vector<uint8_t> active;
   uint8_t* d_active = nullptr;
@@ -176,14 +252,14 @@ struct Factorizer {
   DBuf<int32_t> d_blk_n;
   DBuf<int64_t> d_blk_val_off;
   size_t blk_uploaded = 0;
-  std::vector<std::vector<int32_t>> member;  // live blocks containing a DOF
+  Membership member;
   DBuf<double> bvals;
   DBuf<double> scratch;
   DBuf<int32_t> lists;
   DBuf<int> status;
   DBuf<int32_t> kout;
-  // stamps
-  std::vector<int64_t> dstamp, bstamp;
+  // stamps (serial paths)
+  std::vector<int64_t> dstamp;
   int64_t stamp = 0;
   // block-foreign cache for adaptive partitioning
   std::vector<int64_t> bf_key;
@@ -234,60 +310,83 @@ struct Factorizer {
     blk_n.push_back(nb);
     blk_val_off.push_back(val_off);
     blk_alive.push_back(1);
-    bstamp.push_back(0);
     bf_key.push_back(-2);
     bf_val.push_back(0);
-    for (int32_t i = 0; i < nb; ++i) member[(size_t)h_idx[(size_t)(dof_off + i)]].push_back(id);
+    for (int32_t i = 0; i < nb; ++i) member.add(h_idx[(size_t)(dof_off + i)], id);
     return id;
   }
   void kill_block(int32_t b) {
     blk_alive[(size_t)b] = 0;
     const int32_t* d = h_idx.data() + blk_dof_off[(size_t)b];
-    for (int32_t i = 0; i < blk_n[(size_t)b]; ++i) {
-      auto& v = member[(size_t)d[i]];
-      auto it = std::find(v.begin(), v.end(), b);
-      if (it != v.end()) {
-        *it = v.back();
-        v.pop_back();
-      }
-    }
+    for (int32_t i = 0; i < blk_n[(size_t)b]; ++i) member.remove(d[i], b);
   }
 
   // Neighbour set q of the group c and the live blocks touching c
-  // (src/sparse.py:164-173 on the clique representation).
-  void front_of(const int32_t* c, int nc, std::vector<int32_t>& blks, std::vector<int32_t>& q) {
-    const int64_t tc = ++stamp;
-    for (int i = 0; i < nc; ++i) dstamp[(size_t)c[i]] = tc;
-    const int64_t tq = ++stamp;
-    blks.clear();
-    q.clear();
+  // (src/sparse.py:164-173 on the clique representation), appended to the
+  // thread's buffers.
+  FrontSym front_sym(SymCtx& x, int tid, const int32_t* c, int nc) {
+    if (x.stamp > INT32_MAX - 4) {
+      std::fill(x.dstamp.begin(), x.dstamp.end(), 0);
+      std::fill(x.bstamp.begin(), x.bstamp.end(), 0);
+      x.stamp = 0;
+    }
+    const int32_t tc = ++x.stamp;
+    const int32_t tq = ++x.stamp;
+    FrontSym r;
+    r.tid = tid;
+    r.q_off = (int64_t)x.qbuf.size();
+    r.b_off = (int64_t)x.bbuf.size();
+    for (int i = 0; i < nc; ++i) x.dstamp[(size_t)c[i]] = tc;
     for (int i = 0; i < nc; ++i)
-      for (int32_t b : member[(size_t)c[i]])
-        if (bstamp[(size_t)b] != tq) {
-          bstamp[(size_t)b] = tq;
-          blks.push_back(b);
+      member.for_each(c[i], [&](int32_t b) {
+        if (x.bstamp[(size_t)b] != tq) {
+          x.bstamp[(size_t)b] = tq;
+          x.bbuf.push_back(b);
         }
-    std::sort(blks.begin(), blks.end());
+      });
+    std::sort(x.bbuf.begin() + r.b_off, x.bbuf.end());
+    int maxnb = 0;
     auto consider = [&](int32_t d) {
-      if (active[(size_t)d] && dstamp[(size_t)d] != tc && dstamp[(size_t)d] != tq) {
-        dstamp[(size_t)d] = tq;
-        q.push_back(d);
+      int32_t& st = x.dstamp[(size_t)d];
+      if (st != tc && st != tq && active[(size_t)d]) {
+        st = tq;
+        x.qbuf.push_back(d);
       }
     };
-    for (int32_t b : blks) {
+    for (int64_t j = r.b_off; j < (int64_t)x.bbuf.size(); ++j) {
+      const int32_t b = x.bbuf[(size_t)j];
       const int32_t* d = h_idx.data() + blk_dof_off[(size_t)b];
+      maxnb = std::max(maxnb, blk_n[(size_t)b]);
       for (int32_t i = 0; i < blk_n[(size_t)b]; ++i) consider(d[i]);
     }
     for (int i = 0; i < nc; ++i)
-      for (int64_t k = indptr[(size_t)c[i]]; k < indptr[(size_t)c[i] + 1]; ++k) consider(indices[(size_t)k]);
-    std::sort(q.begin(), q.end());
+      for (int64_t k = indptr[c[i]]; k < indptr[c[i] + 1]; ++k) consider(indices[k]);
+    std::sort(x.qbuf.begin() + r.q_off, x.qbuf.end());
+    r.nq = (int)((int64_t)x.qbuf.size() - r.q_off);
+    r.nb = (int)((int64_t)x.bbuf.size() - r.b_off);
+    r.maxnb = maxnb;
+    return r;
   }
 
-  int maxnb_of(const std::vector<int32_t>& blks) {
-    int m = 0;
-    for (int32_t b : blks) m = std::max(m, blk_n[(size_t)b]);
-    return m;
+  // Symbolic analysis of every group of a level, in parallel over groups.
+  std::vector<FrontSym> fronts(const Groups& gr) {
+    const int64_t nt = gr.size();
+    std::vector<FrontSym> out((size_t)nt);
+    for (auto& x : ctx) {
+      x.qbuf.clear();
+      x.bbuf.clear();
+      if (x.bstamp.size() < blk_n.size()) x.bstamp.resize(blk_n.size() + blk_n.size() / 2 + 1024, 0);
+    }
+    const int nthr = (nt >= 256) ? nthreads : 1;
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, 32)
+    for (int64_t t = 0; t < nt; ++t) {
+      const int tid = omp_get_thread_num();
+      out[(size_t)t] = front_sym(ctx[(size_t)tid], tid, gr.begin(t), gr.count(t));
+    }
+    return out;
   }
+  const int32_t* sym_q(const FrontSym& f) const { return ctx[(size_t)f.tid].qbuf.data() + f.q_off; }
+  const int32_t* sym_b(const FrontSym& f) const { return ctx[(size_t)f.tid].bbuf.data() + f.b_off; }
 
   // cells of an elimination level must not interact (assert_noninteracting,
   // src/partition.py:230-241)
@@ -295,11 +394,11 @@ struct Factorizer {
     std::vector<int64_t> cell_of((size_t)N, -1);
     for (int64_t gi = 0; gi < gr.size(); ++gi)
       for (int i = 0; i < gr.count(gi); ++i) cell_of[(size_t)gr.begin(gi)[i]] = gi;
-    std::vector<int32_t> blks, q;
+    std::vector<FrontSym> fs = fronts(gr);
     for (int64_t gi = 0; gi < gr.size(); ++gi) {
-      front_of(gr.begin(gi), gr.count(gi), blks, q);
-      for (int32_t d : q)
-        if (cell_of[(size_t)d] >= 0 && cell_of[(size_t)d] != gi) {
+      const int32_t* q = sym_q(fs[(size_t)gi]);
+      for (int i = 0; i < fs[(size_t)gi].nq; ++i)
+        if (cell_of[(size_t)q[i]] >= 0 && cell_of[(size_t)q[i]] != gi) {
           char buf[128];
           snprintf(buf, sizeof buf, "cells interact at level %g", tag);
           throw Fail{HIFDE_INTERNAL, buf};
@@ -344,27 +443,28 @@ struct Factorizer {
     L.ngroups = nt;
     std::vector<ElimTask> tasks((size_t)nt);
     std::vector<uint8_t> is_big((size_t)nt, 0);
-    std::vector<std::vector<int32_t>> consumed((size_t)nt);
     std::vector<int32_t> hl;  // block lists of this level
-    std::vector<int32_t> q;
     size_t smem_small = 0, smem_big = 0;
     int max_small_nf = 0;
     scratch.n = 0;
+    const std::vector<FrontSym> fs = fronts(gr);
     for (int64_t t = 0; t < nt; ++t) {
       const int32_t* c = gr.begin(t);
       const int nc = gr.count(t);
-      front_of(c, nc, consumed[(size_t)t], q);
-      const int nq = (int)q.size(), nf = nc + nq;
+      const FrontSym& f = fs[(size_t)t];
+      const int32_t* q = sym_q(f);
+      const int32_t* bl = sym_b(f);
+      const int nq = f.nq, nf = nc + nq;
       ElimTask& T = tasks[(size_t)t];
       T.nc = nc;
       T.nq = nq;
-      T.nblk = (int)consumed[(size_t)t].size();
-      T.maxnb = maxnb_of(consumed[(size_t)t]);
+      T.nblk = f.nb;
+      T.maxnb = f.maxnb;
       T.dofs_off = (int64_t)h_idx.size();
       h_idx.insert(h_idx.end(), c, c + nc);
-      h_idx.insert(h_idx.end(), q.begin(), q.end());
+      h_idx.insert(h_idx.end(), q, q + nq);
       T.blk_off = (int64_t)hl.size();
-      hl.insert(hl.end(), consumed[(size_t)t].begin(), consumed[(size_t)t].end());
+      hl.insert(hl.end(), bl, bl + f.nb);
       const size_t ib = align16(sizeof(int32_t) * (size_t)(nf + T.maxnb));
       const size_t need = ib + sizeof(double) * (size_t)nf * nf;
       if (need <= kSmemCap) {
@@ -403,8 +503,8 @@ struct Factorizer {
     L.t_sym = tp - t_begin;
     // host structure updates: consumed blocks die, new neighbour blocks live
     for (int64_t t = 0; t < nt; ++t) {
-      for (int32_t b : consumed[(size_t)t]) kill_block(b);
       const ElimTask& T = tasks[(size_t)t];
+      for (int j = 0; j < T.nblk; ++j) kill_block(hl[(size_t)(T.blk_off + j)]);
       if (T.nq > 0) add_block(T.dofs_off + T.nc, T.nq, T.U_off);
       const int32_t* c = gr.begin(t);
       for (int i = 0; i < T.nc; ++i) active[(size_t)c[i]] = 0;
@@ -518,7 +618,7 @@ struct Factorizer {
     L.kind = 1;
     L.ngroups = nt;
     std::vector<SkelTask> tasks((size_t)nt);
-    std::vector<int32_t> hl, blks, q;
+    std::vector<int32_t> hl;
     size_t smem = 0;
     int max_nc = 0, max_nq = 0;
     scratch.n = 0;
@@ -532,25 +632,28 @@ struct Factorizer {
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = (int32_t)t;
     int nbatch = 1;
+    const std::vector<FrontSym> fs = fronts(gr);
     for (int64_t t = 0; t < nt; ++t) {
       const int32_t* c = gr.begin(t);
       const int nc = gr.count(t);
-      front_of(c, nc, blks, q);
-      const int nq = (int)q.size(), nf = nc + nq;
+      const FrontSym& f = fs[(size_t)t];
+      const int32_t* q = sym_q(f);
+      const int32_t* blks = sym_b(f);
+      const int nq = f.nq, nf = nc + nq;
       SkelTask& T = tasks[(size_t)t];
       T.nc = nc;
       T.nq = nq;
-      T.nblk = (int)blks.size();
-      T.maxnb = maxnb_of(blks);
+      T.nblk = f.nb;
+      T.maxnb = f.maxnb;
       T.group = (int32_t)t;
       T.pad = 0;
       T.dofs_off = (int64_t)h_idx.size();
       h_idx.insert(h_idx.end(), c, c + nc);
-      h_idx.insert(h_idx.end(), q.begin(), q.end());
+      h_idx.insert(h_idx.end(), q, q + nq);
       T.out_off = (int64_t)h_idx.size();
       h_idx.insert(h_idx.end(), (size_t)nc, 0);
       T.blk_off = (int64_t)hl.size();
-      hl.insert(hl.end(), blks.begin(), blks.end());
+      hl.insert(hl.end(), blks, blks + f.nb);
       const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 5 * nc));
       const size_t q4 = (size_t)nc * nc / 4 + nc;
       const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + (size_t)nc * nc;
@@ -568,8 +671,8 @@ struct Factorizer {
       T.delta_off = (int64_t)bvals.bump((size_t)nc * nc, s);
       L.max_front = std::max<int64_t>(L.max_front, nf);
       int b = 0;
-      for (int32_t d : q) {
-        const int32_t go = group_of[(size_t)d];
+      for (int i = 0; i < nq; ++i) {
+        const int32_t go = group_of[(size_t)q[i]];
         if (go >= 0 && go < t) b = std::max(b, batch[(size_t)go] + 1);
       }
       batch[(size_t)t] = b;
@@ -677,7 +780,9 @@ struct Factorizer {
       if (o != -1 && o != key) return true;
     }
     const int64_t tag = (bf_epoch << 32) + key;
-    for (int32_t b : member[(size_t)d]) {
+    bool found = false;
+    member.for_each(d, [&](int32_t b) {
+      if (found) return;
       if (bf_key[(size_t)b] != tag) {
         bf_key[(size_t)b] = tag;
         uint8_t f = 0;
@@ -690,37 +795,54 @@ struct Factorizer {
         }
         bf_val[(size_t)b] = f;
       }
-      if (bf_val[(size_t)b]) return true;
-    }
-    return false;
+      if (bf_val[(size_t)b]) found = true;
+    });
+    return found;
   }
 
   void run(const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz) {
     const double t0 = now_s();
     N = g.ndof();
-    // A0
+    // A0: the symbolic analysis needs the pattern on the host
     if (opt.input_on_device) {
-      indptr.resize((size_t)N + 1);
-      HCK(cudaMemcpy(indptr.data(), ip, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-      nnz = indptr.back();
-      indices.resize((size_t)nnz);
-      HCK(cudaMemcpy(indices.data(), ix, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      indptr_own.resize((size_t)N + 1);
+      HCK(cudaMemcpy(indptr_own.data(), ip, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      nnz = indptr_own.back();
+      indices_own.resize((size_t)nnz);
+      HCK(cudaMemcpy(indices_own.data(), ix, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      indptr = indptr_own.data();
+      indices = indices_own.data();
+      d_indptr = const_cast<int64_t*>(ip);
+      d_indices = const_cast<int32_t*>(ix);
+      d_a0 = const_cast<double*>(va);
     } else {
-      indptr.assign(ip, ip + N + 1);
-      indices.assign(ix, ix + nnz);
+      indptr = ip;
+      indices = ix;
+      HCK(cudaMallocAsync((void**)&d_indptr, (N + 1) * sizeof(int64_t), s));
+      HCK(cudaMallocAsync((void**)&d_indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t), s));
+      HCK(cudaMallocAsync((void**)&d_a0, std::max<int64_t>(nnz, 1) * sizeof(double), s));
+      HCK(cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      HCK(cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      HCK(cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+      own_a0 = true;
     }
-    HCK(cudaMallocAsync((void**)&d_indptr, (N + 1) * sizeof(int64_t), s));
-    HCK(cudaMallocAsync((void**)&d_indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t), s));
-    HCK(cudaMallocAsync((void**)&d_a0, std::max<int64_t>(nnz, 1) * sizeof(double), s));
-    HCK(cudaMemcpyAsync(d_indptr, indptr.data(), (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    HCK(cudaMemcpyAsync(d_indices, indices.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    HCK(cudaMemcpyAsync(d_a0, va, nnz * sizeof(double),
-                        opt.input_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     active.assign((size_t)N, 1);
     HCK(cudaMallocAsync((void**)&d_active, std::max<int64_t>(N, 1), s));
     HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
-    member.assign((size_t)N, {});
+    X.build(g);
+    act.resize((size_t)N);
+    for (int64_t i = 0; i < N; ++i) act[(size_t)i] = (int32_t)i;
+    member.init(N);
     dstamp.assign((size_t)N, 0);
+    {
+      const char* env = getenv("HIFDE_HOST_THREADS");
+      nthreads = env ? std::max(1, atoi(env)) : std::min(16, std::max(1, omp_get_max_threads()));
+      ctx.resize((size_t)nthreads);
+      for (auto& x : ctx) {
+        x.dstamp.assign((size_t)N, 0);
+        x.stamp = 0;
+      }
+    }
     F->fac.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
     F->idx.reserve((size_t)std::max<int64_t>(16 * N, 1 << 16), s);
     bvals.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
@@ -728,9 +850,11 @@ struct Factorizer {
     const int Lv = g.nlevels;
     const double t_setup = now_s() - t0;
     auto record_trace = [&](LevelRec& L, double tl) {
-      int64_t a = 0;
-      for (int64_t i = 0; i < N; ++i) a += active[(size_t)i];
-      L.active_after = a;
+      size_t w = 0;
+      for (size_t i = 0; i < act.size(); ++i)
+        if (active[(size_t)act[i]]) act[w++] = act[i];
+      act.resize(w);
+      L.active_after = (int64_t)w;
       L.seconds = now_s() - tl;
     };
     for (int ell = 0; ell < Lv; ++ell) {
@@ -739,11 +863,11 @@ struct Factorizer {
         Groups gr;
         if (opt.variant == HIFDE_VARIANT_HIFDE3X && ell > 0) {
           ++bf_epoch;
-          gr = adaptive_groups(g, ell, active.data(), [&](int32_t d, int64_t key, const int64_t* owner) {
+          gr = adaptive_groups(g, X, ell, act, N, [&](int32_t d, int64_t key, const int64_t* owner) {
             return adaptive_foreign(d, key, owner);
           });
         } else {
-          gr = interior_groups(g, ell, active.data());
+          gr = interior_groups(g, X, ell, act);
         }
         if (opt.verify) check_noninteracting(gr, (double)ell);
         F->levels.emplace_back();
@@ -755,7 +879,7 @@ struct Factorizer {
       }
       auto skel = [&](double tag, int kind) {
         const double tl = now_s();
-        Groups gr = interface_groups(g, ell, active.data(), kind);
+        Groups gr = interface_groups(g, X, ell, act, kind);
         F->levels.emplace_back();
         LevelRec& L = F->levels.back();
         L.t_part = now_s() - tl;
@@ -774,8 +898,7 @@ struct Factorizer {
     {
       const double tl = now_s();
       Groups top;
-      for (int64_t i = 0; i < N; ++i)
-        if (active[(size_t)i]) top.members.push_back((int32_t)i);
+      top.members = act;
       F->s_top = (int64_t)top.members.size();
       F->levels.emplace_back();
       LevelRec& L = F->levels.back();
@@ -809,9 +932,11 @@ struct Factorizer {
     d_blk_dof_off.release(s);
     d_blk_n.release(s);
     d_blk_val_off.release(s);
-    cudaFreeAsync(d_indptr, s);
-    cudaFreeAsync(d_indices, s);
-    cudaFreeAsync(d_a0, s);
+    if (own_a0) {
+      cudaFreeAsync(d_indptr, s);
+      cudaFreeAsync(d_indices, s);
+      cudaFreeAsync(d_a0, s);
+    }
     cudaFreeAsync(d_active, s);
     HCK(cudaStreamSynchronize(s));
     F->t_f = now_s() - t0;
@@ -1077,8 +1202,13 @@ int64_t hifde_partition(int dim, int n_grid, int m_leaf, int ell, int level_kind
     int L = 0;
     while (((int64_t)m_leaf << (L + 1)) <= n_grid) ++L;
     g.nlevels = L;
-    Groups gr = level_kind == 0 ? interior_groups(g, ell, active)
-                                : interface_groups(g, ell, active, level_kind == 2 ? 1 : 0);
+    Coords X;
+    X.build(g);
+    std::vector<int32_t> act;
+    for (int64_t i = 0; i < g.ndof(); ++i)
+      if (active[i]) act.push_back((int32_t)i);
+    Groups gr = level_kind == 0 ? interior_groups(g, X, ell, act)
+                                : interface_groups(g, X, ell, act, level_kind == 2 ? 1 : 0);
     if ((int64_t)gr.members.size() > members_cap || gr.size() + 1 > offsets_cap) return -1;
     std::memcpy(members, gr.members.data(), gr.members.size() * sizeof(int32_t));
     std::memcpy(offsets, gr.offsets.data(), gr.offsets.size() * sizeof(int64_t));
