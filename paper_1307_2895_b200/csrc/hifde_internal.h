@@ -29,7 +29,7 @@ struct SkelTask {
   int64_t delta_off;        // block arena: delta block (k x k)
   int64_t out_off;          // idx arena: sk (ascending) then rd (ascending), global ids
   int32_t group;            // index of the group within its level
-  int32_t pad;
+  int32_t mode;             // workspace placement: 0 shared, 1 Mq shared, 2 global
 };
 
 // Solve-sweep record (one per elimination cell / skeleton group with rd != {}).

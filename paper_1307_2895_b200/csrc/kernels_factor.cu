@@ -406,13 +406,26 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   int32_t* sko = rdl + nc;
   int32_t* rdo = sko + nc;
   const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(2 * nf + t.maxnb + 5 * nc), 16);
-  double* ws = t.scratch_off < 0 ? reinterpret_cast<double*>(smem + ibytes) : A.scratch + t.scratch_off;
+  // workspace placement (host-chosen): 0 all shared; 1 Mq + norms shared,
+  // A_cc and the post-CPQR matrices global; 2 all global
+  double* wsh = reinterpret_cast<double*>(smem + ibytes);
+  double* wgl = A.scratch + (t.scratch_off > 0 ? t.scratch_off : 0);
   const int ldq = nq;                                  // Mq column-major, ld nq
-  double* Acc = ws;                                    // nc x nc, row-major (symmetric)
-  double* Mq = Acc + (size_t)nc * nc;                  // nq x nc
-  double* vn1 = Mq + (size_t)nq * nc;
-  double* vn2 = vn1 + nc;
-  double* Z = vn2 + nc;                                // post-CPQR workspace
+  double *Acc, *Mq, *vn1, *vn2, *Z;
+  if (t.mode == 1) {
+    Mq = wsh;
+    vn1 = Mq + (size_t)nq * nc;
+    vn2 = vn1 + nc;
+    Acc = wgl;
+    Z = Acc + (size_t)nc * nc;
+  } else {
+    double* ws = t.mode == 0 ? wsh : wgl;
+    Acc = ws;                                          // nc x nc, row-major (symmetric)
+    Mq = Acc + (size_t)nc * nc;                        // nq x nc
+    vn1 = Mq + (size_t)nq * nc;
+    vn2 = vn1 + nc;
+    Z = vn2 + nc;                                      // post-CPQR workspace
+  }
   const size_t q4 = (size_t)nc * nc / 4 + nc;
   double* Ts = Z;                                      // k x r
   double* Bsr = Ts + q4;                               // k x r

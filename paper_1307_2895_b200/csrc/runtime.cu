@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -163,6 +164,11 @@ struct Membership {
     over_slot.assign((size_t)n, -1);
     over.clear();
   }
+  // empty every list (storage kept)
+  void reset() {
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (size_t i = 0; i < over.size(); ++i) over[i].clear();
+  }
   void add(int32_t d, int32_t b) {
     uint8_t& c = cnt[(size_t)d];
     if (c < kInline) { ids[(size_t)d * kInline + c] = b; ++c; return; }
@@ -202,12 +208,31 @@ struct Membership {
   }
 };
 
+// Host scratch kept across factorizations of the same grid (coordinates,
+// per-thread stamp arrays, block membership storage): avoids re-touching
+// O(N) memory on every call.  hifde_factor holds g_host_mutex while it runs.
+struct HostCache;
+HostCache& host_cache();
+
 // Per-thread scratch of the symbolic analysis.
 struct SymCtx {
   std::vector<int32_t> dstamp, bstamp;
   int32_t stamp = 0;
   std::vector<int32_t> qbuf, bbuf;  // concatenated outputs of this thread
 };
+
+struct HostCache {
+  GridDesc g;
+  bool valid = false;
+  Coords X;
+  std::vector<SymCtx> ctx;
+  Membership& member = host_cache().member;
+};
+HostCache& host_cache() {
+  static HostCache hc;
+  return hc;
+}
+std::mutex g_host_mutex;
 
 struct FrontSym {  // result of the symbolic analysis of one cell / group
   int tid;
@@ -230,9 +255,9 @@ struct Factorizer {
   std::vector<int32_t> indices_own;
   const int64_t* indptr = nullptr;
   const int32_t* indices = nullptr;
-  Coords X;
+  Coords& X = host_cache().X;
   std::vector<int32_t> act;  // ascending active DOFs
-  std::vector<SymCtx> ctx;
+  std::vector<SymCtx>& ctx = host_cache().ctx;
   int nthreads = 1;
   int64_t* d_indptr = nullptr;
   int32_t* d_indices = nullptr;
@@ -252,7 +277,7 @@ struct Factorizer {
   DBuf<int32_t> d_blk_n;
   DBuf<int64_t> d_blk_val_off;
   size_t blk_uploaded = 0;
-  Membership member;
+  Membership& member = host_cache().member;
   DBuf<double> bvals;
   DBuf<double> scratch;
   DBuf<int32_t> lists;
@@ -646,7 +671,6 @@ struct Factorizer {
       T.nblk = f.nb;
       T.maxnb = f.maxnb;
       T.group = (int32_t)t;
-      T.pad = 0;
       T.dofs_off = (int64_t)h_idx.size();
       h_idx.insert(h_idx.end(), c, c + nc);
       h_idx.insert(h_idx.end(), q, q + nq);
@@ -657,14 +681,20 @@ struct Factorizer {
       const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 5 * nc));
       const size_t q4 = (size_t)nc * nc / 4 + nc;
       const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + (size_t)nc * nc;
+      const size_t mq = (size_t)nq * nc + 2 * (size_t)nc;
       max_nc = std::max(max_nc, nc);
       max_nq = std::max(max_nq, nq);
-      const size_t need = ib + sizeof(double) * wsd;
-      if (need <= kSmemCap) {
+      if (ib + sizeof(double) * wsd <= kSmemCap) {
+        T.mode = 0;
         T.scratch_off = -1;
-        smem = std::max(smem, need);
+        smem = std::max(smem, ib + sizeof(double) * wsd);
+      } else if (ib + sizeof(double) * mq <= kSmemCap) {
+        T.mode = 1;
+        T.scratch_off = (int64_t)scratch.bump(2 * (size_t)nc * nc + 3 * q4 + 8, s);
+        smem = std::max(smem, ib + sizeof(double) * mq);
       } else {
-        T.scratch_off = (int64_t)scratch.bump(wsd, s);
+        T.mode = 2;
+        T.scratch_off = (int64_t)scratch.bump(wsd + 8, s);
         smem = std::max(smem, ib);
       }
       T.rec_off = (int64_t)F->fac.bump((size_t)nc * nc + 2 * q4, s);
@@ -681,7 +711,7 @@ struct Factorizer {
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = -1;
     bool exact = opt.order_mode == HIFDE_ORDER_EXACT ||
-                 (opt.order_mode == HIFDE_ORDER_AUTO && nbatch <= opt.exact_max_batches);
+                 (opt.order_mode == HIFDE_ORDER_AUTO && nt <= opt.exact_max_groups);
     if (!exact) {
       std::fill(batch.begin(), batch.end(), 0);
       nbatch = 1;
@@ -829,19 +859,30 @@ struct Factorizer {
     active.assign((size_t)N, 1);
     HCK(cudaMallocAsync((void**)&d_active, std::max<int64_t>(N, 1), s));
     HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
-    X.build(g);
     act.resize((size_t)N);
     for (int64_t i = 0; i < N; ++i) act[(size_t)i] = (int32_t)i;
-    member.init(N);
     dstamp.assign((size_t)N, 0);
     {
       const char* env = getenv("HIFDE_HOST_THREADS");
       nthreads = env ? std::max(1, atoi(env)) : std::min(16, std::max(1, omp_get_max_threads()));
-      ctx.resize((size_t)nthreads);
-      for (auto& x : ctx) {
-        x.dstamp.assign((size_t)N, 0);
-        x.stamp = 0;
+      HostCache& hc = host_cache();
+      const bool same = hc.valid && hc.g.dim == g.dim && hc.g.n == g.n;
+      if (!same) {
+        X.build(g);
+        member.init(N);
+        ctx.clear();
+        hc.g = g;
+        hc.valid = true;
+      } else {
+        member.reset();
       }
+      if ((int)ctx.size() < nthreads) ctx.resize((size_t)nthreads);
+      for (auto& x : ctx)
+        if ((int64_t)x.dstamp.size() != N) {
+          x.dstamp.assign((size_t)N, 0);
+          x.bstamp.clear();
+          x.stamp = 0;
+        }
     }
     F->fac.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
     F->idx.reserve((size_t)std::max<int64_t>(16 * N, 1 << 16), s);
@@ -1062,7 +1103,7 @@ void hifde_default_options(hifde_options_t* o, int variant) {
   o->skip_levels = variant == HIFDE_VARIANT_HIFDE3X ? 1 : 0;
   o->spd = 1;
   o->order_mode = HIFDE_ORDER_AUTO;
-  o->exact_max_batches = 24;
+  o->exact_max_groups = 32;
   o->device = 0;
   o->eps = 0.0;
 }
@@ -1116,6 +1157,7 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
       HCK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
       F->own_stream = true;
     }
+    std::lock_guard<std::mutex> lock(g_host_mutex);
     Factorizer fz;
     fz.g = g;
     fz.opt = *opt;
@@ -1124,7 +1166,7 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
       fz.opt.skip_levels = nlevels;  // factor_mf == factor_hifde(skip_levels=L)
       fz.opt.eps = 0.0;
     }
-    if (fz.opt.exact_max_batches <= 0) fz.opt.exact_max_batches = 24;
+    if (fz.opt.exact_max_groups <= 0) fz.opt.exact_max_groups = 32;
     fz.F = F.get();
     fz.s = F->stream;
     const int64_t nnz = opt->input_on_device ? 0 : indptr[n];
