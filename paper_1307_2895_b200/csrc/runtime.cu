@@ -50,6 +50,19 @@ struct Fail {
 
 constexpr size_t kSmemCap = kSmemCapBytes;
 
+bool trace_on() {
+  static const bool on = getenv("HIFDE_TRACE") != nullptr;
+  return on;
+}
+#define HTRACE(...)                                \
+  do {                                             \
+    if (trace_on()) {                              \
+      fprintf(stderr, "[hifde-trace] " __VA_ARGS__); \
+      fprintf(stderr, "\n");                       \
+      fflush(stderr);                              \
+    }                                              \
+  } while (0)
+
 double now_s() {
   using namespace std::chrono;
   return duration<double>(steady_clock::now().time_since_epoch()).count();
@@ -462,6 +475,7 @@ struct Factorizer {
 
   // -------------------------------------------------------------------------
   void elimination_level(const Groups& gr, double tag, LevelRec& L, bool is_top) {
+    HTRACE("elim level %g: %lld cells", tag, (long long)gr.size());
     const double t_begin = now_s();
     const int64_t nt = gr.size();
     L.kind = is_top ? 2 : 0;
@@ -526,6 +540,7 @@ struct Factorizer {
     }
     double tp = now_s();
     L.t_sym = tp - t_begin;
+    HTRACE("  symbolic done");
     // host structure updates: consumed blocks die, new neighbour blocks live
     for (int64_t t = 0; t < nt; ++t) {
       const ElimTask& T = tasks[(size_t)t];
@@ -548,6 +563,7 @@ struct Factorizer {
       for (int a = 0; a < ntl; ++a)
         for (int b = a; b < ntl; ++b) tiles.push_back(make_int4(bi, a, b, 0));
     }
+    HTRACE("  host updates done (%zu small / %zu big / %zu tiles)", small.size(), big.size(), tiles.size());
     // uploads
     upload_idx();
     upload_blocks();
@@ -587,6 +603,8 @@ struct Factorizer {
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
+    HTRACE("  launched");
+    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
     // (the kernels retire the cells in the device active mask themselves)
     L.t_launch = now_s() - tp;
     tp = now_s();
@@ -638,6 +656,7 @@ struct Factorizer {
 
   // -------------------------------------------------------------------------
   void skeleton_level(const Groups& gr, double tag, LevelRec& L) {
+    HTRACE("skel level %g: %lld groups", tag, (long long)gr.size());
     const double t_begin = now_s();
     const int64_t nt = gr.size();
     L.kind = 1;
@@ -717,6 +736,7 @@ struct Factorizer {
       nbatch = 1;
     }
     L.nbatches = nbatch;
+    HTRACE("  symbolic done, %d batches", nbatch);
     double tp = now_s();
     L.t_sym = tp - t_begin;
     // order tasks by batch (stable keeps the reference order inside a batch)
@@ -754,6 +774,7 @@ struct Factorizer {
       launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
       launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
       g_launches += 2;
+      if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  batch %d done", b); }
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
@@ -768,6 +789,7 @@ struct Factorizer {
                           (h_idx.size() - (size_t)idx_level_start) * sizeof(int32_t),
                           cudaMemcpyDeviceToHost, s));
     check_status();  // synchronizes the stream
+    HTRACE("  readback done");
     L.t_sync = now_s() - tp;
     tp = now_s();
     dt.release(s);
@@ -833,6 +855,7 @@ struct Factorizer {
   void run(const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz) {
     const double t0 = now_s();
     N = g.ndof();
+    HTRACE("factor start N=%lld", (long long)N);
     // A0: the symbolic analysis needs the pattern on the host
     if (opt.input_on_device) {
       indptr_own.resize((size_t)N + 1);
@@ -890,6 +913,7 @@ struct Factorizer {
 
     const int Lv = g.nlevels;
     const double t_setup = now_s() - t0;
+    HTRACE("setup done");
     auto record_trace = [&](LevelRec& L, double tl) {
       size_t w = 0;
       for (size_t i = 0; i < act.size(); ++i)
