@@ -239,7 +239,7 @@ struct HostCache {
   bool valid = false;
   Coords X;
   std::vector<SymCtx> ctx;
-  Membership& member = host_cache().member;
+  Membership member;
 };
 HostCache& host_cache() {
   static HostCache hc;
@@ -1166,8 +1166,10 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
     return HIFDE_BADARG;
   }
   std::unique_ptr<hifde_factor_t> F(new hifde_factor_t);
+  HTRACE("hifde_factor entry");
   try {
     HCK(cudaSetDevice(opt->device));
+    HTRACE("device set");
     set_pool_threshold(opt->device);
     F->device = opt->device;
     F->n = n;
@@ -1181,8 +1183,11 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
       HCK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
       F->own_stream = true;
     }
+    HTRACE("stream ready");
     std::lock_guard<std::mutex> lock(g_host_mutex);
+    HTRACE("locked");
     Factorizer fz;
+    HTRACE("factorizer constructed");
     fz.g = g;
     fz.opt = *opt;
     if (opt->variant == HIFDE_VARIANT_MF) {
