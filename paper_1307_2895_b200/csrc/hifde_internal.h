@@ -61,12 +61,21 @@ struct Arenas {
 
 constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA we use
 constexpr int kSchurTile = 64;                 // schur_tile_kernel tile edge
-constexpr int kTrsmPanel = 16;                 // elim_big_kernel TRSM panel width
+constexpr int kPanelB = 64;                    // blocked Cholesky panel width
 
 // Kernel launchers (kernels_factor.cu / kernels_solve.cu).
 void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,
                        cudaStream_t s);
-void launch_elim_big(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, cudaStream_t s);
+void launch_big_assemble(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A,
+                         double* diag_scale, size_t smem, cudaStream_t s);
+void launch_panel_chol(const ElimTask* tasks, const int32_t* cells, int ncells, int p0, const Arenas& A,
+                       double* dmin, cudaStream_t s);
+void launch_panel_trsm(const ElimTask* tasks, const int4* work, int nwork, int p0, const Arenas& A,
+                       cudaStream_t s);
+void launch_panel_update(const ElimTask* tasks, const int4* work, int nwork, int p0, const Arenas& A,
+                         cudaStream_t s);
+void launch_big_finish(const ElimTask* tasks, int ncells, const Arenas& A, const double* dmin,
+                       const double* diag_scale, cudaStream_t s);
 void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
                         cudaStream_t s);
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,

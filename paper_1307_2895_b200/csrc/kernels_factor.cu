@@ -3,10 +3,8 @@
 // Work decomposition:
 //   * elim_small_kernel  -- one CTA per cell whose whole front fits in shared
 //                           memory: assembly, Cholesky, TRSM and Schur update.
-//   * elim_big_kernel    -- one CTA per large cell: assembles the c rows of the
-//                           front and the q x q clique part, Cholesky (shared
-//                           memory when it fits) and a panelled TRSM; the
-//                           Schur update U -= W^T W is then done by
+//   * large cells        -- blocked multi-CTA path in kernels_big.cu; their
+//                           Schur update U -= W^T W is done by
 //   * schur_tile_kernel  -- many CTAs per cell, 64 x 64 tiles on FP64 DMMA
 //                           tensor cores (mma.sync m8n8k4 f64).
 //   * skel_kernel        -- one CTA per skeletonization group: ID by
@@ -223,98 +221,7 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
 }
 
 // ---------------------------------------------------------------------------
-// Large cells, phase A (one CTA per cell): c rows of the front
-// ([F_cc | F_cq]) and the q x q clique part U; Cholesky of F_cc (shared memory
-// when it fits, otherwise in place in the record); W = C^-1 F_cq by column
-// panels staged in shared memory, written in place in the record.
-// ---------------------------------------------------------------------------
-constexpr int kPanel = kTrsmPanel;
-
-template <int NT>
-__global__ void __launch_bounds__(NT) elim_big_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ double red[NT / 32];
-  const ElimTask t = tasks[blockIdx.x];
-  const int nc = t.nc, nq = t.nq, nf = nc + nq;
-  int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
-  int32_t* smap = sdofs + nf;
-  const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(nf + t.maxnb), 16);
-  double* panel = reinterpret_cast<double*>(smem + ibytes);         // nc x kPanel
-  const bool c_in_smem = t.scratch_off < 0;
-  double* Cg = A.fac + t.C_off;
-  double* F = c_in_smem ? panel + (size_t)nc * kPanel : Cg;          // F_cc, ld nc
-  double* W = A.fac + t.W_off;                                       // nc x nq
-  double* U = A.bvals + t.U_off;                                     // nq x nq
-  const int32_t* gd = A.idx + t.dofs_off;
-  for (int i = threadIdx.x; i < nf; i += NT) sdofs[i] = gd[i];
-  for (int i = threadIdx.x; i < nc; i += NT) A.active[gd[i]] = 0;
-  for (int e = threadIdx.x; e < nc * nc; e += NT) F[e] = 0.0;
-  for (size_t e = threadIdx.x; e < (size_t)nc * nq; e += NT) W[e] = 0.0;
-  for (size_t e = threadIdx.x; e < (size_t)nq * nq; e += NT) U[e] = 0.0;
-  __syncthreads();
-  for (int p = threadIdx.x; p < nc; p += NT) {
-    const int g = sdofs[p];
-    for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
-      const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
-      if (pj < 0) continue;
-      const double v = A.a0[k];
-      if (pj < nc) F[(size_t)p * nc + pj] += v;
-      else W[(size_t)p * nq + pj - nc] += v;
-    }
-  }
-  __syncthreads();
-  const int32_t* bl = A.lists + t.blk_off;
-  for (int b = 0; b < t.nblk; ++b) {
-    const int bid = bl[b];
-    const int nb = A.blk_n[bid];
-    const int32_t* bd = A.idx + A.blk_dof_off[bid];
-    const double* bv = A.bvals + A.blk_val_off[bid];
-    for (int k = threadIdx.x; k < nb; k += NT) smap[k] = front_pos(sdofs, nc, nq, bd[k]);
-    __syncthreads();
-    for (size_t e = threadIdx.x; e < (size_t)nb * nb; e += NT) {
-      const int k = (int)(e / nb), l = (int)(e - (size_t)k * nb);
-      const int pk = smap[k], pl = smap[l];
-      if (pk < 0 || pl < 0) continue;
-      const double v = bv[e];
-      if (pk < nc) {
-        if (pl < nc) F[(size_t)pk * nc + pl] += v;
-        else W[(size_t)pk * nq + pl - nc] += v;
-      } else if (pl >= nc) {
-        U[(size_t)(pk - nc) * nq + pl - nc] += v;
-      }
-    }
-    __syncthreads();
-  }
-  const int st = chol_1sync<NT>(F, nc, nc, red);
-  if (st != 0) {
-    if (threadIdx.x == 0) A.status[blockIdx.x] = st;
-    return;
-  }
-  // W = C^-1 F_cq, kPanel columns at a time through shared memory
-  for (int j0 = 0; j0 < nq; j0 += kPanel) {
-    const int pw = min(kPanel, nq - j0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < nc * kPanel; e += NT) {
-      const int i = e / kPanel, j = e - i * kPanel;
-      panel[e] = j < pw ? W[(size_t)i * nq + j0 + j] : 0.0;
-    }
-    trsm_1sync<NT>(F, nc, nc, panel, kPanel, kPanel);
-    for (int e = threadIdx.x; e < nc * kPanel; e += NT) {
-      const int i = e / kPanel, j = e - i * kPanel;
-      if (j < pw) W[(size_t)i * nq + j0 + j] = panel[e];
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < nc * nc; e += NT) {
-    const int i = e / nc, j = e - i * nc;
-    const double v = (j <= i) ? F[e] : 0.0;
-    if (c_in_smem || j > i) Cg[e] = v;
-  }
-  if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
-}
-
-// ---------------------------------------------------------------------------
-// Large cells, phase B: U[a,b] -= sum_k W[k,a] W[k,b] on 64 x 64 tiles
+// Large cells, Schur update: U[a,b] -= sum_k W[k,a] W[k,b] on 64 x 64 tiles
 // (upper-triangular tile pairs, mirrored), FP64 DMMA m8n8k4.
 // 128 threads = 2 x 2 warps, each warp a 32 x 32 sub-tile (4 x 4 MMA tiles).
 // ---------------------------------------------------------------------------
@@ -703,16 +610,6 @@ void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, siz
   }
   if (nt <= 128) elim_small_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A);
   else elim_small_kernel<256><<<ntasks, 256, smem, s>>>(d_tasks, A);
-}
-
-void launch_elim_big(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, cudaStream_t s) {
-  if (ntasks <= 0) return;
-  static bool once = false;
-  if (!once) {
-    allow_smem(elim_big_kernel<512>);
-    once = true;
-  }
-  elim_big_kernel<512><<<ntasks, 512, smem, s>>>(d_tasks, A);
 }
 
 void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,

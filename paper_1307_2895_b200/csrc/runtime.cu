@@ -12,6 +12,7 @@
 // operation runs in the sm_100a kernels.
 #include <algorithm>
 #include <chrono>
+#include <cfloat>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -512,10 +513,8 @@ struct Factorizer {
         max_small_nf = std::max(max_small_nf, nf);
       } else {
         is_big[(size_t)t] = 1;
-        const size_t pan = sizeof(double) * (size_t)nc * kTrsmPanel;
-        const size_t with_c = ib + pan + sizeof(double) * (size_t)nc * nc;
-        if (with_c <= kSmemCap) { T.scratch_off = -1; smem_big = std::max(smem_big, with_c); }
-        else { T.scratch_off = 0; smem_big = std::max(smem_big, ib + pan); }
+        T.scratch_off = -1;
+        smem_big = std::max(smem_big, align16(sizeof(int32_t) * (size_t)(nf + 2 * T.maxnb)));
       }
       T.C_off = (int64_t)F->fac.bump((size_t)nc * nc, s);
       T.W_off = (int64_t)F->fac.bump((size_t)nc * nq, s);
@@ -551,17 +550,44 @@ struct Factorizer {
     }
     L.t_upd = now_s() - tp;
     tp = now_s();
-    // split into the shared-memory path and the large-front path (+ tiles)
+    // split into the shared-memory path and the blocked large-front path
     std::vector<ElimTask> small, big;
-    std::vector<int4> tiles;
+    std::vector<int4> tiles, asm_work;
+    int max_big_nc = 0;
     for (int64_t t = 0; t < nt; ++t) {
       const ElimTask& T = tasks[(size_t)t];
       if (!is_big[(size_t)t]) { small.push_back(T); continue; }
       const int bi = (int)big.size();
       big.push_back(T);
+      max_big_nc = std::max(max_big_nc, T.nc);
+      const int nf = T.nc + T.nq;
+      for (int r0 = 0; r0 < nf; r0 += 64) asm_work.push_back(make_int4(bi, r0, std::min(r0 + 64, nf), 0));
       const int ntl = (T.nq + kSchurTile - 1) / kSchurTile;
       for (int a = 0; a < ntl; ++a)
         for (int b = a; b < ntl; ++b) tiles.push_back(make_int4(bi, a, b, 0));
+    }
+    // per-panel work lists of the blocked Cholesky / TRSM
+    const int npanel = (max_big_nc + kPanelB - 1) / kPanelB;
+    std::vector<int32_t> pcells;
+    std::vector<int4> ptrsm, pupd;
+    std::vector<int64_t> pc_off(npanel + 1, 0), pt_off(npanel + 1, 0), pu_off(npanel + 1, 0);
+    for (int p = 0; p < npanel; ++p) {
+      const int p0 = p * kPanelB;
+      for (int bi = 0; bi < (int)big.size(); ++bi) {
+        const ElimTask& T = big[(size_t)bi];
+        if (T.nc <= p0) continue;
+        const int p1 = std::min(p0 + kPanelB, T.nc);
+        pcells.push_back(bi);
+        for (int r0 = p1; r0 < T.nc; r0 += 128) ptrsm.push_back(make_int4(bi, 0, r0, 0));
+        for (int c0 = 0; c0 < T.nq; c0 += 128) ptrsm.push_back(make_int4(bi, 1, c0, 0));
+        for (int a0 = p1; a0 < T.nc; a0 += 64) {
+          for (int b0 = p1; b0 <= a0; b0 += 64) pupd.push_back(make_int4(bi, 0, a0, b0));
+          for (int b0 = 0; b0 < T.nq; b0 += 64) pupd.push_back(make_int4(bi, 1, a0, b0));
+        }
+      }
+      pc_off[(size_t)p + 1] = (int64_t)pcells.size();
+      pt_off[(size_t)p + 1] = (int64_t)ptrsm.size();
+      pu_off[(size_t)p + 1] = (int64_t)pupd.size();
     }
     HTRACE("  host updates done (%zu small / %zu big / %zu tiles)", small.size(), big.size(), tiles.size());
     // uploads
@@ -571,15 +597,30 @@ struct Factorizer {
     lists.n = hl.size();
     lists.upload(hl.data(), 0, hl.size(), s);
     DBuf<ElimTask> d_small, d_big;
-    DBuf<int4> d_tiles;
+    DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd;
+    DBuf<int32_t> d_pcells;
+    DBuf<double> d_dmin, d_scale;
+    auto up4 = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
     d_small.reserve(small.size(), s);
     d_small.upload(small.data(), 0, small.size(), s);
     d_big.reserve(big.size(), s);
     d_big.upload(big.data(), 0, big.size(), s);
-    d_tiles.reserve(tiles.size(), s);
-    d_tiles.upload(tiles.data(), 0, tiles.size(), s);
+    up4(d_tiles, tiles);
+    up4(d_asm, asm_work);
+    up4(d_ptrsm, ptrsm);
+    up4(d_pupd, pupd);
+    d_pcells.reserve(pcells.size(), s);
+    d_pcells.upload(pcells.data(), 0, pcells.size(), s);
+    if (!big.empty()) {
+      std::vector<double> dm(big.size(), DBL_MAX);
+      d_dmin.reserve(big.size(), s);
+      d_dmin.upload(dm.data(), 0, dm.size(), s);
+      d_scale.reserve(big.size(), s);
+      HCK(cudaMemsetAsync(d_scale.p, 0, big.size() * sizeof(double), s));
+    }
     const int64_t st_small = (int64_t)status.bump(small.size(), s);
     const int64_t st_big = (int64_t)status.bump(big.size(), s);
+    if (!big.empty()) HCK(cudaMemsetAsync(status.p + st_big, 0, big.size() * sizeof(int), s));
     const char* what = is_top ? "top block" : "cell";
     pending.push_back({st_small, (int64_t)small.size(), tag, what});
     pending.push_back({st_big, (int64_t)big.size(), tag, what});
@@ -594,12 +635,24 @@ struct Factorizer {
     }
     if (!big.empty()) {
       A.status = status.p + st_big;
-      launch_elim_big(d_big.p, (int)big.size(), A, smem_big, s);
+      launch_big_assemble(d_big.p, d_asm.p, (int)asm_work.size(), A, d_scale.p, smem_big, s);
       ++g_launches;
+      for (int p = 0; p < npanel; ++p) {
+        const int p0 = p * kPanelB;
+        launch_panel_chol(d_big.p, d_pcells.p + pc_off[(size_t)p], (int)(pc_off[(size_t)p + 1] - pc_off[(size_t)p]),
+                          p0, A, d_dmin.p, s);
+        launch_panel_trsm(d_big.p, d_ptrsm.p + pt_off[(size_t)p], (int)(pt_off[(size_t)p + 1] - pt_off[(size_t)p]),
+                          p0, A, s);
+        launch_panel_update(d_big.p, d_pupd.p + pu_off[(size_t)p], (int)(pu_off[(size_t)p + 1] - pu_off[(size_t)p]),
+                            p0, A, s);
+        g_launches += 3;
+      }
       if (!tiles.empty()) {
         launch_schur_tiles(d_big.p, d_tiles.p, (int)tiles.size(), A, s);
         ++g_launches;
       }
+      launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
+      ++g_launches;
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
@@ -612,6 +665,12 @@ struct Factorizer {
     d_small.release(s);
     d_big.release(s);
     d_tiles.release(s);
+    d_asm.release(s);
+    d_ptrsm.release(s);
+    d_pupd.release(s);
+    d_pcells.release(s);
+    d_dmin.release(s);
+    d_scale.release(s);
     // solve-side reduction structure for the shared neighbour DOFs
     if (!is_top) build_reduction(L);
     L.t_sync = now_s() - tp;
