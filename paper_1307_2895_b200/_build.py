@@ -18,6 +18,7 @@ LIB = os.path.join(PKG, "libhifde_gpu.so")
 SOURCES = [
     "csrc/kernels_factor.cu",
     "csrc/kernels_big.cu",
+    "csrc/kernels_skelbig.cu",
     "csrc/kernels_solve.cu",
     "csrc/runtime.cu",
     "csrc/partition.cpp",

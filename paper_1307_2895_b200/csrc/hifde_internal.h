@@ -32,6 +32,19 @@ struct SkelTask {
   int32_t mode;             // workspace placement: 0 shared, 1 Mq shared, 2 global
 };
 
+// Skeletonization of a group too large for one CTA (kernels_skelbig.cu).
+struct SkelBigTask {
+  int32_t nc, nq;
+  int32_t nblk, maxnb;
+  int64_t dofs_off, blk_off;
+  int64_t ws_off;           // scratch arena: A_cc, Mq, Tp, norms, candidates
+  int64_t iws_off;          // int scratch: pivots, sk / rd orders
+  int64_t rec_off, delta_off, out_off;
+  int32_t group, pad;
+};
+constexpr int kCL = 16;                        // CTAs per cluster in the large-group CPQR
+constexpr int kMaxBigNc = 4096;                // largest group handled by that path
+
 // Solve-sweep record (one per elimination cell / skeleton group with rd != {}).
 struct SolveRec {
   int32_t nc;               // |cell| (elimination) or |rd| (skeleton)
@@ -57,6 +70,7 @@ struct Arenas {
   uint8_t* active;          // device active mask (exact-order batches)
   int* status;              // per-task status words
   int32_t* kout;            // per-group skeleton rank
+  int32_t* iscratch;        // per-level integer scratch
 };
 
 constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA we use
@@ -81,6 +95,18 @@ void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,
                  cudaStream_t s);
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s);
+
+void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
+                             size_t smem, cudaStream_t s);
+cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
+                                cudaStream_t s);
+void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,
+                         double* dscale, cudaStream_t s);
+void launch_skelbig_t(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
+void launch_skelbig_congruence(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
+                               cudaStream_t s);
+void launch_skelbig_symm(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, double* dscale,
+                         cudaStream_t s);
 
 // solve
 void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256) panel_chol_kernel(const ElimTask* __restr
   if (A.status[cell] != 0) return;
   const ElimTask t = tasks[cell];
   const int nc = t.nc;
+  if (p0 >= nc) return;
   const int pw = min(PB, nc - p0);
   double* F = A.fac + t.C_off;
   for (int e = threadIdx.x; e < pw * pw; e += 256) {
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(kChunk) panel_trsm_kernel(const ElimTask* __re
   if (A.status[cell] != 0) return;
   const ElimTask t = tasks[cell];
   const int nc = t.nc, nq = t.nq;
+  if (p0 >= nc || (w.y == 0 ? w.z >= nc : w.z >= nq)) return;
   const int pw = min(PB, nc - p0);
   const double* F = A.fac + t.C_off;
   for (int e = threadIdx.x; e < pw * pw; e += kChunk) {
@@ -279,8 +281,9 @@ __global__ void __launch_bounds__(128) panel_update_kernel(const ElimTask* __res
   if (A.status[cell] != 0) return;
   const ElimTask t = tasks[cell];
   const int nc = t.nc, nq = t.nq;
-  const int pw = min(PB, nc - p0);
   const int a0 = w.z, b0 = w.w;
+  if (p0 >= nc || a0 >= nc || (w.y == 1 && b0 >= nq)) return;
+  const int pw = min(PB, nc - p0);
   double* F = A.fac + t.C_off;
   double* W = A.fac + t.W_off;
   const bool kindW = w.y == 1;

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
   const ElimTask t = tasks[tl.x];
   const int nc = t.nc, nq = t.nq;
   const int a0 = tl.y * kTile, b0 = tl.z * kTile;
+  if (a0 >= nq || b0 >= nq) return;
   const double* W = A.fac + t.W_off;
   double* U = A.bvals + t.U_off;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

@@ -1,0 +1,562 @@
+// Skeletonization of groups too large for one CTA (sm_100a).
+//
+// Pipeline per batch of large groups (src/factor_ops.py:162-214,
+// src/dense.py:239-264):
+//   skelbig_assemble_kernel  rows of A_cc (row-major) and Mq = A_qc
+//                            (column-major) into scratch; one CTA per row chunk.
+//   cpqr_cluster_kernel      column-pivoted QR of Mq with the rank cut, by a
+//                            thread-block cluster of kCL CTAs per group.
+//                            Columns are owned round-robin by the cluster's
+//                            CTAs and never moved (pivoting = a pivot list);
+//                            each step every CTA rebuilds the reflector from
+//                            the pivot column, updates and downdates its own
+//                            columns, and posts its best remaining norm; one
+//                            cluster barrier per step.  dlaqp2 semantics.
+//   skelbig_sort_kernel      sk / rd ascending, output index lists, inner task.
+//   skelbig_t_kernel         T = R11^-1 R12 (one thread per rd column), written
+//                            row-permuted to ascending sk order in the record.
+//   skelbig_bsr_kernel       B_sr = A_sr - A_ss T   (DMMA), stored as W^T input.
+//   skelbig_brr_kernel       B_rr = A_rr - A_sr^T T - T^T B_sr (DMMA).
+//   skelbig_symm_kernel      B_rr <- (B_rr + B_rr^T)/2, max |diag|.
+// The inner elimination of rd against sk (Cholesky of B_rr, W, delta block
+// -W^T W) reuses the blocked large-cell kernels of kernels_big.cu.
+#include <cfloat>
+#include <cooperative_groups.h>
+#include <cstdint>
+
+#include "hifde_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace hifde {
+
+namespace {
+
+__device__ __forceinline__ int bsearch_i32(const int32_t* s, int n, int32_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (s[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return (lo < n && s[lo] == key) ? lo : -1;
+}
+
+__device__ __forceinline__ int front_pos(const int32_t* dofs, int nc, int nq, int32_t g) {
+  int p = bsearch_i32(dofs, nc, g);
+  if (p >= 0) return p;
+  p = bsearch_i32(dofs + nc, nq, g);
+  return p >= 0 ? nc + p : -1;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// scratch layout of one large group (doubles)
+struct BigWs {
+  double *Acc, *Mq, *Tp, *vn1, *vn2, *rdiag, *cand;
+  int32_t *piv, *skl, *sko, *rdl;
+};
+__device__ __forceinline__ BigWs big_ws(const SkelBigTask& t, const Arenas& A) {
+  BigWs w;
+  const size_t nc = t.nc, nq = t.nq;
+  w.Acc = A.scratch + t.ws_off;
+  w.Mq = w.Acc + nc * nc;
+  w.Tp = w.Mq + nq * nc;
+  w.vn1 = w.Tp + (nc * nc / 4 + nc);
+  w.vn2 = w.vn1 + nc;
+  w.rdiag = w.vn2 + nc;
+  w.cand = w.rdiag + nc;  // 2 x kCL x (value, index)
+  w.piv = A.iscratch + t.iws_off;
+  w.skl = w.piv + nc;
+  w.sko = w.skl + nc;
+  w.rdl = w.sko + nc;
+  return w;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Assembly of [A_cc ; Mq].  Work item int4 {task, r0, r1, 0}: front rows.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask* __restrict__ tasks,
+                                                               const int4* __restrict__ work, Arenas A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int nsel;
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const int nc = t.nc, nq = t.nq, nf = nc + nq;
+  const int r0 = wk.y, r1 = wk.z;
+  int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
+  int32_t* salive = sdofs + nf;
+  int32_t* smap = salive + nf;
+  int32_t* ssel = smap + t.maxnb;
+  const BigWs w = big_ws(t, A);
+  const int32_t* gd = A.idx + t.dofs_off;
+  for (int i = threadIdx.x; i < nf; i += 256) {
+    sdofs[i] = gd[i];
+    salive[i] = i < nc ? 1 : (int)A.active[gd[i]];
+  }
+  for (int r = r0; r < r1; ++r) {
+    if (r < nc) for (int j = threadIdx.x; j < nc; j += 256) w.Acc[(size_t)r * nc + j] = 0.0;
+    else for (int j = threadIdx.x; j < nc; j += 256) w.Mq[(size_t)(r - nc) + (size_t)j * nq] = 0.0;
+  }
+  __syncthreads();
+  // original couplings: c rows give A_cc, alive q rows give their c columns
+  for (int r = r0 + (int)threadIdx.x; r < r1; r += 256) {
+    if (!salive[r]) continue;
+    const int g = sdofs[r];
+    for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
+      const int pj = bsearch_i32(sdofs, nc, A.indices[k]);
+      if (pj < 0) continue;
+      if (r < nc) w.Acc[(size_t)r * nc + pj] += A.a0[k];
+      else w.Mq[(size_t)(r - nc) + (size_t)pj * nq] += A.a0[k];
+    }
+  }
+  __syncthreads();
+  const int32_t* bl = A.lists + t.blk_off;
+  for (int b = 0; b < t.nblk; ++b) {
+    const int bid = bl[b];
+    const int nb = A.blk_n[bid];
+    const int32_t* bd = A.idx + A.blk_dof_off[bid];
+    const double* bv = A.bvals + A.blk_val_off[bid];
+    if (threadIdx.x == 0) nsel = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb; k += 256) {
+      int p = front_pos(sdofs, nc, nq, bd[k]);
+      if (p >= 0 && !salive[p]) p = -1;
+      smap[k] = p;
+      if (p >= r0 && p < r1) ssel[atomicAdd(&nsel, 1)] = k;
+    }
+    __syncthreads();
+    const int ns = nsel;
+    for (int s = 0; s < ns; ++s) {
+      const int k = ssel[s];
+      const int pk = smap[k];
+      const double* brow = bv + (size_t)k * nb;
+      for (int l = threadIdx.x; l < nb; l += 256) {
+        const int pl = smap[l];
+        if (pl < 0 || pl >= nc) continue;
+        if (pk < nc) w.Acc[(size_t)pk * nc + pl] += brow[l];
+        else w.Mq[(size_t)(pk - nc) + (size_t)pl * nq] += brow[l];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster CPQR.  grid = ntasks * kCL, cluster (kCL,1,1), 256 threads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) cpqr_cluster_kernel(const SkelBigTask* __restrict__ tasks, Arenas A,
+                                                           double eps) {
+  extern __shared__ __align__(16) double vsm[];  // reflector column (nq doubles)
+  __shared__ double red[8];
+  __shared__ double sh_best;
+  __shared__ int sh_pvt;
+  __shared__ unsigned char done[kMaxBigNc];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rb = (int)cluster.block_rank();
+  const int CL = (int)cluster.num_blocks();
+  const SkelBigTask t = tasks[blockIdx.x / CL];
+  const int nc = t.nc, nq = t.nq;
+  const BigWs w = big_ws(t, A);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ldq = nq;
+  for (int j = threadIdx.x; j < nc; j += 256) done[j] = 0;
+  int nq_alive = 0;  // rows of inactive DOFs are exact zeros; count the live ones
+  {
+    const int32_t* gd = A.idx + t.dofs_off;
+    int c = 0;
+    for (int i = threadIdx.x; i < nq; i += 256) c += A.active[gd[nc + i]] ? 1 : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) red[wid] = c;
+    __syncthreads();
+    for (int i = 0; i < 8; ++i) nq_alive += (int)red[i];
+    __syncthreads();
+  }
+  // initial norms of the owned columns and the first candidate
+  double best = -1.0;
+  int bidx = nc;
+  for (int j = rb + CL * wid; j < nc; j += CL * 8) {
+    const double* col = w.Mq + (size_t)j * ldq;
+    double s = 0.0;
+    for (int r = lane; r < nq; r += 32) s += col[r] * col[r];
+    s = sqrt(warp_sum(s));
+    if (lane == 0) { w.vn1[j] = s; w.vn2[j] = s; }
+    if (s > best || (s == best && j < bidx)) { best = s; bidx = j; }
+  }
+  // block argmax of (best, bidx) -> this CTA's candidate slot
+  __shared__ double wbest[8];
+  __shared__ int widx[8];
+  auto block_best = [&](double v, int ix, int slot) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+      if (ov > v || (ov == v && oi < ix)) { v = ov; ix = oi; }
+    }
+    if (lane == 0) { wbest[wid] = v; widx[wid] = ix; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bv = wbest[0];
+      int bi = widx[0];
+      for (int q = 1; q < 8; ++q)
+        if (wbest[q] > bv || (wbest[q] == bv && widx[q] < bi)) { bv = wbest[q]; bi = widx[q]; }
+      w.cand[(size_t)(slot * CL + rb) * 2] = bv;
+      w.cand[(size_t)(slot * CL + rb) * 2 + 1] = (double)bi;
+    }
+  };
+  block_best(best, bidx, 0);
+  cluster.sync();
+
+  const int kmax = nq < nc ? nq : nc;
+  const double tol3z = sqrt(DBL_EPSILON * 0.5);
+  double thr = 0.0;
+  int k = kmax;
+  for (int i = 0; i < kmax; ++i) {
+    const int slot = i & 1;
+    if (threadIdx.x == 0) {
+      double bv = -1.0;
+      int bi = nc;
+      for (int q = 0; q < CL; ++q) {
+        const double v = __ldcg(&w.cand[(size_t)(slot * CL + q) * 2]);
+        const int ix = (int)__ldcg(&w.cand[(size_t)(slot * CL + q) * 2 + 1]);
+        if (v > bv || (v == bv && ix < bi)) { bv = v; bi = ix; }
+      }
+      sh_best = bv;
+      sh_pvt = bi;
+    }
+    __syncthreads();
+    const int P = sh_pvt;
+    if (i == 0 && sh_best == 0.0) { k = 0; break; }  // zero block: all redundant
+
+    // reflector from column P rows i.. (every CTA, identical arithmetic)
+    const double* colP = w.Mq + (size_t)P * ldq;
+    double xs = 0.0;
+    for (int r = i + 1 + (int)threadIdx.x; r < nq; r += 256) {
+      const double x = __ldcg(colP + r);
+      vsm[r] = x;
+      xs += x * x;
+    }
+    xs = warp_sum(xs);
+    if (lane == 0) red[wid] = xs;
+    __syncthreads();
+    double xn2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) xn2 += red[q];
+    const double xnorm = sqrt(xn2);
+    const double alpha = __ldcg(colP + i);
+    double beta, tau, scal;
+    if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
+    else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    const double rii = fabs(beta);
+    if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
+    if (rii <= thr) { k = i; break; }
+    if (rb == 0 && threadIdx.x == 0) {
+      w.rdiag[i] = beta;
+      w.piv[i] = P;
+    }
+    // update the owned, not yet pivoted columns (warp per column)
+    best = -1.0;
+    bidx = nc;
+    for (int j = rb + CL * wid; j < nc; j += CL * 8) {
+      if (done[j] || j == P) continue;
+      double* col = w.Mq + (size_t)j * ldq;
+      if (tau != 0.0) {
+        double s = 0.0;
+        for (int r = i + 1 + lane; r < nq; r += 32) s += vsm[r] * col[r];
+        s = warp_sum(s);
+        const double wv = tau * (col[i] + scal * s);
+        __syncwarp();
+        if (lane == 0) col[i] -= wv;
+        const double ws2 = wv * scal;
+        for (int r = i + 1 + lane; r < nq; r += 32) col[r] -= ws2 * vsm[r];
+        __syncwarp();
+      }
+      double nv = w.vn1[j];
+      bool recompute = false;
+      if (nv != 0.0) {
+        double tmp = fabs(col[i]) / nv;
+        tmp = 1.0 - tmp * tmp;
+        tmp = tmp > 0.0 ? tmp : 0.0;
+        const double ratio = nv / w.vn2[j];
+        if (tmp * ratio * ratio <= tol3z) recompute = true;
+        else nv *= sqrt(tmp);
+      }
+      if (recompute) {
+        double s = 0.0;
+        for (int r = i + 1 + lane; r < nq; r += 32) s += col[r] * col[r];
+        s = warp_sum(s);
+        nv = (i + 1 < nq) ? sqrt(s) : 0.0;
+        if (lane == 0) w.vn2[j] = nv;
+      }
+      if (lane == 0) w.vn1[j] = nv;
+      if (nv > best || (nv == best && j < bidx)) { best = nv; bidx = j; }
+    }
+    __syncthreads();
+    if (P % CL == rb && threadIdx.x == 0) done[P] = 1;
+    block_best(best, bidx, slot ^ 1);
+    cluster.sync();
+  }
+  if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
+}
+
+// ---------------------------------------------------------------------------
+// sk / rd ascending, output lists, inner elimination task (one CTA per group)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) skelbig_sort_kernel(const SkelBigTask* __restrict__ tasks, Arenas A,
+                                                           ElimTask* __restrict__ inner, double* __restrict__ dmin,
+                                                           double* __restrict__ dscale) {
+  __shared__ unsigned char piv_flag[kMaxBigNc];
+  const SkelBigTask t = tasks[blockIdx.x];
+  const int nc = t.nc;
+  const BigWs w = big_ws(t, A);
+  const int k = A.kout[t.group], r = nc - k;
+  for (int j = threadIdx.x; j < nc; j += 256) piv_flag[j] = 0;
+  __syncthreads();
+  for (int a = threadIdx.x; a < k; a += 256) piv_flag[w.piv[a]] = 1;
+  __syncthreads();
+  for (int a = threadIdx.x; a < k; a += 256) {
+    const int v = w.piv[a];
+    int rank = 0;
+    for (int b = 0; b < k; ++b) rank += w.piv[b] < v;
+    w.skl[rank] = v;
+    w.sko[rank] = a;
+  }
+  // rd: the non-pivoted columns in ascending order
+  for (int j = threadIdx.x; j < nc; j += 256) {
+    if (piv_flag[j]) continue;
+    int rank = 0;
+    for (int l = 0; l < j; ++l) rank += piv_flag[l] ? 0 : 1;
+    w.rdl[rank] = j;
+  }
+  __syncthreads();
+  const int32_t* gd = A.idx + t.dofs_off;
+  int32_t* out = A.idx + t.out_off;
+  for (int a = threadIdx.x; a < k; a += 256) out[a] = gd[w.skl[a]];
+  for (int b = threadIdx.x; b < r; b += 256) out[k + b] = gd[w.rdl[b]];
+  if (threadIdx.x == 0) {
+    ElimTask e;
+    e.nc = r;
+    e.nq = k;
+    e.nblk = 0;
+    e.maxnb = 0;
+    e.dofs_off = 0;
+    e.blk_off = 0;
+    e.scratch_off = -1;
+    e.C_off = t.rec_off + (int64_t)k * r;
+    e.W_off = e.C_off + (int64_t)r * r;
+    e.U_off = t.delta_off;
+    inner[blockIdx.x] = e;
+    dmin[blockIdx.x] = DBL_MAX;
+    dscale[blockIdx.x] = 0.0;
+    A.status[blockIdx.x] = 0;
+  }
+}
+
+// T = R11^-1 R12, one thread per rd column; stored to the record with rows in
+// ascending sk order.  grid: int4 {task, col0, 0, 0}.
+__global__ void __launch_bounds__(128) skelbig_t_kernel(const SkelBigTask* __restrict__ tasks,
+                                                        const int4* __restrict__ work, Arenas A) {
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const int nc = t.nc, nq = t.nq;
+  const BigWs w = big_ws(t, A);
+  const int k = A.kout[t.group], r = nc - k;
+  const int b = wk.y + (int)threadIdx.x;
+  if (b >= r) return;
+  const double* R = w.Mq;  // R[a][col] = Mq[a + col*nq]
+  const int cb = w.rdl[b];
+  for (int a = k - 1; a >= 0; --a) {
+    double s = R[a + (size_t)cb * nq];
+    for (int l = a + 1; l < k; ++l) s -= R[a + (size_t)w.piv[l] * nq] * w.Tp[(size_t)l * r + b];
+    w.Tp[(size_t)a * r + b] = s / w.rdiag[a];
+  }
+  double* T = A.fac + t.rec_off;
+  for (int a = 0; a < k; ++a) T[(size_t)a * r + b] = w.Tp[(size_t)w.sko[a] * r + b];
+}
+
+// ---------------------------------------------------------------------------
+// Congruence products on 64 x 64 tiles (DMMA m8n8k4, 2 x 2 warps of 32 x 32)
+//   kind 0 (tile a over sk, b over rd): B_sr[a,b] = A_cc[sk_a, rd_b]
+//            - sum_l A_cc[sk_a, sk_l] T[l,b];  stored transposed into W (r x k)
+//   kind 1 (a, b over rd):  B_rr[a,b] = A_cc[rd_a, rd_b]
+//            - sum_l A_cc[rd_a, sk_l] T[l,b] - sum_l T[l,a] B_sr[l,b]; into C
+// work item int4 {task, kind, a0, b0}
+// ---------------------------------------------------------------------------
+constexpr int kT = 64, kKs = 16, kLd = 68;
+
+__global__ void __launch_bounds__(128) skelbig_congruence_kernel(const SkelBigTask* __restrict__ tasks,
+                                                                 const int4* __restrict__ work, Arenas A) {
+  __shared__ double As[kKs][kLd];
+  __shared__ double Bs[kKs][kLd];
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const int nc = t.nc;
+  const BigWs w = big_ws(t, A);
+  const int k = A.kout[t.group], r = nc - k;
+  const int kind = wk.y, a0 = wk.z, b0 = wk.w;
+  const int na = kind == 0 ? k : r;
+  if (r == 0 || a0 >= na || b0 >= r) return;
+  const double* T = A.fac + t.rec_off;            // k x r, ascending sk rows
+  double* C = A.fac + t.rec_off + (size_t)k * r;   // r x r
+  double* W = C + (size_t)r * r;                   // r x k  (= B_sr^T)
+  const int32_t* ra = kind == 0 ? w.skl : w.rdl;   // row index set of the tile
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wy = wid >> 1, wx = wid & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  const int npass = kind == 0 ? 1 : 2;
+  for (int pass = 0; pass < npass; ++pass) {
+    for (int l0 = 0; l0 < k; l0 += kKs) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kKs * kT; e += 128) {
+        const int ll = e / kT, x = e - ll * kT;
+        const int l = l0 + ll;
+        double av = 0.0, bv = 0.0;
+        if (l < k) {
+          if (a0 + x < na) {
+            if (pass == 0) av = w.Acc[(size_t)ra[a0 + x] * nc + w.skl[l]];   // A[row][sk_l]
+            else av = T[(size_t)l * r + a0 + x];                             // T[l][a]
+          }
+          if (b0 + x < r) {
+            if (pass == 0) bv = T[(size_t)l * r + b0 + x];                   // T[l][b]
+            else bv = W[(size_t)(b0 + x) * k + l];                           // B_sr[l][b]
+          }
+        }
+        As[ll][x] = av;
+        Bs[ll][x] = bv;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kKs; kk += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) af[m] = As[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) bf[n] = Bs[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = a0 + wy * 32 + m * 8 + (lane >> 2);
+        const int b = b0 + wx * 32 + n * 8 + 2 * (lane & 3) + h;
+        if (a >= na || b >= r) continue;
+        const double v = w.Acc[(size_t)ra[a] * nc + w.rdl[b]] - acc[m][n][h];
+        if (kind == 0) W[(size_t)b * k + a] = v;
+        else C[(size_t)a * r + b] = v;
+      }
+}
+
+// B_rr <- (B_rr + B_rr^T) / 2 and max |diag|; work item int4 {task, row0, 0, 0}
+__global__ void __launch_bounds__(256) skelbig_symm_kernel(const SkelBigTask* __restrict__ tasks,
+                                                           const int4* __restrict__ work, Arenas A,
+                                                           const int32_t* __restrict__ task_of, double* dscale) {
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const int k = A.kout[t.group], r = t.nc - k;
+  double* C = A.fac + t.rec_off + (size_t)k * r;
+  double m = 0.0;
+  for (int a = wk.y; a < min(wk.y + 64, r); ++a) {
+    for (int b = threadIdx.x; b < a; b += 256) {
+      const double v = 0.5 * (C[(size_t)a * r + b] + C[(size_t)b * r + a]);
+      C[(size_t)a * r + b] = v;
+      C[(size_t)b * r + a] = v;
+    }
+    if (threadIdx.x == 0) m = fmax(m, fabs(C[(size_t)a * r + a]));
+  }
+  (void)task_of;
+  if (threadIdx.x == 0 && wk.y < r) {
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(dscale + wk.x);
+    atomicMax(p, (unsigned long long)__double_as_longlong(m));
+  }
+}
+
+// ---------------------------------------------------------------------------
+void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
+                             size_t smem, cudaStream_t s) {
+  if (nwork <= 0) return;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(skelbig_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemCapBytes);
+    once = true;
+  }
+  skelbig_assemble_kernel<<<nwork, 256, smem, s>>>(tasks, work, A);
+}
+
+cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
+                                cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (size_t)max_nq;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(cpqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cpqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmemCapBytes);
+    once = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(ntasks * kCL), 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cpqr_cluster_kernel, tasks, A, eps);
+}
+
+void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,
+                         double* dscale, cudaStream_t s) {
+  if (ntasks <= 0) return;
+  skelbig_sort_kernel<<<ntasks, 256, 0, s>>>(tasks, A, inner, dmin, dscale);
+}
+
+void launch_skelbig_t(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
+  if (nwork <= 0) return;
+  skelbig_t_kernel<<<nwork, 128, 0, s>>>(tasks, work, A);
+}
+
+void launch_skelbig_congruence(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
+                               cudaStream_t s) {
+  if (nwork <= 0) return;
+  skelbig_congruence_kernel<<<nwork, 128, 0, s>>>(tasks, work, A);
+}
+
+void launch_skelbig_symm(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, double* dscale,
+                         cudaStream_t s) {
+  if (nwork <= 0) return;
+  skelbig_symm_kernel<<<nwork, 256, 0, s>>>(tasks, work, A, nullptr, dscale);
+}
+
+}  // namespace hifde

@@ -297,6 +297,7 @@ struct Factorizer {
   DBuf<int32_t> lists;
   DBuf<int> status;
   DBuf<int32_t> kout;
+  DBuf<int32_t> iscratch;
   // stamps (serial paths)
   std::vector<int64_t> dstamp;
   int64_t stamp = 0;
@@ -340,6 +341,7 @@ struct Factorizer {
     A.active = d_active;
     A.status = status.p;
     A.kout = kout.p;
+    A.iscratch = iscratch.p;
     return A;
   }
 
@@ -771,9 +773,8 @@ struct Factorizer {
         T.scratch_off = (int64_t)scratch.bump(2 * (size_t)nc * nc + 3 * q4 + 8, s);
         smem = std::max(smem, ib + sizeof(double) * mq);
       } else {
-        T.mode = 2;
-        T.scratch_off = (int64_t)scratch.bump(wsd + 8, s);
-        smem = std::max(smem, ib);
+        T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
+        T.scratch_off = -1;
       }
       T.rec_off = (int64_t)F->fac.bump((size_t)nc * nc + 2 * q4, s);
       T.delta_off = (int64_t)bvals.bump((size_t)nc * nc, s);
@@ -803,36 +804,92 @@ struct Factorizer {
     for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
     std::stable_sort(order.begin(), order.end(),
                      [&](int64_t a, int64_t b) { return batch[(size_t)a] < batch[(size_t)b]; });
-    std::vector<SkelTask> sorted((size_t)nt);
-    std::vector<int64_t> bstart((size_t)nbatch + 1, 0);
+    // per batch: small groups (one CTA each) and large groups (cluster path)
+    std::vector<SkelTask> sorted, hsk;        // small tasks; SkelTask view of large ones
+    std::vector<SkelBigTask> huge;
+    std::vector<int64_t> bs((size_t)nbatch + 1, 0), bh((size_t)nbatch + 1, 0);
+    int huge_max_nq = 0, huge_max_nf = 0, huge_max_nb = 0;
+    iscratch.n = 0;
     for (int64_t i = 0; i < nt; ++i) {
-      sorted[(size_t)i] = tasks[(size_t)order[(size_t)i]];
-      bstart[(size_t)batch[(size_t)order[(size_t)i]] + 1]++;
+      const SkelTask& T = tasks[(size_t)order[(size_t)i]];
+      const int b = batch[(size_t)order[(size_t)i]];
+      if (T.mode != 2) {
+        sorted.push_back(T);
+        bs[(size_t)b + 1]++;
+        continue;
+      }
+      if (T.nc > kMaxBigNc) throw Fail{HIFDE_INTERNAL, "skeleton group larger than kMaxBigNc"};
+      SkelBigTask H;
+      H.nc = T.nc;
+      H.nq = T.nq;
+      H.nblk = T.nblk;
+      H.maxnb = T.maxnb;
+      H.dofs_off = T.dofs_off;
+      H.blk_off = T.blk_off;
+      const size_t nc = (size_t)T.nc, nq = (size_t)T.nq;
+      H.ws_off = (int64_t)scratch.bump(nc * nc + nq * nc + (nc * nc / 4 + nc) + 3 * nc + 4 * kCL + 8, s);
+      H.iws_off = (int64_t)iscratch.bump(4 * nc + 4, s);
+      H.rec_off = T.rec_off;
+      H.delta_off = T.delta_off;
+      H.out_off = T.out_off;
+      H.group = T.group;
+      H.pad = 0;
+      huge.push_back(H);
+      hsk.push_back(T);
+      bh[(size_t)b + 1]++;
+      huge_max_nq = std::max(huge_max_nq, T.nq);
+      huge_max_nf = std::max(huge_max_nf, T.nc + T.nq);
+      huge_max_nb = std::max(huge_max_nb, T.maxnb);
     }
-    for (int b = 0; b < nbatch; ++b) bstart[(size_t)b + 1] += bstart[(size_t)b];
+    for (int b = 0; b < nbatch; ++b) {
+      bs[(size_t)b + 1] += bs[(size_t)b];
+      bh[(size_t)b + 1] += bh[(size_t)b];
+    }
     upload_idx();
     upload_blocks();
     lists.reserve(std::max<size_t>(hl.size(), 1), s);
     lists.n = hl.size();
     lists.upload(hl.data(), 0, hl.size(), s);
-    DBuf<SkelTask> dt;
-    dt.reserve((size_t)nt, s);
-    dt.upload(sorted.data(), 0, (size_t)nt, s);
+    DBuf<SkelTask> dt, dth;
+    DBuf<SkelBigTask> dhuge;
+    DBuf<ElimTask> dinner;
+    DBuf<double> ddmin, dscale;
+    dt.reserve(sorted.size(), s);
+    dt.upload(sorted.data(), 0, sorted.size(), s);
+    dth.reserve(hsk.size(), s);
+    dth.upload(hsk.data(), 0, hsk.size(), s);
+    dhuge.reserve(huge.size(), s);
+    dhuge.upload(huge.data(), 0, huge.size(), s);
+    dinner.reserve(huge.size(), s);
+    ddmin.reserve(huge.size(), s);
+    dscale.reserve(huge.size(), s);
     const int64_t st_off = (int64_t)status.bump((size_t)nt, s);
+    HCK(cudaMemsetAsync(status.p + st_off, 0, (size_t)nt * sizeof(int), s));
     pending.push_back({st_off, nt, tag, "group"});
+    const int64_t st_huge = (int64_t)status.bump(huge.size(), s);
+    if (!huge.empty()) {
+      HCK(cudaMemsetAsync(status.p + st_huge, 0, huge.size() * sizeof(int), s));
+      pending.push_back({st_huge, (int64_t)huge.size(), tag, "large group"});
+    }
     kout.n = 0;
     kout.bump((size_t)nt, s);
     Arenas A = arenas();
     A.status = status.p + st_off;
+    Arenas AH = A;
+    AH.status = status.p + st_huge;
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
     for (int b = 0; b < nbatch; ++b) {
-      const int64_t lo = bstart[(size_t)b], hi = bstart[(size_t)b + 1];
-      if (hi <= lo) continue;
-      launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
-      launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
-      g_launches += 2;
+      const int64_t lo = bs[(size_t)b], hi = bs[(size_t)b + 1];
+      if (hi > lo) {
+        launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
+        launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
+        g_launches += 2;
+      }
+      const int64_t hlo = bh[(size_t)b], hhi = bh[(size_t)b + 1];
+      if (hhi > hlo) launch_huge_batch(huge, hlo, hhi, dhuge.p, dth.p, dinner.p, ddmin.p, dscale.p, A, AH,
+                                       huge_max_nq, huge_max_nf, huge_max_nb);
       if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  batch %d done", b); }
     }
     HCK(cudaEventRecord(L.ev1, s));
@@ -852,6 +909,11 @@ struct Factorizer {
     L.t_sync = now_s() - tp;
     tp = now_s();
     dt.release(s);
+    dth.release(s);
+    dhuge.release(s);
+    dinner.release(s);
+    ddmin.release(s);
+    dscale.release(s);
     for (int64_t t = 0; t < nt; ++t) {
       const SkelTask& T = tasks[(size_t)t];
       const int kk = k[(size_t)t], r = T.nc - kk;
@@ -882,6 +944,93 @@ struct Factorizer {
       L.gbytes += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
     }
     L.t_upd = now_s() - tp;
+  }
+
+  // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
+  void launch_huge_batch(const std::vector<SkelBigTask>& huge, int64_t lo, int64_t hi, const SkelBigTask* d_all,
+                         const SkelTask* d_skv, ElimTask* d_inner_all, double* d_dmin_all, double* d_scale_all,
+                         const Arenas& A, const Arenas& AH_all, int max_nq, int max_nf, int max_nb) {
+    const int n = (int)(hi - lo);
+    const SkelBigTask* dtk = d_all + lo;
+    ElimTask* inner = d_inner_all + lo;
+    double* dmin = d_dmin_all + lo;
+    double* dscale = d_scale_all + lo;
+    Arenas AH = AH_all;
+    AH.status = AH_all.status + lo;
+    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles;
+    std::vector<int32_t> pc;
+    int maxnc = 0;
+    for (int i = 0; i < n; ++i) maxnc = std::max(maxnc, huge[(size_t)(lo + i)].nc);
+    const int npanel = (maxnc + kPanelB - 1) / kPanelB;
+    std::vector<int64_t> pco(npanel + 1, 0), pto(npanel + 1, 0), puo(npanel + 1, 0);
+    for (int i = 0; i < n; ++i) {
+      const SkelBigTask& H = huge[(size_t)(lo + i)];
+      const int nc = H.nc, nf = H.nc + H.nq;
+      for (int r0 = 0; r0 < nf; r0 += 64) wasm.push_back(make_int4(i, r0, std::min(r0 + 64, nf), 0));
+      for (int c0 = 0; c0 < nc; c0 += 128) wt.push_back(make_int4(i, c0, 0, 0));
+      for (int a0 = 0; a0 < nc; a0 += 64)
+        for (int b0 = 0; b0 < nc; b0 += 64) {
+          wc0.push_back(make_int4(i, 0, a0, b0));
+          wc1.push_back(make_int4(i, 1, a0, b0));
+        }
+      for (int r0 = 0; r0 < nc; r0 += 64) wsym.push_back(make_int4(i, r0, 0, 0));
+      const int ntl = (nc + kSchurTile - 1) / kSchurTile;  // sk <= nc
+      for (int a = 0; a < ntl; ++a)
+        for (int b = a; b < ntl; ++b) tiles.push_back(make_int4(i, a, b, 0));
+    }
+    // inner elimination work lists on the size bounds (r <= nc, k <= nc);
+    // the kernels skip items beyond the sizes the device actually found
+    for (int p = 0; p < npanel; ++p) {
+      const int p0 = p * kPanelB;
+      for (int i = 0; i < n; ++i) {
+        const int nc = huge[(size_t)(lo + i)].nc;
+        if (nc <= p0) continue;
+        const int p1 = std::min(p0 + kPanelB, nc);
+        pc.push_back(i);
+        for (int r0 = p1; r0 < nc; r0 += 128) pt.push_back(make_int4(i, 0, r0, 0));
+        for (int c0 = 0; c0 < nc; c0 += 128) pt.push_back(make_int4(i, 1, c0, 0));
+        for (int a0 = p1; a0 < nc; a0 += 64) {
+          for (int b0 = p1; b0 <= a0; b0 += 64) pu.push_back(make_int4(i, 0, a0, b0));
+          for (int b0 = 0; b0 < nc; b0 += 64) pu.push_back(make_int4(i, 1, a0, b0));
+        }
+      }
+      pco[(size_t)p + 1] = (int64_t)pc.size();
+      pto[(size_t)p + 1] = (int64_t)pt.size();
+      puo[(size_t)p + 1] = (int64_t)pu.size();
+    }
+    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8;
+    DBuf<int32_t> d9;
+    auto up = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
+    up(d1, wasm); up(d2, wt); up(d3, wc0); up(d4, wc1); up(d5, wsym); up(d6, pt); up(d7, pu); up(d8, tiles);
+    d9.reserve(pc.size(), s);
+    d9.upload(pc.data(), 0, pc.size(), s);
+    for (int i = 0; i < n; ++i) {
+      const SkelBigTask& H = huge[(size_t)(lo + i)];
+      HCK(cudaMemsetAsync(A.bvals + H.delta_off, 0, sizeof(double) * (size_t)H.nc * H.nc, s));
+    }
+    const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 2 * max_nb));
+    launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
+    HCK(launch_cpqr_cluster(dtk, n, max_nq, A, opt.eps, s));
+    launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
+    launch_skelbig_t(dtk, d2.p, (int)wt.size(), A, s);
+    launch_skelbig_congruence(dtk, d3.p, (int)wc0.size(), A, s);
+    launch_skelbig_congruence(dtk, d4.p, (int)wc1.size(), A, s);
+    launch_skelbig_symm(dtk, d5.p, (int)wsym.size(), A, dscale, s);
+    g_launches += 7;
+    for (int p = 0; p < npanel; ++p) {
+      const int p0 = p * kPanelB;
+      launch_panel_chol(inner, d9.p + pco[(size_t)p], (int)(pco[(size_t)p + 1] - pco[(size_t)p]), p0, AH, dmin, s);
+      launch_panel_trsm(inner, d6.p + pto[(size_t)p], (int)(pto[(size_t)p + 1] - pto[(size_t)p]), p0, AH, s);
+      launch_panel_update(inner, d7.p + puo[(size_t)p], (int)(puo[(size_t)p + 1] - puo[(size_t)p]), p0, AH, s);
+      g_launches += 3;
+    }
+    launch_schur_tiles(inner, d8.p, (int)tiles.size(), AH, s);
+    launch_big_finish(inner, n, AH, dmin, dscale, s);
+    launch_apply_rd(d_skv + lo, n, A, s);
+    g_launches += 3;
+    HCK(cudaGetLastError());
+    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8}) d->release(s);
+    d9.release(s);
   }
 
   // -------------------------------------------------------------------------
@@ -1053,6 +1202,7 @@ struct Factorizer {
     lists.release(s);
     status.release(s);
     kout.release(s);
+    iscratch.release(s);
     d_blk_dof_off.release(s);
     d_blk_n.release(s);
     d_blk_val_off.release(s);
