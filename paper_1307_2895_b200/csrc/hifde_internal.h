@@ -42,7 +42,7 @@ struct SkelBigTask {
   int64_t rec_off, delta_off, out_off;
   int32_t group, pad;
 };
-constexpr int kCL = 16;                        // CTAs per cluster in the large-group CPQR
+constexpr int kMaxG = 256;                     // most CTAs serving one large-group CPQR
 constexpr int kMaxBigNc = 4096;                // largest group handled by that path
 
 // Solve-sweep record (one per elimination cell / skeleton group with rd != {}).
@@ -98,8 +98,9 @@ void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaS
 
 void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                              size_t smem, cudaStream_t s);
-cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
-                                cudaStream_t s);
+int cpqr_coop_capacity(size_t smem);
+cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
+                             unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s);
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,
                          double* dscale, cudaStream_t s);
 void launch_skelbig_t(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);

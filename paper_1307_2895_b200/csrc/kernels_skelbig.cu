@@ -4,14 +4,15 @@
 // src/dense.py:239-264):
 //   skelbig_assemble_kernel  rows of A_cc (row-major) and Mq = A_qc
 //                            (column-major) into scratch; one CTA per row chunk.
-//   cpqr_cluster_kernel      column-pivoted QR of Mq with the rank cut, by a
-//                            thread-block cluster of kCL CTAs per group.
-//                            Columns are owned round-robin by the cluster's
-//                            CTAs and never moved (pivoting = a pivot list);
-//                            each step every CTA rebuilds the reflector from
-//                            the pivot column, updates and downdates its own
-//                            columns, and posts its best remaining norm; one
-//                            cluster barrier per step.  dlaqp2 semantics.
+//   cpqr_coop_kernel         column-pivoted QR of Mq with the rank cut, by
+//                            G co-resident CTAs per group (cooperative launch,
+//                            the batch's groups share all SMs).  Columns are
+//                            owned round-robin and never moved (pivoting = a
+//                            pivot list); each step every CTA rebuilds the
+//                            reflector from the pivot column, updates and
+//                            downdates its own columns, and posts its best
+//                            remaining norm; one group barrier per step.
+//                            dlaqp2 semantics.
 //   skelbig_sort_kernel      sk / rd ascending, output index lists, inner task.
 //   skelbig_t_kernel         T = R11^-1 R12 (one thread per rd column), written
 //                            row-permuted to ascending sk order in the record.
@@ -21,12 +22,10 @@
 // The inner elimination of rd against sk (Cholesky of B_rr, W, delta block
 // -W^T W) reuses the blocked large-cell kernels of kernels_big.cu.
 #include <cfloat>
-#include <cooperative_groups.h>
 #include <cstdint>
+#include <cuda/atomic>
 
 #include "hifde_internal.h"
-
-namespace cg = cooperative_groups;
 
 namespace hifde {
 
@@ -60,6 +59,19 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Barrier among the G co-resident CTAs of one group (cooperative launch):
+// a monotonic arrival counter, each CTA waits for G * round arrivals.
+__device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int G, unsigned int& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += G;
+    cuda::atomic_ref<unsigned int, cuda::thread_scope_device> a(*ctr);
+    a.fetch_add(1u, cuda::memory_order_release);
+    while (a.load(cuda::memory_order_acquire) < target) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
 // scratch layout of one large group (doubles)
 struct BigWs {
   double *Acc, *Mq, *Tp, *vn1, *vn2, *rdiag, *cand;
@@ -74,7 +86,7 @@ __device__ __forceinline__ BigWs big_ws(const SkelBigTask& t, const Arenas& A) {
   w.vn1 = w.Tp + (nc * nc / 4 + nc);
   w.vn2 = w.vn1 + nc;
   w.rdiag = w.vn2 + nc;
-  w.cand = w.rdiag + nc;  // 2 x kCL x (value, index)
+  w.cand = w.rdiag + nc;  // 2 x kMaxG x (value, index)
   w.piv = A.iscratch + t.iws_off;
   w.skl = w.piv + nc;
   w.sko = w.skl + nc;
@@ -154,19 +166,24 @@ __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask
 }
 
 // ---------------------------------------------------------------------------
-// Cluster CPQR.  grid = ntasks * kCL, cluster (kCL,1,1), 256 threads.
+// Multi-CTA CPQR.  Cooperative launch; CTAs [gstart[t], gstart[t+1]) serve
+// task t and synchronize through a per-task software barrier.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) cpqr_cluster_kernel(const SkelBigTask* __restrict__ tasks, Arenas A,
-                                                           double eps) {
+__global__ void __launch_bounds__(256) cpqr_coop_kernel(const SkelBigTask* __restrict__ tasks, int ntasks,
+                                                        const int* __restrict__ gstart,
+                                                        unsigned int* __restrict__ bar, Arenas A, double eps) {
   extern __shared__ __align__(16) double vsm[];  // reflector column (nq doubles)
   __shared__ double red[8];
   __shared__ double sh_best;
   __shared__ int sh_pvt;
   __shared__ unsigned char done[kMaxBigNc];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rb = (int)cluster.block_rank();
-  const int CL = (int)cluster.num_blocks();
-  const SkelBigTask t = tasks[blockIdx.x / CL];
+  int tix = 0;
+  while (tix + 1 < ntasks && (int)blockIdx.x >= gstart[tix + 1]) ++tix;
+  const int rb = (int)blockIdx.x - gstart[tix];
+  const int CL = gstart[tix + 1] - gstart[tix];
+  unsigned int* ctr = bar + tix;
+  unsigned int target = 0;
+  const SkelBigTask t = tasks[tix];
   const int nc = t.nc, nq = t.nq;
   const BigWs w = big_ws(t, A);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -216,7 +233,7 @@ __global__ void __launch_bounds__(256) cpqr_cluster_kernel(const SkelBigTask* __
     }
   };
   block_best(best, bidx, 0);
-  cluster.sync();
+  group_barrier(ctr, (unsigned)CL, target);
 
   const int kmax = nq < nc ? nq : nc;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
@@ -309,7 +326,7 @@ __global__ void __launch_bounds__(256) cpqr_cluster_kernel(const SkelBigTask* __
     __syncthreads();
     if (P % CL == rb && threadIdx.x == 0) done[P] = 1;
     block_best(best, bidx, slot ^ 1);
-    cluster.sync();
+    group_barrier(ctr, (unsigned)CL, target);
   }
   if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
 }
@@ -510,30 +527,29 @@ void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwo
   skelbig_assemble_kernel<<<nwork, 256, smem, s>>>(tasks, work, A);
 }
 
-cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
-                                cudaStream_t s) {
+int cpqr_coop_capacity(size_t smem) {
+  static int cap_cached = -1;
+  static size_t smem_cached = 0;
+  if (cap_cached >= 0 && smem_cached == smem) return cap_cached;
+  cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+  int per_sm = 0, dev = 0, nsm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, 256, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cap_cached = per_sm * nsm;
+  smem_cached = smem;
+  return cap_cached;
+}
+
+cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
+                             unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (size_t)max_nq;
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(cpqr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(cpqr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmemCapBytes);
-    once = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3((unsigned)(ntasks * kCL), 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, cpqr_cluster_kernel, tasks, A, eps);
+  size_t smem = sizeof(double) * (size_t)max_nq;
+  cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+  Arenas Ac = A;
+  void* args[] = {(void*)&tasks, (void*)&ntasks, (void*)&d_gstart, (void*)&d_bar, (void*)&Ac, (void*)&eps};
+  return cudaLaunchCooperativeKernel((const void*)cpqr_coop_kernel, dim3((unsigned)nblocks), dim3(256), args,
+                                     smem, s);
 }
 
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,

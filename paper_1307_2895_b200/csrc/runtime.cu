@@ -827,7 +827,7 @@ struct Factorizer {
       H.dofs_off = T.dofs_off;
       H.blk_off = T.blk_off;
       const size_t nc = (size_t)T.nc, nq = (size_t)T.nq;
-      H.ws_off = (int64_t)scratch.bump(nc * nc + nq * nc + (nc * nc / 4 + nc) + 3 * nc + 4 * kCL + 8, s);
+      H.ws_off = (int64_t)scratch.bump(nc * nc + nq * nc + (nc * nc / 4 + nc) + 3 * nc + 4 * kMaxG + 8, s);
       H.iws_off = (int64_t)iscratch.bump(4 * nc + 4, s);
       H.rec_off = T.rec_off;
       H.delta_off = T.delta_off;
@@ -1010,7 +1010,35 @@ struct Factorizer {
     }
     const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 2 * max_nb));
     launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
-    HCK(launch_cpqr_cluster(dtk, n, max_nq, A, opt.eps, s));
+    {
+      // split the co-resident CTA capacity over the batch's groups in
+      // proportion to their work (nq * nc), at most one CTA per column
+      const int cap = std::max(n, std::min(cpqr_coop_capacity(sizeof(double) * (size_t)max_nq), 148 * 8));
+      double tot = 0;
+      for (int i = 0; i < n; ++i) tot += (double)huge[(size_t)(lo + i)].nq * huge[(size_t)(lo + i)].nc;
+      std::vector<int> gs((size_t)n + 1, 0);
+      for (int i = 0; i < n; ++i) {
+        const SkelBigTask& H = huge[(size_t)(lo + i)];
+        int g = (int)((double)cap * ((double)H.nq * H.nc) / std::max(tot, 1.0));
+        g = std::max(1, std::min({g, H.nc, kMaxG}));
+        gs[(size_t)i + 1] = gs[(size_t)i] + g;
+      }
+      while (gs[(size_t)n] > cap) {  // rounding overshoot: trim the largest
+        int im = 0;
+        for (int i = 1; i < n; ++i)
+          if (gs[(size_t)i + 1] - gs[(size_t)i] > gs[(size_t)im + 1] - gs[(size_t)im]) im = i;
+        for (int i = im + 1; i <= n; ++i) gs[(size_t)i] -= 1;
+      }
+      DBuf<int> dgs;
+      DBuf<unsigned int> dbar;
+      dgs.reserve(gs.size(), s);
+      dgs.upload(gs.data(), 0, gs.size(), s);
+      dbar.reserve((size_t)n, s);
+      HCK(cudaMemsetAsync(dbar.p, 0, sizeof(unsigned int) * (size_t)n, s));
+      HCK(launch_cpqr_coop(dtk, n, dgs.p, gs[(size_t)n], dbar.p, max_nq, A, opt.eps, s));
+      dgs.release(s);
+      dbar.release(s);
+    }
     launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
     launch_skelbig_t(dtk, d2.p, (int)wt.size(), A, s);
     launch_skelbig_congruence(dtk, d3.p, (int)wc0.size(), A, s);
