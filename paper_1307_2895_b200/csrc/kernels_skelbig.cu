@@ -536,7 +536,7 @@ int cpqr_coop_capacity(size_t smem) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, 256, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cap_cached = per_sm * nsm;
+  cap_cached = (per_sm >= 1 ? 1 : 0) * nsm;  // one CTA per SM: always co-resident
   smem_cached = smem;
   return cap_cached;
 }
