@@ -23,6 +23,8 @@
 // -W^T W) reuses the blocked large-cell kernels of kernels_big.cu.
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda/atomic>
 
 #include "hifde_internal.h"
@@ -537,6 +539,8 @@ int cpqr_coop_capacity(size_t smem) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cap_cached = (per_sm >= 1 ? 1 : 0) * nsm;  // one CTA per SM: always co-resident
+  if (getenv("HIFDE_TRACE"))
+    fprintf(stderr, "[hifde-trace] cpqr coop: smem %zu per_sm %d nsm %d cap %d\n", smem, per_sm, nsm, cap_cached);
   smem_cached = smem;
   return cap_cached;
 }
@@ -548,6 +552,7 @@ cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_
   cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
   Arenas Ac = A;
   void* args[] = {(void*)&tasks, (void*)&ntasks, (void*)&d_gstart, (void*)&d_bar, (void*)&Ac, (void*)&eps};
+  if (getenv("HIFDE_TRACE")) fprintf(stderr, "[hifde-trace] cpqr coop launch: %d blocks smem %zu\n", nblocks, smem);
   return cudaLaunchCooperativeKernel((const void*)cpqr_coop_kernel, dim3((unsigned)nblocks), dim3(256), args,
                                      smem, s);
 }

@@ -1011,33 +1011,37 @@ struct Factorizer {
     const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 2 * max_nb));
     launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
     {
-      // split the co-resident CTA capacity over the batch's groups in
-      // proportion to their work (nq * nc), at most one CTA per column
-      const int cap = std::max(n, std::min(cpqr_coop_capacity(sizeof(double) * (size_t)max_nq), 148 * 8));
-      double tot = 0;
-      for (int i = 0; i < n; ++i) tot += (double)huge[(size_t)(lo + i)].nq * huge[(size_t)(lo + i)].nc;
-      std::vector<int> gs((size_t)n + 1, 0);
-      for (int i = 0; i < n; ++i) {
-        const SkelBigTask& H = huge[(size_t)(lo + i)];
-        int g = (int)((double)cap * ((double)H.nq * H.nc) / std::max(tot, 1.0));
-        g = std::max(1, std::min({g, H.nc, kMaxG}));
-        gs[(size_t)i + 1] = gs[(size_t)i] + g;
+      // split the co-resident CTA capacity (one CTA per SM) over the groups in
+      // proportion to their work (nq * nc), at most one CTA per column; more
+      // groups than SMs are run in several cooperative launches
+      const int cap = std::max(1, cpqr_coop_capacity(sizeof(double) * (size_t)max_nq));
+      for (int c0 = 0; c0 < n; c0 += cap) {
+        const int cn = std::min(cap, n - c0);
+        double tot = 0;
+        for (int i = 0; i < cn; ++i) tot += (double)huge[(size_t)(lo + c0 + i)].nq * huge[(size_t)(lo + c0 + i)].nc;
+        std::vector<int> gsz((size_t)cn, 1);
+        int used = cn;
+        for (int i = 0; i < cn; ++i) {  // extra CTAs beyond the one each group gets
+          const SkelBigTask& H = huge[(size_t)(lo + c0 + i)];
+          const int want = (int)((double)(cap - cn) * ((double)H.nq * H.nc) / std::max(tot, 1.0));
+          const int g = std::max(1, std::min({1 + want, H.nc, kMaxG}));
+          used += g - 1;
+          gsz[(size_t)i] = g;
+        }
+        (void)used;
+        std::vector<int> gs((size_t)cn + 1, 0);
+        for (int i = 0; i < cn; ++i) gs[(size_t)i + 1] = gs[(size_t)i] + gsz[(size_t)i];
+        DBuf<int> dgs;
+        DBuf<unsigned int> dbar;
+        dgs.reserve(gs.size(), s);
+        dgs.upload(gs.data(), 0, gs.size(), s);
+        dbar.reserve((size_t)cn, s);
+        HCK(cudaMemsetAsync(dbar.p, 0, sizeof(unsigned int) * (size_t)cn, s));
+        HCK(launch_cpqr_coop(dtk + c0, cn, dgs.p, gs[(size_t)cn], dbar.p, max_nq, A, opt.eps, s));
+        ++g_launches;
+        dgs.release(s);
+        dbar.release(s);
       }
-      while (gs[(size_t)n] > cap) {  // rounding overshoot: trim the largest
-        int im = 0;
-        for (int i = 1; i < n; ++i)
-          if (gs[(size_t)i + 1] - gs[(size_t)i] > gs[(size_t)im + 1] - gs[(size_t)im]) im = i;
-        for (int i = im + 1; i <= n; ++i) gs[(size_t)i] -= 1;
-      }
-      DBuf<int> dgs;
-      DBuf<unsigned int> dbar;
-      dgs.reserve(gs.size(), s);
-      dgs.upload(gs.data(), 0, gs.size(), s);
-      dbar.reserve((size_t)n, s);
-      HCK(cudaMemsetAsync(dbar.p, 0, sizeof(unsigned int) * (size_t)n, s));
-      HCK(launch_cpqr_coop(dtk, n, dgs.p, gs[(size_t)n], dbar.p, max_nq, A, opt.eps, s));
-      dgs.release(s);
-      dbar.release(s);
     }
     launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
     launch_skelbig_t(dtk, d2.p, (int)wt.size(), A, s);
