@@ -43,6 +43,7 @@ struct SkelBigTask {
   int32_t group, pad;
 };
 constexpr int kMaxG = 256;                     // most CTAs serving one large-group CPQR
+constexpr int kCL = 16;                        // CTAs per cluster (many-group batches)
 constexpr int kMaxBigNc = 4096;                // largest group handled by that path
 
 // Solve-sweep record (one per elimination cell / skeleton group with rd != {}).
@@ -99,6 +100,8 @@ void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaS
 void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                              size_t smem, cudaStream_t s);
 int cpqr_coop_capacity(size_t smem);
+cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
+                                cudaStream_t s);
 cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
                              unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s);
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,

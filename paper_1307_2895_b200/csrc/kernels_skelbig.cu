@@ -22,6 +22,7 @@
 // The inner elimination of rd against sk (Cholesky of B_rr, W, delta block
 // -W^T W) reuses the blocked large-cell kernels of kernels_big.cu.
 #include <cfloat>
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -171,20 +172,34 @@ __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask
 // Multi-CTA CPQR.  Cooperative launch; CTAs [gstart[t], gstart[t+1]) serve
 // task t and synchronize through a per-task software barrier.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) cpqr_coop_kernel(const SkelBigTask* __restrict__ tasks, int ntasks,
-                                                        const int* __restrict__ gstart,
-                                                        unsigned int* __restrict__ bar, Arenas A, double eps) {
+// kCluster: thread-block clusters of kCL CTAs (hardware cluster barrier),
+// otherwise a cooperative launch with a software barrier per group.
+template <bool kCluster>
+__global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restrict__ tasks, int ntasks,
+                                                      const int* __restrict__ gstart,
+                                                      unsigned int* __restrict__ bar, Arenas A, double eps) {
   extern __shared__ __align__(16) double vsm[];  // reflector column (nq doubles)
   __shared__ double red[8];
   __shared__ double sh_best;
   __shared__ int sh_pvt;
   __shared__ unsigned char done[kMaxBigNc];
-  int tix = 0;
-  while (tix + 1 < ntasks && (int)blockIdx.x >= gstart[tix + 1]) ++tix;
-  const int rb = (int)blockIdx.x - gstart[tix];
-  const int CL = gstart[tix + 1] - gstart[tix];
+  int tix = 0, rb = 0, CL = 1;
+  if (kCluster) {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    rb = (int)cl.block_rank();
+    CL = (int)cl.num_blocks();
+    tix = (int)blockIdx.x / CL;
+  } else {
+    while (tix + 1 < ntasks && (int)blockIdx.x >= gstart[tix + 1]) ++tix;
+    rb = (int)blockIdx.x - gstart[tix];
+    CL = gstart[tix + 1] - gstart[tix];
+  }
   unsigned int* ctr = bar + tix;
   unsigned int target = 0;
+  auto gsync = [&]() {
+    if (kCluster) cooperative_groups::this_cluster().sync();
+    else group_barrier(ctr, (unsigned)CL, target);
+  };
   const SkelBigTask t = tasks[tix];
   const int nc = t.nc, nq = t.nq;
   const BigWs w = big_ws(t, A);
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(256) cpqr_coop_kernel(const SkelBigTask* __res
     }
   };
   block_best(best, bidx, 0);
-  group_barrier(ctr, (unsigned)CL, target);
+  gsync();
 
   const int kmax = nq < nc ? nq : nc;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);
@@ -328,7 +343,7 @@ __global__ void __launch_bounds__(256) cpqr_coop_kernel(const SkelBigTask* __res
     __syncthreads();
     if (P % CL == rb && threadIdx.x == 0) done[P] = 1;
     block_best(best, bidx, slot ^ 1);
-    group_barrier(ctr, (unsigned)CL, target);
+    gsync();
   }
   if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
 }
@@ -533,14 +548,12 @@ int cpqr_coop_capacity(size_t smem) {
   static int cap_cached = -1;
   static size_t smem_cached = 0;
   if (cap_cached >= 0 && smem_cached == smem) return cap_cached;
-  cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+  cudaFuncSetAttribute(cpqr_mc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
   int per_sm = 0, dev = 0, nsm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_coop_kernel, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_mc_kernel<false>, 256, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cap_cached = (per_sm >= 1 ? 1 : 0) * nsm;  // one CTA per SM: always co-resident
-  if (getenv("HIFDE_TRACE"))
-    fprintf(stderr, "[hifde-trace] cpqr coop: smem %zu per_sm %d nsm %d cap %d\n", smem, per_sm, nsm, cap_cached);
   smem_cached = smem;
   return cap_cached;
 }
@@ -549,12 +562,38 @@ cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_
                              unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = sizeof(double) * (size_t)max_nq;
-  cudaFuncSetAttribute(cpqr_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+  cudaFuncSetAttribute(cpqr_mc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
   Arenas Ac = A;
   void* args[] = {(void*)&tasks, (void*)&ntasks, (void*)&d_gstart, (void*)&d_bar, (void*)&Ac, (void*)&eps};
-  if (getenv("HIFDE_TRACE")) fprintf(stderr, "[hifde-trace] cpqr coop launch: %d blocks smem %zu\n", nblocks, smem);
-  return cudaLaunchCooperativeKernel((const void*)cpqr_coop_kernel, dim3((unsigned)nblocks), dim3(256), args,
+  return cudaLaunchCooperativeKernel((const void*)cpqr_mc_kernel<false>, dim3((unsigned)nblocks), dim3(256), args,
                                      smem, s);
+}
+
+cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
+                                cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * (size_t)max_nq;
+  static bool once = false;
+  if (!once) {
+    cudaFuncSetAttribute(cpqr_mc_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(cpqr_mc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+    once = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(ntasks * kCL), 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int* gnull = nullptr;
+  unsigned int* bnull = nullptr;
+  return cudaLaunchKernelEx(&cfg, cpqr_mc_kernel<true>, tasks, ntasks, gnull, bnull, A, eps);
 }
 
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,

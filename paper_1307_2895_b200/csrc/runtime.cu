@@ -1010,8 +1010,12 @@ struct Factorizer {
     }
     const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 2 * max_nb));
     launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
-    {
-      // split the co-resident CTA capacity (one CTA per SM) over the groups in
+    if (n > 8) {
+      // many groups: 16-CTA clusters per group, scheduled in waves
+      HCK(launch_cpqr_cluster(dtk, n, max_nq, A, opt.eps, s));
+      ++g_launches;
+    } else {
+      // few groups (exact-order batches): all SMs, split over the groups in
       // proportion to their work (nq * nc), at most one CTA per column; more
       // groups than SMs are run in several cooperative launches
       const int cap = std::max(1, cpqr_coop_capacity(sizeof(double) * (size_t)max_nq));
