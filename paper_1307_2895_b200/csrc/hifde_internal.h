@@ -106,7 +106,12 @@ cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_
                              unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s);
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,
                          double* dscale, cudaStream_t s);
-void launch_skelbig_t(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
+void launch_skelbig_tinit(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
+void launch_skelbig_tsolve(const SkelBigTask* tasks, const int4* work, int nwork, int b0, const Arenas& A,
+                           cudaStream_t s);
+void launch_skelbig_tupdate(const SkelBigTask* tasks, const int4* work, int nwork, int b0, const Arenas& A,
+                            cudaStream_t s);
+void launch_skelbig_tperm(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
 void launch_skelbig_congruence(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                                cudaStream_t s);
 void launch_skelbig_symm(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, double* dscale,

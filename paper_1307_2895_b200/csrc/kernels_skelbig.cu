@@ -14,7 +14,8 @@
 //                            remaining norm; one group barrier per step.
 //                            dlaqp2 semantics.
 //   skelbig_sort_kernel      sk / rd ascending, output index lists, inner task.
-//   skelbig_t_kernel         T = R11^-1 R12 (one thread per rd column), written
+//   skelbig_t*_kernel        T = R11^-1 R12, blocked back substitution (64-row
+//                            diagonal solves + DMMA updates), then written
 //                            row-permuted to ascending sk order in the record.
 //   skelbig_bsr_kernel       B_sr = A_sr - A_ss T   (DMMA), stored as W^T input.
 //   skelbig_brr_kernel       B_rr = A_rr - A_sr^T T - T^T B_sr (DMMA).
@@ -258,16 +259,31 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
   int k = kmax;
   for (int i = 0; i < kmax; ++i) {
     const int slot = i & 1;
-    if (threadIdx.x == 0) {
+    {
+      // all candidates read in parallel, block argmax (lowest index on ties)
       double bv = -1.0;
       int bi = nc;
-      for (int q = 0; q < CL; ++q) {
+      for (int q = threadIdx.x; q < CL; q += 256) {
         const double v = __ldcg(&w.cand[(size_t)(slot * CL + q) * 2]);
         const int ix = (int)__ldcg(&w.cand[(size_t)(slot * CL + q) * 2 + 1]);
         if (v > bv || (v == bv && ix < bi)) { bv = v; bi = ix; }
       }
-      sh_best = bv;
-      sh_pvt = bi;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { wbest[wid] = bv; widx[wid] = bi; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double b2 = wbest[0];
+        int i2 = widx[0];
+        for (int q = 1; q < 8; ++q)
+          if (wbest[q] > b2 || (wbest[q] == b2 && widx[q] < i2)) { b2 = wbest[q]; i2 = widx[q]; }
+        sh_best = b2;
+        sh_pvt = i2;
+      }
     }
     __syncthreads();
     const int P = sh_pvt;
@@ -401,26 +417,122 @@ __global__ void __launch_bounds__(256) skelbig_sort_kernel(const SkelBigTask* __
   }
 }
 
-// T = R11^-1 R12, one thread per rd column; stored to the record with rows in
-// ascending sk order.  grid: int4 {task, col0, 0, 0}.
-__global__ void __launch_bounds__(128) skelbig_t_kernel(const SkelBigTask* __restrict__ tasks,
-                                                        const int4* __restrict__ work, Arenas A) {
+// ---------------------------------------------------------------------------
+// T = R11^-1 R12 by blocked back substitution over 64-row blocks (bottom-up):
+//   skelbig_tinit_kernel    Tp = R12                (work {task, row0})
+//   skelbig_tsolve_kernel   diagonal block solve    (work {task, col0}, block b0)
+//   skelbig_tupdate_kernel  rows above -= R11 Tp    (work {task, a0, c0}, block b0)
+//   skelbig_tperm_kernel    record T = Tp rows in ascending sk order
+// R11[a][l] = Mq[a + piv[l] nq], R12[a][c] = Mq[a + rd_c nq] (pivot order).
+// Block loops run on the size bound; the kernels skip rows >= k.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) skelbig_tinit_kernel(const SkelBigTask* __restrict__ tasks,
+                                                            const int4* __restrict__ work, Arenas A) {
   const int4 wk = work[blockIdx.x];
   const SkelBigTask t = tasks[wk.x];
-  const int nc = t.nc, nq = t.nq;
   const BigWs w = big_ws(t, A);
-  const int k = A.kout[t.group], r = nc - k;
-  const int b = wk.y + (int)threadIdx.x;
-  if (b >= r) return;
-  const double* R = w.Mq;  // R[a][col] = Mq[a + col*nq]
-  const int cb = w.rdl[b];
-  for (int a = k - 1; a >= 0; --a) {
-    double s = R[a + (size_t)cb * nq];
-    for (int l = a + 1; l < k; ++l) s -= R[a + (size_t)w.piv[l] * nq] * w.Tp[(size_t)l * r + b];
-    w.Tp[(size_t)a * r + b] = s / w.rdiag[a];
+  const int k = A.kout[t.group], r = t.nc - k;
+  for (int a = wk.y; a < min(wk.y + 64, k); ++a)
+    for (int c = threadIdx.x; c < r; c += 256) w.Tp[(size_t)a * r + c] = w.Mq[a + (size_t)w.rdl[c] * t.nq];
+}
+
+__global__ void __launch_bounds__(128) skelbig_tsolve_kernel(const SkelBigTask* __restrict__ tasks,
+                                                             const int4* __restrict__ work, int b0, Arenas A) {
+  __shared__ double R[64][65];
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const BigWs w = big_ws(t, A);
+  const int k = A.kout[t.group], r = t.nc - k;
+  if (b0 >= k || wk.y >= r) return;
+  const int b1 = min(b0 + 64, k), bw = b1 - b0;
+  for (int e = threadIdx.x; e < bw * bw; e += 128) {
+    const int i = e / bw, j = e - i * bw;
+    R[i][j] = (j > i) ? w.Mq[(size_t)(b0 + i) + (size_t)w.piv[b0 + j] * t.nq] : 0.0;
   }
+  __syncthreads();
+  const int c = wk.y + (int)threadIdx.x;
+  if (c >= r) return;
+  double x[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) x[i] = 0.0;
+  for (int i = bw - 1; i >= 0; --i) {
+    double v = w.Tp[(size_t)(b0 + i) * r + c];
+#pragma unroll 8
+    for (int j = i + 1; j < 64; ++j)
+      if (j < bw) v -= R[i][j] * x[j];
+    // x[i] with a dynamic index would spill; select by unrolled compare
+    const double xi = v / w.rdiag[b0 + i];
+#pragma unroll
+    for (int q = 0; q < 64; ++q)
+      if (q == i) x[q] = xi;
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < bw) w.Tp[(size_t)(b0 + i) * r + c] = x[i];
+}
+
+constexpr int kTT = 64, kTK = 16, kTL = 68;
+__global__ void __launch_bounds__(128) skelbig_tupdate_kernel(const SkelBigTask* __restrict__ tasks,
+                                                              const int4* __restrict__ work, int b0, Arenas A) {
+  __shared__ double As[kTK][kTL];
+  __shared__ double Bs[kTK][kTL];
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const BigWs w = big_ws(t, A);
+  const int k = A.kout[t.group], r = t.nc - k;
+  const int a0 = wk.y, c0 = wk.z;
+  if (b0 >= k || a0 >= b0 || c0 >= r) return;
+  const int b1 = min(b0 + 64, k), bw = b1 - b0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wy = wid >> 1, wx = wid & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  for (int l0 = 0; l0 < bw; l0 += kTK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTK * kTT; e += 128) {
+      const int ll = e / kTT, x = e - ll * kTT;
+      const int l = b0 + l0 + ll;
+      As[ll][x] = (l < b1 && a0 + x < b0) ? w.Mq[(size_t)(a0 + x) + (size_t)w.piv[l] * t.nq] : 0.0;
+      Bs[ll][x] = (l < b1 && c0 + x < r) ? w.Tp[(size_t)l * r + c0 + x] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kTK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = As[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bf[n] = Bs[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = a0 + wy * 32 + m * 8 + (lane >> 2);
+        const int c = c0 + wx * 32 + n * 8 + 2 * (lane & 3) + h;
+        if (a < b0 && c < r) w.Tp[(size_t)a * r + c] -= acc[m][n][h];
+      }
+}
+
+__global__ void __launch_bounds__(256) skelbig_tperm_kernel(const SkelBigTask* __restrict__ tasks,
+                                                            const int4* __restrict__ work, Arenas A) {
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const BigWs w = big_ws(t, A);
+  const int k = A.kout[t.group], r = t.nc - k;
   double* T = A.fac + t.rec_off;
-  for (int a = 0; a < k; ++a) T[(size_t)a * r + b] = w.Tp[(size_t)w.sko[a] * r + b];
+  for (int a = wk.y; a < min(wk.y + 64, k); ++a)
+    for (int c = threadIdx.x; c < r; c += 256) T[(size_t)a * r + c] = w.Tp[(size_t)w.sko[a] * r + c];
 }
 
 // ---------------------------------------------------------------------------
@@ -602,9 +714,19 @@ void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, 
   skelbig_sort_kernel<<<ntasks, 256, 0, s>>>(tasks, A, inner, dmin, dscale);
 }
 
-void launch_skelbig_t(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
-  if (nwork <= 0) return;
-  skelbig_t_kernel<<<nwork, 128, 0, s>>>(tasks, work, A);
+void launch_skelbig_tinit(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
+  if (nwork > 0) skelbig_tinit_kernel<<<nwork, 256, 0, s>>>(tasks, work, A);
+}
+void launch_skelbig_tsolve(const SkelBigTask* tasks, const int4* work, int nwork, int b0, const Arenas& A,
+                           cudaStream_t s) {
+  if (nwork > 0) skelbig_tsolve_kernel<<<nwork, 128, 0, s>>>(tasks, work, b0, A);
+}
+void launch_skelbig_tupdate(const SkelBigTask* tasks, const int4* work, int nwork, int b0, const Arenas& A,
+                            cudaStream_t s) {
+  if (nwork > 0) skelbig_tupdate_kernel<<<nwork, 128, 0, s>>>(tasks, work, b0, A);
+}
+void launch_skelbig_tperm(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
+  if (nwork > 0) skelbig_tperm_kernel<<<nwork, 256, 0, s>>>(tasks, work, A);
 }
 
 void launch_skelbig_congruence(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,

@@ -957,7 +957,7 @@ struct Factorizer {
     double* dscale = d_scale_all + lo;
     Arenas AH = AH_all;
     AH.status = AH_all.status + lo;
-    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles;
+    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles, wrow, wtu;
     std::vector<int32_t> pc;
     int maxnc = 0;
     for (int i = 0; i < n; ++i) maxnc = std::max(maxnc, huge[(size_t)(lo + i)].nc);
@@ -968,6 +968,7 @@ struct Factorizer {
       const int nc = H.nc, nf = H.nc + H.nq;
       for (int r0 = 0; r0 < nf; r0 += 64) wasm.push_back(make_int4(i, r0, std::min(r0 + 64, nf), 0));
       for (int c0 = 0; c0 < nc; c0 += 128) wt.push_back(make_int4(i, c0, 0, 0));
+      for (int r0 = 0; r0 < nc; r0 += 64) wrow.push_back(make_int4(i, r0, 0, 0));
       for (int a0 = 0; a0 < nc; a0 += 64)
         for (int b0 = 0; b0 < nc; b0 += 64) {
           wc0.push_back(make_int4(i, 0, a0, b0));
@@ -998,10 +999,24 @@ struct Factorizer {
       pto[(size_t)p + 1] = (int64_t)pt.size();
       puo[(size_t)p + 1] = (int64_t)pu.size();
     }
-    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8;
+    // T update tiles per 64-row block b (rows above b0, all rd columns)
+    const int ntb = (maxnc + 63) / 64;
+    std::vector<int64_t> tuo((size_t)ntb + 1, 0);
+    for (int bb = 0; bb < ntb; ++bb) {
+      const int b0 = bb * 64;
+      for (int i = 0; i < n; ++i) {
+        const int nc = huge[(size_t)(lo + i)].nc;
+        if (b0 >= nc) continue;
+        for (int a0 = 0; a0 < b0; a0 += 64)
+          for (int c0 = 0; c0 < nc; c0 += 64) wtu.push_back(make_int4(i, a0, c0, 0));
+      }
+      tuo[(size_t)bb + 1] = (int64_t)wtu.size();
+    }
+    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8, d10, d11;
     DBuf<int32_t> d9;
     auto up = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
     up(d1, wasm); up(d2, wt); up(d3, wc0); up(d4, wc1); up(d5, wsym); up(d6, pt); up(d7, pu); up(d8, tiles);
+    up(d10, wrow); up(d11, wtu);
     d9.reserve(pc.size(), s);
     d9.upload(pc.data(), 0, pc.size(), s);
     for (int i = 0; i < n; ++i) {
@@ -1048,7 +1063,13 @@ struct Factorizer {
       }
     }
     launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
-    launch_skelbig_t(dtk, d2.p, (int)wt.size(), A, s);
+    launch_skelbig_tinit(dtk, d10.p, (int)wrow.size(), A, s);
+    for (int bb = ntb - 1; bb >= 0; --bb) {
+      launch_skelbig_tsolve(dtk, d2.p, (int)wt.size(), bb * 64, A, s);
+      launch_skelbig_tupdate(dtk, d11.p + tuo[(size_t)bb], (int)(tuo[(size_t)bb + 1] - tuo[(size_t)bb]), bb * 64, A, s);
+      g_launches += 2;
+    }
+    launch_skelbig_tperm(dtk, d10.p, (int)wrow.size(), A, s);
     launch_skelbig_congruence(dtk, d3.p, (int)wc0.size(), A, s);
     launch_skelbig_congruence(dtk, d4.p, (int)wc1.size(), A, s);
     launch_skelbig_symm(dtk, d5.p, (int)wsym.size(), A, dscale, s);
@@ -1065,7 +1086,7 @@ struct Factorizer {
     launch_apply_rd(d_skv + lo, n, A, s);
     g_launches += 3;
     HCK(cudaGetLastError());
-    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8}) d->release(s);
+    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(s);
     d9.release(s);
   }
 
