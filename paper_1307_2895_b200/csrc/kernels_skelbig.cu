@@ -63,6 +63,32 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Warp-strided dot product / axpy over rows [r0, n) with 8 independent loads
+// in flight per lane (the columns live in L2/HBM).
+__device__ __forceinline__ double wdot(const double* __restrict__ a, const double* __restrict__ b, int r0, int n,
+                                       int lane) {
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int r = r0 + lane;
+  for (; r + 7 * 32 < n; r += 8 * 32) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] += a[r + 32 * u] * b[r + 32 * u];
+  }
+  for (; r < n; r += 32) s[0] += a[r] * b[r];
+  return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+}
+__device__ __forceinline__ void waxpy(double* __restrict__ y, const double* __restrict__ x, double alpha, int r0,
+                                      int n, int lane) {
+  int r = r0 + lane;
+  for (; r + 7 * 32 < n; r += 8 * 32) {
+    double yv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) yv[u] = y[r + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) y[r + 32 * u] = yv[u] - alpha * x[r + 32 * u];
+  }
+  for (; r < n; r += 32) y[r] -= alpha * x[r];
+}
+
 // Barrier among the G co-resident CTAs of one group (cooperative launch):
 // a monotonic arrival counter, each CTA waits for G * round arrivals.
 __device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int G, unsigned int& target) {
@@ -223,8 +249,7 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
   int bidx = nc;
   for (int j = rb + CL * wid; j < nc; j += CL * 8) {
     const double* col = w.Mq + (size_t)j * ldq;
-    double s = 0.0;
-    for (int r = lane; r < nq; r += 32) s += col[r] * col[r];
+    double s = wdot(col, col, 0, nq, lane);
     s = sqrt(warp_sum(s));
     if (lane == 0) { w.vn1[j] = s; w.vn2[j] = s; }
     if (s > best || (s == best && j < bidx)) { best = s; bidx = j; }
@@ -326,14 +351,12 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
       if (done[j] || j == P) continue;
       double* col = w.Mq + (size_t)j * ldq;
       if (tau != 0.0) {
-        double s = 0.0;
-        for (int r = i + 1 + lane; r < nq; r += 32) s += vsm[r] * col[r];
+        double s = wdot(vsm, col, i + 1, nq, lane);
         s = warp_sum(s);
         const double wv = tau * (col[i] + scal * s);
         __syncwarp();
         if (lane == 0) col[i] -= wv;
-        const double ws2 = wv * scal;
-        for (int r = i + 1 + lane; r < nq; r += 32) col[r] -= ws2 * vsm[r];
+        waxpy(col, vsm, wv * scal, i + 1, nq, lane);
         __syncwarp();
       }
       double nv = w.vn1[j];
@@ -347,8 +370,7 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
         else nv *= sqrt(tmp);
       }
       if (recompute) {
-        double s = 0.0;
-        for (int r = i + 1 + lane; r < nq; r += 32) s += col[r] * col[r];
+        double s = wdot(col, col, i + 1, nq, lane);
         s = warp_sum(s);
         nv = (i + 1 < nq) ? sqrt(s) : 0.0;
         if (lane == 0) w.vn2[j] = nv;
