@@ -53,6 +53,8 @@ struct SolveRec {
   int64_t idx_off;          // idx arena: cell then nbrs / rd then sk
   int64_t C_off, W_off, T_off;  // factor arena
   int64_t contrib_off;      // elimination: row offset in the contribution buffer
+  int32_t inv;              // 1: C slot holds the packed lower inverse C^-1; 0: C itself
+  int32_t pad;
 };
 
 // Device views of the persistent arenas.

@@ -138,6 +138,21 @@ __device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, in
   __syncthreads();
 }
 
+// Packed row-major lower inverse of the lower-triangular C (n x n, ld),
+// written to P[i(i+1)/2 + j]; one thread per column, no barriers (each
+// thread reads back only its own column).
+template <int NT>
+__device__ void tri_inverse_packed(const double* C, int n, int ld, double* __restrict__ P) {
+  for (int j = threadIdx.x; j < n; j += NT) {
+    P[(size_t)j * (j + 1) / 2 + j] = 1.0 / C[(size_t)j * ld + j];
+    for (int i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int l = j; l < i; ++l) s += C[(size_t)i * ld + l] * P[(size_t)l * (l + 1) / 2 + j];
+      P[(size_t)i * (i + 1) / 2 + j] = -s / C[(size_t)i * ld + i];
+    }
+  }
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -212,11 +227,8 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
       W[e] = F[i * nf + nc + j];
     }
   }
-  double* C = A.fac + t.C_off;
-  for (int e = threadIdx.x; e < nc * nc; e += NT) {
-    const int i = e / nc, j = e - i * nc;
-    C[e] = (j <= i) ? F[i * nf + j] : 0.0;
-  }
+  // the solve applies C^-1 as a product: store it packed (lower, row-major)
+  tri_inverse_packed<NT>(F, nc, nf, A.fac + t.C_off);
   if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
 }
 
@@ -577,10 +589,7 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   double* rec = A.fac + t.rec_off;
   for (int e = threadIdx.x; e < k * r; e += NT) rec[e] = Ts[e];
   double* C = rec + (size_t)k * r;
-  for (int e = threadIdx.x; e < r * r; e += NT) {
-    const int a = e / r, b = e - a * r;
-    C[e] = (b <= a) ? Brr[e] : 0.0;
-  }
+  tri_inverse_packed<NT>(Brr, r, r, C);  // packed C^-1 for the solve
   double* Wo = C + (size_t)r * r;
   for (int e = threadIdx.x; e < r * k; e += NT) Wo[e] = Wm[e];
   if (threadIdx.x == 0) A.status[t.group] = 0;

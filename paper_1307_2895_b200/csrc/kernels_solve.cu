@@ -62,6 +62,25 @@ __device__ void bwd_subst(const double* __restrict__ C, int n, double* x, int nr
   __syncthreads();
 }
 
+// y = P x and y = P^T x for the packed lower inverse P (n x n) and x n x nrhs.
+__device__ void pinv_apply(const double* __restrict__ P, int n, const double* x, double* y, int nrhs) {
+  for (int e = threadIdx.x; e < n * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    const double* row = P + (size_t)i * (i + 1) / 2;
+    double s = 0.0;
+    for (int l = 0; l <= i; ++l) s += row[l] * x[(size_t)l * nrhs + r];
+    y[e] = s;
+  }
+}
+__device__ void pinv_apply_t(const double* __restrict__ P, int n, const double* x, double* y, int nrhs) {
+  for (int e = threadIdx.x; e < n * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    double s = 0.0;
+    for (int l = i; l < n; ++l) s += P[(size_t)l * (l + 1) / 2 + i] * x[(size_t)l * nrhs + r];
+    y[e] = s;
+  }
+}
+
 __device__ __forceinline__ double* workspace(double* smem, double* scratch, int64_t per_rec) {
   return per_rec > 0 ? scratch + (size_t)blockIdx.x * per_rec : smem;
 }
@@ -75,12 +94,20 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
   const SolveRec rc = recs[blockIdx.x];
   const int nc = rc.nc, nq = rc.nq;
   double* s = workspace(sm, scratch, per_rec);
+  double* s2 = s + (size_t)nc * nrhs;
   const int32_t* c = idx + rc.idx_off;
   for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
     const int i = e / nrhs, r = e - i * nrhs;
     s[e] = v[(size_t)c[i] * nrhs + r];
   }
-  fwd_subst(fac + rc.C_off, nc, s, nrhs);
+  if (rc.inv) {
+    __syncthreads();
+    pinv_apply(fac + rc.C_off, nc, s, s2, nrhs);
+    __syncthreads();
+    s = s2;
+  } else {
+    fwd_subst(fac + rc.C_off, nc, s, nrhs);
+  }
   for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
     const int i = e / nrhs, r = e - i * nrhs;
     v[(size_t)c[i] * nrhs + r] = s[e];
@@ -124,7 +151,15 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
     for (int b = 0; b < nq; ++b) a -= W[(size_t)i * nq + b] * v[(size_t)q[b] * nrhs + r];
     t[e] = a;
   }
-  bwd_subst(fac + rc.C_off, nc, t, nrhs);
+  if (rc.inv) {
+    double* t2 = t + (size_t)nc * nrhs;
+    __syncthreads();
+    pinv_apply_t(fac + rc.C_off, nc, t, t2, nrhs);
+    __syncthreads();
+    t = t2;
+  } else {
+    bwd_subst(fac + rc.C_off, nc, t, nrhs);
+  }
   for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
     const int i = e / nrhs, r = e - i * nrhs;
     v[(size_t)c[i] * nrhs + r] = t[e];
@@ -142,6 +177,7 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
   const int r = rc.nc, k = rc.nq;
   double* xs = workspace(sm, scratch, per_rec);
   double* xr = xs + (size_t)k * nrhs;
+  double* x2 = xr + (size_t)r * nrhs;
   const int32_t* sk = idx + rc.idx_off;
   const int32_t* rd = sk + k;
   const double* T = fac + rc.T_off;
@@ -163,7 +199,15 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
       for (int l = 0; l < k; ++l) a -= T[(size_t)l * r + b] * xs[(size_t)l * nrhs + j];
       xr[e] = a;
     }
-    fwd_subst(C, r, xr, nrhs);
+    if (rc.inv) {
+      __syncthreads();
+      pinv_apply(C, r, xr, x2, nrhs);
+      __syncthreads();
+      for (int e = threadIdx.x; e < r * nrhs; e += NT) xr[e] = x2[e];
+      __syncthreads();
+    } else {
+      fwd_subst(C, r, xr, nrhs);
+    }
     for (int e = threadIdx.x; e < k * nrhs; e += NT) {
       const int a = e / nrhs, j = e - a * nrhs;
       double x = xs[e];
@@ -177,7 +221,15 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
       for (int l = 0; l < k; ++l) a -= W[(size_t)b * k + l] * xs[(size_t)l * nrhs + j];
       xr[e] = a;
     }
-    bwd_subst(C, r, xr, nrhs);
+    if (rc.inv) {
+      __syncthreads();
+      pinv_apply_t(C, r, xr, x2, nrhs);
+      __syncthreads();
+      for (int e = threadIdx.x; e < r * nrhs; e += NT) xr[e] = x2[e];
+      __syncthreads();
+    } else {
+      bwd_subst(C, r, xr, nrhs);
+    }
     for (int e = threadIdx.x; e < k * nrhs; e += NT) {
       const int a = e / nrhs, j = e - a * nrhs;
       double x = xs[e];

@@ -530,6 +530,8 @@ struct Factorizer {
       R.W_off = T.W_off;
       R.T_off = 0;
       R.contrib_off = L.ncontrib;
+      R.inv = is_big[(size_t)t] ? 0 : 1;
+      R.pad = 0;
       L.ncontrib += nq;
       L.recs.push_back(R);
       L.max_nc = std::max(L.max_nc, nc);
@@ -931,6 +933,8 @@ struct Factorizer {
         R.C_off = T.rec_off + (int64_t)kk * r;
         R.W_off = R.C_off + (int64_t)r * r;
         R.contrib_off = 0;
+        R.inv = T.mode == 2 ? 0 : 1;
+        R.pad = 0;
         L.recs.push_back(R);
         L.max_nc = std::max(L.max_nc, r);
         L.max_nq = std::max(L.max_nq, kk);
@@ -1304,8 +1308,8 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   };
   for (const auto& L : F->levels) {
     size_t sm; int64_t pr;
-    if (L.kind == 1) ws_plan(L, (int64_t)(L.max_nc + L.max_nq) * nrhs, sm, pr);
-    else ws_plan(L, (int64_t)L.max_nc * nrhs, sm, pr);
+    if (L.kind == 1) ws_plan(L, (int64_t)(2 * L.max_nc + L.max_nq) * nrhs, sm, pr);
+    else ws_plan(L, (int64_t)2 * L.max_nc * nrhs, sm, pr);
   }
   double* scratch = nullptr;
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
@@ -1318,11 +1322,11 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     if (!nr) continue;
     size_t sm; int64_t pr;
     if (L.kind == 1) {
-      ws_plan(L, (int64_t)(L.max_nc + L.max_nq) * nrhs, sm, pr);
+      ws_plan(L, (int64_t)(2 * L.max_nc + L.max_nq) * nrhs, sm, pr);
       launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s);
       ++g_launches;
     } else {
-      ws_plan(L, (int64_t)L.max_nc * nrhs, sm, pr);
+      ws_plan(L, (int64_t)2 * L.max_nc * nrhs, sm, pr);
       launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s);
       ++g_launches;
       if (L.kind == 0) {
@@ -1337,10 +1341,10 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     if (!nr) continue;
     size_t sm; int64_t pr;
     if (L.kind == 1) {
-      ws_plan(L, (int64_t)(L.max_nc + L.max_nq) * nrhs, sm, pr);
+      ws_plan(L, (int64_t)(2 * L.max_nc + L.max_nq) * nrhs, sm, pr);
       launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s);
     } else {
-      ws_plan(L, (int64_t)L.max_nc * nrhs, sm, pr);
+      ws_plan(L, (int64_t)2 * L.max_nc * nrhs, sm, pr);
       launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s);
     }
     ++g_launches;

@@ -46,6 +46,8 @@ CASES = [
 BIG_CASES = [
     ("cfg2", 2, 512, 8, 1e-9, "hifde", "gauss", 0, 16, False),
     ("cfg4", 3, 64, 4, 1e-6, "hifde3x", "const", 0, 16, False),
+    ("cfg3", 2, 2048, 8, 1e-6, "hifde", "const", 0, 4, False),
+    ("cfg5", 3, 128, 4, 1e-3, "hifde3x", "gauss", 0, 4, False),
 ]
 
 
