@@ -16,6 +16,7 @@ struct ElimTask {
   int64_t C_off;            // factor arena: Cholesky factor, nc x nc row-major
   int64_t W_off;            // factor arena: W = C^-1 A_cq, nc x nq row-major
   int64_t U_off;            // block arena: new clique block, nq x nq row-major
+  int64_t P_off;            // factor arena: packed lower C^-1 (what the solve applies)
 };
 
 // Per-group work item of a skeletonization level (src/factor_ops.py:162-214).
@@ -45,6 +46,20 @@ struct SkelBigTask {
 constexpr int kMaxG = 256;                     // most CTAs serving one large-group CPQR
 constexpr int kCL = 16;                        // CTAs per cluster (many-group batches)
 constexpr int kMaxBigNc = 4096;                // largest group handled by that path
+
+// One tiled product of the solve for large records (kernels_solve.cu):
+//   dst(i, :) = src(i, :) + alpha * sum_k A(i, k) X(k, :),  i < M, k < K
+// A: amode 0 packed lower P, 1 its transpose, 2 dense row-major (lda), 3 dense
+// transposed.  X / src / dst rows: mode 0 = rows of v gathered through the
+// index list at *_off, 1 = solve scratch rows from *_off, 2 = contribution rows
+// from *_off; smode -1 = no src.
+struct TileOp {
+  int32_t M, K;
+  int32_t amode, xmode, smode, dmode;
+  int64_t A_off, lda;
+  int64_t x_off, s_off, d_off;
+  double alpha;
+};
 
 // Solve-sweep record (one per elimination cell / skeleton group with rd != {}).
 struct SolveRec {
@@ -93,6 +108,7 @@ void launch_panel_update(const ElimTask* tasks, const int4* work, int nwork, int
                          cudaStream_t s);
 void launch_big_finish(const ElimTask* tasks, int ncells, const Arenas& A, const double* dmin,
                        const double* diag_scale, cudaStream_t s);
+void launch_big_inverse(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
 void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
                         cudaStream_t s);
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,
@@ -132,6 +148,8 @@ void launch_solve_elim_bwd(const SolveRec* recs, int nrec, const int32_t* idx, c
 void launch_solve_skel(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
                        double* v, int nrhs, int forward, double* scratch,
                        int64_t scratch_per_rec, size_t smem, cudaStream_t s);
+void launch_solve_tiles(const TileOp* ops, const int2* work, int nwork, const int32_t* idx, const double* fac,
+                        double* v, int nrhs, double* tscratch, double* contrib, cudaStream_t s);
 
 constexpr int kThreads = 256;
 

@@ -363,7 +363,37 @@ __global__ void __launch_bounds__(256) big_finish_kernel(const ElimTask* __restr
   }
 }
 
+// Packed lower inverse of C for the solve: one thread per column (work item
+// int4 {cell, col0}), C row-major in the record, P packed row-major.
+__global__ void __launch_bounds__(128) big_inverse_kernel(const ElimTask* __restrict__ tasks,
+                                                          const int4* __restrict__ work, Arenas A) {
+  const int4 w = work[blockIdx.x];
+  if (A.status[w.x] != 0) return;
+  const ElimTask t = tasks[w.x];
+  const int nc = t.nc;
+  const int j = w.y + (int)threadIdx.x;
+  if (j >= nc) return;
+  const double* C = A.fac + t.C_off;
+  double* P = A.fac + t.P_off;
+  P[(size_t)j * (j + 1) / 2 + j] = 1.0 / C[(size_t)j * nc + j];
+  for (int i = j + 1; i < nc; ++i) {
+    const double* ci = C + (size_t)i * nc;
+    double s0 = 0.0, s1 = 0.0;
+    int l = j;
+    for (; l + 1 < i; l += 2) {
+      s0 += ci[l] * P[(size_t)l * (l + 1) / 2 + j];
+      s1 += ci[l + 1] * P[(size_t)(l + 1) * (l + 2) / 2 + j];
+    }
+    if (l < i) s0 += ci[l] * P[(size_t)l * (l + 1) / 2 + j];
+    P[(size_t)i * (i + 1) / 2 + j] = -(s0 + s1) / ci[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
+void launch_big_inverse(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
+  if (nwork > 0) big_inverse_kernel<<<nwork, 128, 0, s>>>(tasks, work, A);
+}
+
 void launch_big_assemble(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A,
                          double* diag_scale, size_t smem, cudaStream_t s) {
   if (nwork <= 0) return;

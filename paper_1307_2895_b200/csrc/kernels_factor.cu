@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
     }
   }
   // the solve applies C^-1 as a product: store it packed (lower, row-major)
-  tri_inverse_packed<NT>(F, nc, nf, A.fac + t.C_off);
+  tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
   if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
 }
 

@@ -432,6 +432,8 @@ __global__ void __launch_bounds__(256) skelbig_sort_kernel(const SkelBigTask* __
     e.C_off = t.rec_off + (int64_t)k * r;
     e.W_off = e.C_off + (int64_t)r * r;
     e.U_off = t.delta_off;
+    // packed inverse after the largest T | C | W footprint of the record
+    e.P_off = t.rec_off + (int64_t)nc * nc + 2 * ((int64_t)nc * nc / 4 + nc);
     inner[blockIdx.x] = e;
     dmin[blockIdx.x] = DBL_MAX;
     dscale[blockIdx.x] = 0.0;

@@ -248,6 +248,88 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled products for large records (see TileOp): a CTA computes 64 rows x 32
+// right-hand sides, staging 32-wide K chunks of A and X in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kTM = 64, kTKc = 32, kRW = 32;
+
+__device__ __forceinline__ double* op_row(int mode, int64_t off, int k, const int32_t* __restrict__ idx, double* v,
+                                          double* ts, double* contrib, int nrhs) {
+  if (mode == 0) return v + (size_t)idx[off + k] * nrhs;
+  if (mode == 1) return ts + (size_t)(off + k) * nrhs;
+  return contrib + (size_t)(off + k) * nrhs;
+}
+
+__global__ void __launch_bounds__(256) solve_tile_kernel(const TileOp* __restrict__ ops,
+                                                         const int2* __restrict__ work,
+                                                         const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ fac, double* v, int nrhs,
+                                                         double* ts, double* contrib) {
+  __shared__ double As[kTM][kTKc + 1];
+  __shared__ double Xs[kTKc][kRW];
+  const int2 w = work[blockIdx.x];
+  const TileOp op = ops[w.x];
+  const int i0 = w.y, r0 = blockIdx.y * kRW;
+  if (r0 >= nrhs) return;
+  const int nr = min(kRW, nrhs - r0);
+  const int tr = threadIdx.x & 31, ti = threadIdx.x >> 5;
+  const double* Am = fac + op.A_off;
+  const bool trans = op.amode == 1 || op.amode == 3;
+  double acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+  for (int k0 = 0; k0 < op.K; k0 += kTKc) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTM * kTKc; e += 256) {
+      int ii, kk;
+      if (trans) { kk = e / kTM; ii = e - kk * kTM; }   // consecutive i: coalesced for A^T
+      else { ii = e / kTKc; kk = e - ii * kTKc; }
+      const int i = i0 + ii, k = k0 + kk;
+      double a = 0.0;
+      if (i < op.M && k < op.K) {
+        switch (op.amode) {
+          case 0: a = k <= i ? Am[(size_t)i * (i + 1) / 2 + k] : 0.0; break;
+          case 1: a = k >= i ? Am[(size_t)k * (k + 1) / 2 + i] : 0.0; break;
+          case 2: a = Am[(size_t)i * op.lda + k]; break;
+          default: a = Am[(size_t)k * op.lda + i]; break;
+        }
+      }
+      As[ii][kk] = a;
+    }
+    for (int e = threadIdx.x; e < kTKc * kRW; e += 256) {
+      const int kk = e / kRW, rr = e - kk * kRW;
+      const int k = k0 + kk;
+      double x = 0.0;
+      if (k < op.K && rr < nr) x = op_row(op.xmode, op.x_off, k, idx, v, ts, contrib, nrhs)[r0 + rr];
+      Xs[kk][rr] = x;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kTKc; ++kk) {
+      const double xv = Xs[kk][tr];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += As[ti + 8 * j][kk] * xv;
+    }
+  }
+  if (tr >= nr) return;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int i = i0 + ti + 8 * j;
+    if (i >= op.M) continue;
+    double val = op.alpha * acc[j];
+    if (op.smode >= 0) val += op_row(op.smode, op.s_off, i, idx, v, ts, contrib, nrhs)[r0 + tr];
+    op_row(op.dmode, op.d_off, i, idx, v, ts, contrib, nrhs)[r0 + tr] = val;
+  }
+}
+
+void launch_solve_tiles(const TileOp* ops, const int2* work, int nwork, const int32_t* idx, const double* fac,
+                        double* v, int nrhs, double* tscratch, double* contrib, cudaStream_t s) {
+  if (nwork <= 0) return;
+  dim3 grid((unsigned)nwork, (unsigned)((nrhs + kRW - 1) / kRW));
+  solve_tile_kernel<<<grid, 256, 0, s>>>(ops, work, idx, fac, v, nrhs, tscratch, contrib);
+}
+
 static void set_smem_attr(const void* fn) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }

@@ -111,10 +111,18 @@ struct LevelRec {
   double gpu_seconds = 0;                 // CUDA-event time of the level's kernels
   double t_part = 0, t_sym = 0, t_upd = 0, t_launch = 0, t_sync = 0;  // host phases
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  // solve metadata
+  // solve metadata: records handled one CTA each (recs / d_recs after the
+  // split) and the tiled phases of the large records
   std::vector<SolveRec> recs;
   SolveRec* d_recs = nullptr;
+  int nsmall = 0;
   int max_nc = 0, max_nq = 0;
+  struct Phase {
+    TileOp* d_ops = nullptr;
+    int2* d_work = nullptr;
+    int nwork = 0;
+  };
+  std::vector<Phase> fwd_ph, bwd_ph;
   // elimination forward reduction (targets / CSR of contribution rows)
   int64_t ncontrib = 0;
   int32_t* d_targets = nullptr;
@@ -138,9 +146,15 @@ struct hifde_factor {
   hifde::DBuf<int32_t> idx;
   std::vector<hifde::LevelRec> levels;  // last entry = terminal block (kind 2)
   int64_t max_contrib = 0;
+  int64_t tile_rows = 0;  // solve scratch rows of the tiled phases
   ~hifde_factor() {
     cudaSetDevice(device);
     for (auto& L : levels) {
+      for (auto* ph : {&L.fwd_ph, &L.bwd_ph})
+        for (auto& P : *ph) {
+          if (P.d_ops) cudaFree(P.d_ops);
+          if (P.d_work) cudaFree(P.d_work);
+        }
       if (L.d_recs) cudaFree(L.d_recs);
       if (L.d_targets) cudaFree(L.d_targets);
       if (L.d_ptr) cudaFree(L.d_ptr);
@@ -261,6 +275,7 @@ struct Factorizer {
   GridDesc g;
   hifde_options_t opt;
   hifde_factor_t* F;
+  hifde_factor_t* F_ = nullptr;  // alias used by the solve planner
   cudaStream_t s;
   int64_t N;
   // A0 (host + device); the host pattern aliases the caller's arrays when
@@ -519,6 +534,7 @@ struct Factorizer {
         smem_big = std::max(smem_big, align16(sizeof(int32_t) * (size_t)(nf + 2 * T.maxnb)));
       }
       T.C_off = (int64_t)F->fac.bump((size_t)nc * nc, s);
+      T.P_off = is_big[(size_t)t] ? (int64_t)F->fac.bump((size_t)nc * (nc + 1) / 2, s) : T.C_off;
       T.W_off = (int64_t)F->fac.bump((size_t)nc * nq, s);
       T.U_off = nq > 0 ? (int64_t)bvals.bump((size_t)nq * nq, s) : 0;
       L.max_front = std::max<int64_t>(L.max_front, nf);
@@ -526,11 +542,11 @@ struct Factorizer {
       R.nc = nc;
       R.nq = nq;
       R.idx_off = T.dofs_off;
-      R.C_off = T.C_off;
+      R.C_off = T.P_off;  // the solve applies the packed inverse
       R.W_off = T.W_off;
       R.T_off = 0;
       R.contrib_off = L.ncontrib;
-      R.inv = is_big[(size_t)t] ? 0 : 1;
+      R.inv = 1;
       R.pad = 0;
       L.ncontrib += nq;
       L.recs.push_back(R);
@@ -570,6 +586,9 @@ struct Factorizer {
       for (int a = 0; a < ntl; ++a)
         for (int b = a; b < ntl; ++b) tiles.push_back(make_int4(bi, a, b, 0));
     }
+    std::vector<int4> inv_work;  // packed inverse: 128 columns per CTA
+    for (int bi = 0; bi < (int)big.size(); ++bi)
+      for (int c0 = 0; c0 < big[(size_t)bi].nc; c0 += 128) inv_work.push_back(make_int4(bi, c0, 0, 0));
     // per-panel work lists of the blocked Cholesky / TRSM
     const int npanel = (max_big_nc + kPanelB - 1) / kPanelB;
     std::vector<int32_t> pcells;
@@ -601,7 +620,7 @@ struct Factorizer {
     lists.n = hl.size();
     lists.upload(hl.data(), 0, hl.size(), s);
     DBuf<ElimTask> d_small, d_big;
-    DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd;
+    DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd, d_inv;
     DBuf<int32_t> d_pcells;
     DBuf<double> d_dmin, d_scale;
     auto up4 = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
@@ -613,6 +632,7 @@ struct Factorizer {
     up4(d_asm, asm_work);
     up4(d_ptrsm, ptrsm);
     up4(d_pupd, pupd);
+    up4(d_inv, inv_work);
     d_pcells.reserve(pcells.size(), s);
     d_pcells.upload(pcells.data(), 0, pcells.size(), s);
     if (!big.empty()) {
@@ -656,7 +676,8 @@ struct Factorizer {
         ++g_launches;
       }
       launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
-      ++g_launches;
+      launch_big_inverse(d_big.p, d_inv.p, (int)inv_work.size(), A, s);
+      g_launches += 2;
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
@@ -672,6 +693,7 @@ struct Factorizer {
     d_asm.release(s);
     d_ptrsm.release(s);
     d_pupd.release(s);
+    d_inv.release(s);
     d_pcells.release(s);
     d_dmin.release(s);
     d_scale.release(s);
@@ -778,7 +800,7 @@ struct Factorizer {
         T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
         T.scratch_off = -1;
       }
-      T.rec_off = (int64_t)F->fac.bump((size_t)nc * nc + 2 * q4, s);
+      T.rec_off = (int64_t)F->fac.bump((size_t)nc * nc + 2 * q4 + (T.mode == 2 ? (size_t)nc * (nc + 1) / 2 + nc : 0), s);
       T.delta_off = (int64_t)bvals.bump((size_t)nc * nc, s);
       L.max_front = std::max<int64_t>(L.max_front, nf);
       int b = 0;
@@ -932,8 +954,10 @@ struct Factorizer {
         R.T_off = T.rec_off;
         R.C_off = T.rec_off + (int64_t)kk * r;
         R.W_off = R.C_off + (int64_t)r * r;
+        if (T.mode == 2)  // large groups keep C and put the packed inverse after the record
+          R.C_off = T.rec_off + (int64_t)T.nc * T.nc + 2 * ((int64_t)T.nc * T.nc / 4 + T.nc);
         R.contrib_off = 0;
-        R.inv = T.mode == 2 ? 0 : 1;
+        R.inv = 1;
         R.pad = 0;
         L.recs.push_back(R);
         L.max_nc = std::max(L.max_nc, r);
@@ -961,7 +985,7 @@ struct Factorizer {
     double* dscale = d_scale_all + lo;
     Arenas AH = AH_all;
     AH.status = AH_all.status + lo;
-    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles, wrow, wtu;
+    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles, wrow, wtu, winv;
     std::vector<int32_t> pc;
     int maxnc = 0;
     for (int i = 0; i < n; ++i) maxnc = std::max(maxnc, huge[(size_t)(lo + i)].nc);
@@ -973,6 +997,7 @@ struct Factorizer {
       for (int r0 = 0; r0 < nf; r0 += 64) wasm.push_back(make_int4(i, r0, std::min(r0 + 64, nf), 0));
       for (int c0 = 0; c0 < nc; c0 += 128) wt.push_back(make_int4(i, c0, 0, 0));
       for (int r0 = 0; r0 < nc; r0 += 64) wrow.push_back(make_int4(i, r0, 0, 0));
+      for (int c0 = 0; c0 < nc; c0 += 128) winv.push_back(make_int4(i, c0, 0, 0));
       for (int a0 = 0; a0 < nc; a0 += 64)
         for (int b0 = 0; b0 < nc; b0 += 64) {
           wc0.push_back(make_int4(i, 0, a0, b0));
@@ -1016,11 +1041,11 @@ struct Factorizer {
       }
       tuo[(size_t)bb + 1] = (int64_t)wtu.size();
     }
-    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8, d10, d11;
+    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8, d10, d11, d12;
     DBuf<int32_t> d9;
     auto up = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
     up(d1, wasm); up(d2, wt); up(d3, wc0); up(d4, wc1); up(d5, wsym); up(d6, pt); up(d7, pu); up(d8, tiles);
-    up(d10, wrow); up(d11, wtu);
+    up(d10, wrow); up(d11, wtu); up(d12, winv);
     d9.reserve(pc.size(), s);
     d9.upload(pc.data(), 0, pc.size(), s);
     for (int i = 0; i < n; ++i) {
@@ -1087,11 +1112,73 @@ struct Factorizer {
     }
     launch_schur_tiles(inner, d8.p, (int)tiles.size(), AH, s);
     launch_big_finish(inner, n, AH, dmin, dscale, s);
+    launch_big_inverse(inner, d12.p, (int)winv.size(), AH, s);
     launch_apply_rd(d_skv + lo, n, A, s);
-    g_launches += 3;
+    g_launches += 4;
     HCK(cudaGetLastError());
-    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(s);
+    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11, &d12}) d->release(s);
     d9.release(s);
+  }
+
+  // Split a level's records: large ones (by size) become tiled product phases
+  // (TileOp), the rest stay one-CTA records.
+  void build_solve_plan(LevelRec& L) {
+    auto is_large = [](const SolveRec& R) { return R.nc > 96 || R.nq > 192; };
+    std::vector<SolveRec> small, large;
+    for (const SolveRec& R : L.recs) (is_large(R) ? large : small).push_back(R);
+    L.nsmall = (int)small.size();
+    L.max_nc = L.max_nq = 0;
+    for (const SolveRec& R : small) { L.max_nc = std::max(L.max_nc, R.nc); L.max_nq = std::max(L.max_nq, R.nq); }
+    L.d_recs = to_device(small);
+    if (large.empty()) return;
+    auto mk = [](int M, int K, int am, int64_t A_off, int64_t lda, int xm, int64_t xo, int sm, int64_t so, int dm,
+                 int64_t dof, double alpha) {
+      TileOp o;
+      o.M = M; o.K = K; o.amode = am; o.A_off = A_off; o.lda = lda;
+      o.xmode = xm; o.x_off = xo; o.smode = sm; o.s_off = so; o.dmode = dm; o.d_off = dof; o.alpha = alpha;
+      return o;
+    };
+    const int nph = L.kind == 1 ? 3 : 2;
+    std::vector<std::vector<TileOp>> F(nph), B(nph);
+    int64_t rows = 0;
+    for (const SolveRec& R : large) {
+      if (L.kind != 1) {  // elimination record (and the terminal block): c then q in idx
+        const int nc = R.nc, nq = R.nq;
+        const int64_t c = R.idx_off, q = R.idx_off + nc, S = rows;
+        rows += nc;
+        F[0].push_back(mk(nc, nc, 0, R.C_off, 0, 0, c, -1, 0, 1, S, 1.0));               // S = P v_c
+        if (nq > 0) F[1].push_back(mk(nq, nc, 3, R.W_off, nq, 1, S, -1, 0, 2, R.contrib_off, 1.0));  // g = W^T S
+        F[1].push_back(mk(nc, 0, 2, 0, 0, 1, 0, 1, S, 0, c, 0.0));                        // v_c = S
+        B[0].push_back(mk(nc, nq, 2, R.W_off, nq, 0, q, 0, c, 1, S, -1.0));              // T = v_c - W v_q
+        B[1].push_back(mk(nc, nc, 1, R.C_off, 0, 1, S, -1, 0, 0, c, 1.0));               // v_c = P^T T
+      } else {  // skeleton record: sk[k] then rd[r]; T (k x r), P (r x r), W (r x k)
+        const int r = R.nc, k = R.nq;
+        const int64_t sk = R.idx_off, rd = R.idx_off + k, X = rows, S = rows + r;
+        rows += 2 * r;
+        F[0].push_back(mk(r, k, 3, R.T_off, r, 0, sk, 0, rd, 1, X, -1.0));   // X = v_rd - T^T v_sk
+        F[1].push_back(mk(r, r, 0, R.C_off, 0, 1, X, -1, 0, 1, S, 1.0));     // S = P X
+        F[2].push_back(mk(k, r, 3, R.W_off, k, 1, S, 0, sk, 0, sk, -1.0));   // v_sk -= W^T S
+        F[2].push_back(mk(r, 0, 2, 0, 0, 1, 0, 1, S, 0, rd, 0.0));           // v_rd = S
+        B[0].push_back(mk(r, k, 2, R.W_off, k, 0, sk, 0, rd, 1, X, -1.0));   // X = v_rd - W v_sk
+        B[1].push_back(mk(r, r, 1, R.C_off, 0, 1, X, -1, 0, 0, rd, 1.0));    // v_rd = P^T X
+        B[2].push_back(mk(k, r, 2, R.T_off, r, 0, rd, 0, sk, 0, sk, -1.0));  // v_sk -= T v_rd
+      }
+    }
+    F_->tile_rows = std::max(F_->tile_rows, rows);
+    auto upload = [&](std::vector<std::vector<TileOp>>& ops, std::vector<LevelRec::Phase>& out) {
+      for (auto& v : ops) {
+        std::vector<int2> work;
+        for (int i = 0; i < (int)v.size(); ++i)
+          for (int i0 = 0; i0 < std::max(v[(size_t)i].M, 1); i0 += 64) work.push_back(make_int2(i, i0));
+        LevelRec::Phase P;
+        P.d_ops = to_device(v);
+        P.d_work = to_device(work);
+        P.nwork = (int)work.size();
+        out.push_back(P);
+      }
+    };
+    upload(F, L.fwd_ph);
+    upload(B, L.bwd_ph);
   }
 
   // -------------------------------------------------------------------------
@@ -1246,8 +1333,9 @@ struct Factorizer {
       L.kind = 2;
       record_trace(L, tl);
     }
-    // solve metadata to the device
-    for (auto& L : F->levels) L.d_recs = to_device(L.recs);
+    // solve metadata to the device: small records one CTA each, large ones as
+    // tiled product phases
+    for (auto& L : F->levels) build_solve_plan(L);
     HCK(cudaStreamSynchronize(s));
     for (auto& L : F->levels) {
       if (L.ev0 && L.ev1) {
@@ -1299,37 +1387,45 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   HCK(cudaMemcpyAsync(v, b, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   double* contrib = nullptr;
   HCK(cudaMallocAsync((void**)&contrib, std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
-  // global workspace for records too large for shared memory
+  double* tscr = nullptr;
+  HCK(cudaMallocAsync((void**)&tscr, std::max<size_t>(F->tile_rows * nrhs * sizeof(double), 8), s));
+  // global workspace for one-CTA records too large for shared memory
   size_t scratch_need = 0;
   auto ws_plan = [&](const LevelRec& L, int64_t per_rec_doubles, size_t& smem, int64_t& per_rec) {
     const size_t need = (size_t)per_rec_doubles * sizeof(double);
     if (need <= kSmemCap) { smem = need; per_rec = 0; }
-    else { smem = 0; per_rec = per_rec_doubles; scratch_need = std::max(scratch_need, (size_t)per_rec * L.recs.size()); }
+    else { smem = 0; per_rec = per_rec_doubles; scratch_need = std::max(scratch_need, (size_t)per_rec * L.nsmall); }
+  };
+  auto ws_of = [&](const LevelRec& L) {
+    return L.kind == 1 ? (int64_t)(2 * L.max_nc + L.max_nq) * nrhs : (int64_t)2 * L.max_nc * nrhs;
   };
   for (const auto& L : F->levels) {
     size_t sm; int64_t pr;
-    if (L.kind == 1) ws_plan(L, (int64_t)(2 * L.max_nc + L.max_nq) * nrhs, sm, pr);
-    else ws_plan(L, (int64_t)2 * L.max_nc * nrhs, sm, pr);
+    ws_plan(L, ws_of(L), sm, pr);
   }
   double* scratch = nullptr;
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
+  auto phases = [&](const std::vector<LevelRec::Phase>& ph) {
+    for (const auto& P : ph) {
+      launch_solve_tiles(P.d_ops, P.d_work, P.nwork, idx, fac, v, nrhs, tscr, contrib, s);
+      ++g_launches;
+    }
+  };
   const size_t nl = F->levels.size();
   for (size_t li = 0; li < nl; ++li) {
     const LevelRec& L = F->levels[li];
-    const int nr = (int)L.recs.size();
-    if (!nr) continue;
+    const int nr = L.nsmall;
     size_t sm; int64_t pr;
+    ws_plan(L, ws_of(L), sm, pr);
     if (L.kind == 1) {
-      ws_plan(L, (int64_t)(2 * L.max_nc + L.max_nq) * nrhs, sm, pr);
-      launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s);
-      ++g_launches;
+      if (nr) { launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s); ++g_launches; }
+      phases(L.fwd_ph);
     } else {
-      ws_plan(L, (int64_t)2 * L.max_nc * nrhs, sm, pr);
-      launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s);
-      ++g_launches;
-      if (L.kind == 0) {
+      if (nr) { launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s); ++g_launches; }
+      phases(L.fwd_ph);
+      if (L.kind == 0 && L.ntargets) {
         launch_solve_reduce(L.d_targets, L.d_ptr, L.d_ent, L.ntargets, contrib, v, nrhs, s);
         ++g_launches;
       }
@@ -1337,22 +1433,21 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   }
   for (size_t li = nl; li-- > 0;) {
     const LevelRec& L = F->levels[li];
-    const int nr = (int)L.recs.size();
-    if (!nr) continue;
+    const int nr = L.nsmall;
     size_t sm; int64_t pr;
+    ws_plan(L, ws_of(L), sm, pr);
     if (L.kind == 1) {
-      ws_plan(L, (int64_t)(2 * L.max_nc + L.max_nq) * nrhs, sm, pr);
-      launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s);
+      if (nr) { launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s); ++g_launches; }
     } else {
-      ws_plan(L, (int64_t)2 * L.max_nc * nrhs, sm, pr);
-      launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s);
+      if (nr) { launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s); ++g_launches; }
     }
-    ++g_launches;
+    phases(L.bwd_ph);
   }
   HCK(cudaGetLastError());
   HCK(cudaMemcpyAsync(x, v, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   HCK(cudaFreeAsync(v, s));
   HCK(cudaFreeAsync(contrib, s));
+  HCK(cudaFreeAsync(tscr, s));
   HCK(cudaFreeAsync(scratch, s));
   if (!dev) HCK(cudaStreamSynchronize(s));
 }
@@ -1467,6 +1562,7 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
     }
     if (fz.opt.exact_max_groups <= 0) fz.opt.exact_max_groups = 32;
     fz.F = F.get();
+    fz.F_ = F.get();
     fz.s = F->stream;
     const int64_t nnz = opt->input_on_device ? 0 : indptr[n];
     fz.run(indptr, indices, vals, nnz);
