@@ -165,3 +165,31 @@ def test_verify_noninteracting_passes():
     a = H.assemble(g, H.constant_field(g))
     f = H.factor_hifde3x(a, g, 1e-6, verify=True)
     assert f.metrics["s_top"] > 0
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4", "cfg3", "cfg5"])
+def test_full_size_config_against_reference(name):
+    """BASELINE configs at full size against the reference's own run
+    (tests/golden/<cfg>.npz, summary only): per-level ranks within +-2%,
+    s_top, one-shot residual within 10x, PCG iteration count."""
+    import os
+    if not os.path.exists(os.path.join(G.GOLDEN_DIR, name + ".npz")):
+        pytest.skip(f"golden {name} not generated")
+    gd = G.load(name)
+    g, csr = G.build_problem(gd)
+    assert G.csr_digest(csr) == str(gd["csr_sha256"])
+    gg = _grid(gd)
+    fac = H.factor_hifde3x if str(gd["variant"]) == "hifde3x" else H.factor_hifde
+    f = fac(csr, gg, float(gd["eps"]))
+    counts = [c for _, c in f.metrics["skeleton_counts"]]
+    assert G.ranks_within(counts, gd["skel_ranks"]), (counts, gd["skel_ranks"].tolist())
+    s_ref = int(gd["s_top"])
+    assert abs(f.metrics["s_top"] - s_ref) <= max(1, 0.02 * s_ref)
+    b = G.rhs(gd, gg.ndof)
+    x = f.apply_inverse(b)
+    resid = np.linalg.norm(csr @ x - b, axis=0) / np.linalg.norm(b, axis=0)
+    assert np.all(resid <= 10 * gd["oneshot_resid"]), (resid, gd["oneshot_resid"])
+    rep = H.pcg(csr, b[:, 0], f.apply_inverse, tol=1e-12, max_iter=500)
+    assert rep.converged
+    its = int(gd["pcg_iters"])
+    assert abs(rep.n_i - its) <= max(1, int(0.25 * its)), (rep.n_i, its)
