@@ -153,6 +153,25 @@ __device__ void tri_inverse_packed(const double* C, int n, int ld, double* __res
   }
 }
 
+template <int NT>
+__device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, int ldb);
+
+// Packed lower inverse via B = C^-1 I in the workspace X (n x n), then a
+// coalesced packed store.  All threads busy, one barrier per row.
+template <int NT>
+__device__ void tri_inverse_packed_ws(const double* C, int n, int ld, double* X, double* __restrict__ P) {
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += NT) {
+    const int i = e / n, j = e - i * n;
+    X[e] = (i == j) ? 1.0 : 0.0;
+  }
+  trsm_1sync<NT>(C, n, ld, X, n, n);
+  for (int e = threadIdx.x; e < n * n; e += NT) {
+    const int i = e / n, j = e - i * n;
+    if (j <= i) P[(size_t)i * (i + 1) / 2 + j] = X[e];
+  }
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
@@ -228,7 +247,8 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
     }
   }
   // the solve applies C^-1 as a product: store it packed (lower, row-major)
-  tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
+  if (t.scratch_off == -2) tri_inverse_packed_ws<NT>(F, nc, nf, F + (size_t)nf * nf, A.fac + t.P_off);
+  else tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
   if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
 }
 
@@ -589,7 +609,7 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   double* rec = A.fac + t.rec_off;
   for (int e = threadIdx.x; e < k * r; e += NT) rec[e] = Ts[e];
   double* C = rec + (size_t)k * r;
-  tri_inverse_packed<NT>(Brr, r, r, C);  // packed C^-1 for the solve
+  tri_inverse_packed_ws<NT>(Brr, r, r, Brr + (size_t)nc * nc, C);  // packed C^-1 for the solve
   double* Wo = C + (size_t)r * r;
   for (int e = threadIdx.x; e < r * k; e += NT) Wo[e] = Wm[e];
   if (threadIdx.x == 0) A.status[t.group] = 0;

@@ -524,9 +524,11 @@ struct Factorizer {
       hl.insert(hl.end(), bl, bl + f.nb);
       const size_t ib = align16(sizeof(int32_t) * (size_t)(nf + T.maxnb));
       const size_t need = ib + sizeof(double) * (size_t)nf * nf;
+      const size_t need_inv = need + sizeof(double) * (size_t)nc * nc;
       if (need <= kSmemCap) {
-        T.scratch_off = -1;
-        smem_small = std::max(smem_small, need);
+        // -2: room for the inverse workspace after the front as well
+        T.scratch_off = need_inv <= kSmemCap ? -2 : -1;
+        smem_small = std::max(smem_small, T.scratch_off == -2 ? need_inv : need);
         max_small_nf = std::max(max_small_nf, nf);
       } else {
         is_big[(size_t)t] = 1;
@@ -784,7 +786,7 @@ struct Factorizer {
       hl.insert(hl.end(), blks, blks + f.nb);
       const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 5 * nc));
       const size_t q4 = (size_t)nc * nc / 4 + nc;
-      const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + (size_t)nc * nc;
+      const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
       const size_t mq = (size_t)nq * nc + 2 * (size_t)nc;
       max_nc = std::max(max_nc, nc);
       max_nq = std::max(max_nq, nq);
@@ -794,7 +796,7 @@ struct Factorizer {
         smem = std::max(smem, ib + sizeof(double) * wsd);
       } else if (ib + sizeof(double) * mq <= kSmemCap) {
         T.mode = 1;
-        T.scratch_off = (int64_t)scratch.bump(2 * (size_t)nc * nc + 3 * q4 + 8, s);
+        T.scratch_off = (int64_t)scratch.bump(3 * (size_t)nc * nc + 3 * q4 + 8, s);
         smem = std::max(smem, ib + sizeof(double) * mq);
       } else {
         T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
