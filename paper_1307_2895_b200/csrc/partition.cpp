@@ -73,23 +73,29 @@ Groups interior_groups(const GridDesc& g, const Coords& X, int ell, const std::v
   if (ell < 0 || ell >= std::max(g.nlevels, 1)) throw std::invalid_argument("level out of range");
   const int w = g.m << ell;
   const int k = g.n / w;
-  std::vector<int32_t> dofs, keys;
-  dofs.reserve(act.size());
-  keys.reserve(act.size());
-  for (int32_t d : act) {
-    bool inside = true;
+  const int64_t na = (int64_t)act.size();
+  std::vector<int32_t> kall((size_t)na);
+#pragma omp parallel for schedule(static) if (na > 65536)
+  for (int64_t i = 0; i < na; ++i) {
+    const int32_t d = act[(size_t)i];
     int key = 0, stride = 1;
     for (int ax = 0; ax < g.dim; ++ax) {
       const int x = X.x[ax][(size_t)d];
       const int q = x / w;
-      if (x - q * w == 0) { inside = false; break; }
+      if (x - q * w == 0) { key = -1; break; }
       key += q * stride;
       stride *= k;
     }
-    if (!inside) continue;
-    dofs.push_back(d);
-    keys.push_back(key);
+    kall[(size_t)i] = key;
   }
+  std::vector<int32_t> dofs, keys;
+  dofs.reserve(act.size());
+  keys.reserve(act.size());
+  for (int64_t i = 0; i < na; ++i)
+    if (kall[(size_t)i] >= 0) {
+      dofs.push_back(act[(size_t)i]);
+      keys.push_back(kall[(size_t)i]);
+    }
   return bucket(dofs, keys, ipow(k, g.dim));
 }
 
@@ -100,11 +106,13 @@ Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::
   const int w = g.m << ell;
   const int k = g.n / w;
   const int span = (int)ipow(k, g.dim);
-  std::vector<int32_t> dofs, keys;
-  dofs.reserve(act.size());
-  keys.reserve(act.size());
-  int x2[3];
-  for (int32_t d : act) {
+  const int64_t na = (int64_t)act.size();
+  std::vector<int32_t> kall((size_t)na);
+#pragma omp parallel for schedule(static) if (na > 65536)
+  for (int64_t i = 0; i < na; ++i) {
+    const int32_t d = act[(size_t)i];
+    int x2[3];
+    kall[(size_t)i] = -1;
     int planes = 0;
     for (int ax = 0; ax < g.dim; ++ax) {
       const int x = X.x[ax][(size_t)d];
@@ -132,9 +140,16 @@ Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::
       }
       if (dist < best_d) { best_d = dist; best_key = fam * span + key; }
     }
-    dofs.push_back(d);
-    keys.push_back(best_key);
+    kall[(size_t)i] = best_key;
   }
+  std::vector<int32_t> dofs, keys;
+  dofs.reserve(act.size());
+  keys.reserve(act.size());
+  for (int64_t i = 0; i < na; ++i)
+    if (kall[(size_t)i] >= 0) {
+      dofs.push_back(act[(size_t)i]);
+      keys.push_back(kall[(size_t)i]);
+    }
   return bucket(dofs, keys, (int64_t)span * g.dim);
 }
 

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -700,45 +701,58 @@ struct Factorizer {
     d_dmin.release(s);
     d_scale.release(s);
     // solve-side reduction structure for the shared neighbour DOFs
-    if (!is_top) build_reduction(L);
+    if (!is_top) build_reduction((size_t)(&L - F->levels.data()), L);
     L.t_sync = now_s() - tp;
   }
 
-  void build_reduction(LevelRec& L) {
-    // targets: every q DOF of the level; entries in record order
+  // Solve-side reduction of one elimination level: for every neighbour DOF the
+  // contribution rows (record order) summed by solve_reduce_kernel.  Built on
+  // a background thread from a copy of the q lists; joined at the end.
+  struct Reduction {
     std::vector<int32_t> targets;
-    std::vector<int64_t> cnt;
-    const int64_t tq = ++stamp;
-    std::vector<int32_t> slot_of_dof;  // via dstamp/bstamp trick: use a map vector
-    // map DOF -> target index (use a temporary N-sized vector only when needed)
-    static thread_local std::vector<int32_t> tmap;
-    if ((int64_t)tmap.size() < N) tmap.assign((size_t)N, -1);
+    std::vector<int64_t> ptr, ent;
+  };
+  std::vector<std::pair<size_t, std::future<Reduction>>> reductions;
+
+  void build_reduction(size_t level_index, const LevelRec& L) {
+    std::vector<std::pair<int32_t, int64_t>> pairs;
+    size_t tot = 0;
+    for (const SolveRec& R : L.recs) tot += (size_t)R.nq;
+    pairs.reserve(tot);
     for (const SolveRec& R : L.recs) {
       const int32_t* q = h_idx.data() + R.idx_off + R.nc;
-      for (int a = 0; a < R.nq; ++a) {
-        const int32_t d = q[a];
-        if (dstamp[(size_t)d] != tq) {
-          dstamp[(size_t)d] = tq;
-          tmap[(size_t)d] = (int32_t)targets.size();
-          targets.push_back(d);
-          cnt.push_back(0);
-        }
-        cnt[(size_t)tmap[(size_t)d]]++;
-      }
+      for (int a = 0; a < R.nq; ++a) pairs.emplace_back(q[a], R.contrib_off + a);
     }
-    std::vector<int64_t> ptr(targets.size() + 1, 0);
-    for (size_t i = 0; i < targets.size(); ++i) ptr[i + 1] = ptr[i] + cnt[i];
-    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
-    std::vector<int64_t> ent((size_t)ptr.back());
-    for (const SolveRec& R : L.recs) {
-      const int32_t* q = h_idx.data() + R.idx_off + R.nc;
-      for (int a = 0; a < R.nq; ++a) ent[(size_t)fill[(size_t)tmap[(size_t)q[a]]]++] = R.contrib_off + a;
-    }
-    L.ntargets = (int)targets.size();
-    L.d_targets = to_device(targets);
-    L.d_ptr = to_device(ptr);
-    L.d_ent = to_device(ent);
     F->max_contrib = std::max(F->max_contrib, L.ncontrib);
+    reductions.emplace_back(level_index, std::async(std::launch::async, [p = std::move(pairs)]() mutable {
+      // (dof, entry) with entries increasing in record order: sorting the pairs
+      // groups by DOF and keeps record order inside a group
+      std::sort(p.begin(), p.end());
+      Reduction r;
+      r.ptr.push_back(0);
+      r.ent.reserve(p.size());
+      for (size_t i = 0; i < p.size(); ++i) {
+        if (i == 0 || p[i].first != p[i - 1].first) {
+          if (i) r.ptr.push_back((int64_t)r.ent.size());
+          r.targets.push_back(p[i].first);
+        }
+        r.ent.push_back(p[i].second);
+      }
+      if (!p.empty()) r.ptr.push_back((int64_t)r.ent.size());
+      return r;
+    }));
+  }
+
+  void finish_reductions() {
+    for (auto& pr : reductions) {
+      Reduction r = pr.second.get();
+      LevelRec& L = F->levels[pr.first];
+      L.ntargets = (int)r.targets.size();
+      L.d_targets = to_device(r.targets);
+      L.d_ptr = to_device(r.ptr);
+      L.d_ent = to_device(r.ent);
+    }
+    reductions.clear();
   }
 
   // -------------------------------------------------------------------------
@@ -1335,6 +1349,7 @@ struct Factorizer {
       L.kind = 2;
       record_trace(L, tl);
     }
+    finish_reductions();
     // solve metadata to the device: small records one CTA each, large ones as
     // tiled product phases
     for (auto& L : F->levels) build_solve_plan(L);
