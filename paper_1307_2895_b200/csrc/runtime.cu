@@ -72,6 +72,46 @@ double now_s() {
 
 size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 
+// Pinned host staging arena for H2D uploads: host data is memcpy'd into it
+// and copied with a truly asynchronous cudaMemcpyAsync, so the host never
+// waits for the GPU to drain when it uploads the next level's work.  The arena
+// is bump-allocated per factorization; if it fills up the stream is drained
+// and it is reused.  Kept across factorizations (grown to the peak).
+struct PinnedStage {
+  char* p = nullptr;
+  size_t cap = 0, n = 0, peak = 0;
+  cudaStream_t s = nullptr;
+  void begin(cudaStream_t st) {
+    s = st;
+    n = 0;
+    if (peak > cap) {
+      if (p) cudaFreeHost(p);
+      cap = peak + peak / 4;
+      p = nullptr;
+      if (cudaHostAlloc((void**)&p, cap, cudaHostAllocDefault) != cudaSuccess) { p = nullptr; cap = 0; }
+    }
+  }
+  // returns false when the caller should fall back to a pageable copy
+  bool copy(void* dst, const void* src, size_t bytes) {
+    const size_t need = (bytes + 255) & ~(size_t)255;
+    peak = std::max(peak, n + need);
+    if (!p || need > cap) return false;
+    if (n + need > cap) {  // full: drain the stream, then reuse from the start
+      cudaStreamSynchronize(s);
+      n = 0;
+    }
+    std::memcpy(p + n, src, bytes);
+    cudaMemcpyAsync(dst, p + n, bytes, cudaMemcpyHostToDevice, s);
+    n += need;
+    return true;
+  }
+};
+thread_local PinnedStage* g_stage = nullptr;
+PinnedStage& pinned_stage() {
+  static PinnedStage ps;
+  return ps;
+}
+
 // Growable device array with stream-ordered (pooled) allocation.
 template <class T>
 struct DBuf {
@@ -94,7 +134,9 @@ struct DBuf {
     return off;
   }
   void upload(const T* h, size_t off, size_t cnt, cudaStream_t s) {
-    if (cnt) HCK(cudaMemcpyAsync(p + off, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (!cnt) return;
+    if (g_stage && g_stage->copy(p + off, h, cnt * sizeof(T))) return;
+    HCK(cudaMemcpyAsync(p + off, h, cnt * sizeof(T), cudaMemcpyHostToDevice, s));
   }
   void release(cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
@@ -1228,6 +1270,11 @@ struct Factorizer {
     const double t0 = now_s();
     N = g.ndof();
     HTRACE("factor start N=%lld", (long long)N);
+    pinned_stage().begin(s);
+    g_stage = &pinned_stage();
+    struct StageOff {
+      ~StageOff() { g_stage = nullptr; }
+    } stage_off;
     // A0: the symbolic analysis needs the pattern on the host
     if (opt.input_on_device) {
       indptr_own.resize((size_t)N + 1);
