@@ -49,7 +49,7 @@ extern "C" {
 #define HIFDE_VARIANT_HIFDE3X 2 /* factor_hifde3x: faces + edges (3D)      */
 
 /* ordering of the groups of one skeletonization level */
-#define HIFDE_ORDER_AUTO 0      /* exact order on small levels, else snapshot */
+#define HIFDE_ORDER_AUTO 0      /* exact order unless the chain is too long */
 #define HIFDE_ORDER_SNAPSHOT 1  /* all IDs of a level from one snapshot    */
 #define HIFDE_ORDER_EXACT 2     /* reference's sequential semantics        */
 
@@ -58,7 +58,7 @@ typedef struct hifde_options {
   int skip_levels;      /* skeletonization skipped below this level         */
   int spd;              /* 1: Cholesky mode (the only mode implemented)     */
   int order_mode;       /* HIFDE_ORDER_*                                    */
-  int exact_max_groups; /* AUTO: exact order when a level has <= this groups*/
+  int exact_max_batches;/* AUTO: exact order when its dependency chain <= this */
   int device;           /* CUDA device ordinal                              */
   int input_on_device;  /* CSR arrays are device pointers                   */
   int verify;           /* 1: check cells of each level are non-interacting */

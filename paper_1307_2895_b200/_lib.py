@@ -22,7 +22,7 @@ class Options(C.Structure):
         ("skip_levels", C.c_int),
         ("spd", C.c_int),
         ("order_mode", C.c_int),
-        ("exact_max_groups", C.c_int),
+        ("exact_max_batches", C.c_int),
         ("device", C.c_int),
         ("input_on_device", C.c_int),
         ("verify", C.c_int),

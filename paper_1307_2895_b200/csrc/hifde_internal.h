@@ -114,6 +114,10 @@ void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,
                  cudaStream_t s);
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s);
+int skel_ordered_capacity(size_t smem, int nt);
+cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
+                                int* done, const Arenas& A, double eps, size_t smem, int nt, int grid,
+                                cudaStream_t s);
 
 void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                              size_t smem, cudaStream_t s);

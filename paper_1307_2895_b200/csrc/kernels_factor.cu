@@ -18,6 +18,7 @@
 //   CPQR / ID     src/dense.py:239-264
 #include <cfloat>
 #include <cstdint>
+#include <cuda/atomic>
 
 #include "hifde_internal.h"
 
@@ -326,14 +327,11 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
 //   even scaled into place.
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ tasks, Arenas A,
-                                                  double eps) {
+__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem) {
   constexpr int NW = NT / 32;
-  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[NW];
   __shared__ double sh_beta, sh_tau, sh_scal;
   __shared__ int sh_stop, sh_k;
-  const SkelTask t = tasks[blockIdx.x];
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
@@ -376,7 +374,7 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   for (int i = threadIdx.x; i < nf; i += NT) {
     const int g = gd[i];
     sdofs[i] = g;
-    salive[i] = (i < nc) ? 1 : (int)A.active[g];
+    salive[i] = (i < nc) ? 1 : (int)__ldcg(A.active + g);  // written by other CTAs
   }
   for (int i = threadIdx.x; i < nc; i += NT) perm[i] = i;
   for (int e = threadIdx.x; e < nc * nc; e += NT) Acc[e] = 0.0;
@@ -615,6 +613,48 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   if (threadIdx.x == 0) A.status[t.group] = 0;
 }
 
+template <int NT>
+__global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ tasks, Arenas A, double eps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const SkelTask t = tasks[blockIdx.x];
+  skel_group<NT>(t, A, eps, smem);
+}
+
+// Exact (reference) order in one launch: co-resident CTAs walk the groups in
+// reference order (task j -> CTA j mod grid); a group starts once every
+// earlier neighbouring group has finished (its redundant DOFs are then
+// retired in the device active mask), exactly the state the reference's
+// sequential loop gives it (src/driver.py:190-194, src/factor_ops.py:208).
+// Deadlock-free: the lowest unfinished group always has all predecessors done
+// and its CTA is not blocked.
+template <int NT>
+__global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __restrict__ tasks, int ntasks,
+                                                          const int64_t* __restrict__ pred_ptr,
+                                                          const int32_t* __restrict__ pred,
+                                                          int* __restrict__ done, Arenas A, double eps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  for (int j = blockIdx.x; j < ntasks; j += gridDim.x) {
+    if (threadIdx.x == 0) {
+      for (int64_t p = pred_ptr[j]; p < pred_ptr[j + 1]; ++p) {
+        cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[p]]);
+        while (f.load(cuda::memory_order_acquire) == 0) __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    const SkelTask t = tasks[j];
+    skel_group<NT>(t, A, eps, smem);
+    __syncthreads();
+    const int k = A.kout[t.group];
+    const int32_t* out = A.idx + t.out_off;
+    for (int a = k + threadIdx.x; a < t.nc; a += NT) A.active[out[a]] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      cuda::atomic_ref<int, cuda::thread_scope_device> f(done[j]);
+      f.store(1, cuda::memory_order_release);
+    }
+  }
+}
+
 // Retire the redundant DOFs of a finished batch (device active mask).
 __global__ void apply_rd_kernel(const SkelTask* __restrict__ tasks, Arenas A) {
   const SkelTask t = tasks[blockIdx.x];
@@ -659,6 +699,34 @@ void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double ep
   }
   if (nt <= 128) skel_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A, eps);
   else skel_kernel<512><<<ntasks, 512, smem, s>>>(d_tasks, A, eps);
+}
+
+int skel_ordered_capacity(size_t smem, int nt) {
+  int per_sm = 0, dev = 0, nsm = 0;
+  if (nt <= 128) {
+    allow_smem(skel_ordered_kernel<128>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skel_ordered_kernel<128>, 128, smem);
+  } else {
+    allow_smem(skel_ordered_kernel<512>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skel_ordered_kernel<512>, 512, smem);
+  }
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * nsm;
+}
+
+cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
+                                int* done, const Arenas& A, double eps, size_t smem, int nt, int grid,
+                                cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  Arenas Ac = A;
+  void* args[] = {(void*)&d_tasks, (void*)&ntasks, (void*)&pred_ptr, (void*)&pred, (void*)&done, (void*)&Ac,
+                  (void*)&eps};
+  if (nt <= 128)
+    return cudaLaunchCooperativeKernel((const void*)skel_ordered_kernel<128>, dim3((unsigned)grid), dim3(128), args,
+                                       smem, s);
+  return cudaLaunchCooperativeKernel((const void*)skel_ordered_kernel<512>, dim3((unsigned)grid), dim3(512), args,
+                                     smem, s);
 }
 
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s) {

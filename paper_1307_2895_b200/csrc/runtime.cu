@@ -819,6 +819,8 @@ struct Factorizer {
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = (int32_t)t;
     int nbatch = 1;
+    std::vector<int32_t> preds;          // earlier neighbouring groups (exact order)
+    std::vector<int64_t> pred_ptr{0};
     const std::vector<FrontSym> fs = fronts(gr);
     for (int64_t t = 0; t < nt; ++t) {
       const int32_t* c = gr.begin(t);
@@ -862,17 +864,24 @@ struct Factorizer {
       T.delta_off = (int64_t)bvals.bump((size_t)nc * nc, s);
       L.max_front = std::max<int64_t>(L.max_front, nf);
       int b = 0;
+      const size_t p0 = preds.size();
       for (int i = 0; i < nq; ++i) {
         const int32_t go = group_of[(size_t)q[i]];
-        if (go >= 0 && go < t) b = std::max(b, batch[(size_t)go] + 1);
+        if (go >= 0 && go < t) {
+          b = std::max(b, batch[(size_t)go] + 1);
+          preds.push_back(go);
+        }
       }
+      std::sort(preds.begin() + (int64_t)p0, preds.end());
+      preds.erase(std::unique(preds.begin() + (int64_t)p0, preds.end()), preds.end());
+      pred_ptr.push_back((int64_t)preds.size());
       batch[(size_t)t] = b;
       nbatch = std::max(nbatch, b + 1);
     }
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = -1;
     bool exact = opt.order_mode == HIFDE_ORDER_EXACT ||
-                 (opt.order_mode == HIFDE_ORDER_AUTO && nt <= opt.exact_max_groups);
+                 (opt.order_mode == HIFDE_ORDER_AUTO && nbatch <= opt.exact_max_batches);
     if (!exact) {
       std::fill(batch.begin(), batch.end(), 0);
       nbatch = 1;
@@ -881,6 +890,53 @@ struct Factorizer {
     HTRACE("  symbolic done, %d batches", nbatch);
     double tp = now_s();
     L.t_sym = tp - t_begin;
+    bool any_huge = false;
+    for (const SkelTask& T : tasks) any_huge |= T.mode == 2;
+    if (exact && !any_huge && nt > 1 && opt.order_mode != HIFDE_ORDER_SNAPSHOT) {
+      // one launch, per-group dependencies (skel_ordered_kernel)
+      upload_idx();
+      upload_blocks();
+      lists.reserve(std::max<size_t>(hl.size(), 1), s);
+      lists.n = hl.size();
+      lists.upload(hl.data(), 0, hl.size(), s);
+      DBuf<SkelTask> dt;
+      DBuf<int64_t> dpp;
+      DBuf<int32_t> dpr;
+      DBuf<int> ddone;
+      dt.reserve(tasks.size(), s);
+      dt.upload(tasks.data(), 0, tasks.size(), s);
+      dpp.reserve(pred_ptr.size(), s);
+      dpp.upload(pred_ptr.data(), 0, pred_ptr.size(), s);
+      dpr.reserve(std::max<size_t>(preds.size(), 1), s);
+      dpr.upload(preds.data(), 0, preds.size(), s);
+      ddone.reserve((size_t)nt, s);
+      HCK(cudaMemsetAsync(ddone.p, 0, sizeof(int) * (size_t)nt, s));
+      const int64_t st_off = (int64_t)status.bump((size_t)nt, s);
+      HCK(cudaMemsetAsync(status.p + st_off, 0, (size_t)nt * sizeof(int), s));
+      pending.push_back({st_off, nt, tag, "group"});
+      kout.n = 0;
+      kout.bump((size_t)nt, s);
+      Arenas A = arenas();
+      A.status = status.p + st_off;
+      const int nthr = (max_nc > 32 || max_nq > 128) ? 512 : 128;
+      const int cap = skel_ordered_capacity(smem, nthr);
+      if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
+      const int grid = (int)std::min<int64_t>(nt, cap);
+      HCK(cudaEventCreate(&L.ev0));
+      HCK(cudaEventCreate(&L.ev1));
+      HCK(cudaEventRecord(L.ev0, s));
+      HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
+      ++g_launches;
+      HCK(cudaEventRecord(L.ev1, s));
+      L.t_launch = now_s() - tp;
+      tp = now_s();
+      finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
+      dt.release(s);
+      dpp.release(s);
+      dpr.release(s);
+      ddone.release(s);
+      return;
+    }
     // order tasks by batch (stable keeps the reference order inside a batch)
     std::vector<int64_t> order((size_t)nt);
     for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
@@ -978,6 +1034,21 @@ struct Factorizer {
     HCK(cudaGetLastError());
     L.t_launch = now_s() - tp;
     tp = now_s();
+    dt.release(s);
+    dth.release(s);
+    dhuge.release(s);
+    dinner.release(s);
+    ddmin.release(s);
+    dscale.release(s);
+    finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
+  }
+
+  // Read back ranks and sk/rd lists (the level's one synchronization), then
+  // retire rd on the host, register the delta blocks and the solve records.
+  void finish_skeleton_level(const std::vector<SkelTask>& tasks, int64_t idx_level_start, double tag, LevelRec& L,
+                             double tp) {
+    (void)tag;
+    const int64_t nt = (int64_t)tasks.size();
     std::vector<int32_t> k((size_t)nt);
     HCK(cudaMemcpyAsync(k.data(), kout.p, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     // read back the sk/rd lists written by the kernels: one copy of this
@@ -990,12 +1061,6 @@ struct Factorizer {
     HTRACE("  readback done");
     L.t_sync = now_s() - tp;
     tp = now_s();
-    dt.release(s);
-    dth.release(s);
-    dhuge.release(s);
-    dinner.release(s);
-    ddmin.release(s);
-    dscale.release(s);
     for (int64_t t = 0; t < nt; ++t) {
       const SkelTask& T = tasks[(size_t)t];
       const int kk = k[(size_t)t], r = T.nc - kk;
@@ -1556,7 +1621,7 @@ void hifde_default_options(hifde_options_t* o, int variant) {
   o->skip_levels = variant == HIFDE_VARIANT_HIFDE3X ? 1 : 0;
   o->spd = 1;
   o->order_mode = HIFDE_ORDER_AUTO;
-  o->exact_max_groups = 32;
+  o->exact_max_batches = 64;
   o->device = 0;
   o->eps = 0.0;
 }
@@ -1624,7 +1689,7 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
       fz.opt.skip_levels = nlevels;  // factor_mf == factor_hifde(skip_levels=L)
       fz.opt.eps = 0.0;
     }
-    if (fz.opt.exact_max_groups <= 0) fz.opt.exact_max_groups = 32;
+    if (fz.opt.exact_max_batches <= 0) fz.opt.exact_max_batches = 64;
     fz.F = F.get();
     fz.F_ = F.get();
     fz.s = F->stream;

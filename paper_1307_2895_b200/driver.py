@@ -142,7 +142,7 @@ class GeneralizedLDL:
 
 
 def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
-            order: str = "auto", exact_max_groups: int = 32, device: int = 0,
+            order: str = "auto", exact_max_batches: int = 64, device: int = 0,
             stream: Optional[int] = None) -> GeneralizedLDL:
     lib = L.load()
     if not spd:
@@ -157,7 +157,7 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     opt.spd = 1
     opt.eps = float(eps)
     opt.order_mode = L.ORDER[order]
-    opt.exact_max_groups = int(exact_max_groups)
+    opt.exact_max_batches = int(exact_max_batches)
     opt.device = int(device)
     opt.verify = int(bool(verify))
     opt.stream = stream
