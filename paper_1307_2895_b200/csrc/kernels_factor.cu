@@ -326,8 +326,16 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
 //   The Householder vectors are never needed again (only R), so they are not
 //   even scaled into place.
 // ---------------------------------------------------------------------------
-template <int NT>
-__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem) {
+struct NoWait {
+  __device__ void operator()() const {}
+};
+
+// One skeletonization group.  The front is assembled assuming every neighbour
+// row is alive, then `wait()` runs (exact order: until the earlier
+// neighbouring groups are done), then rows of DOFs retired meanwhile are
+// zeroed -- so the assembly is off the dependency chain's critical path.
+template <int NT, class Wait>
+__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem, const Wait& wait) {
   constexpr int NW = NT / 32;
   __shared__ double red[NW];
   __shared__ double sh_beta, sh_tau, sh_scal;
@@ -374,7 +382,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   for (int i = threadIdx.x; i < nf; i += NT) {
     const int g = gd[i];
     sdofs[i] = g;
-    salive[i] = (i < nc) ? 1 : (int)__ldcg(A.active + g);  // written by other CTAs
+    salive[i] = 1;
   }
   for (int i = threadIdx.x; i < nc; i += NT) perm[i] = i;
   for (int e = threadIdx.x; e < nc * nc; e += NT) Acc[e] = 0.0;
@@ -411,6 +419,17 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     }
     __syncthreads();
   }
+
+  wait();
+  __syncthreads();
+  // rows of DOFs retired by earlier groups (written by other CTAs)
+  for (int i = nc + threadIdx.x; i < nf; i += NT) {
+    if (!__ldcg(A.active + sdofs[i])) {
+      salive[i] = 0;
+      for (int j = 0; j < nc; ++j) Mq[(size_t)(i - nc) + (size_t)j * ldq] = 0.0;
+    }
+  }
+  __syncthreads();
 
   // ---- CPQR of Mq ------------------------------------------------------
   int nq_alive = 0;
@@ -617,7 +636,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ tasks, Arenas A, double eps) {
   extern __shared__ __align__(16) unsigned char smem[];
   const SkelTask t = tasks[blockIdx.x];
-  skel_group<NT>(t, A, eps, smem);
+  skel_group<NT>(t, A, eps, smem, NoWait{});
 }
 
 // Exact (reference) order in one launch: co-resident CTAs walk the groups in
@@ -634,15 +653,16 @@ __global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __rest
                                                           int* __restrict__ done, Arenas A, double eps) {
   extern __shared__ __align__(16) unsigned char smem[];
   for (int j = blockIdx.x; j < ntasks; j += gridDim.x) {
-    if (threadIdx.x == 0) {
-      for (int64_t p = pred_ptr[j]; p < pred_ptr[j + 1]; ++p) {
-        cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[p]]);
-        while (f.load(cuda::memory_order_acquire) == 0) __nanosleep(64);
-      }
-    }
-    __syncthreads();
     const SkelTask t = tasks[j];
-    skel_group<NT>(t, A, eps, smem);
+    auto wait = [&]() {
+      if (threadIdx.x == 0) {
+        for (int64_t p = pred_ptr[j]; p < pred_ptr[j + 1]; ++p) {
+          cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[p]]);
+          while (f.load(cuda::memory_order_acquire) == 0) __nanosleep(32);
+        }
+      }
+    };
+    skel_group<NT>(t, A, eps, smem, wait);
     __syncthreads();
     const int k = A.kout[t.group];
     const int32_t* out = A.idx + t.out_off;
