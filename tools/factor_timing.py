@@ -14,6 +14,8 @@ for r in range(reps):
     f = fac(a, g, eps)
     dt = time.perf_counter() - t
     ts.append(dt)
+    print(f"  rep {r}: wall {dt*1e3:8.2f} ms  gpu-sum {sum(d['gpu_seconds'] for d in f.level_info)*1e3:8.2f} ms  "
+          f"level-wall-sum {sum(d['seconds'] for d in f.level_info)*1e3:8.2f}", flush=True)
     if r > 0 and dt < best_t:
         best_t, best = dt, f.level_info
     f.close()
