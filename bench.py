@@ -23,6 +23,8 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # before torch / libgomp initialize
 import subprocess
 import sys
 import threading

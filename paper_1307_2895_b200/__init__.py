@@ -5,6 +5,10 @@ apply_inverse sweep) runs in hand-written sm_100a CUDA kernels in
 ``libhifde_gpu.so``; this package is the thin Python face of its C ABI.
 """
 
+import os as _os
+
+_os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # before libgomp initializes
+
 from .driver import (FactorizationError, GeneralizedLDL, IndefiniteBlockError,
                      SingularBlockError, apply_inverse, device_count, factor_hifde,
                      factor_hifde3x, factor_mf)

@@ -79,6 +79,9 @@ def load(path: str | None = None):
     if _lib is not None and path is None:
         return _lib
     p = path or LIB
+    # the host symbolic phase uses OpenMP between GPU launches: idle workers
+    # must sleep, not spin (spinning libgomp workers starve the host thread)
+    os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
     if not os.path.exists(p):
         raise RuntimeError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(p)

@@ -519,7 +519,8 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       double nv = vn1[j];
       bool recompute = false;
       if (nv != 0.0) {
-        double tmp = fabs(col[i]) / nv;
+        const double inv = 1.0 / nv;
+        double tmp = fabs(col[i]) * inv;
         tmp = 1.0 - tmp * tmp;
         tmp = tmp > 0.0 ? tmp : 0.0;
         const double ratio = nv / vn2[j];
@@ -655,11 +656,10 @@ __global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __rest
   for (int j = blockIdx.x; j < ntasks; j += gridDim.x) {
     const SkelTask t = tasks[j];
     auto wait = [&]() {
-      if (threadIdx.x == 0) {
-        for (int64_t p = pred_ptr[j]; p < pred_ptr[j + 1]; ++p) {
-          cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[p]]);
-          while (f.load(cuda::memory_order_acquire) == 0) __nanosleep(32);
-        }
+      // one thread per predecessor polls its flag
+      for (int64_t p = pred_ptr[j] + threadIdx.x; p < pred_ptr[j + 1]; p += NT) {
+        cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[p]]);
+        while (f.load(cuda::memory_order_acquire) == 0) __nanosleep(32);
       }
     };
     skel_group<NT>(t, A, eps, smem, wait);
