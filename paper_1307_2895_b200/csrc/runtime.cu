@@ -918,7 +918,7 @@ struct Factorizer {
       kout.bump((size_t)nt, s);
       Arenas A = arenas();
       A.status = status.p + st_off;
-      const int nthr = (max_nc > 48 || max_nq > 256) ? 512 : 128;
+      const int nthr = (max_nc > 32 || max_nq > 128) ? 512 : 128;
       const int cap = skel_ordered_capacity(smem, nthr);
       if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
       const int grid = (int)std::min<int64_t>(nt, cap);
