@@ -30,7 +30,9 @@ struct SkelTask {
   int64_t delta_off;        // block arena: delta block (k x k)
   int64_t out_off;          // idx arena: sk (ascending) then rd (ascending), global ids
   int32_t group;            // index of the group within its level
-  int32_t mode;             // workspace placement: 0 shared, 1 Mq shared, 2 global
+  int32_t mode;             // workspace: 0 shared, 1 Mq shared, 3 Mq global + TSQR, 2 large path
+  int32_t chunk;            // mode 3: Mq rows per TSQR chunk
+  int32_t pad2;
 };
 
 // Skeletonization of a group too large for one CTA (kernels_skelbig.cu).
@@ -109,6 +111,10 @@ void launch_panel_update(const ElimTask* tasks, const int4* work, int nwork, int
 void launch_big_finish(const ElimTask* tasks, int ncells, const Arenas& A, const double* dmin,
                        const double* diag_scale, cudaStream_t s);
 void launch_big_inverse(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
+constexpr int kInvLocalCols = 320;  // cells up to this nc: thread-per-column packed inverse
+void launch_inv_diag(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
+void launch_inv_tiles(const ElimTask* tasks, const int4* work, int nwork, int p0, const Arenas& A,
+                      cudaStream_t s);
 void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
                         cudaStream_t s);
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,

@@ -30,6 +30,7 @@ namespace {
 
 constexpr double kSingularRtol = 1e-14;  // src/dense.py:38
 constexpr int PB = kPanelB;               // panel width
+constexpr int kInvLocal = kInvLocalCols;     // packed-inverse columns kept in local memory
 
 __device__ __forceinline__ int bsearch_i32(const int32_t* s, int n, int32_t key) {
   int lo = 0, hi = n;
@@ -375,23 +376,151 @@ __global__ void __launch_bounds__(128) big_inverse_kernel(const ElimTask* __rest
   if (j >= nc) return;
   const double* C = A.fac + t.C_off;
   double* P = A.fac + t.P_off;
-  P[(size_t)j * (j + 1) / 2 + j] = 1.0 / C[(size_t)j * nc + j];
-  for (int i = j + 1; i < nc; ++i) {
-    const double* ci = C + (size_t)i * nc;
-    double s0 = 0.0, s1 = 0.0;
-    int l = j;
-    for (; l + 1 < i; l += 2) {
-      s0 += ci[l] * P[(size_t)l * (l + 1) / 2 + j];
-      s1 += ci[l + 1] * P[(size_t)(l + 1) * (l + 2) / 2 + j];
+  if (nc <= kInvLocal) {
+    // the column lives in (L1-cached, thread-private) local memory
+    double x[kInvLocal];
+    x[j] = 1.0 / C[(size_t)j * nc + j];
+    P[(size_t)j * (j + 1) / 2 + j] = x[j];
+    for (int i = j + 1; i < nc; ++i) {
+      const double* ci = C + (size_t)i * nc;
+      double s0 = 0.0, s1 = 0.0;
+      int l = j;
+      for (; l + 1 < i; l += 2) {
+        s0 += ci[l] * x[l];
+        s1 += ci[l + 1] * x[l + 1];
+      }
+      if (l < i) s0 += ci[l] * x[l];
+      x[i] = -(s0 + s1) / ci[i];
+      P[(size_t)i * (i + 1) / 2 + j] = x[i];
     }
-    if (l < i) s0 += ci[l] * P[(size_t)l * (l + 1) / 2 + j];
-    P[(size_t)i * (i + 1) / 2 + j] = -(s0 + s1) / ci[i];
+    return;
   }
+  // larger cells take the blocked path (inv_diag_kernel / inv_tile_kernel)
+}
+
+// ---------------------------------------------------------------------------
+// Blocked packed inverse P = C^-1 for large cells (nc > kInvLocal), right-
+// looking over 64-wide panels.  P(i, j) lives at P[i(i+1)/2 + j], j <= i.
+//   inv_diag_kernel:  P_pp = C_pp^-1 for every panel at once (1 CTA each);
+//   inv_tile_kernel, panel p, work {cell, kind, i0, j0}:
+//     kind 0 (j0 < p0):  P_pj := P_pp * S_pj,   S_pj accumulated in place;
+//     kind 1 (i0 > p0):  P_ij := [P_ij] - C_ip * P_pj   (assign when j0 == p0).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(64) inv_diag_kernel(const ElimTask* __restrict__ tasks,
+                                                      const int4* __restrict__ work, Arenas A) {
+  __shared__ double L[PB][PB + 1];
+  const int4 w = work[blockIdx.x];
+  if (A.status[w.x] != 0) return;
+  const ElimTask t = tasks[w.x];
+  const int nc = t.nc, p0 = w.y;
+  if (p0 >= nc) return;  // planned on an upper bound of nc (large skeleton groups)
+  const int pw = min(PB, nc - p0);
+  const double* C = A.fac + t.C_off;
+  double* P = A.fac + t.P_off;
+  for (int e = threadIdx.x; e < pw * pw; e += 64) {
+    const int i = e / pw, j = e - i * pw;
+    L[i][j] = j <= i ? C[(size_t)(p0 + i) * nc + p0 + j] : 0.0;
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j >= pw) return;
+  double x[PB];  // column j of the inverse (thread-private)
+  x[j] = 1.0 / L[j][j];
+  P[(size_t)(p0 + j) * (p0 + j + 1) / 2 + p0 + j] = x[j];
+  for (int i = j + 1; i < pw; ++i) {
+    double s0 = 0.0;
+    for (int l = j; l < i; ++l) s0 += L[i][l] * x[l];
+    x[i] = -s0 / L[i][i];
+    P[(size_t)(p0 + i) * (p0 + i + 1) / 2 + p0 + j] = x[i];
+  }
+}
+
+__global__ void __launch_bounds__(128) inv_tile_kernel(const ElimTask* __restrict__ tasks,
+                                                       const int4* __restrict__ work, int p0, Arenas A) {
+  __shared__ double As[kKs][kLd];
+  __shared__ double Bs[kKs][kLd];
+  const int4 w = work[blockIdx.x];
+  if (A.status[w.x] != 0) return;
+  const ElimTask t = tasks[w.x];
+  const int nc = t.nc;
+  const bool upd = w.y == 1;
+  const int i0 = w.z, j0 = w.w;
+  if (p0 >= nc || (upd && i0 >= nc)) return;
+  const int pw = min(PB, nc - p0);
+  const double* C = A.fac + t.C_off;
+  double* P = A.fac + t.P_off;
+  auto pk = [](int i, int j) { return (size_t)i * (i + 1) / 2 + j; };
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wy = wid >> 1, wx = wid & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  for (int k0 = 0; k0 < pw; k0 += kKs) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kKs * kT; e += 128) {
+      const int r = e / kKs, kk = e - r * kKs;
+      const int k = p0 + k0 + kk, ra = (upd ? i0 : p0) + r;
+      double a = 0.0;
+      if (k0 + kk < pw && ra < nc) {
+        if (upd) a = C[(size_t)ra * nc + k];                 // C_ip
+        else if (k <= ra) a = P[pk(ra, k)];                  // P_pp (lower)
+      }
+      As[kk][r] = a;
+    }
+    for (int e = threadIdx.x; e < kKs * kT; e += 128) {
+      const int kk = e / kT, c = e - kk * kT;
+      const int k = p0 + k0 + kk, cb = j0 + c;
+      Bs[kk][c] = (k0 + kk < pw && cb <= k) ? P[pk(k, cb)] : 0.0;  // S_pj / P_pj
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kKs; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = As[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bf[n] = Bs[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+    }
+  }
+  __syncthreads();  // kind 0 overwrites its own B operand
+  const int r0 = upd ? i0 : p0;
+  const bool first = j0 == p0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = r0 + wy * 32 + m * 8 + (lane >> 2);
+        const int b = j0 + wx * 32 + n * 8 + 2 * (lane & 3) + h;
+        if (a >= nc || b >= j0 + kT || b > a) continue;
+        if (!upd) {
+          if (b < p0) P[pk(a, b)] = acc[m][n][h];
+        } else {
+          const double old = first ? 0.0 : P[pk(a, b)];
+          P[pk(a, b)] = old - acc[m][n][h];
+        }
+      }
 }
 
 // ---------------------------------------------------------------------------
 void launch_big_inverse(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
   if (nwork > 0) big_inverse_kernel<<<nwork, 128, 0, s>>>(tasks, work, A);
+}
+
+void launch_inv_diag(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
+  if (nwork > 0) inv_diag_kernel<<<nwork, 64, 0, s>>>(tasks, work, A);
+}
+
+void launch_inv_tiles(const ElimTask* tasks, const int4* work, int nwork, int p0, const Arenas& A,
+                      cudaStream_t s) {
+  if (nwork > 0) inv_tile_kernel<<<nwork, 128, 0, s>>>(tasks, work, p0, A);
 }
 
 void launch_big_assemble(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A,

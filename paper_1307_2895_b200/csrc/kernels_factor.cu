@@ -364,6 +364,12 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     vn2 = vn1 + nc;
     Acc = wgl;
     Z = Acc + (size_t)nc * nc;
+  } else if (t.mode == 3) {  // Mq in global, compressed to its R factor in shared memory
+    Acc = wgl;
+    Mq = Acc + (size_t)nc * nc;
+    Z = Mq + (size_t)nq * nc;
+    vn1 = wsh + (size_t)(nc + t.chunk) * nc;
+    vn2 = vn1 + nc;
   } else {
     double* ws = t.mode == 0 ? wsh : wgl;
     Acc = ws;                                          // nc x nc, row-major (symmetric)
@@ -431,6 +437,63 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   }
   __syncthreads();
 
+  // ---- mode 3: R factor of Mq by chunked Householder QR in shared memory --
+  int nqm = nq, ldm = ldq;
+  if (t.mode == 3) {
+    const int h = t.chunk, lds = nc + h;
+    double* S = wsh;
+    for (int e = threadIdx.x; e < lds * nc; e += NT) S[e] = 0.0;
+    for (int r0 = 0; r0 < nq; r0 += h) {
+      const int hh = min(h, nq - r0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < h * nc; e += NT) {
+        const int j = e / h, rr = e - j * h;
+        S[nc + rr + (size_t)j * lds] = rr < hh ? Mq[(size_t)(r0 + rr) + (size_t)j * ldq] : 0.0;
+      }
+      __syncthreads();
+      for (int i = 0; i < nc; ++i) {
+        // x = [S_ii ; chunk rows of column i]; the R rows below i are zero
+        if (wid == 0) {
+          const double* ci = S + (size_t)i * lds;
+          double xs = 0.0;
+          for (int r = nc + lane; r < nc + h; r += 32) xs += ci[r] * ci[r];
+          const double xnorm = sqrt(warp_sum(xs));
+          const double alpha = ci[i];
+          double beta, tau, scal;
+          if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
+          else {
+            beta = -copysign(hypot(alpha, xnorm), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+          }
+          if (lane == 0) { sh_beta = beta; sh_tau = tau; sh_scal = scal; }
+        }
+        __syncthreads();
+        const double tau = sh_tau, scal = sh_scal;
+        const double* v = S + (size_t)i * lds;
+        if (tau != 0.0) {
+          for (int j = i + 1 + wid; j < nc; j += NW) {
+            double* col = S + (size_t)j * lds;
+            double s2 = 0.0;
+            for (int r = nc + lane; r < nc + h; r += 32) s2 += v[r] * col[r];
+            s2 = warp_sum(s2);
+            const double w = tau * (col[i] + scal * s2);
+            __syncwarp();
+            if (lane == 0) col[i] -= w;
+            const double ws2 = w * scal;
+            for (int r = nc + lane; r < nc + h; r += 32) col[r] -= ws2 * v[r];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) S[i + (size_t)i * lds] = sh_beta;
+      }
+    }
+    __syncthreads();
+    Mq = S;      // the CPQR runs on R (nc x nc, column-major, ld lds)
+    nqm = nc;
+    ldm = lds;
+  }
+
   // ---- CPQR of Mq ------------------------------------------------------
   int nq_alive = 0;
   if (threadIdx.x == 0) {
@@ -439,14 +502,14 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   }
   for (int j = wid; j < nc; j += NW) {
     double s = 0.0;
-    const double* col = Mq + (size_t)j * ldq;
-    for (int r = lane; r < nq; r += 32) s += col[r] * col[r];
+    const double* col = Mq + (size_t)j * ldm;
+    for (int r = lane; r < nqm; r += 32) s += col[r] * col[r];
     s = warp_sum(s);
     if (lane == 0) { vn1[j] = sqrt(s); vn2[j] = vn1[j]; }
   }
   __syncthreads();
   nq_alive = sh_k;
-  const int kmax = nq < nc ? nq : nc;
+  const int kmax = nqm < nc ? nqm : nc;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);  // sqrt(dlamch('E'))
   double thr = 0.0;
   int k = kmax;
@@ -470,9 +533,9 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       if (i == 0 && vn1[pvt] == 0.0) stop = 2;  // zero block: everything redundant
       if (!stop) {
         if (pvt != i) {
-          double* ci = Mq + (size_t)i * ldq;
-          double* cp = Mq + (size_t)pvt * ldq;
-          for (int r = lane; r < nq; r += 32) { const double x = ci[r]; ci[r] = cp[r]; cp[r] = x; }
+          double* ci = Mq + (size_t)i * ldm;
+          double* cp = Mq + (size_t)pvt * ldm;
+          for (int r = lane; r < nqm; r += 32) { const double x = ci[r]; ci[r] = cp[r]; cp[r] = x; }
           if (lane == 0) {
             const int pi = perm[i]; perm[i] = perm[pvt]; perm[pvt] = pi;
             vn1[pvt] = vn1[i];
@@ -480,9 +543,9 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
           }
         }
         __syncwarp();
-        const double* ci = Mq + (size_t)i * ldq;
+        const double* ci = Mq + (size_t)i * ldm;
         double xs = 0.0;
-        for (int r = i + 1 + lane; r < nq; r += 32) xs += ci[r] * ci[r];
+        for (int r = i + 1 + lane; r < nqm; r += 32) xs += ci[r] * ci[r];
         const double xnorm = sqrt(warp_sum(xs));
         const double alpha = ci[i];
         double beta, tau, scal;
@@ -502,18 +565,18 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     __syncthreads();
     if (sh_stop) { k = sh_stop == 2 ? 0 : i; break; }
     const double tau = sh_tau, scal = sh_scal;
-    const double* v = Mq + (size_t)i * ldq;  // v_r = scal * v[r] for r > i
+    const double* v = Mq + (size_t)i * ldm;  // v_r = scal * v[r] for r > i
     for (int j = i + 1 + wid; j < nc; j += NW) {
-      double* col = Mq + (size_t)j * ldq;
+      double* col = Mq + (size_t)j * ldm;
       if (tau != 0.0) {
         double s = 0.0;
-        for (int r = i + 1 + lane; r < nq; r += 32) s += v[r] * col[r];
+        for (int r = i + 1 + lane; r < nqm; r += 32) s += v[r] * col[r];
         s = warp_sum(s);
         const double w = tau * (col[i] + scal * s);
         __syncwarp();
         if (lane == 0) col[i] -= w;
         const double ws2 = w * scal;
-        for (int r = i + 1 + lane; r < nq; r += 32) col[r] -= ws2 * v[r];
+        for (int r = i + 1 + lane; r < nqm; r += 32) col[r] -= ws2 * v[r];
         __syncwarp();
       }
       double nv = vn1[j];
@@ -529,14 +592,14 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       }
       if (recompute) {
         double s = 0.0;
-        for (int r = i + 1 + lane; r < nq; r += 32) s += col[r] * col[r];
+        for (int r = i + 1 + lane; r < nqm; r += 32) s += col[r] * col[r];
         s = warp_sum(s);
-        nv = (i + 1 < nq) ? sqrt(s) : 0.0;
+        nv = (i + 1 < nqm) ? sqrt(s) : 0.0;
         if (lane == 0) vn2[j] = nv;
       }
       if (lane == 0) vn1[j] = nv;
     }
-    if (threadIdx.x == 0) Mq[i + (size_t)i * ldq] = sh_beta;  // R_ii (column i no longer read)
+    if (threadIdx.x == 0) Mq[i + (size_t)i * ldm] = sh_beta;  // R_ii (column i no longer read)
     __syncthreads();
   }
   __syncthreads();
@@ -544,11 +607,11 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
 
   // T = R11^-1 R12 (back substitution, one thread per column of R12)
   for (int j = threadIdx.x; j < r; j += NT) {
-    double* col = Mq + (size_t)(k + j) * ldq;
+    double* col = Mq + (size_t)(k + j) * ldm;
     for (int i = k - 1; i >= 0; --i) {
       double s = col[i];
-      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)l * ldq] * col[l];
-      col[i] = s / Mq[i + (size_t)i * ldq];
+      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)l * ldm] * col[l];
+      col[i] = s / Mq[i + (size_t)i * ldm];
     }
   }
   // ascending sk / rd with their pivot positions
@@ -576,7 +639,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   }
   for (int e = threadIdx.x; e < k * r; e += NT) {
     const int a = e / r, b = e - a * r;
-    Ts[e] = Mq[sko[a] + (size_t)(k + rdo[b]) * ldq];
+    Ts[e] = Mq[sko[a] + (size_t)(k + rdo[b]) * ldm];
   }
   __syncthreads();
   // B_sr = A_sr - A_ss T

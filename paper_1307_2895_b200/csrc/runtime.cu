@@ -145,6 +145,67 @@ struct DBuf {
   }
 };
 
+// Packed-inverse work of a batch of cells (kernels_big.cu): thread-per-column
+// for nc <= kInvLocalCols, blocked diagonal-inverse + DMMA tiles above.
+struct InvPlan {
+  std::vector<int4> loc, diag, tiles;
+  std::vector<int64_t> off;  // tiles of panel p: kind 0 [off[2p], off[2p+1]), kind 1 up to off[2p+2]
+  DBuf<int4> d_loc, d_diag, d_tiles;
+  void build(const std::vector<int>& ncs) {
+    int maxnc = 0;
+    for (int i = 0; i < (int)ncs.size(); ++i) {
+      const int nc = ncs[(size_t)i];
+      if (nc <= kInvLocalCols) {
+        for (int c0 = 0; c0 < nc; c0 += 128) loc.push_back(make_int4(i, c0, 0, 0));
+      } else {
+        maxnc = std::max(maxnc, nc);
+        for (int p0 = 0; p0 < nc; p0 += kPanelB) diag.push_back(make_int4(i, p0, 0, 0));
+      }
+    }
+    const int np = (maxnc + kPanelB - 1) / kPanelB;
+    off.assign((size_t)2 * np + 1, 0);
+    for (int p = 0; p < np; ++p) {
+      const int p0 = p * kPanelB;
+      for (int kind = 0; kind < 2; ++kind) {
+        for (int i = 0; i < (int)ncs.size(); ++i) {
+          const int nc = ncs[(size_t)i];
+          if (nc <= kInvLocalCols || p0 >= nc) continue;
+          if (kind == 0) {
+            for (int j0 = 0; j0 < p0; j0 += kPanelB) tiles.push_back(make_int4(i, 0, p0, j0));
+          } else {
+            for (int i0 = p0 + kPanelB; i0 < nc; i0 += kPanelB)
+              for (int j0 = 0; j0 <= p0; j0 += kPanelB) tiles.push_back(make_int4(i, 1, i0, j0));
+          }
+        }
+        off[(size_t)2 * p + kind + 1] = (int64_t)tiles.size();
+      }
+    }
+  }
+  void upload(cudaStream_t s) {
+    for (auto pr : {std::make_pair(&d_loc, &loc), std::make_pair(&d_diag, &diag), std::make_pair(&d_tiles, &tiles)}) {
+      pr.first->reserve(pr.second->size(), s);
+      pr.first->upload(pr.second->data(), 0, pr.second->size(), s);
+    }
+  }
+  int launch(const ElimTask* tasks, const Arenas& A, cudaStream_t s) {
+    int nl = 0;
+    if (!loc.empty()) { launch_big_inverse(tasks, d_loc.p, (int)loc.size(), A, s); ++nl; }
+    if (!diag.empty()) { launch_inv_diag(tasks, d_diag.p, (int)diag.size(), A, s); ++nl; }
+    for (size_t q = 0; q + 1 < off.size(); ++q) {
+      const int cnt = (int)(off[q + 1] - off[q]);
+      if (cnt == 0) continue;
+      launch_inv_tiles(tasks, d_tiles.p + off[q], cnt, (int)(q / 2) * kPanelB, A, s);
+      ++nl;
+    }
+    return nl;
+  }
+  void release(cudaStream_t s) {
+    d_loc.release(s);
+    d_diag.release(s);
+    d_tiles.release(s);
+  }
+};
+
 struct LevelRec {
   double tag = 0;
   int kind = 0;  // 0 elimination, 1 skeleton
@@ -631,9 +692,12 @@ struct Factorizer {
       for (int a = 0; a < ntl; ++a)
         for (int b = a; b < ntl; ++b) tiles.push_back(make_int4(bi, a, b, 0));
     }
-    std::vector<int4> inv_work;  // packed inverse: 128 columns per CTA
-    for (int bi = 0; bi < (int)big.size(); ++bi)
-      for (int c0 = 0; c0 < big[(size_t)bi].nc; c0 += 128) inv_work.push_back(make_int4(bi, c0, 0, 0));
+    InvPlan inv;  // packed inverses of the big cells
+    {
+      std::vector<int> ncs;
+      for (const ElimTask& T : big) ncs.push_back(T.nc);
+      inv.build(ncs);
+    }
     // per-panel work lists of the blocked Cholesky / TRSM
     const int npanel = (max_big_nc + kPanelB - 1) / kPanelB;
     std::vector<int32_t> pcells;
@@ -665,7 +729,7 @@ struct Factorizer {
     lists.n = hl.size();
     lists.upload(hl.data(), 0, hl.size(), s);
     DBuf<ElimTask> d_small, d_big;
-    DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd, d_inv;
+    DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd;
     DBuf<int32_t> d_pcells;
     DBuf<double> d_dmin, d_scale;
     auto up4 = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
@@ -677,7 +741,7 @@ struct Factorizer {
     up4(d_asm, asm_work);
     up4(d_ptrsm, ptrsm);
     up4(d_pupd, pupd);
-    up4(d_inv, inv_work);
+    inv.upload(s);
     d_pcells.reserve(pcells.size(), s);
     d_pcells.upload(pcells.data(), 0, pcells.size(), s);
     if (!big.empty()) {
@@ -721,8 +785,7 @@ struct Factorizer {
         ++g_launches;
       }
       launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
-      launch_big_inverse(d_big.p, d_inv.p, (int)inv_work.size(), A, s);
-      g_launches += 2;
+      g_launches += 1 + inv.launch(d_big.p, A, s);
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
@@ -738,7 +801,7 @@ struct Factorizer {
     d_asm.release(s);
     d_ptrsm.release(s);
     d_pupd.release(s);
-    d_inv.release(s);
+    inv.release(s);
     d_pcells.release(s);
     d_dmin.release(s);
     d_scale.release(s);
@@ -835,6 +898,8 @@ struct Factorizer {
       T.nblk = f.nb;
       T.maxnb = f.maxnb;
       T.group = (int32_t)t;
+      T.chunk = 0;
+      T.pad2 = 0;
       T.dofs_off = (int64_t)h_idx.size();
       h_idx.insert(h_idx.end(), c, c + nc);
       h_idx.insert(h_idx.end(), q, q + nq);
@@ -856,6 +921,15 @@ struct Factorizer {
         T.mode = 1;
         T.scratch_off = (int64_t)scratch.bump(3 * (size_t)nc * nc + 3 * q4 + 8, s);
         smem = std::max(smem, ib + sizeof(double) * mq);
+      } else if (nq > nc && nc <= 160 && !getenv("HIFDE_NO_TSQR") &&
+                 ib + sizeof(double) * ((size_t)(2 * nc) * nc + 2 * (size_t)nc) <= kSmemCap) {
+        // Mq in global scratch, compressed to R (nc x nc) in shared memory by
+        // chunked Householder QR: column norms and pivots are unchanged
+        T.mode = 3;
+        const size_t avail = (kSmemCap - ib) / sizeof(double) - 2 * (size_t)nc;
+        T.chunk = (int32_t)std::min<size_t>(avail / nc - nc, (size_t)nq);
+        T.scratch_off = (int64_t)scratch.bump(wsd + 8, s);
+        smem = std::max(smem, ib + sizeof(double) * ((size_t)(nc + T.chunk) * nc + 2 * (size_t)nc));
       } else {
         T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
         T.scratch_off = -1;
@@ -1108,7 +1182,13 @@ struct Factorizer {
     double* dscale = d_scale_all + lo;
     Arenas AH = AH_all;
     AH.status = AH_all.status + lo;
-    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles, wrow, wtu, winv;
+    std::vector<int4> wasm, wt, wc0, wc1, wsym, pt, pu, tiles, wrow, wtu;
+    InvPlan inv;
+    {
+      std::vector<int> ncs;
+      for (int i = 0; i < n; ++i) ncs.push_back(huge[(size_t)(lo + i)].nc);
+      inv.build(ncs);
+    }
     std::vector<int32_t> pc;
     int maxnc = 0;
     for (int i = 0; i < n; ++i) maxnc = std::max(maxnc, huge[(size_t)(lo + i)].nc);
@@ -1120,7 +1200,6 @@ struct Factorizer {
       for (int r0 = 0; r0 < nf; r0 += 64) wasm.push_back(make_int4(i, r0, std::min(r0 + 64, nf), 0));
       for (int c0 = 0; c0 < nc; c0 += 128) wt.push_back(make_int4(i, c0, 0, 0));
       for (int r0 = 0; r0 < nc; r0 += 64) wrow.push_back(make_int4(i, r0, 0, 0));
-      for (int c0 = 0; c0 < nc; c0 += 128) winv.push_back(make_int4(i, c0, 0, 0));
       for (int a0 = 0; a0 < nc; a0 += 64)
         for (int b0 = 0; b0 < nc; b0 += 64) {
           wc0.push_back(make_int4(i, 0, a0, b0));
@@ -1164,11 +1243,12 @@ struct Factorizer {
       }
       tuo[(size_t)bb + 1] = (int64_t)wtu.size();
     }
-    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8, d10, d11, d12;
+    DBuf<int4> d1, d2, d3, d4, d5, d6, d7, d8, d10, d11;
     DBuf<int32_t> d9;
     auto up = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
     up(d1, wasm); up(d2, wt); up(d3, wc0); up(d4, wc1); up(d5, wsym); up(d6, pt); up(d7, pu); up(d8, tiles);
-    up(d10, wrow); up(d11, wtu); up(d12, winv);
+    up(d10, wrow); up(d11, wtu);
+    inv.upload(s);
     d9.reserve(pc.size(), s);
     d9.upload(pc.data(), 0, pc.size(), s);
     for (int i = 0; i < n; ++i) {
@@ -1235,11 +1315,17 @@ struct Factorizer {
     }
     launch_schur_tiles(inner, d8.p, (int)tiles.size(), AH, s);
     launch_big_finish(inner, n, AH, dmin, dscale, s);
-    launch_big_inverse(inner, d12.p, (int)winv.size(), AH, s);
+    if (trace_on()) {
+      HCK(cudaStreamSynchronize(s));
+      HTRACE("    huge: factor done (%d groups)", n);
+    }
+    g_launches += inv.launch(inner, AH, s);
+    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("    huge: inverse done (%zu loc / %zu diag / %zu tiles)", inv.loc.size(), inv.diag.size(), inv.tiles.size()); }
     launch_apply_rd(d_skv + lo, n, A, s);
-    g_launches += 4;
+    g_launches += 3;
     HCK(cudaGetLastError());
-    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11, &d12}) d->release(s);
+    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(s);
+    inv.release(s);
     d9.release(s);
   }
 

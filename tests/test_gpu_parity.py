@@ -110,6 +110,19 @@ def test_mf_top_separator_count():
     assert f.metrics["s_top"] == f.metrics["active_trace"][-1][1]
 
 
+@pytest.mark.parametrize("dim,n,m", [(2, 256, 8), (3, 16, 2), (3, 24, 3)])
+def test_mf_large_top_cell_blocked_inverse(dim, n, m):
+    """Top cells wider than the thread-per-column inverse limit (320) take the
+    blocked packed inverse (ragged last panel included); MF stays exact."""
+    g = H.build_grid(dim, n, m)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=1))
+    f = H.factor_mf(a, g)
+    assert f.metrics["s_top"] > 320
+    b = np.random.default_rng(0).standard_normal((g.ndof, 2))
+    x = f.apply_inverse(b)
+    assert np.max(np.linalg.norm(a @ x - b, axis=0) / np.linalg.norm(b, axis=0)) <= 1e-10
+
+
 def test_single_dof_grid():
     g = H.GridConfig(dim=2, n=2, m=2, nlevels=0, h=0.5)
     a = H.assemble(g, H.constant_field(g))
