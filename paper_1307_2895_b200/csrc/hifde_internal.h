@@ -91,11 +91,13 @@ struct Arenas {
   int* status;              // per-task status words
   int32_t* kout;            // per-group skeleton rank
   int32_t* iscratch;        // per-level integer scratch
+  unsigned long long* tlog; // optional per-group timestamps (HIFDE_SKEL_TLOG), else null
 };
 
 constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA we use
 constexpr int kSchurTile = 64;                 // schur_tile_kernel tile edge
 constexpr int kPanelB = 64;                    // blocked Cholesky panel width
+constexpr int kMaxSkelNc = 192;                // largest group skeletonized by one CTA (skel_group)
 
 // Kernel launchers (kernels_factor.cu / kernels_solve.cu).
 void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,

@@ -51,6 +51,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// sum over aligned groups of G lanes (G a power of two <= 32)
+__device__ __forceinline__ double group_sum(double v, int G) {
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int NT>
 __device__ double block_max(double v, double* red) {
   constexpr int NW = NT / 32;
@@ -329,19 +335,30 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
 struct NoWait {
   __device__ void operator()() const {}
 };
+struct NoPublish {
+  __device__ void operator()(int, const int32_t*, const int32_t*, int) const {}
+};
 
 // One skeletonization group.  The front is assembled assuming every neighbour
 // row is alive, then `wait()` runs (exact order: until the earlier
 // neighbouring groups are done), then rows of DOFs retired meanwhile are
 // zeroed -- so the assembly is off the dependency chain's critical path.
-template <int NT, class Wait>
-__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem, const Wait& wait) {
+template <int NT, class Wait, class Publish = NoPublish>
+__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem, const Wait& wait,
+                           const Publish& publish = Publish{}) {
   constexpr int NW = NT / 32;
   __shared__ double red[NW];
   __shared__ double sh_beta, sh_tau, sh_scal;
-  __shared__ int sh_stop, sh_k;
+  __shared__ int sh_k;
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto mark = [&](int which) {  // debug timestamps (HIFDE_SKEL_TLOG)
+    if (A.tlog && threadIdx.x == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      A.tlog[(size_t)t.group * 16 + which] = g;
+    }
+  };
 
   int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
   int32_t* salive = sdofs + nf;
@@ -351,10 +368,15 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   int32_t* rdl = skl + nc;
   int32_t* sko = rdl + nc;
   int32_t* rdo = sko + nc;
-  const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(2 * nf + t.maxnb + 5 * nc), 16);
+  int32_t* dcol = rdo + nc;                            // column pivoted yet
+  int32_t* cpos = dcol + nc;                           // LAPACK position -> column, x2
+  const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(2 * nf + t.maxnb + 8 * nc), 16);
+  // CPQR vectors (double-buffered norms, next-step Householder norms, R_ii)
+  double* cq = reinterpret_cast<double*>(smem + ibytes);
+  double* rdiag = cq + 4 * nc;                         // vn1 x2 | xn x2 | R_ii
   // workspace placement (host-chosen): 0 all shared; 1 Mq + norms shared,
   // A_cc and the post-CPQR matrices global; 2 all global
-  double* wsh = reinterpret_cast<double*>(smem + ibytes);
+  double* wsh = cq + 5 * nc;
   double* wgl = A.scratch + (t.scratch_off > 0 ? t.scratch_off : 0);
   const int ldq = nq;                                  // Mq column-major, ld nq
   double *Acc, *Mq, *vn1, *vn2, *Z;
@@ -436,6 +458,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     }
   }
   __syncthreads();
+  mark(4);
 
   // ---- mode 3: R factor of Mq by chunked Householder QR in shared memory --
   int nqm = nq, ldm = ldq;
@@ -494,124 +517,210 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     ldm = lds;
   }
 
-  // ---- CPQR of Mq ------------------------------------------------------
+  // ---- CPQR (dgeqp3 pivoting) of the shared-memory matrix Mc ----------
+  // Columns are never moved: every warp tracks the LAPACK column order in
+  // registers (position -> column, identical copies), picks the pivot itself
+  // from the double-buffered partial norms, and the next step's Householder
+  // norm of every candidate is accumulated during the update -- one barrier
+  // per step.
+  double* Mc = t.mode == 0 ? wsh + (size_t)nc * nc : wsh;
+  if (t.mode != 3) { nqm = nq; ldm = ldq; }
   int nq_alive = 0;
   if (threadIdx.x == 0) {
     for (int i = nc; i < nf; ++i) nq_alive += salive[i];
     sh_k = nq_alive;
   }
   for (int j = wid; j < nc; j += NW) {
-    double s = 0.0;
-    const double* col = Mq + (size_t)j * ldm;
-    for (int r = lane; r < nqm; r += 32) s += col[r] * col[r];
-    s = warp_sum(s);
-    if (lane == 0) { vn1[j] = sqrt(s); vn2[j] = vn1[j]; }
+    const double* col = Mc + (size_t)j * ldm;
+    double s1 = 0.0;
+    for (int r = 1 + lane; r < nqm; r += 32) s1 += col[r] * col[r];
+    s1 = warp_sum(s1);                            // rows >= 1
+    const double c0 = nqm > 0 ? col[0] : 0.0;
+    if (lane == 0) {
+      const double nv = sqrt(c0 * c0 + s1);
+      cq[j] = nv;
+      vn2[j] = nv;
+      cq[2 * nc + j] = sqrt(s1);
+      dcol[j] = 0;
+      cpos[j] = j;
+    }
   }
   __syncthreads();
+  mark(5);
   nq_alive = sh_k;
   const int kmax = nqm < nc ? nqm : nc;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);  // sqrt(dlamch('E'))
+  int G = 32;  // lanes per trailing column
+  while (G > 8 && NT / G < nc) G >>= 1;
+  const int nslots = NT / G, sl = lane & (G - 1), slot = wid * (32 / G) + lane / G;
   double thr = 0.0;
   int k = kmax;
+  long long ph[4] = {0, 0, 0, 0}, ph2[3] = {0, 0, 0};
+  long long tc0 = clock64();
   for (int i = 0; i < kmax; ++i) {
-    if (wid == 0) {
-      // pivot: largest partial norm, lowest index on ties (idamax)
-      double bv = -1.0;
-      int bi = nc;
-      for (int j = i + lane; j < nc; j += 32) {
-        const double v = vn1[j];
-        if (v > bv) { bv = v; bi = j; }
-      }
+    const int cur = (i & 1) * nc, nxt = nc - cur;
+    const double* vn1 = cq + cur;
+    double* vn1o = cq + nxt;
+    const double* xn = cq + 2 * nc + cur;
+    double* xno = cq + 2 * nc + nxt;
+    const int32_t* cat = cpos + cur;
+    int32_t* cato = cpos + nxt;
+    // pivot: largest partial norm, lowest position on ties (idamax)
+    double bv = -1.0;
+    int bp = nc, bc = 0;
+    for (int pos = i + lane; pos < nc; pos += 32) {
+      const int c = cat[pos];
+      const double v = vn1[c];
+      if (v > bv) { bv = v; bp = pos; bc = c; }
+    }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bc = oc; }
+    }
+    const int p = bc;
+    if (wid == NW - 1) {  // next position map: LAPACK swaps positions i and bp
+      const int ci = cat[i];
+      for (int pos = lane; pos < nc; pos += 32) cato[pos] = pos == i ? p : (pos == bp ? ci : cat[pos]);
+    }
+    long long tc1 = clock64();
+    ph[0] += tc1 - tc0;
+    if (i == 0 && bv == 0.0) { k = 0; break; }  // zero block: everything redundant
+    const double* v = Mc + (size_t)p * ldm;     // Householder vector: rows > i
+    const double alpha = v[i];
+    const double xnorm = xn[p];
+    double beta, tau, scal;
+    if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
+    else {
+      beta = -copysign(hypot(alpha, xnorm), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    const double rii = fabs(beta);
+    if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
+    if (rii <= thr) { k = i; break; }
+    if (threadIdx.x == 0) { rdiag[i] = beta; dcol[p] = 1; }
+    long long tc2 = clock64();
+    ph[1] += tc2 - tc1;
+    // trailing columns: G lanes per column, NT / G columns at once (the
+    // step's latency is one column's dependency chain, not NW of them)
+    for (int base = 0; base < nc; base += nslots) {
+      const int j = base + slot;
+      const bool act = j < nc && j != p && !dcol[j];
+      double* col = Mc + (size_t)(act ? j : p) * ldm;  // inactive: harmless reads of v
+      double acc = 0.0;                                // sum of squares of rows >= i + 2
+      if (tau != 0.0) {
+        // 4 rows in flight per lane: the loops are load-latency bound
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int r = i + 1 + sl;
+        for (; r + 3 * G < nqm; r += 4 * G) {
+          s0 += v[r] * col[r];
+          s1 += v[r + G] * col[r + G];
+          s2 += v[r + 2 * G] * col[r + 2 * G];
+          s3 += v[r + 3 * G] * col[r + 3 * G];
+        }
+        for (; r < nqm; r += G) s0 += v[r] * col[r];
+        const double sd = group_sum((s0 + s1) + (s2 + s3), G);
+        ph2[0] += clock64() - tc2;
+        const double w = tau * (col[i] + scal * sd);
+        __syncwarp();
+        if (act && sl == 0) col[i] -= w;
+        const double ws2 = w * scal;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        r = i + 1 + sl;
+        if (r == i + 1 && r < nqm) {  // row i + 1: updated, not in the next norm
+          const double x = col[r] - ws2 * v[r];
+          if (act) col[r] = x;
+          r += G;
+        }
+        for (; r + 3 * G < nqm; r += 4 * G) {
+          const double x0 = col[r] - ws2 * v[r];
+          const double x1 = col[r + G] - ws2 * v[r + G];
+          const double x2 = col[r + 2 * G] - ws2 * v[r + 2 * G];
+          const double x3 = col[r + 3 * G] - ws2 * v[r + 3 * G];
+          if (act) {
+            col[r] = x0;
+            col[r + G] = x1;
+            col[r + 2 * G] = x2;
+            col[r + 3 * G] = x3;
+          }
+          a0 += x0 * x0;
+          a1 += x1 * x1;
+          a2 += x2 * x2;
+          a3 += x3 * x3;
+        }
+        for (; r < nqm; r += G) {
+          const double x = col[r] - ws2 * v[r];
+          if (act) col[r] = x;
+          a0 += x * x;
+        }
+        acc = (a0 + a1) + (a2 + a3);
+        ph2[1] += clock64() - tc2;
+      } else {
+        double a0 = 0.0, a1 = 0.0;
+        int r = i + 2 + sl;
+        for (; r + G < nqm; r += 2 * G) {
+          a0 += col[r] * col[r];
+          a1 += col[r + G] * col[r + G];
+        }
+        for (; r < nqm; r += G) a0 += col[r] * col[r];
+        acc = a0 + a1;
       }
-      const int pvt = bi;
-      int stop = 0;
-      if (i == 0 && vn1[pvt] == 0.0) stop = 2;  // zero block: everything redundant
-      if (!stop) {
-        if (pvt != i) {
-          double* ci = Mq + (size_t)i * ldm;
-          double* cp = Mq + (size_t)pvt * ldm;
-          for (int r = lane; r < nqm; r += 32) { const double x = ci[r]; ci[r] = cp[r]; cp[r] = x; }
-          if (lane == 0) {
-            const int pi = perm[i]; perm[i] = perm[pvt]; perm[pvt] = pi;
-            vn1[pvt] = vn1[i];
-            vn2[pvt] = vn2[i];
+      acc = group_sum(acc, G);
+      __syncwarp();
+      ph2[2] += clock64() - tc2;
+      if (act) {
+        const double cn = i + 1 < nqm ? col[i + 1] : 0.0;
+        double nv = vn1[j];
+        if (nv != 0.0) {
+          double tmp = fabs(col[i]) / nv;
+          tmp = 1.0 - tmp * tmp;
+          tmp = tmp > 0.0 ? tmp : 0.0;
+          const double ratio = nv / vn2[j];
+          if (tmp * ratio * ratio <= tol3z) {
+            nv = (i + 1 < nqm) ? sqrt(cn * cn + acc) : 0.0;
+            if (sl == 0) vn2[j] = nv;
+          } else {
+            nv *= sqrt(tmp);
           }
         }
-        __syncwarp();
-        const double* ci = Mq + (size_t)i * ldm;
-        double xs = 0.0;
-        for (int r = i + 1 + lane; r < nqm; r += 32) xs += ci[r] * ci[r];
-        const double xnorm = sqrt(warp_sum(xs));
-        const double alpha = ci[i];
-        double beta, tau, scal;
-        if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
-        else {
-          beta = -copysign(hypot(alpha, xnorm), alpha);
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
-        }
-        const double rii = fabs(beta);
-        if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
-        if (rii <= thr) stop = 1;
-        if (lane == 0) { sh_beta = beta; sh_tau = tau; sh_scal = scal; }
+        if (sl == 0) { vn1o[j] = nv; xno[j] = sqrt(acc); }
       }
-      if (lane == 0) sh_stop = stop;
     }
+    long long tc3 = clock64();
+    ph[2] += tc3 - tc2;
     __syncthreads();
-    if (sh_stop) { k = sh_stop == 2 ? 0 : i; break; }
-    const double tau = sh_tau, scal = sh_scal;
-    const double* v = Mq + (size_t)i * ldm;  // v_r = scal * v[r] for r > i
-    for (int j = i + 1 + wid; j < nc; j += NW) {
-      double* col = Mq + (size_t)j * ldm;
-      if (tau != 0.0) {
-        double s = 0.0;
-        for (int r = i + 1 + lane; r < nqm; r += 32) s += v[r] * col[r];
-        s = warp_sum(s);
-        const double w = tau * (col[i] + scal * s);
-        __syncwarp();
-        if (lane == 0) col[i] -= w;
-        const double ws2 = w * scal;
-        for (int r = i + 1 + lane; r < nqm; r += 32) col[r] -= ws2 * v[r];
-        __syncwarp();
-      }
-      double nv = vn1[j];
-      bool recompute = false;
-      if (nv != 0.0) {
-        const double inv = 1.0 / nv;
-        double tmp = fabs(col[i]) * inv;
-        tmp = 1.0 - tmp * tmp;
-        tmp = tmp > 0.0 ? tmp : 0.0;
-        const double ratio = nv / vn2[j];
-        if (tmp * ratio * ratio <= tol3z) recompute = true;
-        else nv *= sqrt(tmp);
-      }
-      if (recompute) {
-        double s = 0.0;
-        for (int r = i + 1 + lane; r < nqm; r += 32) s += col[r] * col[r];
-        s = warp_sum(s);
-        nv = (i + 1 < nqm) ? sqrt(s) : 0.0;
-        if (lane == 0) vn2[j] = nv;
-      }
-      if (lane == 0) vn1[j] = nv;
-    }
-    if (threadIdx.x == 0) Mq[i + (size_t)i * ldm] = sh_beta;  // R_ii (column i no longer read)
-    __syncthreads();
+    tc0 = clock64();
+    ph[3] += tc0 - tc3;
+  }
+  if (A.tlog && threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) A.tlog[(size_t)t.group * 16 + 8 + q] = (unsigned long long)ph[q];
+  if (A.tlog && threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) A.tlog[(size_t)t.group * 16 + 12 + q] = (unsigned long long)ph2[q];
+  mark(6);
+  // LAPACK order of the columns (the redundant ones as of step k), R_ii into place
+  {
+    const int32_t* cat = cpos + (k & 1) * nc;
+    for (int pos = threadIdx.x; pos < nc; pos += NT) perm[pos] = cat[pos];
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < k; i += NT) Mc[i + (size_t)perm[i] * ldm] = rdiag[i];
+  Mq = Mc;
+  __syncthreads();
   const int r = nc - k;
+  // the redundant set is known: later groups may start (exact order) while
+  // this one finishes its interpolation and elimination off the chain
+  publish(k, perm, sdofs, nc);
 
   // T = R11^-1 R12 (back substitution, one thread per column of R12)
   for (int j = threadIdx.x; j < r; j += NT) {
-    double* col = Mq + (size_t)(k + j) * ldm;
+    double* col = Mq + (size_t)perm[k + j] * ldm;
     for (int i = k - 1; i >= 0; --i) {
       double s = col[i];
-      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)l * ldm] * col[l];
-      col[i] = s / Mq[i + (size_t)i * ldm];
+      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)perm[l] * ldm] * col[l];
+      col[i] = s / Mq[i + (size_t)perm[i] * ldm];
     }
   }
   // ascending sk / rd with their pivot positions
@@ -639,7 +748,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   }
   for (int e = threadIdx.x; e < k * r; e += NT) {
     const int a = e / r, b = e - a * r;
-    Ts[e] = Mq[sko[a] + (size_t)(k + rdo[b]) * ldm];
+    Ts[e] = Mq[sko[a] + (size_t)perm[k + rdo[b]] * ldm];
   }
   __syncthreads();
   // B_sr = A_sr - A_ss T
@@ -716,25 +825,42 @@ __global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __rest
                                                           const int32_t* __restrict__ pred,
                                                           int* __restrict__ done, Arenas A, double eps) {
   extern __shared__ __align__(16) unsigned char smem[];
+  auto stamp = [&](int j, int which) {
+    if (A.tlog && threadIdx.x == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      A.tlog[(size_t)j * 16 + which] = g;
+    }
+  };
   for (int j = blockIdx.x; j < ntasks; j += gridDim.x) {
     const SkelTask t = tasks[j];
+    stamp(j, 0);
     auto wait = [&]() {
       // one thread per predecessor polls its flag
+      // relaxed polling (an acquire load would invalidate the SM's L1 on
+      // every probe, stalling the co-resident groups), then one fence
+      bool polled = false;
       for (int64_t p = pred_ptr[j] + threadIdx.x; p < pred_ptr[j + 1]; p += NT) {
         cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[p]]);
-        while (f.load(cuda::memory_order_acquire) == 0) __nanosleep(32);
+        while (f.load(cuda::memory_order_relaxed) == 0) __nanosleep(32);
+        polled = true;
       }
+      if (polled) cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+      __syncthreads();
+      stamp(j, 1);
     };
-    skel_group<NT>(t, A, eps, smem, wait);
+    auto publish = [&](int k, const int32_t* perm, const int32_t* sdofs, int nc) {
+      for (int a = k + threadIdx.x; a < nc; a += NT) A.active[sdofs[perm[a]]] = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        cuda::atomic_ref<int, cuda::thread_scope_device> f(done[j]);
+        f.store(1, cuda::memory_order_release);
+      }
+      stamp(j, 2);
+    };
+    skel_group<NT>(t, A, eps, smem, wait, publish);
     __syncthreads();
-    const int k = A.kout[t.group];
-    const int32_t* out = A.idx + t.out_off;
-    for (int a = k + threadIdx.x; a < t.nc; a += NT) A.active[out[a]] = 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      cuda::atomic_ref<int, cuda::thread_scope_device> f(done[j]);
-      f.store(1, cuda::memory_order_release);
-    }
+    stamp(j, 3);
   }
 }
 

@@ -214,6 +214,13 @@ struct LevelRec {
   double seconds = 0, gflop = 0, gbytes = 0;
   double gpu_seconds = 0;                 // CUDA-event time of the level's kernels
   double t_part = 0, t_sym = 0, t_upd = 0, t_launch = 0, t_sync = 0;  // host phases
+  std::vector<std::pair<const char*, double>> sub;                     // finer host phases (profile)
+  double t_lap = 0;
+  void lap(const char* what) {
+    const double t = now_s();
+    if (t_lap > 0) sub.emplace_back(what, t - t_lap);
+    t_lap = t;
+  }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // solve metadata: records handled one CTA each (recs / d_recs after the
   // split) and the tiled phases of the large records
@@ -461,6 +468,7 @@ struct Factorizer {
     A.status = status.p;
     A.kout = kout.p;
     A.iscratch = iscratch.p;
+    A.tlog = nullptr;
     return A;
   }
 
@@ -608,7 +616,9 @@ struct Factorizer {
     size_t smem_small = 0, smem_big = 0;
     int max_small_nf = 0;
     scratch.n = 0;
+    L.lap(nullptr);
     const std::vector<FrontSym> fs = fronts(gr);
+    L.lap("fronts");
     for (int64_t t = 0; t < nt; ++t) {
       const int32_t* c = gr.begin(t);
       const int nc = gr.count(t);
@@ -665,6 +675,7 @@ struct Factorizer {
     }
     double tp = now_s();
     L.t_sym = tp - t_begin;
+    L.lap("tasks");
     HTRACE("  symbolic done");
     // host structure updates: consumed blocks die, new neighbour blocks live
     for (int64_t t = 0; t < nt; ++t) {
@@ -675,6 +686,7 @@ struct Factorizer {
       for (int i = 0; i < T.nc; ++i) active[(size_t)c[i]] = 0;
     }
     L.t_upd = now_s() - tp;
+    L.lap("blocks");
     tp = now_s();
     // split into the shared-memory path and the blocked large-front path
     std::vector<ElimTask> small, big;
@@ -793,6 +805,7 @@ struct Factorizer {
     if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
     // (the kernels retire the cells in the device active mask themselves)
     L.t_launch = now_s() - tp;
+    L.lap("launch");
     tp = now_s();
     if (is_top) check_status();
     d_small.release(s);
@@ -884,7 +897,9 @@ struct Factorizer {
     int nbatch = 1;
     std::vector<int32_t> preds;          // earlier neighbouring groups (exact order)
     std::vector<int64_t> pred_ptr{0};
+    L.lap(nullptr);
     const std::vector<FrontSym> fs = fronts(gr);
+    L.lap("fronts");
     for (int64_t t = 0; t < nt; ++t) {
       const int32_t* c = gr.begin(t);
       const int nc = gr.count(t);
@@ -907,13 +922,17 @@ struct Factorizer {
       h_idx.insert(h_idx.end(), (size_t)nc, 0);
       T.blk_off = (int64_t)hl.size();
       hl.insert(hl.end(), blks, blks + f.nb);
-      const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 5 * nc));
+      // index arrays, then the CPQR vectors (kernels_factor.cu skel_group)
+      const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * nc)) + sizeof(double) * 5 * (size_t)nc;
       const size_t q4 = (size_t)nc * nc / 4 + nc;
       const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
       const size_t mq = (size_t)nq * nc + 2 * (size_t)nc;
       max_nc = std::max(max_nc, nc);
       max_nq = std::max(max_nq, nq);
-      if (ib + sizeof(double) * wsd <= kSmemCap) {
+      if (nc > kMaxSkelNc) {
+        T.mode = 2;  // beyond the one-CTA CPQR's register position map
+        T.scratch_off = -1;
+      } else if (ib + sizeof(double) * wsd <= kSmemCap) {
         T.mode = 0;
         T.scratch_off = -1;
         smem = std::max(smem, ib + sizeof(double) * wsd);
@@ -921,7 +940,7 @@ struct Factorizer {
         T.mode = 1;
         T.scratch_off = (int64_t)scratch.bump(3 * (size_t)nc * nc + 3 * q4 + 8, s);
         smem = std::max(smem, ib + sizeof(double) * mq);
-      } else if (nq > nc && nc <= 160 && !getenv("HIFDE_NO_TSQR") &&
+      } else if (nq > nc && nc <= 160 &&
                  ib + sizeof(double) * ((size_t)(2 * nc) * nc + 2 * (size_t)nc) <= kSmemCap) {
         // Mq in global scratch, compressed to R (nc x nc) in shared memory by
         // chunked Householder QR: column norms and pivots are unchanged
@@ -961,6 +980,7 @@ struct Factorizer {
       nbatch = 1;
     }
     L.nbatches = nbatch;
+    L.lap("tasks");
     HTRACE("  symbolic done, %d batches", nbatch);
     double tp = now_s();
     L.t_sym = tp - t_begin;
@@ -992,16 +1012,38 @@ struct Factorizer {
       kout.bump((size_t)nt, s);
       Arenas A = arenas();
       A.status = status.p + st_off;
-      const int nthr = (max_nc > 32 || max_nq > 128) ? 512 : 128;
+      const int nthr = (max_nc > 32 || max_nq > 128 || getenv("HIFDE_SKEL512")) ? 512 : 128;
       const int cap = skel_ordered_capacity(smem, nthr);
       if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
       const int grid = (int)std::min<int64_t>(nt, cap);
       HCK(cudaEventCreate(&L.ev0));
       HCK(cudaEventCreate(&L.ev1));
       HCK(cudaEventRecord(L.ev0, s));
+      const char* tlog_dir = getenv("HIFDE_SKEL_TLOG");
+      DBuf<unsigned long long> dtl;
+      if (tlog_dir) {
+        dtl.reserve((size_t)nt * 16, s);
+        A.tlog = dtl.p;
+      }
       HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
       ++g_launches;
       HCK(cudaEventRecord(L.ev1, s));
+      if (tlog_dir) {  // debug: per-group timestamps + the predecessor CSR
+        std::vector<unsigned long long> h((size_t)nt * 16);
+        HCK(cudaMemcpyAsync(h.data(), dtl.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+        char fn[512];
+        snprintf(fn, sizeof fn, "%s/tlog_%.3f_%lld.bin", tlog_dir, tag, (long long)nt);
+        if (FILE* fp = fopen(fn, "wb")) {
+          const int64_t hdr[3] = {(int64_t)nt, (int64_t)preds.size(), (int64_t)grid};
+          fwrite(hdr, 8, 3, fp);
+          fwrite(h.data(), 8, h.size(), fp);
+          fwrite(pred_ptr.data(), 8, pred_ptr.size(), fp);
+          fwrite(preds.data(), 4, preds.size(), fp);
+          fclose(fp);
+        }
+        dtl.release(s);
+      }
       L.t_launch = now_s() - tp;
       tp = now_s();
       finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
@@ -1131,7 +1173,9 @@ struct Factorizer {
       HCK(cudaMemcpyAsync(h_idx.data() + idx_level_start, F->idx.p + idx_level_start,
                           (h_idx.size() - (size_t)idx_level_start) * sizeof(int32_t),
                           cudaMemcpyDeviceToHost, s));
+    L.lap("launch");
     check_status();  // synchronizes the stream
+    L.lap("wait");
     HTRACE("  readback done");
     L.t_sync = now_s() - tp;
     tp = now_s();
@@ -1169,6 +1213,7 @@ struct Factorizer {
       L.gbytes += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
     }
     L.t_upd = now_s() - tp;
+    L.lap("retire");
   }
 
   // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
@@ -1587,6 +1632,11 @@ struct Factorizer {
                 L.tag, L.kind, (long long)L.ngroups, L.nbatches, (long long)L.max_front, L.t_part * 1e3,
                 L.t_sym * 1e3, L.t_upd * 1e3, L.t_launch * 1e3, L.t_sync * 1e3, L.seconds * 1e3,
                 L.gpu_seconds * 1e3);
+      for (const auto& L : F->levels) {
+        fprintf(stderr, "[hifde]   tag %6.3f sub:", L.tag);
+        for (const auto& p : L.sub) fprintf(stderr, " %s %.3f", p.first, p.second * 1e3);
+        fprintf(stderr, "\n");
+      }
     }
   }
 };
