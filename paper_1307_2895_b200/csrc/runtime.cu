@@ -11,6 +11,7 @@
 // only integer structure (DOF lists, block membership); every floating-point
 // operation runs in the sm_100a kernels.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cfloat>
 #include <cmath>
@@ -18,6 +19,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <thread>
 #include <future>
 #include <memory>
 #include <mutex>
@@ -258,22 +261,17 @@ struct hifde_factor {
   std::vector<hifde::LevelRec> levels;  // last entry = terminal block (kind 2)
   int64_t max_contrib = 0;
   int64_t tile_rows = 0;  // solve scratch rows of the tiled phases
+  char* meta = nullptr;  // every level's solve metadata (one allocation)
   ~hifde_factor() {
+    // stream-ordered frees: no device-wide synchronization on release
     cudaSetDevice(device);
-    for (auto& L : levels) {
-      for (auto* ph : {&L.fwd_ph, &L.bwd_ph})
-        for (auto& P : *ph) {
-          if (P.d_ops) cudaFree(P.d_ops);
-          if (P.d_work) cudaFree(P.d_work);
-        }
-      if (L.d_recs) cudaFree(L.d_recs);
-      if (L.d_targets) cudaFree(L.d_targets);
-      if (L.d_ptr) cudaFree(L.d_ptr);
-      if (L.d_ent) cudaFree(L.d_ent);
+    if (meta) cudaFreeAsync(meta, stream);
+    if (fac.p) cudaFreeAsync(fac.p, stream);
+    if (idx.p) cudaFreeAsync(idx.p, stream);
+    if (own_stream && stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
     }
-    if (fac.p) cudaFree(fac.p);
-    if (idx.p) cudaFree(idx.p);
-    if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
 
@@ -289,30 +287,66 @@ T* to_device(const std::vector<T>& h) {
   return d;
 }
 
+// Solve metadata of a whole factorization packed into one device allocation
+// and one asynchronous upload (instead of an allocation + blocking copy each).
+struct MetaPack {
+  std::vector<char> h;
+  std::vector<std::pair<void**, size_t>> slots;
+  template <class T>
+  void add(T** slot, const std::vector<T>& v) {
+    *slot = nullptr;
+    if (v.empty()) return;
+    const size_t off = (h.size() + 255) & ~(size_t)255;
+    h.resize(off + v.size() * sizeof(T));
+    std::memcpy(h.data() + off, v.data(), v.size() * sizeof(T));
+    slots.emplace_back((void**)slot, off);
+  }
+  // returns the device block (owned by the caller)
+  char* commit(cudaStream_t s, const std::function<void(void*, const void*, size_t)>& up) {
+    if (h.empty()) return nullptr;
+    char* d = nullptr;
+    HCK(cudaMallocAsync((void**)&d, h.size(), s));
+    up(d, h.data(), h.size());
+    for (auto& sl : slots) *sl.first = d + sl.second;
+    return d;
+  }
+};
+
 // Live clique blocks containing each DOF: up to kInline ids stored inline per
 // DOF, the rare overflow in a side table.
 struct Membership {
   static constexpr int kInline = 8;
   std::unique_ptr<int32_t[]> ids;
   std::vector<uint8_t> cnt;
-  std::vector<std::vector<int32_t>> over;  // indexed by overflow slot
+  std::vector<std::vector<int32_t>> over;  // overflow lists, pre-sized; slots taken atomically
+  std::atomic<int32_t> nover{0};
   std::vector<int32_t> over_slot;          // per DOF, -1 if none
   void init(int64_t n) {
     ids.reset(new int32_t[(size_t)n * kInline]);
     cnt.assign((size_t)n, 0);
     over_slot.assign((size_t)n, -1);
     over.clear();
+    over.resize(1024);
+    nover = 0;
   }
   // empty every list (storage kept)
   void reset() {
     std::fill(cnt.begin(), cnt.end(), 0);
+    std::fill(over_slot.begin(), over_slot.end(), -1);
     for (size_t i = 0; i < over.size(); ++i) over[i].clear();
+    nover = 0;
   }
+  // serial phases only: keep room for the overflow slots a parallel phase may take
+  void ensure_room(size_t extra) {
+    const size_t need = (size_t)nover.load() + extra;
+    if (need > over.size()) over.resize(std::max(need, over.size() * 2));
+  }
+  // add / remove: safe concurrently for distinct DOFs (after ensure_room)
   void add(int32_t d, int32_t b) {
     uint8_t& c = cnt[(size_t)d];
     if (c < kInline) { ids[(size_t)d * kInline + c] = b; ++c; return; }
     int32_t& sl = over_slot[(size_t)d];
-    if (sl < 0) { sl = (int32_t)over.size(); over.emplace_back(); }
+    if (sl < 0) sl = nover.fetch_add(1);
     over[(size_t)sl].push_back(b);
   }
   void remove(int32_t d, int32_t b) {
@@ -366,6 +400,10 @@ struct HostCache {
   Coords X;
   std::vector<SymCtx> ctx;
   Membership member;
+  // arena sizes reached by the last factorization of this grid / variant:
+  // reserved up front next time so the arenas do not grow (and copy) mid-run
+  int variant = -1;
+  size_t hint_fac = 0, hint_bv = 0, hint_idx = 0, hint_scr = 0;
 };
 HostCache& host_cache() {
   static HostCache hc;
@@ -383,6 +421,21 @@ struct FrontSym {  // result of the symbolic analysis of one cell / group
 // Factorization state
 // ---------------------------------------------------------------------------
 struct Factorizer {
+  std::thread a0_thread;  // host CSR upload in flight
+  cudaError_t a0_err = cudaSuccess;
+  void a0_ready() {
+    if (a0_thread.joinable()) a0_thread.join();
+    if (a0_err != cudaSuccess) {
+      const cudaError_t e = a0_err;
+      a0_err = cudaSuccess;
+      throw Fail{HIFDE_CUDA, std::string("A0 upload: ") + cudaGetErrorString(e)};
+    }
+  }
+  ~Factorizer() {
+    if (a0_thread.joinable()) a0_thread.join();
+  }
+  LevelRec prof;  // setup / finish phase timings
+  MetaPack meta;  // solve metadata, uploaded once at the end
   GridDesc g;
   hifde_options_t opt;
   hifde_factor_t* F;
@@ -452,6 +505,7 @@ struct Factorizer {
     blk_uploaded = nb;
   }
   Arenas arenas() {
+    a0_ready();  // every launch site takes its arenas here
     Arenas A;
     A.indptr = d_indptr;
     A.indices = d_indices;
@@ -472,7 +526,19 @@ struct Factorizer {
     return A;
   }
 
+  // block table entry only (membership updated by the caller)
+  int32_t new_block(int64_t dof_off, int32_t nb, int64_t val_off) {
+    int32_t id = (int32_t)blk_n.size();
+    blk_dof_off.push_back(dof_off);
+    blk_n.push_back(nb);
+    blk_val_off.push_back(val_off);
+    blk_alive.push_back(1);
+    bf_key.push_back(-2);
+    bf_val.push_back(0);
+    return id;
+  }
   int32_t add_block(int64_t dof_off, int32_t nb, int64_t val_off) {
+    member.ensure_room((size_t)nb);
     int32_t id = (int32_t)blk_n.size();
     blk_dof_off.push_back(dof_off);
     blk_n.push_back(nb);
@@ -619,53 +685,68 @@ struct Factorizer {
     L.lap(nullptr);
     const std::vector<FrontSym> fs = fronts(gr);
     L.lap("fronts");
+    // sizes and placement per cell (parallel), offsets (prefix), fill (parallel)
+    std::vector<size_t> smem_need((size_t)nt, 0);
+    const int nthr = nt >= 256 ? nthreads : 1;
+#pragma omp parallel for num_threads(nthr) schedule(static)
     for (int64_t t = 0; t < nt; ++t) {
-      const int32_t* c = gr.begin(t);
       const int nc = gr.count(t);
       const FrontSym& f = fs[(size_t)t];
-      const int32_t* q = sym_q(f);
-      const int32_t* bl = sym_b(f);
       const int nq = f.nq, nf = nc + nq;
       ElimTask& T = tasks[(size_t)t];
       T.nc = nc;
       T.nq = nq;
       T.nblk = f.nb;
       T.maxnb = f.maxnb;
-      T.dofs_off = (int64_t)h_idx.size();
-      h_idx.insert(h_idx.end(), c, c + nc);
-      h_idx.insert(h_idx.end(), q, q + nq);
-      T.blk_off = (int64_t)hl.size();
-      hl.insert(hl.end(), bl, bl + f.nb);
       const size_t ib = align16(sizeof(int32_t) * (size_t)(nf + T.maxnb));
       const size_t need = ib + sizeof(double) * (size_t)nf * nf;
       const size_t need_inv = need + sizeof(double) * (size_t)nc * nc;
       if (need <= kSmemCap) {
         // -2: room for the inverse workspace after the front as well
         T.scratch_off = need_inv <= kSmemCap ? -2 : -1;
-        smem_small = std::max(smem_small, T.scratch_off == -2 ? need_inv : need);
-        max_small_nf = std::max(max_small_nf, nf);
+        smem_need[(size_t)t] = T.scratch_off == -2 ? need_inv : need;
       } else {
         is_big[(size_t)t] = 1;
         T.scratch_off = -1;
+      }
+    }
+    int64_t idx_tot = 0, hl_tot = 0;
+    size_t fac_tot = 0, bv_tot = 0;
+    L.recs.resize((size_t)nt);
+    for (int64_t t = 0; t < nt; ++t) {
+      ElimTask& T = tasks[(size_t)t];
+      const int nc = T.nc, nq = T.nq, nf = nc + nq;
+      T.dofs_off = idx_tot;
+      idx_tot += nf;
+      T.blk_off = hl_tot;
+      hl_tot += T.nblk;
+      if (!is_big[(size_t)t]) {
+        smem_small = std::max(smem_small, smem_need[(size_t)t]);
+        max_small_nf = std::max(max_small_nf, nf);
+      } else {
         smem_big = std::max(smem_big, align16(sizeof(int32_t) * (size_t)(nf + 2 * T.maxnb)));
       }
-      T.C_off = (int64_t)F->fac.bump((size_t)nc * nc, s);
-      T.P_off = is_big[(size_t)t] ? (int64_t)F->fac.bump((size_t)nc * (nc + 1) / 2, s) : T.C_off;
-      T.W_off = (int64_t)F->fac.bump((size_t)nc * nq, s);
-      T.U_off = nq > 0 ? (int64_t)bvals.bump((size_t)nq * nq, s) : 0;
+      T.C_off = (int64_t)fac_tot;
+      fac_tot += (size_t)nc * nc;
+      if (is_big[(size_t)t]) {
+        T.P_off = (int64_t)fac_tot;
+        fac_tot += (size_t)nc * (nc + 1) / 2;
+      } else {
+        T.P_off = T.C_off;
+      }
+      T.W_off = (int64_t)fac_tot;
+      fac_tot += (size_t)nc * nq;
+      T.U_off = (int64_t)bv_tot;
+      bv_tot += (size_t)nq * nq;
       L.max_front = std::max<int64_t>(L.max_front, nf);
-      SolveRec R;
+      SolveRec& R = L.recs[(size_t)t];
       R.nc = nc;
       R.nq = nq;
-      R.idx_off = T.dofs_off;
-      R.C_off = T.P_off;  // the solve applies the packed inverse
-      R.W_off = T.W_off;
-      R.T_off = 0;
       R.contrib_off = L.ncontrib;
+      R.T_off = 0;
       R.inv = 1;
       R.pad = 0;
       L.ncontrib += nq;
-      L.recs.push_back(R);
       L.max_nc = std::max(L.max_nc, nc);
       L.max_nq = std::max(L.max_nq, nq);
       F->m_f_bytes += 8 * ((int64_t)nc * nc + nc + (int64_t)nc * nq);
@@ -673,17 +754,72 @@ struct Factorizer {
       L.gflop += (dc * dc * dc / 3 + dc * dc * dq + dc * dq + dc * dq * dq) * 1e-9;
       L.gbytes += 8.0 * ((dc + dq) * (dc + dq) + dc * dc + dc + dc * dq + 2 * dq * dq) * 1e-9;
     }
+    const int64_t idx_base = (int64_t)h_idx.size();
+    h_idx.resize((size_t)(idx_base + idx_tot));
+    hl.resize((size_t)hl_tot);
+    const int64_t fac_base = (int64_t)F->fac.bump(fac_tot, s);
+    const int64_t bv_base = bv_tot ? (int64_t)bvals.bump(bv_tot, s) : 0;
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, 64)
+    for (int64_t t = 0; t < nt; ++t) {
+      ElimTask& T = tasks[(size_t)t];
+      const FrontSym& f = fs[(size_t)t];
+      T.dofs_off += idx_base;
+      T.C_off += fac_base;
+      T.P_off += fac_base;
+      T.W_off += fac_base;
+      T.U_off = T.nq > 0 ? T.U_off + bv_base : 0;
+      int32_t* d = h_idx.data() + T.dofs_off;
+      std::copy(gr.begin(t), gr.begin(t) + T.nc, d);
+      std::copy(sym_q(f), sym_q(f) + T.nq, d + T.nc);
+      std::copy(sym_b(f), sym_b(f) + f.nb, hl.data() + T.blk_off);
+      SolveRec& R = L.recs[(size_t)t];
+      R.idx_off = T.dofs_off;
+      R.C_off = T.P_off;  // the solve applies the packed inverse
+      R.W_off = T.W_off;
+    }
     double tp = now_s();
     L.t_sym = tp - t_begin;
     L.lap("tasks");
     HTRACE("  symbolic done");
     // host structure updates: consumed blocks die, new neighbour blocks live
-    for (int64_t t = 0; t < nt; ++t) {
-      const ElimTask& T = tasks[(size_t)t];
-      for (int j = 0; j < T.nblk; ++j) kill_block(hl[(size_t)(T.blk_off + j)]);
-      if (T.nq > 0) add_block(T.dofs_off + T.nc, T.nq, T.U_off);
-      const int32_t* c = gr.begin(t);
-      for (int i = 0; i < T.nc; ++i) active[(size_t)c[i]] = 0;
+    {
+      std::vector<int32_t> newid((size_t)nt, -1);
+      size_t nadd = 0;
+      for (int64_t t = 0; t < nt; ++t) {
+        const ElimTask& T = tasks[(size_t)t];
+        for (int j = 0; j < T.nblk; ++j) blk_alive[(size_t)hl[(size_t)(T.blk_off + j)]] = 0;
+        if (T.nq > 0) newid[(size_t)t] = new_block(T.dofs_off + T.nc, T.nq, T.U_off);
+        nadd += (size_t)T.nq;
+      }
+      member.ensure_room(nadd);
+      // every thread applies the membership edits of its own DOF range
+      const int nthu = nt >= 64 ? nthreads : 1;
+#pragma omp parallel num_threads(nthu)
+      {
+        const int tid = omp_get_thread_num(), nth = omp_get_num_threads();
+        const int64_t lo = N * tid / nth, hi = N * (tid + 1) / nth;
+        for (int64_t t = 0; t < nt; ++t) {
+          const ElimTask& T = tasks[(size_t)t];
+          for (int j = 0; j < T.nblk; ++j) {
+            const int32_t b = hl[(size_t)(T.blk_off + j)];
+            const int32_t* d = h_idx.data() + blk_dof_off[(size_t)b];
+            for (int32_t i = 0; i < blk_n[(size_t)b]; ++i)
+              if (d[i] >= lo && d[i] < hi) member.remove(d[i], b);
+          }
+        }
+        for (int64_t t = 0; t < nt; ++t) {
+          const ElimTask& T = tasks[(size_t)t];
+          if (T.nq <= 0) continue;
+          const int32_t* d = h_idx.data() + T.dofs_off + T.nc;
+          for (int i = 0; i < T.nq; ++i)
+            if (d[i] >= lo && d[i] < hi) member.add(d[i], newid[(size_t)t]);
+        }
+#pragma omp for schedule(static)
+        for (int64_t t = 0; t < nt; ++t) {
+          const int32_t* c = gr.begin(t);
+          for (int i = 0; i < gr.count(t); ++i) active[(size_t)c[i]] = 0;
+        }
+      }
     }
     L.t_upd = now_s() - tp;
     L.lap("blocks");
@@ -824,51 +960,52 @@ struct Factorizer {
   }
 
   // Solve-side reduction of one elimination level: for every neighbour DOF the
-  // contribution rows (record order) summed by solve_reduce_kernel.  Built on
-  // a background thread from a copy of the q lists; joined at the end.
+  // contribution rows (record order) summed by solve_reduce_kernel.  Linear
+  // counting sort by DOF (targets in first-touch order); uploaded at the end.
   struct Reduction {
     std::vector<int32_t> targets;
     std::vector<int64_t> ptr, ent;
   };
-  std::vector<std::pair<size_t, std::future<Reduction>>> reductions;
+  std::vector<std::pair<size_t, Reduction>> reductions;
+  std::vector<int32_t> red_slot;  // per DOF: target index during a build, else -1
 
   void build_reduction(size_t level_index, const LevelRec& L) {
-    std::vector<std::pair<int32_t, int64_t>> pairs;
-    size_t tot = 0;
-    for (const SolveRec& R : L.recs) tot += (size_t)R.nq;
-    pairs.reserve(tot);
+    if ((int64_t)red_slot.size() != N) red_slot.assign((size_t)N, -1);
+    Reduction r;
+    std::vector<int64_t> cnt;
     for (const SolveRec& R : L.recs) {
       const int32_t* q = h_idx.data() + R.idx_off + R.nc;
-      for (int a = 0; a < R.nq; ++a) pairs.emplace_back(q[a], R.contrib_off + a);
-    }
-    F->max_contrib = std::max(F->max_contrib, L.ncontrib);
-    reductions.emplace_back(level_index, std::async(std::launch::async, [p = std::move(pairs)]() mutable {
-      // (dof, entry) with entries increasing in record order: sorting the pairs
-      // groups by DOF and keeps record order inside a group
-      std::sort(p.begin(), p.end());
-      Reduction r;
-      r.ptr.push_back(0);
-      r.ent.reserve(p.size());
-      for (size_t i = 0; i < p.size(); ++i) {
-        if (i == 0 || p[i].first != p[i - 1].first) {
-          if (i) r.ptr.push_back((int64_t)r.ent.size());
-          r.targets.push_back(p[i].first);
+      for (int a = 0; a < R.nq; ++a) {
+        int32_t& sl = red_slot[(size_t)q[a]];
+        if (sl < 0) {
+          sl = (int32_t)r.targets.size();
+          r.targets.push_back(q[a]);
+          cnt.push_back(0);
         }
-        r.ent.push_back(p[i].second);
+        ++cnt[(size_t)sl];
       }
-      if (!p.empty()) r.ptr.push_back((int64_t)r.ent.size());
-      return r;
-    }));
+    }
+    r.ptr.assign(r.targets.size() + 1, 0);
+    for (size_t i = 0; i < cnt.size(); ++i) r.ptr[i + 1] = r.ptr[i] + cnt[i];
+    r.ent.resize((size_t)r.ptr.back());
+    std::vector<int64_t> pos(r.ptr.begin(), r.ptr.end() - 1);
+    for (const SolveRec& R : L.recs) {
+      const int32_t* q = h_idx.data() + R.idx_off + R.nc;
+      for (int a = 0; a < R.nq; ++a) r.ent[(size_t)pos[(size_t)red_slot[(size_t)q[a]]]++] = R.contrib_off + a;
+    }
+    for (int32_t d : r.targets) red_slot[(size_t)d] = -1;
+    F->max_contrib = std::max(F->max_contrib, L.ncontrib);
+    reductions.emplace_back(level_index, std::move(r));
   }
 
   void finish_reductions() {
     for (auto& pr : reductions) {
-      Reduction r = pr.second.get();
+      const Reduction& r = pr.second;
       LevelRec& L = F->levels[pr.first];
       L.ntargets = (int)r.targets.size();
-      L.d_targets = to_device(r.targets);
-      L.d_ptr = to_device(r.ptr);
-      L.d_ent = to_device(r.ent);
+      meta.add(&L.d_targets, r.targets);
+      meta.add(&L.d_ptr, r.ptr);
+      meta.add(&L.d_ent, r.ent);
     }
     reductions.clear();
   }
@@ -890,7 +1027,8 @@ struct Factorizer {
     // holds a DOF of the other's neighbour set)
     std::vector<int> batch((size_t)nt, 0);
     std::vector<int32_t> gof_dofs;  // DOFs of this level's groups, to reset
-    static thread_local std::vector<int32_t> group_of;
+    static thread_local std::vector<int32_t> group_of_tls;
+    std::vector<int32_t>& group_of = group_of_tls;  // this thread's; shared with the OpenMP workers
     if ((int64_t)group_of.size() < N) group_of.assign((size_t)N, -1);
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = (int32_t)t;
@@ -900,76 +1038,131 @@ struct Factorizer {
     L.lap(nullptr);
     const std::vector<FrontSym> fs = fronts(gr);
     L.lap("fronts");
+    // (1) per group, in parallel: workspace mode, arena sizes, earlier
+    // neighbouring groups; (2) prefix sums and exact-order batches; (3) fill
+    struct Sz {
+      size_t scr, fac, smem;
+      int64_t pred_off;
+      int npred;
+    };
+    std::vector<Sz> sz((size_t)nt);
+    std::vector<std::vector<int32_t>> tpred((size_t)nthreads);
+    const int nthr = nt >= 256 ? nthreads : 1;
+#pragma omp parallel num_threads(nthr)
+    {
+      std::vector<int32_t>& mypred = tpred[(size_t)omp_get_thread_num()];
+      mypred.clear();
+#pragma omp for schedule(dynamic, 64)
+      for (int64_t t = 0; t < nt; ++t) {
+        const int nc = gr.count(t);
+        const FrontSym& f = fs[(size_t)t];
+        const int32_t* q = sym_q(f);
+        const int nq = f.nq, nf = nc + nq;
+        SkelTask& T = tasks[(size_t)t];
+        T.nc = nc;
+        T.nq = nq;
+        T.nblk = f.nb;
+        T.maxnb = f.maxnb;
+        T.group = (int32_t)t;
+        T.chunk = 0;
+        T.pad2 = 0;
+        T.scratch_off = -1;
+        Sz& z = sz[(size_t)t];
+        z.scr = 0;
+        z.smem = 0;
+        // index arrays, then the CPQR vectors (kernels_factor.cu skel_group)
+        const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * nc)) + sizeof(double) * 5 * (size_t)nc;
+        const size_t q4 = (size_t)nc * nc / 4 + nc;
+        const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
+        const size_t mq = (size_t)nq * nc + 2 * (size_t)nc;
+        if (nc > kMaxSkelNc) {
+          T.mode = 2;  // beyond the one-CTA CPQR
+        } else if (ib + sizeof(double) * wsd <= kSmemCap) {
+          T.mode = 0;
+          z.smem = ib + sizeof(double) * wsd;
+        } else if (ib + sizeof(double) * mq <= kSmemCap) {
+          T.mode = 1;
+          z.scr = 3 * (size_t)nc * nc + 3 * q4 + 8;
+          z.smem = ib + sizeof(double) * mq;
+        } else if (nq > nc && nc <= 160 &&
+                   ib + sizeof(double) * ((size_t)(2 * nc) * nc + 2 * (size_t)nc) <= kSmemCap) {
+          // Mq in global scratch, compressed to R (nc x nc) in shared memory by
+          // chunked Householder QR: column norms and pivots are unchanged
+          T.mode = 3;
+          const size_t avail = (kSmemCap - ib) / sizeof(double) - 2 * (size_t)nc;
+          T.chunk = (int32_t)std::min<size_t>(avail / nc - nc, (size_t)nq);
+          z.scr = wsd + 8;
+          z.smem = ib + sizeof(double) * ((size_t)(nc + T.chunk) * nc + 2 * (size_t)nc);
+        } else {
+          T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
+        }
+        z.fac = (size_t)nc * nc + 2 * q4 + (T.mode == 2 ? (size_t)nc * (nc + 1) / 2 + nc : 0);
+        const size_t p0 = mypred.size();
+        for (int i = 0; i < nq; ++i) {
+          const int32_t go = group_of[(size_t)q[i]];
+          if (go >= 0 && go < t) mypred.push_back(go);
+        }
+        std::sort(mypred.begin() + (int64_t)p0, mypred.end());
+        mypred.erase(std::unique(mypred.begin() + (int64_t)p0, mypred.end()), mypred.end());
+        z.pred_off = (int64_t)p0 * nthreads + omp_get_thread_num();  // decoded below
+        z.npred = (int)(mypred.size() - p0);
+      }
+    }
+    // (2) serial prefix pass
+    int64_t idx_tot = 0, hl_tot = 0;
+    size_t scr_tot = 0, fac_tot = 0, bv_tot = 0;
+    pred_ptr.resize((size_t)nt + 1);
     for (int64_t t = 0; t < nt; ++t) {
-      const int32_t* c = gr.begin(t);
-      const int nc = gr.count(t);
-      const FrontSym& f = fs[(size_t)t];
-      const int32_t* q = sym_q(f);
-      const int32_t* blks = sym_b(f);
-      const int nq = f.nq, nf = nc + nq;
       SkelTask& T = tasks[(size_t)t];
-      T.nc = nc;
-      T.nq = nq;
-      T.nblk = f.nb;
-      T.maxnb = f.maxnb;
-      T.group = (int32_t)t;
-      T.chunk = 0;
-      T.pad2 = 0;
-      T.dofs_off = (int64_t)h_idx.size();
-      h_idx.insert(h_idx.end(), c, c + nc);
-      h_idx.insert(h_idx.end(), q, q + nq);
-      T.out_off = (int64_t)h_idx.size();
-      h_idx.insert(h_idx.end(), (size_t)nc, 0);
-      T.blk_off = (int64_t)hl.size();
-      hl.insert(hl.end(), blks, blks + f.nb);
-      // index arrays, then the CPQR vectors (kernels_factor.cu skel_group)
-      const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * nc)) + sizeof(double) * 5 * (size_t)nc;
-      const size_t q4 = (size_t)nc * nc / 4 + nc;
-      const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
-      const size_t mq = (size_t)nq * nc + 2 * (size_t)nc;
+      const Sz& z = sz[(size_t)t];
+      const int nc = T.nc, nq = T.nq;
+      T.dofs_off = idx_tot;
+      T.out_off = idx_tot + nc + nq;
+      idx_tot += 2 * nc + nq;
+      T.blk_off = hl_tot;
+      hl_tot += T.nblk;
+      if (z.scr) { T.scratch_off = (int64_t)scr_tot; scr_tot += z.scr; }
+      T.rec_off = (int64_t)fac_tot;
+      fac_tot += z.fac;
+      T.delta_off = (int64_t)bv_tot;
+      bv_tot += (size_t)nc * nc;
+      smem = std::max(smem, z.smem);
       max_nc = std::max(max_nc, nc);
       max_nq = std::max(max_nq, nq);
-      if (nc > kMaxSkelNc) {
-        T.mode = 2;  // beyond the one-CTA CPQR's register position map
-        T.scratch_off = -1;
-      } else if (ib + sizeof(double) * wsd <= kSmemCap) {
-        T.mode = 0;
-        T.scratch_off = -1;
-        smem = std::max(smem, ib + sizeof(double) * wsd);
-      } else if (ib + sizeof(double) * mq <= kSmemCap) {
-        T.mode = 1;
-        T.scratch_off = (int64_t)scratch.bump(3 * (size_t)nc * nc + 3 * q4 + 8, s);
-        smem = std::max(smem, ib + sizeof(double) * mq);
-      } else if (nq > nc && nc <= 160 &&
-                 ib + sizeof(double) * ((size_t)(2 * nc) * nc + 2 * (size_t)nc) <= kSmemCap) {
-        // Mq in global scratch, compressed to R (nc x nc) in shared memory by
-        // chunked Householder QR: column norms and pivots are unchanged
-        T.mode = 3;
-        const size_t avail = (kSmemCap - ib) / sizeof(double) - 2 * (size_t)nc;
-        T.chunk = (int32_t)std::min<size_t>(avail / nc - nc, (size_t)nq);
-        T.scratch_off = (int64_t)scratch.bump(wsd + 8, s);
-        smem = std::max(smem, ib + sizeof(double) * ((size_t)(nc + T.chunk) * nc + 2 * (size_t)nc));
-      } else {
-        T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
-        T.scratch_off = -1;
-      }
-      T.rec_off = (int64_t)F->fac.bump((size_t)nc * nc + 2 * q4 + (T.mode == 2 ? (size_t)nc * (nc + 1) / 2 + nc : 0), s);
-      T.delta_off = (int64_t)bvals.bump((size_t)nc * nc, s);
-      L.max_front = std::max<int64_t>(L.max_front, nf);
+      L.max_front = std::max<int64_t>(L.max_front, nc + nq);
+      pred_ptr[(size_t)t + 1] = pred_ptr[(size_t)t] + z.npred;
+      const int32_t* pp = tpred[(size_t)(z.pred_off % nthreads)].data() + z.pred_off / nthreads;
       int b = 0;
-      const size_t p0 = preds.size();
-      for (int i = 0; i < nq; ++i) {
-        const int32_t go = group_of[(size_t)q[i]];
-        if (go >= 0 && go < t) {
-          b = std::max(b, batch[(size_t)go] + 1);
-          preds.push_back(go);
-        }
-      }
-      std::sort(preds.begin() + (int64_t)p0, preds.end());
-      preds.erase(std::unique(preds.begin() + (int64_t)p0, preds.end()), preds.end());
-      pred_ptr.push_back((int64_t)preds.size());
+      for (int i = 0; i < z.npred; ++i) b = std::max(b, batch[(size_t)pp[i]] + 1);
       batch[(size_t)t] = b;
       nbatch = std::max(nbatch, b + 1);
+    }
+    const int64_t idx_base = (int64_t)h_idx.size();
+    h_idx.resize((size_t)(idx_base + idx_tot));
+    hl.resize((size_t)hl_tot);
+    preds.resize((size_t)pred_ptr[(size_t)nt]);
+    const int64_t scr_base = scr_tot ? (int64_t)scratch.bump(scr_tot, s) : 0;
+    const int64_t fac_base = (int64_t)F->fac.bump(fac_tot, s);
+    const int64_t bv_base = (int64_t)bvals.bump(bv_tot, s);
+    // (3) fill, in parallel
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, 64)
+    for (int64_t t = 0; t < nt; ++t) {
+      SkelTask& T = tasks[(size_t)t];
+      const Sz& z = sz[(size_t)t];
+      const FrontSym& f = fs[(size_t)t];
+      const int nc = T.nc, nq = T.nq;
+      T.dofs_off += idx_base;
+      T.out_off += idx_base;
+      if (T.scratch_off >= 0) T.scratch_off += scr_base;
+      T.rec_off += fac_base;
+      T.delta_off += bv_base;
+      int32_t* d = h_idx.data() + T.dofs_off;
+      std::copy(gr.begin(t), gr.begin(t) + nc, d);
+      std::copy(sym_q(f), sym_q(f) + nq, d + nc);
+      std::fill(d + nc + nq, d + 2 * nc + nq, 0);
+      std::copy(sym_b(f), sym_b(f) + f.nb, hl.data() + T.blk_off);
+      const int32_t* pp = tpred[(size_t)(z.pred_off % nthreads)].data() + z.pred_off / nthreads;
+      std::copy(pp, pp + z.npred, preds.data() + pred_ptr[(size_t)t]);
     }
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = -1;
@@ -1179,6 +1372,8 @@ struct Factorizer {
     HTRACE("  readback done");
     L.t_sync = now_s() - tp;
     tp = now_s();
+    std::vector<int32_t> newid((size_t)nt, -1);
+    size_t nadd = 0;
     for (int64_t t = 0; t < nt; ++t) {
       const SkelTask& T = tasks[(size_t)t];
       const int kk = k[(size_t)t], r = T.nc - kk;
@@ -1186,7 +1381,10 @@ struct Factorizer {
       L.nskel += kk;
       L.nred += r;
       for (int i = kk; i < T.nc; ++i) active[(size_t)out[i]] = 0;
-      if (r > 0 && kk > 0) add_block(T.out_off, kk, T.delta_off);
+      if (r > 0 && kk > 0) {
+        newid[(size_t)t] = new_block(T.out_off, kk, T.delta_off);
+        nadd += (size_t)kk;
+      }
       if (r > 0) {
         SolveRec R;
         R.nc = r;
@@ -1211,6 +1409,20 @@ struct Factorizer {
       if (r > 0) fl += dr * dr * dr / 3 + dr * dr * dk + dk * dk * dr;
       L.gflop += fl * 1e-9;
       L.gbytes += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
+    }
+    // the new delta blocks join the membership lists of their sk DOFs
+    member.ensure_room(nadd);
+    const int nthu = nt >= 64 ? nthreads : 1;
+#pragma omp parallel num_threads(nthu)
+    {
+      const int tid = omp_get_thread_num(), nth = omp_get_num_threads();
+      const int64_t lo = N * tid / nth, hi = N * (tid + 1) / nth;
+      for (int64_t t = 0; t < nt; ++t) {
+        if (newid[(size_t)t] < 0) continue;
+        const int32_t* out = h_idx.data() + tasks[(size_t)t].out_off;
+        for (int i = 0; i < k[(size_t)t]; ++i)
+          if (out[i] >= lo && out[i] < hi) member.add(out[i], newid[(size_t)t]);
+      }
     }
     L.t_upd = now_s() - tp;
     L.lap("retire");
@@ -1383,7 +1595,7 @@ struct Factorizer {
     L.nsmall = (int)small.size();
     L.max_nc = L.max_nq = 0;
     for (const SolveRec& R : small) { L.max_nc = std::max(L.max_nc, R.nc); L.max_nq = std::max(L.max_nq, R.nq); }
-    L.d_recs = to_device(small);
+    meta.add(&L.d_recs, small);
     if (large.empty()) return;
     auto mk = [](int M, int K, int am, int64_t A_off, int64_t lda, int xm, int64_t xo, int sm, int64_t so, int dm,
                  int64_t dof, double alpha) {
@@ -1420,15 +1632,16 @@ struct Factorizer {
     }
     F_->tile_rows = std::max(F_->tile_rows, rows);
     auto upload = [&](std::vector<std::vector<TileOp>>& ops, std::vector<LevelRec::Phase>& out) {
+      out.reserve(out.size() + ops.size());  // slots registered below stay put
       for (auto& v : ops) {
         std::vector<int2> work;
         for (int i = 0; i < (int)v.size(); ++i)
           for (int i0 = 0; i0 < std::max(v[(size_t)i].M, 1); i0 += 64) work.push_back(make_int2(i, i0));
-        LevelRec::Phase P;
-        P.d_ops = to_device(v);
-        P.d_work = to_device(work);
+        out.emplace_back();
+        LevelRec::Phase& P = out.back();
+        meta.add(&P.d_ops, v);
+        meta.add(&P.d_work, work);
         P.nwork = (int)work.size();
-        out.push_back(P);
       }
     };
     upload(F, L.fwd_ph);
@@ -1466,6 +1679,8 @@ struct Factorizer {
     const double t0 = now_s();
     N = g.ndof();
     HTRACE("factor start N=%lld", (long long)N);
+    LevelRec& P = prof;  // setup / finish sub-phases (HIFDE_PROFILE)
+    P.lap(nullptr);
     pinned_stage().begin(s);
     g_stage = &pinned_stage();
     struct StageOff {
@@ -1489,11 +1704,21 @@ struct Factorizer {
       HCK(cudaMallocAsync((void**)&d_indptr, (N + 1) * sizeof(int64_t), s));
       HCK(cudaMallocAsync((void**)&d_indices, std::max<int64_t>(nnz, 1) * sizeof(int32_t), s));
       HCK(cudaMallocAsync((void**)&d_a0, std::max<int64_t>(nnz, 1) * sizeof(double), s));
-      HCK(cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-      HCK(cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      HCK(cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
       own_a0 = true;
+      // pageable H2D copies block the calling thread: a helper thread issues
+      // them while this one runs the level-0 symbolic analysis (joined before
+      // the first kernel launch, a0_ready())
+      int dev = 0;
+      HCK(cudaGetDevice(&dev));
+      a0_thread = std::thread([=]() {
+        cudaSetDevice(dev);
+        cudaError_t e = cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s);
+        a0_err = e;
+      });
     }
+    P.lap("A0");
     active.assign((size_t)N, 1);
     HCK(cudaMallocAsync((void**)&d_active, std::max<int64_t>(N, 1), s));
     HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
@@ -1511,6 +1736,7 @@ struct Factorizer {
         ctx.clear();
         hc.g = g;
         hc.valid = true;
+        hc.variant = -1;  // arena hints belong to the previous grid
       } else {
         member.reset();
       }
@@ -1522,10 +1748,19 @@ struct Factorizer {
           x.stamp = 0;
         }
     }
-    F->fac.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
-    F->idx.reserve((size_t)std::max<int64_t>(16 * N, 1 << 16), s);
-    bvals.reserve((size_t)std::max<int64_t>(64 * N, 1 << 16), s);
+    P.lap("host-state");
+    {
+      HostCache& hc = host_cache();
+      const bool hint = hc.variant == opt.variant;
+      auto want = [&](size_t h, int64_t dflt) { return std::max<size_t>(hint ? h + h / 16 : 0, (size_t)dflt); };
+      F->fac.reserve(want(hc.hint_fac, std::max<int64_t>(64 * N, 1 << 16)), s);
+      F->idx.reserve(want(hc.hint_idx, std::max<int64_t>(16 * N, 1 << 16)), s);
+      bvals.reserve(want(hc.hint_bv, std::max<int64_t>(64 * N, 1 << 16)), s);
+      h_idx.reserve(want(hc.hint_idx, std::max<int64_t>(16 * N, 1 << 16)));
+      if (hint && hc.hint_scr) scratch.reserve(hc.hint_scr, s);
+    }
 
+    P.lap("reserve");
     const int Lv = g.nlevels;
     const double t_setup = now_s() - t0;
     HTRACE("setup done");
@@ -1592,11 +1827,18 @@ struct Factorizer {
       L.kind = 2;
       record_trace(L, tl);
     }
+    P.lap(nullptr);
     finish_reductions();
+    P.lap("reductions");
     // solve metadata to the device: small records one CTA each, large ones as
     // tiled product phases
     for (auto& L : F->levels) build_solve_plan(L);
+    F->meta = meta.commit(s, [&](void* d, const void* h, size_t n) {
+      if (!pinned_stage().copy(d, h, n)) HCK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s));
+    });
+    P.lap("solve-plan");
     HCK(cudaStreamSynchronize(s));
+    P.lap("sync");
     for (auto& L : F->levels) {
       if (L.ev0 && L.ev1) {
         float ms = 0.f;
@@ -1605,6 +1847,14 @@ struct Factorizer {
         cudaEventDestroy(L.ev1);
         L.ev0 = L.ev1 = nullptr;
       }
+    }
+    {
+      HostCache& hc = host_cache();
+      hc.variant = opt.variant;
+      hc.hint_fac = F->fac.n;
+      hc.hint_bv = bvals.n;
+      hc.hint_idx = h_idx.size();
+      hc.hint_scr = scratch.cap;
     }
     bvals.release(s);
     scratch.release(s);
@@ -1622,8 +1872,12 @@ struct Factorizer {
     }
     cudaFreeAsync(d_active, s);
     HCK(cudaStreamSynchronize(s));
+    P.lap("release");
     F->t_f = now_s() - t0;
     if (getenv("HIFDE_PROFILE")) {
+      fprintf(stderr, "[hifde] setup/finish:");
+      for (const auto& p : P.sub) fprintf(stderr, " %s %.3f", p.first, p.second * 1e3);
+      fprintf(stderr, "\n");
       fprintf(stderr, "[hifde] factor %.3f ms (setup %.3f ms)\n", F->t_f * 1e3, t_setup * 1e3);
       for (const auto& L : F->levels)
         fprintf(stderr,
