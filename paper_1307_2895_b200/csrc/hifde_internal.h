@@ -97,7 +97,8 @@ struct Arenas {
 constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA we use
 constexpr int kSchurTile = 64;                 // schur_tile_kernel tile edge
 constexpr int kPanelB = 64;                    // blocked Cholesky panel width
-constexpr int kMaxSkelNc = 192;                // largest group skeletonized by one CTA (skel_group)
+constexpr int kMaxSkelNc = 192;
+constexpr size_t kSolveDynSmem = 190 * 1024;   // solve record kernels: dynamic smem beside the 25 KB staging tile                // largest group skeletonized by one CTA (skel_group)
 
 // Kernel launchers (kernels_factor.cu / kernels_solve.cu).
 void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,

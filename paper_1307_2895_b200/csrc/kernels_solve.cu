@@ -62,27 +62,67 @@ __device__ void bwd_subst(const double* __restrict__ C, int n, double* x, int nr
   __syncthreads();
 }
 
-// y = P x and y = P^T x for the packed lower inverse P (n x n) and x n x nrhs.
-__device__ void pinv_apply(const double* __restrict__ P, int n, const double* x, double* y, int nrhs) {
-  for (int e = threadIdx.x; e < n * nrhs; e += NT) {
-    const int i = e / nrhs, r = e - i * nrhs;
-    const double* row = P + (size_t)i * (i + 1) / 2;
-    double s = 0.0;
-    for (int l = 0; l <= i; ++l) s += row[l] * x[(size_t)l * nrhs + r];
-    y[e] = s;
-  }
-}
-__device__ void pinv_apply_t(const double* __restrict__ P, int n, const double* x, double* y, int nrhs) {
-  for (int e = threadIdx.x; e < n * nrhs; e += NT) {
-    const int i = e / nrhs, r = e - i * nrhs;
-    double s = 0.0;
-    for (int l = i; l < n; ++l) s += P[(size_t)l * (l + 1) / 2 + i] * x[(size_t)l * nrhs + r];
-    y[e] = s;
-  }
-}
-
 __device__ __forceinline__ double* workspace(double* smem, double* scratch, int64_t per_rec) {
   return per_rec > 0 ? scratch + (size_t)blockIdx.x * per_rec : smem;
+}
+
+// One-CTA product Y (+)= alpha op(A) X, op(A) M x K, X K x nrhs and Y M x nrhs
+// row-major (ld nrhs).  A is streamed from global memory in 32-wide K chunks
+// staged (coalesced) in shared memory; 16 right-hand sides x 16 row groups
+// per pass, 6 rows per thread.  amode: 0 packed lower P, 1 its transpose,
+// 2 dense row-major (ld lda), 3 dense transposed.
+constexpr int kGKC = 32, kGRB = 16, kGMI = 6;
+constexpr int kGRows = (NT / kGRB) * kGMI;  // rows per pass (96)
+__device__ void cta_gemm(int M, int K, int amode, const double* __restrict__ A, int64_t lda, const double* X,
+                         double* Y, int nrhs, double alpha, bool accumulate, double* As) {
+  constexpr int RG = NT / kGRB;
+  const int rr = threadIdx.x % kGRB, rg = threadIdx.x / kGRB;
+  for (int m0 = 0; m0 < M; m0 += kGRows) {
+    const int mrows = min(kGRows, M - m0);
+    for (int r0 = 0; r0 < nrhs; r0 += kGRB) {
+      double acc[kGMI];
+#pragma unroll
+      for (int m = 0; m < kGMI; ++m) acc[m] = 0.0;
+      const int r = r0 + rr;
+      for (int k0 = 0; k0 < K; k0 += kGKC) {
+        const int kc = min(kGKC, K - k0);
+        __syncthreads();
+        if (amode == 0 || amode == 2) {
+          for (int e = threadIdx.x; e < mrows * kGKC; e += NT) {
+            const int ii = e / kGKC, kk = e - ii * kGKC, i = m0 + ii, k = k0 + kk;
+            double a = 0.0;
+            if (kk < kc) a = amode == 0 ? (k <= i ? A[(size_t)i * (i + 1) / 2 + k] : 0.0) : A[(size_t)i * lda + k];
+            As[ii * (kGKC + 1) + kk] = a;
+          }
+        } else {
+          for (int e = threadIdx.x; e < mrows * kGKC; e += NT) {
+            const int kk = e / mrows, ii = e - kk * mrows, i = m0 + ii, k = k0 + kk;
+            double a = 0.0;
+            if (kk < kc) a = amode == 1 ? (k >= i ? A[(size_t)k * (k + 1) / 2 + i] : 0.0) : A[(size_t)k * lda + i];
+            As[ii * (kGKC + 1) + kk] = a;
+          }
+        }
+        __syncthreads();
+        if (r < nrhs) {
+          for (int kk = 0; kk < kc; ++kk) {
+            const double x = X[(size_t)(k0 + kk) * nrhs + r];
+#pragma unroll
+            for (int m = 0; m < kGMI; ++m) acc[m] += As[(rg + RG * m) * (kGKC + 1) + kk] * x;
+          }
+        }
+      }
+      if (r < nrhs) {
+#pragma unroll
+        for (int m = 0; m < kGMI; ++m) {
+          const int ii = rg + RG * m;
+          if (ii >= mrows) continue;
+          double* y = Y + (size_t)(m0 + ii) * nrhs + r;
+          *y = (accumulate ? *y : 0.0) + alpha * acc[m];
+        }
+      }
+    }
+  }
+  __syncthreads();
 }
 
 }  // namespace
@@ -91,6 +131,7 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
     const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
     double* __restrict__ v, int nrhs, double* __restrict__ contrib, double* scratch, int64_t per_rec) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ double As[kGRows * (kGKC + 1)];
   const SolveRec rc = recs[blockIdx.x];
   const int nc = rc.nc, nq = rc.nq;
   double* s = workspace(sm, scratch, per_rec);
@@ -101,9 +142,7 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
     s[e] = v[(size_t)c[i] * nrhs + r];
   }
   if (rc.inv) {
-    __syncthreads();
-    pinv_apply(fac + rc.C_off, nc, s, s2, nrhs);
-    __syncthreads();
+    cta_gemm(nc, nc, 0, fac + rc.C_off, 0, s, s2, nrhs, 1.0, false, As);  // s2 = P s
     s = s2;
   } else {
     fwd_subst(fac + rc.C_off, nc, s, nrhs);
@@ -112,15 +151,8 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
     const int i = e / nrhs, r = e - i * nrhs;
     v[(size_t)c[i] * nrhs + r] = s[e];
   }
-  if (nq > 0) {
-    const double* W = fac + rc.W_off;
-    for (int e = threadIdx.x; e < nq * nrhs; e += NT) {
-      const int a = e / nrhs, r = e - a * nrhs;
-      double g = 0.0;
-      for (int k = 0; k < nc; ++k) g += W[(size_t)k * nq + a] * s[(size_t)k * nrhs + r];
-      contrib[(size_t)(rc.contrib_off + a) * nrhs + r] = g;
-    }
-  }
+  // contributions g = W^T s (W nc x nq row-major), summed per DOF later
+  if (nq > 0) cta_gemm(nq, nc, 3, fac + rc.W_off, nq, s, contrib + (size_t)rc.contrib_off * nrhs, nrhs, 1.0, false, As);
 }
 
 __global__ void solve_reduce_kernel(const int32_t* __restrict__ targets, const int64_t* __restrict__ ptr,
@@ -139,23 +171,27 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
     const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
     double* __restrict__ v, int nrhs, double* scratch, int64_t per_rec) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ double As[kGRows * (kGKC + 1)];
   const SolveRec rc = recs[blockIdx.x];
   const int nc = rc.nc, nq = rc.nq;
   double* t = workspace(sm, scratch, per_rec);
+  double* t2 = t + (size_t)nc * nrhs;
+  double* xq = t2 + (size_t)nc * nrhs;
   const int32_t* c = idx + rc.idx_off;
   const int32_t* q = c + nc;
-  const double* W = fac + rc.W_off;
   for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
     const int i = e / nrhs, r = e - i * nrhs;
-    double a = v[(size_t)c[i] * nrhs + r];
-    for (int b = 0; b < nq; ++b) a -= W[(size_t)i * nq + b] * v[(size_t)q[b] * nrhs + r];
-    t[e] = a;
+    t[e] = v[(size_t)c[i] * nrhs + r];
   }
+  for (int e = threadIdx.x; e < nq * nrhs; e += NT) {
+    const int b = e / nrhs, r = e - b * nrhs;
+    xq[e] = v[(size_t)q[b] * nrhs + r];
+  }
+  // t = v_c - W v_q  (W nc x nq row-major)
+  if (nq > 0) cta_gemm(nc, nq, 2, fac + rc.W_off, nq, xq, t, nrhs, -1.0, true, As);
+  else __syncthreads();
   if (rc.inv) {
-    double* t2 = t + (size_t)nc * nrhs;
-    __syncthreads();
-    pinv_apply_t(fac + rc.C_off, nc, t, t2, nrhs);
-    __syncthreads();
+    cta_gemm(nc, nc, 1, fac + rc.C_off, 0, t, t2, nrhs, 1.0, false, As);  // t2 = P^T t
     t = t2;
   } else {
     bwd_subst(fac + rc.C_off, nc, t, nrhs);
@@ -173,6 +209,7 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
     const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
     double* __restrict__ v, int nrhs, int forward, double* scratch, int64_t per_rec) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ double As[kGRows * (kGKC + 1)];
   const SolveRec rc = recs[blockIdx.x];
   const int r = rc.nc, k = rc.nq;
   double* xs = workspace(sm, scratch, per_rec);
@@ -192,50 +229,25 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
     xr[e] = v[(size_t)rd[b] * nrhs + j];
   }
   __syncthreads();
+  double* xo = xr;  // final v_rd
   if (forward) {
-    for (int e = threadIdx.x; e < r * nrhs; e += NT) {
-      const int b = e / nrhs, j = e - b * nrhs;
-      double a = xr[e];
-      for (int l = 0; l < k; ++l) a -= T[(size_t)l * r + b] * xs[(size_t)l * nrhs + j];
-      xr[e] = a;
-    }
+    if (k > 0) cta_gemm(r, k, 3, T, r, xs, xr, nrhs, -1.0, true, As);  // v_rd -= T^T v_sk
     if (rc.inv) {
-      __syncthreads();
-      pinv_apply(C, r, xr, x2, nrhs);
-      __syncthreads();
-      for (int e = threadIdx.x; e < r * nrhs; e += NT) xr[e] = x2[e];
-      __syncthreads();
+      cta_gemm(r, r, 0, C, 0, xr, x2, nrhs, 1.0, false, As);           // s = P v_rd
+      xo = x2;
     } else {
       fwd_subst(C, r, xr, nrhs);
     }
-    for (int e = threadIdx.x; e < k * nrhs; e += NT) {
-      const int a = e / nrhs, j = e - a * nrhs;
-      double x = xs[e];
-      for (int l = 0; l < r; ++l) x -= W[(size_t)l * k + a] * xr[(size_t)l * nrhs + j];
-      xs[e] = x;
-    }
+    if (k > 0) cta_gemm(k, r, 3, W, k, xo, xs, nrhs, -1.0, true, As);  // v_sk -= W^T s
   } else {
-    for (int e = threadIdx.x; e < r * nrhs; e += NT) {
-      const int b = e / nrhs, j = e - b * nrhs;
-      double a = xr[e];
-      for (int l = 0; l < k; ++l) a -= W[(size_t)b * k + l] * xs[(size_t)l * nrhs + j];
-      xr[e] = a;
-    }
+    if (k > 0) cta_gemm(r, k, 2, W, k, xs, xr, nrhs, -1.0, true, As);  // v_rd -= W v_sk
     if (rc.inv) {
-      __syncthreads();
-      pinv_apply_t(C, r, xr, x2, nrhs);
-      __syncthreads();
-      for (int e = threadIdx.x; e < r * nrhs; e += NT) xr[e] = x2[e];
-      __syncthreads();
+      cta_gemm(r, r, 1, C, 0, xr, x2, nrhs, 1.0, false, As);           // v_rd = P^T (...)
+      xo = x2;
     } else {
       bwd_subst(C, r, xr, nrhs);
     }
-    for (int e = threadIdx.x; e < k * nrhs; e += NT) {
-      const int a = e / nrhs, j = e - a * nrhs;
-      double x = xs[e];
-      for (int l = 0; l < r; ++l) x -= T[(size_t)a * r + l] * xr[(size_t)l * nrhs + j];
-      xs[e] = x;
-    }
+    if (k > 0) cta_gemm(k, r, 2, T, r, xo, xs, nrhs, -1.0, true, As);  // v_sk -= T v_rd
   }
   __syncthreads();
   for (int e = threadIdx.x; e < k * nrhs; e += NT) {
@@ -244,7 +256,7 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
   }
   for (int e = threadIdx.x; e < r * nrhs; e += NT) {
     const int b = e / nrhs, j = e - b * nrhs;
-    v[(size_t)rd[b] * nrhs + j] = xr[e];
+    v[(size_t)rd[b] * nrhs + j] = xo[e];
   }
 }
 
@@ -331,7 +343,7 @@ void launch_solve_tiles(const TileOp* ops, const int2* work, int nwork, const in
 }
 
 static void set_smem_attr(const void* fn) {
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveDynSmem);
 }
 
 void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,

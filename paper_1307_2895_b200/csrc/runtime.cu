@@ -1912,11 +1912,11 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   size_t scratch_need = 0;
   auto ws_plan = [&](const LevelRec& L, int64_t per_rec_doubles, size_t& smem, int64_t& per_rec) {
     const size_t need = (size_t)per_rec_doubles * sizeof(double);
-    if (need <= kSmemCap) { smem = need; per_rec = 0; }
+    if (need <= kSolveDynSmem) { smem = need; per_rec = 0; }
     else { smem = 0; per_rec = per_rec_doubles; scratch_need = std::max(scratch_need, (size_t)per_rec * L.nsmall); }
   };
   auto ws_of = [&](const LevelRec& L) {
-    return L.kind == 1 ? (int64_t)(2 * L.max_nc + L.max_nq) * nrhs : (int64_t)2 * L.max_nc * nrhs;
+    return (int64_t)(2 * L.max_nc + L.max_nq) * nrhs;  // two nc blocks + the neighbour block
   };
   for (const auto& L : F->levels) {
     size_t sm; int64_t pr;
