@@ -10,6 +10,7 @@
  *                     factor_hifde3x (src/driver.py:228-251)
  *                     factor_mf      (src/driver.py:201-209)
  *   hifde_solve    <- GeneralizedLDL.apply_inverse (src/driver.py:113-129)
+ *   hifde_apply    <- GeneralizedLDL.apply (src/driver.py:95-111)
  *                     and module-level apply_inverse (src/driver.py:258-259)
  *   hifde_get_info / hifde_get_level
  *                  <- GeneralizedLDL.metrics (src/driver.py:165-171)
@@ -123,6 +124,13 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
  * Reentrant for a finished factor; b and x may alias.
  */
 int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n,
+                int nrhs, int device_ptrs, void* stream);
+
+/*
+ * y = F x (the factored operator, ~ A x), same layout and pointer rules as
+ * hifde_solve; apply(apply_inverse(b)) == b up to rounding.
+ */
+int hifde_apply(const hifde_factor_t* f, const double* x, double* y, int64_t n,
                 int nrhs, int device_ptrs, void* stream);
 
 int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info);

@@ -154,7 +154,12 @@ void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, c
                            int64_t scratch_per_rec, size_t smem, cudaStream_t s);
 void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,
                          int ntargets, const double* contrib, double* v, int nrhs,
-                         cudaStream_t s);
+                         cudaStream_t s, double sign = -1.0);
+void launch_apply_elim(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,
+                       double* contrib, double* scratch, int64_t scratch_per_rec, size_t smem, int fwdinv,
+                       cudaStream_t s);
+void launch_apply_skel(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,
+                       double* scratch, int64_t scratch_per_rec, size_t smem, int fwdinv, cudaStream_t s);
 void launch_solve_elim_bwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
                            double* v, int nrhs, double* scratch, int64_t scratch_per_rec,
                            size_t smem, cudaStream_t s);

@@ -62,6 +62,38 @@ __device__ void bwd_subst(const double* __restrict__ C, int n, double* x, int nr
   __syncthreads();
 }
 
+// x <- P^{-1} x and x <- P^{-T} x for the packed lower P (i.e. x <- C x and
+// x <- C^T x for the Cholesky factor C = P^{-1}); column-oriented, one
+// barrier per row.
+__device__ void psolve_lower(const double* __restrict__ P, int n, double* x, int nrhs) {
+  for (int i = 0; i < n; ++i) {
+    __syncthreads();
+    const double pinv = 1.0 / P[(size_t)i * (i + 1) / 2 + i];
+    for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)i * nrhs + r] *= pinv;
+    __syncthreads();
+    const int rows = n - i - 1;
+    for (int e = threadIdx.x; e < rows * nrhs; e += NT) {
+      const int l = i + 1 + e / nrhs, r = e - (e / nrhs) * nrhs;
+      x[(size_t)l * nrhs + r] -= P[(size_t)l * (l + 1) / 2 + i] * x[(size_t)i * nrhs + r];
+    }
+  }
+  __syncthreads();
+}
+__device__ void psolve_upper(const double* __restrict__ P, int n, double* x, int nrhs) {
+  for (int i = n - 1; i >= 0; --i) {
+    __syncthreads();
+    const double pinv = 1.0 / P[(size_t)i * (i + 1) / 2 + i];
+    for (int r = threadIdx.x; r < nrhs; r += NT) x[(size_t)i * nrhs + r] *= pinv;
+    __syncthreads();
+    const double* row = P + (size_t)i * (i + 1) / 2;
+    for (int e = threadIdx.x; e < i * nrhs; e += NT) {
+      const int l = e / nrhs, r = e - l * nrhs;
+      x[(size_t)l * nrhs + r] -= row[l] * x[(size_t)i * nrhs + r];
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ double* workspace(double* smem, double* scratch, int64_t per_rec) {
   return per_rec > 0 ? scratch + (size_t)blockIdx.x * per_rec : smem;
 }
@@ -158,13 +190,13 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
 __global__ void solve_reduce_kernel(const int32_t* __restrict__ targets, const int64_t* __restrict__ ptr,
                                     const int64_t* __restrict__ ent, int ntargets,
                                     const double* __restrict__ contrib, double* __restrict__ v,
-                                    int nrhs) {
+                                    int nrhs, double sign) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)ntargets * nrhs) return;
   const int t = (int)(e / nrhs), r = (int)(e % nrhs);
   double acc = 0.0;
   for (int64_t p = ptr[t]; p < ptr[t + 1]; ++p) acc += contrib[(size_t)ent[p] * nrhs + r];
-  v[(size_t)targets[t] * nrhs + r] -= acc;
+  v[(size_t)targets[t] * nrhs + r] += sign * acc;
 }
 
 __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
@@ -257,6 +289,94 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
   for (int e = threadIdx.x; e < r * nrhs; e += NT) {
     const int b = e / nrhs, j = e - b * nrhs;
     v[(size_t)rd[b] * nrhs + j] = xo[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// F x (GeneralizedLDL.apply, src/driver.py:95-111): the solve sweep inverted.
+// apply_inverse = Fwd_0 .. Fwd_top, Bwd_top .. Bwd_0, so
+// apply = BwdInv_0 .. BwdInv_top, FwdInv_top .. FwdInv_0 with, per record
+// (C = P^-1 the Cholesky factor, P the stored packed inverse):
+//   elimination BwdInv: v_c = C^T v_c + W v_q
+//               FwdInv: v_q += W^T v_c (contributions), v_c = C v_c
+//   skeleton    BwdInv: v_sk += T v_rd ; v_rd = C^T v_rd + W v_sk
+//               FwdInv: v_sk += W^T v_rd ; v_rd = C v_rd + T^T v_sk
+// Every record of a level (small and large) runs one CTA.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) apply_elim_kernel(
+    const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
+    double* __restrict__ v, int nrhs, double* __restrict__ contrib, double* scratch, int64_t per_rec, int fwdinv) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double As[kGRows * (kGKC + 1)];
+  const SolveRec rc = recs[blockIdx.x];
+  const int nc = rc.nc, nq = rc.nq;
+  double* t = workspace(sm, scratch, per_rec);
+  double* xq = t + (size_t)nc * nrhs;
+  const int32_t* c = idx + rc.idx_off;
+  const int32_t* q = c + nc;
+  const double* P = fac + rc.C_off;
+  for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    t[e] = v[(size_t)c[i] * nrhs + r];
+  }
+  if (!fwdinv) {
+    for (int e = threadIdx.x; e < nq * nrhs; e += NT) {
+      const int b = e / nrhs, r = e - b * nrhs;
+      xq[e] = v[(size_t)q[b] * nrhs + r];
+    }
+    psolve_upper(P, nc, t, nrhs);                                                   // C^T v_c
+    if (nq > 0) cta_gemm(nc, nq, 2, fac + rc.W_off, nq, xq, t, nrhs, 1.0, true, As);  // + W v_q
+  } else {
+    __syncthreads();
+    if (nq > 0) cta_gemm(nq, nc, 3, fac + rc.W_off, nq, t, contrib + (size_t)rc.contrib_off * nrhs, nrhs, 1.0, false, As);
+    psolve_lower(P, nc, t, nrhs);                                                   // C v_c
+  }
+  for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    v[(size_t)c[i] * nrhs + r] = t[e];
+  }
+}
+
+__global__ void __launch_bounds__(NT) apply_skel_kernel(
+    const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
+    double* __restrict__ v, int nrhs, double* scratch, int64_t per_rec, int fwdinv) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double As[kGRows * (kGKC + 1)];
+  const SolveRec rc = recs[blockIdx.x];
+  const int r = rc.nc, k = rc.nq;
+  double* xs = workspace(sm, scratch, per_rec);
+  double* xr = xs + (size_t)k * nrhs;
+  const int32_t* sk = idx + rc.idx_off;
+  const int32_t* rd = sk + k;
+  const double* T = fac + rc.T_off;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < k * nrhs; e += NT) {
+    const int a = e / nrhs, j = e - a * nrhs;
+    xs[e] = v[(size_t)sk[a] * nrhs + j];
+  }
+  for (int e = threadIdx.x; e < r * nrhs; e += NT) {
+    const int b = e / nrhs, j = e - b * nrhs;
+    xr[e] = v[(size_t)rd[b] * nrhs + j];
+  }
+  __syncthreads();
+  if (!fwdinv) {
+    if (k > 0) cta_gemm(k, r, 2, T, r, xr, xs, nrhs, 1.0, true, As);   // v_sk += T v_rd
+    psolve_upper(P, r, xr, nrhs);                                       // C^T v_rd
+    if (k > 0) cta_gemm(r, k, 2, W, k, xs, xr, nrhs, 1.0, true, As);   // + W v_sk
+  } else {
+    if (k > 0) cta_gemm(k, r, 3, W, k, xr, xs, nrhs, 1.0, true, As);   // v_sk += W^T v_rd
+    psolve_lower(P, r, xr, nrhs);                                       // C v_rd
+    if (k > 0) cta_gemm(r, k, 3, T, r, xs, xr, nrhs, 1.0, true, As);   // + T^T v_sk
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * nrhs; e += NT) {
+    const int a = e / nrhs, j = e - a * nrhs;
+    v[(size_t)sk[a] * nrhs + j] = xs[e];
+  }
+  for (int e = threadIdx.x; e < r * nrhs; e += NT) {
+    const int b = e / nrhs, j = e - b * nrhs;
+    v[(size_t)rd[b] * nrhs + j] = xr[e];
   }
 }
 
@@ -356,11 +476,12 @@ void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, c
 }
 
 void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,
-                         int ntargets, const double* contrib, double* v, int nrhs, cudaStream_t s) {
+                         int ntargets, const double* contrib, double* v, int nrhs, cudaStream_t s,
+                         double sign) {
   if (ntargets <= 0) return;
   const int64_t total = (int64_t)ntargets * nrhs;
   const int blocks = (int)((total + 255) / 256);
-  solve_reduce_kernel<<<blocks, 256, 0, s>>>(targets, ptr, ent, ntargets, contrib, v, nrhs);
+  solve_reduce_kernel<<<blocks, 256, 0, s>>>(targets, ptr, ent, ntargets, contrib, v, nrhs, sign);
 }
 
 void launch_solve_elim_bwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
@@ -379,6 +500,23 @@ void launch_solve_skel(const SolveRec* recs, int nrec, const int32_t* idx, const
   static bool once = (set_smem_attr((const void*)solve_skel_kernel), true);
   (void)once;
   solve_skel_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward, scratch, scratch_per_rec);
+}
+
+void launch_apply_elim(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,
+                       double* contrib, double* scratch, int64_t scratch_per_rec, size_t smem, int fwdinv,
+                       cudaStream_t s) {
+  if (nrec <= 0) return;
+  static bool once = (set_smem_attr((const void*)apply_elim_kernel), true);
+  (void)once;
+  apply_elim_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib, scratch, scratch_per_rec, fwdinv);
+}
+
+void launch_apply_skel(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,
+                       double* scratch, int64_t scratch_per_rec, size_t smem, int fwdinv, cudaStream_t s) {
+  if (nrec <= 0) return;
+  static bool once = (set_smem_attr((const void*)apply_skel_kernel), true);
+  (void)once;
+  apply_skel_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, scratch, scratch_per_rec, fwdinv);
 }
 
 }  // namespace hifde

@@ -230,6 +230,8 @@ struct LevelRec {
   std::vector<SolveRec> recs;
   SolveRec* d_recs = nullptr;
   int nsmall = 0;
+  SolveRec* d_all = nullptr;  // every record of the level (apply)
+  int nall = 0, all_max_nc = 0, all_max_nq = 0;
   int max_nc = 0, max_nq = 0;
   struct Phase {
     TileOp* d_ops = nullptr;
@@ -1589,6 +1591,12 @@ struct Factorizer {
   // Split a level's records: large ones (by size) become tiled product phases
   // (TileOp), the rest stay one-CTA records.
   void build_solve_plan(LevelRec& L) {
+    L.nall = (int)L.recs.size();
+    for (const SolveRec& R : L.recs) {
+      L.all_max_nc = std::max(L.all_max_nc, R.nc);
+      L.all_max_nq = std::max(L.all_max_nq, R.nq);
+    }
+    meta.add(&L.d_all, L.recs);
     auto is_large = [](const SolveRec& R) { return R.nc > 96 || R.nq > 192; };
     std::vector<SolveRec> small, large;
     for (const SolveRec& R : L.recs) (is_large(R) ? large : small).push_back(R);
@@ -1971,6 +1979,59 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   if (!dev) HCK(cudaStreamSynchronize(s));
 }
 
+// y = F x: the solve sweep inverted record by record (kernels_solve.cu).
+void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, bool dev, cudaStream_t s) {
+  const int64_t N = F->n;
+  const size_t bytes = (size_t)N * nrhs * sizeof(double);
+  double* v = nullptr;
+  HCK(cudaMallocAsync((void**)&v, std::max<size_t>(bytes, 8), s));
+  HCK(cudaMemcpyAsync(v, x, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  double* contrib = nullptr;
+  HCK(cudaMallocAsync((void**)&contrib, std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
+  size_t scratch_need = 0;
+  auto plan = [&](const LevelRec& L, size_t& smem, int64_t& per_rec) {
+    const int64_t d = (int64_t)(L.all_max_nc + L.all_max_nq) * nrhs;
+    const size_t need = (size_t)d * sizeof(double);
+    if (need <= kSolveDynSmem) { smem = need; per_rec = 0; }
+    else { smem = 0; per_rec = d; scratch_need = std::max(scratch_need, (size_t)d * L.nall); }
+  };
+  for (const auto& L : F->levels) { size_t a; int64_t b; plan(L, a, b); }
+  double* scratch = nullptr;
+  HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
+  const int32_t* idx = F->idx.p;
+  const double* fac = F->fac.p;
+  const size_t nl = F->levels.size();
+  for (size_t li = 0; li < nl; ++li) {  // inverse of the backward sweep, level 0 first
+    const LevelRec& L = F->levels[li];
+    size_t sm; int64_t pr;
+    plan(L, sm, pr);
+    if (L.kind == 1) launch_apply_skel(L.d_all, L.nall, idx, fac, v, nrhs, scratch, pr, sm, 0, s);
+    else launch_apply_elim(L.d_all, L.nall, idx, fac, v, nrhs, contrib, scratch, pr, sm, 0, s);
+    if (L.nall) ++g_launches;
+  }
+  for (size_t li = nl; li-- > 0;) {  // inverse of the forward sweep, top first
+    const LevelRec& L = F->levels[li];
+    size_t sm; int64_t pr;
+    plan(L, sm, pr);
+    if (L.kind == 1) {
+      launch_apply_skel(L.d_all, L.nall, idx, fac, v, nrhs, scratch, pr, sm, 1, s);
+    } else {
+      launch_apply_elim(L.d_all, L.nall, idx, fac, v, nrhs, contrib, scratch, pr, sm, 1, s);
+      if (L.kind == 0 && L.ntargets) {
+        launch_solve_reduce(L.d_targets, L.d_ptr, L.d_ent, L.ntargets, contrib, v, nrhs, s, 1.0);
+        ++g_launches;
+      }
+    }
+    if (L.nall) ++g_launches;
+  }
+  HCK(cudaGetLastError());
+  HCK(cudaMemcpyAsync(y, v, bytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  HCK(cudaFreeAsync(v, s));
+  HCK(cudaFreeAsync(contrib, s));
+  HCK(cudaFreeAsync(scratch, s));
+  if (!dev) HCK(cudaStreamSynchronize(s));
+}
+
 int fail_to_status(const Fail& f) {
   g_err = f.msg;
   return f.code;
@@ -2105,6 +2166,22 @@ int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n, 
     HCK(cudaSetDevice(f->device));
     cudaStream_t s = stream ? (cudaStream_t)stream : f->stream;
     do_solve(f, b, x, nrhs, device_ptrs != 0, s);
+  } catch (const Fail& e) {
+    return fail_to_status(e);
+  }
+  return HIFDE_OK;
+}
+
+int hifde_apply(const hifde_factor_t* f, const double* x, double* y, int64_t n, int nrhs,
+                int device_ptrs, void* stream) {
+  g_err.clear();
+  g_launches = 0;
+  if (!f || !x || !y) { g_err = "null argument"; return HIFDE_BADARG; }
+  if (n != f->n || nrhs < 1) { g_err = "vector shape mismatch"; return HIFDE_BADARG; }
+  try {
+    HCK(cudaSetDevice(f->device));
+    cudaStream_t s = stream ? (cudaStream_t)stream : f->stream;
+    do_apply(f, x, y, nrhs, device_ptrs != 0, s);
   } catch (const Fail& e) {
     return fail_to_status(e);
   }

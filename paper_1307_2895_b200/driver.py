@@ -122,6 +122,26 @@ class GeneralizedLDL:
                 _raise(self._lib, code)
         return out
 
+    def apply(self, x) -> np.ndarray:
+        """y ~= A x through the factored operator (src/driver.py:95-111); host arrays."""
+        arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+        if arr.shape[0] != self.n:
+            raise ValueError("vector has the wrong length")
+        nrhs = 1 if arr.ndim == 1 else arr.shape[1]
+        out = np.empty_like(arr)
+        if arr.size:
+            code = self._lib.hifde_apply(self._h, arr.ctypes.data, out.ctypes.data, self.n, nrhs, 0, None)
+            if code:
+                _raise(self._lib, code)
+        return out
+
+    def apply_device(self, x_ptr: int, y_ptr: int, nrhs: int, stream: Optional[int] = None):
+        """Device-pointer variant of apply (row-major N x nrhs float64 buffers)."""
+        code = self._lib.hifde_apply(self._h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), self.n, nrhs, 1,
+                                     C.c_void_p(stream) if stream else None)
+        if code:
+            _raise(self._lib, code)
+
     def apply_inverse_device(self, b_ptr: int, x_ptr: int, nrhs: int, stream: Optional[int] = None):
         """Device-pointer variant (row-major N x nrhs float64 buffers)."""
         code = self._lib.hifde_solve(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), self.n, nrhs, 1,

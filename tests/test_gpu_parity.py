@@ -69,6 +69,39 @@ def test_gpu_matches_reference_golden(name, order):
     assert abs(rep.n_i - int(gd["pcg_iters"])) <= max(1, int(0.2 * int(gd["pcg_iters"])))
 
 
+@pytest.mark.parametrize("name", NAMES)
+def test_apply_matches_reference_golden(name):
+    """F x through the GPU factor (GeneralizedLDL.apply, src/driver.py:95-111):
+    ||F x - A x|| / ||A x|| within 10x the reference's on the golden vector,
+    and apply inverts apply_inverse."""
+    gd = G.load(name)
+    _, csr = G.build_problem(gd)
+    g, f = _factor(gd, csr)
+    xa = np.random.default_rng(2).standard_normal(g.ndof)
+    ax = csr @ xa
+    err = np.linalg.norm(f.apply(xa) - ax) / np.linalg.norm(ax)
+    assert err <= 10 * float(gd["apply_err"]) + 1e-13, (err, float(gd["apply_err"]))
+    b = G.rhs(gd, g.ndof)
+    back = f.apply(f.apply_inverse(b))
+    assert np.linalg.norm(back - b) <= 1e-9 * np.linalg.norm(b)
+    y = np.empty_like(b)
+    y2 = f.apply(b)
+    for j in range(b.shape[1]):  # vector and block right-hand sides agree
+        y[:, j] = f.apply(b[:, j])
+    assert np.allclose(y, y2, rtol=1e-12, atol=1e-14 * np.abs(y2).max())
+
+
+def test_apply_large_cells_round_trip():
+    """apply on factors with cells beyond the one-CTA paths (blocked inverse,
+    tiled solve records): still the exact inverse of apply_inverse."""
+    g = H.build_grid(3, 24, 3)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=1))
+    f = H.factor_mf(a, g)
+    b = np.random.default_rng(3).standard_normal((g.ndof, 3))
+    assert np.linalg.norm(f.apply(f.apply_inverse(b)) - b) <= 1e-9 * np.linalg.norm(b)
+    assert np.linalg.norm(f.apply(b) - a @ b) <= 1e-10 * np.linalg.norm(a @ b)
+
+
 @pytest.mark.parametrize("name", ["g2d_n32_m4", "g2d_n64_m4_hc", "g3d_n16_m4_x_hc", "g3d_n16_m2_x"])
 def test_gpu_exact_order_matches_oracle(name):
     """In exact (reference) order the GPU's ranks equal the sequential oracle's
@@ -87,6 +120,8 @@ def test_gpu_exact_order_matches_oracle(name):
     r = np.max(np.linalg.norm(csr @ x - b, axis=0) / np.linalg.norm(b, axis=0))
     ro = np.max(np.linalg.norm(csr @ xo - b, axis=0) / np.linalg.norm(b, axis=0))
     assert r <= 10 * ro + 1e-14
+    y, yo = f.apply(b), fo.apply(b)  # the factored operators agree
+    assert np.linalg.norm(y - yo) <= 1e-6 * np.linalg.norm(yo)
 
 
 def test_mf_exact_and_matches_oracle_operator():
