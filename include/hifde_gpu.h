@@ -11,6 +11,7 @@
  *                     factor_mf      (src/driver.py:201-209)
  *   hifde_solve    <- GeneralizedLDL.apply_inverse (src/driver.py:113-129)
  *   hifde_apply    <- GeneralizedLDL.apply (src/driver.py:95-111)
+ *   hifde_pcg      <- pcg(A, b, F.apply_inverse) (src/krylov.py:48-77)
  *                     and module-level apply_inverse (src/driver.py:258-259)
  *   hifde_get_info / hifde_get_level
  *                  <- GeneralizedLDL.metrics (src/driver.py:165-171)
@@ -132,6 +133,17 @@ int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n,
  */
 int hifde_apply(const hifde_factor_t* f, const double* x, double* y, int64_t n,
                 int nrhs, int device_ptrs, void* stream);
+
+/*
+ * Preconditioned CG on A x = b (A in CSR, the matrix the factor approximates)
+ * with F^{-1} as preconditioner, run on the device: converged when
+ * ||b - A x|| / ||b|| <= tol.  One right-hand side; host (device_ptrs = 0) or
+ * device pointers for A, b and x alike.
+ */
+int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* indices,
+              const double* vals, const double* b, double* x, int64_t n, double tol,
+              int max_iter, int device_ptrs, void* stream, int* iters, double* residual,
+              int* converged);
 
 int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info);
 int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info);

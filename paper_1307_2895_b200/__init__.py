@@ -14,6 +14,6 @@ from .driver import (FactorizationError, GeneralizedLDL, IndefiniteBlockError,
                      factor_hifde3x, factor_mf)
 from .problems import (CoeffField, GridConfig, assemble, baseline_problem, build_grid,
                        constant_field, gaussian_contrast_field, high_contrast_field)
-from .solvers import pcg
+from .solvers import pcg, pcg_gpu
 
 __version__ = "0.1.0"

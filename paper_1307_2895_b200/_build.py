@@ -20,6 +20,7 @@ SOURCES = [
     "csrc/kernels_big.cu",
     "csrc/kernels_skelbig.cu",
     "csrc/kernels_solve.cu",
+    "csrc/kernels_krylov.cu",
     "csrc/runtime.cu",
     "csrc/partition.cpp",
 ]

@@ -66,7 +66,7 @@ class LevelInfo(C.Structure):
 # every symbol the public header declares
 EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
-    "hifde_solve", "hifde_apply", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
+    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
     "hifde_free", "hifde_last_error", "hifde_partition",
 ]
 
@@ -98,6 +98,10 @@ def load(path: str | None = None):
     lib.hifde_solve.restype = C.c_int
     lib.hifde_apply.argtypes = lib.hifde_solve.argtypes
     lib.hifde_apply.restype = C.c_int
+    lib.hifde_pcg.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_int64, C.c_double, C.c_int, C.c_int, C.c_void_p,
+                              C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int)]
+    lib.hifde_pcg.restype = C.c_int
     lib.hifde_get_info.argtypes = [C.c_void_p, P(Info)]
     lib.hifde_get_info.restype = C.c_int
     lib.hifde_get_level.argtypes = [C.c_void_p, C.c_int, P(LevelInfo)]

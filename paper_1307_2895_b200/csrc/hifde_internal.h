@@ -155,6 +155,14 @@ void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, c
 void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,
                          int ntargets, const double* contrib, double* v, int nrhs,
                          cudaStream_t s, double sign = -1.0);
+// kernels_krylov.cu (device-resident PCG)
+void launch_spmv(const int64_t* ip, const int32_t* ix, const double* va, const double* x, double* y, int64_t n,
+                 cudaStream_t s);
+void launch_dot(const double* a, const double* c, int64_t n, double* partial, double* out, cudaStream_t s);
+int dot_partials();
+void launch_cg_xr(double* x, double* r, const double* p, const double* ap, const double* sc, int64_t n,
+                  cudaStream_t s);
+void launch_cg_p(double* p, const double* z, double* sc, int64_t n, cudaStream_t s);
 void launch_apply_elim(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,
                        double* contrib, double* scratch, int64_t scratch_per_rec, size_t smem, int fwdinv,
                        cudaStream_t s);

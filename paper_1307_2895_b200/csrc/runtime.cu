@@ -2032,6 +2032,82 @@ void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, boo
   if (!dev) HCK(cudaStreamSynchronize(s));
 }
 
+// Preconditioned CG with A (CSR) and the factor as preconditioner, all on the
+// device (src/krylov.py:48-77): the host only reads ||r|| each iteration.
+void do_pcg(const hifde_factor_t* F, const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz,
+            const double* b, double* x, double tol, int max_iter, bool dev, cudaStream_t s, int* iters,
+            double* resid, int* converged) {
+  const int64_t N = F->n;
+  const size_t vb = (size_t)std::max<int64_t>(N, 1) * sizeof(double);
+  const int64_t *d_ip = ip;
+  const int32_t* d_ix = ix;
+  const double* d_va = va;
+  std::vector<void*> owned;
+  auto dalloc = [&](size_t bytes) {
+    void* p = nullptr;
+    HCK(cudaMallocAsync(&p, std::max<size_t>(bytes, 8), s));
+    owned.push_back(p);
+    return p;
+  };
+  if (!dev) {
+    int64_t* a = (int64_t*)dalloc((N + 1) * sizeof(int64_t));
+    int32_t* c = (int32_t*)dalloc(nnz * sizeof(int32_t));
+    double* v = (double*)dalloc(nnz * sizeof(double));
+    HCK(cudaMemcpyAsync(a, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    HCK(cudaMemcpyAsync(c, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    HCK(cudaMemcpyAsync(v, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+    d_ip = a; d_ix = c; d_va = v;
+  }
+  double* xv = (double*)dalloc(vb);
+  double* r = (double*)dalloc(vb);
+  double* z = (double*)dalloc(vb);
+  double* p = (double*)dalloc(vb);
+  double* ap = (double*)dalloc(vb);
+  double* part = (double*)dalloc(sizeof(double) * dot_partials());
+  double* sc = (double*)dalloc(sizeof(double) * 8);  // rz, pAp, rr, rz_new, bb
+  HCK(cudaMemcpyAsync(r, b, vb, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  HCK(cudaMemsetAsync(xv, 0, vb, s));
+  double* hs = nullptr;  // pinned readback of the residual
+  HCK(cudaMallocHost((void**)&hs, 2 * sizeof(double)));
+  struct Free {
+    std::vector<void*>& o; double* h; cudaStream_t s;
+    ~Free() { for (void* q : o) cudaFreeAsync(q, s); if (h) cudaFreeHost(h); }
+  } fr{owned, hs, s};
+  launch_dot(r, r, N, part, sc + 4, s);
+  HCK(cudaMemcpyAsync(hs, sc + 4, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HCK(cudaStreamSynchronize(s));
+  const double bnorm = std::sqrt(hs[0]);
+  *iters = 0; *resid = 0.0; *converged = 1;
+  if (bnorm == 0.0) {
+    HCK(cudaMemcpyAsync(x, xv, vb, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    return;
+  }
+  do_solve(F, r, z, 1, true, s);
+  HCK(cudaMemcpyAsync(p, z, vb, cudaMemcpyDeviceToDevice, s));
+  launch_dot(r, z, N, part, sc + 0, s);
+  double res = 1.0;
+  *converged = 0;
+  int it = 1;
+  for (; it <= max_iter; ++it) {
+    launch_spmv(d_ip, d_ix, d_va, p, ap, N, s);
+    launch_dot(p, ap, N, part, sc + 1, s);
+    launch_cg_xr(xv, r, p, ap, sc, N, s);
+    launch_dot(r, r, N, part, sc + 2, s);
+    HCK(cudaMemcpyAsync(hs, sc + 2, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    res = std::sqrt(hs[0]) / bnorm;
+    if (res <= tol) { *converged = 1; break; }
+    do_solve(F, r, z, 1, true, s);
+    launch_dot(r, z, N, part, sc + 3, s);
+    launch_cg_p(p, z, sc, N, s);
+  }
+  *iters = std::min(it, max_iter);
+  *resid = res;
+  HCK(cudaMemcpyAsync(x, xv, vb, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  HCK(cudaStreamSynchronize(s));
+}
+
 int fail_to_status(const Fail& f) {
   g_err = f.msg;
   return f.code;
@@ -2182,6 +2258,29 @@ int hifde_apply(const hifde_factor_t* f, const double* x, double* y, int64_t n, 
     HCK(cudaSetDevice(f->device));
     cudaStream_t s = stream ? (cudaStream_t)stream : f->stream;
     do_apply(f, x, y, nrhs, device_ptrs != 0, s);
+  } catch (const Fail& e) {
+    return fail_to_status(e);
+  }
+  return HIFDE_OK;
+}
+
+int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* indices, const double* vals,
+              const double* b, double* x, int64_t n, double tol, int max_iter, int device_ptrs, void* stream,
+              int* iters, double* residual, int* converged) {
+  g_err.clear();
+  g_launches = 0;
+  if (!f || !indptr || !indices || !vals || !b || !x || !iters || !residual || !converged) {
+    g_err = "null argument";
+    return HIFDE_BADARG;
+  }
+  if (n != f->n || max_iter < 1 || !(tol >= 0.0)) { g_err = "bad pcg arguments"; return HIFDE_BADARG; }
+  try {
+    HCK(cudaSetDevice(f->device));
+    cudaStream_t s = stream ? (cudaStream_t)stream : f->stream;
+    int64_t nnz = 0;
+    if (device_ptrs) HCK(cudaMemcpy(&nnz, indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    else nnz = indptr[n];
+    do_pcg(f, indptr, indices, vals, nnz, b, x, tol, max_iter, device_ptrs != 0, s, iters, residual, converged);
   } catch (const Fail& e) {
     return fail_to_status(e);
   }

@@ -46,3 +46,28 @@ def pcg(a, b, precond=None, tol: float = 1e-12, max_iter: int = 1000) -> SolveRe
         p = z + (rz_new / rz) * p
         rz = rz_new
     return SolveReport(x, max_iter, res, False)
+
+
+def pcg_gpu(f, a, b, tol: float = 1e-12, max_iter: int = 1000) -> SolveReport:
+    """The same PCG run on the device (hifde_pcg): SpMV, dot products and
+    updates in CUDA kernels, ``f.apply_inverse`` as the preconditioner without
+    host round trips (the host reads one residual per iteration)."""
+    import ctypes as C
+    import scipy.sparse as sp
+
+    csr = sp.csr_matrix(a) if not sp.isspmatrix_csr(a) else a
+    ip = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(csr.indices, dtype=np.int32)
+    va = np.ascontiguousarray(csr.data, dtype=np.float64)
+    bb = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    if bb.ndim != 1 or bb.shape[0] != f.n:
+        raise ValueError("pcg_gpu takes one right-hand side of length N")
+    x = np.empty_like(bb)
+    it, res, conv = C.c_int(), C.c_double(), C.c_int()
+    code = f._lib.hifde_pcg(f._h, ip.ctypes.data, ix.ctypes.data, va.ctypes.data, bb.ctypes.data,
+                            x.ctypes.data, f.n, float(tol), int(max_iter), 0, None,
+                            C.byref(it), C.byref(res), C.byref(conv))
+    if code:
+        from .driver import _raise
+        _raise(f._lib, code)
+    return SolveReport(x, int(it.value), float(res.value), bool(conv.value))

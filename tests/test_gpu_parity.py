@@ -91,6 +91,27 @@ def test_apply_matches_reference_golden(name):
     assert np.allclose(y, y2, rtol=1e-12, atol=1e-14 * np.abs(y2).max())
 
 
+@pytest.mark.parametrize("name", ["g2d_n64_m8_gauss", "g2d_n64_m4_hc", "g3d_n16_m4_x_gauss", "g2d_cfg1"])
+def test_pcg_gpu_matches_reference(name):
+    """Device-resident PCG (hifde_pcg) against the reference's pcg on its own
+    factor (src/krylov.py:48-77): iteration count and the converged solution."""
+    gd = G.load(name)
+    _, csr = G.build_problem(gd)
+    g, f = _factor(gd, csr)
+    b = G.rhs(gd, g.ndof)[:, 0]
+    rep = H.pcg_gpu(f, csr, b, tol=1e-12)
+    host = H.pcg(csr, b, f.apply_inverse, tol=1e-12)
+    assert rep.converged and host.converged
+    assert abs(rep.n_i - host.n_i) <= 1
+    assert abs(rep.n_i - int(gd["pcg_iters"])) <= max(1, int(0.2 * int(gd["pcg_iters"])))
+    assert np.linalg.norm(csr @ rep.x - b) <= 1e-12 * np.linalg.norm(b) * 1.0001
+    if "u_pcg" in gd:
+        ref = gd["u_pcg"]
+        assert np.linalg.norm(rep.x - ref) / np.linalg.norm(ref) <= max(10 * float(gd["eps"]), 1e-10)
+    zero = H.pcg_gpu(f, csr, np.zeros(g.ndof))
+    assert zero.converged and zero.n_i == 0 and not zero.x.any()
+
+
 def test_apply_large_cells_round_trip():
     """apply on factors with cells beyond the one-CTA paths (blocked inverse,
     tiled solve records): still the exact inverse of apply_inverse."""
