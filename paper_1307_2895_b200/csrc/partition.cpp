@@ -13,6 +13,9 @@
 
 #include <algorithm>
 #include <stdexcept>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace hifde {
 
@@ -50,6 +53,70 @@ Groups bucket(const std::vector<int32_t>& dofs, const std::vector<int32_t>& keys
   return out;
 }
 
+// Bucket act[i] by kall[i] (>= 0; -1 = not selected) into nkeys groups,
+// members ascending, empty buckets dropped.  Per-thread counts over
+// contiguous chunks, a prefix over (key, thread), then a parallel scatter:
+// the thread chunks are in ascending order, so members stay ascending.
+Groups bucket_keys(const std::vector<int32_t>& act, const std::vector<int32_t>& kall, int64_t nkeys) {
+  const int64_t na = (int64_t)act.size();
+  int nth = 1;
+#ifdef _OPENMP
+  nth = std::min(omp_get_max_threads(), 16);
+#endif
+  if (na < 16384 || nkeys * nth > 4 * na) {  // small: the serial counting sort
+    std::vector<int32_t> dofs, keys;
+    dofs.reserve(act.size());
+    keys.reserve(act.size());
+    for (int64_t i = 0; i < na; ++i)
+      if (kall[(size_t)i] >= 0) {
+        dofs.push_back(act[(size_t)i]);
+        keys.push_back(kall[(size_t)i]);
+      }
+    return bucket(dofs, keys, nkeys);
+  }
+  std::vector<int64_t> cnt((size_t)nth * (size_t)nkeys, 0);  // [thread][key]
+#pragma omp parallel num_threads(nth)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    const int64_t lo = na * tid / nth, hi = na * (tid + 1) / nth;
+    int64_t* c = cnt.data() + (size_t)tid * (size_t)nkeys;
+    for (int64_t i = lo; i < hi; ++i)
+      if (kall[(size_t)i] >= 0) ++c[kall[(size_t)i]];
+  }
+  Groups out;
+  out.offsets.clear();
+  out.offsets.push_back(0);
+  int64_t run = 0;
+  for (int64_t k = 0; k < nkeys; ++k) {
+    const int64_t start = run;
+    for (int t = 0; t < nth; ++t) {
+      int64_t& c = cnt[(size_t)t * (size_t)nkeys + (size_t)k];
+      const int64_t v = c;
+      c = run;  // becomes the thread's write position for key k
+      run += v;
+    }
+    if (run > start) out.offsets.push_back(run);
+  }
+  out.members.resize((size_t)run);
+#pragma omp parallel num_threads(nth)
+  {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    const int64_t lo = na * tid / nth, hi = na * (tid + 1) / nth;
+    int64_t* c = cnt.data() + (size_t)tid * (size_t)nkeys;
+    for (int64_t i = lo; i < hi; ++i) {
+      const int32_t k = kall[(size_t)i];
+      if (k >= 0) out.members[(size_t)c[k]++] = act[(size_t)i];
+    }
+  }
+  return out;
+}
+
 inline int64_t ipow(int64_t b, int e) {
   int64_t r = 1;
   for (int i = 0; i < e; ++i) r *= b;
@@ -75,7 +142,7 @@ Groups interior_groups(const GridDesc& g, const Coords& X, int ell, const std::v
   const int k = g.n / w;
   const int64_t na = (int64_t)act.size();
   std::vector<int32_t> kall((size_t)na);
-#pragma omp parallel for schedule(static) if (na > 65536)
+#pragma omp parallel for schedule(static) if (na > 16384)
   for (int64_t i = 0; i < na; ++i) {
     const int32_t d = act[(size_t)i];
     int key = 0, stride = 1;
@@ -88,15 +155,7 @@ Groups interior_groups(const GridDesc& g, const Coords& X, int ell, const std::v
     }
     kall[(size_t)i] = key;
   }
-  std::vector<int32_t> dofs, keys;
-  dofs.reserve(act.size());
-  keys.reserve(act.size());
-  for (int64_t i = 0; i < na; ++i)
-    if (kall[(size_t)i] >= 0) {
-      dofs.push_back(act[(size_t)i]);
-      keys.push_back(kall[(size_t)i]);
-    }
-  return bucket(dofs, keys, ipow(k, g.dim));
+  return bucket_keys(act, kall, ipow(k, g.dim));
 }
 
 Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
@@ -108,7 +167,7 @@ Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::
   const int span = (int)ipow(k, g.dim);
   const int64_t na = (int64_t)act.size();
   std::vector<int32_t> kall((size_t)na);
-#pragma omp parallel for schedule(static) if (na > 65536)
+#pragma omp parallel for schedule(static) if (na > 16384)
   for (int64_t i = 0; i < na; ++i) {
     const int32_t d = act[(size_t)i];
     int x2[3];
@@ -142,15 +201,7 @@ Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::
     }
     kall[(size_t)i] = best_key;
   }
-  std::vector<int32_t> dofs, keys;
-  dofs.reserve(act.size());
-  keys.reserve(act.size());
-  for (int64_t i = 0; i < na; ++i)
-    if (kall[(size_t)i] >= 0) {
-      dofs.push_back(act[(size_t)i]);
-      keys.push_back(kall[(size_t)i]);
-    }
-  return bucket(dofs, keys, (int64_t)span * g.dim);
+  return bucket_keys(act, kall, (int64_t)span * g.dim);
 }
 
 Groups adaptive_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,

@@ -1772,11 +1772,36 @@ struct Factorizer {
     const int Lv = g.nlevels;
     const double t_setup = now_s() - t0;
     HTRACE("setup done");
+    std::vector<int32_t> act_tmp;
     auto record_trace = [&](LevelRec& L, double tl) {
       size_t w = 0;
-      for (size_t i = 0; i < act.size(); ++i)
-        if (active[(size_t)act[i]]) act[w++] = act[i];
-      act.resize(w);
+      const int64_t na = (int64_t)act.size();
+      if (na < 16384) {
+        for (size_t i = 0; i < act.size(); ++i)
+          if (active[(size_t)act[i]]) act[w++] = act[i];
+        act.resize(w);
+      } else {  // parallel stable compaction: chunk counts, prefix, scatter
+        const int nth = nthreads;
+        std::vector<int64_t> cnt((size_t)nth + 1, 0);
+        act_tmp.resize(act.size());
+#pragma omp parallel num_threads(nth)
+        {
+          const int tid = omp_get_thread_num();
+          const int64_t lo = na * tid / nth, hi = na * (tid + 1) / nth;
+          int64_t c = 0;
+          for (int64_t i = lo; i < hi; ++i) c += active[(size_t)act[(size_t)i]] ? 1 : 0;
+          cnt[(size_t)tid + 1] = c;
+#pragma omp barrier
+#pragma omp single
+          for (int t = 0; t < nth; ++t) cnt[(size_t)t + 1] += cnt[(size_t)t];
+          int64_t o = cnt[(size_t)tid];
+          for (int64_t i = lo; i < hi; ++i)
+            if (active[(size_t)act[(size_t)i]]) act_tmp[(size_t)o++] = act[(size_t)i];
+        }
+        w = (size_t)cnt[(size_t)nth];
+        act_tmp.resize(w);
+        act.swap(act_tmp);
+      }
       L.active_after = (int64_t)w;
       L.seconds = now_s() - tl;
     };

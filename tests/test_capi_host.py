@@ -83,3 +83,20 @@ def test_partition_matches_reference_semantics(lib, dim, n, m):
                 got = _partition(lib, dim, n, m, ell, code, active)
                 ref = [c.tolist() for c in O.interface_groups(g, ell, active, kind)]
                 assert got == ref, (dim, n, m, ell, kind)
+
+
+@pytest.mark.parametrize("dim,n,m", [(2, 512, 8), (3, 64, 4)])
+def test_partition_large_grids_parallel_buckets(lib, dim, n, m):
+    """Grids above the 65536-DOF threshold take the parallel bucket path
+    (per-thread counts, prefix, scatter): same groups, same member order."""
+    g = O.make_grid(dim, n, m)
+    rng = np.random.default_rng(7)
+    for active in (np.ones(g.ndof, bool), rng.random(g.ndof) < 0.7):
+        for ell in (0, 1):
+            got = _partition(lib, dim, n, m, ell, 0, active)
+            ref = [c.tolist() for c in O.interior_groups(g, ell, active)]
+            assert got == ref
+            code, kind = (1, "edge") if dim == 2 else (2, "face")
+            got = _partition(lib, dim, n, m, ell, code, active)
+            ref = [c.tolist() for c in O.interface_groups(g, ell, active, kind)]
+            assert got == ref
