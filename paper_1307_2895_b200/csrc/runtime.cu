@@ -613,8 +613,12 @@ struct Factorizer {
       x.bbuf.clear();
       if (x.bstamp.size() < blk_n.size()) x.bstamp.resize(blk_n.size() + blk_n.size() / 2 + 1024, 0);
     }
-    const int nthr = (nt >= 256) ? nthreads : 1;
-#pragma omp parallel for num_threads(nthr) schedule(dynamic, 32)
+    // few large groups (coarse levels) are worth threads too: weight by size
+    int64_t work = 0;
+    for (int64_t t = 0; t < nt; ++t) work += gr.count(t);
+    const int nthr = (nt >= 8 && work >= 4096) ? (int)std::min<int64_t>(nthreads, nt) : 1;
+    const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(32, nt / (4 * std::max(nthr, 1))));
+#pragma omp parallel for num_threads(nthr) schedule(dynamic, chunk)
     for (int64_t t = 0; t < nt; ++t) {
       const int tid = omp_get_thread_num();
       out[(size_t)t] = front_sym(ctx[(size_t)tid], tid, gr.begin(t), gr.count(t));
