@@ -81,7 +81,28 @@ typedef struct hifde_info {
   double eps;
   int32_t spd;
   int32_t variant;
+  int64_t fac_len;      /* doubles in the factor arena (hifde_copy_arenas)  */
+  int64_t idx_len;      /* int32 entries in the index arena                 */
 } hifde_info_t;
+
+/*
+ * One record of a level, for export (hifde_level_records): offsets into the
+ * factor arena (doubles) and the index arena (int32) copied by
+ * hifde_copy_arenas.  Cholesky form: C C^T = the eliminated block, stored as
+ * its packed lower inverse P = C^-1 (row i at P_off + i(i+1)/2); the
+ * reference's L = C diag(C)^-1, D = diag(C)^2, coupling X = diag(C)^-1 W.
+ */
+typedef struct hifde_record {
+  int32_t kind;         /* 0 elimination cell, 1 skeleton group, 2 terminal */
+  int32_t nc;           /* |cell| (0/2) or |group| (1)                      */
+  int32_t nq;           /* |nbrs| (0) or k = |sk| (1); 0 for the terminal   */
+  int32_t nr;           /* |rd| (1), else 0; 0 = no-op skeleton record      */
+  int64_t cell_off;     /* cell / group DOFs, ascending                     */
+  int64_t idx_off;      /* 0/2: cell then nbrs; 1: sk[k] then rd[r]         */
+  int64_t P_off;        /* packed C^-1 (nc x nc, or r x r)                  */
+  int64_t W_off;        /* 0: W (nc x nq) row-major; 1: W (r x k)           */
+  int64_t T_off;        /* 1: interpolation T (k x r) row-major             */
+} hifde_record_t;
 
 typedef struct hifde_level_info {
   double tag;           /* level tag: l, l+1/2, l+1/3, l+2/3                */
@@ -146,6 +167,32 @@ int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* ind
               int* converged);
 
 int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info);
+
+/*
+ * Export (hifde_export of SURVEY 8(b)): the records of level `level` in the
+ * reference's record order -- every cell of an elimination level, every
+ * group of a skeletonization level (no-op groups included), the terminal
+ * block as the last level -- into out[0..cap); *count = number of records.
+ * With out == NULL only *count is set.
+ */
+int hifde_level_records(const hifde_factor_t* f, int level, hifde_record_t* out, int64_t cap,
+                        int64_t* count);
+
+/*
+ * Import (load_factor, src/driver.py:318-376): build a device factor from
+ * records in the export layout.  Level li holds recs[rec_ptr[li] ..
+ * rec_ptr[li+1]) with tag tags[li] and kind kinds[li] (0 elimination, 1
+ * skeletonization, 2 terminal block -- the last level, one record); offsets
+ * index the host arenas fac (doubles) and idx (int32), which are copied.
+ */
+int hifde_import(int64_t n, int dim, double eps, int nlevels, const double* tags, const int32_t* kinds,
+                 const int64_t* rec_ptr, const hifde_record_t* recs, const double* fac, int64_t fac_len,
+                 const int32_t* idx, int64_t idx_len, int device, hifde_factor_t** out);
+
+/* Copy the factor arena (fac_len doubles) and the index arena (idx_len
+ * int32) to host buffers; either pointer may be NULL. */
+int hifde_copy_arenas(const hifde_factor_t* f, double* fac, int64_t fac_len, int32_t* idx,
+                      int64_t idx_len);
 int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info);
 
 /* Number of kernel launches issued by the last hifde_factor / hifde_solve

@@ -43,6 +43,16 @@ class Info(C.Structure):
         ("eps", C.c_double),
         ("spd", C.c_int32),
         ("variant", C.c_int32),
+        ("fac_len", C.c_int64),
+        ("idx_len", C.c_int64),
+    ]
+
+
+class Record(C.Structure):  # hifde_record_t
+    _fields_ = [
+        ("kind", C.c_int32), ("nc", C.c_int32), ("nq", C.c_int32), ("nr", C.c_int32),
+        ("cell_off", C.c_int64), ("idx_off", C.c_int64), ("P_off", C.c_int64),
+        ("W_off", C.c_int64), ("T_off", C.c_int64),
     ]
 
 
@@ -66,7 +76,7 @@ class LevelInfo(C.Structure):
 # every symbol the public header declares
 EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
-    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
+    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
     "hifde_free", "hifde_last_error", "hifde_partition",
 ]
 
@@ -102,6 +112,14 @@ def load(path: str | None = None):
                               C.c_int64, C.c_double, C.c_int, C.c_int, C.c_void_p,
                               C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int)]
     lib.hifde_pcg.restype = C.c_int
+    lib.hifde_level_records.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+    lib.hifde_level_records.restype = C.c_int
+    lib.hifde_copy_arenas.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
+    lib.hifde_copy_arenas.restype = C.c_int
+    lib.hifde_import.argtypes = [C.c_int64, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int,
+                                 C.POINTER(C.c_void_p)]
+    lib.hifde_import.restype = C.c_int
     lib.hifde_get_info.argtypes = [C.c_void_p, P(Info)]
     lib.hifde_get_info.restype = C.c_int
     lib.hifde_get_level.argtypes = [C.c_void_p, C.c_int, P(LevelInfo)]

@@ -231,6 +231,7 @@ struct LevelRec {
   SolveRec* d_recs = nullptr;
   int nsmall = 0;
   SolveRec* d_all = nullptr;  // every record of the level (apply)
+  std::vector<hifde_record_t> xrec;  // export view of every record (hifde_level_records)
   int nall = 0, all_max_nc = 0, all_max_nq = 0;
   int max_nc = 0, max_nq = 0;
   struct Phase {
@@ -782,6 +783,20 @@ struct Factorizer {
       R.idx_off = T.dofs_off;
       R.C_off = T.P_off;  // the solve applies the packed inverse
       R.W_off = T.W_off;
+    }
+    L.xrec.resize((size_t)nt);
+    for (int64_t t = 0; t < nt; ++t) {
+      const ElimTask& T = tasks[(size_t)t];
+      hifde_record_t& X = L.xrec[(size_t)t];
+      X.kind = is_top ? 2 : 0;
+      X.nc = T.nc;
+      X.nq = T.nq;
+      X.nr = 0;
+      X.cell_off = T.dofs_off;
+      X.idx_off = T.dofs_off;
+      X.P_off = T.P_off;
+      X.W_off = T.W_off;
+      X.T_off = 0;
     }
     double tp = now_s();
     L.t_sym = tp - t_begin;
@@ -1391,6 +1406,20 @@ struct Factorizer {
         newid[(size_t)t] = new_block(T.out_off, kk, T.delta_off);
         nadd += (size_t)kk;
       }
+      {
+        hifde_record_t X;
+        X.kind = 1;
+        X.nc = T.nc;
+        X.nq = kk;
+        X.nr = r;
+        X.cell_off = T.dofs_off;
+        X.idx_off = T.out_off;
+        X.T_off = T.rec_off;
+        X.P_off = T.mode == 2 ? T.rec_off + (int64_t)T.nc * T.nc + 2 * ((int64_t)T.nc * T.nc / 4 + T.nc)
+                              : T.rec_off + (int64_t)kk * r;
+        X.W_off = T.rec_off + (int64_t)kk * r + (int64_t)r * r;
+        L.xrec.push_back(X);
+      }
       if (r > 0) {
         SolveRec R;
         R.nc = r;
@@ -1685,6 +1714,75 @@ struct Factorizer {
       if (bf_val[(size_t)b]) found = true;
     });
     return found;
+  }
+
+  // Rebuild a factor from exported records (hifde_import): arenas to the
+  // device, solve records, reductions and the solve plan as after run().
+  void import_records(int nlevels, const double* tags, const int32_t* kinds, const int64_t* rec_ptr,
+                      const hifde_record_t* recs, const double* fac, int64_t fac_len, const int32_t* idx,
+                      int64_t idx_len) {
+    N = F->n;
+    pinned_stage().begin(s);
+    g_stage = &pinned_stage();
+    struct StageOff {
+      ~StageOff() { g_stage = nullptr; }
+    } stage_off;
+    h_idx.assign(idx, idx + idx_len);
+    F->fac.reserve((size_t)std::max<int64_t>(fac_len, 1), s);
+    F->fac.n = (size_t)fac_len;
+    F->fac.upload(fac, 0, (size_t)fac_len, s);
+    F->idx.reserve((size_t)std::max<int64_t>(idx_len, 1), s);
+    F->idx.n = (size_t)idx_len;
+    F->idx.upload(idx, 0, (size_t)idx_len, s);
+    for (int li = 0; li < nlevels; ++li) {
+      F->levels.emplace_back();
+      LevelRec& L = F->levels.back();
+      L.tag = tags[li];
+      L.kind = kinds[li];
+      const hifde_record_t* r0 = recs + rec_ptr[li];
+      const int64_t nr = rec_ptr[li + 1] - rec_ptr[li];
+      L.ngroups = nr;
+      L.xrec.assign(r0, r0 + nr);
+      for (int64_t t = 0; t < nr; ++t) {
+        const hifde_record_t& X = r0[t];
+        if ((X.kind == 1) != (L.kind == 1)) throw Fail{HIFDE_BADARG, "record kind does not match its level"};
+        SolveRec R;
+        R.T_off = 0;
+        R.inv = 1;
+        R.pad = 0;
+        R.contrib_off = 0;
+        if (X.kind == 1) {
+          L.nskel += X.nq;
+          L.nred += X.nr;
+          if (X.nr == 0) continue;
+          R.nc = X.nr;
+          R.nq = X.nq;
+          R.idx_off = X.idx_off;
+          R.T_off = X.T_off;
+        } else {
+          R.nc = X.nc;
+          R.nq = X.nq;
+          R.idx_off = X.idx_off;
+          R.contrib_off = L.ncontrib;
+          L.ncontrib += X.nq;
+          if (X.kind == 2) F->s_top = X.nc;
+        }
+        R.C_off = X.P_off;
+        R.W_off = X.W_off;
+        L.recs.push_back(R);
+        L.max_nc = std::max(L.max_nc, R.nc);
+        L.max_nq = std::max(L.max_nq, R.nq);
+        F->m_f_bytes += X.kind == 1 ? 8 * ((int64_t)X.nq * X.nr + (int64_t)X.nr * X.nr + X.nr + (int64_t)X.nr * X.nq)
+                                    : 8 * ((int64_t)X.nc * X.nc + X.nc + (int64_t)X.nc * X.nq);
+      }
+      if (L.kind == 0) build_reduction((size_t)li, L);
+    }
+    finish_reductions();
+    for (auto& L : F->levels) build_solve_plan(L);
+    F->meta = meta.commit(s, [&](void* d, const void* h, size_t n) {
+      if (!pinned_stage().copy(d, h, n)) HCK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s));
+    });
+    HCK(cudaStreamSynchronize(s));
   }
 
   void run(const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz) {
@@ -2261,6 +2359,45 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
   return HIFDE_OK;
 }
 
+int hifde_import(int64_t n, int dim, double eps, int nlevels, const double* tags, const int32_t* kinds,
+                 const int64_t* rec_ptr, const hifde_record_t* recs, const double* fac, int64_t fac_len,
+                 const int32_t* idx, int64_t idx_len, int device, hifde_factor_t** out) {
+  g_err.clear();
+  g_launches = 0;
+  if (!out || !tags || !kinds || !rec_ptr || (!recs && rec_ptr[nlevels] > 0) || (!fac && fac_len) ||
+      (!idx && idx_len) || n < 1 || nlevels < 1 || kinds[nlevels - 1] != 2) {
+    g_err = "bad import arguments (the last level must be the terminal block)";
+    return HIFDE_BADARG;
+  }
+  *out = nullptr;
+  std::unique_ptr<hifde_factor_t> F(new hifde_factor_t);
+  try {
+    HCK(cudaSetDevice(device));
+    set_pool_threshold(device);
+    F->device = device;
+    F->n = n;
+    F->dim = dim;
+    F->variant = 0;
+    F->spd = 1;
+    F->eps = eps;
+    HCK(cudaStreamCreateWithFlags(&F->stream, cudaStreamNonBlocking));
+    F->own_stream = true;
+    std::lock_guard<std::mutex> lock(g_host_mutex);
+    Factorizer fz;
+    fz.F = F.get();
+    fz.F_ = F.get();
+    fz.s = F->stream;
+    fz.import_records(nlevels, tags, kinds, rec_ptr, recs, fac, fac_len, idx, idx_len);
+  } catch (const Fail& f) {
+    return fail_to_status(f);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
+  }
+  *out = F.release();
+  return HIFDE_OK;
+}
+
 int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n, int nrhs,
                 int device_ptrs, void* stream) {
   g_err.clear();
@@ -2316,6 +2453,36 @@ int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* ind
   return HIFDE_OK;
 }
 
+int hifde_level_records(const hifde_factor_t* f, int level, hifde_record_t* out, int64_t cap,
+                        int64_t* count) {
+  g_err.clear();
+  if (!f || !count || level < 0 || level >= (int)f->levels.size()) { g_err = "bad level"; return HIFDE_BADARG; }
+  const auto& X = f->levels[(size_t)level].xrec;
+  *count = (int64_t)X.size();
+  if (out) {
+    if (cap < (int64_t)X.size()) { g_err = "record buffer too small"; return HIFDE_BADARG; }
+    std::memcpy(out, X.data(), X.size() * sizeof(hifde_record_t));
+  }
+  return HIFDE_OK;
+}
+
+int hifde_copy_arenas(const hifde_factor_t* f, double* fac, int64_t fac_len, int32_t* idx, int64_t idx_len) {
+  g_err.clear();
+  if (!f) { g_err = "null factor"; return HIFDE_BADARG; }
+  if ((fac && fac_len != (int64_t)f->fac.n) || (idx && idx_len != (int64_t)f->idx.n)) {
+    g_err = "arena length mismatch";
+    return HIFDE_BADARG;
+  }
+  try {
+    HCK(cudaSetDevice(f->device));
+    if (fac && fac_len) HCK(cudaMemcpy(fac, f->fac.p, (size_t)fac_len * sizeof(double), cudaMemcpyDeviceToHost));
+    if (idx && idx_len) HCK(cudaMemcpy(idx, f->idx.p, (size_t)idx_len * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  } catch (const Fail& e) {
+    return fail_to_status(e);
+  }
+  return HIFDE_OK;
+}
+
 int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
   if (!f || !info) return HIFDE_BADARG;
   std::memset(info, 0, sizeof *info);
@@ -2329,6 +2496,8 @@ int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
   info->eps = f->eps;
   info->spd = f->spd;
   info->variant = f->variant;
+  info->fac_len = (int64_t)f->fac.n;
+  info->idx_len = (int64_t)f->idx.n;
   return HIFDE_OK;
 }
 

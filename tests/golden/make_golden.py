@@ -43,6 +43,9 @@ CASES = [
     ("g3d_n32_m4_x", 3, 32, 4, 1e-6, "hifde3x", "const", 0, 1, False),
 ]
 
+# small cases whose factor files (GLDL v1) are committed for record-level parity
+GLDL_CASES = ("g2d_n16_m2", "g2d_n32_m4", "g3d_n8_m2")
+
 BIG_CASES = [
     ("cfg2", 2, 512, 8, 1e-9, "hifde", "gauss", 0, 16, False),
     ("cfg4", 3, 64, 4, 1e-6, "hifde3x", "const", 0, 16, False),
@@ -122,6 +125,8 @@ def run_case(hifde, case):
         out["x_oneshot"] = x
         out["u_pcg"] = rep.x
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    if name in GLDL_CASES:  # the reference's own factor file (src/driver.py:292-315)
+        hifde.save_factor(f, os.path.join(HERE, f"{name}.gldl"))
     print(f"{name}: N={g.ndof} t_f={tf:.2f}s s_L={out['s_top']} ranks={ranks} "
           f"resid={resid.max():.2e} pcg={rep.n_i}", flush=True)
 
