@@ -12,6 +12,7 @@
  *   hifde_solve    <- GeneralizedLDL.apply_inverse (src/driver.py:113-129)
  *   hifde_apply    <- GeneralizedLDL.apply (src/driver.py:95-111)
  *   hifde_pcg      <- pcg(A, b, F.apply_inverse) (src/krylov.py:48-77)
+ *   hifde_power_norm <- _power_norm / estimate_*_error (src/krylov.py:153-201)
  *                     and module-level apply_inverse (src/driver.py:258-259)
  *   hifde_get_info / hifde_get_level
  *                  <- GeneralizedLDL.metrics (src/driver.py:165-171)
@@ -165,6 +166,16 @@ int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* ind
               const double* vals, const double* b, double* x, int64_t n, double tol,
               int max_iter, int device_ptrs, void* stream, int* iters, double* residual,
               int* converged);
+
+/*
+ * Power iteration for sqrt(lambda_max(G^T G)) on the device, the reference's
+ * _power_norm: kind 0 G = A - F, 1 G = A, 2 G = I - A F^-1 (G^T = I - F^-1 A).
+ * x0 (host, length n) is the normalized start vector; stops when two
+ * successive estimates agree to rtol, or after max_iter iterations.
+ */
+int hifde_power_norm(const hifde_factor_t* f, const int64_t* indptr, const int32_t* indices,
+                     const double* vals, int64_t n, int kind, const double* x0, double rtol,
+                     int max_iter, double* value, int* converged, int* iters);
 
 int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info);
 

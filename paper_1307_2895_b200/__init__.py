@@ -15,6 +15,6 @@ from .driver import (FactorizationError, GeneralizedLDL, IndefiniteBlockError,
 from .problems import (CoeffField, GridConfig, assemble, baseline_problem, build_grid,
                        constant_field, gaussian_contrast_field, high_contrast_field)
 from .gldl import export_factor, import_factor, load_factor, read_gldl, save_factor, write_gldl
-from .solvers import pcg, pcg_gpu
+from .solvers import EstimateResult, estimate_apply_error, estimate_solve_error, pcg, pcg_gpu
 
 __version__ = "0.1.0"

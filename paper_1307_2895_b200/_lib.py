@@ -76,7 +76,7 @@ class LevelInfo(C.Structure):
 # every symbol the public header declares
 EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
-    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
+    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
     "hifde_free", "hifde_last_error", "hifde_partition",
 ]
 
@@ -120,6 +120,10 @@ def load(path: str | None = None):
                                  C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int,
                                  C.POINTER(C.c_void_p)]
     lib.hifde_import.restype = C.c_int
+    lib.hifde_power_norm.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int,
+                                     C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    lib.hifde_power_norm.restype = C.c_int
     lib.hifde_get_info.argtypes = [C.c_void_p, P(Info)]
     lib.hifde_get_info.restype = C.c_int
     lib.hifde_get_level.argtypes = [C.c_void_p, C.c_int, P(LevelInfo)]

@@ -163,6 +163,8 @@ int dot_partials();
 void launch_cg_xr(double* x, double* r, const double* p, const double* ap, const double* sc, int64_t n,
                   cudaStream_t s);
 void launch_cg_p(double* p, const double* z, double* sc, int64_t n, cudaStream_t s);
+void launch_sub(double* z, const double* x, const double* y, int64_t n, cudaStream_t s);
+void launch_scale(double* x, const double* y, const double* nn, int64_t n, cudaStream_t s);
 void launch_apply_elim(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,
                        double* contrib, double* scratch, int64_t scratch_per_rec, size_t smem, int fwdinv,
                        cudaStream_t s);

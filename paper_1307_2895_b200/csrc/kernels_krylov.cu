@@ -77,6 +77,19 @@ __global__ void cg_p_kernel(double* __restrict__ p, const double* __restrict__ z
 }
 __global__ void cg_shift_kernel(double* sc) { sc[0] = sc[3]; }
 
+// z = x - y
+__global__ void sub_kernel(double* __restrict__ z, const double* __restrict__ x, const double* __restrict__ y,
+                           int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) z[i] = x[i] - y[i];
+}
+// x = y / sqrt(*nn)   (nn = ||y||^2 on the device)
+__global__ void scale_kernel(double* __restrict__ x, const double* __restrict__ y, const double* __restrict__ nn,
+                             int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = y[i] / sqrt(*nn);
+}
+
 void launch_spmv(const int64_t* ip, const int32_t* ix, const double* va, const double* x, double* y, int64_t n,
                  cudaStream_t s) {
   if (n > 0) spmv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ip, ix, va, x, y, n);
@@ -93,6 +106,13 @@ void launch_cg_xr(double* x, double* r, const double* p, const double* ap, const
 void launch_cg_p(double* p, const double* z, double* sc, int64_t n, cudaStream_t s) {
   if (n > 0) cg_p_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, z, sc, n);
   cg_shift_kernel<<<1, 1, 0, s>>>(sc);
+}
+
+void launch_sub(double* z, const double* x, const double* y, int64_t n, cudaStream_t s) {
+  if (n > 0) sub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(z, x, y, n);
+}
+void launch_scale(double* x, const double* y, const double* nn, int64_t n, cudaStream_t s) {
+  if (n > 0) scale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(x, y, nn, n);
 }
 
 }  // namespace hifde

@@ -2235,6 +2235,91 @@ void do_pcg(const hifde_factor_t* F, const int64_t* ip, const int32_t* ix, const
   HCK(cudaStreamSynchronize(s));
 }
 
+// sqrt of the dominant eigenvalue of G^T G by power iteration (src/krylov.py:
+// 153-170), on the device.  kind 0: G = G^T = A - F; 1: G = G^T = A;
+// 2: G = I - A F^-1, G^T = I - F^-1 A.  x0 = the reference's start vector.
+void do_power(const hifde_factor_t* F, const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz,
+              int kind, const double* x0, double rtol, int max_iter, cudaStream_t s, double* value, int* conv,
+              int* iters) {
+  const int64_t N = F->n;
+  const size_t vb = (size_t)std::max<int64_t>(N, 1) * sizeof(double);
+  std::vector<void*> owned;
+  auto dalloc = [&](size_t bytes) {
+    void* p = nullptr;
+    HCK(cudaMallocAsync(&p, std::max<size_t>(bytes, 8), s));
+    owned.push_back(p);
+    return p;
+  };
+  int64_t* d_ip = (int64_t*)dalloc((N + 1) * sizeof(int64_t));
+  int32_t* d_ix = (int32_t*)dalloc(nnz * sizeof(int32_t));
+  double* d_va = (double*)dalloc(nnz * sizeof(double));
+  HCK(cudaMemcpyAsync(d_ip, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  HCK(cudaMemcpyAsync(d_ix, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  HCK(cudaMemcpyAsync(d_va, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s));
+  double* x = (double*)dalloc(vb);
+  double* t = (double*)dalloc(vb);
+  double* u = (double*)dalloc(vb);
+  double* y = (double*)dalloc(vb);
+  double* z = (double*)dalloc(vb);
+  double* part = (double*)dalloc(sizeof(double) * dot_partials());
+  double* nn = (double*)dalloc(sizeof(double));
+  double* hs = nullptr;
+  HCK(cudaMallocHost((void**)&hs, sizeof(double)));
+  struct Free {
+    std::vector<void*>& o; double* h; cudaStream_t s;
+    ~Free() { for (void* q : o) cudaFreeAsync(q, s); if (h) cudaFreeHost(h); }
+  } fr{owned, hs, s};
+  HCK(cudaMemcpyAsync(x, x0, vb, cudaMemcpyHostToDevice, s));
+  // out = G v  (or G^T v when trans), using t as scratch
+  auto gapply = [&](const double* v, double* out, bool trans) {
+    if (kind == 1) {
+      launch_spmv(d_ip, d_ix, d_va, v, out, N, s);
+    } else if (kind == 0) {
+      launch_spmv(d_ip, d_ix, d_va, v, t, N, s);
+      do_apply(F, v, u, 1, true, s);
+      launch_sub(out, t, u, N, s);
+    } else if (!trans) {  // v - A F^-1 v
+      do_solve(F, v, u, 1, true, s);
+      launch_spmv(d_ip, d_ix, d_va, u, t, N, s);
+      launch_sub(out, v, t, N, s);
+    } else {              // v - F^-1 A v
+      launch_spmv(d_ip, d_ix, d_va, v, t, N, s);
+      do_solve(F, t, u, 1, true, s);
+      launch_sub(out, v, u, N, s);
+    }
+  };
+  double est = 0.0;
+  *conv = 0;
+  *iters = max_iter;
+  *value = 0.0;
+  for (int it = 1; it <= max_iter; ++it) {
+    gapply(x, y, false);
+    gapply(y, z, true);  // z = G^T (G x)
+    launch_dot(z, z, N, part, nn, s);
+    HCK(cudaMemcpyAsync(hs, nn, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    const double lam = std::sqrt(hs[0]);
+    const double new_est = std::sqrt(lam);
+    if (lam == 0.0 || !std::isfinite(lam)) {
+      *value = std::isfinite(lam) ? new_est : INFINITY;
+      *conv = 1;
+      *iters = it;
+      return;
+    }
+    launch_scale(x, z, nn, N, s);
+    if (it > 1 && std::fabs(new_est - est) <= rtol * new_est) {
+      *value = new_est;
+      *conv = 1;
+      *iters = it;
+      HCK(cudaStreamSynchronize(s));
+      return;
+    }
+    est = new_est;
+  }
+  *value = est;
+  HCK(cudaStreamSynchronize(s));
+}
+
 int fail_to_status(const Fail& f) {
   g_err = f.msg;
   return f.code;
@@ -2477,6 +2562,25 @@ int hifde_copy_arenas(const hifde_factor_t* f, double* fac, int64_t fac_len, int
     HCK(cudaSetDevice(f->device));
     if (fac && fac_len) HCK(cudaMemcpy(fac, f->fac.p, (size_t)fac_len * sizeof(double), cudaMemcpyDeviceToHost));
     if (idx && idx_len) HCK(cudaMemcpy(idx, f->idx.p, (size_t)idx_len * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  } catch (const Fail& e) {
+    return fail_to_status(e);
+  }
+  return HIFDE_OK;
+}
+
+int hifde_power_norm(const hifde_factor_t* f, const int64_t* indptr, const int32_t* indices, const double* vals,
+                     int64_t n, int kind, const double* x0, double rtol, int max_iter, double* value,
+                     int* converged, int* iters) {
+  g_err.clear();
+  g_launches = 0;
+  if (!f || !indptr || !indices || !vals || !x0 || !value || !converged || !iters || n != f->n || kind < 0 ||
+      kind > 2 || max_iter < 1) {
+    g_err = "bad power-iteration arguments";
+    return HIFDE_BADARG;
+  }
+  try {
+    HCK(cudaSetDevice(f->device));
+    do_power(f, indptr, indices, vals, indptr[n], kind, x0, rtol, max_iter, f->stream, value, converged, iters);
   } catch (const Fail& e) {
     return fail_to_status(e);
   }

@@ -8,6 +8,7 @@ solvers are a consumer of the hot path, not part of it.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 
@@ -71,3 +72,51 @@ def pcg_gpu(f, a, b, tol: float = 1e-12, max_iter: int = 1000) -> SolveReport:
         from .driver import _raise
         _raise(f._lib, code)
     return SolveReport(x, int(it.value), float(res.value), bool(conv.value))
+
+
+class EstimateResult(NamedTuple):
+    """Power-iteration norm estimate (src/krylov.py:140-149)."""
+    value: float
+    converged: bool
+    iterations: int
+
+    def __float__(self) -> float:
+        return self.value
+
+
+POWER_ITER_RTOL = 1e-2
+POWER_ITER_CAP = 512
+
+
+def _power_norm_gpu(f, a, kind: int, seed) -> EstimateResult:
+    import ctypes as C
+    import scipy.sparse as sp
+
+    csr = sp.csr_matrix(a) if not sp.isspmatrix_csr(a) else a
+    ip = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(csr.indices, dtype=np.int32)
+    va = np.ascontiguousarray(csr.data, dtype=np.float64)
+    rng = np.random.default_rng(seed)  # the reference's start vector
+    x = rng.random(f.n)
+    x /= np.linalg.norm(x)
+    val, conv, it = C.c_double(), C.c_int(), C.c_int()
+    code = f._lib.hifde_power_norm(f._h, ip.ctypes.data, ix.ctypes.data, va.ctypes.data, f.n, kind,
+                                   x.ctypes.data, POWER_ITER_RTOL, POWER_ITER_CAP, C.byref(val), C.byref(conv),
+                                   C.byref(it))
+    if code:
+        from .driver import _raise
+        _raise(f._lib, code)
+    return EstimateResult(float(val.value), bool(conv.value), int(it.value))
+
+
+def estimate_apply_error(a, f, seed: int = 0) -> EstimateResult:
+    """||A - F|| / ||A|| by power iteration on the device (src/krylov.py:173-186)."""
+    num = _power_norm_gpu(f, a, 0, (seed, 0xA))
+    den = _power_norm_gpu(f, a, 1, (seed, 0xB))
+    value = num.value / den.value if den.value else np.inf
+    return EstimateResult(value, num.converged and den.converged, num.iterations + den.iterations)
+
+
+def estimate_solve_error(a, f, seed: int = 0) -> EstimateResult:
+    """||I - A F^-1|| by power iteration on the device (src/krylov.py:189-201)."""
+    return _power_norm_gpu(f, a, 2, (seed, 0xC))

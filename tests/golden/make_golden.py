@@ -109,6 +109,12 @@ def run_case(hifde, case):
     ax = csr @ xa
     apply_err = float(np.linalg.norm(f.apply(xa) - ax) / np.linalg.norm(ax))
     rep = hifde.pcg(csr, b[:, 0], f.apply_inverse, tol=1e-12)
+    est = {}
+    if g.ndof <= 20000:  # power-iteration error estimators (src/krylov.py:153-201)
+        ea = hifde.estimate_apply_error(csr, f, seed=0)
+        es = hifde.estimate_solve_error(csr, f, seed=0)
+        est = dict(e_a=ea.value, e_a_iters=ea.iterations, e_a_conv=ea.converged,
+                   e_s=es.value, e_s_iters=es.iterations, e_s_conv=es.converged)
     out = dict(
         dim=dim, n=n, m=m, eps=eps, variant=variant, field=fld, seed=seed,
         skip_levels=-1 if skip is None else skip, nrhs=nrhs,
@@ -119,7 +125,7 @@ def run_case(hifde, case):
         trace=np.array([t[1] for t in f.metrics["active_trace"]], dtype=np.int64),
         s_top=f.metrics["s_top"], m_f_bytes=f.metrics["m_f_bytes"],
         oneshot_resid=resid, apply_err=apply_err,
-        pcg_iters=rep.n_i, pcg_resid=rep.residual, t_f_ref=tf,
+        pcg_iters=rep.n_i, pcg_resid=rep.residual, t_f_ref=tf, **est,
     )
     if vectors:
         out["x_oneshot"] = x

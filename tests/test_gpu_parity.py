@@ -112,6 +112,28 @@ def test_pcg_gpu_matches_reference(name):
     assert zero.converged and zero.n_i == 0 and not zero.x.any()
 
 
+@pytest.mark.parametrize("name", [n for n in NAMES if n != "g3d_n32_m4_x"])
+def test_error_estimators_match_reference(name):
+    """estimate_apply_error / estimate_solve_error (src/krylov.py:153-201) on
+    the device, same start vectors: the reference's estimates on its own
+    factor, to the power iteration's 1e-2 stopping tolerance."""
+    gd = G.load(name)
+    if "e_a" not in gd:
+        pytest.skip("no estimator golden")
+    _, csr = G.build_problem(gd)
+    g, f = _factor(gd, csr)
+    ea = H.estimate_apply_error(csr, f, seed=0)
+    es = H.estimate_solve_error(csr, f, seed=0)
+    assert ea.converged == bool(gd["e_a_conv"]) and es.converged == bool(gd["e_s_conv"])
+    for got, ref in ((ea.value, float(gd["e_a"])), (es.value, float(gd["e_s"]))):
+        assert abs(got - ref) <= 0.05 * ref + 200 * np.finfo(float).eps, (got, ref)  # MF: rounding level
+    # iteration counts are meaningful unless the operator error is rounding noise (MF)
+    if float(gd["e_a"]) > 1e-12:
+        assert abs(ea.iterations - int(gd["e_a_iters"])) <= 2
+    if float(gd["e_s"]) > 1e-12:
+        assert abs(es.iterations - int(gd["e_s_iters"])) <= 2
+
+
 def test_apply_large_cells_round_trip():
     """apply on factors with cells beyond the one-CTA paths (blocked inverse,
     tiled solve records): still the exact inverse of apply_inverse."""
