@@ -19,6 +19,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <deque>
+#include <exception>
 #include <functional>
 #include <thread>
 #include <future>
@@ -423,6 +426,68 @@ struct FrontSym {  // result of the symbolic analysis of one cell / group
 // ---------------------------------------------------------------------------
 // Factorization state
 // ---------------------------------------------------------------------------
+// One background host thread per factorization for work that only the solve
+// needs (reductions, solve plans): jobs run in order, off the level loop.
+struct Helper {
+  std::thread th;
+  std::mutex m;
+  std::condition_variable cv;
+  std::deque<std::function<void()>> q;
+  bool stop = false, running = false;
+  std::exception_ptr err;
+  void start() {
+    running = true;
+    th = std::thread([this]() {
+      for (;;) {
+        std::function<void()> job;
+        {
+          std::unique_lock<std::mutex> lk(m);
+          cv.wait(lk, [&]() { return stop || !q.empty(); });
+          if (q.empty()) return;
+          job = std::move(q.front());
+          q.pop_front();
+        }
+        try {
+          job();
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(m);
+          if (!err) err = std::current_exception();
+        }
+      }
+    });
+  }
+  void post(std::function<void()> job) {
+    if (!running) { job(); return; }
+    {
+      std::lock_guard<std::mutex> lk(m);
+      q.push_back(std::move(job));
+    }
+    cv.notify_one();
+  }
+  void drain() {  // wait for every posted job; rethrow the first failure
+    if (running) {
+      {
+        std::lock_guard<std::mutex> lk(m);
+        stop = true;
+      }
+      cv.notify_one();
+      th.join();
+      running = false;
+    }
+    if (err) std::rethrow_exception(err);
+  }
+  ~Helper() {
+    if (running) {
+      {
+        std::lock_guard<std::mutex> lk(m);
+        stop = true;
+      }
+      cv.notify_one();
+      th.join();
+    }
+  }
+};
+
 struct Factorizer {
   std::thread a0_thread;  // host CSR upload in flight
   cudaError_t a0_err = cudaSuccess;
@@ -990,33 +1055,44 @@ struct Factorizer {
   std::vector<std::pair<size_t, Reduction>> reductions;
   std::vector<int32_t> red_slot;  // per DOF: target index during a build, else -1
 
+  Helper helper;
+
+  // Copies the level's neighbour lists now (h_idx keeps growing) and builds
+  // the reduction on the helper thread.
   void build_reduction(size_t level_index, const LevelRec& L) {
-    if ((int64_t)red_slot.size() != N) red_slot.assign((size_t)N, -1);
-    Reduction r;
-    std::vector<int64_t> cnt;
+    std::vector<int32_t> qflat;
+    std::vector<int64_t> qptr{0}, coff;
+    qflat.reserve((size_t)L.ncontrib);
     for (const SolveRec& R : L.recs) {
       const int32_t* q = h_idx.data() + R.idx_off + R.nc;
-      for (int a = 0; a < R.nq; ++a) {
-        int32_t& sl = red_slot[(size_t)q[a]];
+      qflat.insert(qflat.end(), q, q + R.nq);
+      qptr.push_back((int64_t)qflat.size());
+      coff.push_back(R.contrib_off);
+    }
+    F->max_contrib = std::max(F->max_contrib, L.ncontrib);
+    helper.post([this, level_index, qflat = std::move(qflat), qptr = std::move(qptr), coff = std::move(coff)]() {
+      if ((int64_t)red_slot.size() != N) red_slot.assign((size_t)N, -1);
+      Reduction r;
+      std::vector<int64_t> cnt;
+      for (int32_t d : qflat) {
+        int32_t& sl = red_slot[(size_t)d];
         if (sl < 0) {
           sl = (int32_t)r.targets.size();
-          r.targets.push_back(q[a]);
+          r.targets.push_back(d);
           cnt.push_back(0);
         }
         ++cnt[(size_t)sl];
       }
-    }
-    r.ptr.assign(r.targets.size() + 1, 0);
-    for (size_t i = 0; i < cnt.size(); ++i) r.ptr[i + 1] = r.ptr[i] + cnt[i];
-    r.ent.resize((size_t)r.ptr.back());
-    std::vector<int64_t> pos(r.ptr.begin(), r.ptr.end() - 1);
-    for (const SolveRec& R : L.recs) {
-      const int32_t* q = h_idx.data() + R.idx_off + R.nc;
-      for (int a = 0; a < R.nq; ++a) r.ent[(size_t)pos[(size_t)red_slot[(size_t)q[a]]]++] = R.contrib_off + a;
-    }
-    for (int32_t d : r.targets) red_slot[(size_t)d] = -1;
-    F->max_contrib = std::max(F->max_contrib, L.ncontrib);
-    reductions.emplace_back(level_index, std::move(r));
+      r.ptr.assign(r.targets.size() + 1, 0);
+      for (size_t i = 0; i < cnt.size(); ++i) r.ptr[i + 1] = r.ptr[i] + cnt[i];
+      r.ent.resize((size_t)r.ptr.back());
+      std::vector<int64_t> pos(r.ptr.begin(), r.ptr.end() - 1);
+      for (size_t rec = 0; rec + 1 < qptr.size(); ++rec)
+        for (int64_t a = qptr[rec]; a < qptr[rec + 1]; ++a)
+          r.ent[(size_t)pos[(size_t)red_slot[(size_t)qflat[(size_t)a]]]++] = coff[rec] + (a - qptr[rec]);
+      for (int32_t d : r.targets) red_slot[(size_t)d] = -1;
+      reductions.emplace_back(level_index, std::move(r));
+    });
   }
 
   void finish_reductions() {
@@ -1837,7 +1913,7 @@ struct Factorizer {
     dstamp.assign((size_t)N, 0);
     {
       const char* env = getenv("HIFDE_HOST_THREADS");
-      nthreads = env ? std::max(1, atoi(env)) : std::min(16, std::max(1, omp_get_max_threads()));
+      nthreads = env ? std::max(1, atoi(env)) : std::min(15, std::max(1, omp_get_max_threads() - 1));
       HostCache& hc = host_cache();
       const bool same = hc.valid && hc.g.dim == g.dim && hc.g.n == g.n;
       if (!same) {
@@ -1872,6 +1948,8 @@ struct Factorizer {
 
     P.lap("reserve");
     const int Lv = g.nlevels;
+    F->levels.reserve((size_t)3 * std::max(Lv, 1) + 4);  // stable LevelRec addresses for the helper
+    helper.start();
     const double t_setup = now_s() - t0;
     HTRACE("setup done");
     std::vector<int32_t> act_tmp;
@@ -1926,6 +2004,7 @@ struct Factorizer {
         L.tag = (double)ell;
         elimination_level(gr, L.tag, L, false);
         record_trace(L, tl);
+        helper.post([this, &L]() { build_solve_plan(L); });
       }
       auto skel = [&](double tag, int kind) {
         const double tl = now_s();
@@ -1936,6 +2015,7 @@ struct Factorizer {
         L.tag = tag;
         skeleton_level(gr, tag, L);
         record_trace(L, tl);
+        helper.post([this, &L]() { build_solve_plan(L); });
       };
       if (opt.variant == HIFDE_VARIANT_HIFDE) {
         if (ell >= opt.skip_levels) skel(ell + 0.5, g.dim == 2 ? 0 : 1);
@@ -1963,11 +2043,12 @@ struct Factorizer {
       record_trace(L, tl);
     }
     P.lap(nullptr);
+    helper.drain();
+    build_solve_plan(F->levels.back());  // the terminal block
     finish_reductions();
     P.lap("reductions");
     // solve metadata to the device: small records one CTA each, large ones as
-    // tiled product phases
-    for (auto& L : F->levels) build_solve_plan(L);
+    // tiled product phases (built level by level on the helper thread)
     F->meta = meta.commit(s, [&](void* d, const void* h, size_t n) {
       if (!pinned_stage().copy(d, h, n)) HCK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s));
     });
