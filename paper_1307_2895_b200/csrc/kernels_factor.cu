@@ -555,8 +555,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   const int nslots = NT / G, sl = lane & (G - 1), slot = wid * (32 / G) + lane / G;
   double thr = 0.0;
   int k = kmax;
-  long long ph[4] = {0, 0, 0, 0}, ph2[3] = {0, 0, 0};
-  long long tc0 = clock64();
   for (int i = 0; i < kmax; ++i) {
     const int cur = (i & 1) * nc, nxt = nc - cur;
     const double* vn1 = cq + cur;
@@ -585,8 +583,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       const int ci = cat[i];
       for (int pos = lane; pos < nc; pos += 32) cato[pos] = pos == i ? p : (pos == bp ? ci : cat[pos]);
     }
-    long long tc1 = clock64();
-    ph[0] += tc1 - tc0;
     if (i == 0 && bv == 0.0) { k = 0; break; }  // zero block: everything redundant
     const double* v = Mc + (size_t)p * ldm;     // Householder vector: rows > i
     const double alpha = v[i];
@@ -602,8 +598,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
     if (rii <= thr) { k = i; break; }
     if (threadIdx.x == 0) { rdiag[i] = beta; dcol[p] = 1; }
-    long long tc2 = clock64();
-    ph[1] += tc2 - tc1;
     // trailing columns: G lanes per column, NT / G columns at once (the
     // step's latency is one column's dependency chain, not NW of them)
     for (int base = 0; base < nc; base += nslots) {
@@ -623,7 +617,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         }
         for (; r < nqm; r += G) s0 += v[r] * col[r];
         const double sd = group_sum((s0 + s1) + (s2 + s3), G);
-        ph2[0] += clock64() - tc2;
         const double w = tau * (col[i] + scal * sd);
         __syncwarp();
         if (act && sl == 0) col[i] -= w;
@@ -657,7 +650,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
           a0 += x * x;
         }
         acc = (a0 + a1) + (a2 + a3);
-        ph2[1] += clock64() - tc2;
       } else {
         double a0 = 0.0, a1 = 0.0;
         int r = i + 2 + sl;
@@ -670,7 +662,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       }
       acc = group_sum(acc, G);
       __syncwarp();
-      ph2[2] += clock64() - tc2;
       if (act) {
         const double cn = i + 1 < nqm ? col[i + 1] : 0.0;
         double nv = vn1[j];
@@ -689,16 +680,8 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         if (sl == 0) { vn1o[j] = nv; xno[j] = sqrt(acc); }
       }
     }
-    long long tc3 = clock64();
-    ph[2] += tc3 - tc2;
     __syncthreads();
-    tc0 = clock64();
-    ph[3] += tc0 - tc3;
   }
-  if (A.tlog && threadIdx.x == 0)
-    for (int q = 0; q < 4; ++q) A.tlog[(size_t)t.group * 16 + 8 + q] = (unsigned long long)ph[q];
-  if (A.tlog && threadIdx.x == 0)
-    for (int q = 0; q < 3; ++q) A.tlog[(size_t)t.group * 16 + 12 + q] = (unsigned long long)ph2[q];
   mark(6);
   // LAPACK order of the columns (the redundant ones as of step k), R_ii into place
   {
