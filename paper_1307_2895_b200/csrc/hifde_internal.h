@@ -98,6 +98,10 @@ constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA w
 constexpr int kSchurTile = 64;                 // schur_tile_kernel tile edge
 constexpr int kPanelB = 64;                    // blocked Cholesky panel width
 constexpr int kMaxSkelNc = 192;
+// cells this wide (or with fronts this large) take the multi-CTA blocked path
+// even when the front fits one CTA's shared memory: one CTA per wide cell is
+// latency-bound (measured: 0.5 ms for a 93-wide terminal block)
+constexpr int kBigCellNc = 64, kBigCellNf = 128;
 constexpr size_t kSolveDynSmem = 190 * 1024;   // solve record kernels: dynamic smem beside the 25 KB staging tile                // largest group skeletonized by one CTA (skel_group)
 
 // Kernel launchers (kernels_factor.cu / kernels_solve.cu).
@@ -114,7 +118,7 @@ void launch_panel_update(const ElimTask* tasks, const int4* work, int nwork, int
 void launch_big_finish(const ElimTask* tasks, int ncells, const Arenas& A, const double* dmin,
                        const double* diag_scale, cudaStream_t s);
 void launch_big_inverse(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
-constexpr int kInvLocalCols = 320;  // cells up to this nc: thread-per-column packed inverse
+constexpr int kInvLocalCols = 64;   // cells up to this nc: thread-per-column packed inverse
 void launch_inv_diag(const ElimTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
 void launch_inv_tiles(const ElimTask* tasks, const int4* work, int nwork, int p0, const Arenas& A,
                       cudaStream_t s);

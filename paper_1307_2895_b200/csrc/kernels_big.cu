@@ -172,10 +172,9 @@ __global__ void __launch_bounds__(256) panel_chol_kernel(const ElimTask* __restr
       for (int i = k + threadIdx.x; i < pw; i += 256) D[i][k - 1] *= prev_inv;
       if (threadIdx.x == 0) D[k - 1][k - 1] = prev_piv;
     }
-    const int m = pw - k - 1;
-    for (int e = threadIdx.x; e < m * m; e += 256) {
-      const int ii = e / m, jj = e - ii * m;
-      if (jj <= ii) D[k + 1 + ii][k + 1 + jj] -= D[k + 1 + ii][k] * (D[k + 1 + jj][k] * rakk);
+    for (int i = k + 1 + (int)(threadIdx.x >> 5); i < pw; i += 8) {  // warp per row
+      const double dik = D[i][k];
+      for (int j = k + 1 + (int)(threadIdx.x & 31); j <= i; j += 32) D[i][j] -= dik * (D[j][k] * rakk);
     }
     prev_piv = sqrt(akk);
     prev_inv = 1.0 / prev_piv;

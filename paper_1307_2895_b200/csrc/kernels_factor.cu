@@ -104,13 +104,11 @@ __device__ int chol_1sync(double* A, int n, int ld, double* red) {
       for (int i = k + threadIdx.x; i < n; i += NT) A[(size_t)i * ld + k - 1] *= prev_inv;
       if (threadIdx.x == 0) A[(size_t)(k - 1) * ld + k - 1] = prev_piv;
     }
-    const int m = n - k - 1;
-    for (int e = threadIdx.x; e < m * m; e += NT) {
-      const int ii = e / m, jj = e - ii * m;
-      if (jj <= ii) {
-        const int i = k + 1 + ii, j = k + 1 + jj;
-        A[(size_t)i * ld + j] -= A[(size_t)i * ld + k] * (A[(size_t)j * ld + k] * rakk);
-      }
+    // trailing update, lower triangle: warp per row, lanes over columns
+    for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
+      const double aik = A[(size_t)i * ld + k];
+      for (int j = k + 1 + (int)(threadIdx.x & 31); j <= i; j += 32)
+        A[(size_t)i * ld + j] -= aik * (A[(size_t)j * ld + k] * rakk);
     }
     prev_piv = piv;
     prev_inv = 1.0 / piv;
@@ -132,10 +130,9 @@ __device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, in
     const double cinv = 1.0 / C[(size_t)i * ldc + i];
     if (i > 0)
       for (int j = threadIdx.x; j < m; j += NT) B[(size_t)(i - 1) * ldb + j] *= prev;
-    const int rows = n - i - 1;
-    for (int e = threadIdx.x; e < rows * m; e += NT) {
-      const int l = i + 1 + e / m, j = e - (e / m) * m;
-      B[(size_t)l * ldb + j] -= C[(size_t)l * ldc + i] * (B[(size_t)i * ldb + j] * cinv);
+    for (int l = i + 1 + (int)(threadIdx.x >> 5); l < n; l += NT / 32) {  // warp per row
+      const double c = C[(size_t)l * ldc + i];
+      for (int j = (int)(threadIdx.x & 31); j < m; j += 32) B[(size_t)l * ldb + j] -= c * (B[(size_t)i * ldb + j] * cinv);
     }
     prev = cinv;
   }
@@ -226,10 +223,13 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
     const double* bv = A.bvals + A.blk_val_off[bid];
     for (int k = threadIdx.x; k < nb; k += NT) smap[k] = front_pos(sdofs, nc, nq, bd[k]);
     __syncthreads();
-    for (int e = threadIdx.x; e < nb * nb; e += NT) {
-      const int k = e / nb, l = e - k * nb;
-      const int pk = smap[k], pl = smap[l];
-      if (pk >= 0 && pl >= 0) F[pk * nf + pl] += bv[e];
+    for (int k = (int)(threadIdx.x >> 5); k < nb; k += NT / 32) {  // warp per block row
+      const int pk = smap[k];
+      if (pk < 0) continue;
+      for (int l = (int)(threadIdx.x & 31); l < nb; l += 32) {
+        const int pl = smap[l];
+        if (pl >= 0) F[pk * nf + pl] += bv[(size_t)k * nb + l];
+      }
     }
     __syncthreads();
   }
@@ -438,12 +438,15 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       smap[k] = (p >= 0 && salive[p]) ? p : -1;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nb * nb; e += NT) {
-      const int k = e / nb, l = e - k * nb;
-      const int pk = smap[k], pl = smap[l];
-      if (pk < 0 || pl < 0 || pl >= nc) continue;
-      if (pk < nc) Acc[pk * nc + pl] += bv[e];
-      else Mq[(pk - nc) + (size_t)pl * ldq] += bv[e];
+    for (int k = (int)(threadIdx.x >> 5); k < nb; k += NT / 32) {  // warp per block row
+      const int pk = smap[k];
+      if (pk < 0) continue;
+      for (int l = (int)(threadIdx.x & 31); l < nb; l += 32) {
+        const int pl = smap[l];
+        if (pl < 0 || pl >= nc) continue;
+        if (pk < nc) Acc[pk * nc + pl] += bv[(size_t)k * nb + l];
+        else Mq[(pk - nc) + (size_t)pl * ldq] += bv[(size_t)k * nb + l];
+      }
     }
     __syncthreads();
   }

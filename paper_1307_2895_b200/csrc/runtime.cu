@@ -773,7 +773,7 @@ struct Factorizer {
       const size_t ib = align16(sizeof(int32_t) * (size_t)(nf + T.maxnb));
       const size_t need = ib + sizeof(double) * (size_t)nf * nf;
       const size_t need_inv = need + sizeof(double) * (size_t)nc * nc;
-      if (need <= kSmemCap) {
+      if (need <= kSmemCap && (is_top || (nc < kBigCellNc && nf < kBigCellNf))) {
         // -2: room for the inverse workspace after the front as well
         T.scratch_off = need_inv <= kSmemCap ? -2 : -1;
         smem_need[(size_t)t] = T.scratch_off == -2 ? need_inv : need;
