@@ -272,38 +272,36 @@ def run_gpu(args, world, rank, local):
 
 
 def roofline(level_info, pk, pk_kind, args):
-    """HBM roofline of the dominant kernel class.
+    """HBM roofline of the dominant kernel launch.
 
-    Algorithmic bytes per level follow SURVEY.md 8(d) (elimination:
-    8[(nc+nq)^2 + nc^2 + nc + nc nq + 2 nq^2] per cell; skeletonization:
-    8[nq nc + nc^2 + k r + r^2 + r + r k + 2k^2] per group), summed over the
-    cells each launch processes; the duration is the CUDA-event time of the
-    level's kernel launches on the library's stream (recorded by the library).
-    The kernel class (elim_kernel / skel_kernel) with the larger total time is
-    reported."""
-    classes = {"elim_kernel": [0.0, 0.0, 0.0, 0], "skel_kernel": [0.0, 0.0, 0.0, 0]}
-    for d in level_info:
-        key = "skel_kernel" if d["kind"] == 1 else "elim_kernel"
-        c = classes[key]
-        c[0] += d["gbytes"]
-        c[1] += d["gpu_seconds"]
-        c[2] += d["gflop"]
-        c[3] += 1
-    name, (gb, sec, gf, nl) = max(classes.items(), key=lambda kv: kv[1][1])
+    In exact order every skeletonization level is ONE launch of
+    skel_ordered_kernel, and every level's launches are timed by CUDA events
+    on the library's stream; the dominant launch is the level with the
+    largest event time.  achieved = that level's algorithmic bytes (SURVEY.md
+    8(d): 8[nq nc + nc^2 + k r + r^2 + r + r k + 2k^2] per group, 8[(nc+nq)^2
+    + nc^2 + nc + nc nq + 2 nq^2] per cell) / its event time.  traffic = the
+    DRAM bytes ncu measured for the same launch (profiles/roofline_r01.json).
+    The launch is bound by the reference-order dependency chain, not by HBM
+    (profiles/r01_summary.md), hence the small fraction."""
+    dom = max(level_info[:-1], key=lambda d: d["gpu_seconds"])
+    sec, gb, gf = dom["gpu_seconds"], dom["gbytes"], dom["gflop"]
     achieved = gb / sec if sec > 0 else None
     peak = pk.get("hbm_gbs")
+    traffic = None
     prof = os.path.join(ROOT, "profiles", "roofline_r01.json")
-    extra = {}
     if os.path.exists(prof):
         try:
-            extra = json.load(open(prof)).get(name, {})
+            tb = json.load(open(prof))["skel_levels_dram_bytes"].get(f"{dom['tag']:.1f}")
+            traffic = tb / 1e9 if tb else None
         except Exception:
-            extra = {}
+            traffic = None
+    name = "skel_ordered_kernel" if dom["kind"] == 1 else "elim_kernels"
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved and peak else None,
-            "traffic": extra.get("traffic_gbytes"), "kernel": name, "levels": nl,
-            "kernel_seconds": sec, "algorithmic_gbytes": gb, "algorithmic_gflop": gf,
+            "traffic": traffic, "traffic_unit": "GB per launch", "kernel": name, "level": dom["tag"],
+            "launch_seconds": sec, "algorithmic_gbytes": gb, "algorithmic_gflop": gf,
             "achieved_gflops": gf / sec if sec > 0 else None,
+            "limiter": "reference-order dependency chain (latency), see profiles/r01_summary.md",
             "peak_kind": pk_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
 
 
