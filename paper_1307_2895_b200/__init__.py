@@ -10,11 +10,11 @@ import os as _os
 _os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # before libgomp initializes
 
 from .driver import (FactorizationError, GeneralizedLDL, IndefiniteBlockError,
-                     SingularBlockError, apply_inverse, device_count, factor_hifde,
+                     SingularBlockError, apply_inverse, densify, device_count, factor_hifde,
                      factor_hifde3x, factor_mf)
 from .problems import (CoeffField, GridConfig, assemble, baseline_problem, build_grid,
                        constant_field, gaussian_contrast_field, high_contrast_field)
 from .gldl import export_factor, import_factor, load_factor, read_gldl, save_factor, write_gldl
-from .solvers import EstimateResult, estimate_apply_error, estimate_solve_error, pcg, pcg_gpu
+from .solvers import EstimateResult, estimate_apply_error, estimate_solve_error, gmres, pcg, pcg_gpu
 
 __version__ = "0.1.0"

@@ -214,5 +214,11 @@ def apply_inverse(f: GeneralizedLDL, b) -> np.ndarray:
     return f.apply_inverse(b)
 
 
+def densify(f: GeneralizedLDL) -> np.ndarray:
+    """Dense N x N matrix of the factored operator, F I (src/driver.py:262-264);
+    testing oracle for small N."""
+    return f.apply(np.eye(f.n))
+
+
 def device_count() -> int:
     return int(L.load().hifde_device_count())

@@ -120,3 +120,59 @@ def estimate_apply_error(a, f, seed: int = 0) -> EstimateResult:
 def estimate_solve_error(a, f, seed: int = 0) -> EstimateResult:
     """||I - A F^-1|| by power iteration on the device (src/krylov.py:189-201)."""
     return _power_norm_gpu(f, a, 2, (seed, 0xC))
+
+
+def gmres(a, b, precond=None, tol: float = 1e-12, max_iter: int = 1000, restart: int = 32) -> SolveReport:
+    """Right-preconditioned restarted GMRES (src/krylov.py:80-137 semantics):
+    modified Gram-Schmidt Arnoldi on A M, Givens rotations on the Hessenberg
+    matrix; n_i counts operator applications; stops on ||b - A x|| / ||b||."""
+    M = precond if precond is not None else (lambda v: v)
+    A = a.__matmul__ if hasattr(a, "__matmul__") else a
+    b = np.asarray(b, dtype=float)
+    bn = float(np.linalg.norm(b))
+    if bn == 0.0:
+        return SolveReport(np.zeros_like(b), 0, 0.0, True)
+    x = np.zeros_like(b)
+    its = 0
+    while True:
+        r = b - A(x)
+        res = float(np.linalg.norm(r)) / bn
+        if res <= tol:
+            return SolveReport(x, its, res, True)
+        if its >= max_iter:
+            return SolveReport(x, its, res, False)
+        m = min(restart, max_iter - its)
+        V = np.zeros((m + 1, b.size))
+        Hm = np.zeros((m + 1, m))
+        c, sn = np.zeros(m), np.zeros(m)
+        rhs = np.zeros(m + 1)
+        beta = res * bn
+        V[0] = r / beta
+        rhs[0] = beta
+        used = 0
+        for j in range(m):
+            w = A(M(V[j]))
+            its += 1
+            for i in range(j + 1):          # modified Gram-Schmidt
+                Hm[i, j] = float(w @ V[i])
+                w = w - Hm[i, j] * V[i]
+            hn = float(np.linalg.norm(w))
+            Hm[j + 1, j] = hn
+            if hn != 0.0:
+                V[j + 1] = w / hn
+            for i in range(j):              # earlier rotations
+                hi, hi1 = Hm[i, j], Hm[i + 1, j]
+                Hm[i, j] = c[i] * hi + sn[i] * hi1
+                Hm[i + 1, j] = -sn[i] * hi + c[i] * hi1
+            rho = float(np.hypot(Hm[j, j], Hm[j + 1, j]))
+            c[j], sn[j] = (1.0, 0.0) if rho == 0.0 else (Hm[j, j] / rho, Hm[j + 1, j] / rho)
+            Hm[j, j], Hm[j + 1, j] = rho, 0.0
+            rhs[j + 1] = -sn[j] * rhs[j]
+            rhs[j] = c[j] * rhs[j]
+            used = j + 1
+            if abs(rhs[j + 1]) / bn <= tol or hn == 0.0:
+                break
+        y = np.zeros(used)
+        for i in range(used - 1, -1, -1):   # back substitution on the rotated H
+            y[i] = (rhs[i] - Hm[i, i + 1:used] @ y[i + 1:]) / Hm[i, i]
+        x = x + M(V[:used].T @ y)

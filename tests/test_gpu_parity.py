@@ -134,6 +134,24 @@ def test_error_estimators_match_reference(name):
         assert abs(es.iterations - int(gd["e_s_iters"])) <= 2
 
 
+def test_densify_and_gmres():
+    """densify (F I, src/driver.py:262-264) and right-preconditioned GMRES
+    (src/krylov.py:80-137) on the GPU factor: the dense operator matches A
+    to the factor's accuracy, GMRES converges like PCG."""
+    gd = G.load("g2d_n16_m2")
+    _, csr = G.build_problem(gd)
+    g, f = _factor(gd, csr)
+    Fd = H.densify(f)
+    A = csr.toarray()
+    assert Fd.shape == A.shape
+    assert np.linalg.norm(Fd - A) <= 10 * float(gd["apply_err"]) * np.linalg.norm(A) + 1e-12
+    assert np.allclose(Fd, Fd.T, rtol=0, atol=1e-12 * np.abs(A).max())
+    b = G.rhs(gd, g.ndof)[:, 0]
+    rep = H.gmres(csr, b, f.apply_inverse, tol=1e-12)
+    assert rep.converged and np.linalg.norm(csr @ rep.x - b) <= 1.01e-12 * np.linalg.norm(b)
+    assert abs(rep.n_i - H.pcg(csr, b, f.apply_inverse, tol=1e-12).n_i) <= 2
+
+
 def test_apply_large_cells_round_trip():
     """apply on factors with cells beyond the one-CTA paths (blocked inverse,
     tiled solve records): still the exact inverse of apply_inverse."""
