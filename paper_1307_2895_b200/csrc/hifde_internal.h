@@ -98,6 +98,10 @@ constexpr size_t kSmemCapBytes = 220 * 1024;  // dynamic shared memory per CTA w
 constexpr int kSchurTile = 64;                 // schur_tile_kernel tile edge
 constexpr int kPanelB = 64;                    // blocked Cholesky panel width
 constexpr int kMaxSkelNc = 192;
+// Column stride of a shared-memory neighbour block: = 8 (mod 16) doubles, so
+// the G-lane column slices of one warp's 4 columns fall on disjoint banks
+// (2 wavefronts per 64-bit warp access instead of 3-4).
+__host__ __device__ inline int skel_ldq(int nq) { return nq < 32 ? nq : nq + ((24 - nq % 16) % 16); }
 // cells this wide (or with fronts this large) take the multi-CTA blocked path
 // even when the front fits one CTA's shared memory: one CTA per wide cell is
 // latency-bound (measured: 0.5 ms for a 93-wide terminal block)

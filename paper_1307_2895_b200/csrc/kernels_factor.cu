@@ -378,11 +378,11 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   // A_cc and the post-CPQR matrices global; 2 all global
   double* wsh = cq + 5 * nc;
   double* wgl = A.scratch + (t.scratch_off > 0 ? t.scratch_off : 0);
-  const int ldq = nq;                                  // Mq column-major, ld nq
+  const int ldq = t.mode <= 1 ? skel_ldq(nq) : nq;    // Mq column-major (padded in shared memory)
   double *Acc, *Mq, *vn1, *vn2, *Z;
   if (t.mode == 1) {
     Mq = wsh;
-    vn1 = Mq + (size_t)nq * nc;
+    vn1 = Mq + (size_t)ldq * nc;
     vn2 = vn1 + nc;
     Acc = wgl;
     Z = Acc + (size_t)nc * nc;
@@ -395,8 +395,8 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   } else {
     double* ws = t.mode == 0 ? wsh : wgl;
     Acc = ws;                                          // nc x nc, row-major (symmetric)
-    Mq = Acc + (size_t)nc * nc;                        // nq x nc
-    vn1 = Mq + (size_t)nq * nc;
+    Mq = Acc + (size_t)nc * nc;                        // nq x nc, ld ldq
+    vn1 = Mq + (size_t)ldq * nc;
     vn2 = vn1 + nc;
     Z = vn2 + nc;                                      // post-CPQR workspace
   }
@@ -414,7 +414,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   }
   for (int i = threadIdx.x; i < nc; i += NT) perm[i] = i;
   for (int e = threadIdx.x; e < nc * nc; e += NT) Acc[e] = 0.0;
-  for (size_t e = threadIdx.x; e < (size_t)nq * nc; e += NT) Mq[e] = 0.0;
+  for (size_t e = threadIdx.x; e < (size_t)ldq * nc; e += NT) Mq[e] = 0.0;
   __syncthreads();
   for (int p = threadIdx.x; p < nc; p += NT) {
     const int g = sdofs[p];

@@ -1170,8 +1170,9 @@ struct Factorizer {
         // index arrays, then the CPQR vectors (kernels_factor.cu skel_group)
         const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * nc)) + sizeof(double) * 5 * (size_t)nc;
         const size_t q4 = (size_t)nc * nc / 4 + nc;
-        const size_t wsd = (size_t)nf * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
-        const size_t mq = (size_t)nq * nc + 2 * (size_t)nc;
+        const size_t lq = (size_t)skel_ldq(nq);  // padded column stride in shared memory
+        const size_t wsd = (size_t)(nc + lq) * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
+        const size_t mq = lq * nc + 2 * (size_t)nc;
         if (nc > kMaxSkelNc) {
           T.mode = 2;  // beyond the one-CTA CPQR
         } else if (ib + sizeof(double) * wsd <= kSmemCap) {

@@ -20,19 +20,19 @@ __device__ __forceinline__ double group_sum(double v, int G) {
 
 template <int NT, int VAR>
 __global__ void __launch_bounds__(NT) cpqr(const double* __restrict__ Min, int nq, int nc, double eps,
-                                          long long* cyc, int* kout) {
+                                          long long* cyc, int* kout, int ldpad) {
   extern __shared__ double sm[];
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int ldm = nq, nqm = nq;
+  const int ldm = ldpad, nqm = nq;
   double* Mc = sm;
-  double* cq = Mc + (size_t)nq * nc;     // vn1 x2 | xn x2 | rdiag | vn2 | hb x2 (beta,tau,scal)
+  double* cq = Mc + (size_t)ldm * nc;     // vn1 x2 | xn x2 | rdiag | vn2 | hb x2 (beta,tau,scal)
   double* rdiag = cq + 4 * nc;
   double* vn2 = cq + 5 * nc;
   double* hb = cq + 6 * nc;              // 2 buffers x 3 x nc
   int* dcol = (int*)(hb + 6 * nc);
   int* cpos = dcol + nc;
-  for (int e = threadIdx.x; e < nq * nc; e += NT) Mc[e] = Min[e];
+  for (int e = threadIdx.x; e < nq * nc; e += NT) Mc[(e / nq) * ldm + e % nq] = Min[e];
   __syncthreads();
   for (int j = wid; j < nc; j += NW) {
     const double* col = Mc + (size_t)j * ldm;
@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(NT) cpqr(const double* __restrict__ Min, int n
 }
 
 template <int NT, int VAR>
-void run(int nq, int nc, double eps) {
+void run(int nq, int nc, double eps, bool pad = false) {
+  const int ld = pad ? ((nq + 7) / 16) * 16 + 8 : nq;  // column stride = 16 mod 32 words
   std::vector<double> h((size_t)nq * nc);
   srand(1);
   for (auto& x : h) x = (double)rand() / RAND_MAX - 0.5;
@@ -191,10 +192,10 @@ void run(int nq, int nc, double eps) {
   double* d; long long* cyc; int* k;
   cudaMalloc(&d, h.size() * 8); cudaMallocManaged(&cyc, 8); cudaMallocManaged(&k, 4);
   cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
-  size_t smem = 8 * ((size_t)nq * nc + 12 * nc) + 8 * nc * 4;
+  size_t smem = 8 * ((size_t)ld * nc + 12 * nc) + 8 * nc * 4;
   cudaFuncSetAttribute(cpqr<NT, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int it = 0; it < 3; ++it) { cpqr<NT, VAR><<<1, NT, smem>>>(d, nq, nc, eps, cyc, k); cudaDeviceSynchronize(); }
-  printf("NT %3d var %d nq %3d nc %3d: k %3d  cycles %7lld  per step %6.0f  (%s)\n", NT, VAR, nq, nc, *k, *cyc,
+  for (int it = 0; it < 3; ++it) { cpqr<NT, VAR><<<1, NT, smem>>>(d, nq, nc, eps, cyc, k, ld); cudaDeviceSynchronize(); }
+  printf("NT %3d var %d ld %3d nq %3d nc %3d: k %3d  cycles %7lld  per step %6.0f  (%s)\n", NT, VAR, ld, nq, nc, *k, *cyc,
          (double)*cyc / (*k + 1), cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -203,5 +204,7 @@ int main() {
   run<512, 0>(83, 15, 1e-9);  run<512, 1>(83, 15, 1e-9);
   run<512, 0>(185, 31, 1e-9); run<512, 1>(185, 31, 1e-9);
   run<512, 0>(298, 60, 1e-9); run<512, 1>(298, 60, 1e-9);
+  run<128, 0>(83, 15, 1e-9, true);
+  run<512, 0>(185, 31, 1e-9, true); run<512, 0>(298, 60, 1e-9, true);
   return 0;
 }
