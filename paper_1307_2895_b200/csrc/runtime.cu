@@ -426,6 +426,84 @@ struct FrontSym {  // result of the symbolic analysis of one cell / group
 // ---------------------------------------------------------------------------
 // Factorization state
 // ---------------------------------------------------------------------------
+// Host <-> device copies of the user's pageable right-hand sides/solutions
+// through a persistent pinned double buffer: chunks are copied by several
+// host threads into pinned memory while the previous chunk's DMA runs (a
+// pageable cudaMemcpy stages through the driver at one thread's memcpy speed).
+struct PinnedXfer {
+  static constexpr size_t kChunk = 8u << 20;
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int dev = -1;
+  std::mutex m;
+  bool ready(int device) {
+    if (buf[0] && dev == device) return true;
+    if (buf[0]) return false;  // bound to another device: fall back to plain copies
+    for (int i = 0; i < 2; ++i) {
+      if (cudaHostAlloc((void**)&buf[i], kChunk, cudaHostAllocDefault) != cudaSuccess) return false;
+      if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) return false;
+    }
+    dev = device;
+    return true;
+  }
+  static void pmemcpy(char* d, const char* s, size_t n) {
+    const int nth = n >= (1u << 20) ? 8 : 1;
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int t = 0; t < nth; ++t) {
+      const size_t lo = n * t / nth, hi = n * (t + 1) / nth;
+      std::memcpy(d + lo, s + lo, hi - lo);
+    }
+  }
+  void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    int device = 0;
+    HCK(cudaGetDevice(&device));
+    std::lock_guard<std::mutex> lk(m);
+    if (bytes < (1u << 20) || !ready(device)) {
+      HCK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+      return;
+    }
+    for (size_t off = 0, c = 0; off < bytes; off += kChunk, ++c) {
+      const int b = (int)(c & 1);
+      const size_t n = std::min(kChunk, bytes - off);
+      HCK(cudaEventSynchronize(ev[b]));  // the slot's previous DMA is done
+      pmemcpy(buf[b], (const char*)src + off, n);
+      HCK(cudaMemcpyAsync((char*)dst + off, buf[b], n, cudaMemcpyHostToDevice, s));
+      HCK(cudaEventRecord(ev[b], s));
+    }
+    HCK(cudaEventSynchronize(ev[0]));  // the slots may be reused by the next call at once
+    HCK(cudaEventSynchronize(ev[1]));
+  }
+  void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    int device = 0;
+    HCK(cudaGetDevice(&device));
+    std::lock_guard<std::mutex> lk(m);
+    if (bytes < (1u << 20) || !ready(device)) {
+      HCK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+      HCK(cudaStreamSynchronize(s));
+      return;
+    }
+    const size_t nch = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t c) {
+      const int b = (int)(c & 1);
+      const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+      HCK(cudaMemcpyAsync(buf[b], (const char*)src + off, n, cudaMemcpyDeviceToHost, s));
+      HCK(cudaEventRecord(ev[b], s));
+    };
+    issue(0);
+    for (size_t c = 0; c < nch; ++c) {
+      const int b = (int)(c & 1);
+      HCK(cudaEventSynchronize(ev[b]));
+      if (c + 1 < nch) issue(c + 1);  // the other slot's DMA overlaps this copy-out
+      const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+      pmemcpy((char*)dst + off, buf[b], n);
+    }
+  }
+};
+PinnedXfer& pinned_xfer() {
+  static PinnedXfer x;
+  return x;
+}
+
 // One background host thread per factorization for work that only the solve
 // needs (reductions, solve plans): jobs run in order, off the level loop.
 struct Helper {
@@ -1876,10 +1954,10 @@ struct Factorizer {
     // A0: the symbolic analysis needs the pattern on the host
     if (opt.input_on_device) {
       indptr_own.resize((size_t)N + 1);
-      HCK(cudaMemcpy(indptr_own.data(), ip, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      pinned_xfer().d2h(indptr_own.data(), ip, (N + 1) * sizeof(int64_t), s);
       nnz = indptr_own.back();
       indices_own.resize((size_t)nnz);
-      HCK(cudaMemcpy(indices_own.data(), ix, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      pinned_xfer().d2h(indices_own.data(), ix, nnz * sizeof(int32_t), s);
       indptr = indptr_own.data();
       indices = indices_own.data();
       d_indptr = const_cast<int64_t*>(ip);
@@ -2115,84 +2193,6 @@ struct Factorizer {
 // ---------------------------------------------------------------------------
 // Solve sweep
 // ---------------------------------------------------------------------------
-// Host <-> device copies of the user's pageable right-hand sides/solutions
-// through a persistent pinned double buffer: chunks are copied by several
-// host threads into pinned memory while the previous chunk's DMA runs (a
-// pageable cudaMemcpy stages through the driver at one thread's memcpy speed).
-struct PinnedXfer {
-  static constexpr size_t kChunk = 8u << 20;
-  char* buf[2] = {nullptr, nullptr};
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  int dev = -1;
-  std::mutex m;
-  bool ready(int device) {
-    if (buf[0] && dev == device) return true;
-    if (buf[0]) return false;  // bound to another device: fall back to plain copies
-    for (int i = 0; i < 2; ++i) {
-      if (cudaHostAlloc((void**)&buf[i], kChunk, cudaHostAllocDefault) != cudaSuccess) return false;
-      if (cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess) return false;
-    }
-    dev = device;
-    return true;
-  }
-  static void pmemcpy(char* d, const char* s, size_t n) {
-    const int nth = n >= (1u << 20) ? 8 : 1;
-#pragma omp parallel for num_threads(nth) schedule(static)
-    for (int t = 0; t < nth; ++t) {
-      const size_t lo = n * t / nth, hi = n * (t + 1) / nth;
-      std::memcpy(d + lo, s + lo, hi - lo);
-    }
-  }
-  void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    int device = 0;
-    HCK(cudaGetDevice(&device));
-    std::lock_guard<std::mutex> lk(m);
-    if (bytes < (1u << 20) || !ready(device)) {
-      HCK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-      return;
-    }
-    for (size_t off = 0, c = 0; off < bytes; off += kChunk, ++c) {
-      const int b = (int)(c & 1);
-      const size_t n = std::min(kChunk, bytes - off);
-      HCK(cudaEventSynchronize(ev[b]));  // the slot's previous DMA is done
-      pmemcpy(buf[b], (const char*)src + off, n);
-      HCK(cudaMemcpyAsync((char*)dst + off, buf[b], n, cudaMemcpyHostToDevice, s));
-      HCK(cudaEventRecord(ev[b], s));
-    }
-    HCK(cudaEventSynchronize(ev[0]));  // the slots may be reused by the next call at once
-    HCK(cudaEventSynchronize(ev[1]));
-  }
-  void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    int device = 0;
-    HCK(cudaGetDevice(&device));
-    std::lock_guard<std::mutex> lk(m);
-    if (bytes < (1u << 20) || !ready(device)) {
-      HCK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
-      HCK(cudaStreamSynchronize(s));
-      return;
-    }
-    const size_t nch = (bytes + kChunk - 1) / kChunk;
-    auto issue = [&](size_t c) {
-      const int b = (int)(c & 1);
-      const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
-      HCK(cudaMemcpyAsync(buf[b], (const char*)src + off, n, cudaMemcpyDeviceToHost, s));
-      HCK(cudaEventRecord(ev[b], s));
-    };
-    issue(0);
-    for (size_t c = 0; c < nch; ++c) {
-      const int b = (int)(c & 1);
-      HCK(cudaEventSynchronize(ev[b]));
-      if (c + 1 < nch) issue(c + 1);  // the other slot's DMA overlaps this copy-out
-      const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
-      pmemcpy((char*)dst + off, buf[b], n);
-    }
-  }
-};
-PinnedXfer& pinned_xfer() {
-  static PinnedXfer x;
-  return x;
-}
-
 void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, bool dev, cudaStream_t s) {
   const int64_t N = F->n;
   const size_t bytes = (size_t)N * nrhs * sizeof(double);
