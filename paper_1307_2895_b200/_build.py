@@ -23,8 +23,9 @@ SOURCES = [
     "csrc/kernels_krylov.cu",
     "csrc/runtime.cu",
     "csrc/partition.cpp",
+    "csrc/hostprof.cpp",
 ]
-HEADERS = ["csrc/hifde_internal.h", "csrc/partition.h"]
+HEADERS = ["csrc/hifde_internal.h", "csrc/partition.h", "csrc/hostprof.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -48,7 +49,7 @@ def _stale() -> bool:
 def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3,-fopenmp", "-lgomp",
+    cmd = [_nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-O3,-fopenmp,-g", "-lgomp", "-ldl",
            "-shared", "-cudart", "static", "--threads", "4",
            "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
            *[os.path.join(PKG, s) for s in SOURCES]]

@@ -33,6 +33,7 @@
 
 #include "../../include/hifde_gpu.h"
 #include "hifde_internal.h"
+#include "hostprof.h"
 #include "partition.h"
 
 #include <omp.h>
@@ -284,32 +285,52 @@ struct hifde_factor {
 namespace hifde {
 namespace {
 
+
+// Growable array of trivially copyable T whose resize does not initialize
+// (the index arena's host mirror is always written before it is read).
 template <class T>
-T* to_device(const std::vector<T>& h) {
-  if (h.empty()) return nullptr;
-  T* d = nullptr;
-  HCK(cudaMalloc((void**)&d, h.size() * sizeof(T)));
-  HCK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
-  return d;
-}
+struct PodVec {
+  std::unique_ptr<T[]> p;
+  size_t n = 0, cap = 0;
+  T* data() { return p.get(); }
+  const T* data() const { return p.get(); }
+  size_t size() const { return n; }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+  void reserve(size_t c) {
+    if (c <= cap) return;
+    std::unique_ptr<T[]> q(new T[c]);
+    if (n) std::memcpy(q.get(), p.get(), n * sizeof(T));
+    p.swap(q);
+    cap = c;
+  }
+  void resize(size_t m) {
+    if (m > cap) reserve(std::max(m, cap + cap / 2));
+    n = m;
+  }
+  void assign(const T* b, const T* e) {
+    resize((size_t)(e - b));
+    if (n) std::memcpy(p.get(), b, n * sizeof(T));
+  }
+};
 
 // Solve metadata of a whole factorization packed into one device allocation
 // and one asynchronous upload (instead of an allocation + blocking copy each).
 struct MetaPack {
-  std::vector<char> h;
+  PodVec<char> h;
   std::vector<std::pair<void**, size_t>> slots;
   template <class T>
   void add(T** slot, const std::vector<T>& v) {
     *slot = nullptr;
     if (v.empty()) return;
     const size_t off = (h.size() + 255) & ~(size_t)255;
-    h.resize(off + v.size() * sizeof(T));
+    h.resize(off + v.size() * sizeof(T));  // PodVec: grows x1.5, no zero fill
     std::memcpy(h.data() + off, v.data(), v.size() * sizeof(T));
     slots.emplace_back((void**)slot, off);
   }
   // returns the device block (owned by the caller)
   char* commit(cudaStream_t s, const std::function<void(void*, const void*, size_t)>& up) {
-    if (h.empty()) return nullptr;
+    if (h.size() == 0) return nullptr;
     char* d = nullptr;
     HCK(cudaMallocAsync((void**)&d, h.size(), s));
     up(d, h.data(), h.size());
@@ -507,70 +528,97 @@ PinnedXfer& pinned_xfer() {
 // One background host thread per factorization for work that only the solve
 // needs (reductions, solve plans): jobs run in order, off the level loop.
 struct Helper {
+  // Persistent worker (one per process, g_host_mutex serializes factorizations):
+  // jobs run in order; wait(seq) blocks until job `seq` has finished.
   std::thread th;
   std::mutex m;
-  std::condition_variable cv;
+  std::condition_variable cv, cv_done;
   std::deque<std::function<void()>> q;
-  bool stop = false, running = false;
+  uint64_t posted = 0, finished = 0;
+  bool started = false, inline_mode = false;
   std::exception_ptr err;
-  void start() {
-    running = true;
+  void ensure_started() {
+    if (started) return;
+    started = true;
     th = std::thread([this]() {
       for (;;) {
         std::function<void()> job;
         {
           std::unique_lock<std::mutex> lk(m);
-          cv.wait(lk, [&]() { return stop || !q.empty(); });
-          if (q.empty()) return;
+          cv.wait(lk, [&]() { return !q.empty(); });
           job = std::move(q.front());
           q.pop_front();
         }
+        if (!job) return;  // shutdown
         try {
           job();
         } catch (...) {
           std::lock_guard<std::mutex> lk(m);
           if (!err) err = std::current_exception();
         }
+        {
+          std::lock_guard<std::mutex> lk(m);
+          ++finished;
+        }
+        cv_done.notify_all();
       }
     });
   }
-  void post(std::function<void()> job) {
-    if (!running) { job(); return; }
+  uint64_t post(std::function<void()> job) {
+    if (inline_mode) { job(); return 0; }
+    ensure_started();
+    uint64_t id;
     {
       std::lock_guard<std::mutex> lk(m);
       q.push_back(std::move(job));
+      id = ++posted;
     }
     cv.notify_one();
+    return id;
   }
-  void drain() {  // wait for every posted job; rethrow the first failure
-    if (running) {
-      {
-        std::lock_guard<std::mutex> lk(m);
-        stop = true;
-      }
-      cv.notify_one();
-      th.join();
-      running = false;
+  void wait(uint64_t id) {
+    if (inline_mode || id == 0) return;
+    std::unique_lock<std::mutex> lk(m);
+    cv_done.wait(lk, [&]() { return finished >= id; });
+  }
+  void drain() {  // every posted job finished; rethrow (and clear) the first failure
+    uint64_t id;
+    {
+      std::lock_guard<std::mutex> lk(m);
+      id = posted;
     }
-    if (err) std::rethrow_exception(err);
+    wait(id);
+    std::exception_ptr e;
+    {
+      std::lock_guard<std::mutex> lk(m);
+      e = err;
+      err = nullptr;
+    }
+    if (e) std::rethrow_exception(e);
   }
   ~Helper() {
-    if (running) {
-      {
-        std::lock_guard<std::mutex> lk(m);
-        stop = true;
-      }
-      cv.notify_one();
-      th.join();
+    if (!started) return;
+    {
+      std::lock_guard<std::mutex> lk(m);
+      q.push_back(nullptr);
     }
+    cv.notify_one();
+    th.join();
   }
 };
+Helper& helper_thread() {
+  static Helper h;
+  return h;
+}
 
 struct Factorizer {
-  std::thread a0_thread;  // host CSR upload in flight
+  uint64_t a0_job = 0;  // host CSR upload in flight on the helper thread
   cudaError_t a0_err = cudaSuccess;
   void a0_ready() {
-    if (a0_thread.joinable()) a0_thread.join();
+    if (a0_job) {
+      helper.wait(a0_job);
+      a0_job = 0;
+    }
     if (a0_err != cudaSuccess) {
       const cudaError_t e = a0_err;
       a0_err = cudaSuccess;
@@ -578,7 +626,11 @@ struct Factorizer {
     }
   }
   ~Factorizer() {
-    if (a0_thread.joinable()) a0_thread.join();
+    // jobs capture this factorizer: none may outlive it (also on error paths)
+    try {
+      helper.drain();
+    } catch (...) {
+    }
   }
   LevelRec prof;  // setup / finish phase timings
   MetaPack meta;  // solve metadata, uploaded once at the end
@@ -606,7 +658,7 @@ struct Factorizer {
   std::vector<uint8_t> active;
   uint8_t* d_active = nullptr;
   // idx arena host mirror
-  std::vector<int32_t> h_idx;
+  PodVec<int32_t> h_idx;  // host mirror of the index arena (grows without zero-filling)
   // block table
   std::vector<int64_t> blk_dof_off;
   std::vector<int32_t> blk_n;
@@ -624,7 +676,6 @@ struct Factorizer {
   DBuf<int32_t> kout;
   DBuf<int32_t> iscratch;
   // stamps (serial paths)
-  std::vector<int64_t> dstamp;
   int64_t stamp = 0;
   // block-foreign cache for adaptive partitioning
   std::vector<int64_t> bf_key;
@@ -1133,7 +1184,7 @@ struct Factorizer {
   std::vector<std::pair<size_t, Reduction>> reductions;
   std::vector<int32_t> red_slot;  // per DOF: target index during a build, else -1
 
-  Helper helper;
+  Helper& helper = helper_thread();
 
   // Copies the level's neighbour lists now (h_idx keeps growing) and builds
   // the reduction on the helper thread.
@@ -1932,6 +1983,7 @@ struct Factorizer {
       }
       if (L.kind == 0) build_reduction((size_t)li, L);
     }
+    helper.drain();
     finish_reductions();
     for (auto& L : F->levels) build_solve_plan(L);
     F->meta = meta.commit(s, [&](void* d, const void* h, size_t n) {
@@ -1975,9 +2027,9 @@ struct Factorizer {
       // the first kernel launch, a0_ready())
       int dev = 0;
       HCK(cudaGetDevice(&dev));
-      a0_thread = std::thread([=]() {
-        cudaSetDevice(dev);
-        cudaError_t e = cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+      a0_job = helper.post([=]() {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) e = cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s);
         a0_err = e;
@@ -1989,7 +2041,6 @@ struct Factorizer {
     HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
     act.resize((size_t)N);
     for (int64_t i = 0; i < N; ++i) act[(size_t)i] = (int32_t)i;
-    dstamp.assign((size_t)N, 0);
     {
       const char* env = getenv("HIFDE_HOST_THREADS");
       nthreads = env ? std::max(1, atoi(env)) : std::min(15, std::max(1, omp_get_max_threads() - 1));
@@ -2028,7 +2079,6 @@ struct Factorizer {
     P.lap("reserve");
     const int Lv = g.nlevels;
     F->levels.reserve((size_t)3 * std::max(Lv, 1) + 4);  // stable LevelRec addresses for the helper
-    helper.start();
     const double t_setup = now_s() - t0;
     HTRACE("setup done");
     std::vector<int32_t> act_tmp;
@@ -2597,7 +2647,10 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
     fz.F_ = F.get();
     fz.s = F->stream;
     const int64_t nnz = opt->input_on_device ? 0 : indptr[n];
+    const char* sample = getenv("HIFDE_SAMPLE");  // host sampling profile (diagnostics)
+    if (sample) host_sampler_start();
     fz.run(indptr, indices, vals, nnz);
+    if (sample) host_sampler_stop(sample);
   } catch (const Fail& f) {
     return fail_to_status(f);
   } catch (const std::exception& e) {
