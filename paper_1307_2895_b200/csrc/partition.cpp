@@ -74,28 +74,32 @@ Groups bucket_keys(const std::vector<int32_t>& act, const std::vector<int32_t>& 
       }
     return bucket(dofs, keys, nkeys);
   }
-  std::vector<int64_t> cnt((size_t)nth * (size_t)nkeys, 0);  // [thread][key]
+  // counts and then write positions, [key][thread] so the prefix walks memory in order
+  std::vector<int64_t> cnt((size_t)nth * (size_t)nkeys);
 #pragma omp parallel num_threads(nth)
   {
     int tid = 0;
 #ifdef _OPENMP
     tid = omp_get_thread_num();
 #endif
+    for (int64_t k = tid; k < nkeys; k += nth)
+      for (int t = 0; t < nth; ++t) cnt[(size_t)k * nth + t] = 0;
+#pragma omp barrier
     const int64_t lo = na * tid / nth, hi = na * (tid + 1) / nth;
-    int64_t* c = cnt.data() + (size_t)tid * (size_t)nkeys;
     for (int64_t i = lo; i < hi; ++i)
-      if (kall[(size_t)i] >= 0) ++c[kall[(size_t)i]];
+      if (kall[(size_t)i] >= 0) ++cnt[(size_t)kall[(size_t)i] * nth + tid];
   }
   Groups out;
   out.offsets.clear();
+  out.offsets.reserve((size_t)nkeys + 1);
   out.offsets.push_back(0);
   int64_t run = 0;
   for (int64_t k = 0; k < nkeys; ++k) {
     const int64_t start = run;
+    int64_t* c = cnt.data() + (size_t)k * nth;
     for (int t = 0; t < nth; ++t) {
-      int64_t& c = cnt[(size_t)t * (size_t)nkeys + (size_t)k];
-      const int64_t v = c;
-      c = run;  // becomes the thread's write position for key k
+      const int64_t v = c[t];
+      c[t] = run;  // becomes the thread's write position for key k
       run += v;
     }
     if (run > start) out.offsets.push_back(run);
@@ -108,10 +112,9 @@ Groups bucket_keys(const std::vector<int32_t>& act, const std::vector<int32_t>& 
     tid = omp_get_thread_num();
 #endif
     const int64_t lo = na * tid / nth, hi = na * (tid + 1) / nth;
-    int64_t* c = cnt.data() + (size_t)tid * (size_t)nkeys;
     for (int64_t i = lo; i < hi; ++i) {
       const int32_t k = kall[(size_t)i];
-      if (k >= 0) out.members[(size_t)c[k]++] = act[(size_t)i];
+      if (k >= 0) out.members[(size_t)cnt[(size_t)k * nth + tid]++] = act[(size_t)i];
     }
   }
   return out;

@@ -107,7 +107,16 @@ struct PinnedStage {
       cudaStreamSynchronize(s);
       n = 0;
     }
-    std::memcpy(p + n, src, bytes);
+    if (bytes >= (1u << 20)) {  // large uploads: several threads fill the pinned slice
+      const int nth = 8;
+#pragma omp parallel for num_threads(nth) schedule(static)
+      for (int t = 0; t < nth; ++t) {
+        const size_t lo = bytes * t / nth, hi = bytes * (t + 1) / nth;
+        std::memcpy(p + n + lo, (const char*)src + lo, hi - lo);
+      }
+    } else {
+      std::memcpy(p + n, src, bytes);
+    }
     cudaMemcpyAsync(dst, p + n, bytes, cudaMemcpyHostToDevice, s);
     n += need;
     return true;
@@ -430,7 +439,7 @@ struct HostCache {
   // arena sizes reached by the last factorization of this grid / variant:
   // reserved up front next time so the arenas do not grow (and copy) mid-run
   int variant = -1;
-  size_t hint_fac = 0, hint_bv = 0, hint_idx = 0, hint_scr = 0;
+  size_t hint_fac = 0, hint_bv = 0, hint_idx = 0, hint_scr = 0, hint_meta = 0;
 };
 HostCache& host_cache() {
   static HostCache hc;
@@ -634,6 +643,7 @@ struct Factorizer {
   }
   LevelRec prof;  // setup / finish phase timings
   MetaPack meta;  // solve metadata, uploaded once at the end
+  size_t meta_bytes = 0;
   GridDesc g;
   hifde_options_t opt;
   hifde_factor_t* F;
@@ -1601,6 +1611,8 @@ struct Factorizer {
     tp = now_s();
     std::vector<int32_t> newid((size_t)nt, -1);
     size_t nadd = 0;
+    L.xrec.reserve((size_t)nt);
+    L.recs.reserve((size_t)nt);
     for (int64_t t = 0; t < nt; ++t) {
       const SkelTask& T = tasks[(size_t)t];
       const int kk = k[(size_t)t], r = T.nc - kk;
@@ -2074,6 +2086,7 @@ struct Factorizer {
       bvals.reserve(want(hc.hint_bv, std::max<int64_t>(64 * N, 1 << 16)), s);
       h_idx.reserve(want(hc.hint_idx, std::max<int64_t>(16 * N, 1 << 16)));
       if (hint && hc.hint_scr) scratch.reserve(hc.hint_scr, s);
+      if (hint && hc.hint_meta) meta.h.reserve(hc.hint_meta + hc.hint_meta / 8);
     }
 
     P.lap("reserve");
@@ -2178,6 +2191,7 @@ struct Factorizer {
     P.lap("reductions");
     // solve metadata to the device: small records one CTA each, large ones as
     // tiled product phases (built level by level on the helper thread)
+    meta_bytes = meta.h.size();
     F->meta = meta.commit(s, [&](void* d, const void* h, size_t n) {
       if (!pinned_stage().copy(d, h, n)) HCK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s));
     });
@@ -2200,6 +2214,7 @@ struct Factorizer {
       hc.hint_bv = bvals.n;
       hc.hint_idx = h_idx.size();
       hc.hint_scr = scratch.cap;
+      hc.hint_meta = meta_bytes;
     }
     bvals.release(s);
     scratch.release(s);
