@@ -88,12 +88,13 @@ struct PinnedStage {
   char* p = nullptr;
   size_t cap = 0, n = 0, peak = 0;
   cudaStream_t s = nullptr;
+  static constexpr size_t kMaxCap = (size_t)256 << 20;  // larger factorizations wrap (drain) instead
   void begin(cudaStream_t st) {
     s = st;
     n = 0;
-    if (peak > cap) {
+    if (peak > cap && cap < kMaxCap) {
       if (p) cudaFreeHost(p);
-      cap = peak + peak / 4;
+      cap = std::min(peak + peak / 4, kMaxCap);
       p = nullptr;
       if (cudaHostAlloc((void**)&p, cap, cudaHostAllocDefault) != cudaSuccess) { p = nullptr; cap = 0; }
     }
@@ -367,9 +368,14 @@ struct Membership {
   }
   // empty every list (storage kept)
   void reset() {
-    std::fill(cnt.begin(), cnt.end(), 0);
-    std::fill(over_slot.begin(), over_slot.end(), -1);
-    for (size_t i = 0; i < over.size(); ++i) over[i].clear();
+    const int64_t n = (int64_t)cnt.size();
+#pragma omp parallel for schedule(static) if (n > (1 << 18))
+    for (int64_t i = 0; i < n; ++i) {
+      cnt[(size_t)i] = 0;
+      over_slot[(size_t)i] = -1;
+    }
+    const int32_t used = std::min<int32_t>(nover.load(), (int32_t)over.size());
+    for (int32_t i = 0; i < used; ++i) over[(size_t)i].clear();
     nover = 0;
   }
   // serial phases only: keep room for the overflow slots a parallel phase may take
@@ -1266,6 +1272,7 @@ struct Factorizer {
     static thread_local std::vector<int32_t> group_of_tls;
     std::vector<int32_t>& group_of = group_of_tls;  // this thread's; shared with the OpenMP workers
     if ((int64_t)group_of.size() < N) group_of.assign((size_t)N, -1);
+#pragma omp parallel for schedule(static) if (nt > 4096)
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = (int32_t)t;
     int nbatch = 1;
@@ -1401,6 +1408,7 @@ struct Factorizer {
       const int32_t* pp = tpred[(size_t)(z.pred_off % nthreads)].data() + z.pred_off / nthreads;
       std::copy(pp, pp + z.npred, preds.data() + pred_ptr[(size_t)t]);
     }
+#pragma omp parallel for schedule(static) if (nt > 4096)
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = -1;
     bool exact = opt.order_mode == HIFDE_ORDER_EXACT ||
@@ -2039,20 +2047,35 @@ struct Factorizer {
       // the first kernel launch, a0_ready())
       int dev = 0;
       HCK(cudaGetDevice(&dev));
+      const bool big = (size_t)nnz * 12 > (size_t)(48u << 20);  // large inputs: pinned staging
       a0_job = helper.post([=]() {
         cudaError_t e = cudaSetDevice(dev);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && big) {
+          try {
+            pinned_xfer().h2d(d_indptr, ip, (N + 1) * sizeof(int64_t), s);
+            pinned_xfer().h2d(d_indices, ix, nnz * sizeof(int32_t), s);
+            pinned_xfer().h2d(d_a0, va, nnz * sizeof(double), s);
+          } catch (const Fail&) {
+            e = cudaErrorUnknown;
+          }
+        } else {
+          if (e == cudaSuccess) e = cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) e = cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s);
+        }
         a0_err = e;
       });
     }
     P.lap("A0");
-    active.assign((size_t)N, 1);
+    active.resize((size_t)N);
+    act.resize((size_t)N);
+#pragma omp parallel for schedule(static) if (N > (1 << 18))
+    for (int64_t i = 0; i < N; ++i) {
+      active[(size_t)i] = 1;
+      act[(size_t)i] = (int32_t)i;
+    }
     HCK(cudaMallocAsync((void**)&d_active, std::max<int64_t>(N, 1), s));
     HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
-    act.resize((size_t)N);
-    for (int64_t i = 0; i < N; ++i) act[(size_t)i] = (int32_t)i;
     {
       const char* env = getenv("HIFDE_HOST_THREADS");
       nthreads = env ? std::max(1, atoi(env)) : std::min(15, std::max(1, omp_get_max_threads() - 1));
