@@ -1272,7 +1272,7 @@ struct Factorizer {
     static thread_local std::vector<int32_t> group_of_tls;
     std::vector<int32_t>& group_of = group_of_tls;  // this thread's; shared with the OpenMP workers
     if ((int64_t)group_of.size() < N) group_of.assign((size_t)N, -1);
-#pragma omp parallel for schedule(static) if (nt > 4096)
+#pragma omp parallel for schedule(static) if (nt > 32768)
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = (int32_t)t;
     int nbatch = 1;
@@ -1408,7 +1408,7 @@ struct Factorizer {
       const int32_t* pp = tpred[(size_t)(z.pred_off % nthreads)].data() + z.pred_off / nthreads;
       std::copy(pp, pp + z.npred, preds.data() + pred_ptr[(size_t)t]);
     }
-#pragma omp parallel for schedule(static) if (nt > 4096)
+#pragma omp parallel for schedule(static) if (nt > 32768)
     for (int64_t t = 0; t < nt; ++t)
       for (int i = 0; i < gr.count(t); ++i) group_of[(size_t)gr.begin(t)[i]] = -1;
     bool exact = opt.order_mode == HIFDE_ORDER_EXACT ||
