@@ -339,6 +339,112 @@ struct NoPublish {
   __device__ void operator()(int, const int32_t*, const int32_t*, int) const {}
 };
 
+// After the pivoted QR of a group: T = R11^-1 R12 from the R rows of Mq
+// (columns in place, LAPACK order perm), ascending sk/rd lists, the
+// congruence B_sr / B_rr from A_cc, the inner Cholesky, W, the delta block
+// and the record (T | packed C^-1 | W).  Z is the post-CPQR workspace
+// (3 q4 + 2 nc^2 doubles); red holds NT/32 partials.
+template <int NT>
+__device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, double* Mq, int ldm,
+                          const int32_t* perm, int32_t* skl, int32_t* rdl, int32_t* sko, int32_t* rdo,
+                          const int32_t* sdofs, const double* Acc, double* Z, double* red) {
+  const int r = nc - k;
+  const size_t q4 = (size_t)nc * nc / 4 + nc;
+  double* Ts = Z;                                      // k x r
+  double* Bsr = Ts + q4;                               // k x r
+  double* Wm = Bsr + q4;                               // r x k
+  double* Brr = Wm + q4;                               // r x r
+  // T = R11^-1 R12 (back substitution, one thread per column of R12)
+  for (int j = threadIdx.x; j < r; j += NT) {
+    double* col = Mq + (size_t)perm[k + j] * ldm;
+    for (int i = k - 1; i >= 0; --i) {
+      double s = col[i];
+      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)perm[l] * ldm] * col[l];
+      col[i] = s / Mq[i + (size_t)perm[i] * ldm];
+    }
+  }
+  // ascending sk / rd with their pivot positions
+  for (int a = threadIdx.x; a < nc; a += NT) {
+    const int pv = perm[a];
+    int rank = 0;
+    if (a < k) {
+      for (int b = 0; b < k; ++b) rank += perm[b] < pv;
+      skl[rank] = pv;
+      sko[rank] = a;
+    } else {
+      for (int b = k; b < nc; ++b) rank += perm[b] < pv;
+      rdl[rank] = pv;
+      rdo[rank] = a - k;
+    }
+  }
+  __syncthreads();
+  int32_t* out = A.idx + t.out_off;
+  for (int a = threadIdx.x; a < k; a += NT) out[a] = sdofs[skl[a]];
+  for (int a = threadIdx.x; a < r; a += NT) out[k + a] = sdofs[rdl[a]];
+  if (threadIdx.x == 0) A.kout[t.group] = k;
+  if (r == 0) {
+    if (threadIdx.x == 0) A.status[t.group] = 0;
+    return;
+  }
+  for (int e = threadIdx.x; e < k * r; e += NT) {
+    const int a = e / r, b = e - a * r;
+    Ts[e] = Mq[sko[a] + (size_t)perm[k + rdo[b]] * ldm];
+  }
+  __syncthreads();
+  // B_sr = A_sr - A_ss T
+  for (int e = threadIdx.x; e < k * r; e += NT) {
+    const int a = e / r, b = e - a * r;
+    const double* arow = Acc + skl[a] * nc;
+    double s = arow[rdl[b]];
+    for (int l = 0; l < k; ++l) s -= arow[skl[l]] * Ts[l * r + b];
+    Bsr[e] = s;
+  }
+  __syncthreads();
+  // B_rr = A_rr - A_sr^T T - T^T B_sr  (then symmetrized)
+  for (int e = threadIdx.x; e < r * r; e += NT) {
+    const int a = e / r, b = e - a * r;
+    double s = Acc[rdl[a] * nc + rdl[b]];
+    for (int l = 0; l < k; ++l)
+      s -= Acc[skl[l] * nc + rdl[a]] * Ts[l * r + b] + Ts[l * r + a] * Bsr[l * r + b];
+    Brr[e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += NT) {
+    const int a = e / r, b = e - a * r;
+    if (a < b) {
+      const double m = 0.5 * (Brr[e] + Brr[b * r + a]);
+      Brr[e] = m;
+      Brr[b * r + a] = m;
+    }
+  }
+  __syncthreads();
+  const int st = chol_1sync<NT>(Brr, r, r, red);
+  if (st != 0) {
+    if (threadIdx.x == 0) A.status[t.group] = st;
+    return;
+  }
+  for (int e = threadIdx.x; e < r * k; e += NT) {
+    const int a = e / k, b = e - a * k;
+    Wm[e] = Bsr[b * r + a];
+  }
+  if (k > 0) trsm_1sync<NT>(Brr, r, r, Wm, k, k);
+  __syncthreads();
+  double* dl = A.bvals + t.delta_off;
+  for (int e = threadIdx.x; e < k * k; e += NT) {
+    const int a = e / k, b = e - a * k;
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s -= Wm[l * k + a] * Wm[l * k + b];
+    dl[e] = s;
+  }
+  double* rec = A.fac + t.rec_off;
+  for (int e = threadIdx.x; e < k * r; e += NT) rec[e] = Ts[e];
+  double* C = rec + (size_t)k * r;
+  tri_inverse_packed_ws<NT>(Brr, r, r, Brr + (size_t)nc * nc, C);  // packed C^-1 for the solve
+  double* Wo = C + (size_t)r * r;
+  for (int e = threadIdx.x; e < r * k; e += NT) Wo[e] = Wm[e];
+  if (threadIdx.x == 0) A.status[t.group] = 0;
+}
+
 // One skeletonization group.  The front is assembled assuming every neighbour
 // row is alive, then `wait()` runs (exact order: until the earlier
 // neighbouring groups are done), then rows of DOFs retired meanwhile are
@@ -400,11 +506,6 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     vn2 = vn1 + nc;
     Z = vn2 + nc;                                      // post-CPQR workspace
   }
-  const size_t q4 = (size_t)nc * nc / 4 + nc;
-  double* Ts = Z;                                      // k x r
-  double* Bsr = Ts + q4;                               // k x r
-  double* Wm = Bsr + q4;                               // r x k
-  double* Brr = Wm + q4;                               // r x r
 
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += NT) {
@@ -695,100 +796,11 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   for (int i = threadIdx.x; i < k; i += NT) Mc[i + (size_t)perm[i] * ldm] = rdiag[i];
   Mq = Mc;
   __syncthreads();
-  const int r = nc - k;
   // the redundant set is known: later groups may start (exact order) while
   // this one finishes its interpolation and elimination off the chain
   publish(k, perm, sdofs, nc);
 
-  // T = R11^-1 R12 (back substitution, one thread per column of R12)
-  for (int j = threadIdx.x; j < r; j += NT) {
-    double* col = Mq + (size_t)perm[k + j] * ldm;
-    for (int i = k - 1; i >= 0; --i) {
-      double s = col[i];
-      for (int l = i + 1; l < k; ++l) s -= Mq[i + (size_t)perm[l] * ldm] * col[l];
-      col[i] = s / Mq[i + (size_t)perm[i] * ldm];
-    }
-  }
-  // ascending sk / rd with their pivot positions
-  for (int a = threadIdx.x; a < nc; a += NT) {
-    const int pv = perm[a];
-    int rank = 0;
-    if (a < k) {
-      for (int b = 0; b < k; ++b) rank += perm[b] < pv;
-      skl[rank] = pv;
-      sko[rank] = a;
-    } else {
-      for (int b = k; b < nc; ++b) rank += perm[b] < pv;
-      rdl[rank] = pv;
-      rdo[rank] = a - k;
-    }
-  }
-  __syncthreads();
-  int32_t* out = A.idx + t.out_off;
-  for (int a = threadIdx.x; a < k; a += NT) out[a] = sdofs[skl[a]];
-  for (int a = threadIdx.x; a < r; a += NT) out[k + a] = sdofs[rdl[a]];
-  if (threadIdx.x == 0) A.kout[t.group] = k;
-  if (r == 0) {
-    if (threadIdx.x == 0) A.status[t.group] = 0;
-    return;
-  }
-  for (int e = threadIdx.x; e < k * r; e += NT) {
-    const int a = e / r, b = e - a * r;
-    Ts[e] = Mq[sko[a] + (size_t)perm[k + rdo[b]] * ldm];
-  }
-  __syncthreads();
-  // B_sr = A_sr - A_ss T
-  for (int e = threadIdx.x; e < k * r; e += NT) {
-    const int a = e / r, b = e - a * r;
-    const double* arow = Acc + skl[a] * nc;
-    double s = arow[rdl[b]];
-    for (int l = 0; l < k; ++l) s -= arow[skl[l]] * Ts[l * r + b];
-    Bsr[e] = s;
-  }
-  __syncthreads();
-  // B_rr = A_rr - A_sr^T T - T^T B_sr  (then symmetrized)
-  for (int e = threadIdx.x; e < r * r; e += NT) {
-    const int a = e / r, b = e - a * r;
-    double s = Acc[rdl[a] * nc + rdl[b]];
-    for (int l = 0; l < k; ++l)
-      s -= Acc[skl[l] * nc + rdl[a]] * Ts[l * r + b] + Ts[l * r + a] * Bsr[l * r + b];
-    Brr[e] = s;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < r * r; e += NT) {
-    const int a = e / r, b = e - a * r;
-    if (a < b) {
-      const double m = 0.5 * (Brr[e] + Brr[b * r + a]);
-      Brr[e] = m;
-      Brr[b * r + a] = m;
-    }
-  }
-  __syncthreads();
-  const int st = chol_1sync<NT>(Brr, r, r, red);
-  if (st != 0) {
-    if (threadIdx.x == 0) A.status[t.group] = st;
-    return;
-  }
-  for (int e = threadIdx.x; e < r * k; e += NT) {
-    const int a = e / k, b = e - a * k;
-    Wm[e] = Bsr[b * r + a];
-  }
-  if (k > 0) trsm_1sync<NT>(Brr, r, r, Wm, k, k);
-  __syncthreads();
-  double* dl = A.bvals + t.delta_off;
-  for (int e = threadIdx.x; e < k * k; e += NT) {
-    const int a = e / k, b = e - a * k;
-    double s = 0.0;
-    for (int l = 0; l < r; ++l) s -= Wm[l * k + a] * Wm[l * k + b];
-    dl[e] = s;
-  }
-  double* rec = A.fac + t.rec_off;
-  for (int e = threadIdx.x; e < k * r; e += NT) rec[e] = Ts[e];
-  double* C = rec + (size_t)k * r;
-  tri_inverse_packed_ws<NT>(Brr, r, r, Brr + (size_t)nc * nc, C);  // packed C^-1 for the solve
-  double* Wo = C + (size_t)r * r;
-  for (int e = threadIdx.x; e < r * k; e += NT) Wo[e] = Wm[e];
-  if (threadIdx.x == 0) A.status[t.group] = 0;
+  skel_tail<NT>(t, A, nc, k, Mq, ldm, perm, skl, rdl, sko, rdo, sdofs, Acc, Z, red);
 }
 
 template <int NT>
