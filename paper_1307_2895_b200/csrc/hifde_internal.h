@@ -132,6 +132,12 @@ void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double ep
                  cudaStream_t s);
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s);
 int skel_ordered_capacity(size_t smem, int nt);
+constexpr int kClusterThreads = 256;           // threads per CTA of the cluster skeleton kernel
+constexpr int kClusterMinNc = 24;              // levels whose widest group reaches this may use it
+int skel_cluster_capacity(size_t smem, int cs);  // resident clusters of cs CTAs
+cudaError_t launch_skel_cluster(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
+                                int* done, const Arenas& A, double eps, size_t smem, int nclusters, int cs,
+                                cudaStream_t s);
 cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
                                 int* done, const Arenas& A, double eps, size_t smem, int nt, int grid,
                                 cudaStream_t s);

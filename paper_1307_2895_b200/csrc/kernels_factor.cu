@@ -18,6 +18,7 @@
 //   CPQR / ID     src/dense.py:239-264
 #include <cfloat>
 #include <cstdint>
+#include <cooperative_groups.h>
 #include <cuda/atomic>
 
 #include "hifde_internal.h"
@@ -862,6 +863,334 @@ __global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact order with a CTA cluster per group (the large 2D groups): the
+// neighbour block's columns are dealt round-robin to the kClusterSkel CTAs
+// (each keeps its slice in its own shared memory, so the per-step update is
+// split kClusterSkel ways); per pivot step the CTAs exchange one candidate
+// each and copy the pivot column from its owner over DSMEM -- one cluster
+// barrier per step.  Rank 0 waits for the predecessors, publishes the
+// redundant set, gathers the R rows and runs the tail (skel_tail).
+// Shared layout per CTA: ints as skel_group | vn1 x2 | xn x2 | R_ii | vn2 |
+// v (nq) | own slice (ldq x ceil(nc / kClusterSkel)).  Global scratch per
+// group (t.scratch_off): A_cc (nc^2) | R rows (nc^2) | tail workspace.
+// ---------------------------------------------------------------------------
+template <int NT, int CS>
+__global__ void __launch_bounds__(NT) skel_cluster_kernel(const SkelTask* __restrict__ tasks, int ntasks,
+                                                          const int64_t* __restrict__ pred_ptr,
+                                                          const int32_t* __restrict__ pred,
+                                                          int* __restrict__ done, Arenas A, double eps) {
+  namespace cg = cooperative_groups;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[NW];
+  __shared__ double cand[2][3];
+  __shared__ double sh_x;
+  __shared__ int sh_k;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int ncls = gridDim.x / CS, cid = blockIdx.x / CS;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int j = cid; j < ntasks; j += ncls) {
+    const SkelTask t = tasks[j];
+    const int nc = t.nc, nq = t.nq, nf = nc + nq;
+    int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
+    int32_t* salive = sdofs + nf;
+    int32_t* smap = salive + nf;
+    int32_t* perm = smap + t.maxnb;
+    int32_t* skl = perm + nc;
+    int32_t* rdl = skl + nc;
+    int32_t* sko = rdl + nc;
+    int32_t* rdo = sko + nc;
+    int32_t* dcol = rdo + nc;
+    int32_t* cpos = dcol + nc;
+    const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(2 * nf + t.maxnb + 8 * nc), 16);
+    double* cq = reinterpret_cast<double*>(smem + ibytes);
+    double* rdiag = cq + 4 * nc;
+    double* vn2 = cq + 5 * nc;
+    double* vbuf = vn2 + nc;
+    double* Ms = vbuf + nq;                         // own column slice, ld ldq
+    const int ldq = skel_ldq(nq);
+    const int ncl = (nc - rank + CS - 1) / CS;      // owned columns rank, rank + CS, ...
+    double* Acc = A.scratch + t.scratch_off;
+    double* Rf = Acc + (size_t)nc * nc;
+    double* Z = Rf + (size_t)nc * nc;
+    const int32_t* gd = A.idx + t.dofs_off;
+    for (int i = threadIdx.x; i < nf; i += NT) {
+      sdofs[i] = gd[i];
+      salive[i] = 1;
+    }
+    for (size_t e = threadIdx.x; e < (size_t)ldq * ncl; e += NT) Ms[e] = 0.0;
+    if (rank == 0)
+      for (int e = threadIdx.x; e < nc * nc; e += NT) Acc[e] = 0.0;
+    __syncthreads();
+    // assembly of the own slice (and of A_cc by rank 0), same order as skel_group
+    for (int p = threadIdx.x; p < nc; p += NT) {
+      const bool mine = p % CS == rank;
+      if (!mine && rank != 0) continue;
+      const int g = sdofs[p];
+      for (int64_t kk = A.indptr[g]; kk < A.indptr[g + 1]; ++kk) {
+        const int pj = front_pos(sdofs, nc, nq, A.indices[kk]);
+        if (pj < 0) continue;
+        const double v = A.a0[kk];
+        if (pj < nc) {
+          if (rank == 0) Acc[p * nc + pj] += v;
+        } else if (mine) {
+          Ms[(pj - nc) + (size_t)(p / CS) * ldq] += v;
+        }
+      }
+    }
+    __syncthreads();
+    const int32_t* bl = A.lists + t.blk_off;
+    for (int b = 0; b < t.nblk; ++b) {
+      const int bid = bl[b];
+      const int nb = A.blk_n[bid];
+      const int32_t* bd = A.idx + A.blk_dof_off[bid];
+      const double* bv = A.bvals + A.blk_val_off[bid];
+      for (int kk = threadIdx.x; kk < nb; kk += NT) smap[kk] = front_pos(sdofs, nc, nq, bd[kk]);
+      __syncthreads();
+      for (int kk = wid; kk < nb; kk += NW) {
+        const int pk = smap[kk];
+        if (pk < 0) continue;
+        for (int l = lane; l < nb; l += 32) {
+          const int pl = smap[l];
+          if (pl < 0 || pl >= nc) continue;
+          if (pk < nc) {
+            if (rank == 0) Acc[pk * nc + pl] += bv[(size_t)kk * nb + l];
+          } else if (pl % CS == rank) {
+            Ms[(pk - nc) + (size_t)(pl / CS) * ldq] += bv[(size_t)kk * nb + l];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // exact order: rank 0 waits for the earlier neighbouring groups
+    if (rank == 0) {
+      bool polled = false;
+      for (int64_t q = pred_ptr[j] + threadIdx.x; q < pred_ptr[j + 1]; q += NT) {
+        cuda::atomic_ref<int, cuda::thread_scope_device> f(done[pred[q]]);
+        while (f.load(cuda::memory_order_relaxed) == 0) __nanosleep(32);
+        polled = true;
+      }
+      if (polled) cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+    }
+    cl.sync();
+    if (threadIdx.x == 0) cuda::atomic_thread_fence(cuda::memory_order_acquire, cuda::thread_scope_device);
+    __syncthreads();
+    for (int i = nc + threadIdx.x; i < nf; i += NT) {
+      if (!__ldcg(A.active + sdofs[i])) {
+        salive[i] = 0;
+        for (int jl = 0; jl < ncl; ++jl) Ms[(size_t)(i - nc) + (size_t)jl * ldq] = 0.0;
+      }
+    }
+    __syncthreads();
+    // CPQR over the slices
+    if (threadIdx.x == 0) {
+      int na = 0;
+      for (int i = nc; i < nf; ++i) na += salive[i];
+      sh_k = na;
+    }
+    for (int jl = wid; jl < ncl; jl += NW) {
+      const double* col = Ms + (size_t)jl * ldq;
+      double s1 = 0.0;
+      for (int r = 1 + lane; r < nq; r += 32) s1 += col[r] * col[r];
+      s1 = warp_sum(s1);
+      const double c0 = nq > 0 ? col[0] : 0.0;
+      if (lane == 0) {
+        const int jj = rank + CS * jl;
+        const double nv = sqrt(c0 * c0 + s1);
+        cq[jj] = nv;
+        vn2[jj] = nv;
+        cq[2 * nc + jj] = sqrt(s1);
+      }
+    }
+    for (int jj = threadIdx.x; jj < nc; jj += NT) {
+      dcol[jj] = 0;
+      cpos[jj] = jj;
+    }
+    __syncthreads();
+    const int nq_alive = sh_k;
+    const int kmax = nq < nc ? nq : nc;
+    const double tol3z = sqrt(DBL_EPSILON * 0.5);
+    int Gl = 32;
+    while (Gl > 8 && NT / Gl < ncl) Gl >>= 1;
+    const int nslots = NT / Gl, sl = lane & (Gl - 1), slot = wid * (32 / Gl) + lane / Gl;
+    double thr = 0.0;
+    int k = kmax;
+    for (int i = 0; i < kmax; ++i) {
+      const int cur = (i & 1) * nc, nxt = nc - cur;
+      const double* vn1 = cq + cur;
+      double* vn1o = cq + nxt;
+      const double* xn = cq + 2 * nc + cur;
+      double* xno = cq + 2 * nc + nxt;
+      const int32_t* cat = cpos + cur;
+      int32_t* cato = cpos + nxt;
+      if (wid == 0) {  // this CTA's best candidate (largest norm, lowest LAPACK position)
+        double bv = -1.0;
+        int bp = nc, bc = 0;
+        for (int pos = i + lane; pos < nc; pos += 32) {
+          const int c = cat[pos];
+          if (c % CS != rank) continue;
+          const double v = vn1[c];
+          if (v > bv) { bv = v; bp = pos; bc = c; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          if (ov > bv || (ov == bv && op < bp)) { bv = ov; bp = op; bc = oc; }
+        }
+        if (lane == 0) {
+          cand[i & 1][0] = bv;
+          cand[i & 1][1] = bp;
+          cand[i & 1][2] = bc;
+        }
+      }
+      cl.sync();  // every candidate (and every owner's updated slice) visible
+      double gbv = -1.0;
+      int gbp = nc, p = 0;
+      for (int q = 0; q < CS; ++q) {
+        const double* cr = cl.map_shared_rank(&cand[i & 1][0], q);
+        const double v = cr[0];
+        const int pp = (int)cr[1];
+        if (v > gbv || (v == gbv && pp < gbp)) { gbv = v; gbp = pp; p = (int)cr[2]; }
+      }
+      if (wid == NW - 1) {
+        const int ci = cat[i];
+        for (int pos = lane; pos < nc; pos += 32) cato[pos] = pos == i ? p : (pos == gbp ? ci : cat[pos]);
+      }
+      if (i == 0 && gbv == 0.0) { k = 0; break; }
+      // the pivot column (rows >= i) and its Householder norm, from the owner
+      const int owner = p % CS;
+      const double* Mo = cl.map_shared_rank(Ms, owner) + (size_t)(p / CS) * ldq;
+      for (int r = i + threadIdx.x; r < nq; r += NT) vbuf[r] = Mo[r];
+      if (threadIdx.x == 0) sh_x = cl.map_shared_rank(cq + 2 * nc + cur, owner)[p];
+      __syncthreads();
+      const double alpha = vbuf[i], xnorm = sh_x;
+      double beta, tau, scal;
+      if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
+      else {
+        beta = -copysign(hypot(alpha, xnorm), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      const double rii = fabs(beta);
+      if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
+      if (rii <= thr) { k = i; break; }
+      if (threadIdx.x == 0) { rdiag[i] = beta; dcol[p] = 1; }
+      const double* v = vbuf;
+      for (int base = 0; base < ncl; base += nslots) {
+        const int jl = base + slot;
+        const int jj = rank + CS * jl;
+        const bool act = jl < ncl && jj != p && !dcol[jj];
+        double* col = Ms + (size_t)(act ? jl : 0) * ldq;
+        double acc = 0.0;
+        if (tau != 0.0) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int r = i + 1 + sl;
+          for (; r + 3 * Gl < nq; r += 4 * Gl) {
+            s0 += v[r] * col[r];
+            s1 += v[r + Gl] * col[r + Gl];
+            s2 += v[r + 2 * Gl] * col[r + 2 * Gl];
+            s3 += v[r + 3 * Gl] * col[r + 3 * Gl];
+          }
+          for (; r < nq; r += Gl) s0 += v[r] * col[r];
+          const double sd = group_sum((s0 + s1) + (s2 + s3), Gl);
+          const double w = tau * (col[i] + scal * sd);
+          __syncwarp();
+          if (act && sl == 0) col[i] -= w;
+          const double ws2 = w * scal;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          r = i + 1 + sl;
+          if (r == i + 1 && r < nq) {
+            const double x = col[r] - ws2 * v[r];
+            if (act) col[r] = x;
+            r += Gl;
+          }
+          for (; r + 3 * Gl < nq; r += 4 * Gl) {
+            const double x0 = col[r] - ws2 * v[r];
+            const double x1 = col[r + Gl] - ws2 * v[r + Gl];
+            const double x2 = col[r + 2 * Gl] - ws2 * v[r + 2 * Gl];
+            const double x3 = col[r + 3 * Gl] - ws2 * v[r + 3 * Gl];
+            if (act) {
+              col[r] = x0;
+              col[r + Gl] = x1;
+              col[r + 2 * Gl] = x2;
+              col[r + 3 * Gl] = x3;
+            }
+            a0 += x0 * x0;
+            a1 += x1 * x1;
+            a2 += x2 * x2;
+            a3 += x3 * x3;
+          }
+          for (; r < nq; r += Gl) {
+            const double x = col[r] - ws2 * v[r];
+            if (act) col[r] = x;
+            a0 += x * x;
+          }
+          acc = (a0 + a1) + (a2 + a3);
+        } else {
+          double a0 = 0.0, a1 = 0.0;
+          int r = i + 2 + sl;
+          for (; r + Gl < nq; r += 2 * Gl) {
+            a0 += col[r] * col[r];
+            a1 += col[r + Gl] * col[r + Gl];
+          }
+          for (; r < nq; r += Gl) a0 += col[r] * col[r];
+          acc = a0 + a1;
+        }
+        acc = group_sum(acc, Gl);
+        __syncwarp();
+        if (act) {
+          const double cn = i + 1 < nq ? col[i + 1] : 0.0;
+          double nv = vn1[jj];
+          if (nv != 0.0) {
+            double tmp = fabs(col[i]) / nv;
+            tmp = 1.0 - tmp * tmp;
+            tmp = tmp > 0.0 ? tmp : 0.0;
+            const double ratio = nv / vn2[jj];
+            if (tmp * ratio * ratio <= tol3z) {
+              nv = (i + 1 < nq) ? sqrt(cn * cn + acc) : 0.0;
+              if (sl == 0) vn2[jj] = nv;
+            } else {
+              nv *= sqrt(tmp);
+            }
+          }
+          if (sl == 0) { vn1o[jj] = nv; xno[jj] = sqrt(acc); }
+        }
+      }
+      __syncthreads();
+    }
+    {
+      const int32_t* cat = cpos + (k & 1) * nc;
+      for (int pos = threadIdx.x; pos < nc; pos += NT) perm[pos] = cat[pos];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += NT) {
+      const int pc = perm[i];
+      if (pc % CS == rank) Ms[i + (size_t)(pc / CS) * ldq] = rdiag[i];
+    }
+    if (rank == 0) {  // publish: later groups may start
+      for (int a = k + threadIdx.x; a < nc; a += NT) A.active[sdofs[perm[a]]] = 0;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        cuda::atomic_ref<int, cuda::thread_scope_device> f(done[j]);
+        f.store(1, cuda::memory_order_release);
+      }
+    }
+    cl.sync();  // R rows complete in every slice
+    if (rank == 0)
+      for (int e = threadIdx.x; e < k * nc; e += NT) {
+        const int jc = e / k, i = e - jc * k;
+        Rf[i + (size_t)jc * nc] = cl.map_shared_rank(Ms, jc % CS)[i + (size_t)(jc / CS) * ldq];
+      }
+    cl.sync();  // the slices may be reused
+    if (rank == 0) skel_tail<NT>(t, A, nc, k, Rf, nc, perm, skl, rdl, sko, rdo, sdofs, Acc, Z, red);
+    __syncthreads();
+  }
+}
+
 // Retire the redundant DOFs of a finished batch (device active mask).
 __global__ void apply_rd_kernel(const SkelTask* __restrict__ tasks, Arenas A) {
   const SkelTask t = tasks[blockIdx.x];
@@ -934,6 +1263,70 @@ cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64
                                        smem, s);
   return cudaLaunchCooperativeKernel((const void*)skel_ordered_kernel<512>, dim3((unsigned)grid), dim3(512), args,
                                      smem, s);
+}
+
+template <int CS>
+static int cluster_capacity(size_t smem) {
+  auto kern = skel_cluster_kernel<kClusterThreads, CS>;
+  allow_smem(kern);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(CS * 148);
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int skel_cluster_capacity(size_t smem, int cs) {
+  return cs == 4 ? cluster_capacity<4>(smem) : cluster_capacity<2>(smem);
+}
+
+template <int CS>
+static cudaError_t cluster_launch(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
+                                  int* done, const Arenas& A, double eps, size_t smem, int nclusters,
+                                  cudaStream_t s) {
+  auto kern = skel_cluster_kernel<kClusterThreads, CS>;
+  allow_smem(kern);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;  // every cluster resident: the waits spin
+  at[1].val.cooperative = 1;
+  cfg.gridDim = dim3((unsigned)(CS * nclusters));
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, d_tasks, ntasks, pred_ptr, pred, done, A, eps);
+  if (e != cudaSuccess) {  // cooperative + cluster refused: the grid is sized to be resident anyway
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, d_tasks, ntasks, pred_ptr, pred, done, A, eps);
+  }
+  return e;
+}
+
+cudaError_t launch_skel_cluster(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
+                                int* done, const Arenas& A, double eps, size_t smem, int nclusters, int cs,
+                                cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  return cs == 4 ? cluster_launch<4>(d_tasks, ntasks, pred_ptr, pred, done, A, eps, smem, nclusters, s)
+                 : cluster_launch<2>(d_tasks, ntasks, pred_ptr, pred, done, A, eps, smem, nclusters, s);
 }
 
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s) {

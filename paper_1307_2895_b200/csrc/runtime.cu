@@ -1450,6 +1450,65 @@ struct Factorizer {
       kout.bump((size_t)nt, s);
       Arenas A = arenas();
       A.status = status.p + st_off;
+      // large groups: a CTA cluster per group (skel_cluster_kernel), 4 or 2 CTAs
+      // each, when every group's column slice fits and every group gets a
+      // resident cluster of its own (more groups than clusters: the one-CTA
+      // kernel's throughput wins)
+      size_t smem_cl = 0;
+      int cs = 0, ncls = 0;
+      bool cluster_ok = max_nc >= kClusterMinNc && !getenv("HIFDE_NO_CLUSTER");
+      for (int csz : {4, 2}) {
+        if (!cluster_ok) break;
+        size_t need_max = 0;
+        bool fits = true;
+        for (int64_t t = 0; t < nt && fits; ++t) {
+          const SkelTask& T = tasks[(size_t)t];
+          const int nf = T.nc + T.nq;
+          const size_t need = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * T.nc)) +
+                              sizeof(double) * (6 * (size_t)T.nc + (size_t)T.nq +
+                                                (size_t)skel_ldq(T.nq) * ((T.nc + csz - 1) / csz));
+          need_max = std::max(need_max, need);
+          fits = need <= kSmemCap;
+        }
+        if (!fits) continue;
+        const int capc = skel_cluster_capacity(need_max, csz);
+        const char* cf = getenv("HIFDE_CLUSTER_LOAD");  // groups per resident cluster allowed (study)
+        const double load = cf ? atof(cf) : 1.0;
+        if (capc >= 1 && (double)nt <= load * capc) {
+          cs = csz;
+          ncls = (int)std::min<int64_t>(nt, capc);
+          smem_cl = need_max;
+          break;
+        }
+      }
+      cluster_ok = cluster_ok && cs > 0;
+      if (cluster_ok) {
+        std::vector<SkelTask> ct(tasks);  // per-group global workspace of the cluster kernel
+        size_t tot = 0;
+        for (auto& T : ct) {
+          const size_t q4 = (size_t)T.nc * T.nc / 4 + T.nc;
+          T.scratch_off = (int64_t)tot;
+          tot += 4 * (size_t)T.nc * T.nc + 3 * q4 + 8;
+        }
+        const int64_t base = (int64_t)scratch.bump(tot, s);
+        for (auto& T : ct) T.scratch_off += base;
+        A.scratch = scratch.p;
+        dt.upload(ct.data(), 0, ct.size(), s);
+        HCK(cudaEventCreate(&L.ev0));
+        HCK(cudaEventCreate(&L.ev1));
+        HCK(cudaEventRecord(L.ev0, s));
+        HCK(launch_skel_cluster(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem_cl, ncls, cs, s));
+        ++g_launches;
+        HCK(cudaEventRecord(L.ev1, s));
+        L.t_launch = now_s() - tp;
+        tp = now_s();
+        finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
+        dt.release(s);
+        dpp.release(s);
+        dpr.release(s);
+        ddone.release(s);
+        return;
+      }
       const int nthr = (max_nc > 32 || max_nq > 128 || getenv("HIFDE_SKEL512")) ? 512 : 128;
       const int cap = skel_ordered_capacity(smem, nthr);
       if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
