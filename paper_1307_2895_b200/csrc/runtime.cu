@@ -369,7 +369,7 @@ struct Membership {
   // empty every list (storage kept)
   void reset() {
     const int64_t n = (int64_t)cnt.size();
-#pragma omp parallel for schedule(static) if (n > (1 << 18))
+#pragma omp parallel for schedule(static) if (n > (1 << 16))
     for (int64_t i = 0; i < n; ++i) {
       cnt[(size_t)i] = 0;
       over_slot[(size_t)i] = -1;
@@ -2128,7 +2128,7 @@ struct Factorizer {
     P.lap("A0");
     active.resize((size_t)N);
     act.resize((size_t)N);
-#pragma omp parallel for schedule(static) if (N > (1 << 18))
+#pragma omp parallel for schedule(static) if (N > (1 << 16))
     for (int64_t i = 0; i < N; ++i) {
       active[(size_t)i] = 1;
       act[(size_t)i] = (int32_t)i;
