@@ -77,13 +77,14 @@ __global__ void __launch_bounds__(256) big_assemble_kernel(const ElimTask* __res
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += 256) sdofs[i] = gd[i];
   for (int r = r0 + (int)threadIdx.x; r < r1 && r < nc; r += 256) A.active[gd[r]] = 0;
-  // zero the owned rows
-  for (int r = r0; r < r1; ++r) {
+  // zero the owned rows (warp per row)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int r = r0 + wid; r < r1; r += 8) {
     if (r < nc) {
-      for (int j = threadIdx.x; j < nc; j += 256) F[(size_t)r * nc + j] = 0.0;
-      for (int j = threadIdx.x; j < nq; j += 256) W[(size_t)r * nq + j] = 0.0;
+      for (int j = lane; j < nc; j += 32) F[(size_t)r * nc + j] = 0.0;
+      for (int j = lane; j < nq; j += 32) W[(size_t)r * nq + j] = 0.0;
     } else {
-      for (int j = threadIdx.x; j < nq; j += 256) U[(size_t)(r - nc) * nq + j] = 0.0;
+      for (int j = lane; j < nq; j += 32) U[(size_t)(r - nc) * nq + j] = 0.0;
     }
   }
   __syncthreads();
@@ -112,11 +113,11 @@ __global__ void __launch_bounds__(256) big_assemble_kernel(const ElimTask* __res
     }
     __syncthreads();
     const int ns = nsel;
-    for (int s = 0; s < ns; ++s) {
+    for (int s = wid; s < ns; s += 8) {  // warp per owned block row
       const int k = ssel[s];
       const int pk = smap[k];
       const double* brow = bv + (size_t)k * nb;
-      for (int l = threadIdx.x; l < nb; l += 256) {
+      for (int l = lane; l < nb; l += 32) {
         const int pl = smap[l];
         if (pl < 0) continue;
         if (pk < nc) {
