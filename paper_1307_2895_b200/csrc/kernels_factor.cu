@@ -1299,26 +1299,20 @@ static cudaError_t cluster_launch(const SkelTask* d_tasks, int ntasks, const int
   auto kern = skel_cluster_kernel<kClusterThreads, CS>;
   allow_smem(kern);
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CS;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeCooperative;  // every cluster resident: the waits spin
-  at[1].val.cooperative = 1;
+  // the waits spin, so every cluster must be resident: the grid never exceeds
+  // cudaOccupancyMaxActiveClusters (skel_cluster_capacity) for this launch
   cfg.gridDim = dim3((unsigned)(CS * nclusters));
   cfg.blockDim = dim3(kClusterThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, d_tasks, ntasks, pred_ptr, pred, done, A, eps);
-  if (e != cudaSuccess) {  // cooperative + cluster refused: the grid is sized to be resident anyway
-    cudaGetLastError();
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, d_tasks, ntasks, pred_ptr, pred, done, A, eps);
-  }
-  return e;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, d_tasks, ntasks, pred_ptr, pred, done, A, eps);
 }
 
 cudaError_t launch_skel_cluster(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
