@@ -20,6 +20,12 @@ namespace {
 
 constexpr int NT = kThreads;
 
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // x (n x nrhs, row-major) <- C^{-1} x, C lower n x n row-major.  One barrier
 // per row: row i's scaling by 1/C_ii is deferred to the next step.
 __device__ void fwd_subst(const double* __restrict__ C, int n, double* x, int nrhs) {
@@ -105,8 +111,60 @@ __device__ __forceinline__ double* workspace(double* smem, double* scratch, int6
 // 2 dense row-major (ld lda), 3 dense transposed.
 constexpr int kGKC = 32, kGRB = 16, kGMI = 6;
 constexpr int kGRows = (NT / kGRB) * kGMI;  // rows per pass (96)
+// One right-hand side: a matrix-vector product read straight from global
+// memory.  Row-major operands (P, dense): a warp per row, lanes along k
+// (coalesced); transposed operands: lanes along 32 consecutive rows, warps
+// split k, partial sums reduced through shared memory (As).
+__device__ void cta_gemv(int M, int K, int amode, const double* __restrict__ A, int64_t lda, const double* x,
+                         double* y, double alpha, bool accumulate, double* As) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();  // x complete
+  if (amode == 0 || amode == 2) {
+    for (int i = wid; i < M; i += NW) {
+      const int kend = amode == 0 ? min(i + 1, K) : K;
+      const double* row = amode == 0 ? A + (size_t)i * (i + 1) / 2 : A + (size_t)i * lda;
+      double s0 = 0.0, s1 = 0.0;
+      int k = lane;
+      for (; k + 32 < kend; k += 64) {
+        s0 += row[k] * x[k];
+        s1 += row[k + 32] * x[k + 32];
+      }
+      if (k < kend) s0 += row[k] * x[k];
+      const double sum = warp_sum(s0 + s1);
+      if (lane == 0) y[i] = (accumulate ? y[i] : 0.0) + alpha * sum;
+    }
+  } else {
+    for (int i0 = 0; i0 < M; i0 += 32) {
+      const int i = i0 + lane;
+      const int kbeg = amode == 1 ? i0 : 0;  // P^T: rows i need k >= i
+      const int span = (K - kbeg + NW - 1) / NW;
+      const int k0 = kbeg + wid * span, k1 = min(K, k0 + span);
+      double s = 0.0;
+      if (i < M)
+        for (int k = k0; k < k1; ++k) {
+          const double a = amode == 1 ? (k >= i ? A[(size_t)k * (k + 1) / 2 + i] : 0.0) : A[(size_t)k * lda + i];
+          s += a * x[k];
+        }
+      As[wid * 32 + lane] = s;
+      __syncthreads();
+      if (wid == 0 && i < M) {
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += As[w * 32 + lane];
+        y[i] = (accumulate ? y[i] : 0.0) + alpha * t;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+}
+
 __device__ void cta_gemm(int M, int K, int amode, const double* __restrict__ A, int64_t lda, const double* X,
                          double* Y, int nrhs, double alpha, bool accumulate, double* As) {
+  if (nrhs == 1) {
+    cta_gemv(M, K, amode, A, lda, X, Y, alpha, accumulate, As);
+    return;
+  }
   constexpr int RG = NT / kGRB;
   const int rr = threadIdx.x % kGRB, rg = threadIdx.x / kGRB;
   for (int m0 = 0; m0 < M; m0 += kGRows) {
@@ -404,6 +462,70 @@ __global__ void __launch_bounds__(256) solve_tile_kernel(const TileOp* __restric
   const TileOp op = ops[w.x];
   const int i0 = w.y, r0 = blockIdx.y * kRW;
   if (r0 >= nrhs) return;
+  if (nrhs == 1) {  // matrix-vector: stream A at full width (the 32-RHS tiling would idle 31/32 lanes)
+    __shared__ double xs[1024];
+    __shared__ double part[8][64];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const double* Am = fac + op.A_off;
+    const bool rowmaj = op.amode == 0 || op.amode == 2;
+    const int mrows = min(kTM, op.M - i0);
+    double acc8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc8[q] = 0.0;
+    for (int k0 = 0; k0 < op.K; k0 += 1024) {
+      const int kc = min(1024, op.K - k0);
+      __syncthreads();
+      for (int kk = threadIdx.x; kk < kc; kk += 256) xs[kk] = op_row(op.xmode, op.x_off, k0 + kk, idx, v, ts, contrib, 1)[0];
+      __syncthreads();
+      if (rowmaj) {  // warp per row (8 rows each), lanes along k
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int i = i0 + wid * 8 + q;
+          if (i >= op.M) continue;
+          const int kend = op.amode == 0 ? min(kc, i + 1 - k0) : kc;
+          const double* row = op.amode == 0 ? Am + (size_t)i * (i + 1) / 2 + k0 : Am + (size_t)i * op.lda + k0;
+          double s = 0.0;
+          for (int kk = lane; kk < kend; kk += 32) s += row[kk] * xs[kk];
+          acc8[q] += s;
+        }
+      } else {  // lanes along rows (2 x 32), warps split k
+        const int span = (kc + 7) / 8, ka = wid * span, kb = min(kc, ka + span);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = i0 + h * 32 + lane;
+          if (i >= op.M) continue;
+          double s = 0.0;
+          for (int kk = ka; kk < kb; ++kk) {
+            const int k = k0 + kk;
+            const double a = op.amode == 1 ? (k >= i ? Am[(size_t)k * (k + 1) / 2 + i] : 0.0) : Am[(size_t)k * op.lda + i];
+            s += a * xs[kk];
+          }
+          acc8[h] += s;
+        }
+      }
+    }
+    if (rowmaj) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc8[q] = warp_sum(acc8[q]);
+      if (lane == 0)
+        for (int q = 0; q < 8; ++q) part[0][wid * 8 + q] = acc8[q];
+    } else {
+      part[wid][lane] = acc8[0];
+      part[wid][32 + lane] = acc8[1];
+    }
+    __syncthreads();
+    for (int ii = threadIdx.x; ii < mrows; ii += 256) {
+      double a = 0.0;
+      if (rowmaj) a = part[0][ii];
+      else
+        for (int q = 0; q < 8; ++q) a += part[q][ii];
+      const int i = i0 + ii;
+      double val = op.alpha * a;
+      if (op.smode >= 0) val += op_row(op.smode, op.s_off, i, idx, v, ts, contrib, 1)[0];
+      op_row(op.dmode, op.d_off, i, idx, v, ts, contrib, 1)[0] = val;
+    }
+    return;
+  }
   const int nr = min(kRW, nrhs - r0);
   const int tr = threadIdx.x & 31, ti = threadIdx.x >> 5;
   const double* Am = fac + op.A_off;
