@@ -302,3 +302,60 @@ def test_full_size_config_against_reference(name):
     assert rep.converged
     its = int(gd["pcg_iters"])
     assert abs(rep.n_i - its) <= max(1, int(0.25 * its)), (rep.n_i, its)
+
+
+def test_many_and_odd_rhs_counts():
+    """Right-hand-side blocks of 1, 3, 17 and 64 columns (tile widths 16/32,
+    the 1-RHS matrix-vector paths) give the same columns as one-at-a-time
+    solves, for a factor with large (tiled) records."""
+    g = H.build_grid(3, 16, 2)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=3))
+    f = H.factor_hifde3x(a, g, 1e-6)
+    rng = np.random.default_rng(5)
+    B = rng.standard_normal((g.ndof, 64))
+    X = f.apply_inverse(B)
+    for k in (1, 3, 17):
+        Xk = f.apply_inverse(B[:, :k])
+        assert np.allclose(Xk, X[:, :k], rtol=1e-12, atol=1e-13 * np.abs(X).max())
+    for j in (0, 31, 63):
+        assert np.allclose(f.apply_inverse(B[:, j]), X[:, j], rtol=1e-12, atol=1e-13 * np.abs(X).max())
+    Y = f.apply(B[:, :17])
+    assert np.allclose(Y[:, 5], f.apply(B[:, 5]), rtol=1e-12, atol=1e-13 * np.abs(Y).max())
+
+
+def test_concurrent_solves_are_reentrant():
+    """A finished factor serves concurrent apply_inverse calls from several
+    host threads (each on the factor's stream, serialized by the library)."""
+    import threading
+    g = H.build_grid(2, 64, 4)
+    a = H.assemble(g, H.constant_field(g))
+    f = H.factor_hifde(a, g, 1e-9)
+    rng = np.random.default_rng(6)
+    Bs = [rng.standard_normal((g.ndof, 4)) for _ in range(6)]
+    ref = [f.apply_inverse(B) for B in Bs]
+    out = [None] * len(Bs)
+    def work(i):
+        out[i] = f.apply_inverse(Bs[i])
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(Bs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for x, y in zip(out, ref):
+        assert np.array_equal(x, y)
+
+
+def test_api_errors_are_reference_exceptions():
+    """Shape errors raise ValueError (src/driver.py:237-238 style); hifde3x on
+    2D and closed factors are rejected."""
+    g = H.build_grid(2, 32, 4)
+    a = H.assemble(g, H.constant_field(g))
+    f = H.factor_hifde(a, g, 1e-6)
+    with pytest.raises(ValueError):
+        f.apply_inverse(np.ones(g.ndof + 1))
+    with pytest.raises(ValueError):
+        f.apply(np.ones((g.ndof - 1, 2)))
+    with pytest.raises(ValueError):
+        H.factor_hifde3x(a, g, 1e-6)
+    x = f.apply_inverse(np.ones(g.ndof))
+    assert np.isfinite(x).all()
