@@ -11,6 +11,10 @@
 //                           column-pivoted QR (LAPACK dlaqp2 pivoting and norm
 //                           downdating, early stop at the rank cut), congruence,
 //                           inner elimination of rd against sk, delta block.
+//   * skel_ordered_kernel -- the same in the reference's sequential order, one
+//                           cooperative launch with per-group done flags.
+//   * skel_cluster_kernel -- exact order with a CTA cluster per large group
+//                           (column slices, DSMEM pivot exchange).
 //
 // Reference semantics followed:
 //   elimination   src/factor_ops.py:138-159, src/dense.py:187-219
@@ -327,11 +331,11 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
 // ---------------------------------------------------------------------------
 // Skeletonization of one group.
 //   M = A[c+q, c]: A_cc (nc x nc) and Mq = A_qc (nq x nc), column-major.
-//   CPQR of Mq: per step one warp picks the pivot, swaps and builds the
-//   Householder reflector; all warps then update the trailing columns
-//   (warp per column) and downdate their norms -- two barriers per step.
-//   The Householder vectors are never needed again (only R), so they are not
-//   even scaled into place.
+//   CPQR of Mq: columns stay in place; every warp picks the pivot from the
+//   double-buffered partial norms (LAPACK position map for ties) and G-lane
+//   sub-warps update the trailing columns and downdate their norms -- one
+//   barrier per step.  The Householder vectors are never needed again (only
+//   R), so they are not even scaled into place.
 // ---------------------------------------------------------------------------
 struct NoWait {
   __device__ void operator()() const {}
