@@ -45,7 +45,7 @@ struct SkelBigTask {
   int64_t rec_off, delta_off, out_off;
   int32_t group, pad;
 };
-constexpr int kMaxG = 256;                     // most CTAs serving one large-group CPQR
+constexpr int kMaxG = 1024;                    // most CTAs serving one large-group CPQR
 constexpr int kCL = 16;                        // CTAs per cluster (many-group batches)
 constexpr int kMaxBigNc = 4096;                // largest group handled by that path
 

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
                                                       unsigned int* __restrict__ bar, Arenas A, double eps) {
   extern __shared__ __align__(16) double vsm[];  // reflector column (nq doubles)
   __shared__ double red[8];
+  __shared__ double spart[16];  // split-column partial dots
   __shared__ double sh_best;
   __shared__ int sh_pvt;
   __shared__ unsigned char done[kMaxBigNc];
@@ -344,9 +345,78 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
       w.rdiag[i] = beta;
       w.piv[i] = P;
     }
-    // update the owned, not yet pivoted columns (warp per column)
     best = -1.0;
     bidx = nc;
+    // owned, not yet pivoted columns of this CTA
+    int nown = 0;
+    for (int j = rb; j < nc; j += CL) nown += (done[j] || j == P) ? 0 : 1;
+    if (nown > 0 && nown <= 4) {
+      // few columns per CTA (many CTAs per group): the rows of each column
+      // are split over S warps, partial dots combined in a fixed order
+      const int S = 8 / nown;
+      const int c = wid / S, sl = wid - c * S;
+      int j = -1;
+      if (c < nown) {
+        int q = 0;
+        for (int jj = rb; jj < nc; jj += CL) {
+          if (done[jj] || jj == P) continue;
+          if (q++ == c) { j = jj; break; }
+        }
+      }
+      const int m1 = nq - (i + 1);
+      const int chunk = ((m1 + S - 1) / S + 31) & ~31;
+      const int ra = i + 1 + sl * chunk, rz = min(nq, ra + chunk);
+      double* col = j >= 0 ? w.Mq + (size_t)j * ldq : nullptr;
+      double ci = 0.0;
+      if (j >= 0 && tau != 0.0) {
+        ci = col[i];
+        const double s = warp_sum(wdot(vsm, col, ra, rz, lane));
+        if (lane == 0) spart[wid] = s;
+      }
+      __syncthreads();
+      double nv = 0.0;
+      bool recompute = false;
+      if (j >= 0) {
+        double civ = ci;
+        if (tau != 0.0) {
+          double s = 0.0;
+          for (int q = 0; q < S; ++q) s += spart[c * S + q];
+          const double wv = tau * (ci + scal * s);
+          civ = ci - wv;
+          waxpy(col, vsm, wv * scal, ra, rz, lane);
+          if (sl == 0 && lane == 0) col[i] = civ;
+        } else {
+          civ = col[i];
+        }
+        nv = w.vn1[j];
+        if (nv != 0.0) {
+          double tmp = fabs(civ) / nv;
+          tmp = 1.0 - tmp * tmp;
+          tmp = tmp > 0.0 ? tmp : 0.0;
+          const double ratio = nv / w.vn2[j];
+          if (tmp * ratio * ratio <= tol3z) recompute = true;
+          else nv *= sqrt(tmp);
+        }
+      }
+      if (__syncthreads_or(recompute ? 1 : 0)) {  // rare: norms recomputed from the rows
+        if (recompute) {
+          const double s = warp_sum(wdot(col, col, ra, rz, lane));
+          if (lane == 0) spart[8 + wid] = s;
+        }
+        __syncthreads();
+        if (recompute) {
+          double s = 0.0;
+          for (int q = 0; q < S; ++q) s += spart[8 + c * S + q];
+          nv = (i + 1 < nq) ? sqrt(s) : 0.0;
+          if (sl == 0 && lane == 0) w.vn2[j] = nv;
+        }
+      }
+      if (j >= 0 && sl == 0) {
+        if (lane == 0) w.vn1[j] = nv;
+        if (nv > best || (nv == best && j < bidx)) { best = nv; bidx = j; }
+      }
+    } else
+    // update the owned, not yet pivoted columns (warp per column)
     for (int j = rb + CL * wid; j < nc; j += CL * 8) {
       if (done[j] || j == P) continue;
       double* col = w.Mq + (size_t)j * ldq;
@@ -689,7 +759,7 @@ int cpqr_coop_capacity(size_t smem) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_mc_kernel<false>, 256, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cap_cached = (per_sm >= 1 ? 1 : 0) * nsm;  // one CTA per SM: always co-resident
+  cap_cached = per_sm * nsm;  // the cooperative co-residency limit
   smem_cached = smem;
   return cap_cached;
 }

@@ -1639,8 +1639,36 @@ struct Factorizer {
         g_launches += 2;
       }
       const int64_t hlo = bh[(size_t)b], hhi = bh[(size_t)b + 1];
-      if (hhi > hlo) launch_huge_batch(huge, hlo, hhi, dhuge.p, dth.p, dinner.p, ddmin.p, dscale.p, A, AH,
-                                       huge_max_nq, huge_max_nf, huge_max_nb);
+      if (hhi > hlo) {
+        static const bool shapes = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: per-batch shapes and time
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (shapes) {
+          HCK(cudaEventCreate(&e0));
+          HCK(cudaEventCreate(&e1));
+          HCK(cudaEventRecord(e0, s));
+        }
+        launch_huge_batch(huge, hlo, hhi, dhuge.p, dth.p, dinner.p, ddmin.p, dscale.p, A, AH, huge_max_nq,
+                          huge_max_nf, huge_max_nb);
+        if (shapes) {
+          HCK(cudaEventRecord(e1, s));
+          std::vector<int32_t> kk((size_t)nt);
+          HCK(cudaMemcpyAsync(kk.data(), kout.p, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+          HCK(cudaStreamSynchronize(s));
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, e0, e1);
+          double trf = 0;
+          fprintf(stderr, "[hifde] tag %.3f batch %d: %lld large groups, %.3f ms:", tag, b, (long long)(hhi - hlo), ms);
+          for (int64_t i = hlo; i < hhi; ++i) {
+            const SkelBigTask& H = huge[(size_t)i];
+            const int k = kk[(size_t)H.group];
+            fprintf(stderr, " (%d,%d,k%d)", H.nc, H.nq, k);
+            for (int st = 0; st < k; ++st) trf += 24.0 * H.nq * (H.nc - st);
+          }
+          fprintf(stderr, " | cpqr-traffic %.2f GB\n", trf * 1e-9);
+          cudaEventDestroy(e0);
+          cudaEventDestroy(e1);
+        }
+      }
       if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  batch %d done", b); }
     }
     HCK(cudaEventRecord(L.ev1, s));
@@ -1833,8 +1861,14 @@ struct Factorizer {
       HCK(cudaMemsetAsync(A.bvals + H.delta_off, 0, sizeof(double) * (size_t)H.nc * H.nc, s));
     }
     const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 2 * max_nb));
+    static const bool split_t = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: phase times
+    cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (split_t) for (auto& e : pe) HCK(cudaEventCreate(&e));
+    if (split_t) HCK(cudaEventRecord(pe[0], s));
     launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
-    if (n > 8) {
+    if (split_t) HCK(cudaEventRecord(pe[1], s));
+    static const int cl_min = getenv("HIFDE_CPQR_CLUSTER_MIN") ? atoi(getenv("HIFDE_CPQR_CLUSTER_MIN")) : 1 << 30;
+    if (n >= cl_min) {
       // many groups: 16-CTA clusters per group, scheduled in waves
       HCK(launch_cpqr_cluster(dtk, n, max_nq, A, opt.eps, s));
       ++g_launches;
@@ -1871,6 +1905,7 @@ struct Factorizer {
         dbar.release(s);
       }
     }
+    if (split_t) HCK(cudaEventRecord(pe[2], s));
     launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
     launch_skelbig_tinit(dtk, d10.p, (int)wrow.size(), A, s);
     for (int bb = ntb - 1; bb >= 0; --bb) {
@@ -1901,6 +1936,16 @@ struct Factorizer {
     launch_apply_rd(d_skv + lo, n, A, s);
     g_launches += 3;
     HCK(cudaGetLastError());
+    if (split_t) {
+      HCK(cudaEventRecord(pe[3], s));
+      HCK(cudaStreamSynchronize(s));
+      float t01 = 0.f, t12 = 0.f, t23 = 0.f;
+      cudaEventElapsedTime(&t01, pe[0], pe[1]);
+      cudaEventElapsedTime(&t12, pe[1], pe[2]);
+      cudaEventElapsedTime(&t23, pe[2], pe[3]);
+      fprintf(stderr, "[hifde]   assemble %.3f cpqr %.3f rest %.3f ms\n", t01, t12, t23);
+      for (auto& e : pe) cudaEventDestroy(e);
+    }
     for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(s);
     inv.release(s);
     d9.release(s);
