@@ -88,7 +88,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB
+    p = path or os.environ.get("HIFDE_LIB_PATH") or LIB  # override: A/B builds (tools/)
     # the host symbolic phase uses OpenMP between GPU launches: idle workers
     # must sleep, not spin (spinning libgomp workers starve the host thread)
     os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")

@@ -28,6 +28,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cuda/atomic>
+#include <utility>
+#include <vector>
 
 #include "hifde_internal.h"
 
@@ -420,19 +422,24 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
     for (int j = rb + CL * wid; j < nc; j += CL * 8) {
       if (done[j] || j == P) continue;
       double* col = w.Mq + (size_t)j * ldq;
+      double civ;  // R(i, j) after this step, kept in a register
       if (tau != 0.0) {
+        const double ci = col[i];
         double s = wdot(vsm, col, i + 1, nq, lane);
         s = warp_sum(s);
-        const double wv = tau * (col[i] + scal * s);
+        const double wv = tau * (ci + scal * s);
+        civ = ci - wv;
         __syncwarp();
-        if (lane == 0) col[i] -= wv;
+        if (lane == 0) col[i] = civ;
         waxpy(col, vsm, wv * scal, i + 1, nq, lane);
         __syncwarp();
+      } else {
+        civ = col[i];
       }
       double nv = w.vn1[j];
       bool recompute = false;
       if (nv != 0.0) {
-        double tmp = fabs(col[i]) / nv;
+        double tmp = fabs(civ) / nv;
         tmp = 1.0 - tmp * tmp;
         tmp = tmp > 0.0 ? tmp : 0.0;
         const double ratio = nv / w.vn2[j];
@@ -751,24 +758,34 @@ void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwo
 }
 
 int cpqr_coop_capacity(size_t smem) {
-  static int cap_cached = -1;
-  static size_t smem_cached = 0;
-  if (cap_cached >= 0 && smem_cached == smem) return cap_cached;
-  cudaFuncSetAttribute(cpqr_mc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+  // cached per shared-memory size (the occupancy query is slow enough to
+  // starve the GPU between batches)
+  static std::vector<std::pair<size_t, int>> cache;
+  for (const auto& c : cache)
+    if (c.first == smem) return c.second;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cpqr_mc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+    attr = true;
+  }
   int per_sm = 0, dev = 0, nsm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cpqr_mc_kernel<false>, 256, smem);
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cap_cached = per_sm * nsm;  // the cooperative co-residency limit
-  smem_cached = smem;
-  return cap_cached;
+  const int cap = per_sm * nsm;  // the cooperative co-residency limit
+  cache.emplace_back(smem, cap);
+  return cap;
 }
 
 cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
                              unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   size_t smem = sizeof(double) * (size_t)max_nq;
-  cudaFuncSetAttribute(cpqr_mc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cpqr_mc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+    attr = true;
+  }
   Arenas Ac = A;
   void* args[] = {(void*)&tasks, (void*)&ntasks, (void*)&d_gstart, (void*)&d_bar, (void*)&Ac, (void*)&eps};
   return cudaLaunchCooperativeKernel((const void*)cpqr_mc_kernel<false>, dim3((unsigned)nblocks), dim3(256), args,
