@@ -570,10 +570,18 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   mark(4);
 
   // ---- mode 3: R factor of Mq by chunked Householder QR in shared memory --
+  // [R ; chunk] is reduced column by column.  G lanes per trailing column,
+  // all trailing columns at once; the chunk norm of column i + 1 is
+  // accumulated while it is updated at step i, so every thread builds the
+  // reflector itself and a column step has one barrier.
   int nqm = nq, ldm = ldq;
   if (t.mode == 3) {
     const int h = t.chunk, lds = nc + h;
     double* S = wsh;
+    double* cn2 = cq;  // chunk-part squared norms (the CPQR vectors are not live yet)
+    int Gq = 32;
+    while (Gq > 8 && NT / Gq < nc) Gq >>= 1;
+    const int nsq = NT / Gq, slq = lane & (Gq - 1), slotq = wid * (32 / Gq) + lane / Gq;
     for (int e = threadIdx.x; e < lds * nc; e += NT) S[e] = 0.0;
     for (int r0 = 0; r0 < nq; r0 += h) {
       const int hh = min(h, nq - r0);
@@ -583,41 +591,71 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         S[nc + rr + (size_t)j * lds] = rr < hh ? Mq[(size_t)(r0 + rr) + (size_t)j * ldq] : 0.0;
       }
       __syncthreads();
+      for (int base = 0; base < nc; base += nsq) {
+        const int j = base + slotq;
+        const double* col = S + (size_t)min(j, nc - 1) * lds;
+        double a = 0.0;
+        for (int r = nc + slq; r < nc + hh; r += Gq) a += col[r] * col[r];
+        a = group_sum(a, Gq);
+        if (j < nc && slq == 0) cn2[j] = a;
+      }
+      __syncthreads();
       for (int i = 0; i < nc; ++i) {
         // x = [S_ii ; chunk rows of column i]; the R rows below i are zero
-        if (wid == 0) {
-          const double* ci = S + (size_t)i * lds;
-          double xs = 0.0;
-          for (int r = nc + lane; r < nc + h; r += 32) xs += ci[r] * ci[r];
-          const double xnorm = sqrt(warp_sum(xs));
-          const double alpha = ci[i];
-          double beta, tau, scal;
-          if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
-          else {
-            beta = -copysign(hypot(alpha, xnorm), alpha);
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
-          }
-          if (lane == 0) { sh_beta = beta; sh_tau = tau; sh_scal = scal; }
-        }
-        __syncthreads();
-        const double tau = sh_tau, scal = sh_scal;
         const double* v = S + (size_t)i * lds;
+        const double xnorm = sqrt(cn2[i]);
+        const double alpha = v[i];
+        double beta, tau, scal;
+        if (xnorm == 0.0) { beta = alpha; tau = 0.0; scal = 0.0; }
+        else {
+          beta = -copysign(hypot(alpha, xnorm), alpha);
+          tau = (beta - alpha) / beta;
+          scal = 1.0 / (alpha - beta);
+        }
         if (tau != 0.0) {
-          for (int j = i + 1 + wid; j < nc; j += NW) {
-            double* col = S + (size_t)j * lds;
-            double s2 = 0.0;
-            for (int r = nc + lane; r < nc + h; r += 32) s2 += v[r] * col[r];
-            s2 = warp_sum(s2);
-            const double w = tau * (col[i] + scal * s2);
-            __syncwarp();
-            if (lane == 0) col[i] -= w;
+          for (int base = i + 1; base < nc; base += nsq) {
+            const int j = base + slotq;
+            const bool act = j < nc;
+            double* col = S + (size_t)(act ? j : i) * lds;  // inactive: harmless reads of v
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int r = nc + slq;
+            const int rend = act ? nc + hh : 0;  // inactive slots: no loads, shuffles only
+            for (; r + 3 * Gq < rend; r += 4 * Gq) {
+              s0 += v[r] * col[r];
+              s1 += v[r + Gq] * col[r + Gq];
+              s2 += v[r + 2 * Gq] * col[r + 2 * Gq];
+              s3 += v[r + 3 * Gq] * col[r + 3 * Gq];
+            }
+            for (; r < rend; r += Gq) s0 += v[r] * col[r];
+            const double sd = group_sum((s0 + s1) + (s2 + s3), Gq);
+            const double w = tau * (col[i] + scal * sd);
             const double ws2 = w * scal;
-            for (int r = nc + lane; r < nc + h; r += 32) col[r] -= ws2 * v[r];
+            double a0 = 0.0, a1 = 0.0;
+            r = nc + slq;
+            for (; r + Gq < rend; r += 2 * Gq) {
+              const double x0 = col[r] - ws2 * v[r];
+              const double x1 = col[r + Gq] - ws2 * v[r + Gq];
+              if (act) {
+                col[r] = x0;
+                col[r + Gq] = x1;
+              }
+              a0 += x0 * x0;
+              a1 += x1 * x1;
+            }
+            for (; r < rend; r += Gq) {
+              const double x = col[r] - ws2 * v[r];
+              if (act) col[r] = x;
+              a0 += x * x;
+            }
+            const double an = group_sum(a0 + a1, Gq);
+            if (act && slq == 0) {
+              col[i] -= w;
+              cn2[j] = an;
+            }
           }
         }
         __syncthreads();
-        if (threadIdx.x == 0) S[i + (size_t)i * lds] = sh_beta;
+        if (threadIdx.x == 0) S[i + (size_t)i * lds] = beta;
       }
     }
     __syncthreads();
@@ -713,18 +751,19 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       const int j = base + slot;
       const bool act = j < nc && j != p && !dcol[j];
       double* col = Mc + (size_t)(act ? j : p) * ldm;  // inactive: harmless reads of v
+      const int nqa = act ? nqm : 0;                   // inactive slots: no row loads, shuffles only
       double acc = 0.0;                                // sum of squares of rows >= i + 2
       if (tau != 0.0) {
         // 4 rows in flight per lane: the loops are load-latency bound
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int r = i + 1 + sl;
-        for (; r + 3 * G < nqm; r += 4 * G) {
+        for (; r + 3 * G < nqa; r += 4 * G) {
           s0 += v[r] * col[r];
           s1 += v[r + G] * col[r + G];
           s2 += v[r + 2 * G] * col[r + 2 * G];
           s3 += v[r + 3 * G] * col[r + 3 * G];
         }
-        for (; r < nqm; r += G) s0 += v[r] * col[r];
+        for (; r < nqa; r += G) s0 += v[r] * col[r];
         const double sd = group_sum((s0 + s1) + (s2 + s3), G);
         const double w = tau * (col[i] + scal * sd);
         __syncwarp();
@@ -732,41 +771,39 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         const double ws2 = w * scal;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         r = i + 1 + sl;
-        if (r == i + 1 && r < nqm) {  // row i + 1: updated, not in the next norm
+        if (r == i + 1 && r < nqa) {  // row i + 1: updated, not in the next norm
           const double x = col[r] - ws2 * v[r];
-          if (act) col[r] = x;
+          col[r] = x;
           r += G;
         }
-        for (; r + 3 * G < nqm; r += 4 * G) {
+        for (; r + 3 * G < nqa; r += 4 * G) {
           const double x0 = col[r] - ws2 * v[r];
           const double x1 = col[r + G] - ws2 * v[r + G];
           const double x2 = col[r + 2 * G] - ws2 * v[r + 2 * G];
           const double x3 = col[r + 3 * G] - ws2 * v[r + 3 * G];
-          if (act) {
-            col[r] = x0;
-            col[r + G] = x1;
-            col[r + 2 * G] = x2;
-            col[r + 3 * G] = x3;
-          }
+          col[r] = x0;
+          col[r + G] = x1;
+          col[r + 2 * G] = x2;
+          col[r + 3 * G] = x3;
           a0 += x0 * x0;
           a1 += x1 * x1;
           a2 += x2 * x2;
           a3 += x3 * x3;
         }
-        for (; r < nqm; r += G) {
+        for (; r < nqa; r += G) {
           const double x = col[r] - ws2 * v[r];
-          if (act) col[r] = x;
+          col[r] = x;
           a0 += x * x;
         }
         acc = (a0 + a1) + (a2 + a3);
       } else {
         double a0 = 0.0, a1 = 0.0;
         int r = i + 2 + sl;
-        for (; r + G < nqm; r += 2 * G) {
+        for (; r + G < nqa; r += 2 * G) {
           a0 += col[r] * col[r];
           a1 += col[r + G] * col[r + G];
         }
-        for (; r < nqm; r += G) a0 += col[r] * col[r];
+        for (; r < nqa; r += G) a0 += col[r] * col[r];
         acc = a0 + a1;
       }
       acc = group_sum(acc, G);

@@ -1418,6 +1418,24 @@ struct Factorizer {
       nbatch = 1;
     }
     L.nbatches = nbatch;
+    if (getenv("HIFDE_BIGSHAPES")) {  // debug: workspace modes and shapes of the level's groups
+      int64_t cnt[4] = {0, 0, 0, 0}, mnc[4] = {0, 0, 0, 0}, mnq[4] = {0, 0, 0, 0};
+      double snc[4] = {0, 0, 0, 0}, snq[4] = {0, 0, 0, 0};
+      for (const SkelTask& T : tasks) {
+        const int md = T.mode & 3;
+        ++cnt[md];
+        mnc[md] = std::max<int64_t>(mnc[md], T.nc);
+        mnq[md] = std::max<int64_t>(mnq[md], T.nq);
+        snc[md] += T.nc;
+        snq[md] += T.nq;
+      }
+      fprintf(stderr, "[hifde] tag %.3f modes:", tag);
+      for (int md = 0; md < 4; ++md)
+        if (cnt[md])
+          fprintf(stderr, " m%d n=%lld nc(avg %.0f max %lld) nq(avg %.0f max %lld)", md, (long long)cnt[md],
+                  snc[md] / cnt[md], (long long)mnc[md], snq[md] / cnt[md], (long long)mnq[md]);
+      fprintf(stderr, "\n");
+    }
     L.lap("tasks");
     HTRACE("  symbolic done, %d batches", nbatch);
     double tp = now_s();
