@@ -56,6 +56,17 @@ extern "C" {
 #define HIFDE_ORDER_SNAPSHOT 1  /* all IDs of a level from one snapshot    */
 #define HIFDE_ORDER_EXACT 2     /* reference's sequential semantics        */
 
+/*
+ * Rank communicator of the sharded factorization: the fine
+ * levels are partitioned spatially over the ranks, each group factored by its
+ * owner, and only the blocks a rank consumes from another rank's groups are
+ * exchanged (NCCL over NVLink); coarse exact-order levels run on rank 0.
+ * Every rank passes the same matrix and ends with the whole factor.  The
+ * reference has no multi-process path (src/driver.py:183 runs one thread).
+ */
+typedef struct hifde_comm hifde_comm_t;
+#define HIFDE_COMM_ID_BYTES 128
+
 typedef struct hifde_options {
   int variant;          /* HIFDE_VARIANT_*                                  */
   int skip_levels;      /* skeletonization skipped below this level         */
@@ -67,6 +78,7 @@ typedef struct hifde_options {
   int verify;           /* 1: check cells of each level are non-interacting */
   double eps;           /* ID relative tolerance (0 -> exact rank)          */
   void* stream;         /* cudaStream_t or NULL                             */
+  hifde_comm_t* comm;   /* NULL: one GPU; else shard over comm's ranks      */
 } hifde_options_t;
 
 typedef struct hifde_factor hifde_factor_t;
@@ -84,6 +96,9 @@ typedef struct hifde_info {
   int32_t variant;
   int64_t fac_len;      /* doubles in the factor arena (hifde_copy_arenas)  */
   int64_t idx_len;      /* int32 entries in the index arena                 */
+  int32_t nranks;       /* ranks the factorization was sharded over (1)     */
+  int32_t pad;
+  int64_t xfer_bytes;   /* block bytes this rank exchanged with its peers   */
 } hifde_info_t;
 
 /*
@@ -226,6 +241,37 @@ const char* hifde_last_error(void);
 int64_t hifde_partition(int dim, int n_grid, int m_leaf, int ell, int level_kind,
                         const uint8_t* active, int32_t* members, int64_t members_cap,
                         int64_t* offsets, int64_t offsets_cap);
+
+/*
+ * Communicators.  Rank 0 creates a unique id (HIFDE_COMM_ID_BYTES bytes) and
+ * the caller distributes it; every rank then calls hifde_comm_init with its
+ * rank and CUDA device (ncclCommInitRank; libnccl.so.2 is loaded at run time,
+ * preferring the copy torch already loaded).  hifde_comm_emulated builds P
+ * virtual ranks inside one process on one device (tests: each virtual rank
+ * keeps a private block arena, so a missing transfer corrupts the factor).
+ */
+int hifde_comm_unique_id(uint8_t* id);
+int hifde_comm_init(const uint8_t* id, int nranks, int rank, int device, hifde_comm_t** out);
+int hifde_comm_emulated(int nranks, int device, hifde_comm_t** out);
+int hifde_comm_info(const hifde_comm_t* c, int* nranks, int* rank, int* emulated);
+void hifde_comm_free(hifde_comm_t* c);
+const char* hifde_comm_last_error(void);
+
+/*
+ * Host-only sharding hooks (no GPU needed; the CPU multi-process tests):
+ * hifde_shard_owner: subdomain rank of each DOF for nranks ranks (boxes split
+ * round-robin over the axes by twos).  hifde_shard_plan: the block transfers
+ * that make every block listed by a task (task t lists
+ * lists[list_ptr[t] .. list_ptr[t+1])) resident on the task's owner, given
+ * each block's producer and holders (have[], a bit per rank, updated);
+ * out[3i..3i+2] = (src, dst, block) sorted by (src, dst, block).  Returns the
+ * number of transfers (out == NULL: count only), -2-count if cap is too small,
+ * -1 on bad input.
+ */
+int hifde_shard_owner(int nranks, int dim, int n_grid, const int32_t* dofs, int64_t count, int32_t* owner);
+int64_t hifde_shard_plan(int nranks, int64_t nblocks, const int32_t* producer, uint32_t* have, int64_t ntasks,
+                         const int32_t* owner, const int64_t* list_ptr, const int32_t* lists, int32_t* out,
+                         int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -22,10 +22,12 @@ SOURCES = [
     "csrc/kernels_solve.cu",
     "csrc/kernels_krylov.cu",
     "csrc/runtime.cu",
+    "csrc/comm.cu",
     "csrc/partition.cpp",
+    "csrc/shard.cpp",
     "csrc/hostprof.cpp",
 ]
-HEADERS = ["csrc/hifde_internal.h", "csrc/partition.h", "csrc/hostprof.h"]
+HEADERS = ["csrc/hifde_internal.h", "csrc/partition.h", "csrc/hostprof.h", "csrc/comm.h", "csrc/shard.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

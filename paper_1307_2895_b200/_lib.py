@@ -28,6 +28,7 @@ class Options(C.Structure):
         ("verify", C.c_int),
         ("eps", C.c_double),
         ("stream", C.c_void_p),
+        ("comm", C.c_void_p),
     ]
 
 
@@ -45,6 +46,9 @@ class Info(C.Structure):
         ("variant", C.c_int32),
         ("fac_len", C.c_int64),
         ("idx_len", C.c_int64),
+        ("nranks", C.c_int32),
+        ("pad", C.c_int32),
+        ("xfer_bytes", C.c_int64),
     ]
 
 
@@ -78,6 +82,8 @@ EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
     "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
     "hifde_free", "hifde_last_error", "hifde_partition",
+    "hifde_comm_unique_id", "hifde_comm_init", "hifde_comm_emulated", "hifde_comm_info", "hifde_comm_free",
+    "hifde_comm_last_error", "hifde_shard_owner", "hifde_shard_plan",
 ]
 
 _lib = None
@@ -135,6 +141,22 @@ def load(path: str | None = None):
     lib.hifde_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                     C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]
     lib.hifde_partition.restype = C.c_int64
+    lib.hifde_comm_unique_id.argtypes = [C.c_void_p]
+    lib.hifde_comm_unique_id.restype = C.c_int
+    lib.hifde_comm_init.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    lib.hifde_comm_init.restype = C.c_int
+    lib.hifde_comm_emulated.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    lib.hifde_comm_emulated.restype = C.c_int
+    lib.hifde_comm_info.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    lib.hifde_comm_info.restype = C.c_int
+    lib.hifde_comm_free.argtypes = [C.c_void_p]
+    lib.hifde_comm_free.restype = None
+    lib.hifde_comm_last_error.restype = C.c_char_p
+    lib.hifde_shard_owner.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
+    lib.hifde_shard_owner.restype = C.c_int
+    lib.hifde_shard_plan.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+    lib.hifde_shard_plan.restype = C.c_int64
     if path is None:
         _lib = lib
     return lib

@@ -1,0 +1,47 @@
+// Rank communicator of the sharded factorization (hifde_comm_t).
+//
+// Real mode: one process per GPU, an NCCL communicator over NVLink/NVSwitch
+// created from a unique id the caller distributes (torch.distributed in the
+// Python shim).  NCCL is resolved at run time (dlopen; the copy torch already
+// loaded is preferred), so the library itself has no link-time NCCL
+// dependency.
+//
+// Emulated mode (tests on one GPU): P virtual ranks inside one process and one
+// stream.  Each virtual rank owns a private copy of the block arena, so a
+// block a rank consumes but never received is NaN and the factor is wrong;
+// the factor, index arena and active mask stay shared (their unions are
+// whole-slice collectives in real mode).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+struct hifde_comm {
+  int P = 1, rank = 0, device = 0;
+  bool emulated = false;
+  void* nccl = nullptr;  // ncclComm_t
+};
+
+namespace hifde {
+
+enum CommType { kI32 = 0, kU8 = 1, kF64 = 2 };
+enum CommOp { kSum = 0, kMax = 1, kMin = 2 };
+
+// In-place all-reduce over the ranks (no-op for P = 1 or emulated).
+// Throws std::runtime_error on NCCL failure.
+void comm_allreduce(const hifde_comm* c, void* buf, size_t count, CommType t, CommOp op, cudaStream_t s);
+// Grouped point-to-point: sends[i] = (peer, ptr, bytes), likewise recvs.
+struct P2P {
+  int peer;
+  void* ptr;
+  size_t bytes;
+};
+void comm_sendrecv(const hifde_comm* c, const P2P* sends, int nsend, const P2P* recvs, int nrecv, cudaStream_t s);
+
+// dst[dst_off[i] + j] = src[src_off[i] + j], j < len[i] (one CTA per segment).
+void launch_seg_copy(const double* src, double* dst, const int64_t* src_off, const int64_t* dst_off,
+                     const int64_t* len, int nseg, cudaStream_t s);
+void launch_seg_copy_i32(const int32_t* src, int32_t* dst, const int64_t* src_off, const int64_t* dst_off,
+                         const int64_t* len, int nseg, cudaStream_t s);
+
+}  // namespace hifde

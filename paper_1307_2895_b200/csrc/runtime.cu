@@ -35,6 +35,8 @@
 #include "hifde_internal.h"
 #include "hostprof.h"
 #include "partition.h"
+#include "comm.h"
+#include "shard.h"
 
 #include <omp.h>
 
@@ -270,6 +272,8 @@ struct hifde_factor {
   int dim = 0, variant = 0, spd = 1, device = 0;
   double eps = 0;
   int64_t s_top = 0, m_f_bytes = 0;
+  int nranks = 1;           // ranks the factorization was sharded over
+  int64_t xfer_bytes = 0;   // block bytes moved between ranks
   double t_f = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -699,6 +703,201 @@ struct Factorizer {
   int64_t bf_epoch = 0;
   size_t idx_uploaded = 0;
 
+  // --- sharding over ranks (opt.comm, shard.h) -------------------------------
+  // Every rank runs this host analysis identically; a group's kernels run on
+  // its owner only.  Real ranks (NCCL): the blocks a rank's groups consume
+  // from other ranks arrive before the launch, and the state every rank reads
+  // (active mask, ranks, sk/rd lists) is merged after each launch by
+  // whole-slice all-reduces (min / max over slices the non-owners left at
+  // 1 / 0); the factor arena is summed once at the end (non-owners hold
+  // zeros).  Emulated ranks: one process launches every virtual rank's groups
+  // with that rank's private block arena.
+  const hifde_comm* comm = nullptr;
+  int P = 1, me = 0;
+  bool emu = false, real = false;
+  ShardGeom geom;
+  BlockLedger ledger;
+  std::vector<DBuf<double>> lanes;  // emulated: block arenas of virtual ranks 1..P-1 (rank 0: bvals)
+  DBuf<double> xsend, xrecv;        // packed block transfers
+  DBuf<int64_t> xseg;               // segment tables of the packs
+  DBuf<int> agree;                  // status agreement scalar
+  std::vector<uint8_t> own_;        // owner rank per group of the current level
+  int64_t xfer_blocks = 0, xfer_bytes = 0;  // totals (metrics)
+
+  bool sharded() const { return comm != nullptr && P > 1; }
+  // ranks whose groups this process launches: all (unsharded / emulated) or its own
+  int rank_lo() const { return sharded() && !emu ? me : 0; }
+  int rank_hi() const { return sharded() && !emu ? me + 1 : (sharded() ? P : 1); }
+  DBuf<double>& bv_of(int r) { return (emu && r > 0) ? lanes[(size_t)r - 1] : bvals; }
+  Arenas arenas_for(int r) {
+    Arenas A = arenas();
+    A.bvals = bv_of(r).p;
+    return A;
+  }
+  // owner of a group: the subdomain box of its first DOF
+  uint8_t owner_of(const int32_t* c) const { return sharded() ? (uint8_t)shard_owner(geom, X, c[0]) : 0; }
+  // after a bump of the block arena: the emulated lanes follow its size, and
+  // the new region of every virtual rank is NaN until its producer writes it
+  void bvals_grown(size_t old_n) {
+    if (!emu || bvals.n == old_n) return;
+    const size_t add = bvals.n - old_n;
+    for (auto& l : lanes) {
+      l.reserve(bvals.n, s);
+      l.n = bvals.n;
+      HCK(cudaMemsetAsync(l.p + old_n, 0xFF, add * sizeof(double), s));
+    }
+    HCK(cudaMemsetAsync(bvals.p + old_n, 0xFF, add * sizeof(double), s));
+  }
+  // real ranks: non-owners must contribute zeros to the final factor sum
+  void fac_grown(size_t off, size_t cnt) {
+    if (real && cnt) HCK(cudaMemsetAsync(F->fac.p + off, 0, cnt * sizeof(double), s));
+  }
+  // Real ranks: merge the ranks kout[0, nk), the index-arena regions
+  // [off[i], off[i] + len[i]) (sk/rd lists, zero on non-owners: packed,
+  // max-reduced, scattered back) and the active masks (min).
+  DBuf<int32_t> xi32;
+  DBuf<int64_t> xiseg;
+  void union_state(const int64_t* off, const int* len, int nreg, int64_t nk) {
+    if (!real) return;
+    try {
+      if (nk > 0) comm_allreduce(comm, kout.p, (size_t)nk, kI32, kMax, s);
+      if (nreg > 0) {
+        std::vector<int64_t> seg((size_t)3 * nreg);
+        int64_t tot = 0;
+        for (int i = 0; i < nreg; ++i) {
+          seg[(size_t)i] = off[i];
+          seg[(size_t)nreg + i] = tot;
+          seg[(size_t)2 * nreg + i] = len[i];
+          tot += len[i];
+        }
+        if (tot > 0) {
+          xiseg.reserve(seg.size(), s);
+          xiseg.upload(seg.data(), 0, seg.size(), s);
+          xi32.reserve((size_t)tot, s);
+          launch_seg_copy_i32(F->idx.p, xi32.p, xiseg.p, xiseg.p + nreg, xiseg.p + 2 * nreg, nreg, s);
+          comm_allreduce(comm, xi32.p, (size_t)tot, kI32, kMax, s);
+          launch_seg_copy_i32(xi32.p, F->idx.p, xiseg.p + nreg, xiseg.p, xiseg.p + 2 * nreg, nreg, s);
+          g_launches += 2;
+        }
+      }
+      comm_allreduce(comm, d_active, (size_t)N, kU8, kMin, s);
+    } catch (const std::exception& e) {
+      throw Fail{HIFDE_CUDA, e.what()};
+    }
+  }
+  void union_level(const std::vector<SkelTask>& tasks, int64_t nt) {
+    if (!real) return;
+    std::vector<int64_t> off((size_t)nt);
+    std::vector<int> len((size_t)nt);
+    for (int64_t t = 0; t < nt; ++t) {
+      off[(size_t)t] = tasks[(size_t)t].out_off;
+      len[(size_t)t] = tasks[(size_t)t].nc;
+    }
+    union_state(off.data(), len.data(), (int)nt, nt);
+  }
+  // Make every block listed by the tasks resident on the task's owner.
+  void exchange_blocks(int64_t nt, const uint8_t* owner, const int64_t* ptr, const int32_t* cnt,
+                       const int32_t* lists) {
+    if (!sharded()) return;
+    std::vector<Xfer> xf;
+    ledger.plan(nt, owner, ptr, cnt, lists, xf);
+    if (xf.empty()) return;
+    // pairs in plan order; blocks packed contiguously per pair in block order
+    struct Pair {
+      int src, dst;
+      size_t lo, hi;  // xf range
+      int64_t doubles;
+    };
+    std::vector<Pair> pairs;
+    for (size_t i = 0; i < xf.size(); ++i) {
+      const int64_t nb = blk_n[(size_t)xf[i].blk];
+      if (pairs.empty() || pairs.back().src != xf[i].src || pairs.back().dst != xf[i].dst)
+        pairs.push_back(Pair{xf[i].src, xf[i].dst, i, i, 0});
+      pairs.back().hi = i + 1;
+      pairs.back().doubles += nb * nb;
+    }
+    for (const Xfer& x : xf) {
+      const int64_t nb = blk_n[(size_t)x.blk];
+      ++xfer_blocks;
+      xfer_bytes += 8 * nb * nb;
+    }
+    // segment table: (src_off, dst_off, len) triples, one table per launch
+    std::vector<int64_t> seg;
+    auto pack_table = [&](const Pair& p, bool pack, int64_t base) {
+      const size_t n0 = seg.size();
+      const size_t cnt_seg = p.hi - p.lo;
+      seg.resize(n0 + 3 * cnt_seg);
+      int64_t o = base;
+      for (size_t i = p.lo; i < p.hi; ++i) {
+        const int32_t b = xf[i].blk;
+        const int64_t len = (int64_t)blk_n[(size_t)b] * blk_n[(size_t)b];
+        const size_t j = i - p.lo;
+        seg[n0 + j] = pack ? blk_val_off[(size_t)b] : o;
+        seg[n0 + cnt_seg + j] = pack ? o : blk_val_off[(size_t)b];
+        seg[n0 + 2 * cnt_seg + j] = len;
+        o += len;
+      }
+      return n0;
+    };
+    if (emu) {
+      for (const Pair& p : pairs) {
+        seg.clear();
+        xsend.reserve((size_t)p.doubles, s);
+        const size_t a = pack_table(p, true, 0);
+        const size_t b = pack_table(p, false, 0);
+        xseg.reserve(seg.size(), s);
+        xseg.upload(seg.data(), 0, seg.size(), s);
+        const int ns = (int)(p.hi - p.lo);
+        launch_seg_copy(bv_of(p.src).p, xsend.p, xseg.p + a, xseg.p + a + ns, xseg.p + a + 2 * ns, ns, s);
+        launch_seg_copy(xsend.p, bv_of(p.dst).p, xseg.p + b, xseg.p + b + ns, xseg.p + b + 2 * ns, ns, s);
+        g_launches += 2;
+        // the staging buffer is reused by the next pair: keep the stream order
+      }
+      return;
+    }
+    int64_t nsend = 0, nrecv = 0;
+    for (const Pair& p : pairs) {
+      if (p.src == me) nsend += p.doubles;
+      if (p.dst == me) nrecv += p.doubles;
+    }
+    xsend.reserve((size_t)std::max<int64_t>(nsend, 1), s);
+    xrecv.reserve((size_t)std::max<int64_t>(nrecv, 1), s);
+    std::vector<P2P> sends, recvs;
+    std::vector<std::pair<size_t, int>> packs, unpacks;  // (table offset, segments)
+    int64_t so = 0, ro = 0;
+    for (const Pair& p : pairs) {
+      const int ns = (int)(p.hi - p.lo);
+      if (p.src == me) {
+        packs.emplace_back(pack_table(p, true, so), ns);
+        sends.push_back(P2P{p.dst, xsend.p + so, (size_t)p.doubles * sizeof(double)});
+        so += p.doubles;
+      }
+      if (p.dst == me) {
+        unpacks.emplace_back(pack_table(p, false, ro), ns);
+        recvs.push_back(P2P{p.src, xrecv.p + ro, (size_t)p.doubles * sizeof(double)});
+        ro += p.doubles;
+      }
+    }
+    if (seg.empty()) return;
+    xseg.reserve(seg.size(), s);
+    xseg.upload(seg.data(), 0, seg.size(), s);
+    for (auto& pk : packs) {
+      const int64_t* t = xseg.p + pk.first;
+      launch_seg_copy(bvals.p, xsend.p, t, t + pk.second, t + 2 * pk.second, pk.second, s);
+      ++g_launches;
+    }
+    try {
+      comm_sendrecv(comm, sends.data(), (int)sends.size(), recvs.data(), (int)recvs.size(), s);
+    } catch (const std::exception& e) {
+      throw Fail{HIFDE_CUDA, e.what()};
+    }
+    for (auto& up : unpacks) {
+      const int64_t* t = xseg.p + up.first;
+      launch_seg_copy(xrecv.p, bvals.p, t, t + up.second, t + 2 * up.second, up.second, s);
+      ++g_launches;
+    }
+  }
+
   void upload_idx() {
     F->idx.reserve(h_idx.size(), s);
     F->idx.n = h_idx.size();
@@ -740,26 +939,15 @@ struct Factorizer {
   }
 
   // block table entry only (membership updated by the caller)
-  int32_t new_block(int64_t dof_off, int32_t nb, int64_t val_off) {
+  int32_t new_block(int64_t dof_off, int32_t nb, int64_t val_off, int producer) {
     int32_t id = (int32_t)blk_n.size();
+    if (sharded()) ledger.add(id, producer);
     blk_dof_off.push_back(dof_off);
     blk_n.push_back(nb);
     blk_val_off.push_back(val_off);
     blk_alive.push_back(1);
     bf_key.push_back(-2);
     bf_val.push_back(0);
-    return id;
-  }
-  int32_t add_block(int64_t dof_off, int32_t nb, int64_t val_off) {
-    member.ensure_room((size_t)nb);
-    int32_t id = (int32_t)blk_n.size();
-    blk_dof_off.push_back(dof_off);
-    blk_n.push_back(nb);
-    blk_val_off.push_back(val_off);
-    blk_alive.push_back(1);
-    bf_key.push_back(-2);
-    bf_val.push_back(0);
-    for (int32_t i = 0; i < nb; ++i) member.add(h_idx[(size_t)(dof_off + i)], id);
     return id;
   }
   void kill_block(int32_t b) {
@@ -867,23 +1055,46 @@ struct Factorizer {
   // Per-task status words of every launch since the last check: one D2H copy
   // at the next synchronization point (no extra stream syncs per level).
   void check_status() {
-    if (status.n == status_checked) { pending.clear(); return; }
-    const size_t cnt = status.n - status_checked;
-    std::vector<int> st(cnt);
-    HCK(cudaMemcpyAsync(st.data(), status.p + status_checked, cnt * sizeof(int), cudaMemcpyDeviceToHost, s));
-    HCK(cudaStreamSynchronize(s));
-    for (const Pending& P : pending)
-      for (int64_t i = 0; i < P.cnt; ++i) {
-        const int v = st[(size_t)(P.off - (int64_t)status_checked + i)];
-        if (v != 0) {
-          char buf[256];
-          const char* kind = v == 1 ? "matrix is not positive definite" : "singular pivot";
-          snprintf(buf, sizeof buf, "%s (%s %lld of level %g)", kind, P.what, (long long)i, P.tag);
-          throw Fail{v == 1 ? HIFDE_INDEFINITE : HIFDE_SINGULAR, buf};
+    int code = 0;
+    std::string msg;
+    if (status.n != status_checked) {
+      const size_t cnt = status.n - status_checked;
+      std::vector<int> st(cnt);
+      HCK(cudaMemcpyAsync(st.data(), status.p + status_checked, cnt * sizeof(int), cudaMemcpyDeviceToHost, s));
+      HCK(cudaStreamSynchronize(s));
+      for (const Pending& P : pending) {
+        for (int64_t i = 0; i < P.cnt && !code; ++i) {
+          const int v = st[(size_t)(P.off - (int64_t)status_checked + i)];
+          if (v != 0) {
+            char buf[256];
+            const char* kind = v == 1 ? "matrix is not positive definite" : "singular pivot";
+            snprintf(buf, sizeof buf, "%s (%s %lld of level %g)", kind, P.what, (long long)i, P.tag);
+            code = v == 1 ? HIFDE_INDEFINITE : HIFDE_SINGULAR;
+            msg = buf;
+          }
         }
+        if (code) break;
       }
+    }
     status_checked = status.n;
     pending.clear();
+    if (real) {  // every rank reaches this point: agree on the outcome
+      agree.reserve(1, s);
+      HCK(cudaMemcpyAsync(agree.p, &code, sizeof(int), cudaMemcpyHostToDevice, s));
+      try {
+        comm_allreduce(comm, agree.p, 1, kI32, kMax, s);
+      } catch (const std::exception& e) {
+        throw Fail{HIFDE_CUDA, e.what()};
+      }
+      int all = 0;
+      HCK(cudaMemcpyAsync(&all, agree.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      HCK(cudaStreamSynchronize(s));
+      if (all && !code) {
+        code = all;
+        msg = "factorization failed on another rank";
+      }
+    }
+    if (code) throw Fail{code, msg};
   }
 
   // -------------------------------------------------------------------------
@@ -975,7 +1186,13 @@ struct Factorizer {
     h_idx.resize((size_t)(idx_base + idx_tot));
     hl.resize((size_t)hl_tot);
     const int64_t fac_base = (int64_t)F->fac.bump(fac_tot, s);
+    fac_grown((size_t)fac_base, fac_tot);
+    const size_t bv_old = bvals.n;
     const int64_t bv_base = bv_tot ? (int64_t)bvals.bump(bv_tot, s) : 0;
+    bvals_grown(bv_old);
+    own_.assign((size_t)nt, 0);
+    if (sharded())
+      for (int64_t t = 0; t < nt; ++t) own_[(size_t)t] = owner_of(gr.begin(t));
 #pragma omp parallel for num_threads(nthr) schedule(dynamic, 64)
     for (int64_t t = 0; t < nt; ++t) {
       ElimTask& T = tasks[(size_t)t];
@@ -1019,7 +1236,7 @@ struct Factorizer {
       for (int64_t t = 0; t < nt; ++t) {
         const ElimTask& T = tasks[(size_t)t];
         for (int j = 0; j < T.nblk; ++j) blk_alive[(size_t)hl[(size_t)(T.blk_off + j)]] = 0;
-        if (T.nq > 0) newid[(size_t)t] = new_block(T.dofs_off + T.nc, T.nq, T.U_off);
+        if (T.nq > 0) newid[(size_t)t] = new_block(T.dofs_off + T.nc, T.nq, T.U_off, own_[(size_t)t]);
         nadd += (size_t)T.nq;
       }
       member.ensure_room(nadd);
@@ -1055,11 +1272,32 @@ struct Factorizer {
     L.t_upd = now_s() - tp;
     L.lap("blocks");
     tp = now_s();
-    // split into the shared-memory path and the blocked large-front path
+    // blocks this process's groups consume from other ranks
+    if (sharded()) {
+      std::vector<int64_t> bptr((size_t)nt);
+      std::vector<int32_t> bcnt((size_t)nt);
+      for (int64_t t = 0; t < nt; ++t) {
+        bptr[(size_t)t] = tasks[(size_t)t].blk_off;
+        bcnt[(size_t)t] = tasks[(size_t)t].nblk;
+      }
+      exchange_blocks(nt, own_.data(), bptr.data(), bcnt.data(), hl.data());
+    }
+    upload_idx();
+    upload_blocks();
+    lists.reserve(std::max<size_t>(hl.size(), 1), s);
+    lists.n = hl.size();
+    lists.upload(hl.data(), 0, hl.size(), s);
+    HCK(cudaEventCreate(&L.ev0));
+    HCK(cudaEventCreate(&L.ev1));
+    HCK(cudaEventRecord(L.ev0, s));
+    // the groups of rank r (all of them unsharded): shared-memory path and
+    // blocked large-front path
+    auto launch_rank = [&](int r) {
     std::vector<ElimTask> small, big;
     std::vector<int4> tiles, asm_work;
     int max_big_nc = 0;
     for (int64_t t = 0; t < nt; ++t) {
+      if (sharded() && own_[(size_t)t] != r) continue;
       const ElimTask& T = tasks[(size_t)t];
       if (!is_big[(size_t)t]) { small.push_back(T); continue; }
       const int bi = (int)big.size();
@@ -1102,11 +1340,6 @@ struct Factorizer {
     }
     HTRACE("  host updates done (%zu small / %zu big / %zu tiles)", small.size(), big.size(), tiles.size());
     // uploads
-    upload_idx();
-    upload_blocks();
-    lists.reserve(std::max<size_t>(hl.size(), 1), s);
-    lists.n = hl.size();
-    lists.upload(hl.data(), 0, hl.size(), s);
     DBuf<ElimTask> d_small, d_big;
     DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd;
     DBuf<int32_t> d_pcells;
@@ -1136,10 +1369,7 @@ struct Factorizer {
     const char* what = is_top ? "top block" : "cell";
     pending.push_back({st_small, (int64_t)small.size(), tag, what});
     pending.push_back({st_big, (int64_t)big.size(), tag, what});
-    Arenas A = arenas();
-    HCK(cudaEventCreate(&L.ev0));
-    HCK(cudaEventCreate(&L.ev1));
-    HCK(cudaEventRecord(L.ev0, s));
+    Arenas A = arenas_for(r);
     if (!small.empty()) {
       A.status = status.p + st_small;
       launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= 64 ? 128 : 256, s);
@@ -1166,15 +1396,6 @@ struct Factorizer {
       launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
       g_launches += 1 + inv.launch(d_big.p, A, s);
     }
-    HCK(cudaEventRecord(L.ev1, s));
-    HCK(cudaGetLastError());
-    HTRACE("  launched");
-    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
-    // (the kernels retire the cells in the device active mask themselves)
-    L.t_launch = now_s() - tp;
-    L.lap("launch");
-    tp = now_s();
-    if (is_top) check_status();
     d_small.release(s);
     d_big.release(s);
     d_tiles.release(s);
@@ -1185,6 +1406,19 @@ struct Factorizer {
     d_pcells.release(s);
     d_dmin.release(s);
     d_scale.release(s);
+    };
+    for (int r = rank_lo(); r < rank_hi(); ++r) launch_rank(r);
+    HCK(cudaEventRecord(L.ev1, s));
+    HCK(cudaGetLastError());
+    HTRACE("  launched");
+    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
+    // (the kernels retire the cells in the device active mask themselves;
+    // real ranks merge the masks)
+    union_state(nullptr, nullptr, 0, 0);
+    L.t_launch = now_s() - tp;
+    L.lap("launch");
+    tp = now_s();
+    if (is_top) check_status();
     // solve-side reduction structure for the shared neighbour DOFs
     if (!is_top) build_reduction((size_t)(&L - F->levels.data()), L);
     L.t_sync = now_s() - tp;
@@ -1387,7 +1621,10 @@ struct Factorizer {
     preds.resize((size_t)pred_ptr[(size_t)nt]);
     const int64_t scr_base = scr_tot ? (int64_t)scratch.bump(scr_tot, s) : 0;
     const int64_t fac_base = (int64_t)F->fac.bump(fac_tot, s);
+    fac_grown((size_t)fac_base, fac_tot);
+    const size_t bv_old = bvals.n;
     const int64_t bv_base = (int64_t)bvals.bump(bv_tot, s);
+    bvals_grown(bv_old);
     // (3) fill, in parallel
 #pragma omp parallel for num_threads(nthr) schedule(dynamic, 64)
     for (int64_t t = 0; t < nt; ++t) {
@@ -1442,7 +1679,22 @@ struct Factorizer {
     L.t_sym = tp - t_begin;
     bool any_huge = false;
     for (const SkelTask& T : tasks) any_huge |= T.mode == 2;
-    if (exact && !any_huge && nt > 1 && opt.order_mode != HIFDE_ORDER_SNAPSHOT) {
+    const bool one_launch = exact && !any_huge && nt > 1 && opt.order_mode != HIFDE_ORDER_SNAPSHOT;
+    // owners: the one-launch exact order runs on rank 0 (its groups wait on
+    // one another); otherwise groups go to their subdomain's rank
+    own_.assign((size_t)nt, 0);
+    if (sharded() && !one_launch)
+      for (int64_t t = 0; t < nt; ++t) own_[(size_t)t] = owner_of(gr.begin(t));
+    if (sharded()) {
+      std::vector<int64_t> bptr((size_t)nt);
+      std::vector<int32_t> bcnt((size_t)nt);
+      for (int64_t t = 0; t < nt; ++t) {
+        bptr[(size_t)t] = tasks[(size_t)t].blk_off;
+        bcnt[(size_t)t] = tasks[(size_t)t].nblk;
+      }
+      exchange_blocks(nt, own_.data(), bptr.data(), bcnt.data(), hl.data());
+    }
+    if (one_launch) {
       // one launch, per-group dependencies (skel_ordered_kernel)
       upload_idx();
       upload_blocks();
@@ -1466,7 +1718,9 @@ struct Factorizer {
       pending.push_back({st_off, nt, tag, "group"});
       kout.n = 0;
       kout.bump((size_t)nt, s);
-      Arenas A = arenas();
+      if (real) HCK(cudaMemsetAsync(kout.p, 0, (size_t)nt * sizeof(int32_t), s));
+      const bool run_here = rank_lo() == 0;  // rank 0 owns the whole level
+      Arenas A = arenas_for(0);
       A.status = status.p + st_off;
       // large groups: a CTA cluster per group (skel_cluster_kernel), 4 or 2 CTAs
       // each, when every group's column slice fits and every group gets a
@@ -1515,9 +1769,12 @@ struct Factorizer {
         HCK(cudaEventCreate(&L.ev0));
         HCK(cudaEventCreate(&L.ev1));
         HCK(cudaEventRecord(L.ev0, s));
-        HCK(launch_skel_cluster(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem_cl, ncls, cs, s));
-        ++g_launches;
+        if (run_here) {
+          HCK(launch_skel_cluster(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem_cl, ncls, cs, s));
+          ++g_launches;
+        }
         HCK(cudaEventRecord(L.ev1, s));
+        union_level(tasks, nt);
         L.t_launch = now_s() - tp;
         tp = now_s();
         finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
@@ -1540,9 +1797,12 @@ struct Factorizer {
         dtl.reserve((size_t)nt * 16, s);
         A.tlog = dtl.p;
       }
-      HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
-      ++g_launches;
+      if (run_here) {
+        HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
+        ++g_launches;
+      }
       HCK(cudaEventRecord(L.ev1, s));
+      union_level(tasks, nt);
       if (tlog_dir) {  // debug: per-group timestamps + the predecessor CSR
         std::vector<unsigned long long> h((size_t)nt * 16);
         HCK(cudaMemcpyAsync(h.data(), dtl.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
@@ -1571,17 +1831,23 @@ struct Factorizer {
     // order tasks by batch (stable keeps the reference order inside a batch)
     std::vector<int64_t> order((size_t)nt);
     for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return batch[(size_t)a] < batch[(size_t)b]; });
-    // per batch: small groups (one CTA each) and large groups (cluster path)
+    // (then by owner: a batch's groups are independent, each rank takes a
+    // contiguous range)
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      if (batch[(size_t)a] != batch[(size_t)b]) return batch[(size_t)a] < batch[(size_t)b];
+      return own_[(size_t)a] < own_[(size_t)b];
+    });
+    const int PP = sharded() ? P : 1;
+    // per batch and rank: small groups (one CTA each) and large groups
+    // (cluster path); ranges indexed by b * PP + r
     std::vector<SkelTask> sorted, hsk;        // small tasks; SkelTask view of large ones
     std::vector<SkelBigTask> huge;
-    std::vector<int64_t> bs((size_t)nbatch + 1, 0), bh((size_t)nbatch + 1, 0);
+    std::vector<int64_t> bs((size_t)nbatch * PP + 1, 0), bh((size_t)nbatch * PP + 1, 0);
     int huge_max_nq = 0, huge_max_nf = 0, huge_max_nb = 0;
     iscratch.n = 0;
     for (int64_t i = 0; i < nt; ++i) {
       const SkelTask& T = tasks[(size_t)order[(size_t)i]];
-      const int b = batch[(size_t)order[(size_t)i]];
+      const int b = batch[(size_t)order[(size_t)i]] * PP + own_[(size_t)order[(size_t)i]];
       if (T.mode != 2) {
         sorted.push_back(T);
         bs[(size_t)b + 1]++;
@@ -1610,7 +1876,7 @@ struct Factorizer {
       huge_max_nf = std::max(huge_max_nf, T.nc + T.nq);
       huge_max_nb = std::max(huge_max_nb, T.maxnb);
     }
-    for (int b = 0; b < nbatch; ++b) {
+    for (int b = 0; b < nbatch * PP; ++b) {
       bs[(size_t)b + 1] += bs[(size_t)b];
       bh[(size_t)b + 1] += bh[(size_t)b];
     }
@@ -1642,22 +1908,48 @@ struct Factorizer {
     }
     kout.n = 0;
     kout.bump((size_t)nt, s);
-    Arenas A = arenas();
-    A.status = status.p + st_off;
-    Arenas AH = A;
-    AH.status = status.p + st_huge;
+    if (real) HCK(cudaMemsetAsync(kout.p, 0, (size_t)nt * sizeof(int32_t), s));
+    auto arenas_r = [&](int r, bool big_status) {
+      Arenas A = arenas_for(r);
+      A.status = status.p + (big_status ? st_huge : st_off);
+      return A;
+    };
+    // real ranks: merge the ranks, sk/rd lists and active masks of a batch's
+    // groups [lo, hi) of `v` (all ranks' ranges)
+    auto merge = [&](const auto& v, int64_t lo, int64_t hi) {
+      if (!real || hi <= lo) return;
+      std::vector<int64_t> off;
+      std::vector<int> len;
+      for (int64_t i = lo; i < hi; ++i) {
+        off.push_back(v[(size_t)i].out_off);
+        len.push_back(v[(size_t)i].nc);
+      }
+      union_state(off.data(), len.data(), (int)off.size(), nt);
+    };
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
     for (int b = 0; b < nbatch; ++b) {
-      const int64_t lo = bs[(size_t)b], hi = bs[(size_t)b + 1];
-      if (hi > lo) {
-        launch_skel(dt.p + lo, (int)(hi - lo), A, opt.eps, smem, (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
-        launch_apply_rd(dt.p + lo, (int)(hi - lo), A, s);
-        g_launches += 2;
+      const size_t b0 = (size_t)b * PP, b1 = (size_t)(b + 1) * PP;
+      for (int r = rank_lo(); r < rank_hi(); ++r) {
+        const int64_t lo = bs[b0 + r], hi = bs[b0 + r + 1];
+        if (hi > lo) {
+          launch_skel(dt.p + lo, (int)(hi - lo), arenas_r(r, false), opt.eps, smem,
+                      (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
+          ++g_launches;
+        }
       }
-      const int64_t hlo = bh[(size_t)b], hhi = bh[(size_t)b + 1];
-      if (hhi > hlo) {
+      for (int r = rank_lo(); r < rank_hi(); ++r) {
+        const int64_t lo = bs[b0 + r], hi = bs[b0 + r + 1];
+        if (hi > lo) {
+          launch_apply_rd(dt.p + lo, (int)(hi - lo), arenas_r(r, false), s);
+          ++g_launches;
+        }
+      }
+      merge(sorted, bs[b0], bs[b1]);
+      for (int r = rank_lo(); r < rank_hi(); ++r) {
+        const int64_t hlo = bh[b0 + r], hhi = bh[b0 + r + 1];
+        if (hhi <= hlo) continue;
         static const bool shapes = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: per-batch shapes and time
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (shapes) {
@@ -1665,8 +1957,8 @@ struct Factorizer {
           HCK(cudaEventCreate(&e1));
           HCK(cudaEventRecord(e0, s));
         }
-        launch_huge_batch(huge, hlo, hhi, dhuge.p, dth.p, dinner.p, ddmin.p, dscale.p, A, AH, huge_max_nq,
-                          huge_max_nf, huge_max_nb);
+        launch_huge_batch(huge, hlo, hhi, dhuge.p, dinner.p, ddmin.p, dscale.p, arenas_r(r, false),
+                          arenas_r(r, true), huge_max_nq, huge_max_nf, huge_max_nb);
         if (shapes) {
           HCK(cudaEventRecord(e1, s));
           std::vector<int32_t> kk((size_t)nt);
@@ -1687,6 +1979,15 @@ struct Factorizer {
           cudaEventDestroy(e1);
         }
       }
+      // the large groups retire their rd once every rank's pipeline is done
+      for (int r = rank_lo(); r < rank_hi(); ++r) {
+        const int64_t hlo = bh[b0 + r], hhi = bh[b0 + r + 1];
+        if (hhi > hlo) {
+          launch_apply_rd(dth.p + hlo, (int)(hhi - hlo), arenas_r(r, false), s);
+          ++g_launches;
+        }
+      }
+      merge(huge, bh[b0], bh[b1]);
       if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  batch %d done", b); }
     }
     HCK(cudaEventRecord(L.ev1, s));
@@ -1734,7 +2035,7 @@ struct Factorizer {
       L.nred += r;
       for (int i = kk; i < T.nc; ++i) active[(size_t)out[i]] = 0;
       if (r > 0 && kk > 0) {
-        newid[(size_t)t] = new_block(T.out_off, kk, T.delta_off);
+        newid[(size_t)t] = new_block(T.out_off, kk, T.delta_off, own_[(size_t)t]);
         nadd += (size_t)kk;
       }
       {
@@ -1796,7 +2097,7 @@ struct Factorizer {
 
   // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
   void launch_huge_batch(const std::vector<SkelBigTask>& huge, int64_t lo, int64_t hi, const SkelBigTask* d_all,
-                         const SkelTask* d_skv, ElimTask* d_inner_all, double* d_dmin_all, double* d_scale_all,
+                         ElimTask* d_inner_all, double* d_dmin_all, double* d_scale_all,
                          const Arenas& A, const Arenas& AH_all, int max_nq, int max_nf, int max_nb) {
     const int n = (int)(hi - lo);
     const SkelBigTask* dtk = d_all + lo;
@@ -1951,8 +2252,7 @@ struct Factorizer {
     }
     g_launches += inv.launch(inner, AH, s);
     if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("    huge: inverse done (%zu loc / %zu diag / %zu tiles)", inv.loc.size(), inv.diag.size(), inv.tiles.size()); }
-    launch_apply_rd(d_skv + lo, n, A, s);
-    g_launches += 3;
+    g_launches += 2;
     HCK(cudaGetLastError());
     if (split_t) {
       HCK(cudaEventRecord(pe[3], s));
@@ -2137,9 +2437,21 @@ struct Factorizer {
   void run(const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz) {
     const double t0 = now_s();
     N = g.ndof();
+    comm = opt.comm;
+    if (comm && comm->P > 1) {
+      P = comm->P;
+      me = comm->rank;
+      emu = comm->emulated;
+      real = !emu;
+      geom = shard_geom(P, g.dim, g.n);
+      ledger.reset(P);
+      if (emu) lanes.resize((size_t)P - 1);
+    } else {
+      comm = nullptr;
+    }
     HTRACE("factor start N=%lld", (long long)N);
-    LevelRec& P = prof;  // setup / finish sub-phases (HIFDE_PROFILE)
-    P.lap(nullptr);
+    LevelRec& PR = prof;  // setup / finish sub-phases (HIFDE_PROFILE)
+    PR.lap(nullptr);
     pinned_stage().begin(s);
     g_stage = &pinned_stage();
     struct StageOff {
@@ -2188,7 +2500,7 @@ struct Factorizer {
         a0_err = e;
       });
     }
-    P.lap("A0");
+    PR.lap("A0");
     active.resize((size_t)N);
     act.resize((size_t)N);
 #pragma omp parallel for schedule(static) if (N > (1 << 16))
@@ -2221,7 +2533,7 @@ struct Factorizer {
           x.stamp = 0;
         }
     }
-    P.lap("host-state");
+    PR.lap("host-state");
     {
       HostCache& hc = host_cache();
       const bool hint = hc.variant == opt.variant;
@@ -2234,7 +2546,7 @@ struct Factorizer {
       if (hint && hc.hint_meta) meta.h.reserve(hc.hint_meta + hc.hint_meta / 8);
     }
 
-    P.lap("reserve");
+    PR.lap("reserve");
     const int Lv = g.nlevels;
     F->levels.reserve((size_t)3 * std::max(Lv, 1) + 4);  // stable LevelRec addresses for the helper
     const double t_setup = now_s() - t0;
@@ -2329,20 +2641,29 @@ struct Factorizer {
       L.kind = 2;
       record_trace(L, tl);
     }
-    P.lap(nullptr);
+    PR.lap(nullptr);
+    if (real) {  // every record lives on its owner, zeros elsewhere: sum
+      try {
+        comm_allreduce(comm, F->fac.p, F->fac.n, kF64, kSum, s);
+      } catch (const std::exception& e) {
+        throw Fail{HIFDE_CUDA, e.what()};
+      }
+    }
+    F->nranks = sharded() ? P : 1;
+    F->xfer_bytes = xfer_bytes;
     helper.drain();
     build_solve_plan(F->levels.back());  // the terminal block
     finish_reductions();
-    P.lap("reductions");
+    PR.lap("reductions");
     // solve metadata to the device: small records one CTA each, large ones as
     // tiled product phases (built level by level on the helper thread)
     meta_bytes = meta.h.size();
     F->meta = meta.commit(s, [&](void* d, const void* h, size_t n) {
       if (!pinned_stage().copy(d, h, n)) HCK(cudaMemcpyAsync(d, h, n, cudaMemcpyHostToDevice, s));
     });
-    P.lap("solve-plan");
+    PR.lap("solve-plan");
     HCK(cudaStreamSynchronize(s));
-    P.lap("sync");
+    PR.lap("sync");
     for (auto& L : F->levels) {
       if (L.ev0 && L.ev1) {
         float ms = 0.f;
@@ -2362,6 +2683,12 @@ struct Factorizer {
       hc.hint_meta = meta_bytes;
     }
     bvals.release(s);
+    for (auto& l : lanes) l.release(s);
+    for (auto* d : {&xsend, &xrecv}) d->release(s);
+    xseg.release(s);
+    xiseg.release(s);
+    xi32.release(s);
+    agree.release(s);
     scratch.release(s);
     lists.release(s);
     status.release(s);
@@ -2377,11 +2704,11 @@ struct Factorizer {
     }
     cudaFreeAsync(d_active, s);
     HCK(cudaStreamSynchronize(s));
-    P.lap("release");
+    PR.lap("release");
     F->t_f = now_s() - t0;
     if (getenv("HIFDE_PROFILE")) {
       fprintf(stderr, "[hifde] setup/finish:");
-      for (const auto& p : P.sub) fprintf(stderr, " %s %.3f", p.first, p.second * 1e3);
+      for (const auto& p : PR.sub) fprintf(stderr, " %s %.3f", p.first, p.second * 1e3);
       fprintf(stderr, "\n");
       fprintf(stderr, "[hifde] factor %.3f ms (setup %.3f ms)\n", F->t_f * 1e3, t_setup * 1e3);
       for (const auto& L : F->levels)
@@ -2759,6 +3086,10 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
     g_err = "indefinite (Bunch-Kaufman) factorization is not implemented on the GPU path";
     return HIFDE_BADARG;
   }
+  if (opt->comm && !opt->comm->emulated && opt->comm->P > 1 && opt->comm->device != opt->device) {
+    g_err = "options.device differs from the communicator's device";
+    return HIFDE_BADARG;
+  }
   GridDesc g;
   g.dim = dim;
   g.n = n_grid;
@@ -2979,6 +3310,8 @@ int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
   info->variant = f->variant;
   info->fac_len = (int64_t)f->fac.n;
   info->idx_len = (int64_t)f->idx.n;
+  info->nranks = f->nranks;
+  info->xfer_bytes = f->xfer_bytes;
   return HIFDE_OK;
 }
 

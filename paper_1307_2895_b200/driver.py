@@ -99,6 +99,8 @@ class GeneralizedLDL:
             "factor_gflop": sum(d["gflop"] for d in self.level_info),
             "factor_gbytes": sum(d["gbytes"] for d in self.level_info),
             "launches": int(lib.hifde_last_launch_count()),
+            "nranks": int(info.nranks),
+            "xfer_bytes": int(info.xfer_bytes),
         }
 
     @property
@@ -162,8 +164,8 @@ class GeneralizedLDL:
 
 
 def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
-            order: str = "auto", exact_max_batches: int = 64, device: int = 0,
-            stream: Optional[int] = None) -> GeneralizedLDL:
+            order: str = "auto", exact_max_batches: int = 64, device: Optional[int] = None,
+            stream: Optional[int] = None, comm=None) -> GeneralizedLDL:
     lib = L.load()
     if not spd:
         raise NotImplementedError("indefinite (Bunch-Kaufman) mode is outside the GPU hot path")
@@ -178,9 +180,12 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     opt.eps = float(eps)
     opt.order_mode = L.ORDER[order]
     opt.exact_max_batches = int(exact_max_batches)
+    if device is None:
+        device = comm.device if comm is not None else 0
     opt.device = int(device)
     opt.verify = int(bool(verify))
     opt.stream = stream
+    opt.comm = comm.handle if comm is not None else None  # distributed.Comm: sharded sweep
     h = C.c_void_p()
     code = lib.hifde_factor(indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, csr.shape[0],
                             int(grid.dim), int(grid.n), int(grid.m), int(grid.nlevels),
