@@ -14,8 +14,14 @@ One step = factor_hifde of the matrix + apply_inverse of the 16-RHS block.
 `--impl reference` times the CPU oracle port of the reference algorithm
 (oracle/hifde_oracle.py) on this host on the same workload.
 
-Multi-GPU (torchrun, --gpus N): every rank factors and solves its own
-independently seeded instance (replicas; weak scaling) -- see DESIGN.md 8(e).
+Multi-GPU (torchrun, --gpus N): by default every rank factors and solves its
+own independently seeded instance of config 2 (replicas; weak scaling).
+`--shard --config {2,3,4,5}` instead factors ONE instance of that BASELINE
+config sharded over the N ranks (spatial group owners, NCCL block exchange,
+exact-order coarse levels on rank 0; strong scaling) and splits the
+right-hand sides over the ranks -- DESIGN.md (e).  `--emulate P` runs the
+sharded code path with P virtual ranks on one GPU (a correctness check; its
+timing is not a multi-GPU number).
 """
 
 from __future__ import annotations
@@ -271,6 +277,140 @@ def run_gpu(args, world, rank, local):
         dist.destroy_process_group()
 
 
+def run_sharded(args, world, rank, local):
+    """One BASELINE config sharded over the ranks (strong scaling)."""
+    import ctypes as C
+
+    import torch
+    import paper_1307_2895_b200 as H
+    from paper_1307_2895_b200 import _lib
+    from paper_1307_2895_b200 import distributed as D
+
+    dist = None
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = D.init_comm(device=local)
+    else:
+        comm = D.emulated_comm(args.emulate, local) if args.emulate > 1 else None
+    nr = comm.nranks if comm is not None else 1
+    stream = torch.cuda.Stream(device=dev)
+    g, a, eps, variant, nrhs = H.baseline_problem(args.config)
+    N = g.ndof
+    cols = D.rhs_columns(nrhs, world, rank)
+    nloc = cols.stop - cols.start
+    b_host = np.random.default_rng(1).standard_normal((N, nrhs))
+    b_loc = np.ascontiguousarray(b_host[:, cols])
+    indptr_d = torch.from_numpy(a.indptr.astype(np.int64)).to(dev)
+    indices_d = torch.from_numpy(a.indices.astype(np.int32)).to(dev)
+    data_d = torch.from_numpy(a.data.astype(np.float64)).to(dev)
+    b_d = torch.from_numpy(b_loc).to(dev)
+    x_d = torch.empty_like(b_d)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    vcode = _lib.VARIANT_HIFDE if variant == "hifde" else _lib.VARIANT_HIFDE3X
+
+    def factor_device():
+        opt = _lib.Options()
+        lib.hifde_default_options(C.byref(opt), vcode)
+        opt.eps = eps
+        opt.device = local
+        opt.input_on_device = 1
+        opt.stream = stream.cuda_stream
+        opt.comm = comm.handle if comm is not None else None
+        h = C.c_void_p()
+        code = lib.hifde_factor(indptr_d.data_ptr(), indices_d.data_ptr(), data_d.data_ptr(), N,
+                                g.dim, g.n, g.m, g.nlevels, C.byref(opt), C.byref(h))
+        if code:
+            raise RuntimeError(lib.hifde_last_error().decode())
+        return H.GeneralizedLDL(h.value, lib, True), lib.hifde_last_launch_count()
+
+    fac = H.factor_hifde if variant == "hifde" else H.factor_hifde3x
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            f, _ = factor_device()
+            if nloc:
+                f.apply_inverse_device(b_d.data_ptr(), x_d.data_ptr(), nloc, stream.cuda_stream)
+            stream.synchronize()
+        x = x_d.cpu().numpy()
+        resid = float(np.max(np.linalg.norm(a @ x - b_loc, axis=0) / np.linalg.norm(b_loc, axis=0))) if nloc else 0.0
+        skel = f.metrics["skeleton_counts"]
+        xfer = f.metrics["xfer_bytes"]
+        f.close()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        times, tfs, launches = [], [], 0
+        with ClockSampler(local) as clk:
+            for _ in range(args.steps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e2 = torch.cuda.Event(enable_timing=True)
+                stream.wait_stream(torch.cuda.current_stream())
+                e0.record(stream)
+                f, nl = factor_device()
+                e1.record(stream)
+                if nloc:
+                    f.apply_inverse_device(b_d.data_ptr(), x_d.data_ptr(), nloc, stream.cuda_stream)
+                    nl += lib.hifde_last_launch_count()
+                launches += nl
+                e2.record(stream)
+                e2.synchronize()
+                times.append(e0.elapsed_time(e2) / 1e3)
+                tfs.append(e0.elapsed_time(e1) / 1e3)
+                level_info = f.level_info
+                f.close()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t_step, t_f = float(np.mean(times)), float(np.mean(tfs))
+        e2e_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fe = fac(a, g, eps, stream=stream.cuda_stream, device=local, comm=comm)
+            if nloc:
+                fe.apply_inverse(b_loc)
+            e2e_times.append(time.perf_counter() - t0)
+            fe.close()
+        t_e2e = float(np.median(e2e_times))
+    t_s = t_step - t_f
+    if dist:
+        tt = torch.tensor([t_step, t_e2e, t_f, t_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_e2e, t_f, t_s = [float(v) for v in tt.cpu()]
+    pk, pk_kind = peaks()
+    h2d = a.indptr.size * 8 + a.indices.size * 4 + a.data.size * 8 + b_loc.nbytes
+    line = {
+        "metric": METRIC, "value": N / t_step, "unit": "unknowns/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded BASELINE cfg{args.config} inputs)",
+        "config": {"workload": f"cfg{args.config}: {variant}, N={N}, eps={eps}, {nrhs} RHS; one instance "
+                               f"sharded over {nr} rank(s){' (emulated on one GPU)' if comm is not None and comm.emulated else ''}; "
+                               "step = factor + this rank's RHS columns",
+                   "parallelism": f"shard x{nr}", "l2": "flushed between timed steps (256 MiB write)"},
+        "factor_ms": t_f * 1e3, "solve_ms": t_s * 1e3,
+        "factor_unknowns_per_s": N / t_f,
+        "e2e": {"value": N / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(b_loc.nbytes)},
+        "gpu_launches": int(launches), "clocks": clk.summary(), "resid": resid,
+        "skeleton_counts": [c for _, c in skel], "xfer_bytes_rank0": int(xfer),
+    }
+    line["roofline"] = roofline(level_info, pk, pk_kind, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+
+
 def roofline(level_info, pk, pk_kind, args):
     """HBM roofline of the dominant kernel launch.
 
@@ -325,10 +465,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="one instance sharded over the ranks")
+    ap.add_argument("--config", type=int, default=CONFIG, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--emulate", type=int, default=1, help="virtual ranks on one GPU (--shard, N=1)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
         cpu_reference(args, world, rank)
+        return
+    if args.shard:
+        run_sharded(args, world, rank, local)
         return
     run_gpu(args, world, rank, local)
 
