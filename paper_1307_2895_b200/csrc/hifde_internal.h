@@ -145,6 +145,18 @@ cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64
 void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                              size_t smem, cudaStream_t s);
 int cpqr_coop_capacity(size_t smem);
+// Gram path of the large-group ID (kernels_skelbig.cu): G = Mq^T Mq tiles,
+// then a cooperative pivoted Cholesky of G with the CPQR's outputs
+constexpr double kGramMinEps = 1e-4;
+constexpr double kPromoteWork = 4e6;  // nq nc^2 above which a one-CTA group joins the pipeline
+constexpr int kGramRows = 1024;  // rows per split of a Gram tile
+void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, const int4* tiles, int ntiles,
+                         double* part, const Arenas& A, cudaStream_t s);
+size_t pchol_smem(int nc, int G);
+int pchol_min_ctas(int nc);
+int pchol_coop_capacity(size_t smem);
+cudaError_t launch_pchol_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
+                              unsigned int* d_bar, size_t smem, const Arenas& A, double eps, cudaStream_t s);
 cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
                                 cudaStream_t s);
 cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,

@@ -106,7 +106,7 @@ __device__ __forceinline__ void group_barrier(unsigned int* ctr, unsigned int G,
 
 // scratch layout of one large group (doubles)
 struct BigWs {
-  double *Acc, *Mq, *Tp, *vn1, *vn2, *rdiag, *cand;
+  double *Acc, *Mq, *Tp, *vn1, *vn2, *rdiag, *cand, *G;
   int32_t *piv, *skl, *sko, *rdl;
 };
 __device__ __forceinline__ BigWs big_ws(const SkelBigTask& t, const Arenas& A) {
@@ -119,6 +119,7 @@ __device__ __forceinline__ BigWs big_ws(const SkelBigTask& t, const Arenas& A) {
   w.vn2 = w.vn1 + nc;
   w.rdiag = w.vn2 + nc;
   w.cand = w.rdiag + nc;  // 2 x kMaxG x (value, index)
+  w.G = w.cand + 4 * kMaxG + 8;  // Gram matrix Mq^T Mq (nc x nc), the Gram path only
   w.piv = A.iscratch + t.iws_off;
   w.skl = w.piv + nc;
   w.sko = w.skl + nc;
@@ -463,6 +464,249 @@ __global__ void __launch_bounds__(256) cpqr_mc_kernel(const SkelBigTask* __restr
   if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
 }
 
+constexpr int kTT = 64, kTK = 16, kTL = 68;  // DMMA tile kernels: 64 x 64 tiles, K chunks of 16
+
+// ---------------------------------------------------------------------------
+// Gram path of the large-group ID (tolerances eps >= kGramMinEps, tall groups):
+//   skelbig_gram_kernel   G = Mq^T Mq on 64 x 64 DMMA tiles, one pass over Mq
+//   pchol_mc_kernel       pivoted Cholesky of G with the CPQR's rank cut
+// Pivoted Cholesky of G picks, step by step, the column of Mq whose component
+// orthogonal to the columns already chosen is largest: the pivots, the
+// rank cut |R_ii| <= eps |R_00| and R itself (up to row signs, which T =
+// R11^-1 R12 does not see) are those of the column-pivoted QR of Mq, in exact
+// arithmetic.  The Schur diagonal carries an absolute error ~u |G| against a
+// cut at eps^2 |G|, and T = G11^-1 G12 loses u cond(G11) ~ u / eps^2, so the
+// path is used only when eps^3 >> u.  Traffic: one read of Mq plus
+// O(nc k) per step against O(nq nc) per step for the CPQR on Mq itself.
+// ---------------------------------------------------------------------------
+// Work item int4 {task, a0, b0, split}: rows [split * kGramRows, +kGramRows)
+// of the 64 x 64 tile (a0, b0), a0 <= b0.  One split: G directly; several:
+// the tile's partial goes to part[item] and skelbig_gram_reduce_kernel sums
+// the splits in order (deterministic).  Rows are staged 32 at a time with the
+// next stage prefetched into registers during the DMMA loop.
+constexpr int kGK = 32;
+__global__ void __launch_bounds__(128) skelbig_gram_kernel(const SkelBigTask* __restrict__ tasks,
+                                                           const int4* __restrict__ work, Arenas A,
+                                                           double* __restrict__ part) {
+  __shared__ double As[kGK][kTL];
+  __shared__ double Bs[kGK][kTL];
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const BigWs w = big_ws(t, A);
+  const int nc = t.nc, nq = t.nq;
+  const int a0 = wk.y, b0 = wk.z;
+  const int r_lo = wk.w * kGramRows, r_hi = min(nq, r_lo + kGramRows);
+  const bool split = nq > kGramRows;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wy = wid >> 1, wx = wid & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  double pa[16], pb[16];
+  // thread e = tid + 128 u stages row (e & 31) of column (e >> 5): a warp reads
+  // 32 consecutive rows of one column (256 contiguous bytes)
+  auto load = [&](int r0) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = (int)threadIdx.x + 128 * u;
+      const int r = r0 + (e & 31), x = e >> 5;
+      pa[u] = (r < r_hi && a0 + x < nc) ? __ldcg(w.Mq + (size_t)r + (size_t)(a0 + x) * nq) : 0.0;
+      pb[u] = (r < r_hi && b0 + x < nc) ? __ldcg(w.Mq + (size_t)r + (size_t)(b0 + x) * nq) : 0.0;
+    }
+  };
+  load(r_lo);
+  for (int r0 = r_lo; r0 < r_hi; r0 += kGK) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = (int)threadIdx.x + 128 * u;
+      As[e & 31][e >> 5] = pa[u];
+      Bs[e & 31][e >> 5] = pb[u];
+    }
+    __syncthreads();
+    if (r0 + kGK < r_hi) load(r0 + kGK);
+#pragma unroll
+    for (int kk = 0; kk < kGK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) af[m] = As[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
+#pragma unroll
+      for (int n = 0; n < 4; ++n) bf[n] = Bs[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ta = wy * 32 + m * 8 + (lane >> 2);
+        const int tb = wx * 32 + n * 8 + 2 * (lane & 3) + h;
+        if (split) {
+          part[(size_t)blockIdx.x * 4096 + ta * 64 + tb] = acc[m][n][h];
+          continue;
+        }
+        const int a = a0 + ta, b = b0 + tb;
+        // G is symmetric: each (a, b), a <= b, written once and mirrored
+        if (a < nc && b < nc && (a0 != b0 || a <= b)) {
+          w.G[(size_t)a + (size_t)b * nc] = acc[m][n][h];
+          w.G[(size_t)b + (size_t)a * nc] = acc[m][n][h];
+        }
+      }
+}
+
+// Sum of a tile's row splits in split order.  Work int4 {task, a0, b0, first
+// item}; the splits of a tile are consecutive work items.
+__global__ void __launch_bounds__(256) skelbig_gram_reduce_kernel(const SkelBigTask* __restrict__ tasks,
+                                                                  const int4* __restrict__ work, Arenas A,
+                                                                  const double* __restrict__ part) {
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const BigWs w = big_ws(t, A);
+  const int nc = t.nc, nq = t.nq;
+  const int ns = (nq + kGramRows - 1) / kGramRows;
+  const int a0 = wk.y, b0 = wk.z;
+  for (int e = threadIdx.x; e < 4096; e += 256) {
+    const int a = a0 + (e >> 6), b = b0 + (e & 63);
+    if (a >= nc || b >= nc || (a0 == b0 && a > b)) continue;
+    double v = 0.0;
+    for (int q = 0; q < ns; ++q) v += part[(size_t)(wk.w + q) * 4096 + e];
+    w.G[(size_t)a + (size_t)b * nc] = v;
+    w.G[(size_t)b + (size_t)a * nc] = v;
+  }
+}
+
+// Cooperative launch; CTAs [gstart[t], gstart[t+1]) serve task t.  CTA rb of
+// CL owns columns rb, rb + CL, ... and keeps their R rows in shared memory;
+// R(i, j) also goes to Mq[i + j nq], the CPQR's output layout (rdiag, piv,
+// kout likewise), so the T / congruence kernels run unchanged.
+__global__ void __launch_bounds__(256) pchol_mc_kernel(const SkelBigTask* __restrict__ tasks, int ntasks,
+                                                       const int* __restrict__ gstart,
+                                                       unsigned int* __restrict__ bar, Arenas A, double eps) {
+  extern __shared__ __align__(16) double psm[];
+  __shared__ double wbest[8];
+  __shared__ int widx[8];
+  __shared__ double sh_best;
+  __shared__ int sh_pvt;
+  int tix = 0;
+  while (tix + 1 < ntasks && (int)blockIdx.x >= gstart[tix + 1]) ++tix;
+  const int rb = (int)blockIdx.x - gstart[tix];
+  const int CL = gstart[tix + 1] - gstart[tix];
+  unsigned int* ctr = bar + tix;
+  unsigned int target = 0;
+  const SkelBigTask t = tasks[tix];
+  const int nc = t.nc, nq = t.nq;
+  const BigWs w = big_ws(t, A);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nown = rb < nc ? (nc - rb + CL - 1) / CL : 0;
+  double* Rs = psm;                       // [nc][nown]: R(l, rb + c CL) at l * nown + c
+  double* rp = Rs + (size_t)nc * nown;    // R(0..i-1, P)
+  double* dd = rp + nc;                   // Schur diagonal of the owned columns (< 0: pivoted)
+  for (int c = threadIdx.x; c < nown; c += 256) {
+    const int j = rb + c * CL;
+    dd[c] = w.G[(size_t)j + (size_t)j * nc];
+  }
+  __syncthreads();
+  auto post = [&](int slot) {  // this CTA's best remaining column -> candidate slot
+    double bv = -1.0;
+    int bi = nc;
+    for (int c = threadIdx.x; c < nown; c += 256)
+      if (dd[c] > bv) { bv = dd[c]; bi = rb + c * CL; }  // ascending j: first max wins
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { wbest[wid] = bv; widx[wid] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b2 = wbest[0];
+      int i2 = widx[0];
+      for (int q = 1; q < 8; ++q)
+        if (wbest[q] > b2 || (wbest[q] == b2 && widx[q] < i2)) { b2 = wbest[q]; i2 = widx[q]; }
+      w.cand[(size_t)(slot * CL + rb) * 2] = b2;
+      w.cand[(size_t)(slot * CL + rb) * 2 + 1] = (double)i2;
+    }
+  };
+  post(0);
+  group_barrier(ctr, (unsigned)CL, target);
+  double thr = 0.0;
+  int k = nc;
+  for (int i = 0; i < nc; ++i) {
+    const int slot = i & 1;
+    {
+      double bv = -1.0;
+      int bi = nc;
+      for (int q = threadIdx.x; q < CL; q += 256) {
+        const double v = __ldcg(&w.cand[(size_t)(slot * CL + q) * 2]);
+        const int ix = (int)__ldcg(&w.cand[(size_t)(slot * CL + q) * 2 + 1]);
+        if (v > bv || (v == bv && ix < bi)) { bv = v; bi = ix; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { wbest[wid] = bv; widx[wid] = bi; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double b2 = wbest[0];
+        int i2 = widx[0];
+        for (int q = 1; q < 8; ++q)
+          if (wbest[q] > b2 || (wbest[q] == b2 && widx[q] < i2)) { b2 = wbest[q]; i2 = widx[q]; }
+        sh_best = b2;
+        sh_pvt = i2;
+      }
+      __syncthreads();
+    }
+    const int P = sh_pvt;
+    const double dP = sh_best;
+    if (i == 0 && !(dP > 0.0)) { k = 0; break; }  // zero block: all redundant
+    const double rii = sqrt(dP > 0.0 ? dP : 0.0);
+    if (i == 0) thr = eps * rii;
+    if (rii <= thr || P >= nc) { k = i; break; }
+    if (rb == 0 && threadIdx.x == 0) {
+      w.rdiag[i] = rii;
+      w.piv[i] = P;
+    }
+    for (int l = threadIdx.x; l < i; l += 256) rp[l] = __ldcg(w.Mq + (size_t)l + (size_t)P * nq);
+    __syncthreads();
+    const double inv = 1.0 / rii;
+    for (int c = wid; c < nown; c += 8) {
+      const int j = rb + c * CL;
+      if (dd[c] < 0.0) continue;  // pivoted earlier
+      if (j == P) {
+        __syncwarp();
+        if (lane == 0) dd[c] = -1.0;
+        continue;
+      }
+      double sacc = 0.0;
+      for (int l = lane; l < i; l += 32) sacc += rp[l] * Rs[(size_t)l * nown + c];
+      sacc = warp_sum(sacc);
+      const double rij = (__ldcg(w.G + (size_t)j + (size_t)P * nc) - sacc) * inv;
+      __syncwarp();
+      if (lane == 0) {
+        Rs[(size_t)i * nown + c] = rij;
+        w.Mq[(size_t)i + (size_t)j * nq] = rij;
+        const double nd = dd[c] - rij * rij;
+        dd[c] = nd > 0.0 ? nd : 0.0;
+      }
+    }
+    __syncthreads();
+    post(slot ^ 1);
+    group_barrier(ctr, (unsigned)CL, target);
+  }
+  if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
+}
+
 // ---------------------------------------------------------------------------
 // sk / rd ascending, output lists, inner elimination task (one CTA per group)
 // ---------------------------------------------------------------------------
@@ -572,7 +816,6 @@ __global__ void __launch_bounds__(128) skelbig_tsolve_kernel(const SkelBigTask* 
     if (i < bw) w.Tp[(size_t)(b0 + i) * r + c] = x[i];
 }
 
-constexpr int kTT = 64, kTK = 16, kTL = 68;
 __global__ void __launch_bounds__(128) skelbig_tupdate_kernel(const SkelBigTask* __restrict__ tasks,
                                                               const int4* __restrict__ work, int b0, Arenas A) {
   __shared__ double As[kTK][kTL];
@@ -790,6 +1033,56 @@ cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_
   void* args[] = {(void*)&tasks, (void*)&ntasks, (void*)&d_gstart, (void*)&d_bar, (void*)&Ac, (void*)&eps};
   return cudaLaunchCooperativeKernel((const void*)cpqr_mc_kernel<false>, dim3((unsigned)nblocks), dim3(256), args,
                                      smem, s);
+}
+
+void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, const int4* tiles, int ntiles,
+                         double* part, const Arenas& A, cudaStream_t s) {
+  if (nwork <= 0) return;
+  skelbig_gram_kernel<<<nwork, 128, 0, s>>>(tasks, work, A, part);
+  if (ntiles > 0) skelbig_gram_reduce_kernel<<<ntiles, 256, 0, s>>>(tasks, tiles, A, part);
+}
+
+size_t pchol_smem(int nc, int G) {
+  const size_t nown = (size_t)((nc + G - 1) / G);
+  return sizeof(double) * ((size_t)nc * nown + (size_t)nc + nown);
+}
+
+int pchol_min_ctas(int nc) {
+  for (int G = 1; G <= kMaxG; ++G)
+    if (pchol_smem(nc, G) <= kSmemCapBytes) return G;
+  return -1;
+}
+
+int pchol_coop_capacity(size_t smem) {
+  static std::vector<std::pair<size_t, int>> cache;
+  for (const auto& c : cache)
+    if (c.first == smem) return c.second;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pchol_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+    attr = true;
+  }
+  int per_sm = 0, dev = 0, nsm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pchol_mc_kernel, 256, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int cap = per_sm * nsm;
+  cache.emplace_back(smem, cap);
+  return cap;
+}
+
+cudaError_t launch_pchol_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
+                              unsigned int* d_bar, size_t smem, const Arenas& A, double eps, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pchol_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
+    attr = true;
+  }
+  Arenas Ac = A;
+  void* args[] = {(void*)&tasks, (void*)&ntasks, (void*)&d_gstart, (void*)&d_bar, (void*)&Ac, (void*)&eps};
+  return cudaLaunchCooperativeKernel((const void*)pchol_mc_kernel, dim3((unsigned)nblocks), dim3(256), args, smem,
+                                     s);
 }
 
 cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,

@@ -721,6 +721,7 @@ struct Factorizer {
   DBuf<double> xsend, xrecv;        // packed block transfers
   DBuf<int64_t> xseg;               // segment tables of the packs
   DBuf<int> agree;                  // status agreement scalar
+  DBuf<double> gpart;               // split-tile partials of the Gram matrices
   std::vector<uint8_t> own_;        // owner rank per group of the current level
   int64_t xfer_blocks = 0, xfer_bytes = 0;  // totals (metrics)
 
@@ -1523,6 +1524,7 @@ struct Factorizer {
       int npred;
     };
     std::vector<Sz> sz((size_t)nt);
+    std::vector<uint8_t> promote((size_t)nt, 0);
     std::vector<std::vector<int32_t>> tpred((size_t)nthreads);
     const int nthr = nt >= 256 ? nthreads : 1;
 #pragma omp parallel num_threads(nthr)
@@ -1574,7 +1576,12 @@ struct Factorizer {
         } else {
           T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
         }
-        z.fac = (size_t)nc * nc + 2 * q4 + (T.mode == 2 ? (size_t)nc * (nc + 1) / 2 + nc : 0);
+        // one-CTA groups the Gram path can take keep room for the large-group
+        // record: they join the large-group pipeline in exact batches
+        // (promote[] below), where a one-CTA launch per batch would be exposed
+        promote[(size_t)t] = (T.mode == 1 || T.mode == 3) && (double)nq * nc * nc >= kPromoteWork && gram_ok(nc, nq);
+        z.fac = (size_t)nc * nc + 2 * q4 +
+                ((T.mode == 2 || promote[(size_t)t]) ? (size_t)nc * (nc + 1) / 2 + nc : 0);
         const size_t p0 = mypred.size();
         for (int i = 0; i < nq; ++i) {
           const int32_t go = group_of[(size_t)q[i]];
@@ -1679,6 +1686,9 @@ struct Factorizer {
     L.t_sym = tp - t_begin;
     bool any_huge = false;
     for (const SkelTask& T : tasks) any_huge |= T.mode == 2;
+    if (exact && nbatch > 1 && any_huge)
+      for (int64_t t = 0; t < nt; ++t)
+        if (promote[(size_t)t]) tasks[(size_t)t].mode = 2;
     const bool one_launch = exact && !any_huge && nt > 1 && opt.order_mode != HIFDE_ORDER_SNAPSHOT;
     // owners: the one-launch exact order runs on rank 0 (its groups wait on
     // one another); otherwise groups go to their subdomain's rank
@@ -1862,7 +1872,8 @@ struct Factorizer {
       H.dofs_off = T.dofs_off;
       H.blk_off = T.blk_off;
       const size_t nc = (size_t)T.nc, nq = (size_t)T.nq;
-      H.ws_off = (int64_t)scratch.bump(nc * nc + nq * nc + (nc * nc / 4 + nc) + 3 * nc + 4 * kMaxG + 8, s);
+      H.ws_off = (int64_t)scratch.bump(nc * nc + nq * nc + (nc * nc / 4 + nc) + 3 * nc + 4 * kMaxG + 8 +
+                                           (gram_ok(T.nc, T.nq) ? nc * nc : 0), s);
       H.iws_off = (int64_t)iscratch.bump(4 * nc + 4, s);
       H.rec_off = T.rec_off;
       H.delta_off = T.delta_off;
@@ -2095,6 +2106,13 @@ struct Factorizer {
     L.lap("retire");
   }
 
+  // Large groups whose ID goes through the Gram matrix (kernels_skelbig.cu):
+  // loose tolerances only (eps^3 >> u), tall fronts, R columns in shared memory
+  bool gram_ok(int nc, int nq) const {
+    static const bool off = getenv("HIFDE_NO_GRAM") != nullptr;
+    return !off && opt.eps >= kGramMinEps && nq >= 2 * nc && nc <= 1024 && pchol_min_ctas(nc) > 0;
+  }
+
   // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
   void launch_huge_batch(const std::vector<SkelBigTask>& huge, int64_t lo, int64_t hi, const SkelBigTask* d_all,
                          ElimTask* d_inner_all, double* d_dmin_all, double* d_scale_all,
@@ -2187,7 +2205,70 @@ struct Factorizer {
     launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
     if (split_t) HCK(cudaEventRecord(pe[1], s));
     static const int cl_min = getenv("HIFDE_CPQR_CLUSTER_MIN") ? atoi(getenv("HIFDE_CPQR_CLUSTER_MIN")) : 1 << 30;
-    if (n >= cl_min) {
+    bool gram = true;
+    for (int i = 0; i < n && gram; ++i) gram = gram_ok(huge[(size_t)(lo + i)].nc, huge[(size_t)(lo + i)].nq);
+    if (gram) {
+      // G = Mq^T Mq (DMMA tiles), then pivoted Cholesky of G: cooperative,
+      // CTAs per group in proportion to nc^2, at least what keeps its R
+      // columns in shared memory; groups beyond one launch's residency go to
+      // further launches
+      std::vector<int4> wg, wr;  // split tiles; tiles to reduce (several splits)
+      for (int i = 0; i < n; ++i) {
+        const int nc = huge[(size_t)(lo + i)].nc, nq = huge[(size_t)(lo + i)].nq;
+        const int ns = (nq + kGramRows - 1) / kGramRows;
+        for (int a0 = 0; a0 < nc; a0 += 64)
+          for (int b0 = a0; b0 < nc; b0 += 64) {
+            if (ns > 1) wr.push_back(make_int4(i, a0, b0, (int)wg.size()));
+            for (int q = 0; q < ns; ++q) wg.push_back(make_int4(i, a0, b0, q));
+          }
+      }
+      DBuf<int4> dg, dr;
+      up(dg, wg);
+      up(dr, wr);
+      if (!wr.empty()) gpart.reserve(wg.size() * 4096, s);
+      launch_skelbig_gram(dtk, dg.p, (int)wg.size(), dr.p, (int)wr.size(), gpart.p, A, s);
+      g_launches += wr.empty() ? 1 : 2;
+      int c0 = 0;
+      while (c0 < n) {
+        size_t smem0 = 0;
+        int cn = 0, need = 0;
+        for (int i = c0; i < n; ++i) {
+          const int nc = huge[(size_t)(lo + i)].nc;
+          const int gm = pchol_min_ctas(nc);
+          const size_t sm = std::max(smem0, pchol_smem(nc, gm));
+          if (cn > 0 && need + gm > pchol_coop_capacity(sm)) break;
+          smem0 = sm;
+          need += gm;
+          ++cn;
+        }
+        const int cap = pchol_coop_capacity(smem0);
+        double tot = 0;
+        for (int i = 0; i < cn; ++i) tot += std::pow((double)huge[(size_t)(lo + c0 + i)].nc, 2);
+        std::vector<int> gs((size_t)cn + 1, 0);
+        size_t smem = 0;
+        for (int i = 0; i < cn; ++i) {
+          const int nc = huge[(size_t)(lo + c0 + i)].nc;
+          const int gm = pchol_min_ctas(nc);
+          const int extra = (int)((double)(cap - need) * ((double)nc * nc) / std::max(tot, 1.0));
+          const int g = std::max(gm, std::min({gm + extra, nc, kMaxG}));
+          gs[(size_t)i + 1] = gs[(size_t)i] + g;
+          smem = std::max(smem, pchol_smem(nc, g));
+        }
+        DBuf<int> dgs;
+        DBuf<unsigned int> dbar;
+        dgs.reserve(gs.size(), s);
+        dgs.upload(gs.data(), 0, gs.size(), s);
+        dbar.reserve((size_t)cn, s);
+        HCK(cudaMemsetAsync(dbar.p, 0, sizeof(unsigned int) * (size_t)cn, s));
+        HCK(launch_pchol_coop(dtk + c0, cn, dgs.p, gs[(size_t)cn], dbar.p, smem, A, opt.eps, s));
+        ++g_launches;
+        dgs.release(s);
+        dbar.release(s);
+        c0 += cn;
+      }
+      dg.release(s);
+      dr.release(s);
+    } else if (n >= cl_min) {
       // many groups: 16-CTA clusters per group, scheduled in waves
       HCK(launch_cpqr_cluster(dtk, n, max_nq, A, opt.eps, s));
       ++g_launches;
@@ -2689,6 +2770,7 @@ struct Factorizer {
     xiseg.release(s);
     xi32.release(s);
     agree.release(s);
+    gpart.release(s);
     scratch.release(s);
     lists.release(s);
     status.release(s);
