@@ -474,10 +474,13 @@ constexpr int kTT = 64, kTK = 16, kTL = 68;  // DMMA tile kernels: 64 x 64 tiles
 // orthogonal to the columns already chosen is largest: the pivots, the
 // rank cut |R_ii| <= eps |R_00| and R itself (up to row signs, which T =
 // R11^-1 R12 does not see) are those of the column-pivoted QR of Mq, in exact
-// arithmetic.  The Schur diagonal carries an absolute error ~u |G| against a
-// cut at eps^2 |G|, and T = G11^-1 G12 loses u cond(G11) ~ u / eps^2, so the
-// path is used only when eps^3 >> u.  Traffic: one read of Mq plus
-// O(nc k) per step against O(nq nc) per step for the CPQR on Mq itself.
+// arithmetic.  The Schur diagonal carries an absolute error ~k u |G| against
+// the cut at eps^2 |G|; T = G11^-1 G12 is off by ~u cond(G11) ~ u / eps^2, but
+// only along the small singular directions of M_sk, so the ID residual
+// |M_rd - M_sk T| moves by ~u / eps.  Both are far below eps for eps >= 1e-6
+// (kGramMinEps; ranks identical to the CPQR path on configs 4 and
+// 5).  Traffic: one read of Mq plus O(nc k) per step against O(nq nc) per step
+// for the CPQR on Mq itself.
 // ---------------------------------------------------------------------------
 // Work item int4 {task, a0, b0, split}: rows [split * kGramRows, +kGramRows)
 // of the 64 x 64 tile (a0, b0), a0 <= b0.  One split: G directly; several:

@@ -2110,7 +2110,8 @@ struct Factorizer {
   // loose tolerances only (eps^3 >> u), tall fronts, R columns in shared memory
   bool gram_ok(int nc, int nq) const {
     static const bool off = getenv("HIFDE_NO_GRAM") != nullptr;
-    return !off && opt.eps >= kGramMinEps && nq >= 2 * nc && nc <= 1024 && pchol_min_ctas(nc) > 0;
+    static const double min_eps = getenv("HIFDE_GRAM_MIN_EPS") ? atof(getenv("HIFDE_GRAM_MIN_EPS")) : kGramMinEps;
+    return !off && opt.eps >= min_eps && nq >= 2 * nc && nc <= 1024 && pchol_min_ctas(nc) > 0;
   }
 
   // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
