@@ -242,4 +242,79 @@ Groups adaptive_groups(const GridDesc& g, const Coords& X, int ell, const std::v
   return out;
 }
 
+Groups adaptive_groups_par(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
+                           int64_t ndof, const CouplingTestTid& foreign, int nthreads) {
+  const int w = g.m << ell;
+  const int k = g.n / w;
+  std::vector<int32_t> dofs(act.size()), keys(act.size());
+  std::vector<int64_t> owner((size_t)ndof, -1);
+#pragma omp parallel for num_threads(nthreads) schedule(static) if (act.size() > 65536)
+  for (int64_t i = 0; i < (int64_t)act.size(); ++i) {
+    const int32_t d = act[(size_t)i];
+    int key = 0, stride = 1;
+    for (int ax = 0; ax < g.dim; ++ax) {
+      key += (near_half(2 * X.x[ax][(size_t)d], w, k) - 1) * stride;
+      stride *= k;
+    }
+    owner[(size_t)d] = key;
+    dofs[(size_t)i] = d;
+    keys[(size_t)i] = key;
+  }
+  Groups vor = bucket(dofs, keys, ipow(k, g.dim));
+  const int64_t ng = vor.size();
+  // waves of mutually non-adjacent cells (cell coordinates from the key)
+  std::vector<int> wave((size_t)ng);
+  int nwave = 0;
+  for (int64_t gi = 0; gi < ng; ++gi) {
+    int64_t key = owner[(size_t)vor.begin(gi)[0]];
+    int wv = 0, mul = 1;
+    for (int ax = 0; ax < g.dim; ++ax) {
+      wv += (int)(key % k) * mul;
+      key /= k;
+      mul *= 2;
+    }
+    wave[(size_t)gi] = wv;
+    nwave = std::max(nwave, wv + 1);
+  }
+  std::vector<int64_t> wptr((size_t)nwave + 1, 0), worder((size_t)ng);
+  for (int64_t gi = 0; gi < ng; ++gi) ++wptr[(size_t)wave[(size_t)gi] + 1];
+  for (int v = 0; v < nwave; ++v) wptr[(size_t)v + 1] += wptr[(size_t)v];
+  {
+    std::vector<int64_t> fill(wptr.begin(), wptr.end() - 1);
+    for (int64_t gi = 0; gi < ng; ++gi) worder[(size_t)fill[(size_t)wave[(size_t)gi]]++] = gi;
+  }
+  std::vector<char> shed(vor.members.size(), 0);
+#pragma omp parallel num_threads(nthreads)
+  {
+    const int tid = omp_get_thread_num();
+    for (int v = 0; v < nwave; ++v) {
+#pragma omp for schedule(dynamic, 2)
+      for (int64_t j = wptr[(size_t)v]; j < wptr[(size_t)v + 1]; ++j) {
+        const int64_t gi = worder[(size_t)j];
+        const int32_t* mem = vor.begin(gi);
+        const int cnt = vor.count(gi);
+        const int64_t key = owner[(size_t)mem[0]];
+        char* sh = shed.data() + vor.offsets[(size_t)gi];
+        for (int i = 0; i < cnt; ++i) sh[i] = foreign(mem[i], key, owner.data(), tid) ? 1 : 0;
+        for (int i = 0; i < cnt; ++i)
+          if (sh[i]) owner[(size_t)mem[i]] = -1;
+      }  // implicit barrier: the next wave sees this wave's owners
+    }
+  }
+  Groups out;
+  out.members.reserve(vor.members.size());
+  for (int64_t gi = 0; gi < ng; ++gi) {
+    const int32_t* mem = vor.begin(gi);
+    const char* sh = shed.data() + vor.offsets[(size_t)gi];
+    int kept = 0;
+    for (int i = 0; i < vor.count(gi); ++i)
+      if (!sh[i]) {
+        out.members.push_back(mem[i]);
+        ++kept;
+      }
+    if (kept) out.offsets.push_back((int64_t)out.members.size());
+  }
+  return out;
+}
+
 }  // namespace hifde

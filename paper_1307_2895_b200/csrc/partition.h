@@ -48,4 +48,14 @@ using CouplingTest = std::function<bool(int32_t d, int64_t key, const int64_t* o
 Groups adaptive_groups(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
                        int64_t ndof, const CouplingTest& foreign);
 
+// The same partition with the shedding pass run in wavefronts of cells on
+// nthreads threads.  A cell's decisions read the current owners of DOFs in
+// adjacent cells only; with wave = cx + 2 cy + 4 cz every earlier adjacent
+// cell (ascending key order) lies in an earlier wave and no two cells of one
+// wave are adjacent, so the result is the sequential one.  foreign(d, key,
+// owner, tid) must be safe to call concurrently for different cells.
+using CouplingTestTid = std::function<bool(int32_t d, int64_t key, const int64_t* owner, int tid)>;
+Groups adaptive_groups_par(const GridDesc& g, const Coords& X, int ell, const std::vector<int32_t>& act,
+                           int64_t ndof, const CouplingTestTid& foreign, int nthreads);
+
 }  // namespace hifde

@@ -89,16 +89,28 @@ size_t align16(size_t x) { return (x + 15) / 16 * 16; }
 struct PinnedStage {
   char* p = nullptr;
   size_t cap = 0, n = 0, peak = 0;
+  size_t failed = SIZE_MAX;  // smallest size a pinned allocation failed at
   cudaStream_t s = nullptr;
   static constexpr size_t kMaxCap = (size_t)256 << 20;  // larger factorizations wrap (drain) instead
   void begin(cudaStream_t st) {
     s = st;
     n = 0;
+    // grow (geometrically, to the cap) only when the last factorization
+    // needed more; a pinned allocation is tens of ms at these sizes, so a
+    // failed size is never retried
     if (peak > cap && cap < kMaxCap) {
-      if (p) cudaFreeHost(p);
-      cap = std::min(peak + peak / 4, kMaxCap);
-      p = nullptr;
-      if (cudaHostAlloc((void**)&p, cap, cudaHostAllocDefault) != cudaSuccess) { p = nullptr; cap = 0; }
+      const size_t want = std::min(std::max(peak + peak / 4, 2 * cap), kMaxCap);
+      if (want < failed) {
+        char* q = nullptr;
+        if (cudaHostAlloc((void**)&q, want, cudaHostAllocDefault) == cudaSuccess) {
+          if (p) cudaFreeHost(p);
+          p = q;
+          cap = want;
+        } else {
+          cudaGetLastError();
+          failed = want;
+        }
+      }
     }
   }
   // returns false when the caller should fall back to a pageable copy
@@ -450,6 +462,22 @@ struct HostCache {
   // reserved up front next time so the arenas do not grow (and copy) mid-run
   int variant = -1;
   size_t hint_fac = 0, hint_bv = 0, hint_idx = 0, hint_scr = 0, hint_meta = 0;
+  // pinned host copies of a device-resident CSR pattern (input_on_device):
+  // DMA lands in them directly, pages stay resident across factorizations
+  struct Pinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+      if (bytes <= cap) return p;
+      if (p) cudaFreeHost(p);
+      cap = bytes + bytes / 8;
+      if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+        p = nullptr;
+        cap = 0;
+      }
+      return p;
+    }
+  } pat_ip, pat_ix;
 };
 HostCache& host_cache() {
   static HostCache hc;
@@ -2420,6 +2448,49 @@ struct Factorizer {
   }
 
   // -------------------------------------------------------------------------
+  // Thread-safe variant for the wavefront partition: the block verdicts are
+  // cached per thread for the cell being processed (owners do not change
+  // while one cell decides).
+  struct AfCache {
+    int64_t key = -1;
+    std::vector<std::pair<int32_t, uint8_t>> v;
+  };
+  std::vector<AfCache> afc;
+  bool adaptive_foreign_tid(int32_t d, int64_t key, const int64_t* owner, int tid) {
+    for (int64_t k = indptr[(size_t)d]; k < indptr[(size_t)d + 1]; ++k) {
+      const int64_t o = owner[indices[(size_t)k]];
+      if (o != -1 && o != key) return true;
+    }
+    AfCache& c = afc[(size_t)tid];
+    if (c.key != key) {
+      c.key = key;
+      c.v.clear();
+    }
+    bool found = false;
+    member.for_each(d, [&](int32_t b) {
+      if (found) return;
+      int f = -1;
+      for (const auto& e : c.v)
+        if (e.first == b) {
+          f = e.second;
+          break;
+        }
+      if (f < 0) {
+        f = 0;
+        const int32_t* dd = h_idx.data() + blk_dof_off[(size_t)b];
+        for (int32_t i = 0; i < blk_n[(size_t)b] && !f; ++i) {
+          const int32_t e = dd[i];
+          if (!active[(size_t)e]) continue;
+          const int64_t o = owner[e];
+          if (o != -1 && o != key) f = 1;
+        }
+        c.v.emplace_back(b, (uint8_t)f);
+      }
+      if (f) found = true;
+    });
+    return found;
+  }
+
   bool adaptive_foreign(int32_t d, int64_t key, const int64_t* owner) {
     for (int64_t k = indptr[(size_t)d]; k < indptr[(size_t)d + 1]; ++k) {
       const int64_t o = owner[indices[(size_t)k]];
@@ -2535,19 +2606,36 @@ struct Factorizer {
     LevelRec& PR = prof;  // setup / finish sub-phases (HIFDE_PROFILE)
     PR.lap(nullptr);
     pinned_stage().begin(s);
+    PR.lap("stage");
     g_stage = &pinned_stage();
     struct StageOff {
       ~StageOff() { g_stage = nullptr; }
     } stage_off;
     // A0: the symbolic analysis needs the pattern on the host
     if (opt.input_on_device) {
-      indptr_own.resize((size_t)N + 1);
-      pinned_xfer().d2h(indptr_own.data(), ip, (N + 1) * sizeof(int64_t), s);
-      nnz = indptr_own.back();
-      indices_own.resize((size_t)nnz);
-      pinned_xfer().d2h(indices_own.data(), ix, nnz * sizeof(int32_t), s);
-      indptr = indptr_own.data();
-      indices = indices_own.data();
+      HostCache& hc = host_cache();
+      int64_t* hip = (int64_t*)hc.pat_ip.get((N + 1) * sizeof(int64_t));
+      if (hip) {
+        HCK(cudaMemcpyAsync(hip, ip, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+        nnz = hip[N];
+      } else {
+        indptr_own.resize((size_t)N + 1);
+        pinned_xfer().d2h(indptr_own.data(), ip, (N + 1) * sizeof(int64_t), s);
+        hip = indptr_own.data();
+        nnz = indptr_own.back();
+      }
+      int32_t* hix = (int32_t*)hc.pat_ix.get((size_t)std::max<int64_t>(nnz, 1) * sizeof(int32_t));
+      if (hix) {
+        HCK(cudaMemcpyAsync(hix, ix, nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+      } else {
+        indices_own.resize((size_t)nnz);
+        pinned_xfer().d2h(indices_own.data(), ix, nnz * sizeof(int32_t), s);
+        hix = indices_own.data();
+      }
+      indptr = hip;
+      indices = hix;
       d_indptr = const_cast<int64_t*>(ip);
       d_indices = const_cast<int32_t*>(ix);
       d_a0 = const_cast<double*>(va);
@@ -2671,10 +2759,23 @@ struct Factorizer {
         const double tl = now_s();
         Groups gr;
         if (opt.variant == HIFDE_VARIANT_HIFDE3X && ell > 0) {
-          ++bf_epoch;
-          gr = adaptive_groups(g, X, ell, act, N, [&](int32_t d, int64_t key, const int64_t* owner) {
-            return adaptive_foreign(d, key, owner);
-          });
+          afc.resize((size_t)std::max(nthreads, 1));
+          for (auto& c : afc) c.key = -1;
+          gr = adaptive_groups_par(
+              g, X, ell, act, N,
+              [&](int32_t d, int64_t key, const int64_t* owner, int tid) {
+                return adaptive_foreign_tid(d, key, owner, tid);
+              },
+              nthreads);
+          static const bool check = getenv("HIFDE_CHECK_ADAPTIVE") != nullptr;  // debug: sequential cross-check
+          if (check) {
+            ++bf_epoch;
+            Groups ref = adaptive_groups(g, X, ell, act, N, [&](int32_t d, int64_t key, const int64_t* owner) {
+              return adaptive_foreign(d, key, owner);
+            });
+            if (ref.members != gr.members || ref.offsets != gr.offsets)
+              throw Fail{HIFDE_INTERNAL, "wavefront adaptive partition differs from the sequential one"};
+          }
         } else {
           gr = interior_groups(g, X, ell, act);
         }
