@@ -269,8 +269,10 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
 // (upper-triangular tile pairs, mirrored), FP64 DMMA m8n8k4.
 // 128 threads = 2 x 2 warps, each warp a 32 x 32 sub-tile (4 x 4 MMA tiles).
 // ---------------------------------------------------------------------------
-constexpr int kTile = kSchurTile, kKc = 16, kLdS = 68;
+constexpr int kTile = kSchurTile, kKc = 32, kLdS = 68;
 
+// Rows of W are staged 32 at a time; the next stage is prefetched into
+// registers while the DMMA loop runs on the current one.
 __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restrict__ tasks,
                                                          const int4* __restrict__ tiles, Arenas A) {
   __shared__ double Wa[kKc][kLdS];
@@ -289,15 +291,27 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
   for (int m = 0; m < 4; ++m)
 #pragma unroll
     for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+  double pa[16], pb[16];
+  auto load = [&](int k0) {  // thread e = tid + 128 u: row e / 64, column e % 64 (coalesced)
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = (int)threadIdx.x + 128 * u;
+      const int k = k0 + (e >> 6), aa = e & 63;
+      pa[u] = (k < nc && a0 + aa < nq) ? W[(size_t)k * nq + a0 + aa] : 0.0;
+      pb[u] = (k < nc && b0 + aa < nq) ? W[(size_t)k * nq + b0 + aa] : 0.0;
+    }
+  };
+  load(0);
   for (int k0 = 0; k0 < nc; k0 += kKc) {
     __syncthreads();
-    for (int e = threadIdx.x; e < kKc * kTile; e += 128) {
-      const int kk = e / kTile, aa = e - kk * kTile;
-      const int k = k0 + kk;
-      Wa[kk][aa] = (k < nc && a0 + aa < nq) ? W[(size_t)k * nq + a0 + aa] : 0.0;
-      Wb[kk][aa] = (k < nc && b0 + aa < nq) ? W[(size_t)k * nq + b0 + aa] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = (int)threadIdx.x + 128 * u;
+      Wa[e >> 6][e & 63] = pa[u];
+      Wb[e >> 6][e & 63] = pb[u];
     }
     __syncthreads();
+    if (k0 + kKc < nc) load(k0 + kKc);
 #pragma unroll
     for (int kk = 0; kk < kKc; kk += 4) {
       double af[4], bf[4];

@@ -894,8 +894,8 @@ constexpr int kT = 64, kKs = 16, kLd = 68;
 
 __global__ void __launch_bounds__(128) skelbig_congruence_kernel(const SkelBigTask* __restrict__ tasks,
                                                                  const int4* __restrict__ work, Arenas A) {
-  __shared__ double As[kKs][kLd];
-  __shared__ double Bs[kKs][kLd];
+  __shared__ double As[kGK][kTL];
+  __shared__ double Bs[kGK][kTL];
   const int4 wk = work[blockIdx.x];
   const SkelBigTask t = tasks[wk.x];
   const int nc = t.nc;
@@ -915,40 +915,52 @@ __global__ void __launch_bounds__(128) skelbig_congruence_kernel(const SkelBigTa
   for (int m = 0; m < 4; ++m)
 #pragma unroll
     for (int n = 0; n < 4; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-  const int npass = kind == 0 ? 1 : 2;
-  for (int pass = 0; pass < npass; ++pass) {
-    for (int l0 = 0; l0 < k; l0 += kKs) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < kKs * kT; e += 128) {
-        const int ll = e / kT, x = e - ll * kT;
-        const int l = l0 + ll;
-        double av = 0.0, bv = 0.0;
-        if (l < k) {
-          if (a0 + x < na) {
-            if (pass == 0) av = w.Acc[(size_t)ra[a0 + x] * nc + w.skl[l]];   // A[row][sk_l]
-            else av = T[(size_t)l * r + a0 + x];                             // T[l][a]
-          }
-          if (b0 + x < r) {
-            if (pass == 0) bv = T[(size_t)l * r + b0 + x];                   // T[l][b]
-            else bv = W[(size_t)(b0 + x) * k + l];                           // B_sr[l][b]
-          }
+  // 32-deep stages, the next one prefetched into registers during the DMMA loop
+  double pa[16], pb[16];
+  auto load = [&](int pass, int l0) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = (int)threadIdx.x + 128 * u;
+      const int l = l0 + (e >> 6), x = e & 63;
+      double av = 0.0, bv = 0.0;
+      if (l < k) {
+        if (a0 + x < na) {
+          if (pass == 0) av = w.Acc[(size_t)ra[a0 + x] * nc + w.skl[l]];   // A[row][sk_l]
+          else av = T[(size_t)l * r + a0 + x];                             // T[l][a]
         }
-        As[ll][x] = av;
-        Bs[ll][x] = bv;
+        if (b0 + x < r) {
+          if (pass == 0) bv = T[(size_t)l * r + b0 + x];                   // T[l][b]
+          else bv = W[(size_t)(b0 + x) * k + l];                           // B_sr[l][b]
+        }
       }
-      __syncthreads();
+      pa[u] = av;
+      pb[u] = bv;
+    }
+  };
+  const int npass = kind == 0 ? 1 : 2;
+  const int nst = (k + kGK - 1) / kGK;
+  if (nst > 0) load(0, 0);
+  for (int it = 0; it < npass * nst; ++it) {
+    __syncthreads();
 #pragma unroll
-      for (int kk = 0; kk < kKs; kk += 4) {
-        double af[4], bf[4];
+    for (int u = 0; u < 16; ++u) {
+      const int e = (int)threadIdx.x + 128 * u;
+      As[e >> 6][e & 63] = pa[u];
+      Bs[e >> 6][e & 63] = pb[u];
+    }
+    __syncthreads();
+    if (it + 1 < npass * nst) load((it + 1) / nst, ((it + 1) % nst) * kGK);
 #pragma unroll
-        for (int m = 0; m < 4; ++m) af[m] = As[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
+    for (int kk = 0; kk < kGK; kk += 4) {
+      double af[4], bf[4];
 #pragma unroll
-        for (int n = 0; n < 4; ++n) bf[n] = Bs[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
+      for (int m = 0; m < 4; ++m) af[m] = As[kk + (lane & 3)][wy * 32 + m * 8 + (lane >> 2)];
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+      for (int n = 0; n < 4; ++n) bf[n] = Bs[kk + (lane & 3)][wx * 32 + n * 8 + (lane >> 2)];
 #pragma unroll
-          for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
-      }
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 4; ++n) dmma_8x8x4(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
     }
   }
 #pragma unroll

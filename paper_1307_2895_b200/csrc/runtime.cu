@@ -2759,8 +2759,21 @@ struct Factorizer {
         const double tl = now_s();
         Groups gr;
         if (opt.variant == HIFDE_VARIANT_HIFDE3X && ell > 0) {
+          // few (large) cells: the sequential pass with its per-block cache;
+          // many: wavefronts of cells on the host threads
+          const int64_t ncell_est = [&] {
+            int64_t c = 1;
+            for (int ax = 0; ax < g.dim; ++ax) c *= g.n / (g.m << ell);
+            return c;
+          }();
           afc.resize((size_t)std::max(nthreads, 1));
           for (auto& c : afc) c.key = -1;
+          if (ncell_est < 256 || nthreads < 2) {
+            ++bf_epoch;
+            gr = adaptive_groups(g, X, ell, act, N, [&](int32_t d, int64_t key, const int64_t* owner) {
+              return adaptive_foreign(d, key, owner);
+            });
+          } else
           gr = adaptive_groups_par(
               g, X, ell, act, N,
               [&](int32_t d, int64_t key, const int64_t* owner, int tid) {
