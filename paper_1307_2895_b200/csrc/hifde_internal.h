@@ -44,6 +44,7 @@ struct SkelBigTask {
   int64_t iws_off;          // int scratch: pivots, sk / rd orders
   int64_t rec_off, delta_off, out_off;
   int32_t group, pad;
+  int64_t map_off;          // int scratch: front position of every block entry (-1: none)
 };
 constexpr int kMaxG = 1024;                    // most CTAs serving one large-group CPQR
 constexpr int kCL = 16;                        // CTAs per cluster (many-group batches)
@@ -142,6 +143,8 @@ cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64
                                 int* done, const Arenas& A, double eps, size_t smem, int nt, int grid,
                                 cudaStream_t s);
 
+// work int4 {task, block index, map offset of the block, 0}
+void launch_skelbig_posmap(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
 void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                              size_t smem, cudaStream_t s);
 int cpqr_coop_capacity(size_t smem);

@@ -130,6 +130,28 @@ __device__ __forceinline__ BigWs big_ws(const SkelBigTask& t, const Arenas& A) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// Front position of every entry of every block a large group consumes (-1:
+// not in the front or retired), computed once per (group, block) instead of
+// once per row chunk of the assembly.  Work item int4 {task, block, offset}.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) skelbig_posmap_kernel(const SkelBigTask* __restrict__ tasks,
+                                                             const int4* __restrict__ work, Arenas A) {
+  const int4 wk = work[blockIdx.x];
+  const SkelBigTask t = tasks[wk.x];
+  const int nc = t.nc, nq = t.nq;
+  const int32_t* gd = A.idx + t.dofs_off;
+  const int bid = A.lists[t.blk_off + wk.y];
+  const int nb = A.blk_n[bid];
+  const int32_t* bd = A.idx + A.blk_dof_off[bid];
+  int32_t* out = A.iscratch + t.map_off + wk.z;
+  for (int k = threadIdx.x; k < nb; k += 256) {
+    int p = front_pos(gd, nc, nq, bd[k]);
+    if (p >= nc && !A.active[gd[p]]) p = -1;
+    out[k] = p;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Assembly of [A_cc ; Mq].  Work item int4 {task, r0, r1, 0}: front rows.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask* __restrict__ tasks,
@@ -168,19 +190,19 @@ __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask
   }
   __syncthreads();
   const int32_t* bl = A.lists + t.blk_off;
+  const int32_t* pmap = A.iscratch + t.map_off;  // front positions, skelbig_posmap_kernel
   for (int b = 0; b < t.nblk; ++b) {
     const int bid = bl[b];
     const int nb = A.blk_n[bid];
-    const int32_t* bd = A.idx + A.blk_dof_off[bid];
     const double* bv = A.bvals + A.blk_val_off[bid];
     if (threadIdx.x == 0) nsel = 0;
     __syncthreads();
     for (int k = threadIdx.x; k < nb; k += 256) {
-      int p = front_pos(sdofs, nc, nq, bd[k]);
-      if (p >= 0 && !salive[p]) p = -1;
+      const int p = pmap[k];
       smap[k] = p;
       if (p >= r0 && p < r1) ssel[atomicAdd(&nsel, 1)] = k;
     }
+    pmap += nb;
     __syncthreads();
     const int ns = nsel;
     for (int s = 0; s < ns; ++s) {
@@ -1003,6 +1025,10 @@ __global__ void __launch_bounds__(256) skelbig_symm_kernel(const SkelBigTask* __
 }
 
 // ---------------------------------------------------------------------------
+void launch_skelbig_posmap(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s) {
+  if (nwork > 0) skelbig_posmap_kernel<<<nwork, 256, 0, s>>>(tasks, work, A);
+}
+
 void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A,
                              size_t smem, cudaStream_t s) {
   if (nwork <= 0) return;

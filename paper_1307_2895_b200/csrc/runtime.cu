@@ -1903,6 +1903,11 @@ struct Factorizer {
       H.ws_off = (int64_t)scratch.bump(nc * nc + nq * nc + (nc * nc / 4 + nc) + 3 * nc + 4 * kMaxG + 8 +
                                            (gram_ok(T.nc, T.nq) ? nc * nc : 0), s);
       H.iws_off = (int64_t)iscratch.bump(4 * nc + 4, s);
+      {
+        size_t mtot = 0;
+        for (int j = 0; j < T.nblk; ++j) mtot += (size_t)blk_n[(size_t)hl[(size_t)(T.blk_off + j)]];
+        H.map_off = (int64_t)iscratch.bump(mtot + 1, s);
+      }
       H.rec_off = T.rec_off;
       H.delta_off = T.delta_off;
       H.out_off = T.out_off;
@@ -1997,7 +2002,7 @@ struct Factorizer {
           HCK(cudaEventRecord(e0, s));
         }
         launch_huge_batch(huge, hlo, hhi, dhuge.p, dinner.p, ddmin.p, dscale.p, arenas_r(r, false),
-                          arenas_r(r, true), huge_max_nq, huge_max_nf, huge_max_nb);
+                          arenas_r(r, true), huge_max_nq, huge_max_nf, huge_max_nb, hl);
         if (shapes) {
           HCK(cudaEventRecord(e1, s));
           std::vector<int32_t> kk((size_t)nt);
@@ -2145,7 +2150,8 @@ struct Factorizer {
   // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
   void launch_huge_batch(const std::vector<SkelBigTask>& huge, int64_t lo, int64_t hi, const SkelBigTask* d_all,
                          ElimTask* d_inner_all, double* d_dmin_all, double* d_scale_all,
-                         const Arenas& A, const Arenas& AH_all, int max_nq, int max_nf, int max_nb) {
+                         const Arenas& A, const Arenas& AH_all, int max_nq, int max_nf, int max_nb,
+                         const std::vector<int32_t>& hlist) {
     const int n = (int)(hi - lo);
     const SkelBigTask* dtk = d_all + lo;
     ElimTask* inner = d_inner_all + lo;
@@ -2225,6 +2231,22 @@ struct Factorizer {
     for (int i = 0; i < n; ++i) {
       const SkelBigTask& H = huge[(size_t)(lo + i)];
       HCK(cudaMemsetAsync(A.bvals + H.delta_off, 0, sizeof(double) * (size_t)H.nc * H.nc, s));
+    }
+    {  // block entry -> front position maps, one CTA per (group, block)
+      std::vector<int4> wm;
+      for (int i = 0; i < n; ++i) {
+        const SkelBigTask& H = huge[(size_t)(lo + i)];
+        int off = 0;
+        for (int j = 0; j < H.nblk; ++j) {
+          wm.push_back(make_int4(i, j, off, 0));
+          off += blk_n[(size_t)hlist[(size_t)(H.blk_off + j)]];
+        }
+      }
+      DBuf<int4> dm;
+      up(dm, wm);
+      launch_skelbig_posmap(dtk, dm.p, (int)wm.size(), A, s);
+      ++g_launches;
+      dm.release(s);
     }
     const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 2 * max_nb));
     static const bool split_t = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: phase times
