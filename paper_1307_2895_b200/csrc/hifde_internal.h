@@ -158,6 +158,9 @@ void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, 
 size_t pchol_smem(int nc, int G);
 int pchol_min_ctas(int nc);
 int pchol_coop_capacity(size_t smem);
+// one cl-CTA cluster per group (cl in 2, 4, 8, 16), smem = pchol_smem(max nc, cl)
+cudaError_t launch_pchol_cluster(const SkelBigTask* tasks, int ntasks, int cl, size_t smem, const Arenas& A,
+                                 double eps, cudaStream_t s);
 cudaError_t launch_pchol_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
                               unsigned int* d_bar, size_t smem, const Arenas& A, double eps, cudaStream_t s);
 cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,

@@ -2279,7 +2279,25 @@ struct Factorizer {
       if (!wr.empty()) gpart.reserve(wg.size() * 4096, s);
       launch_skelbig_gram(dtk, dg.p, (int)wg.size(), dr.p, (int)wr.size(), gpart.p, A, s);
       g_launches += wr.empty() ? 1 : 2;
-      int c0 = 0;
+      // HIFDE_PCHOL_CL = 2/4/8/16 (or -1: smallest fitting >= 4): one cluster
+      // per group, DSMEM candidates and hardware cluster barriers.  Measured
+      // within +-3% of the cooperative path on configs 4 and 5, which stays
+      // the default (0).
+      static const int cl_env = getenv("HIFDE_PCHOL_CL") ? atoi(getenv("HIFDE_PCHOL_CL")) : 0;
+      int maxnc = 0;
+      for (int i = 0; i < n; ++i) maxnc = std::max(maxnc, huge[(size_t)(lo + i)].nc);
+      int clz = 0;
+      if (cl_env != 0)
+        for (int c : {2, 4, 8, 16}) {
+          if (cl_env > 0 && c != cl_env) continue;
+          if (c < (cl_env > 0 ? 2 : 4)) continue;
+          if (pchol_smem(maxnc, c) <= kSmemCapBytes) { clz = c; break; }
+        }
+      int c0 = clz ? n : 0;
+      if (clz) {
+        HCK(launch_pchol_cluster(dtk, n, clz, pchol_smem(maxnc, clz), A, opt.eps, s));
+        ++g_launches;
+      }
       while (c0 < n) {
         size_t smem0 = 0;
         int cn = 0, need = 0;
