@@ -338,6 +338,11 @@ struct PodVec {
     resize((size_t)(e - b));
     if (n) std::memcpy(p.get(), b, n * sizeof(T));
   }
+  void swap(PodVec& o) {
+    p.swap(o.p);
+    std::swap(n, o.n);
+    std::swap(cap, o.cap);
+  }
 };
 
 // Solve metadata of a whole factorization packed into one device allocation
@@ -478,6 +483,11 @@ struct HostCache {
       return p;
     }
   } pat_ip, pat_ix;
+  // host mirror of the index arena and the solve-metadata staging buffer,
+  // lent to each factorization: their pages stay mapped (a fresh multi-100 MB
+  // buffer per factorization costs its page faults on first touch)
+  PodVec<int32_t> idx_buf;
+  PodVec<char> meta_buf;
 };
 HostCache& host_cache() {
   static HostCache hc;
@@ -2711,6 +2721,13 @@ struct Factorizer {
       });
     }
     PR.lap("A0");
+    {  // borrow the persistent host buffers (returned at the end of run)
+      HostCache& hc = host_cache();
+      h_idx.swap(hc.idx_buf);
+      h_idx.resize(0);
+      meta.h.swap(hc.meta_buf);
+      meta.h.resize(0);
+    }
     active.resize((size_t)N);
     act.resize((size_t)N);
 #pragma omp parallel for schedule(static) if (N > (1 << 16))
@@ -2917,6 +2934,8 @@ struct Factorizer {
       hc.hint_idx = h_idx.size();
       hc.hint_scr = scratch.cap;
       hc.hint_meta = meta_bytes;
+      hc.idx_buf.swap(h_idx);
+      hc.meta_buf.swap(meta.h);
     }
     bvals.release(s);
     for (auto& l : lanes) l.release(s);
