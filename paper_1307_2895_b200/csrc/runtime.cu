@@ -1640,8 +1640,7 @@ struct Factorizer {
       const Sz& z = sz[(size_t)t];
       const int nc = T.nc, nq = T.nq;
       T.dofs_off = idx_tot;
-      T.out_off = idx_tot + nc + nq;
-      idx_tot += 2 * nc + nq;
+      idx_tot += nc + nq;  // the sk/rd output lists follow all groups' fronts (below)
       T.blk_off = hl_tot;
       hl_tot += T.nblk;
       if (z.scr) { T.scratch_off = (int64_t)scr_tot; scr_tot += z.scr; }
@@ -1659,6 +1658,13 @@ struct Factorizer {
       for (int i = 0; i < z.npred; ++i) b = std::max(b, batch[(size_t)pp[i]] + 1);
       batch[(size_t)t] = b;
       nbatch = std::max(nbatch, b + 1);
+    }
+    // output lists of every group, contiguous after the fronts: the level's
+    // one readback copies only this tail
+    const int64_t out_base = idx_tot;
+    for (int64_t t = 0; t < nt; ++t) {
+      tasks[(size_t)t].out_off = idx_tot;
+      idx_tot += tasks[(size_t)t].nc;
     }
     const int64_t idx_base = (int64_t)h_idx.size();
     h_idx.resize((size_t)(idx_base + idx_tot));
@@ -1685,7 +1691,7 @@ struct Factorizer {
       int32_t* d = h_idx.data() + T.dofs_off;
       std::copy(gr.begin(t), gr.begin(t) + nc, d);
       std::copy(sym_q(f), sym_q(f) + nq, d + nc);
-      std::fill(d + nc + nq, d + 2 * nc + nq, 0);
+      std::fill(h_idx.data() + T.out_off, h_idx.data() + T.out_off + nc, 0);
       std::copy(sym_b(f), sym_b(f) + f.nb, hl.data() + T.blk_off);
       const int32_t* pp = tpred[(size_t)(z.pred_off % nthreads)].data() + z.pred_off / nthreads;
       std::copy(pp, pp + z.npred, preds.data() + pred_ptr[(size_t)t]);
@@ -1825,7 +1831,7 @@ struct Factorizer {
         union_level(tasks, nt);
         L.t_launch = now_s() - tp;
         tp = now_s();
-        finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
+        finish_skeleton_level(tasks, idx_level_start + out_base, tag, L, tp);
         dt.release(s);
         dpp.release(s);
         dpr.release(s);
@@ -1869,7 +1875,7 @@ struct Factorizer {
       }
       L.t_launch = now_s() - tp;
       tp = now_s();
-      finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
+      finish_skeleton_level(tasks, idx_level_start + out_base, tag, L, tp);
       dt.release(s);
       dpp.release(s);
       dpr.release(s);
@@ -2054,7 +2060,7 @@ struct Factorizer {
     dinner.release(s);
     ddmin.release(s);
     dscale.release(s);
-    finish_skeleton_level(tasks, idx_level_start, tag, L, tp);
+    finish_skeleton_level(tasks, idx_level_start + out_base, tag, L, tp);
   }
 
   // Read back ranks and sk/rd lists (the level's one synchronization), then
