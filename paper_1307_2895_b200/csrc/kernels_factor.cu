@@ -243,8 +243,35 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
     if (threadIdx.x == 0) A.status[blockIdx.x] = st;
     return;
   }
+  // W = C^-1 F_cq and (with room) X = C^-1 I in ONE barrier-free pass: a
+  // thread per right-hand-side column, forward substitution down the rows.
+  // Each column's sums run in the same order as the row-sweep TRSM
+  // (trsm_1sync), so the results are bit-identical to it; the identity
+  // columns start at their diagonal (the skipped terms are exact zeros).
+  double* X = t.scratch_off == -2 ? F + (size_t)nf * nf : nullptr;
+  const int ncol = nq + (X ? nc : 0);
+  for (int j = threadIdx.x; j < ncol; j += NT) {
+    if (j < nq) {
+      double* B = F + nc + j;
+      for (int i = 0; i < nc; ++i) {
+        const double* Ci = F + (size_t)i * nf;
+        double sacc = B[(size_t)i * nf];
+        for (int l = 0; l < i; ++l) sacc -= Ci[l] * B[(size_t)l * nf];
+        B[(size_t)i * nf] = sacc * (1.0 / Ci[i]);
+      }
+    } else {
+      const int jj = j - nq;
+      for (int i = 0; i < jj; ++i) X[(size_t)i * nc + jj] = 0.0;
+      for (int i = jj; i < nc; ++i) {
+        const double* Ci = F + (size_t)i * nf;
+        double sacc = i == jj ? 1.0 : 0.0;
+        for (int l = jj; l < i; ++l) sacc -= Ci[l] * X[(size_t)l * nc + jj];
+        X[(size_t)i * nc + jj] = sacc * (1.0 / Ci[i]);
+      }
+    }
+  }
+  __syncthreads();
   if (nq > 0) {
-    trsm_1sync<NT>(F, nc, nf, F + nc, nq, nf);
     double* U = A.bvals + t.U_off;
     for (int e = threadIdx.x; e < nq * nq; e += NT) {
       const int a = e / nq, b = e - a * nq;
@@ -259,8 +286,15 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
     }
   }
   // the solve applies C^-1 as a product: store it packed (lower, row-major)
-  if (t.scratch_off == -2) tri_inverse_packed_ws<NT>(F, nc, nf, F + (size_t)nf * nf, A.fac + t.P_off);
-  else tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
+  if (X) {
+    double* P = A.fac + t.P_off;
+    for (int e = threadIdx.x; e < nc * nc; e += NT) {
+      const int i = e / nc, j = e - i * nc;
+      if (j <= i) P[(size_t)i * (i + 1) / 2 + j] = X[e];
+    }
+  } else {
+    tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
+  }
   if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
 }
 
