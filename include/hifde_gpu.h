@@ -33,6 +33,7 @@
 #ifndef HIFDE_GPU_H
 #define HIFDE_GPU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -253,6 +254,20 @@ int64_t hifde_partition(int dim, int n_grid, int m_leaf, int ell, int level_kind
 int hifde_comm_unique_id(uint8_t* id);
 int hifde_comm_init(const uint8_t* id, int nranks, int rank, int device, hifde_comm_t** out);
 int hifde_comm_emulated(int nranks, int device, hifde_comm_t** out);
+/*
+ * Host-staged communicator (testing the real-rank path without NCCL, e.g.
+ * two processes on one GPU over gloo): the library copies each collective's
+ * device data to host buffers and calls
+ *   allreduce(ctx, buf, count, dtype (0 int32, 1 uint8, 2 float64), op (0 sum, 1 max, 2 min))
+ *   sendrecv(ctx, nsend, send_peer[], send_buf[], send_bytes[], nrecv, recv_peer[], recv_buf[], recv_bytes[])
+ * in place; callbacks return 0 on success.
+ */
+typedef int (*hifde_allreduce_fn)(void* ctx, void* buf, size_t count, int dtype, int op);
+typedef int (*hifde_sendrecv_fn)(void* ctx, int nsend, const int* send_peer, void* const* send_buf,
+                                 const size_t* send_bytes, int nrecv, const int* recv_peer, void* const* recv_buf,
+                                 const size_t* recv_bytes);
+int hifde_comm_host(int nranks, int rank, int device, hifde_allreduce_fn allreduce, hifde_sendrecv_fn sendrecv,
+                    void* ctx, hifde_comm_t** out);
 int hifde_comm_info(const hifde_comm_t* c, int* nranks, int* rank, int* emulated);
 void hifde_comm_free(hifde_comm_t* c);
 const char* hifde_comm_last_error(void);

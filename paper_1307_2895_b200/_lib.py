@@ -82,7 +82,8 @@ EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
     "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
     "hifde_free", "hifde_last_error", "hifde_partition",
-    "hifde_comm_unique_id", "hifde_comm_init", "hifde_comm_emulated", "hifde_comm_info", "hifde_comm_free",
+    "hifde_comm_unique_id", "hifde_comm_init", "hifde_comm_emulated", "hifde_comm_host", "hifde_comm_info",
+    "hifde_comm_free",
     "hifde_comm_last_error", "hifde_shard_owner", "hifde_shard_plan",
 ]
 

@@ -8,6 +8,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/hifde_gpu.h"
 #include "comm.h"
@@ -101,14 +102,59 @@ __global__ void seg_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, 
 
 }  // namespace
 
+namespace {
+size_t type_bytes(CommType t) { return t == kI32 ? 4 : t == kU8 ? 1 : 8; }
+void cuck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
 void comm_allreduce(const hifde_comm* c, void* buf, size_t count, CommType t, CommOp op, cudaStream_t s) {
   if (!c || c->P <= 1 || c->emulated || count == 0) return;
+  if (c->cb_allreduce) {  // host-staged transport
+    std::vector<char> h(count * type_bytes(t));
+    cuck(cudaMemcpyAsync(h.data(), buf, h.size(), cudaMemcpyDeviceToHost, s), "staged allreduce D2H");
+    cuck(cudaStreamSynchronize(s), "staged allreduce sync");
+    if (c->cb_allreduce(c->cb_ctx, h.data(), count, (int)t, (int)op) != 0)
+      throw std::runtime_error("host transport: allreduce callback failed");
+    cuck(cudaMemcpyAsync(buf, h.data(), h.size(), cudaMemcpyHostToDevice, s), "staged allreduce H2D");
+    cuck(cudaStreamSynchronize(s), "staged allreduce sync");
+    return;
+  }
   NcclApi& a = nccl();
   nck(a.AllReduce(buf, buf, count, dtype(t), redop(op), (ncclComm_t)c->nccl, s), "ncclAllReduce");
 }
 
 void comm_sendrecv(const hifde_comm* c, const P2P* sends, int nsend, const P2P* recvs, int nrecv, cudaStream_t s) {
   if (!c || c->P <= 1 || c->emulated || (nsend == 0 && nrecv == 0)) return;
+  if (c->cb_sendrecv) {  // host-staged transport
+    std::vector<std::vector<char>> hs((size_t)nsend), hr((size_t)nrecv);
+    std::vector<int> sp((size_t)nsend), rp((size_t)nrecv);
+    std::vector<void*> sb((size_t)nsend), rbuf((size_t)nrecv);
+    std::vector<size_t> sz((size_t)nsend), rz((size_t)nrecv);
+    for (int i = 0; i < nsend; ++i) {
+      hs[(size_t)i].resize(sends[i].bytes);
+      cuck(cudaMemcpyAsync(hs[(size_t)i].data(), sends[i].ptr, sends[i].bytes, cudaMemcpyDeviceToHost, s),
+           "staged send D2H");
+      sp[(size_t)i] = sends[i].peer;
+      sb[(size_t)i] = hs[(size_t)i].data();
+      sz[(size_t)i] = sends[i].bytes;
+    }
+    for (int i = 0; i < nrecv; ++i) {
+      hr[(size_t)i].resize(recvs[i].bytes);
+      rp[(size_t)i] = recvs[i].peer;
+      rbuf[(size_t)i] = hr[(size_t)i].data();
+      rz[(size_t)i] = recvs[i].bytes;
+    }
+    cuck(cudaStreamSynchronize(s), "staged sendrecv sync");
+    if (c->cb_sendrecv(c->cb_ctx, nsend, sp.data(), sb.data(), sz.data(), nrecv, rp.data(), rbuf.data(), rz.data()) != 0)
+      throw std::runtime_error("host transport: sendrecv callback failed");
+    for (int i = 0; i < nrecv; ++i)
+      cuck(cudaMemcpyAsync(recvs[i].ptr, hr[(size_t)i].data(), recvs[i].bytes, cudaMemcpyHostToDevice, s),
+           "staged recv H2D");
+    cuck(cudaStreamSynchronize(s), "staged sendrecv sync");
+    return;
+  }
   NcclApi& a = nccl();
   nck(a.GroupStart(), "ncclGroupStart");
   for (int i = 0; i < nsend; ++i)
@@ -201,6 +247,20 @@ int hifde_comm_emulated(int nranks, int device, hifde_comm_t** out) {
   c->rank = 0;
   c->device = device;
   c->emulated = true;
+  *out = c;
+  return HIFDE_OK;
+}
+
+int hifde_comm_host(int nranks, int rank, int device, hifde_allreduce_cb allreduce, hifde_sendrecv_cb sendrecv,
+                    void* ctx, hifde_comm_t** out) {
+  if (!out || !allreduce || !sendrecv || nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks) return HIFDE_BADARG;
+  hifde_comm* c = new hifde_comm;
+  c->P = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->cb_allreduce = allreduce;
+  c->cb_sendrecv = sendrecv;
+  c->cb_ctx = ctx;
   *out = c;
   return HIFDE_OK;
 }

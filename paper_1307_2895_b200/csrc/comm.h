@@ -16,10 +16,21 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Host-staged transport (tests of the real-rank path without NCCL: two
+// processes on one GPU over gloo): device buffers are copied to the host,
+// handed to the caller's callbacks, and copied back.
+typedef int (*hifde_allreduce_cb)(void* ctx, void* buf, size_t count, int dtype, int op);
+typedef int (*hifde_sendrecv_cb)(void* ctx, int nsend, const int* send_peer, void* const* send_buf,
+                                 const size_t* send_bytes, int nrecv, const int* recv_peer, void* const* recv_buf,
+                                 const size_t* recv_bytes);
+
 struct hifde_comm {
   int P = 1, rank = 0, device = 0;
   bool emulated = false;
   void* nccl = nullptr;  // ncclComm_t
+  hifde_allreduce_cb cb_allreduce = nullptr;
+  hifde_sendrecv_cb cb_sendrecv = nullptr;
+  void* cb_ctx = nullptr;
 };
 
 namespace hifde {

@@ -1411,7 +1411,8 @@ struct Factorizer {
     Arenas A = arenas_for(r);
     if (!small.empty()) {
       A.status = status.p + st_small;
-      launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= 64 ? 128 : 256, s);
+      static const int nt128_nf = getenv("HIFDE_ELIM128_NF") ? atoi(getenv("HIFDE_ELIM128_NF")) : 64;
+      launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= nt128_nf ? 128 : 256, s);
       ++g_launches;
     }
     if (!big.empty()) {

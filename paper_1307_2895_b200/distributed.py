@@ -114,6 +114,64 @@ def init_comm(group=None, device: Optional[int] = None) -> Comm:
     return Comm(h.value, int(device))
 
 
+_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int)
+_SENDRECV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p),
+                        C.POINTER(C.c_size_t), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p),
+                        C.POINTER(C.c_size_t))
+
+
+def host_comm(group=None, device: Optional[int] = None) -> Comm:
+    """Real-rank communicator whose collectives are staged through host memory
+    and carried by ``torch.distributed`` (any backend, gloo included).  It runs
+    the sharded path's real-rank code (exchange, merges, factor sum) without
+    NCCL, e.g. two processes on one GPU; it is a test transport, not a fast one."""
+    import torch
+    import torch.distributed as dist
+
+    lib = L.load()
+    rank, size = dist.get_rank(group), dist.get_world_size(group)
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", rank))
+    dtypes = {0: np.int32, 1: np.uint8, 2: np.float64}
+    ops = {0: dist.ReduceOp.SUM, 1: dist.ReduceOp.MAX, 2: dist.ReduceOp.MIN}
+
+    def view(ptr, nbytes, dtype=np.uint8):
+        raw = (C.c_char * nbytes).from_address(ptr)
+        return torch.from_numpy(np.frombuffer(raw, dtype=np.uint8).view(dtype))
+
+    def allreduce(ctx, buf, count, dtype, op):
+        try:
+            dt = dtypes[dtype]
+            dist.all_reduce(view(buf, count * np.dtype(dt).itemsize, dt), op=ops[op], group=group)
+            return 0
+        except Exception:
+            return 1
+
+    def sendrecv(ctx, nsend, speer, sbuf, sbytes, nrecv, rpeer, rbuf, rbytes):
+        try:
+            reqs = []
+            for i in range(nsend):
+                reqs.append(dist.isend(view(sbuf[i], sbytes[i]), int(speer[i]), group=group))
+            for i in range(nrecv):
+                reqs.append(dist.irecv(view(rbuf[i], rbytes[i]), int(rpeer[i]), group=group))
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception:
+            return 1
+
+    cb_a, cb_s = _ALLREDUCE(allreduce), _SENDRECV(sendrecv)
+    lib.hifde_comm_host.argtypes = [C.c_int, C.c_int, C.c_int, _ALLREDUCE, _SENDRECV, C.c_void_p,
+                                    C.POINTER(C.c_void_p)]
+    lib.hifde_comm_host.restype = C.c_int
+    h = C.c_void_p()
+    if lib.hifde_comm_host(size, rank, int(device), cb_a, cb_s, None, C.byref(h)):
+        raise ValueError("bad host communicator arguments")
+    c = Comm(h.value, int(device))
+    c._callbacks = (cb_a, cb_s)  # kept alive with the communicator
+    return c
+
+
 def emulated_comm(nranks: int, device: int = 0) -> Comm:
     """P virtual ranks inside this process on one device (testing)."""
     lib = L.load()

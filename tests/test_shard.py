@@ -339,3 +339,70 @@ def test_emulated_single_rank_is_the_plain_path():
     f = H.factor_hifde(a, g, 1e-6, comm=c)
     assert f.metrics["nranks"] == 1 and f.metrics["xfer_bytes"] == 0
     assert _gldl_bytes(f) == _gldl_bytes(H.factor_hifde(a, g, 1e-6))
+
+
+# ---------------------------------------------------------------------------
+# GPU: the real-rank path (not emulated) with two processes on one GPU, the
+# collectives staged through the host and carried by gloo (hifde_comm_host)
+
+
+def _real_rank_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    import paper_1307_2895_b200 as H
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        comm = D.host_comm(device=0)
+        out = {}
+        for name, (dim, n, m, eps, contrast, var) in {
+                "2d": (2, 64, 8, 1e-6, True, "hifde"), "3d": (3, 16, 4, 1e-6, False, "hifde3x")}.items():
+            g, a = _problem(dim, n, m, contrast)
+            fac = H.factor_hifde if var == "hifde" else H.factor_hifde3x
+            f = fac(a, g, eps, comm=comm, device=0)
+            b = np.random.default_rng(0).standard_normal((g.ndof, 2))
+            out[name] = (_gldl_bytes(f), f.apply_inverse(b), f.metrics["skeleton_counts"], f.metrics["nranks"],
+                         f.metrics["xfer_bytes"])
+            if rank == 0:
+                f0 = fac(a, g, eps, device=0)
+                out[name + "_ref"] = (_gldl_bytes(f0), f0.apply_inverse(b), f0.metrics["skeleton_counts"])
+        comm.close()
+        q.put((rank, "ok", out))
+    except Exception as e:
+        import traceback
+        q.put((rank, traceback.format_exc(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_real_ranks_over_host_transport_two_processes():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_real_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, status, out = q.get(timeout=600)
+        res[r] = (status, out)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(v[0] == "ok" for v in res.values()), res
+    o0, o1 = res[0][1], res[1][1]
+    for name in ("2d", "3d"):
+        b0, x0, k0, nr, xb = o0[name]
+        b1, x1, k1, _, _ = o1[name]
+        rb, rx, rk = o0[name + "_ref"]
+        assert nr == 2 and xb > 0
+        assert b0 == b1 and np.array_equal(x0, x1)  # both ranks hold the same whole factor
+        assert k0 == rk
+        if name == "2d":
+            assert b0 == rb and np.array_equal(x0, rx)  # the single-GPU factor, byte for byte
+        else:
+            assert np.linalg.norm(x0 - rx) <= 1e-8 * np.linalg.norm(rx)
