@@ -99,7 +99,7 @@ struct PinnedStage {
     // needed more; a pinned allocation is tens of ms at these sizes, so a
     // failed size is never retried
     if (peak > cap && cap < kMaxCap) {
-      const size_t want = std::min(std::max(peak + peak / 4, 2 * cap), kMaxCap);
+      const size_t want = std::min(std::max(4 * peak, 2 * cap), kMaxCap);
       if (want < failed) {
         char* q = nullptr;
         if (cudaHostAlloc((void**)&q, want, cudaHostAllocDefault) == cudaSuccess) {
