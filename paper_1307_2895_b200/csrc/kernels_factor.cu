@@ -109,11 +109,31 @@ __device__ int chol_1sync(double* A, int n, int ld, double* red) {
       for (int i = k + threadIdx.x; i < n; i += NT) A[(size_t)i * ld + k - 1] *= prev_inv;
       if (threadIdx.x == 0) A[(size_t)(k - 1) * ld + k - 1] = prev_piv;
     }
-    // trailing update, lower triangle: warp per row, lanes over columns
-    for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
-      const double aik = A[(size_t)i * ld + k];
-      for (int j = k + 1 + (int)(threadIdx.x & 31); j <= i; j += 32)
-        A[(size_t)i * ld + j] -= aik * (A[(size_t)j * ld + k] * rakk);
+    // trailing update, lower triangle: warp per row, lanes over columns.
+    // A lane's column factors A[j][k] / akk are formed once per step (same
+    // rounding as forming them per row) and kept in registers.
+    const int lane = (int)(threadIdx.x & 31);
+    if (n - k - 1 <= 128) {
+      double tj[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int j = k + 1 + lane + 32 * m;
+        tj[m] = j < n ? A[(size_t)j * ld + k] * rakk : 0.0;
+      }
+      for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
+        const double aik = A[(size_t)i * ld + k];
+        double* Ai = A + (size_t)i * ld;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int j = k + 1 + lane + 32 * m;
+          if (j <= i) Ai[j] -= aik * tj[m];
+        }
+      }
+    } else {
+      for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
+        const double aik = A[(size_t)i * ld + k];
+        for (int j = k + 1 + lane; j <= i; j += 32) A[(size_t)i * ld + j] -= aik * (A[(size_t)j * ld + k] * rakk);
+      }
     }
     prev_piv = piv;
     prev_inv = 1.0 / piv;
