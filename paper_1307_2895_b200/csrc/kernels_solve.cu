@@ -111,6 +111,8 @@ __device__ __forceinline__ double* workspace(double* smem, double* scratch, int6
 // 2 dense row-major (ld lda), 3 dense transposed.
 constexpr int kGKC = 32, kGRB = 16, kGMI = 6;
 constexpr int kGRows = (NT / kGRB) * kGMI;  // rows per pass (96)
+constexpr int kDmmaMinRhs = 48;             // right-hand sides from which products use DMMA (measured: 16 and 32
+                                            // RHS have too few tiles per warp to hide DMMA latency)
 // One right-hand side: a matrix-vector product read straight from global
 // memory.  Row-major operands (P, dense): a warp per row, lanes along k
 // (coalesced); transposed operands: lanes along 32 consecutive rows, warps
@@ -159,10 +161,107 @@ __device__ void cta_gemv(int M, int K, int amode, const double* __restrict__ A, 
   __syncthreads();
 }
 
-__device__ void cta_gemm(int M, int K, int amode, const double* __restrict__ A, int64_t lda, const double* X,
-                         double* Y, int nrhs, double alpha, bool accumulate, double* As) {
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// The same product on the FP64 tensor cores (DMMA m8n8k4) for blocks of 8
+// or more right-hand sides: per pass 96 rows x 64 right-hand sides as 8 x 8
+// tiles, tile t = warp + 8 i (row tile t / ntc, column tile t % ntc), A staged
+// in 32-wide K chunks as in cta_gemm, X read from shared memory.
+__device__ void cta_gemm_dmma(int M, int K, int amode, const double* __restrict__ A, int64_t lda, const double* X,
+                              double* Y, int nrhs, double alpha, bool accumulate, double* As) {
+  constexpr int kCW = 64, kMaxT = (kGRows / 8) * (kCW / 8) / (NT / 32);  // 12 tiles per warp
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int m0 = 0; m0 < M; m0 += kGRows) {
+    const int mrows = min(kGRows, M - m0);
+    const int mt = (mrows + 7) / 8;
+    for (int c0 = 0; c0 < nrhs; c0 += kCW) {
+      const int cw = min(kCW, nrhs - c0);
+      const int ntc = (cw + 7) / 8;
+      const int ntiles = mt * ntc;
+      double acc[kMaxT][2];
+#pragma unroll
+      for (int i = 0; i < kMaxT; ++i) acc[i][0] = acc[i][1] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += kGKC) {
+        const int kc = min(kGKC, K - k0);
+        __syncthreads();
+        if (amode == 0 || amode == 2) {
+          for (int e = threadIdx.x; e < mrows * kGKC; e += NT) {
+            const int ii = e / kGKC, kk = e - ii * kGKC, i = m0 + ii, k = k0 + kk;
+            double a = 0.0;
+            if (kk < kc) a = amode == 0 ? (k <= i ? A[(size_t)i * (i + 1) / 2 + k] : 0.0) : A[(size_t)i * lda + k];
+            As[ii * (kGKC + 1) + kk] = a;
+          }
+        } else {
+          for (int e = threadIdx.x; e < mrows * kGKC; e += NT) {
+            const int kk = e / mrows, ii = e - kk * mrows, i = m0 + ii, k = k0 + kk;
+            double a = 0.0;
+            if (kk < kc) a = amode == 1 ? (k >= i ? A[(size_t)k * (k + 1) / 2 + i] : 0.0) : A[(size_t)k * lda + i];
+            As[ii * (kGKC + 1) + kk] = a;
+          }
+        }
+        __syncthreads();
+        // with ntc | 8 a warp's tiles share one column tile: its X fragment
+        // is loaded once per k step
+        const bool one_ct = (NT / 32) % ntc == 0;
+        for (int ks = 0; ks < kc; ks += 4) {
+          const int kl = ks + (lane & 3);  // this lane's k in the chunk
+          double b0 = 0.0;
+          if (one_ct) {
+            const int col = c0 + (wid % ntc) * 8 + (lane >> 2);
+            b0 = (kl < kc && col < nrhs) ? X[(size_t)(k0 + kl) * nrhs + col] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < kMaxT; ++i) {
+            const int t = wid + (NT / 32) * i;
+            if (t >= ntiles) break;
+            const int rt = t / ntc, ct = t - rt * ntc;
+            const int row = rt * 8 + (lane >> 2);
+            const double a = (kl < kc && row < mrows) ? As[row * (kGKC + 1) + kl] : 0.0;
+            double b = b0;
+            if (!one_ct) {
+              const int col = c0 + ct * 8 + (lane >> 2);
+              b = (kl < kc && col < nrhs) ? X[(size_t)(k0 + kl) * nrhs + col] : 0.0;
+            }
+            dmma_8x8x4(acc[i][0], acc[i][1], a, b);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxT; ++i) {
+        const int t = wid + (NT / 32) * i;
+        if (t >= ntiles) break;
+        const int rt = t / ntc, ct = t - rt * ntc;
+        const int row = m0 + rt * 8 + (lane >> 2);
+        if (row >= M) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c0 + ct * 8 + 2 * (lane & 3) + h;
+          if (col >= nrhs) continue;
+          double* y = Y + (size_t)row * nrhs + col;
+          *y = (accumulate ? *y : 0.0) + alpha * acc[i][h];
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// kD: the kernel instantiation that may take the DMMA path (a separate
+// instantiation, so the register budget of the DMMA tiles does not lower the
+// occupancy of the CUDA-core path used for fewer right-hand sides)
+template <bool kD>
+__device__ void cta_gemm_t(int M, int K, int amode, const double* __restrict__ A, int64_t lda, const double* X,
+                           double* Y, int nrhs, double alpha, bool accumulate, double* As) {
   if (nrhs == 1) {
     cta_gemv(M, K, amode, A, lda, X, Y, alpha, accumulate, As);
+    return;
+  }
+  if (kD && nrhs >= kDmmaMinRhs) {
+    cta_gemm_dmma(M, K, amode, A, lda, X, Y, nrhs, alpha, accumulate, As);
     return;
   }
   constexpr int RG = NT / kGRB;
@@ -215,8 +314,15 @@ __device__ void cta_gemm(int M, int K, int amode, const double* __restrict__ A, 
   __syncthreads();
 }
 
+__device__ __forceinline__ void cta_gemm(int M, int K, int amode, const double* __restrict__ A, int64_t lda,
+                                         const double* X, double* Y, int nrhs, double alpha, bool accumulate,
+                                         double* As) {
+  cta_gemm_t<false>(M, K, amode, A, lda, X, Y, nrhs, alpha, accumulate, As);
+}
+
 }  // namespace
 
+template <bool kD>
 __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
     const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
     double* __restrict__ v, int nrhs, double* __restrict__ contrib, double* scratch, int64_t per_rec) {
@@ -232,7 +338,7 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
     s[e] = v[(size_t)c[i] * nrhs + r];
   }
   if (rc.inv) {
-    cta_gemm(nc, nc, 0, fac + rc.C_off, 0, s, s2, nrhs, 1.0, false, As);  // s2 = P s
+    cta_gemm_t<kD>(nc, nc, 0, fac + rc.C_off, 0, s, s2, nrhs, 1.0, false, As);  // s2 = P s
     s = s2;
   } else {
     fwd_subst(fac + rc.C_off, nc, s, nrhs);
@@ -242,7 +348,7 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_kernel(
     v[(size_t)c[i] * nrhs + r] = s[e];
   }
   // contributions g = W^T s (W nc x nq row-major), summed per DOF later
-  if (nq > 0) cta_gemm(nq, nc, 3, fac + rc.W_off, nq, s, contrib + (size_t)rc.contrib_off * nrhs, nrhs, 1.0, false, As);
+  if (nq > 0) cta_gemm_t<kD>(nq, nc, 3, fac + rc.W_off, nq, s, contrib + (size_t)rc.contrib_off * nrhs, nrhs, 1.0, false, As);
 }
 
 __global__ void solve_reduce_kernel(const int32_t* __restrict__ targets, const int64_t* __restrict__ ptr,
@@ -257,6 +363,7 @@ __global__ void solve_reduce_kernel(const int32_t* __restrict__ targets, const i
   v[(size_t)targets[t] * nrhs + r] += sign * acc;
 }
 
+template <bool kD>
 __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
     const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
     double* __restrict__ v, int nrhs, double* scratch, int64_t per_rec) {
@@ -278,10 +385,10 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
     xq[e] = v[(size_t)q[b] * nrhs + r];
   }
   // t = v_c - W v_q  (W nc x nq row-major)
-  if (nq > 0) cta_gemm(nc, nq, 2, fac + rc.W_off, nq, xq, t, nrhs, -1.0, true, As);
+  if (nq > 0) cta_gemm_t<kD>(nc, nq, 2, fac + rc.W_off, nq, xq, t, nrhs, -1.0, true, As);
   else __syncthreads();
   if (rc.inv) {
-    cta_gemm(nc, nc, 1, fac + rc.C_off, 0, t, t2, nrhs, 1.0, false, As);  // t2 = P^T t
+    cta_gemm_t<kD>(nc, nc, 1, fac + rc.C_off, 0, t, t2, nrhs, 1.0, false, As);  // t2 = P^T t
     t = t2;
   } else {
     bwd_subst(fac + rc.C_off, nc, t, nrhs);
@@ -295,6 +402,7 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
 // Skeleton record: idx = sk[k] then rd[r]; T (k x r), C (r x r), W (r x k).
 //   forward  (apply_ut): v_rd -= T^T v_sk ; s = C^-1 v_rd ; v_sk -= W^T s ; v_rd = s
 //   backward (apply_u) : v_rd = C^-T (v_rd - W v_sk) ; v_sk -= T v_rd
+template <bool kD>
 __global__ void __launch_bounds__(NT) solve_skel_kernel(
     const SolveRec* __restrict__ recs, const int32_t* __restrict__ idx, const double* __restrict__ fac,
     double* __restrict__ v, int nrhs, int forward, double* scratch, int64_t per_rec) {
@@ -321,23 +429,23 @@ __global__ void __launch_bounds__(NT) solve_skel_kernel(
   __syncthreads();
   double* xo = xr;  // final v_rd
   if (forward) {
-    if (k > 0) cta_gemm(r, k, 3, T, r, xs, xr, nrhs, -1.0, true, As);  // v_rd -= T^T v_sk
+    if (k > 0) cta_gemm_t<kD>(r, k, 3, T, r, xs, xr, nrhs, -1.0, true, As);  // v_rd -= T^T v_sk
     if (rc.inv) {
-      cta_gemm(r, r, 0, C, 0, xr, x2, nrhs, 1.0, false, As);           // s = P v_rd
+      cta_gemm_t<kD>(r, r, 0, C, 0, xr, x2, nrhs, 1.0, false, As);           // s = P v_rd
       xo = x2;
     } else {
       fwd_subst(C, r, xr, nrhs);
     }
-    if (k > 0) cta_gemm(k, r, 3, W, k, xo, xs, nrhs, -1.0, true, As);  // v_sk -= W^T s
+    if (k > 0) cta_gemm_t<kD>(k, r, 3, W, k, xo, xs, nrhs, -1.0, true, As);  // v_sk -= W^T s
   } else {
-    if (k > 0) cta_gemm(r, k, 2, W, k, xs, xr, nrhs, -1.0, true, As);  // v_rd -= W v_sk
+    if (k > 0) cta_gemm_t<kD>(r, k, 2, W, k, xs, xr, nrhs, -1.0, true, As);  // v_rd -= W v_sk
     if (rc.inv) {
-      cta_gemm(r, r, 1, C, 0, xr, x2, nrhs, 1.0, false, As);           // v_rd = P^T (...)
+      cta_gemm_t<kD>(r, r, 1, C, 0, xr, x2, nrhs, 1.0, false, As);           // v_rd = P^T (...)
       xo = x2;
     } else {
       bwd_subst(C, r, xr, nrhs);
     }
-    if (k > 0) cta_gemm(k, r, 2, T, r, xo, xs, nrhs, -1.0, true, As);  // v_sk -= T v_rd
+    if (k > 0) cta_gemm_t<kD>(k, r, 2, T, r, xo, xs, nrhs, -1.0, true, As);  // v_sk -= T v_rd
   }
   __syncthreads();
   for (int e = threadIdx.x; e < k * nrhs; e += NT) {
@@ -592,9 +700,13 @@ void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, c
                            double* v, int nrhs, double* contrib, double* scratch,
                            int64_t scratch_per_rec, size_t smem, cudaStream_t s) {
   if (nrec <= 0) return;
-  static bool once = (set_smem_attr((const void*)solve_elim_fwd_kernel), true);
+  static bool once = (set_smem_attr((const void*)solve_elim_fwd_kernel<false>),
+                      set_smem_attr((const void*)solve_elim_fwd_kernel<true>), true);
   (void)once;
-  solve_elim_fwd_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib, scratch, scratch_per_rec);
+  if (nrhs >= kDmmaMinRhs)
+    solve_elim_fwd_kernel<true><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib, scratch, scratch_per_rec);
+  else
+    solve_elim_fwd_kernel<false><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib, scratch, scratch_per_rec);
 }
 
 void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,
@@ -610,18 +722,26 @@ void launch_solve_elim_bwd(const SolveRec* recs, int nrec, const int32_t* idx, c
                            double* v, int nrhs, double* scratch, int64_t scratch_per_rec,
                            size_t smem, cudaStream_t s) {
   if (nrec <= 0) return;
-  static bool once = (set_smem_attr((const void*)solve_elim_bwd_kernel), true);
+  static bool once = (set_smem_attr((const void*)solve_elim_bwd_kernel<false>),
+                      set_smem_attr((const void*)solve_elim_bwd_kernel<true>), true);
   (void)once;
-  solve_elim_bwd_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, scratch, scratch_per_rec);
+  if (nrhs >= kDmmaMinRhs)
+    solve_elim_bwd_kernel<true><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, scratch, scratch_per_rec);
+  else
+    solve_elim_bwd_kernel<false><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, scratch, scratch_per_rec);
 }
 
 void launch_solve_skel(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
                        double* v, int nrhs, int forward, double* scratch,
                        int64_t scratch_per_rec, size_t smem, cudaStream_t s) {
   if (nrec <= 0) return;
-  static bool once = (set_smem_attr((const void*)solve_skel_kernel), true);
+  static bool once = (set_smem_attr((const void*)solve_skel_kernel<false>),
+                      set_smem_attr((const void*)solve_skel_kernel<true>), true);
   (void)once;
-  solve_skel_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward, scratch, scratch_per_rec);
+  if (nrhs >= kDmmaMinRhs)
+    solve_skel_kernel<true><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward, scratch, scratch_per_rec);
+  else
+    solve_skel_kernel<false><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward, scratch, scratch_per_rec);
 }
 
 void launch_apply_elim(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v, int nrhs,

@@ -13,8 +13,9 @@ for _ in range(3):
     f.apply_inverse_device(b.data_ptr(), x.data_ptr(), nrhs)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
+st = torch.cuda.Stream()  # events and solves on one non-default stream
+e0.record(st)
 for _ in range(5):
-    f.apply_inverse_device(b.data_ptr(), x.data_ptr(), nrhs, torch.cuda.current_stream().cuda_stream)
-e1.record(); torch.cuda.synchronize()
+    f.apply_inverse_device(b.data_ptr(), x.data_ptr(), nrhs, st.cuda_stream)
+e1.record(st); torch.cuda.synchronize()
 print("solve ms", e0.elapsed_time(e1) / 5)
