@@ -269,6 +269,7 @@ def run_gpu(args, world, rank, local):
         "resid": resid, "skeleton_counts": [c for _, c in skel],
     }
     line["roofline"] = roofline(level_info, pk, pk_kind, args)
+    line["roofline_by_class"] = roofline_classes(level_info, pk)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
@@ -403,12 +404,31 @@ def run_sharded(args, world, rank, local):
         "skeleton_counts": [c for _, c in skel], "xfer_bytes_rank0": int(xfer),
     }
     line["roofline"] = roofline(level_info, pk, pk_kind, args)
+    line["roofline_by_class"] = roofline_classes(level_info, pk)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
     if dist:
         dist.destroy_process_group()
+
+
+def roofline_classes(level_info, pk, fp64_tflops=35.5):
+    """Whole-class fractions: the algorithmic bytes / FLOPs of
+    all elimination levels, all skeletonization levels and the terminal block,
+    over their summed CUDA-event time, against the HBM copy roof and the
+    measured DGEMM roof (profiles/r01_fp64_peak.json)."""
+    out = {}
+    for name, kinds in (("elimination", (0,)), ("skeletonization", (1,)), ("terminal", (2,))):
+        lv = [d for d in level_info if d["kind"] in kinds]
+        sec = sum(d["gpu_seconds"] for d in lv)
+        gb = sum(d["gbytes"] for d in lv)
+        gf = sum(d["gflop"] for d in lv)
+        if sec <= 0:
+            continue
+        out[name] = {"gpu_ms": sec * 1e3, "gb_per_s": gb / sec, "tflops": gf / sec * 1e-3,
+                     "hbm_frac": gb / sec / pk.get("hbm_gbs", 6556.0), "fp64_frac": gf / sec * 1e-3 / fp64_tflops}
+    return out
 
 
 def roofline(level_info, pk, pk_kind, args):
