@@ -1379,6 +1379,7 @@ struct Factorizer {
     }
     HTRACE("  host updates done (%zu small / %zu big / %zu tiles)", small.size(), big.size(), tiles.size());
     // uploads
+    L.lap("e-lists");
     DBuf<ElimTask> d_small, d_big;
     DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd;
     DBuf<int32_t> d_pcells;
@@ -1408,6 +1409,7 @@ struct Factorizer {
     const char* what = is_top ? "top block" : "cell";
     pending.push_back({st_small, (int64_t)small.size(), tag, what});
     pending.push_back({st_big, (int64_t)big.size(), tag, what});
+    L.lap("e-uploads");
     Arenas A = arenas_for(r);
     if (!small.empty()) {
       A.status = status.p + st_small;
@@ -1436,6 +1438,7 @@ struct Factorizer {
       launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
       g_launches += 1 + inv.launch(d_big.p, A, s);
     }
+    L.lap("e-launches");
     d_small.release(s);
     d_big.release(s);
     d_tiles.release(s);
