@@ -181,6 +181,10 @@ void launch_skelbig_symm(const SkelBigTask* tasks, const int4* work, int nwork, 
                          cudaStream_t s);
 
 // solve
+// small elimination records (nc, nq <= 64, 2..16 RHS): one shared-memory load phase
+size_t solve_small_smem(int max_nc, int max_nq, int nrhs);
+void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
+                             int nrhs, double* contrib, size_t smem, int forward, cudaStream_t s);
 void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac,
                            double* v, int nrhs, double* contrib, double* scratch,
                            int64_t scratch_per_rec, size_t smem, cudaStream_t s);

@@ -399,6 +399,104 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small elimination records (nc, nq <= 64, 2..16 right-hand sides: the fine
+// levels, thousands of cells).  Every load of the record -- P, W and the
+// gathered rows of v -- is issued up front into shared memory with one
+// barrier, so a CTA exposes one memory latency instead of one per product
+// phase.  The products sum in the same order as cta_gemm (including its zero
+// terms of the triangular factor), so results are bit-identical to the
+// general kernels.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) solve_elim_fwd_small_kernel(const SolveRec* __restrict__ recs,
+                                                                  const int32_t* __restrict__ idx,
+                                                                  const double* __restrict__ fac,
+                                                                  double* __restrict__ v, int nrhs,
+                                                                  double* __restrict__ contrib) {
+  extern __shared__ __align__(16) double sm[];
+  const SolveRec rc = recs[blockIdx.x];
+  const int nc = rc.nc, nq = rc.nq;
+  const int np = nc * (nc + 1) / 2;
+  double* sP = sm;
+  double* sW = sP + np;
+  double* sx = sW + (size_t)nc * nq;
+  double* ss = sx + (size_t)nc * nrhs;
+  const int32_t* c = idx + rc.idx_off;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < np; e += NT) sP[e] = P[e];
+  for (int e = threadIdx.x; e < nc * nq; e += NT) sW[e] = W[e];
+  for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    sx[e] = v[(size_t)c[i] * nrhs + r];
+  }
+  __syncthreads();
+  // s = P x_c
+  for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    const double* Pi = sP + i * (i + 1) / 2;
+    double acc = 0.0;
+    for (int k = 0; k < nc; ++k) acc += (k <= i ? Pi[k] : 0.0) * sx[k * nrhs + r];
+    const double y = 0.0 + 1.0 * acc;
+    ss[e] = y;
+    v[(size_t)c[i] * nrhs + r] = y;
+  }
+  __syncthreads();
+  // contributions g = W^T s
+  double* g = contrib + (size_t)rc.contrib_off * nrhs;
+  for (int e = threadIdx.x; e < nq * nrhs; e += NT) {
+    const int b = e / nrhs, r = e - b * nrhs;
+    double acc = 0.0;
+    for (int k = 0; k < nc; ++k) acc += sW[k * nq + b] * ss[k * nrhs + r];
+    g[e] = 0.0 + 1.0 * acc;
+  }
+}
+
+__global__ void __launch_bounds__(NT) solve_elim_bwd_small_kernel(const SolveRec* __restrict__ recs,
+                                                                  const int32_t* __restrict__ idx,
+                                                                  const double* __restrict__ fac,
+                                                                  double* __restrict__ v, int nrhs) {
+  extern __shared__ __align__(16) double sm[];
+  const SolveRec rc = recs[blockIdx.x];
+  const int nc = rc.nc, nq = rc.nq;
+  const int np = nc * (nc + 1) / 2;
+  double* sP = sm;
+  double* sW = sP + np;
+  double* st = sW + (size_t)nc * nq;
+  double* sq = st + (size_t)nc * nrhs;
+  const int32_t* c = idx + rc.idx_off;
+  const int32_t* q = c + nc;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < np; e += NT) sP[e] = P[e];
+  for (int e = threadIdx.x; e < nc * nq; e += NT) sW[e] = W[e];
+  for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    st[e] = v[(size_t)c[i] * nrhs + r];
+  }
+  for (int e = threadIdx.x; e < nq * nrhs; e += NT) {
+    const int b = e / nrhs, r = e - b * nrhs;
+    sq[e] = v[(size_t)q[b] * nrhs + r];
+  }
+  __syncthreads();
+  // t = v_c - W v_q
+  if (nq > 0)
+    for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+      const int i = e / nrhs, r = e - i * nrhs;
+      double acc = 0.0;
+      for (int b = 0; b < nq; ++b) acc += sW[i * nq + b] * sq[b * nrhs + r];
+      st[e] = st[e] + -1.0 * acc;
+    }
+  __syncthreads();
+  // v_c = P^T t
+  for (int e = threadIdx.x; e < nc * nrhs; e += NT) {
+    const int i = e / nrhs, r = e - i * nrhs;
+    double acc = 0.0;
+    for (int k = 0; k < nc; ++k) acc += (k >= i ? sP[k * (k + 1) / 2 + i] : 0.0) * st[k * nrhs + r];
+    v[(size_t)c[i] * nrhs + r] = 0.0 + 1.0 * acc;
+  }
+}
+
 // Skeleton record: idx = sk[k] then rd[r]; T (k x r), C (r x r), W (r x k).
 //   forward  (apply_ut): v_rd -= T^T v_sk ; s = C^-1 v_rd ; v_sk -= W^T s ; v_rd = s
 //   backward (apply_u) : v_rd = C^-T (v_rd - W v_sk) ; v_sk -= T v_rd
@@ -707,6 +805,24 @@ void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, c
     solve_elim_fwd_kernel<true><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib, scratch, scratch_per_rec);
   else
     solve_elim_fwd_kernel<false><<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib, scratch, scratch_per_rec);
+}
+
+size_t solve_small_smem(int max_nc, int max_nq, int nrhs) {
+  return sizeof(double) * ((size_t)max_nc * (max_nc + 1) / 2 + (size_t)max_nc * max_nq + 2 * (size_t)max_nc * nrhs +
+                           (size_t)max_nq * nrhs);
+}
+
+void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
+                             int nrhs, double* contrib, size_t smem, int forward, cudaStream_t s) {
+  if (nrec <= 0) return;
+  static bool once = (cudaFuncSetAttribute(solve_elim_fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmemCapBytes),
+                      cudaFuncSetAttribute(solve_elim_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmemCapBytes),
+                      true);
+  (void)once;
+  if (forward) solve_elim_fwd_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib);
+  else solve_elim_bwd_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs);
 }
 
 void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,

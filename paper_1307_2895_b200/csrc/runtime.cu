@@ -3023,6 +3023,13 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   }
   double* scratch = nullptr;
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
+  // fine elimination levels: the single-load-phase kernels
+  static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
+  static const int small_max_rhs = getenv("HIFDE_SOLVE_SMALL_RHS") ? atoi(getenv("HIFDE_SOLVE_SMALL_RHS")) : 64;
+  auto small_path = [&](const LevelRec& L) {
+    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
+           solve_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
+  };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
   auto phases = [&](const std::vector<LevelRec::Phase>& ph) {
@@ -3041,7 +3048,14 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
       if (nr) { launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s); ++g_launches; }
       phases(L.fwd_ph);
     } else {
-      if (nr) { launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s); ++g_launches; }
+      if (nr && small_path(L)) {
+        launch_solve_elim_small(L.d_recs, nr, idx, fac, v, nrhs, contrib, solve_small_smem(L.max_nc, L.max_nq, nrhs),
+                                1, s);
+        ++g_launches;
+      } else if (nr) {
+        launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s);
+        ++g_launches;
+      }
       phases(L.fwd_ph);
       if (L.kind == 0 && L.ntargets) {
         launch_solve_reduce(L.d_targets, L.d_ptr, L.d_ent, L.ntargets, contrib, v, nrhs, s);
@@ -3057,7 +3071,14 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     if (L.kind == 1) {
       if (nr) { launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s); ++g_launches; }
     } else {
-      if (nr) { launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s); ++g_launches; }
+      if (nr && small_path(L)) {
+        launch_solve_elim_small(L.d_recs, nr, idx, fac, v, nrhs, nullptr, solve_small_smem(L.max_nc, L.max_nq, nrhs),
+                                0, s);
+        ++g_launches;
+      } else if (nr) {
+        launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s);
+        ++g_launches;
+      }
     }
     phases(L.bwd_ph);
   }
@@ -3091,6 +3112,13 @@ void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, boo
   for (const auto& L : F->levels) { size_t a; int64_t b; plan(L, a, b); }
   double* scratch = nullptr;
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
+  // fine elimination levels: the single-load-phase kernels
+  static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
+  static const int small_max_rhs = getenv("HIFDE_SOLVE_SMALL_RHS") ? atoi(getenv("HIFDE_SOLVE_SMALL_RHS")) : 64;
+  auto small_path = [&](const LevelRec& L) {
+    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
+           solve_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
+  };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
   const size_t nl = F->levels.size();
