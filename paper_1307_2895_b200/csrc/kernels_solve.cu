@@ -497,6 +497,102 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_small_kernel(const SolveRec
   }
 }
 
+// Small skeleton records (r, k <= 64): the same single-load-phase scheme,
+// bit-identical to solve_skel_kernel's products.
+__global__ void __launch_bounds__(NT) solve_skel_small_kernel(const SolveRec* __restrict__ recs,
+                                                              const int32_t* __restrict__ idx,
+                                                              const double* __restrict__ fac,
+                                                              double* __restrict__ v, int nrhs, int forward) {
+  extern __shared__ __align__(16) double sm[];
+  const SolveRec rc = recs[blockIdx.x];
+  const int r = rc.nc, k = rc.nq;
+  const int np = r * (r + 1) / 2;
+  double* sT = sm;                          // k x r
+  double* sP = sT + (size_t)k * r;          // packed r x r
+  double* sW = sP + np;                     // r x k
+  double* xs = sW + (size_t)r * k;          // k x nrhs
+  double* xr = xs + (size_t)k * nrhs;       // r x nrhs
+  double* x2 = xr + (size_t)r * nrhs;       // r x nrhs
+  const int32_t* sk = idx + rc.idx_off;
+  const int32_t* rd = sk + k;
+  const double* T = fac + rc.T_off;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < k * r; e += NT) sT[e] = T[e];
+  for (int e = threadIdx.x; e < np; e += NT) sP[e] = P[e];
+  for (int e = threadIdx.x; e < r * k; e += NT) sW[e] = W[e];
+  for (int e = threadIdx.x; e < k * nrhs; e += NT) {
+    const int a = e / nrhs, j = e - a * nrhs;
+    xs[e] = v[(size_t)sk[a] * nrhs + j];
+  }
+  for (int e = threadIdx.x; e < r * nrhs; e += NT) {
+    const int b = e / nrhs, j = e - b * nrhs;
+    xr[e] = v[(size_t)rd[b] * nrhs + j];
+  }
+  __syncthreads();
+  if (forward) {
+    if (k > 0) {  // v_rd -= T^T v_sk
+      for (int e = threadIdx.x; e < r * nrhs; e += NT) {
+        const int i = e / nrhs, j = e - i * nrhs;
+        double acc = 0.0;
+        for (int l = 0; l < k; ++l) acc += sT[l * r + i] * xs[l * nrhs + j];
+        xr[e] = xr[e] + -1.0 * acc;
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < r * nrhs; e += NT) {  // s = P v_rd
+      const int i = e / nrhs, j = e - i * nrhs;
+      const double* Pi = sP + i * (i + 1) / 2;
+      double acc = 0.0;
+      for (int l = 0; l < r; ++l) acc += (l <= i ? Pi[l] : 0.0) * xr[l * nrhs + j];
+      x2[e] = 0.0 + 1.0 * acc;
+    }
+    __syncthreads();
+    if (k > 0) {  // v_sk -= W^T s
+      for (int e = threadIdx.x; e < k * nrhs; e += NT) {
+        const int i = e / nrhs, j = e - i * nrhs;
+        double acc = 0.0;
+        for (int l = 0; l < r; ++l) acc += sW[l * k + i] * x2[l * nrhs + j];
+        xs[e] = xs[e] + -1.0 * acc;
+      }
+    }
+  } else {
+    if (k > 0) {  // v_rd -= W v_sk
+      for (int e = threadIdx.x; e < r * nrhs; e += NT) {
+        const int i = e / nrhs, j = e - i * nrhs;
+        double acc = 0.0;
+        for (int l = 0; l < k; ++l) acc += sW[i * k + l] * xs[l * nrhs + j];
+        xr[e] = xr[e] + -1.0 * acc;
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < r * nrhs; e += NT) {  // v_rd = P^T (...)
+      const int i = e / nrhs, j = e - i * nrhs;
+      double acc = 0.0;
+      for (int l = 0; l < r; ++l) acc += (l >= i ? sP[l * (l + 1) / 2 + i] : 0.0) * xr[l * nrhs + j];
+      x2[e] = 0.0 + 1.0 * acc;
+    }
+    __syncthreads();
+    if (k > 0) {  // v_sk -= T v_rd
+      for (int e = threadIdx.x; e < k * nrhs; e += NT) {
+        const int i = e / nrhs, j = e - i * nrhs;
+        double acc = 0.0;
+        for (int l = 0; l < r; ++l) acc += sT[i * r + l] * x2[l * nrhs + j];
+        xs[e] = xs[e] + -1.0 * acc;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * nrhs; e += NT) {
+    const int a = e / nrhs, j = e - a * nrhs;
+    v[(size_t)sk[a] * nrhs + j] = xs[e];
+  }
+  for (int e = threadIdx.x; e < r * nrhs; e += NT) {
+    const int b = e / nrhs, j = e - b * nrhs;
+    v[(size_t)rd[b] * nrhs + j] = x2[e];
+  }
+}
+
 // Skeleton record: idx = sk[k] then rd[r]; T (k x r), C (r x r), W (r x k).
 //   forward  (apply_ut): v_rd -= T^T v_sk ; s = C^-1 v_rd ; v_sk -= W^T s ; v_rd = s
 //   backward (apply_u) : v_rd = C^-T (v_rd - W v_sk) ; v_sk -= T v_rd
@@ -823,6 +919,21 @@ void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx,
   (void)once;
   if (forward) solve_elim_fwd_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib);
   else solve_elim_bwd_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs);
+}
+
+size_t solve_skel_small_smem(int max_r, int max_k, int nrhs) {
+  return sizeof(double) * (2 * (size_t)max_k * max_r + (size_t)max_r * (max_r + 1) / 2 + (size_t)max_k * nrhs +
+                           2 * (size_t)max_r * nrhs);
+}
+
+void launch_solve_skel_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
+                             int nrhs, size_t smem, int forward, cudaStream_t s) {
+  if (nrec <= 0) return;
+  static bool once = (cudaFuncSetAttribute(solve_skel_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmemCapBytes),
+                      true);
+  (void)once;
+  solve_skel_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward);
 }
 
 void launch_solve_reduce(const int32_t* targets, const int64_t* ptr, const int64_t* ent,

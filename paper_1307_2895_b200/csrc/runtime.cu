@@ -3030,6 +3030,10 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
            solve_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
   };
+  auto small_skel = [&](const LevelRec& L) {
+    return !no_small && L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
+           solve_skel_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
+  };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
   auto phases = [&](const std::vector<LevelRec::Phase>& ph) {
@@ -3045,7 +3049,14 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
     if (L.kind == 1) {
-      if (nr) { launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s); ++g_launches; }
+      if (nr && small_skel(L)) {
+        launch_solve_skel_small(L.d_recs, nr, idx, fac, v, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 1,
+                                s);
+        ++g_launches;
+      } else if (nr) {
+        launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s);
+        ++g_launches;
+      }
       phases(L.fwd_ph);
     } else {
       if (nr && small_path(L)) {
@@ -3069,7 +3080,14 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
     if (L.kind == 1) {
-      if (nr) { launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s); ++g_launches; }
+      if (nr && small_skel(L)) {
+        launch_solve_skel_small(L.d_recs, nr, idx, fac, v, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 0,
+                                s);
+        ++g_launches;
+      } else if (nr) {
+        launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s);
+        ++g_launches;
+      }
     } else {
       if (nr && small_path(L)) {
         launch_solve_elim_small(L.d_recs, nr, idx, fac, v, nrhs, nullptr, solve_small_smem(L.max_nc, L.max_nq, nrhs),
