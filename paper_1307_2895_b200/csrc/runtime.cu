@@ -3026,13 +3026,16 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   // fine elimination levels: the single-load-phase kernels
   static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
   static const int small_max_rhs = getenv("HIFDE_SOLVE_SMALL_RHS") ? atoi(getenv("HIFDE_SOLVE_SMALL_RHS")) : 64;
+  static const int small_max_n = getenv("HIFDE_SOLVE_SMALL_N") ? atoi(getenv("HIFDE_SOLVE_SMALL_N")) : 96;
+  static const size_t small_max_smem = getenv("HIFDE_SOLVE_SMALL_SMEM") ? (size_t)atoi(getenv("HIFDE_SOLVE_SMALL_SMEM")) * 1024
+                                                                          : (size_t)200 * 1024;
   auto small_path = [&](const LevelRec& L) {
-    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
-           solve_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
+    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+           L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   auto small_skel = [&](const LevelRec& L) {
-    return !no_small && L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
-           solve_skel_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
+    return !no_small && L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+           L.max_nq <= 2 * small_max_n && solve_skel_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
@@ -3133,9 +3136,12 @@ void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, boo
   // fine elimination levels: the single-load-phase kernels
   static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
   static const int small_max_rhs = getenv("HIFDE_SOLVE_SMALL_RHS") ? atoi(getenv("HIFDE_SOLVE_SMALL_RHS")) : 64;
+  static const int small_max_n = getenv("HIFDE_SOLVE_SMALL_N") ? atoi(getenv("HIFDE_SOLVE_SMALL_N")) : 96;
+  static const size_t small_max_smem = getenv("HIFDE_SOLVE_SMALL_SMEM") ? (size_t)atoi(getenv("HIFDE_SOLVE_SMALL_SMEM")) * 1024
+                                                                          : (size_t)200 * 1024;
   auto small_path = [&](const LevelRec& L) {
-    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= 64 && L.max_nq <= 64 &&
-           solve_small_smem(L.max_nc, L.max_nq, nrhs) <= (size_t)112 * 1024;
+    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+           L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
