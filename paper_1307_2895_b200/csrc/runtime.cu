@@ -3133,16 +3133,6 @@ void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, boo
   for (const auto& L : F->levels) { size_t a; int64_t b; plan(L, a, b); }
   double* scratch = nullptr;
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
-  // fine elimination levels: the single-load-phase kernels
-  static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
-  static const int small_max_rhs = getenv("HIFDE_SOLVE_SMALL_RHS") ? atoi(getenv("HIFDE_SOLVE_SMALL_RHS")) : 64;
-  static const int small_max_n = getenv("HIFDE_SOLVE_SMALL_N") ? atoi(getenv("HIFDE_SOLVE_SMALL_N")) : 96;
-  static const size_t small_max_smem = getenv("HIFDE_SOLVE_SMALL_SMEM") ? (size_t)atoi(getenv("HIFDE_SOLVE_SMALL_SMEM")) * 1024
-                                                                          : (size_t)200 * 1024;
-  auto small_path = [&](const LevelRec& L) {
-    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
-           L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
-  };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
   const size_t nl = F->levels.size();
