@@ -688,6 +688,12 @@ struct Factorizer {
       helper.drain();
     } catch (...) {
     }
+    if (tail_s) {
+      cudaStreamSynchronize(tail_s);
+      cudaStreamDestroy(tail_s);
+      cudaEventDestroy(ev_id);
+      cudaEventDestroy(ev_tail);
+    }
   }
   LevelRec prof;  // setup / finish phase timings
   MetaPack meta;  // solve metadata, uploaded once at the end
@@ -761,6 +767,30 @@ struct Factorizer {
   DBuf<int> agree;                  // status agreement scalar
   DBuf<double> gpart;               // split-tile partials of the Gram matrices
   std::vector<uint8_t> own_;        // owner rank per group of the current level
+  // Large-group pipelines: the tail of a batch (T, congruence, inner
+  // elimination, inverse) runs on a second stream while the next batch's
+  // assembly and ID proceed on the main one -- the next batch depends only on
+  // the ranks and the retired rows, not on the tail.
+  cudaStream_t tail_s = nullptr;
+  cudaEvent_t ev_id = nullptr, ev_tail = nullptr;
+  bool tail_pending = false;
+  cudaStream_t tail_stream() {
+    static const bool off = getenv("HIFDE_NO_TAIL_STREAM") != nullptr;
+    if (off) return s;
+    if (!tail_s) {
+      HCK(cudaStreamCreateWithFlags(&tail_s, cudaStreamNonBlocking));
+      HCK(cudaEventCreateWithFlags(&ev_id, cudaEventDisableTiming));
+      HCK(cudaEventCreateWithFlags(&ev_tail, cudaEventDisableTiming));
+    }
+    return tail_s;
+  }
+  // main stream waits for every tail issued so far
+  void join_tails() {
+    if (!tail_pending || !tail_s) return;
+    HCK(cudaEventRecord(ev_tail, tail_s));
+    HCK(cudaStreamWaitEvent(s, ev_tail, 0));
+    tail_pending = false;
+  }
   int64_t xfer_blocks = 0, xfer_bytes = 0;  // totals (metrics)
 
   bool sharded() const { return comm != nullptr && P > 1; }
@@ -2054,6 +2084,7 @@ struct Factorizer {
       merge(huge, bh[b0], bh[b1]);
       if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  batch %d done", b); }
     }
+    join_tails();  // the delta blocks and records of every tail before the level ends
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
     L.t_launch = now_s() - tp;
@@ -2396,35 +2427,44 @@ struct Factorizer {
     }
     if (split_t) HCK(cudaEventRecord(pe[2], s));
     launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
-    launch_skelbig_tinit(dtk, d10.p, (int)wrow.size(), A, s);
+    // the tail: on the tail stream once the ID, the sort and this batch's
+    // uploads (all on the main stream) are done
+    const cudaStream_t ts = tail_stream();
+    if (ts != s) {
+      HCK(cudaEventRecord(ev_id, s));
+      HCK(cudaStreamWaitEvent(ts, ev_id, 0));
+      tail_pending = true;
+    }
+    launch_skelbig_tinit(dtk, d10.p, (int)wrow.size(), A, ts);
     for (int bb = ntb - 1; bb >= 0; --bb) {
-      launch_skelbig_tsolve(dtk, d2.p, (int)wt.size(), bb * 64, A, s);
-      launch_skelbig_tupdate(dtk, d11.p + tuo[(size_t)bb], (int)(tuo[(size_t)bb + 1] - tuo[(size_t)bb]), bb * 64, A, s);
+      launch_skelbig_tsolve(dtk, d2.p, (int)wt.size(), bb * 64, A, ts);
+      launch_skelbig_tupdate(dtk, d11.p + tuo[(size_t)bb], (int)(tuo[(size_t)bb + 1] - tuo[(size_t)bb]), bb * 64, A, ts);
       g_launches += 2;
     }
-    launch_skelbig_tperm(dtk, d10.p, (int)wrow.size(), A, s);
-    launch_skelbig_congruence(dtk, d3.p, (int)wc0.size(), A, s);
-    launch_skelbig_congruence(dtk, d4.p, (int)wc1.size(), A, s);
-    launch_skelbig_symm(dtk, d5.p, (int)wsym.size(), A, dscale, s);
+    launch_skelbig_tperm(dtk, d10.p, (int)wrow.size(), A, ts);
+    launch_skelbig_congruence(dtk, d3.p, (int)wc0.size(), A, ts);
+    launch_skelbig_congruence(dtk, d4.p, (int)wc1.size(), A, ts);
+    launch_skelbig_symm(dtk, d5.p, (int)wsym.size(), A, dscale, ts);
     g_launches += 7;
     for (int p = 0; p < npanel; ++p) {
       const int p0 = p * kPanelB;
-      launch_panel_chol(inner, d9.p + pco[(size_t)p], (int)(pco[(size_t)p + 1] - pco[(size_t)p]), p0, AH, dmin, s);
-      launch_panel_trsm(inner, d6.p + pto[(size_t)p], (int)(pto[(size_t)p + 1] - pto[(size_t)p]), p0, AH, s);
-      launch_panel_update(inner, d7.p + puo[(size_t)p], (int)(puo[(size_t)p + 1] - puo[(size_t)p]), p0, AH, s);
+      launch_panel_chol(inner, d9.p + pco[(size_t)p], (int)(pco[(size_t)p + 1] - pco[(size_t)p]), p0, AH, dmin, ts);
+      launch_panel_trsm(inner, d6.p + pto[(size_t)p], (int)(pto[(size_t)p + 1] - pto[(size_t)p]), p0, AH, ts);
+      launch_panel_update(inner, d7.p + puo[(size_t)p], (int)(puo[(size_t)p + 1] - puo[(size_t)p]), p0, AH, ts);
       g_launches += 3;
     }
-    launch_schur_tiles(inner, d8.p, (int)tiles.size(), AH, s);
-    launch_big_finish(inner, n, AH, dmin, dscale, s);
+    launch_schur_tiles(inner, d8.p, (int)tiles.size(), AH, ts);
+    launch_big_finish(inner, n, AH, dmin, dscale, ts);
     if (trace_on()) {
-      HCK(cudaStreamSynchronize(s));
+      HCK(cudaStreamSynchronize(ts));
       HTRACE("    huge: factor done (%d groups)", n);
     }
-    g_launches += inv.launch(inner, AH, s);
-    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("    huge: inverse done (%zu loc / %zu diag / %zu tiles)", inv.loc.size(), inv.diag.size(), inv.tiles.size()); }
+    g_launches += inv.launch(inner, AH, ts);
+    if (trace_on()) { HCK(cudaStreamSynchronize(ts)); HTRACE("    huge: inverse done (%zu loc / %zu diag / %zu tiles)", inv.loc.size(), inv.diag.size(), inv.tiles.size()); }
     g_launches += 2;
     HCK(cudaGetLastError());
     if (split_t) {
+      join_tails();
       HCK(cudaEventRecord(pe[3], s));
       HCK(cudaStreamSynchronize(s));
       float t01 = 0.f, t12 = 0.f, t23 = 0.f;
@@ -2434,9 +2474,10 @@ struct Factorizer {
       fprintf(stderr, "[hifde]   assemble %.3f cpqr %.3f rest %.3f ms\n", t01, t12, t23);
       for (auto& e : pe) cudaEventDestroy(e);
     }
-    for (auto* d : {&d1, &d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(s);
-    inv.release(s);
-    d9.release(s);
+    d1.release(s);
+    for (auto* d : {&d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(ts);  // tail-stream order
+    inv.release(ts);
+    d9.release(ts);
   }
 
   // Split a level's records: large ones (by size) become tiled product phases
