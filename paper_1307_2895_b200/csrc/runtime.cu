@@ -1597,6 +1597,7 @@ struct Factorizer {
     };
     std::vector<Sz> sz((size_t)nt);
     std::vector<uint8_t> promote((size_t)nt, 0);
+    static const double promote_work = getenv("HIFDE_PROMOTE_WORK") ? atof(getenv("HIFDE_PROMOTE_WORK")) : kPromoteWork;
     std::vector<std::vector<int32_t>> tpred((size_t)nthreads);
     const int nthr = nt >= 256 ? nthreads : 1;
 #pragma omp parallel num_threads(nthr)
@@ -1651,7 +1652,7 @@ struct Factorizer {
         // one-CTA groups the Gram path can take keep room for the large-group
         // record: they join the large-group pipeline in exact batches
         // (promote[] below), where a one-CTA launch per batch would be exposed
-        promote[(size_t)t] = (T.mode == 1 || T.mode == 3) && (double)nq * nc * nc >= kPromoteWork && gram_ok(nc, nq);
+        promote[(size_t)t] = (T.mode == 1 || T.mode == 3) && (double)nq * nc * nc >= promote_work && gram_ok(nc, nq);
         z.fac = (size_t)nc * nc + 2 * q4 +
                 ((T.mode == 2 || promote[(size_t)t]) ? (size_t)nc * (nc + 1) / 2 + nc : 0);
         const size_t p0 = mypred.size();
