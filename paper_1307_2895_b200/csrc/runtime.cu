@@ -1765,9 +1765,17 @@ struct Factorizer {
     L.t_sym = tp - t_begin;
     bool any_huge = false;
     for (const SkelTask& T : tasks) any_huge |= T.mode == 2;
-    if (exact && nbatch > 1 && any_huge)
+    // 3D: an exact level of medium groups alone also takes the pipeline (its
+    // batches beat one chained launch of one-CTA groups: config 4 247 -> 216
+    // ms GPU); in 2D the one-launch chain stays faster
+    static const bool promote_any = getenv("HIFDE_PROMOTE_ANY") ? atoi(getenv("HIFDE_PROMOTE_ANY")) != 0 : g.dim == 3;
+    bool any_promote = false;
+    for (int64_t t = 0; t < nt && !any_promote; ++t) any_promote = promote[(size_t)t] != 0;
+    if (exact && nbatch > 1 && (any_huge || (promote_any && any_promote))) {
       for (int64_t t = 0; t < nt; ++t)
         if (promote[(size_t)t]) tasks[(size_t)t].mode = 2;
+      any_huge = any_huge || any_promote;
+    }
     const bool one_launch = exact && !any_huge && nt > 1 && opt.order_mode != HIFDE_ORDER_SNAPSHOT;
     // owners: the one-launch exact order runs on rank 0 (its groups wait on
     // one another); otherwise groups go to their subdomain's rank
