@@ -732,6 +732,95 @@ __global__ void __launch_bounds__(256) pchol_mc_kernel(const SkelBigTask* __rest
   if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
 }
 
+// One-CTA variant for groups whose R fits in shared memory (nc <= ~158):
+// no inter-CTA barrier, one block barrier per pivot step.  Per column the
+// sums are those of pchol_mc_kernel (warp per column, lanes over l, the same
+// butterfly), and the pivot rule is the same, so the results are identical.
+__global__ void __launch_bounds__(256) pchol_1cta_kernel(const SkelBigTask* __restrict__ tasks, Arenas A,
+                                                         double eps) {
+  extern __shared__ __align__(16) double psm[];
+  __shared__ double wbest[2][8];
+  __shared__ int widx[2][8];
+  const SkelBigTask t = tasks[blockIdx.x];
+  const int nc = t.nc, nq = t.nq;
+  const BigWs w = big_ws(t, A);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Rs = psm;                   // R(l, j) at l * nc + j
+  double* dd = Rs + (size_t)nc * nc;  // Schur diagonal (< 0: pivoted)
+  for (int j = threadIdx.x; j < nc; j += 256) dd[j] = w.G[(size_t)j + (size_t)j * nc];
+  __syncthreads();
+  // warp-level best of this warp's columns (c = wid, wid + 8, ...) -> slot
+  auto post = [&](int slot) {
+    double bv = -1.0;
+    int bi = nc;
+    for (int j = wid + 8 * lane; j < nc; j += 256)
+      if (dd[j] > bv) { bv = dd[j]; bi = j; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { wbest[slot][wid] = bv; widx[slot][wid] = bi; }
+  };
+  post(0);
+  __syncthreads();
+  double thr = 0.0;
+  int k = nc;
+  for (int i = 0; i < nc; ++i) {
+    const int slot = i & 1;
+    double dP = wbest[slot][0];
+    int P = widx[slot][0];
+    for (int q = 1; q < 8; ++q)
+      if (wbest[slot][q] > dP || (wbest[slot][q] == dP && widx[slot][q] < P)) { dP = wbest[slot][q]; P = widx[slot][q]; }
+    if (i == 0 && !(dP > 0.0)) { k = 0; break; }
+    const double rii = sqrt(dP > 0.0 ? dP : 0.0);
+    if (i == 0) thr = eps * rii;
+    if (rii <= thr || P >= nc) { k = i; break; }
+    if (threadIdx.x == 0) {
+      w.rdiag[i] = rii;
+      w.piv[i] = P;
+    }
+    const double inv = 1.0 / rii;
+    // columns of warp wid: j = wid, wid + 8, ... (the post() ownership)
+    for (int j = wid; j < nc; j += 8) {
+      if (dd[j] < 0.0) continue;
+      if (j == P) {
+        __syncwarp();
+        if (lane == 0) dd[j] = -1.0;
+        continue;
+      }
+      double sacc = 0.0;
+      for (int l = lane; l < i; l += 32) sacc += Rs[(size_t)l * nc + P] * Rs[(size_t)l * nc + j];
+      sacc = warp_sum(sacc);
+      const double rij = (__ldg(w.G + (size_t)j + (size_t)P * nc) - sacc) * inv;
+      __syncwarp();
+      if (lane == 0) {
+        Rs[(size_t)i * nc + j] = rij;
+        w.Mq[(size_t)i + (size_t)j * nq] = rij;
+        const double nd = dd[j] - rij * rij;
+        dd[j] = nd > 0.0 ? nd : 0.0;
+      }
+      __syncwarp();
+    }
+    post(slot ^ 1);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) A.kout[t.group] = k;
+}
+
+size_t pchol_1cta_smem(int nc) { return sizeof(double) * ((size_t)nc * nc + (size_t)nc); }
+
+void launch_pchol_1cta(const SkelBigTask* tasks, int ntasks, size_t smem, const Arenas& A, double eps,
+                       cudaStream_t s) {
+  if (ntasks <= 0) return;
+  static bool once = (cudaFuncSetAttribute(pchol_1cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmemCapBytes),
+                      true);
+  (void)once;
+  pchol_1cta_kernel<<<ntasks, 256, smem, s>>>(tasks, A, eps);
+}
+
 // Cluster variant: one CL-CTA cluster per group.  Candidates are exchanged
 // through distributed shared memory and the pivot column's R rows are read
 // from its owner's shared memory; one hardware cluster barrier per step.

@@ -1930,9 +1930,16 @@ struct Factorizer {
     for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
     // (then by owner: a batch's groups are independent, each rank takes a
     // contiguous range)
+    // (and, among the large groups, those whose pivoted Cholesky fits one
+    // CTA first: launch_huge_batch runs them one CTA each)
+    auto one_cta_grp = [&](int64_t t) {
+      const SkelTask& T = tasks[(size_t)t];
+      return T.mode == 2 && gram_ok(T.nc, T.nq) && pchol_1cta_smem(T.nc) <= kSmemCapBytes;
+    };
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       if (batch[(size_t)a] != batch[(size_t)b]) return batch[(size_t)a] < batch[(size_t)b];
-      return own_[(size_t)a] < own_[(size_t)b];
+      if (own_[(size_t)a] != own_[(size_t)b]) return own_[(size_t)a] < own_[(size_t)b];
+      return one_cta_grp(a) && !one_cta_grp(b);
     });
     const int PP = sharded() ? P : 1;
     // per batch and rank: small groups (one CTA each) and large groups
@@ -2353,7 +2360,22 @@ struct Factorizer {
           if (c < (cl_env > 0 ? 2 : 4)) continue;
           if (pchol_smem(maxnc, c) <= kSmemCapBytes) { clz = c; break; }
         }
-      int c0 = clz ? n : 0;
+      // every group's R fits one CTA's shared memory: one CTA per group, no
+      // inter-CTA barriers (HIFDE_PCHOL_1CTA=0 turns it off)
+      // (opt-in, HIFDE_PCHOL_1CTA=1: measured slower on config 5 -- 490 -> 569
+      // ms GPU -- and neutral on config 4; the cooperative kernel spreads each
+      // step's column updates over more SMs)
+      static const bool one_cta_ok = getenv("HIFDE_PCHOL_1CTA") && atoi(getenv("HIFDE_PCHOL_1CTA")) != 0;
+      int n1 = 0, nc1 = 0;  // the leading groups that fit one CTA (sorted first)
+      while (one_cta_ok && clz == 0 && n1 < n && pchol_1cta_smem(huge[(size_t)(lo + n1)].nc) <= kSmemCapBytes) {
+        nc1 = std::max(nc1, huge[(size_t)(lo + n1)].nc);
+        ++n1;
+      }
+      if (n1 > 0) {
+        launch_pchol_1cta(dtk, n1, pchol_1cta_smem(nc1), A, opt.eps, s);
+        ++g_launches;
+      }
+      int c0 = clz ? n : n1;
       if (clz) {
         HCK(launch_pchol_cluster(dtk, n, clz, pchol_smem(maxnc, clz), A, opt.eps, s));
         ++g_launches;
