@@ -1768,10 +1768,18 @@ struct Factorizer {
     // 3D: an exact level of medium groups alone also takes the pipeline (its
     // batches beat one chained launch of one-CTA groups: config 4 247 -> 216
     // ms GPU); in 2D the one-launch chain stays faster
-    static const bool promote_any = getenv("HIFDE_PROMOTE_ANY") ? atoi(getenv("HIFDE_PROMOTE_ANY")) != 0 : g.dim == 3;
-    bool any_promote = false;
-    for (int64_t t = 0; t < nt && !any_promote; ++t) any_promote = promote[(size_t)t] != 0;
-    if (exact && nbatch > 1 && (any_huge || (promote_any && any_promote))) {
+    static const int promote_env = getenv("HIFDE_PROMOTE_ANY") ? atoi(getenv("HIFDE_PROMOTE_ANY")) : -1;
+    const bool promote_any = promote_env >= 0 ? promote_env != 0 : g.dim == 3;  // per grid, not per process
+    // (a level whose largest medium group is small keeps the one-launch
+    // chain: config 5's level 1.333, nq nc^2 <= 1.3e6, is faster chained)
+    bool any_promote = false, big_promote = false;
+    for (int64_t t = 0; t < nt; ++t)
+      if (promote[(size_t)t]) {
+        any_promote = true;
+        const SkelTask& T = tasks[(size_t)t];
+        big_promote = big_promote || (double)T.nq * T.nc * T.nc >= 4e6;
+      }
+    if (exact && nbatch > 1 && (any_huge || (promote_any && big_promote))) {
       for (int64_t t = 0; t < nt; ++t)
         if (promote[(size_t)t]) tasks[(size_t)t].mode = 2;
       any_huge = any_huge || any_promote;
