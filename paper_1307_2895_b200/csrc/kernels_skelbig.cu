@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) skelbig_posmap_kernel(const SkelBigTask* 
 __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask* __restrict__ tasks,
                                                                const int4* __restrict__ work, Arenas A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int nsel;
+  __shared__ int nsel, ncol;
   const int4 wk = work[blockIdx.x];
   const SkelBigTask t = tasks[wk.x];
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask
   int32_t* salive = sdofs + nf;
   int32_t* smap = salive + nf;
   int32_t* ssel = smap + t.maxnb;
+  int32_t* scol = ssel + t.maxnb;  // block entries that land in a c column
   const BigWs w = big_ws(t, A);
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += 256) {
@@ -195,26 +196,29 @@ __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask
     const int bid = bl[b];
     const int nb = A.blk_n[bid];
     const double* bv = A.bvals + A.blk_val_off[bid];
-    if (threadIdx.x == 0) nsel = 0;
+    if (threadIdx.x == 0) {
+      nsel = 0;
+      ncol = 0;
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < nb; k += 256) {
       const int p = pmap[k];
       smap[k] = p;
       if (p >= r0 && p < r1) ssel[atomicAdd(&nsel, 1)] = k;
+      if (p >= 0 && p < nc) scol[atomicAdd(&ncol, 1)] = k;
     }
     pmap += nb;
     __syncthreads();
-    const int ns = nsel;
-    for (int s = 0; s < ns; ++s) {
-      const int k = ssel[s];
-      const int pk = smap[k];
-      const double* brow = bv + (size_t)k * nb;
-      for (int l = threadIdx.x; l < nb; l += 256) {
-        const int pl = smap[l];
-        if (pl < 0 || pl >= nc) continue;
-        if (pk < nc) w.Acc[(size_t)pk * nc + pl] += brow[l];
-        else w.Mq[(size_t)(pk - nc) + (size_t)pl * nq] += brow[l];
-      }
+    // every (selected row, c column) pair of the block: each destination
+    // entry has exactly one source in a block, so the order is immaterial
+    const int ns = nsel, nco = ncol;
+    for (int e = threadIdx.x; e < ns * nco; e += 256) {
+      const int sr = e / nco, cc = e - sr * nco;
+      const int k = ssel[sr], l = scol[cc];
+      const int pk = smap[k], pl = smap[l];
+      const double val = bv[(size_t)k * nb + l];
+      if (pk < nc) w.Acc[(size_t)pk * nc + pl] += val;
+      else w.Mq[(size_t)(pk - nc) + (size_t)pl * nq] += val;
     }
     __syncthreads();
   }
