@@ -2409,7 +2409,8 @@ struct Factorizer {
           const int nc = huge[(size_t)(lo + c0 + i)].nc;
           const int gm = pchol_min_ctas(nc);
           const int extra = (int)((double)(cap - need) * ((double)nc * nc) / std::max(tot, 1.0));
-          const int g = std::max(gm, std::min({gm + extra, nc, kMaxG}));
+          static const int maxg = getenv("HIFDE_PCHOL_MAXG") ? atoi(getenv("HIFDE_PCHOL_MAXG")) : kMaxG;
+          const int g = std::max(gm, std::min({gm + extra, nc, maxg}));
           gs[(size_t)i + 1] = gs[(size_t)i] + g;
           smem = std::max(smem, pchol_smem(nc, g));
         }

@@ -55,9 +55,12 @@ def _raise(lib, code: int):
 def _as_csr(a) -> sp.csr_matrix:
     if hasattr(a, "to_scipy"):
         a = a.to_scipy()
-    m = sp.csr_matrix(a, dtype=np.float64)
-    m.sum_duplicates()
-    m.sort_indices()
+    if sp.issparse(a) and a.format == "csr" and a.dtype == np.float64 and a.has_canonical_format:
+        m = a  # read only: the factor never modifies A, so no copy
+    else:
+        m = sp.csr_matrix(a, dtype=np.float64)
+        m.sum_duplicates()
+        m.sort_indices()
     if m.shape[0] != m.shape[1]:
         raise ValueError("matrix must be square")
     return m
