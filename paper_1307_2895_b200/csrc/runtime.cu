@@ -2792,7 +2792,9 @@ struct Factorizer {
       // the first kernel launch, a0_ready())
       int dev = 0;
       HCK(cudaGetDevice(&dev));
-      const bool big = (size_t)nnz * 12 > (size_t)(48u << 20);  // large inputs: pinned staging
+      static const size_t pin_min = getenv("HIFDE_A0_PIN_MB") ? (size_t)atoi(getenv("HIFDE_A0_PIN_MB")) << 20
+                                                              : (size_t)1 << 20;
+      const bool big = (size_t)nnz * 12 > pin_min;  // large inputs: pinned staging
       a0_job = helper.post([=]() {
         cudaError_t e = cudaSetDevice(dev);
         if (e == cudaSuccess && big) {
