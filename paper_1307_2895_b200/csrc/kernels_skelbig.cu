@@ -2,6 +2,7 @@
 //
 // Pipeline per batch of large groups (src/factor_ops.py:162-214,
 // src/dense.py:239-264):
+//   skelbig_posmap_kernel    front position of every consumed block entry.
 //   skelbig_assemble_kernel  rows of A_cc (row-major) and Mq = A_qc
 //                            (column-major) into scratch; one CTA per row chunk.
 //   cpqr_coop_kernel         column-pivoted QR of Mq with the rank cut, by
@@ -13,6 +14,11 @@
 //                            downdates its own columns, and posts its best
 //                            remaining norm; one group barrier per step.
 //                            dlaqp2 semantics.
+//   skelbig_gram_kernel +    (loose tolerances, eps >= kGramMinEps, instead of
+//   pchol_mc_kernel          the CPQR) G = Mq^T Mq on DMMA tiles, then a
+//                            cooperative pivoted Cholesky of G writing the
+//                            CPQR's outputs (same pivots and rank cut in
+//                            exact arithmetic).
 //   skelbig_sort_kernel      sk / rd ascending, output index lists, inner task.
 //   skelbig_t*_kernel        T = R11^-1 R12, blocked back substitution (64-row
 //                            diagonal solves + DMMA updates), then written

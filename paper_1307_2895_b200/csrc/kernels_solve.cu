@@ -10,6 +10,10 @@
 // level share neighbour DOFs, so their v_q updates are written to a
 // contribution buffer and summed per DOF in record order by a second kernel
 // (deterministic, no atomics).
+//
+// Fine levels (records up to 96 x 192) use the single-load-phase kernels
+// (solve_*_small_kernel); 48+ right-hand sides take the DMMA products in the
+// general kernels; both sum in cta_gemm's order where they replace it.
 #include <cstdint>
 
 #include "hifde_internal.h"

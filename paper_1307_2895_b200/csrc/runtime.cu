@@ -10,6 +10,12 @@
 // partitions and order-dependent steps match the reference.  The host keeps
 // only integer structure (DOF lists, block membership); every floating-point
 // operation runs in the sm_100a kernels.
+//
+// Sharding (options.comm, shard.h / comm.h): every rank runs this host
+// analysis; a group's kernels run on its owner, consumed blocks are exchanged
+// before each level and the state every rank reads is merged after each
+// launch.  Exact-order 3D batches queue each large-group tail on a second
+// stream so it overlaps the next batch's assembly and ID.
 #include <algorithm>
 #include <atomic>
 #include <chrono>
