@@ -1946,14 +1946,18 @@ struct Factorizer {
     // contiguous range)
     // (and, among the large groups, those whose pivoted Cholesky fits one
     // CTA first: launch_huge_batch runs them one CTA each)
-    auto one_cta_grp = [&](int64_t t) {
-      const SkelTask& T = tasks[(size_t)t];
-      return T.mode == 2 && gram_ok(T.nc, T.nq) && pchol_1cta_smem(T.nc) <= kSmemCapBytes;
-    };
+    // (the flag only matters for the opt-in one-CTA pivoted Cholesky)
+    static const bool one_cta_env = getenv("HIFDE_PCHOL_1CTA") && atoi(getenv("HIFDE_PCHOL_1CTA")) != 0;
+    std::vector<uint8_t> one_cta_grp((size_t)nt, 0);
+    if (one_cta_env)
+      for (int64_t t = 0; t < nt; ++t) {
+        const SkelTask& T = tasks[(size_t)t];
+        one_cta_grp[(size_t)t] = T.mode == 2 && gram_ok(T.nc, T.nq) && pchol_1cta_smem(T.nc) <= kSmemCapBytes;
+      }
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       if (batch[(size_t)a] != batch[(size_t)b]) return batch[(size_t)a] < batch[(size_t)b];
       if (own_[(size_t)a] != own_[(size_t)b]) return own_[(size_t)a] < own_[(size_t)b];
-      return one_cta_grp(a) && !one_cta_grp(b);
+      return one_cta_grp[(size_t)a] > one_cta_grp[(size_t)b];
     });
     const int PP = sharded() ? P : 1;
     // per batch and rank: small groups (one CTA each) and large groups
