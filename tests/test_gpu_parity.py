@@ -321,6 +321,12 @@ def test_many_and_odd_rhs_counts():
         assert np.allclose(f.apply_inverse(B[:, j]), X[:, j], rtol=1e-12, atol=1e-13 * np.abs(X).max())
     Y = f.apply(B[:, :17])
     assert np.allclose(Y[:, 5], f.apply(B[:, 5]), rtol=1e-12, atol=1e-13 * np.abs(Y).max())
+    # beyond 64 columns: DMMA record products in 64-column chunks plus a remainder
+    B2 = rng.standard_normal((g.ndof, 100))
+    X2 = f.apply_inverse(B2)
+    for lo, hi in ((0, 64), (64, 100), (99, 100)):
+        Xk = f.apply_inverse(np.ascontiguousarray(B2[:, lo:hi]))
+        assert np.allclose(Xk, X2[:, lo:hi], rtol=1e-12, atol=1e-13 * np.abs(X2).max())
 
 
 def test_concurrent_solves_are_reentrant():
