@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(256) pchol_mc_kernel(const SkelBigTask* __rest
   double* Rs = psm;                       // [nc][nown]: R(l, rb + c CL) at l * nown + c
   double* rp = Rs + (size_t)nc * nown;    // R(0..i-1, P)
   double* dd = rp + nc;                   // Schur diagonal of the owned columns (< 0: pivoted)
+  double* gcol = dd + nown;               // G(j, P) of the owned columns, this step
   for (int c = threadIdx.x; c < nown; c += 256) {
     const int j = rb + c * CL;
     dd[c] = w.G[(size_t)j + (size_t)j * nc];
@@ -712,7 +713,9 @@ __global__ void __launch_bounds__(256) pchol_mc_kernel(const SkelBigTask* __rest
       w.rdiag[i] = rii;
       w.piv[i] = P;
     }
+    // every load of the step issued together (one L2 latency, not one per column)
     for (int l = threadIdx.x; l < i; l += 256) rp[l] = __ldcg(w.Mq + (size_t)l + (size_t)P * nq);
+    for (int c = threadIdx.x; c < nown; c += 256) gcol[c] = __ldcg(w.G + (size_t)(rb + c * CL) + (size_t)P * nc);
     __syncthreads();
     const double inv = 1.0 / rii;
     for (int c = wid; c < nown; c += 8) {
@@ -726,7 +729,7 @@ __global__ void __launch_bounds__(256) pchol_mc_kernel(const SkelBigTask* __rest
       double sacc = 0.0;
       for (int l = lane; l < i; l += 32) sacc += rp[l] * Rs[(size_t)l * nown + c];
       sacc = warp_sum(sacc);
-      const double rij = (__ldcg(w.G + (size_t)j + (size_t)P * nc) - sacc) * inv;
+      const double rij = (gcol[c] - sacc) * inv;
       __syncwarp();
       if (lane == 0) {
         Rs[(size_t)i * nown + c] = rij;
@@ -1303,7 +1306,7 @@ void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, 
 
 size_t pchol_smem(int nc, int G) {
   const size_t nown = (size_t)((nc + G - 1) / G);
-  return sizeof(double) * ((size_t)nc * nown + (size_t)nc + nown);
+  return sizeof(double) * ((size_t)nc * nown + (size_t)nc + 2 * nown);
 }
 
 int pchol_min_ctas(int nc) {
