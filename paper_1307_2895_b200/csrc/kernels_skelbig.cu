@@ -136,12 +136,19 @@ __device__ __forceinline__ BigWs big_ws(const SkelBigTask& t, const Arenas& A) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Front position of every entry of every block a large group consumes (-1:
-// not in the front or retired), computed once per (group, block) instead of
-// once per row chunk of the assembly.  Work item int4 {task, block, offset}.
+// Per (group, block): the block's entries that land in the front, as two
+// arrays sorted by front position -- first the entries in c (positions < nc),
+// then those in q -- so an assembly CTA finds its rows by binary search and
+// takes the c columns as a prefix, instead of scanning every entry.  Work
+// item int4 {task, block, offset}; region = [cnt_c, cnt_q, pos[nb], ent[nb]].
+// The block's DOFs ascend, so its c entries and its q entries each ascend in
+// position: a stable partition (ballots + warp offsets) sorts them.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) skelbig_posmap_kernel(const SkelBigTask* __restrict__ tasks,
                                                              const int4* __restrict__ work, Arenas A) {
+  __shared__ int wsum[2][8];
+  __shared__ int base[2];
+  __shared__ int ctot;
   const int4 wk = work[blockIdx.x];
   const SkelBigTask t = tasks[wk.x];
   const int nc = t.nc, nq = t.nq;
@@ -149,11 +156,68 @@ __global__ void __launch_bounds__(256) skelbig_posmap_kernel(const SkelBigTask* 
   const int bid = A.lists[t.blk_off + wk.y];
   const int nb = A.blk_n[bid];
   const int32_t* bd = A.idx + A.blk_dof_off[bid];
-  int32_t* out = A.iscratch + t.map_off + wk.z;
-  for (int k = threadIdx.x; k < nb; k += 256) {
+  int32_t* reg = A.iscratch + t.map_off + wk.z;
+  int32_t* pos = reg + 2;
+  int32_t* ent = pos + nb;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  auto position = [&](int k) {
     int p = front_pos(gd, nc, nq, bd[k]);
     if (p >= nc && !A.active[gd[p]]) p = -1;
-    out[k] = p;
+    return p;
+  };
+  int c = 0;  // pass 1: the number of c entries
+  for (int k = threadIdx.x; k < nb; k += 256) {
+    const int p = position(k);
+    c += (p >= 0 && p < nc) ? 1 : 0;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if (lane == 0) wsum[0][wid] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < 8; ++w) tot += wsum[0][w];
+    ctot = tot;
+    base[0] = 0;
+    base[1] = tot;
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < nb; k0 += 256) {  // pass 2: stable partition, 256 entries at a time
+    const int k = k0 + (int)threadIdx.x;
+    const int p = k < nb ? position(k) : -1;
+    const bool isc = p >= 0 && p < nc, isq = p >= nc;
+    const unsigned mc = __ballot_sync(0xffffffffu, isc), mq = __ballot_sync(0xffffffffu, isq);
+    if (lane == 0) {
+      wsum[0][wid] = __popc(mc);
+      wsum[1][wid] = __popc(mq);
+    }
+    __syncthreads();
+    int oc = base[0], oq = base[1];
+    for (int w = 0; w < wid; ++w) {
+      oc += wsum[0][w];
+      oq += wsum[1][w];
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    if (isc) {
+      const int o = oc + __popc(mc & lt);
+      pos[o] = p;
+      ent[o] = k;
+    }
+    if (isq) {
+      const int o = oq + __popc(mq & lt);
+      pos[o] = p;
+      ent[o] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < 8; ++w) {
+        base[0] += wsum[0][w];
+        base[1] += wsum[1][w];
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    reg[0] = ctot;
+    reg[1] = base[1] - ctot;
   }
 }
 
@@ -197,35 +261,37 @@ __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask
   }
   __syncthreads();
   const int32_t* bl = A.lists + t.blk_off;
-  const int32_t* pmap = A.iscratch + t.map_off;  // front positions, skelbig_posmap_kernel
+  const int32_t* reg = A.iscratch + t.map_off;  // per block: [cnt_c, cnt_q, pos[nb], ent[nb]] by position
   for (int b = 0; b < t.nblk; ++b) {
     const int bid = bl[b];
     const int nb = A.blk_n[bid];
     const double* bv = A.bvals + A.blk_val_off[bid];
-    if (threadIdx.x == 0) {
-      nsel = 0;
-      ncol = 0;
+    const int ncn = reg[0], ntot = reg[0] + reg[1];
+    const int32_t* pos = reg + 2;
+    const int32_t* ent = pos + nb;
+    // this CTA's rows: positions in [r0, r1), a contiguous range of the list
+    int lo = 0, hi = ntot;
+    while (lo < hi) {
+      const int m = (lo + hi) >> 1;
+      if (pos[m] < r0) lo = m + 1; else hi = m;
     }
-    __syncthreads();
-    for (int k = threadIdx.x; k < nb; k += 256) {
-      const int p = pmap[k];
-      smap[k] = p;
-      if (p >= r0 && p < r1) ssel[atomicAdd(&nsel, 1)] = k;
-      if (p >= 0 && p < nc) scol[atomicAdd(&ncol, 1)] = k;
+    const int s0 = lo;
+    hi = ntot;
+    while (lo < hi) {
+      const int m = (lo + hi) >> 1;
+      if (pos[m] < r1) lo = m + 1; else hi = m;
     }
-    pmap += nb;
-    __syncthreads();
-    // every (selected row, c column) pair of the block: each destination
-    // entry has exactly one source in a block, so the order is immaterial
-    const int ns = nsel, nco = ncol;
-    for (int e = threadIdx.x; e < ns * nco; e += 256) {
-      const int sr = e / nco, cc = e - sr * nco;
-      const int k = ssel[sr], l = scol[cc];
-      const int pk = smap[k], pl = smap[l];
+    const int ns = lo - s0;
+    // every (row, c column) pair: one source per destination entry in a block
+    for (int e = threadIdx.x; e < ns * ncn; e += 256) {
+      const int sr = e / ncn, cc = e - sr * ncn;
+      const int k = ent[s0 + sr], l = ent[cc];
+      const int pk = pos[s0 + sr], pl = pos[cc];
       const double val = bv[(size_t)k * nb + l];
       if (pk < nc) w.Acc[(size_t)pk * nc + pl] += val;
       else w.Mq[(size_t)(pk - nc) + (size_t)pl * nq] += val;
     }
+    reg += 2 + 2 * nb;
     __syncthreads();
   }
 }

@@ -1989,7 +1989,7 @@ struct Factorizer {
       H.iws_off = (int64_t)iscratch.bump(4 * nc + 4, s);
       {
         size_t mtot = 0;
-        for (int j = 0; j < T.nblk; ++j) mtot += (size_t)blk_n[(size_t)hl[(size_t)(T.blk_off + j)]];
+        for (int j = 0; j < T.nblk; ++j) mtot += 2 + 2 * (size_t)blk_n[(size_t)hl[(size_t)(T.blk_off + j)]];
         H.map_off = (int64_t)iscratch.bump(mtot + 1, s);
       }
       H.rec_off = T.rec_off;
@@ -2324,7 +2324,7 @@ struct Factorizer {
         int off = 0;
         for (int j = 0; j < H.nblk; ++j) {
           wm.push_back(make_int4(i, j, off, 0));
-          off += blk_n[(size_t)hlist[(size_t)(H.blk_off + j)]];
+          off += 2 + 2 * blk_n[(size_t)hlist[(size_t)(H.blk_off + j)]];
         }
       }
       DBuf<int4> dm;
