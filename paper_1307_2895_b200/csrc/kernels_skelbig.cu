@@ -227,16 +227,12 @@ __global__ void __launch_bounds__(256) skelbig_posmap_kernel(const SkelBigTask* 
 __global__ void __launch_bounds__(256) skelbig_assemble_kernel(const SkelBigTask* __restrict__ tasks,
                                                                const int4* __restrict__ work, Arenas A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int nsel, ncol;
   const int4 wk = work[blockIdx.x];
   const SkelBigTask t = tasks[wk.x];
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
   const int r0 = wk.y, r1 = wk.z;
   int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
   int32_t* salive = sdofs + nf;
-  int32_t* smap = salive + nf;
-  int32_t* ssel = smap + t.maxnb;
-  int32_t* scol = ssel + t.maxnb;  // block entries that land in a c column
   const BigWs w = big_ws(t, A);
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += 256) {

@@ -2333,7 +2333,7 @@ struct Factorizer {
       ++g_launches;
       dm.release(s);
     }
-    const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf + 3 * max_nb));
+    const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf));  // front DOFs + alive flags
     static const bool split_t = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: phase times
     cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};
     if (split_t) for (auto& e : pe) HCK(cudaEventCreate(&e));
