@@ -1,27 +1,29 @@
 """HIF-DE factor & solve benchmark (BASELINE.json metric) on B200.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on and the
-largest that is a single-GPU case): 2D five-point high-contrast operator,
-n = 511 interior points per side (N = 261,121), Gaussian-noise field smoothed
-with width 4h thresholded at zero to {1e-2, 1e2}, leaf 8x8, eps = 1e-9,
-16 right-hand sides ~ N(0,1).  Synthetic, seeded inputs generated in-process.
+Workload: BASELINE.json configs[2] ("config 3"), the largest configuration
+that fits one B200 and the one the metric is quoted on at 1/2/4/8 GPUs:
+2D five-point Laplacian, n = 2047 interior points per side (N = 4,190,209),
+a = 1, b = 0, leaf 8x8, eps = 1e-6, 64 right-hand sides ~ N(0,1).  Synthetic,
+seeded inputs generated in-process (the reference's own problems are
+synthetic PDEs generated in code).
 
-One step = factor_hifde of the matrix + apply_inverse of the 16-RHS block.
+One step = factor_hifde of the matrix + apply_inverse of the 64-RHS block.
   value = N / (t_factor + t_solve)  [unknowns/s], inputs resident in HBM,
-          timed with CUDA events on the library's stream;
-  e2e   = the same through the public API with host buffers (CSR and RHS
-          host->device, solution device->host inside the timed region).
-`--impl reference` times the CPU oracle port of the reference algorithm
-(oracle/hifde_oracle.py) on this host on the same workload.
+          CUDA events on the library's stream, L2 flushed between steps;
+  e2e   = the same through the public Python API with host buffers (CSR and
+          RHS host->device, solution device->host inside the timed region).
+The line also carries config 5 (3D high-contrast hifde3x, N = 2,048,383,
+eps = 1e-3, 32 RHS), the other 1/2/4/8-GPU configuration, as extra keys.
 
-Multi-GPU (torchrun, --gpus N): by default every rank factors and solves its
-own independently seeded instance of config 2 (replicas; weak scaling).
-`--shard --config {2,3,4,5}` instead factors ONE instance of that BASELINE
-config sharded over the N ranks (spatial group owners, NCCL block exchange,
-exact-order coarse levels on rank 0; strong scaling) and splits the
-right-hand sides over the ranks -- DESIGN.md (e).  `--emulate P` runs the
-sharded code path with P virtual ranks on one GPU (a correctness check; its
-timing is not a multi-GPU number).
+Multi-GPU (torchrun, --gpus N > 1): ONE instance of the config is factored
+sharded over the N ranks (spatial group owners, NCCL block exchange; DESIGN.md
+(e)) and the right-hand-side columns are split over the ranks: strong scaling.
+
+`--impl reference` times the CPU oracle port of the reference algorithm
+(oracle/hifde_oracle.py; the reference is pure Python and does not travel to
+the GPU box) on this host: each step one bounded sample of the workload on
+every host core (an independent process per core, each a 255x255 instance of
+the config-3 operator, same leaf, eps and 64 RHS).
 """
 
 from __future__ import annotations
@@ -41,18 +43,38 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = 2
-WORKLOAD = ("cfg2: 2D 5-point high-contrast (Gaussian, 4h, thr 0) n=511 N=261121, "
-            "leaf 8x8, eps=1e-9, hifde, 16 RHS; step = factor + 16-RHS solve")
+CONFIG = 3
 METRIC = "HIF-DE factor & solve unknowns/sec"
+WORKLOADS = {
+    2: "cfg2: 2D 5-point high-contrast (Gaussian, 4h, thr 0) n=511 N=261121, leaf 8x8, eps=1e-9, hifde, 16 RHS",
+    3: "cfg3: 2D 5-point Laplacian n=2047 N=4190209, leaf 8x8, eps=1e-6, hifde, 64 RHS",
+    4: "cfg4: 3D 7-point Laplacian n=63 N=250047, leaf 4^3, eps=1e-6, hifde3x, 16 RHS",
+    5: "cfg5: 3D 7-point high-contrast (Gaussian, 4h, thr 0) n=127 N=2048383, leaf 4^3, eps=1e-3, hifde3x, 32 RHS",
+}
+# CPU sample of the reference arm / cpu_baseline: config 3's operator on a
+# 255 x 255 grid (1/64 of its unknowns), same leaf, eps and RHS count
+SAMPLE = (2, 256, 8, 1e-6, 64)
+SAMPLE_TEXT = ("per host core one oracle-port factor_hifde + 64-RHS apply_inverse of the config-3 operator "
+               "(2D Laplacian, leaf 8x8, eps 1e-6) on a 255x255 grid (N=65025), cores running concurrently")
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return json.load(fh), "measured"
+            pk, kind = json.load(fh), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0}, "fallback"
+        pk, kind = {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+    # FP64 roof: cuBLAS DGEMM 8192^3 sustained on this pool's B200
+    # (profiles/r01_fp64_peak.json, tools/fp64_peak.py); not in MEASURED_PEAKS.json
+    fp64 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_fp64_peak.json")) as fh:
+            fp64 = float(json.load(fh)["dgemm_tflops_sustained"])
+    except Exception:
+        pass
+    pk = dict(pk)
+    pk["fp64_tflops"] = fp64 or 35.5
+    return pk, kind
 
 
 class ClockSampler:
@@ -109,302 +131,358 @@ def dist_setup():
     return world, rank, local
 
 
+def config_dict(cfg, world, nranks=None):
+    return {"workload": WORKLOADS[cfg] + "; step = factor + RHS-block solve",
+            "parallelism": f"shard x{nranks or world}" if (nranks or world) > 1 else "single GPU",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# --------------------------------------------------------------------------
+# CPU side: the oracle port of the reference algorithm (reference arm and
+# cpu_baseline).  Each worker process factors and solves one sample.
+# --------------------------------------------------------------------------
+_SAMPLE_PROBLEM = None
+
+
+def _pool_init():
+    """Worker start-up: BLAS on one thread (the reference pins its level loop to
+    one, src/driver.py:35-41) and the sample problem assembled once."""
+    global _SAMPLE_PROBLEM
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    sys.path.insert(0, ROOT)
+    import paper_1307_2895_b200.problems as P
+    dim, n, m, eps, nrhs = SAMPLE
+    g = P.build_grid(dim, n, m)
+    a = P.assemble(g, P.constant_field(g))
+    b = np.random.default_rng(1).standard_normal((g.ndof, nrhs))
+    _SAMPLE_PROBLEM = (g, a, b)
+
+
+def _sample_worker(_):
+    from oracle import hifde_oracle as O
+    g, a, b = _SAMPLE_PROBLEM
+    dim, n, m, eps, nrhs = SAMPLE
+    t0 = time.perf_counter()
+    f = O.factor(a, O.make_grid(dim, n, m), eps, "hifde")
+    tf = time.perf_counter() - t0
+    x = f.apply_inverse(b)
+    t = time.perf_counter() - t0
+    resid = float(np.max(np.linalg.norm(a @ x - b, axis=0) / np.linalg.norm(b, axis=0)))
+    return g.ndof, t, tf, resid, os.getpid()
+
+
+class CpuPool:
+    """One worker process per host core; a step runs one sample on each.  The
+    step time is the slowest worker's factor + solve time (the samples run
+    concurrently), or the pool's wall time if a worker ran two samples."""
+
+    def __init__(self, cores):
+        import multiprocessing as mp
+        self.cores = cores
+        self.pool = mp.get_context("spawn").Pool(cores, initializer=_pool_init)
+
+    def step(self):
+        t0 = time.perf_counter()
+        res = self.pool.map(_sample_worker, range(self.cores), chunksize=1)
+        wall = time.perf_counter() - t0
+        t = max(r[1] for r in res) if len({r[4] for r in res}) == len(res) else wall
+        return sum(r[0] for r in res), t, res
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def host_cores():
+    try:
+        return max(1, min(len(os.sched_getaffinity(0)), 32))
+    except Exception:
+        return max(1, min(os.cpu_count() or 1, 32))
+
+
 def cpu_reference(args, world, rank):
-    """Reference arm: the CPU oracle port of the reference algorithm."""
+    """Reference arm: the oracle port on all host cores, rank 0 only."""
     if rank != 0:
         return
-    import paper_1307_2895_b200.problems as P
-    from oracle import hifde_oracle as O
-    g, a, eps, variant, nrhs = P.baseline_problem(CONFIG)
-    og = O.make_grid(g.dim, g.n, g.m)
-    b = np.random.default_rng(1).standard_normal((g.ndof, nrhs))
-    steps = max(1, min(args.steps, 4))
-    warm = min(args.warmup, 1)
-    times = []
-    for i in range(warm + steps):
-        t0 = time.perf_counter()
-        f = O.factor(a, og, eps, variant)
-        tf = time.perf_counter() - t0
-        x = f.apply_inverse(b)
-        t = time.perf_counter() - t0
-        if i >= warm:
-            times.append((t, tf, t - tf))
-    tt = float(np.mean([t[0] for t in times]))
-    value = g.ndof / tt
+    cores = host_cores()
+    pool = CpuPool(cores)
+    pool.step()  # worker start-up and imports, untimed
+    times, unknowns, tfs, resid = [], 0, [], 0.0
+    for i in range(args.warmup + args.steps):
+        n, wall, res = pool.step()
+        if i >= args.warmup:
+            times.append(wall)
+            unknowns = n
+            tfs.append(max(r[2] for r in res))
+            resid = max(r[3] for r in res)
+    pool.close()
+    tt = float(np.mean(times))
+    value = unknowns / tt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "unknowns/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": tt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE cfg2 inputs)",
-        "config": {"workload": WORKLOAD},
-        "factor_unknowns_per_s": g.ndof / float(np.mean([t[1] for t in times])),
-        "solve_unknown_rhs_per_s": g.ndof * nrhs / float(np.mean([t[2] for t in times])),
-        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": 1, "kind": "port",
-                         "sample": f"full cfg2 factor+16-RHS solve x{steps} (oracle port, BLAS 1 thread in the cell sweep as the reference)"},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tt * 1e3,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": f"synthetic (seeded BASELINE cfg{args.config}-shaped sample)",
+        "config": config_dict(args.config, world),
+        "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": cores, "kind": "port",
+                         "sample": SAMPLE_TEXT + "; oracle port = CPU restatement of the reference "
+                                                 "(pure-Python reference cannot travel to the GPU box)"},
         "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "resid": float(np.max(np.linalg.norm(a @ x - b, axis=0) / np.linalg.norm(b, axis=0))),
+        "resid": resid,
     }
     print(json.dumps(line), flush=True)
 
 
-def run_gpu(args, world, rank, local):
-    import torch
-    import paper_1307_2895_b200 as H
-    from paper_1307_2895_b200 import _lib
+def cpu_baseline():
+    cores = host_cores()
+    pool = CpuPool(cores)
+    pool.step()
+    vals = []
+    for _ in range(2):
+        n, wall, _ = pool.step()
+        vals.append(n / wall)
+    pool.close()
+    return {"value": float(np.mean(vals)), "unit": "unknowns/s", "cores": cores, "kind": "port",
+            "sample": SAMPLE_TEXT + ", 2 rounds"}
 
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.Stream(device=dev)
-    g, a, eps, variant, nrhs = H.baseline_problem(CONFIG, seed=rank)
-    N = g.ndof
-    rng = np.random.default_rng(1 + rank)
-    b_host = rng.standard_normal((N, nrhs))
-    # device-resident inputs for `value`
-    indptr_d = torch.from_numpy(a.indptr.astype(np.int64)).to(dev)
-    indices_d = torch.from_numpy(a.indices.astype(np.int32)).to(dev)
-    data_d = torch.from_numpy(a.data.astype(np.float64)).to(dev)
-    b_d = torch.from_numpy(b_host).to(dev)
-    x_d = torch.empty_like(b_d)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    lib = _lib.load()
 
-    import ctypes as C
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+class Runner:
+    """One configuration on this rank: device-resident inputs, the timed
+    step through the C ABI, and the e2e step through the Python API."""
 
-    def factor_device():
+    def __init__(self, cfg, dev, local, stream, comm, world, rank):
+        import torch
+        import paper_1307_2895_b200 as H
+        from paper_1307_2895_b200 import distributed as D
+        self.H, self.torch = H, torch
+        self.cfg, self.local, self.stream, self.comm = cfg, local, stream, comm
+        g, a, eps, variant, nrhs = H.baseline_problem(cfg)
+        self.g, self.a, self.eps, self.variant, self.nrhs = g, a, eps, variant, nrhs
+        self.N = g.ndof
+        cols = D.rhs_columns(nrhs, world, rank) if world > 1 else slice(0, nrhs)
+        self.nloc = cols.stop - cols.start
+        b_full = np.random.default_rng(1).standard_normal((self.N, nrhs))
+        self.b_host = np.ascontiguousarray(b_full[:, cols])
+        self.b_pin = torch.from_numpy(self.b_host).pin_memory()  # e2e: inputs from pinned host memory
+        self.indptr_d = torch.from_numpy(a.indptr.astype(np.int64)).to(dev)
+        self.indices_d = torch.from_numpy(a.indices.astype(np.int32)).to(dev)
+        self.data_d = torch.from_numpy(a.data.astype(np.float64)).to(dev)
+        self.b_d = torch.from_numpy(self.b_host).to(dev)
+        self.x_d = torch.empty_like(self.b_d)
+        self.fac = H.factor_hifde if variant == "hifde" else H.factor_hifde3x
+
+    def factor_device(self, kernel_log=True):
+        import ctypes as C
+        from paper_1307_2895_b200 import _lib
+        lib = _lib.load()
         opt = _lib.Options()
-        lib.hifde_default_options(C.byref(opt), _lib.VARIANT_HIFDE)
-        opt.eps = eps
-        opt.device = local
+        lib.hifde_default_options(C.byref(opt), _lib.VARIANT_HIFDE if self.variant == "hifde" else _lib.VARIANT_HIFDE3X)
+        opt.eps = self.eps
+        opt.device = self.local
         opt.input_on_device = 1
-        opt.stream = stream.cuda_stream
+        opt.stream = self.stream.cuda_stream
+        opt.comm = self.comm.handle if self.comm is not None else None
+        opt.kernel_log = int(kernel_log)
         h = C.c_void_p()
-        code = lib.hifde_factor(indptr_d.data_ptr(), indices_d.data_ptr(), data_d.data_ptr(), N,
-                                g.dim, g.n, g.m, g.nlevels, C.byref(opt), C.byref(h))
+        code = lib.hifde_factor(self.indptr_d.data_ptr(), self.indices_d.data_ptr(), self.data_d.data_ptr(),
+                                self.N, self.g.dim, self.g.n, self.g.m, self.g.nlevels, C.byref(opt), C.byref(h))
         if code:
             raise RuntimeError(lib.hifde_last_error().decode())
-        launches = lib.hifde_last_launch_count()
-        return H.GeneralizedLDL(h.value, lib, True), launches
+        return self.H.GeneralizedLDL(h.value, lib, True), int(lib.hifde_last_launch_count())
 
-    def one_step():
-        f, nl_f = factor_device()
-        f.apply_inverse_device(b_d.data_ptr(), x_d.data_ptr(), nrhs, stream.cuda_stream)
-        nl_s = lib.hifde_last_launch_count()
-        return f, nl_f + nl_s
+    def solve_device(self, f):
+        from paper_1307_2895_b200 import _lib
+        if not self.nloc:
+            return 0
+        f.apply_inverse_device(self.b_d.data_ptr(), self.x_d.data_ptr(), self.nloc, self.stream.cuda_stream)
+        return int(_lib.load().hifde_last_launch_count())
 
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            f, _ = one_step()
-            stream.synchronize()
-        # correctness guard on the warm factor (not timed)
-        x = x_d.cpu().numpy()
-        resid = float(np.max(np.linalg.norm(a @ x - b_host, axis=0) / np.linalg.norm(b_host, axis=0)))
-        level_info = f.level_info
-        skel = f.metrics["skeleton_counts"]
-        del f
-        if dist:
-            dist.barrier()
+    def timed(self, steps, warmup, flush, clock=None):
+        torch = self.torch
+        s = self.stream
+        for _ in range(warmup):
+            f, _ = self.factor_device()
+            self.solve_device(f)
+            s.synchronize()
+            f.close()
         torch.cuda.synchronize()
         times, tfs, launches = [], [], 0
-        with ClockSampler(local) as clk:
-            for _ in range(args.steps):
-                flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e2 = torch.cuda.Event(enable_timing=True)
-                stream.wait_stream(torch.cuda.current_stream())
-                e0.record(stream)
-                f, nl_f = factor_device()
-                e1.record(stream)
-                f.apply_inverse_device(b_d.data_ptr(), x_d.data_ptr(), nrhs, stream.cuda_stream)
-                launches += nl_f + lib.hifde_last_launch_count()
-                e2.record(stream)
-                e2.synchronize()
-                times.append(e0.elapsed_time(e2) / 1e3)
-                tfs.append(e0.elapsed_time(e1) / 1e3)
-                level_info = f.level_info
-                f.close()
+        kstats = None
+        for i in range(steps):
+            flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            s.wait_stream(torch.cuda.current_stream())
+            e0.record(s)
+            f, nl = self.factor_device()
+            e1.record(s)
+            nl += self.solve_device(f)
+            e2.record(s)
+            e2.synchronize()
+            launches += nl
+            times.append(e0.elapsed_time(e2) / 1e3)
+            tfs.append(e0.elapsed_time(e1) / 1e3)
+            if kstats is None:
+                kstats = []
+            for ph in (0, 1):
+                for k in f.kernel_stats(ph):
+                    kstats.append(k)
+            if i == steps - 1:
+                self.level_info = f.level_info
+                self.skel = f.metrics["skeleton_counts"]
+                self.xfer = f.metrics["xfer_bytes"]
+                x = self.x_d.cpu().numpy()
+                self.resid = (float(np.max(np.linalg.norm(self.a @ x - self.b_host, axis=0)
+                                           / np.linalg.norm(self.b_host, axis=0))) if self.nloc else 0.0)
+            f.close()
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t_step = float(np.mean(times))
-        t_f = float(np.mean(tfs))
-        t_s = t_step - t_f
-        # end-to-end through the public API with host buffers
-        e2e_times = []
-        for _ in range(max(1, min(args.steps, 5))):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            fe = H.factor_hifde(a, g, eps, stream=stream.cuda_stream, device=local)
-            xe = fe.apply_inverse(b_host)
-            e2e_times.append(time.perf_counter() - t0)
-            fe.close()
-        t_e2e = float(np.median(e2e_times))
-    if dist:
-        tt = torch.tensor([t_step, t_e2e, t_f, t_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step, t_e2e, t_f, t_s = [float(v) for v in tt.cpu()]
+        self.kstats = kstats
+        return float(np.mean(times)), float(np.mean(tfs)), launches
 
-    # roofline of the dominant kernel class from the per-level accounting
-    pk, pk_kind = peaks()
-    dominant = max(level_info[:-1], key=lambda d: d["seconds"])
-    h2d = a.indptr.size * 8 + a.indices.size * 4 + a.data.size * 8 + b_host.nbytes
-    d2h = b_host.nbytes
-    line = {
-        "metric": METRIC, "value": world * N / t_step, "unit": "unknowns/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE cfg2 inputs)",
-        "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}",
-                   "l2": "flushed between timed steps (256 MiB write)"},
-        "factor_ms": t_f * 1e3, "solve_ms": t_s * 1e3,
-        "factor_unknowns_per_s": N / t_f, "solve_unknown_rhs_per_s": N * nrhs / t_s,
-        "e2e": {"value": world * N / t_e2e, "unit": "unknowns/s",
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-        "resid": resid, "skeleton_counts": [c for _, c in skel],
-    }
-    line["roofline"] = roofline(level_info, pk, pk_kind, args)
-    line["roofline_by_class"] = roofline_classes(level_info, pk)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline()
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
-
-
-def run_sharded(args, world, rank, local):
-    """One BASELINE config sharded over the ranks (strong scaling)."""
-    import ctypes as C
-
-    import torch
-    import paper_1307_2895_b200 as H
-    from paper_1307_2895_b200 import _lib
-    from paper_1307_2895_b200 import distributed as D
-
-    dist = None
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-        comm = D.init_comm(device=local)
-    else:
-        comm = D.emulated_comm(args.emulate, local) if args.emulate > 1 else None
-    nr = comm.nranks if comm is not None else 1
-    stream = torch.cuda.Stream(device=dev)
-    g, a, eps, variant, nrhs = H.baseline_problem(args.config)
-    N = g.ndof
-    cols = D.rhs_columns(nrhs, world, rank)
-    nloc = cols.stop - cols.start
-    b_host = np.random.default_rng(1).standard_normal((N, nrhs))
-    b_loc = np.ascontiguousarray(b_host[:, cols])
-    indptr_d = torch.from_numpy(a.indptr.astype(np.int64)).to(dev)
-    indices_d = torch.from_numpy(a.indices.astype(np.int32)).to(dev)
-    data_d = torch.from_numpy(a.data.astype(np.float64)).to(dev)
-    b_d = torch.from_numpy(b_loc).to(dev)
-    x_d = torch.empty_like(b_d)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    lib = _lib.load()
-    vcode = _lib.VARIANT_HIFDE if variant == "hifde" else _lib.VARIANT_HIFDE3X
-
-    def factor_device():
-        opt = _lib.Options()
-        lib.hifde_default_options(C.byref(opt), vcode)
-        opt.eps = eps
-        opt.device = local
-        opt.input_on_device = 1
-        opt.stream = stream.cuda_stream
-        opt.comm = comm.handle if comm is not None else None
-        h = C.c_void_p()
-        code = lib.hifde_factor(indptr_d.data_ptr(), indices_d.data_ptr(), data_d.data_ptr(), N,
-                                g.dim, g.n, g.m, g.nlevels, C.byref(opt), C.byref(h))
-        if code:
-            raise RuntimeError(lib.hifde_last_error().decode())
-        return H.GeneralizedLDL(h.value, lib, True), lib.hifde_last_launch_count()
-
-    fac = H.factor_hifde if variant == "hifde" else H.factor_hifde3x
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            f, _ = factor_device()
-            if nloc:
-                f.apply_inverse_device(b_d.data_ptr(), x_d.data_ptr(), nloc, stream.cuda_stream)
-            stream.synchronize()
-        x = x_d.cpu().numpy()
-        resid = float(np.max(np.linalg.norm(a @ x - b_loc, axis=0) / np.linalg.norm(b_loc, axis=0))) if nloc else 0.0
-        skel = f.metrics["skeleton_counts"]
-        xfer = f.metrics["xfer_bytes"]
-        f.close()
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        times, tfs, launches = [], [], 0
-        with ClockSampler(local) as clk:
-            for _ in range(args.steps):
-                flush.zero_()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e2 = torch.cuda.Event(enable_timing=True)
-                stream.wait_stream(torch.cuda.current_stream())
-                e0.record(stream)
-                f, nl = factor_device()
-                e1.record(stream)
-                if nloc:
-                    f.apply_inverse_device(b_d.data_ptr(), x_d.data_ptr(), nloc, stream.cuda_stream)
-                    nl += lib.hifde_last_launch_count()
-                launches += nl
-                e2.record(stream)
-                e2.synchronize()
-                times.append(e0.elapsed_time(e2) / 1e3)
-                tfs.append(e0.elapsed_time(e1) / 1e3)
-                level_info = f.level_info
-                f.close()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t_step, t_f = float(np.mean(times)), float(np.mean(tfs))
-        e2e_times = []
-        for _ in range(max(1, min(args.steps, 3))):
+    def e2e(self, steps, dist):
+        torch = self.torch
+        ts = []
+        for i in range(steps + 1):
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            fe = fac(a, g, eps, stream=stream.cuda_stream, device=local, comm=comm)
-            if nloc:
-                fe.apply_inverse(b_loc)
-            e2e_times.append(time.perf_counter() - t0)
+            fe = self.fac(self.a, self.g, self.eps, stream=self.stream.cuda_stream, device=self.local,
+                          comm=self.comm)
+            if self.nloc:
+                fe.apply_inverse(self.b_pin.numpy())
+            t = time.perf_counter() - t0
             fe.close()
-        t_e2e = float(np.median(e2e_times))
+            if i > 0:  # first call warms the host caches of the public path
+                ts.append(t)
+        return float(np.mean(ts))
+
+
+def roofline(kstats, steps, pk, pk_kind):
+    """Dominant kernel of the step by CUDA-event time (the kernel log of the
+    library: every main launch bracketed by events on the library's stream).
+    achieved = its algorithmic bytes (or FLOPs) per launch over its average
+    launch duration; bound = FP64 tensor pipe when the work's arithmetic
+    intensity is above the ridge (measured DGEMM / measured copy), else HBM."""
+    agg = {}
+    for k in kstats:
+        key = (k["name"], round(k["tag"], 4), k["phase"])
+        a = agg.setdefault(key, {"name": k["name"], "tag": k["tag"], "phase": k["phase"],
+                                 "launches": 0, "seconds": 0.0, "gbytes": 0.0, "gflop": 0.0})
+        for f in ("launches", "seconds", "gbytes", "gflop"):
+            a[f] += k[f]
+    total = sum(a["seconds"] for a in agg.values())
+    dom = max(agg.values(), key=lambda a: a["seconds"])
+    per_launch_s = dom["seconds"] / max(dom["launches"], 1)
+    gb_l = dom["gbytes"] / max(dom["launches"], 1)
+    gf_l = dom["gflop"] / max(dom["launches"], 1)
+    ridge = pk["fp64_tflops"] * 1e3 / pk["hbm_gbs"]
+    ai = gf_l / gb_l if gb_l > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_r02.json")) as fh:
+            tr = json.load(fh)["dram_bytes_per_launch"]
+            v = tr.get(f"{dom['name']}@{dom['tag']:.3f}")
+            traffic = v / 1e9 if v else None
+    except Exception:
+        pass
+    if ai > ridge:
+        achieved, peak, unit, bound = gf_l / per_launch_s * 1e-3, pk["fp64_tflops"], "TFLOP/s", "tensor"
+        peak_kind = "measured cuBLAS DGEMM 8192^3 (profiles/r01_fp64_peak.json; FP64 DMMA pipe)"
+    else:
+        achieved, peak, unit, bound = gb_l / per_launch_s, pk["hbm_gbs"], "GB/s", "hbm"
+        peak_kind = pk_kind + " hbm_gbs"
+    top = sorted(agg.values(), key=lambda a: -a["seconds"])[:8]
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": traffic, "traffic_unit": "GB per launch (ncu dram__bytes_read+write)",
+            "kernel": dom["name"], "level": dom["tag"], "phase": "solve" if dom["phase"] else "factor",
+            "launches_per_step": dom["launches"] / steps, "launch_seconds": per_launch_s,
+            "algorithmic_gbytes_per_launch": gb_l, "algorithmic_gflop_per_launch": gf_l,
+            "share_of_logged_time": dom["seconds"] / total if total else None,
+            "peak_kind": peak_kind,
+            "top_kernels": [{"kernel": a["name"], "level": a["tag"], "phase": a["phase"],
+                             "ms_per_step": a["seconds"] / steps * 1e3,
+                             "gb_s": a["gbytes"] / a["seconds"] if a["seconds"] else None,
+                             "tflop_s": a["gflop"] / a["seconds"] * 1e-3 if a["seconds"] else None}
+                            for a in top]}
+
+
+def run_gpu(args, world, rank, local):
+    import torch
+    from paper_1307_2895_b200 import distributed as D
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_base = cpu_baseline()  # before CUDA initializes (spawned worker processes)
+    dist = None
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = D.init_comm(device=local)
+    elif args.emulate > 1:
+        comm = D.emulated_comm(args.emulate, local)
+    nranks = comm.nranks if comm is not None else 1
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    R = Runner(args.config, dev, local, stream, comm, world, rank)
+    with torch.cuda.stream(stream):
+        if dist:
+            dist.barrier()
+        with ClockSampler(local) as clk:
+            t_step, t_f, launches = R.timed(args.steps, args.warmup, flush)
+        if dist:
+            dist.barrier()
+        t_e2e = R.e2e(max(1, min(args.steps, 5)), dist)
+        extra = None
+        if world == 1 and args.config == 3 and not args.no_extra:
+            R5 = Runner(5, dev, local, stream, None, 1, 0)
+            t5, tf5, _ = R5.timed(2, 1, flush)
+            extra = {"workload": WORKLOADS[5] + "; device-resident, 1 warm-up + 2 timed steps",
+                     "ms_per_step": t5 * 1e3, "factor_ms": tf5 * 1e3, "solve_ms": (t5 - tf5) * 1e3,
+                     "unknowns_per_s": R5.N / t5, "factor_unknowns_per_s": R5.N / tf5,
+                     "solve_unknown_rhs_per_s": R5.N * R5.nrhs / (t5 - tf5), "resid": R5.resid,
+                     "skeleton_counts": [c for _, c in R5.skel],
+                     "roofline": roofline(R5.kstats, 2, *peaks())}
+            del R5
     t_s = t_step - t_f
     if dist:
         tt = torch.tensor([t_step, t_e2e, t_f, t_s], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_e2e, t_f, t_s = [float(v) for v in tt.cpu()]
     pk, pk_kind = peaks()
-    h2d = a.indptr.size * 8 + a.indices.size * 4 + a.data.size * 8 + b_loc.nbytes
+    a = R.a
+    h2d = a.indptr.size * 8 + a.indices.size * 4 + a.data.size * 8 + R.b_host.nbytes
+    N = R.N
     line = {
         "metric": METRIC, "value": N / t_step, "unit": "unknowns/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": t_step * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": f"synthetic (seeded BASELINE cfg{args.config} inputs)",
-        "config": {"workload": f"cfg{args.config}: {variant}, N={N}, eps={eps}, {nrhs} RHS; one instance "
-                               f"sharded over {nr} rank(s){' (emulated on one GPU)' if comm is not None and comm.emulated else ''}; "
-                               "step = factor + this rank's RHS columns",
-                   "parallelism": f"shard x{nr}", "l2": "flushed between timed steps (256 MiB write)"},
+        "config": config_dict(args.config, world, nranks),
         "factor_ms": t_f * 1e3, "solve_ms": t_s * 1e3,
-        "factor_unknowns_per_s": N / t_f,
+        "factor_unknowns_per_s": N / t_f, "solve_unknown_rhs_per_s": N * R.nrhs / t_s if t_s > 0 else None,
         "e2e": {"value": N / t_e2e, "unit": "unknowns/s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(b_loc.nbytes)},
-        "gpu_launches": int(launches), "clocks": clk.summary(), "resid": resid,
-        "skeleton_counts": [c for _, c in skel], "xfer_bytes_rank0": int(xfer),
+                "d2h_bytes_per_step": int(R.b_host.nbytes),
+                "note": "public API (factor_hifde + apply_inverse) with host CSR and pinned host RHS, "
+                        f"mean of {max(1, min(args.steps, 5))} steps after one warm-up"},
+        "gpu_launches": int(launches // max(args.steps, 1)),
+        "gpu_launches_note": "kernel launches of this library per step (factor + solve)",
+        "clocks": clk.summary(),
+        "resid": R.resid, "skeleton_counts": [c for _, c in R.skel],
     }
-    line["roofline"] = roofline(level_info, pk, pk_kind, args)
-    line["roofline_by_class"] = roofline_classes(level_info, pk)
+    if world > 1:
+        line["xfer_bytes_rank0"] = int(R.xfer)
+    line["roofline"] = roofline(R.kstats, args.steps, pk, pk_kind)
+    if extra:
+        line["cfg5"] = extra
+    if cpu_base:
+        line["cpu_baseline"] = cpu_base
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
@@ -413,88 +491,21 @@ def run_sharded(args, world, rank, local):
         dist.destroy_process_group()
 
 
-def roofline_classes(level_info, pk, fp64_tflops=35.5):
-    """Whole-class fractions: the algorithmic bytes / FLOPs of
-    all elimination levels, all skeletonization levels and the terminal block,
-    over their summed CUDA-event time, against the HBM copy roof and the
-    measured DGEMM roof (profiles/r01_fp64_peak.json)."""
-    out = {}
-    for name, kinds in (("elimination", (0,)), ("skeletonization", (1,)), ("terminal", (2,))):
-        lv = [d for d in level_info if d["kind"] in kinds]
-        sec = sum(d["gpu_seconds"] for d in lv)
-        gb = sum(d["gbytes"] for d in lv)
-        gf = sum(d["gflop"] for d in lv)
-        if sec <= 0:
-            continue
-        out[name] = {"gpu_ms": sec * 1e3, "gb_per_s": gb / sec, "tflops": gf / sec * 1e-3,
-                     "hbm_frac": gb / sec / pk.get("hbm_gbs", 6556.0), "fp64_frac": gf / sec * 1e-3 / fp64_tflops}
-    return out
-
-
-def roofline(level_info, pk, pk_kind, args):
-    """HBM roofline of the dominant kernel launch.
-
-    In exact order every skeletonization level is ONE launch of
-    skel_ordered_kernel, and every level's launches are timed by CUDA events
-    on the library's stream; the dominant launch is the level with the
-    largest event time.  achieved = that level's algorithmic bytes (SURVEY.md
-    8(d): 8[nq nc + nc^2 + k r + r^2 + r + r k + 2k^2] per group, 8[(nc+nq)^2
-    + nc^2 + nc + nc nq + 2 nq^2] per cell) / its event time.  traffic = the
-    DRAM bytes ncu measured for the same launch (profiles/roofline_r01.json).
-    The launch is bound by the reference-order dependency chain, not by HBM
-    (profiles/r01_summary.md), hence the small fraction."""
-    dom = max(level_info[:-1], key=lambda d: d["gpu_seconds"])
-    sec, gb, gf = dom["gpu_seconds"], dom["gbytes"], dom["gflop"]
-    achieved = gb / sec if sec > 0 else None
-    peak = pk.get("hbm_gbs")
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "roofline_r01.json")
-    if os.path.exists(prof):
-        try:
-            tb = json.load(open(prof))["skel_levels_dram_bytes"].get(f"{dom['tag']:.1f}")
-            traffic = tb / 1e9 if tb else None
-        except Exception:
-            traffic = None
-    name = "skel_ordered_kernel" if dom["kind"] == 1 else "elim_kernels"
-    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved and peak else None,
-            "traffic": traffic, "traffic_unit": "GB per launch", "kernel": name, "level": dom["tag"],
-            "launch_seconds": sec, "algorithmic_gbytes": gb, "algorithmic_gflop": gf,
-            "achieved_gflops": gf / sec if sec > 0 else None,
-            "limiter": "reference-order dependency chain (latency), see profiles/r01_summary.md",
-            "peak_kind": pk_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
-
-
-def cpu_baseline():
-    import paper_1307_2895_b200.problems as P
-    from oracle import hifde_oracle as O
-    g, a, eps, variant, nrhs = P.baseline_problem(CONFIG)
-    b = np.random.default_rng(1).standard_normal((g.ndof, nrhs))
-    t0 = time.perf_counter()
-    f = O.factor(a, O.make_grid(g.dim, g.n, g.m), eps, variant)
-    f.apply_inverse(b)
-    t = time.perf_counter() - t0
-    return {"value": g.ndof / t, "unit": "unknowns/s", "cores": 1, "kind": "port",
-            "sample": "one full cfg2 factor + 16-RHS solve (oracle port, 1 BLAS thread)"}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG, choices=[2, 3, 4, 5])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--shard", action="store_true", help="one instance sharded over the ranks")
-    ap.add_argument("--config", type=int, default=CONFIG, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--emulate", type=int, default=1, help="virtual ranks on one GPU (--shard, N=1)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the config-5 extra keys")
+    ap.add_argument("--emulate", type=int, default=1, help="virtual ranks on one GPU (sharded code path, N=1)")
+    ap.add_argument("--shard", action="store_true", help=argparse.SUPPRESS)  # sharded is the N>1 default
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
         cpu_reference(args, world, rank)
-        return
-    if args.shard:
-        run_sharded(args, world, rank, local)
         return
     run_gpu(args, world, rank, local)
 

@@ -80,6 +80,8 @@ typedef struct hifde_options {
   double eps;           /* ID relative tolerance (0 -> exact rank)          */
   void* stream;         /* cudaStream_t or NULL                             */
   hifde_comm_t* comm;   /* NULL: one GPU; else shard over comm's ranks      */
+  int kernel_log;       /* 1: time the main launches (hifde_kernel_stats)   */
+  int pad_;
 } hifde_options_t;
 
 typedef struct hifde_factor hifde_factor_t;
@@ -226,6 +228,25 @@ int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info
  * on this thread (the bench's gpu_launches count). */
 int64_t hifde_last_launch_count(void);
 
+/*
+ * Kernel log of a factor created with options.kernel_log = 1: per (kernel,
+ * level) the launches, their summed CUDA-event time and the algorithmic bytes
+ * and FLOPs of the work they cover.  phase 0: the factorization;
+ * phase 1: the last hifde_solve of this factor (per level and direction).
+ * With out == NULL only *count is set.  No reference counterpart (the
+ * reference times levels with perf_counter, src/driver.py:170).
+ */
+typedef struct hifde_kernel_stat {
+  char name[40];
+  double tag;           /* level tag                                        */
+  int32_t phase;        /* 0 factor, 1 solve                                */
+  int32_t launches;     /* launches (or pipelines) aggregated               */
+  double seconds;       /* summed CUDA-event time                           */
+  double gbytes;        /* algorithmic GB of the covered work               */
+  double gflop;         /* algorithmic GFLOP of the covered work            */
+} hifde_kernel_stat_t;
+int hifde_kernel_stats(const hifde_factor_t* f, int phase, hifde_kernel_stat_t* out, int64_t cap,
+                       int64_t* count);
 void hifde_free(hifde_factor_t* f);
 
 /* Thread-local message describing the last non-zero status. */

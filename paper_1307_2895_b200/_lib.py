@@ -29,6 +29,8 @@ class Options(C.Structure):
         ("eps", C.c_double),
         ("stream", C.c_void_p),
         ("comm", C.c_void_p),
+        ("kernel_log", C.c_int),
+        ("pad_", C.c_int),
     ]
 
 
@@ -77,10 +79,17 @@ class LevelInfo(C.Structure):
     ]
 
 
+class KernelStat(C.Structure):  # hifde_kernel_stat_t
+    _fields_ = [
+        ("name", C.c_char * 40), ("tag", C.c_double), ("phase", C.c_int32), ("launches", C.c_int32),
+        ("seconds", C.c_double), ("gbytes", C.c_double), ("gflop", C.c_double),
+    ]
+
+
 # every symbol the public header declares
 EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
-    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count",
+    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count", "hifde_kernel_stats",
     "hifde_free", "hifde_last_error", "hifde_partition",
     "hifde_comm_unique_id", "hifde_comm_init", "hifde_comm_emulated", "hifde_comm_host", "hifde_comm_info",
     "hifde_comm_free",
@@ -136,6 +145,8 @@ def load(path: str | None = None):
     lib.hifde_get_level.argtypes = [C.c_void_p, C.c_int, P(LevelInfo)]
     lib.hifde_get_level.restype = C.c_int
     lib.hifde_last_launch_count.restype = C.c_int64
+    lib.hifde_kernel_stats.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+    lib.hifde_kernel_stats.restype = C.c_int
     lib.hifde_free.argtypes = [C.c_void_p]
     lib.hifde_free.restype = None
     lib.hifde_last_error.restype = C.c_char_p

@@ -150,7 +150,9 @@ void launch_skelbig_assemble(const SkelBigTask* tasks, const int4* work, int nwo
 int cpqr_coop_capacity(size_t smem);
 // Gram path of the large-group ID (kernels_skelbig.cu): G = Mq^T Mq tiles,
 // then a cooperative pivoted Cholesky of G with the CPQR's outputs
-constexpr double kGramMinEps = 1e-6;  // rank cut eps^2 |G| >> u |G|; ID residual error ~ u / eps << eps
+// Used only when u cond(G11) ~ u / eps^2 <= 1e-8 << eps (T = R11^-1 R12 from
+// the Cholesky factor of G loses u cond(G11)); the rank cut eps^2 |G| >> u |G|
+constexpr double kGramMinEps = 1e-4;
 constexpr double kPromoteWork = 2.5e5;  // nq nc^2 above which a one-CTA group joins the pipeline
 constexpr int kGramRows = 1024;  // rows per split of a Gram tile
 void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, const int4* tiles, int ntiles,

@@ -571,9 +571,10 @@ constexpr int kTT = 64, kTK = 16, kTL = 68;  // DMMA tile kernels: 64 x 64 tiles
 // arithmetic.  The Schur diagonal carries an absolute error ~k u |G| against
 // the cut at eps^2 |G|; T = G11^-1 G12 is off by ~u cond(G11) ~ u / eps^2, but
 // only along the small singular directions of M_sk, so the ID residual
-// |M_rd - M_sk T| moves by ~u / eps.  Both are far below eps for eps >= 1e-6
-// (kGramMinEps; ranks identical to the CPQR path on configs 4 and
-// 5).  Traffic: one read of Mq plus O(nc k) per step against O(nq nc) per step
+// |M_rd - M_sk T| moves by ~u / eps.  The path is taken only for eps >=
+// kGramMinEps = 1e-4, where even the worst-case T error u / eps^2 <= 1e-8 is
+// far below eps (config 5, eps = 1e-3: ranks identical to the CPQR path;
+// config 4, eps = 1e-6, takes the CPQR).  Traffic: one read of Mq plus O(nc k) per step against O(nq nc) per step
 // for the CPQR on Mq itself.
 // ---------------------------------------------------------------------------
 // Work item int4 {task, a0, b0, split}: rows [split * kGramRows, +kGramRows)

@@ -125,7 +125,7 @@ struct PinnedStage {
     peak = std::max(peak, n + need);
     if (!p || need > cap) return false;
     if (n + need > cap) {  // full: drain the stream, then reuse from the start
-      cudaStreamSynchronize(s);
+      HCK(cudaStreamSynchronize(s));
       n = 0;
     }
     if (bytes >= (1u << 20)) {  // large uploads: several threads fill the pinned slice
@@ -138,7 +138,7 @@ struct PinnedStage {
     } else {
       std::memcpy(p + n, src, bytes);
     }
-    cudaMemcpyAsync(dst, p + n, bytes, cudaMemcpyHostToDevice, s);
+    HCK(cudaMemcpyAsync(dst, p + n, bytes, cudaMemcpyHostToDevice, s));
     n += need;
     return true;
   }
@@ -280,6 +280,68 @@ struct LevelRec {
   int64_t* d_ptr = nullptr;
   int64_t* d_ent = nullptr;
   int ntargets = 0;
+  // skeleton levels: algorithmic GB / GFLOP of the one-CTA groups [0] and of
+  // the large-group pipeline [1] (kernel log)
+  double gb_cls[2] = {0, 0}, gf_cls[2] = {0, 0};
+  // solve sweep: factor doubles and touched vector rows of the level's records
+  double solve_fac = 0, solve_rows = 0;
+};
+
+// Kernel log (options.kernel_log): CUDA events around the main launches of
+// a factorization and of the solves of its factor, with the algorithmic
+// bytes / FLOPs of the work each launch covers.  bench.py's
+// roofline divides them by the event times (hifde_kernel_stats).
+struct KLog {
+  struct Entry {
+    std::string name;
+    double tag;
+    int phase;  // 0 factor, 1 solve
+    cudaEvent_t e0, e1;
+    double gbytes, gflop;
+  };
+  bool on = false;
+  std::vector<Entry> v;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t ev() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  // returns the entry index, or -1 when the log is off
+  int begin(const char* name, double tag, int phase, double gb, double gf, cudaStream_t s) {
+    if (!on) return -1;
+    Entry E{name, tag, phase, ev(), ev(), gb, gf};
+    cudaEventRecord(E.e0, s);
+    v.push_back(E);
+    return (int)v.size() - 1;
+  }
+  void end(int i, cudaStream_t s) {
+    if (i >= 0) cudaEventRecord(v[(size_t)i].e1, s);
+  }
+  void clear(int phase) {
+    std::vector<Entry> keep;
+    for (auto& E : v) {
+      if (E.phase == phase) {
+        pool.push_back(E.e0);
+        pool.push_back(E.e1);
+      } else {
+        keep.push_back(E);
+      }
+    }
+    v.swap(keep);
+  }
+  ~KLog() {
+    for (auto& E : v) {
+      cudaEventDestroy(E.e0);
+      cudaEventDestroy(E.e1);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
 };
 
 }  // namespace
@@ -301,6 +363,8 @@ struct hifde_factor {
   int64_t max_contrib = 0;
   int64_t tile_rows = 0;  // solve scratch rows of the tiled phases
   char* meta = nullptr;  // every level's solve metadata (one allocation)
+  mutable hifde::KLog klog;  // options.kernel_log (the solve appends its launches)
+  mutable std::mutex klog_m;
   ~hifde_factor() {
     // stream-ordered frees: no device-wide synchronization on release
     cudaSetDevice(device);
@@ -694,6 +758,10 @@ struct Factorizer {
       helper.drain();
     } catch (...) {
     }
+    // a failed factorization (IndefiniteBlockError, CUDA error, ...) leaves
+    // its working buffers here: free them so a caller that retries does not
+    // run out of HBM
+    release_all();
     if (tail_s) {
       cudaStreamSynchronize(tail_s);
       cudaStreamDestroy(tail_s);
@@ -701,14 +769,61 @@ struct Factorizer {
       cudaEventDestroy(ev_tail);
     }
   }
+  // Frees every working buffer of the factorization (stream-ordered) and
+  // hands the borrowed host buffers back to the cache; idempotent.
+  bool released = false;
+  void release_all() {
+    if (released) return;
+    released = true;
+    if (borrowed) {
+      HostCache& hc = host_cache();
+      hc.idx_buf.swap(h_idx);
+      hc.meta_buf.swap(meta.h);
+      borrowed = false;
+    }
+    bvals.release(s);
+    for (auto& l : lanes) l.release(s);
+    for (auto* d : {&xsend, &xrecv}) d->release(s);
+    xseg.release(s);
+    xiseg.release(s);
+    xi32.release(s);
+    agree.release(s);
+    gpart.release(s);
+    scratch.release(s);
+    lists.release(s);
+    status.release(s);
+    kout.release(s);
+    iscratch.release(s);
+    d_blk_dof_off.release(s);
+    d_blk_n.release(s);
+    d_blk_val_off.release(s);
+    if (own_a0) {
+      if (d_indptr) cudaFreeAsync(d_indptr, s);
+      if (d_indices) cudaFreeAsync(d_indices, s);
+      if (d_a0) cudaFreeAsync(d_a0, s);
+      d_indptr = nullptr;
+      d_indices = nullptr;
+      d_a0 = nullptr;
+      own_a0 = false;
+    }
+    if (d_active) cudaFreeAsync(d_active, s);
+    d_active = nullptr;
+    for (auto& L : F ? F->levels : no_levels) {  // a failed run leaves level events behind
+      if (L.ev0) cudaEventDestroy(L.ev0);
+      if (L.ev1) cudaEventDestroy(L.ev1);
+      L.ev0 = L.ev1 = nullptr;
+    }
+  }
+  bool borrowed = false;
+  std::vector<LevelRec> no_levels;
   LevelRec prof;  // setup / finish phase timings
   MetaPack meta;  // solve metadata, uploaded once at the end
   size_t meta_bytes = 0;
   GridDesc g;
   hifde_options_t opt;
-  hifde_factor_t* F;
+  hifde_factor_t* F = nullptr;
   hifde_factor_t* F_ = nullptr;  // alias used by the solve planner
-  cudaStream_t s;
+  cudaStream_t s = nullptr;
   int64_t N;
   // A0 (host + device); the host pattern aliases the caller's arrays when
   // they are host arrays
@@ -1254,8 +1369,12 @@ struct Factorizer {
       L.max_nq = std::max(L.max_nq, nq);
       F->m_f_bytes += 8 * ((int64_t)nc * nc + nc + (int64_t)nc * nq);
       const double dc = nc, dq = nq;
-      L.gflop += (dc * dc * dc / 3 + dc * dc * dq + dc * dq + dc * dq * dq) * 1e-9;
-      L.gbytes += 8.0 * ((dc + dq) * (dc + dq) + dc * dc + dc + dc * dq + 2 * dq * dq) * 1e-9;
+      const double gf = (dc * dc * dc / 3 + dc * dc * dq + dc * dq + dc * dq * dq) * 1e-9;
+      const double gb = 8.0 * ((dc + dq) * (dc + dq) + dc * dc + dc + dc * dq + 2 * dq * dq) * 1e-9;
+      L.gflop += gf;
+      L.gbytes += gb;
+      L.gf_cls[is_big[(size_t)t]] += gf;
+      L.gb_cls[is_big[(size_t)t]] += gb;
     }
     const int64_t idx_base = (int64_t)h_idx.size();
     h_idx.resize((size_t)(idx_base + idx_tot));
@@ -1450,11 +1569,16 @@ struct Factorizer {
     if (!small.empty()) {
       A.status = status.p + st_small;
       static const int nt128_nf = getenv("HIFDE_ELIM128_NF") ? atoi(getenv("HIFDE_ELIM128_NF")) : 64;
+      const int kl = F->klog.begin(is_top ? "elim_small_kernel(top)" : "elim_small_kernel", tag, 0, L.gb_cls[0],
+                                   L.gf_cls[0], s);
       launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= nt128_nf ? 128 : 256, s);
+      F->klog.end(kl, s);
       ++g_launches;
     }
     if (!big.empty()) {
       A.status = status.p + st_big;
+      const int kl = F->klog.begin(is_top ? "elim_blocked_pipeline(top)" : "elim_blocked_pipeline", tag, 0,
+                                   L.gb_cls[1], L.gf_cls[1], s);
       launch_big_assemble(d_big.p, d_asm.p, (int)asm_work.size(), A, d_scale.p, smem_big, s);
       ++g_launches;
       for (int p = 0; p < npanel; ++p) {
@@ -1473,6 +1597,7 @@ struct Factorizer {
       }
       launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
       g_launches += 1 + inv.launch(d_big.p, A, s);
+      F->klog.end(kl, s);
     }
     L.lap("e-launches");
     d_small.release(s);
@@ -1881,7 +2006,9 @@ struct Factorizer {
         HCK(cudaEventCreate(&L.ev1));
         HCK(cudaEventRecord(L.ev0, s));
         if (run_here) {
+          const int kl = F->klog.begin("skel_cluster_kernel", tag, 0, 0, 0, s);
           HCK(launch_skel_cluster(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem_cl, ncls, cs, s));
+          F->klog.end(kl, s);
           ++g_launches;
         }
         HCK(cudaEventRecord(L.ev1, s));
@@ -1909,7 +2036,9 @@ struct Factorizer {
         A.tlog = dtl.p;
       }
       if (run_here) {
+        const int kl = F->klog.begin("skel_ordered_kernel", tag, 0, 0, 0, s);
         HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
+        F->klog.end(kl, s);
         ++g_launches;
       }
       HCK(cudaEventRecord(L.ev1, s));
@@ -2057,13 +2186,16 @@ struct Factorizer {
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
+    int kl_huge = -1;  // kernel log: the large-group pipeline of the level, first batch to the joined tails
     for (int b = 0; b < nbatch; ++b) {
       const size_t b0 = (size_t)b * PP, b1 = (size_t)(b + 1) * PP;
       for (int r = rank_lo(); r < rank_hi(); ++r) {
         const int64_t lo = bs[b0 + r], hi = bs[b0 + r + 1];
         if (hi > lo) {
+          const int kl = F->klog.begin("skel_kernel", tag, 0, 0, 0, s);
           launch_skel(dt.p + lo, (int)(hi - lo), arenas_r(r, false), opt.eps, smem,
                       (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
+          F->klog.end(kl, s);
           ++g_launches;
         }
       }
@@ -2085,6 +2217,7 @@ struct Factorizer {
           HCK(cudaEventCreate(&e1));
           HCK(cudaEventRecord(e0, s));
         }
+        if (kl_huge < 0) kl_huge = F->klog.begin("skel_large_pipeline", tag, 0, 0, 0, s);
         launch_huge_batch(huge, hlo, hhi, dhuge.p, dinner.p, ddmin.p, dscale.p, arenas_r(r, false),
                           arenas_r(r, true), huge_max_nq, huge_max_nf, huge_max_nb, hl);
         if (shapes) {
@@ -2119,6 +2252,7 @@ struct Factorizer {
       if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  batch %d done", b); }
     }
     join_tails();  // the delta blocks and records of every tail before the level ends
+    F->klog.end(kl_huge, s);
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
     L.t_launch = now_s() - tp;
@@ -2203,8 +2337,23 @@ struct Factorizer {
       double fl = 4 * dq * dc * dk - 2 * dk * dk * (dq + dc) + 4 * dk * dk * dk / 3 + 2 * dq * dc +
                   dk * dk * dr + 2 * dk * dk * dr + 4 * dk * dr * dr;
       if (r > 0) fl += dr * dr * dr / 3 + dr * dr * dk + dk * dk * dr;
+      const double gb = 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
       L.gflop += fl * 1e-9;
-      L.gbytes += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
+      L.gbytes += gb;
+      L.gf_cls[T.mode == 2] += fl * 1e-9;
+      L.gb_cls[T.mode == 2] += gb;
+    }
+    // kernel log: the level's totals go to its first launch of each class
+    {
+      bool done[2] = {false, false};
+      for (auto& E : F->klog.v) {
+        if (E.phase != 0 || E.tag != L.tag) continue;
+        const int c = E.name == "skel_large_pipeline" ? 1 : (E.name.rfind("skel_", 0) == 0 ? 0 : -1);
+        if (c < 0) continue;
+        E.gbytes = done[c] ? 0.0 : L.gb_cls[c];
+        E.gflop = done[c] ? 0.0 : L.gf_cls[c];
+        done[c] = true;
+      }
     }
     // the new delta blocks join the membership lists of their sk DOFs
     member.ensure_room(nadd);
@@ -2225,7 +2374,7 @@ struct Factorizer {
   }
 
   // Large groups whose ID goes through the Gram matrix (kernels_skelbig.cu):
-  // loose tolerances only (eps^3 >> u), tall fronts, R columns in shared memory
+  // loose tolerances only (u / eps^2 << eps, kGramMinEps), tall fronts, R columns in shared memory
   bool gram_ok(int nc, int nq) const {
     static const bool off = getenv("HIFDE_NO_GRAM") != nullptr;
     static const double min_eps = getenv("HIFDE_GRAM_MIN_EPS") ? atof(getenv("HIFDE_GRAM_MIN_EPS")) : kGramMinEps;
@@ -2537,6 +2686,9 @@ struct Factorizer {
     for (const SolveRec& R : L.recs) {
       L.all_max_nc = std::max(L.all_max_nc, R.nc);
       L.all_max_nq = std::max(L.all_max_nq, R.nq);
+      const double nc = R.nc, nq = R.nq;  // skeleton: r, k (T, P, W); else P, W
+      L.solve_fac += nc * (nc + 1) / 2 + nc * nq + (L.kind == 1 ? nc * nq : 0.0);
+      L.solve_rows += nc + nq;
     }
     meta.add(&L.d_all, L.recs);
     auto is_large = [](const SolveRec& R) { return R.nc > 96 || R.nq > 192; };
@@ -2830,6 +2982,7 @@ struct Factorizer {
       h_idx.resize(0);
       meta.h.swap(hc.meta_buf);
       meta.h.resize(0);
+      borrowed = true;
     }
     active.resize((size_t)N);
     act.resize((size_t)N);
@@ -3037,31 +3190,8 @@ struct Factorizer {
       hc.hint_idx = h_idx.size();
       hc.hint_scr = scratch.cap;
       hc.hint_meta = meta_bytes;
-      hc.idx_buf.swap(h_idx);
-      hc.meta_buf.swap(meta.h);
     }
-    bvals.release(s);
-    for (auto& l : lanes) l.release(s);
-    for (auto* d : {&xsend, &xrecv}) d->release(s);
-    xseg.release(s);
-    xiseg.release(s);
-    xi32.release(s);
-    agree.release(s);
-    gpart.release(s);
-    scratch.release(s);
-    lists.release(s);
-    status.release(s);
-    kout.release(s);
-    iscratch.release(s);
-    d_blk_dof_off.release(s);
-    d_blk_n.release(s);
-    d_blk_val_off.release(s);
-    if (own_a0) {
-      cudaFreeAsync(d_indptr, s);
-      cudaFreeAsync(d_indices, s);
-      cudaFreeAsync(d_a0, s);
-    }
-    cudaFreeAsync(d_active, s);
+    release_all();
     HCK(cudaStreamSynchronize(s));
     PR.lap("release");
     F->t_f = now_s() - t0;
@@ -3139,11 +3269,30 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     }
   };
   const size_t nl = F->levels.size();
+  // kernel log: one entry per level and direction; algorithmic bytes = the
+  // level's factor entries + one read and one write of every touched row
+  std::unique_lock<std::mutex> klk(F->klog_m, std::defer_lock);
+  if (F->klog.on) {
+    klk.lock();
+    F->klog.clear(1);
+  }
+  auto kbegin = [&](const LevelRec& L, bool fwd) {
+    if (!F->klog.on || (L.nall == 0 && L.recs.empty())) return -1;
+    const char* nm = L.kind == 1 ? (fwd ? "solve_skel_fwd" : "solve_skel_bwd")
+                                 : (fwd ? "solve_elim_fwd" : "solve_elim_bwd");
+    return F->klog.begin(nm, L.tag, 1, 8.0 * (L.solve_fac + 2.0 * L.solve_rows * nrhs) * 1e-9,
+                         2.0 * L.solve_fac * nrhs * 1e-9, s);
+  };
   for (size_t li = 0; li < nl; ++li) {
     const LevelRec& L = F->levels[li];
     const int nr = L.nsmall;
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
+    const int kl = kbegin(L, true);
+    struct KEnd {
+      const hifde_factor_t* F; int kl; cudaStream_t s;
+      ~KEnd() { F->klog.end(kl, s); }
+    } kend{F, kl, s};
     if (L.kind == 1) {
       if (nr && small_skel(L)) {
         launch_solve_skel_small(L.d_recs, nr, idx, fac, v, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 1,
@@ -3175,6 +3324,11 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     const int nr = L.nsmall;
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
+    const int kl = kbegin(L, false);
+    struct KEnd {
+      const hifde_factor_t* F; int kl; cudaStream_t s;
+      ~KEnd() { F->klog.end(kl, s); }
+    } kend{F, kl, s};
     if (L.kind == 1) {
       if (nr && small_skel(L)) {
         launch_solve_skel_small(L.d_recs, nr, idx, fac, v, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 0,
@@ -3538,6 +3692,7 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
     fz.F = F.get();
     fz.F_ = F.get();
     fz.s = F->stream;
+    F->klog.on = opt->kernel_log != 0;
     const int64_t nnz = opt->input_on_device ? 0 : indptr[n];
     const char* sample = getenv("HIFDE_SAMPLE");  // host sampling profile (diagnostics)
     if (sample) host_sampler_start();
@@ -3604,6 +3759,9 @@ int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n, 
     do_solve(f, b, x, nrhs, device_ptrs != 0, s);
   } catch (const Fail& e) {
     return fail_to_status(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
   }
   return HIFDE_OK;
 }
@@ -3620,6 +3778,9 @@ int hifde_apply(const hifde_factor_t* f, const double* x, double* y, int64_t n, 
     do_apply(f, x, y, nrhs, device_ptrs != 0, s);
   } catch (const Fail& e) {
     return fail_to_status(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
   }
   return HIFDE_OK;
 }
@@ -3643,6 +3804,9 @@ int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* ind
     do_pcg(f, indptr, indices, vals, nnz, b, x, tol, max_iter, device_ptrs != 0, s, iters, residual, converged);
   } catch (const Fail& e) {
     return fail_to_status(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
   }
   return HIFDE_OK;
 }
@@ -3673,6 +3837,9 @@ int hifde_copy_arenas(const hifde_factor_t* f, double* fac, int64_t fac_len, int
     if (idx && idx_len) HCK(cudaMemcpy(idx, f->idx.p, (size_t)idx_len * sizeof(int32_t), cudaMemcpyDeviceToHost));
   } catch (const Fail& e) {
     return fail_to_status(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
   }
   return HIFDE_OK;
 }
@@ -3692,6 +3859,9 @@ int hifde_power_norm(const hifde_factor_t* f, const int64_t* indptr, const int32
     do_power(f, indptr, indices, vals, indptr[n], kind, x0, rtol, max_iter, f->stream, value, converged, iters);
   } catch (const Fail& e) {
     return fail_to_status(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
   }
   return HIFDE_OK;
 }
@@ -3731,6 +3901,49 @@ int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info
   info->gflop = L.gflop;
   info->gbytes = L.gbytes;
   info->gpu_seconds = L.gpu_seconds;
+  return HIFDE_OK;
+}
+
+int hifde_kernel_stats(const hifde_factor_t* f, int phase, hifde_kernel_stat_t* out, int64_t cap, int64_t* count) {
+  g_err.clear();
+  if (!f || !count || phase < 0 || phase > 1) { g_err = "bad arguments"; return HIFDE_BADARG; }
+  try {
+    HCK(cudaSetDevice(f->device));
+    std::lock_guard<std::mutex> lk(f->klog_m);
+    // aggregate by (name, tag) in first-launch order
+    std::vector<hifde_kernel_stat_t> agg;
+    for (const auto& E : f->klog.v) {
+      if (E.phase != phase) continue;
+      HCK(cudaEventSynchronize(E.e1));
+      float ms = 0.f;
+      HCK(cudaEventElapsedTime(&ms, E.e0, E.e1));
+      hifde_kernel_stat_t* a = nullptr;
+      for (auto& x : agg)
+        if (x.tag == E.tag && E.name == x.name) a = &x;
+      if (!a) {
+        agg.emplace_back();
+        a = &agg.back();
+        std::memset(a, 0, sizeof *a);
+        std::snprintf(a->name, sizeof a->name, "%s", E.name.c_str());
+        a->tag = E.tag;
+        a->phase = phase;
+      }
+      a->launches += 1;
+      a->seconds += ms * 1e-3;
+      a->gbytes += E.gbytes;
+      a->gflop += E.gflop;
+    }
+    *count = (int64_t)agg.size();
+    if (out) {
+      if (cap < (int64_t)agg.size()) { g_err = "stat buffer too small"; return HIFDE_BADARG; }
+      std::memcpy(out, agg.data(), agg.size() * sizeof(hifde_kernel_stat_t));
+    }
+  } catch (const Fail& e) {
+    return fail_to_status(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
+  }
   return HIFDE_OK;
 }
 

@@ -154,6 +154,21 @@ class GeneralizedLDL:
         if code:
             _raise(self._lib, code)
 
+    def kernel_stats(self, phase: int = 0) -> list:
+        """Per (kernel, level): launches, CUDA-event seconds, algorithmic GB
+        and GFLOP (factors created with ``kernel_log=True``; phase 0 the
+        factorization, 1 the last solve)."""
+        n = C.c_int64()
+        code = self._lib.hifde_kernel_stats(self._h, phase, None, 0, C.byref(n))
+        if code:
+            _raise(self._lib, code)
+        arr = (L.KernelStat * max(n.value, 1))()
+        code = self._lib.hifde_kernel_stats(self._h, phase, arr, n.value, C.byref(n))
+        if code:
+            _raise(self._lib, code)
+        return [{"name": a.name.decode(), "tag": a.tag, "phase": a.phase, "launches": a.launches,
+                 "seconds": a.seconds, "gbytes": a.gbytes, "gflop": a.gflop} for a in arr[:n.value]]
+
     def close(self):
         if self._h is not None and self._h.value:
             self._lib.hifde_free(self._h)
@@ -168,7 +183,7 @@ class GeneralizedLDL:
 
 def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
             order: str = "auto", exact_max_batches: int = 64, device: Optional[int] = None,
-            stream: Optional[int] = None, comm=None) -> GeneralizedLDL:
+            stream: Optional[int] = None, comm=None, kernel_log: bool = False) -> GeneralizedLDL:
     lib = L.load()
     if not spd:
         raise NotImplementedError("indefinite (Bunch-Kaufman) mode is outside the GPU hot path")
@@ -189,6 +204,7 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     opt.verify = int(bool(verify))
     opt.stream = stream
     opt.comm = comm.handle if comm is not None else None  # distributed.Comm: sharded sweep
+    opt.kernel_log = int(bool(kernel_log))
     h = C.c_void_p()
     code = lib.hifde_factor(indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, csr.shape[0],
                             int(grid.dim), int(grid.n), int(grid.m), int(grid.nlevels),
