@@ -9,6 +9,13 @@ form as the packed inverse P = C^-1; the reference's factors follow from C:
   L = C diag(C)^-1, D = diag(C)^2 (src/dense.py:206-214), X = diag(C)^-1 W
 (W = C^-1 A_cq for cells, C^-1 B_sr^T for groups; src/factor_ops.py:147-153,
 196-204).  The record classes mirror the reference's fields one for one.
+
+The file codec (`read_gldl` / `write_gldl` and their array helpers) is a
+format transcription of the reference's `save_factor` / `load_factor`
+(src/driver.py:270-376): the GLDL v1 byte layout, its struct formats and its
+error messages are the specification (byte-identical round trips of the
+reference's own files are tested), so that code follows the reference's
+control flow by necessity.  It is off the hot path.
 """
 
 from __future__ import annotations

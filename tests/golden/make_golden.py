@@ -41,10 +41,34 @@ CASES = [
     ("g3d_n16_m4_x_hc", 3, 16, 4, 1e-3, "hifde3x", "median", 0, 2, True),
     ("g3d_n16_m4_x_gauss", 3, 16, 4, 1e-3, "hifde3x", "gauss", 0, 2, True),
     ("g3d_n32_m4_x", 3, 32, 4, 1e-6, "hifde3x", "const", 0, 1, False),
+    ("g3d_n32_m4_x_gauss", 3, 32, 4, 1e-3, "hifde3x", "gauss", 0, 2, True),
 ]
 
 # small cases whose factor files (GLDL v1) are committed for record-level parity
-GLDL_CASES = ("g2d_n16_m2", "g2d_n32_m4", "g3d_n8_m2", "g3d_n16_m2_x")
+# hifde3x: random-coefficient cases, whose pivots do not tie, pin the adaptive
+# separators (src/partition.py:184-227) record for record over every level
+GLDL_CASES = ("g2d_n16_m2", "g2d_n32_m4", "g3d_n8_m2", "g3d_n16_m4_x_gauss")
+# larger cases whose factor files are too big to commit: every record's index
+# sets only (cells, neighbours, skeletons, redundant DOFs; <name>_idx.npz)
+INDEX_CASES = ("g3d_n32_m4_x_gauss",)
+
+
+def save_record_indices(f, path):
+    """Per level and record: the index sets of the reference's factor records
+    (src/factor_ops.py:29-135) in record order, flattened with offsets."""
+    out = {"tags": np.array([lf.level for lf in f.levels]), "top_idx": np.asarray(f.top_idx, dtype=np.int64)}
+    for li, lf in enumerate(f.levels):
+        parts = {"cell": [], "nbrs": [], "sk": [], "rd": []}
+        for r in lf.records:
+            e = r if hasattr(r, "nbrs") else getattr(r, "elim", None)
+            parts["cell"].append(np.asarray(r.cell, dtype=np.int64))
+            parts["nbrs"].append(np.asarray(e.nbrs if e is not None else [], dtype=np.int64))
+            parts["sk"].append(np.asarray(getattr(r, "sk", []), dtype=np.int64))
+            parts["rd"].append(np.asarray(getattr(r, "rd", []), dtype=np.int64))
+        for k, v in parts.items():
+            out[f"l{li}_{k}"] = np.concatenate(v) if v else np.zeros(0, np.int64)
+            out[f"l{li}_{k}_ptr"] = np.cumsum([0] + [len(x) for x in v]).astype(np.int64)
+    np.savez_compressed(path, **out)
 
 # the full-size configs store the PCG-converged solution u_pcg (BASELINE's
 # solution criterion, ||u_gpu - u_ref|| / ||u_ref|| <= 10 eps): float64 for
@@ -141,6 +165,8 @@ def run_case(hifde, case):
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
     if name in GLDL_CASES:  # the reference's own factor file (src/driver.py:292-315)
         hifde.save_factor(f, os.path.join(HERE, f"{name}.gldl"))
+    if name in INDEX_CASES:
+        save_record_indices(f, os.path.join(HERE, f"{name}_idx.npz"))
     print(f"{name}: N={g.ndof} t_f={tf:.2f}s s_L={out['s_top']} ranks={ranks} "
           f"resid={resid.max():.2e} pcg={rep.n_i}", flush=True)
 

@@ -279,8 +279,9 @@ def test_verify_noninteracting_passes():
 @pytest.mark.parametrize("name", ["cfg2", "cfg4", "cfg3", "cfg5"])
 def test_full_size_config_against_reference(name):
     """BASELINE configs at full size against the reference's own run
-    (tests/golden/<cfg>.npz, summary only): per-level ranks within +-2%,
-    s_top, one-shot residual within 10x, PCG iteration count."""
+    (tests/golden/<cfg>.npz): per-level ranks within +-2%, s_top, one-shot
+    residual within 10x, PCG iteration count within 10% (+-1), and the
+    PCG(tol 1e-12)-converged solution within 10 eps of the reference's."""
     import os
     if not os.path.exists(os.path.join(G.GOLDEN_DIR, name + ".npz")):
         pytest.skip(f"golden {name} not generated")
@@ -301,7 +302,14 @@ def test_full_size_config_against_reference(name):
     rep = H.pcg(csr, b[:, 0], f.apply_inverse, tol=1e-12, max_iter=500)
     assert rep.converged
     its = int(gd["pcg_iters"])
-    assert abs(rep.n_i - its) <= max(1, int(0.25 * its)), (rep.n_i, its)
+    assert abs(rep.n_i - its) <= max(1, round(0.1 * its)), (rep.n_i, its)
+    # BASELINE's solution criterion on the PCG-converged solutions: the
+    # reference's u_pcg is stored in float64 (configs 2, 4) or float32
+    # (configs 3, 5; storage rounding <= 6e-8 relative, far below 10 eps)
+    assert "u_pcg" in gd, "golden lacks the PCG solution (regenerate with make_golden.py --big)"
+    ref = gd["u_pcg"].astype(np.float64)
+    diff = np.linalg.norm(rep.x - ref) / float(gd["u_pcg_norm"])
+    assert diff <= 10 * float(gd["eps"]), (diff, 10 * float(gd["eps"]))
 
 
 def test_many_and_odd_rhs_counts():
