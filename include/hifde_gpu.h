@@ -56,6 +56,10 @@ extern "C" {
 #define HIFDE_ORDER_AUTO 0      /* exact order unless the chain is too long */
 #define HIFDE_ORDER_SNAPSHOT 1  /* all IDs of a level from one snapshot    */
 #define HIFDE_ORDER_EXACT 2     /* reference's sequential semantics        */
+/* where the per-level symbolic analysis (partition, neighbour sets, task
+ * tables) runs; both give identical factors */
+#define HIFDE_SYMBOLIC_AUTO 0   /* on the GPU while levels allow, then host */
+#define HIFDE_SYMBOLIC_HOST 1   /* host analysis for every level           */
 
 /*
  * Rank communicator of the sharded factorization: the fine
@@ -81,7 +85,7 @@ typedef struct hifde_options {
   void* stream;         /* cudaStream_t or NULL                             */
   hifde_comm_t* comm;   /* NULL: one GPU; else shard over comm's ranks      */
   int kernel_log;       /* 1: time the main launches (hifde_kernel_stats)   */
-  int pad_;
+  int symbolic;         /* HIFDE_SYMBOLIC_*: where the level analysis runs  */
 } hifde_options_t;
 
 typedef struct hifde_factor hifde_factor_t;

@@ -21,13 +21,14 @@ SOURCES = [
     "csrc/kernels_skelbig.cu",
     "csrc/kernels_solve.cu",
     "csrc/kernels_krylov.cu",
+    "csrc/symbolic.cu",
     "csrc/runtime.cu",
     "csrc/comm.cu",
     "csrc/partition.cpp",
     "csrc/shard.cpp",
     "csrc/hostprof.cpp",
 ]
-HEADERS = ["csrc/hifde_internal.h", "csrc/partition.h", "csrc/hostprof.h", "csrc/comm.h", "csrc/shard.h"]
+HEADERS = ["csrc/keys.h", "csrc/hifde_internal.h", "csrc/partition.h", "csrc/hostprof.h", "csrc/comm.h", "csrc/shard.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -14,6 +14,7 @@ from ._build import LIB
 HIFDE_OK, HIFDE_INDEFINITE, HIFDE_SINGULAR, HIFDE_BADARG, HIFDE_CUDA, HIFDE_INTERNAL = range(6)
 VARIANT_MF, VARIANT_HIFDE, VARIANT_HIFDE3X = 0, 1, 2
 ORDER = {"auto": 0, "snapshot": 1, "exact": 2}
+SYMBOLIC = {"auto": 0, "device": 0, "host": 1}
 
 
 class Options(C.Structure):
@@ -30,7 +31,7 @@ class Options(C.Structure):
         ("stream", C.c_void_p),
         ("comm", C.c_void_p),
         ("kernel_log", C.c_int),
-        ("pad_", C.c_int),
+        ("symbolic", C.c_int),
     ]
 
 

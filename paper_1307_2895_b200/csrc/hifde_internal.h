@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/hifde_gpu.h"
+
 namespace hifde {
 
 // Per-cell work item of an elimination level (src/factor_ops.py:138-159).
@@ -108,6 +110,96 @@ __host__ __device__ inline int skel_ldq(int nq) { return nq < 32 ? nq : nq + ((2
 // latency-bound (measured: 0.5 ms for a 93-wide terminal block)
 constexpr int kBigCellNc = 64, kBigCellNf = 128;
 constexpr size_t kSolveDynSmem = 190 * 1024;   // solve record kernels: dynamic smem beside the 25 KB staging tile                // largest group skeletonized by one CTA (skel_group)
+
+// ---------------------------------------------------------------------------
+// Workspace sizing of one cell / group, shared by the host task builder and
+// the device symbolic pass (symbolic.cu) so both place work identically.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline size_t hd_align16(size_t x) { return (x + 15) / 16 * 16; }
+
+struct ElimSizes {
+  size_t smem;          // dynamic shared memory of elim_small_kernel (small cells)
+  int32_t big;          // 1: the blocked multi-CTA path
+  int32_t scratch_off;  // ElimTask.scratch_off: -2 room for the inverse workspace, -1 not
+};
+__host__ __device__ inline ElimSizes elim_sizes(int nc, int nq, int maxnb, bool is_top) {
+  const int nf = nc + nq;
+  const size_t ib = hd_align16(sizeof(int32_t) * (size_t)(nf + maxnb));
+  const size_t need = ib + sizeof(double) * (size_t)nf * nf;
+  const size_t need_inv = need + sizeof(double) * (size_t)nc * nc;
+  ElimSizes z;
+  if (need <= kSmemCapBytes && (is_top || (nc < kBigCellNc && nf < kBigCellNf))) {
+    z.big = 0;
+    z.scratch_off = need_inv <= kSmemCapBytes ? -2 : -1;
+    z.smem = z.scratch_off == -2 ? need_inv : need;
+  } else {
+    z.big = 1;
+    z.scratch_off = -1;
+    z.smem = 0;
+  }
+  return z;
+}
+// shared memory of big_assemble for a large cell
+__host__ __device__ inline size_t elim_big_smem(int nf, int maxnb) {
+  return hd_align16(sizeof(int32_t) * (size_t)(nf + 2 * maxnb));
+}
+
+struct SkelSizes {
+  int32_t mode;   // SkelTask.mode: 0 / 1 / 3 one CTA, 2 the large-group pipeline
+  int32_t chunk;  // mode 3: rows per TSQR chunk
+  size_t smem;    // dynamic shared memory of the one-CTA kernels
+  size_t scr;     // doubles of global scratch
+  size_t fac;     // factor-arena doubles without the large-group extra
+  size_t fac_big; // extra doubles when the group takes the large-group pipeline
+};
+// (kernels_factor.cu skel_group: index arrays, then the CPQR vectors)
+__host__ __device__ inline SkelSizes skel_sizes(int nc, int nq, int maxnb) {
+  const int nf = nc + nq;
+  const size_t ib = hd_align16(sizeof(int32_t) * (size_t)(2 * nf + maxnb + 8 * nc)) + sizeof(double) * 5 * (size_t)nc;
+  const size_t q4 = (size_t)nc * nc / 4 + nc;
+  const size_t lq = (size_t)skel_ldq(nq);  // padded column stride in shared memory
+  const size_t wsd = (size_t)(nc + lq) * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
+  const size_t mq = lq * nc + 2 * (size_t)nc;
+  SkelSizes z;
+  z.chunk = 0;
+  z.smem = 0;
+  z.scr = 0;
+  if (nc > kMaxSkelNc) {
+    z.mode = 2;  // beyond the one-CTA CPQR
+  } else if (ib + sizeof(double) * wsd <= kSmemCapBytes) {
+    z.mode = 0;
+    z.smem = ib + sizeof(double) * wsd;
+  } else if (ib + sizeof(double) * mq <= kSmemCapBytes) {
+    z.mode = 1;
+    z.scr = 3 * (size_t)nc * nc + 3 * q4 + 8;
+    z.smem = ib + sizeof(double) * mq;
+  } else if (nq > nc && nc <= 160 && ib + sizeof(double) * ((size_t)(2 * nc) * nc + 2 * (size_t)nc) <= kSmemCapBytes) {
+    // Mq in global scratch, compressed to R (nc x nc) in shared memory by
+    // chunked Householder QR: column norms and pivots are unchanged
+    z.mode = 3;
+    const size_t avail = (kSmemCapBytes - ib) / sizeof(double) - 2 * (size_t)nc;
+    const size_t ch = avail / nc - nc;
+    z.chunk = (int32_t)(ch < (size_t)nq ? ch : (size_t)nq);
+    z.scr = wsd + 8;
+    z.smem = ib + sizeof(double) * ((size_t)(nc + z.chunk) * nc + 2 * (size_t)nc);
+  } else {
+    z.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
+  }
+  z.fac = (size_t)nc * nc + 2 * q4;
+  z.fac_big = (size_t)nc * (nc + 1) / 2 + nc;
+  return z;
+}
+// shared memory of skel_cluster_kernel with cs CTAs per group
+__host__ __device__ inline size_t skel_cluster_need(int nc, int nq, int maxnb, int cs) {
+  const int nf = nc + nq;
+  return hd_align16(sizeof(int32_t) * (size_t)(2 * nf + maxnb + 8 * nc)) +
+         sizeof(double) * (6 * (size_t)nc + (size_t)nq + (size_t)skel_ldq(nq) * ((nc + cs - 1) / cs));
+}
+// global workspace (doubles) of a group in skel_cluster_kernel
+__host__ __device__ inline size_t skel_cluster_scratch(int nc) {
+  const size_t q4 = (size_t)nc * nc / 4 + nc;
+  return 4 * (size_t)nc * nc + 3 * q4 + 8;
+}
 
 // Kernel launchers (kernels_factor.cu / kernels_solve.cu).
 void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,
@@ -225,5 +317,161 @@ void launch_solve_tiles(const TileOp* ops, const int2* work, int nwork, const in
                         double* v, int nrhs, double* tscratch, double* contrib, cudaStream_t s);
 
 constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Device symbolic pass (symbolic.cu): partition, membership, fronts, task
+// tables and block-table updates of a level on the GPU, identical to the host
+// analysis (runtime.cu Factorizer::front_sym / elimination_level /
+// skeleton_level / finish_skeleton_level).
+// ---------------------------------------------------------------------------
+struct SymWork {           // CUB temporary storage (grown on demand, stream-ordered)
+  char* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+};
+struct SymPartArgs {
+  const int32_t* act;      // active DOFs, ascending (act[0, *nact))
+  const int64_t* nact;
+  int64_t nact_ub;         // host bound on *nact (sort length)
+  int dim, side, w, k, kind;  // kind 0 interior cells, 1 edges, 2 faces
+  int32_t nkeys;           // keys are < nkeys; nkeys marks "no group"
+  int32_t* keys;
+  int32_t* skeys;
+  int32_t* gmem;           // members sorted by group (ascending inside a group)
+  int32_t* head;           // scratch: group number of each sorted member
+  int64_t* goff;           // group offsets (ng + 1)
+  int32_t* ng;             // number of groups (device scalar)
+  int32_t* group_of;       // skeleton levels: group of each member DOF, else null
+};
+struct SymMemberArgs {
+  const uint8_t* blk_alive;
+  int64_t nblk_ub;
+  int32_t* alive_list;
+  int64_t* nalive;
+  const int32_t* blk_n;
+  const int64_t* blk_dof_off;
+  const int32_t* idx;
+  const uint8_t* active;
+  int64_t N;
+  int32_t* cnt;            // N + 1
+  int32_t* mptr;           // N + 1: membership CSR (active DOF -> live blocks)
+  int32_t* mblk;
+};
+struct SymFront {
+  const int64_t* goff;
+  const int32_t* gmem;
+  const int32_t* ng;
+  const int32_t* mptr;
+  const int32_t* mblk;
+  const int32_t* blk_n;
+  const int64_t* blk_dof_off;
+  const int32_t* idx;
+  const int64_t* indptr;
+  const int32_t* indices;
+  const uint8_t* active;
+  const int32_t* group_of;  // predecessors (skeleton levels) when non-null
+  // count pass outputs (per group)
+  int32_t* nq;
+  int32_t* nb;
+  int32_t* maxnb;
+  int32_t* npred;
+  int32_t* flag;            // 1: the small shared-memory tier overflowed
+  int32_t* retry;           // groups for the large tier
+  int32_t* nretry;
+  int32_t* fatal;           // even the large tier overflowed (host fallback)
+  // fill pass: offsets from the level's prefix sums (int64 words of the
+  // per-group increment struct), destinations
+  const int64_t* exc;
+  int32_t exc_stride, o_nf, o_nb, o_pred;
+  int64_t idx_base;
+  int32_t* idx_out;
+  int32_t* lists;
+  int32_t* preds;
+};
+constexpr int kElimIncN = 8;  // idx, lists, fac, block arena, contributions, new blocks, small, big
+struct ElimInc { int64_t v[kElimIncN]; };
+constexpr int kSkelIncN = 8;  // idx, lists, scratch, fac, delta blocks, preds, out lists, cluster scratch
+struct SkelInc { int64_t v[kSkelIncN]; };
+struct LevelTotals {          // read back by the host once per level
+  int64_t ng;
+  int64_t sum[8];
+  int64_t smem, max_small_nf, smem_big, max_big_nc, max_front, max_nc, max_nq;
+  int64_t cl_need4, cl_need2, any_mode2, any_promote, max_chain;
+  int64_t pad[2];
+};
+struct LevelStat {            // per device level, read back at the end of the factorization
+  int64_t ngroups, nskel, nred, max_front, mf_bytes, nrecs, max_nc, max_nq;
+  int64_t ntargets, active_after;
+  double gflop, gbytes, solve_fac, solve_rows;
+  double gf_cls[2], gb_cls[2];
+};
+struct ElimFillArgs {
+  int is_top;
+  int64_t idx_base, fac_base, bv_base;
+  const ElimInc* exc;
+  ElimTask* small;
+  ElimTask* big;
+  SolveRec* recs;
+  hifde_record_t* xrec;
+  int64_t* blk_dof_off;
+  int32_t* blk_n;
+  int64_t* blk_val_off;
+  uint8_t* blk_alive;
+  int64_t* nblk;            // device block count (advanced by the stats kernel)
+  const int64_t* newblk_total;
+  const int32_t* lists;
+  const int32_t* idx;
+  int32_t* red_key;         // reduction pairs (neighbour DOF, contribution row)
+  int64_t* red_val;
+  int32_t* red_key2;        // sorted
+  int64_t* red_ent;
+  int32_t* red_targets;
+  int64_t* red_cnt;
+  int64_t* red_ptr;
+  int64_t* red_nt;          // distinct targets (device scalar)
+  int64_t N;
+  double4* cellstat;
+  uint8_t* cellcls;
+  LevelStat* stat;
+};
+struct SkelFillArgs {
+  int64_t idx_base, scr_base, fac_base, bv_base, tot_nf;
+  const SkelInc* exc;
+  SkelTask* tasks;
+  int64_t* pred_ptr;
+  int64_t* cl_rel;          // cluster workspace offset of each group (relative)
+  int32_t* idx;
+};
+struct SkelFinishArgs {
+  int2* inc;
+  int2* exc;
+  SolveRec* recs;
+  hifde_record_t* xrec;
+  int64_t* blk_dof_off;
+  int32_t* blk_n;
+  int64_t* blk_val_off;
+  uint8_t* blk_alive;
+  int64_t* nblk;
+  LevelStat* stat;
+};
+cudaError_t sym_active_list(const uint8_t* active, int64_t N, int32_t* act, int64_t* nact, SymWork& W, cudaStream_t s);
+cudaError_t sym_partition(const SymPartArgs& A, SymWork& W, cudaStream_t s);
+cudaError_t sym_membership(const SymMemberArgs& A, SymWork& W, cudaStream_t s);
+cudaError_t sym_fronts_count(const SymFront& P, cudaStream_t s);
+cudaError_t sym_fronts_fill(const SymFront& P, cudaStream_t s);
+cudaError_t sym_elim_sizes(const SymFront& P, int is_top, int ng_ub, ElimInc* inc, ElimInc* exc, LevelTotals* tot,
+                           SymWork& W, cudaStream_t s);
+cudaError_t sym_elim_fill(const SymFront& P, const ElimFillArgs& A, int64_t nred_ub, SymWork& W, cudaStream_t s);
+cudaError_t sym_skel_sizes(const SymFront& P, double promote_work, int gram_eps_ok, int ng_ub, SkelInc* inc,
+                           SkelInc* exc, LevelTotals* tot, SymWork& W, cudaStream_t s);
+cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t s);
+cudaError_t sym_skel_chain(const int64_t* pred_ptr, const int32_t* preds, const int32_t* ng, int ng_ub, int iters,
+                           int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot, cudaStream_t s);
+cudaError_t sym_skel_cluster_tasks(SkelTask* tasks, const int64_t* cl_rel, int64_t base, const int32_t* ng,
+                                   int ng_ub, cudaStream_t s);
+cudaError_t sym_skel_finish(const SkelTask* tasks, const int32_t* kout, const int32_t* ng, int ng_ub,
+                            const SkelFinishArgs& A, SymWork& W, cudaStream_t s);
+cudaError_t sym_reset_groups(const int32_t* gmem, const int64_t* goff, const int32_t* ng, int32_t* group_of,
+                             cudaStream_t s);
+cudaError_t sym_copy_count(const int64_t* n, int64_t* dst, cudaStream_t s);
 
 }  // namespace hifde

@@ -10,6 +10,7 @@
 // Groups come out in the reference's order: ascending key (family-major for
 // interfaces), members ascending.
 #include "partition.h"
+#include "keys.h"
 
 #include <algorithm>
 #include <stdexcept>
@@ -126,16 +127,7 @@ inline int64_t ipow(int64_t b, int e) {
   return r;
 }
 
-// nearest centre w*j, j in [1, top], ties to the lower j (doubled coords x2)
-inline int near_mult(int x2, int w, int top) {
-  int j = (x2 + w - 1) / (2 * w);
-  return std::min(std::max(j, 1), top);
-}
-// nearest centre w*(j - 1/2), j in [1, top], ties to the lower j
-inline int near_half(int x2, int w, int top) {
-  int j = (x2 + 2 * w - 1) / (2 * w);
-  return std::min(std::max(j, 1), top);
-}
+inline int near_half(int x2, int w, int top) { return key_near_half(x2, w, top); }
 
 }  // namespace
 
@@ -148,15 +140,9 @@ Groups interior_groups(const GridDesc& g, const Coords& X, int ell, const std::v
 #pragma omp parallel for schedule(static) if (na > 16384)
   for (int64_t i = 0; i < na; ++i) {
     const int32_t d = act[(size_t)i];
-    int key = 0, stride = 1;
-    for (int ax = 0; ax < g.dim; ++ax) {
-      const int x = X.x[ax][(size_t)d];
-      const int q = x / w;
-      if (x - q * w == 0) { key = -1; break; }
-      key += q * stride;
-      stride *= k;
-    }
-    kall[(size_t)i] = key;
+    int x[3] = {0, 0, 0};
+    for (int ax = 0; ax < g.dim; ++ax) x[ax] = X.x[ax][(size_t)d];
+    kall[(size_t)i] = interior_key(x, g.dim, w, k);
   }
   return bucket_keys(act, kall, ipow(k, g.dim));
 }
@@ -173,36 +159,9 @@ Groups interface_groups(const GridDesc& g, const Coords& X, int ell, const std::
 #pragma omp parallel for schedule(static) if (na > 16384)
   for (int64_t i = 0; i < na; ++i) {
     const int32_t d = act[(size_t)i];
-    int x2[3];
-    kall[(size_t)i] = -1;
-    int planes = 0;
-    for (int ax = 0; ax < g.dim; ++ax) {
-      const int x = X.x[ax][(size_t)d];
-      x2[ax] = 2 * x;
-      planes += (x % w == 0);
-    }
-    bool excluded;
-    if (g.dim == 2) excluded = planes == 2;
-    else if (face) excluded = planes >= 2;
-    else excluded = planes == 3;
-    if (excluded) continue;
-    int64_t best_d = INT64_MAX;
-    int best_key = 0;
-    for (int fam = 0; fam < g.dim; ++fam) {
-      int64_t dist = 0;
-      int key = 0, stride = 1;
-      for (int ax = 0; ax < g.dim; ++ax) {
-        const bool on_plane = face ? (ax == fam) : (ax != fam);
-        int j, c2, sp;
-        if (on_plane) { j = near_mult(x2[ax], w, k - 1); c2 = 2 * w * j; sp = k - 1; }
-        else { j = near_half(x2[ax], w, k); c2 = w * (2 * j - 1); sp = k; }
-        dist += (int64_t)(x2[ax] - c2) * (x2[ax] - c2);
-        key += (j - 1) * stride;
-        stride *= sp;
-      }
-      if (dist < best_d) { best_d = dist; best_key = fam * span + key; }
-    }
-    kall[(size_t)i] = best_key;
+    int x[3] = {0, 0, 0};
+    for (int ax = 0; ax < g.dim; ++ax) x[ax] = X.x[ax][(size_t)d];
+    kall[(size_t)i] = interface_key(x, g.dim, w, k, face);
   }
   return bucket_keys(act, kall, (int64_t)span * g.dim);
 }

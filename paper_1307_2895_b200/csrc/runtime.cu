@@ -266,6 +266,9 @@ struct LevelRec {
   int nsmall = 0;
   SolveRec* d_all = nullptr;  // every record of the level (apply)
   std::vector<hifde_record_t> xrec;  // export view of every record (hifde_level_records)
+  hifde_record_t* d_xrec = nullptr;  // device-symbolic levels: the export view on the device (copied on demand)
+  int64_t nxrec = 0;
+  int dev_stat = -1;                 // device-symbolic levels: index of the level's LevelStat
   int nall = 0, all_max_nc = 0, all_max_nq = 0;
   int max_nc = 0, max_nq = 0;
   struct Phase {
@@ -364,11 +367,13 @@ struct hifde_factor {
   int64_t tile_rows = 0;  // solve scratch rows of the tiled phases
   char* meta = nullptr;  // every level's solve metadata (one allocation)
   mutable hifde::KLog klog;  // options.kernel_log (the solve appends its launches)
+  std::vector<void*> dev_allocs;  // device-symbolic levels' solve / export tables
   mutable std::mutex klog_m;
   ~hifde_factor() {
     // stream-ordered frees: no device-wide synchronization on release
     cudaSetDevice(device);
     if (meta) cudaFreeAsync(meta, stream);
+    for (void* q : dev_allocs) cudaFreeAsync(q, stream);
     if (fac.p) cudaFreeAsync(fac.p, stream);
     if (idx.p) cudaFreeAsync(idx.p, stream);
     if (own_stream && stream) {
@@ -808,6 +813,7 @@ struct Factorizer {
     }
     if (d_active) cudaFreeAsync(d_active, s);
     d_active = nullptr;
+    dev_release();
     for (auto& L : F ? F->levels : no_levels) {  // a failed run leaves level events behind
       if (L.ev0) cudaEventDestroy(L.ev0);
       if (L.ev1) cudaEventDestroy(L.ev1);
@@ -1316,17 +1322,11 @@ struct Factorizer {
       T.nq = nq;
       T.nblk = f.nb;
       T.maxnb = f.maxnb;
-      const size_t ib = align16(sizeof(int32_t) * (size_t)(nf + T.maxnb));
-      const size_t need = ib + sizeof(double) * (size_t)nf * nf;
-      const size_t need_inv = need + sizeof(double) * (size_t)nc * nc;
-      if (need <= kSmemCap && (is_top || (nc < kBigCellNc && nf < kBigCellNf))) {
-        // -2: room for the inverse workspace after the front as well
-        T.scratch_off = need_inv <= kSmemCap ? -2 : -1;
-        smem_need[(size_t)t] = T.scratch_off == -2 ? need_inv : need;
-      } else {
-        is_big[(size_t)t] = 1;
-        T.scratch_off = -1;
-      }
+      (void)nf;
+      const ElimSizes z = elim_sizes(nc, nq, T.maxnb, is_top);  // -2: room for the inverse workspace too
+      T.scratch_off = z.scratch_off;
+      is_big[(size_t)t] = (uint8_t)z.big;
+      smem_need[(size_t)t] = z.smem;
     }
     int64_t idx_tot = 0, hl_tot = 0;
     size_t fac_tot = 0, bv_tot = 0;
@@ -1342,7 +1342,7 @@ struct Factorizer {
         smem_small = std::max(smem_small, smem_need[(size_t)t]);
         max_small_nf = std::max(max_small_nf, nf);
       } else {
-        smem_big = std::max(smem_big, align16(sizeof(int32_t) * (size_t)(nf + 2 * T.maxnb)));
+        smem_big = std::max(smem_big, elim_big_smem(nf, T.maxnb));
       }
       T.C_off = (int64_t)fac_tot;
       fac_tot += (size_t)nc * nc;
@@ -1488,14 +1488,63 @@ struct Factorizer {
     // blocked large-front path
     auto launch_rank = [&](int r) {
     std::vector<ElimTask> small, big;
-    std::vector<int4> tiles, asm_work;
-    int max_big_nc = 0;
     for (int64_t t = 0; t < nt; ++t) {
       if (sharded() && own_[(size_t)t] != r) continue;
       const ElimTask& T = tasks[(size_t)t];
-      if (!is_big[(size_t)t]) { small.push_back(T); continue; }
-      const int bi = (int)big.size();
-      big.push_back(T);
+      (is_big[(size_t)t] ? big : small).push_back(T);
+    }
+    HTRACE("  host updates done (%zu small / %zu big)", small.size(), big.size());
+    L.lap("e-lists");
+    DBuf<ElimTask> d_small, d_big;
+    d_small.reserve(small.size(), s);
+    d_small.upload(small.data(), 0, small.size(), s);
+    d_big.reserve(big.size(), s);
+    d_big.upload(big.data(), 0, big.size(), s);
+    const int64_t st_small = (int64_t)status.bump(small.size(), s);
+    const char* what = is_top ? "top block" : "cell";
+    pending.push_back({st_small, (int64_t)small.size(), tag, what});
+    L.lap("e-uploads");
+    Arenas A = arenas_for(r);
+    if (!small.empty()) {
+      A.status = status.p + st_small;
+      const int kl = F->klog.begin(is_top ? "elim_small_kernel(top)" : "elim_small_kernel", tag, 0, L.gb_cls[0],
+                                   L.gf_cls[0], s);
+      launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= 64 ? 128 : 256, s);
+      F->klog.end(kl, s);
+      ++g_launches;
+    }
+    launch_big_cells(big, d_big.p, smem_big, A, tag, is_top, L.gb_cls[1], L.gf_cls[1]);
+    L.lap("e-launches");
+    d_small.release(s);
+    d_big.release(s);
+    };
+    for (int r = rank_lo(); r < rank_hi(); ++r) launch_rank(r);
+    HCK(cudaEventRecord(L.ev1, s));
+    HCK(cudaGetLastError());
+    HTRACE("  launched");
+    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
+    // (the kernels retire the cells in the device active mask themselves;
+    // real ranks merge the masks)
+    union_state(nullptr, nullptr, 0, 0);
+    L.t_launch = now_s() - tp;
+    L.lap("launch");
+    tp = now_s();
+    if (is_top) check_status();
+    // solve-side reduction structure for the shared neighbour DOFs
+    if (!is_top) build_reduction((size_t)(&L - F->levels.data()), L);
+    L.t_sync = now_s() - tp;
+  }
+
+  // Blocked multi-CTA path of the large cells of an elimination level
+  // (kernels_big.cu): per-cell work lists on the host from (nc, nq), the
+  // cells' ElimTasks already on the device at d_big.
+  void launch_big_cells(const std::vector<ElimTask>& big, const ElimTask* d_big, size_t smem_big, Arenas A,
+                        double tag, bool is_top, double gb, double gf) {
+    if (big.empty()) return;
+    std::vector<int4> tiles, asm_work;
+    int max_big_nc = 0;
+    for (int bi = 0; bi < (int)big.size(); ++bi) {
+      const ElimTask& T = big[(size_t)bi];
       max_big_nc = std::max(max_big_nc, T.nc);
       const int nf = T.nc + T.nq;
       for (int r0 = 0; r0 < nf; r0 += 64) asm_work.push_back(make_int4(bi, r0, std::min(r0 + 64, nf), 0));
@@ -1532,18 +1581,10 @@ struct Factorizer {
       pt_off[(size_t)p + 1] = (int64_t)ptrsm.size();
       pu_off[(size_t)p + 1] = (int64_t)pupd.size();
     }
-    HTRACE("  host updates done (%zu small / %zu big / %zu tiles)", small.size(), big.size(), tiles.size());
-    // uploads
-    L.lap("e-lists");
-    DBuf<ElimTask> d_small, d_big;
     DBuf<int4> d_tiles, d_asm, d_ptrsm, d_pupd;
     DBuf<int32_t> d_pcells;
     DBuf<double> d_dmin, d_scale;
     auto up4 = [&](DBuf<int4>& d, const std::vector<int4>& h) { d.reserve(h.size(), s); d.upload(h.data(), 0, h.size(), s); };
-    d_small.reserve(small.size(), s);
-    d_small.upload(small.data(), 0, small.size(), s);
-    d_big.reserve(big.size(), s);
-    d_big.upload(big.data(), 0, big.size(), s);
     up4(d_tiles, tiles);
     up4(d_asm, asm_work);
     up4(d_ptrsm, ptrsm);
@@ -1551,57 +1592,35 @@ struct Factorizer {
     inv.upload(s);
     d_pcells.reserve(pcells.size(), s);
     d_pcells.upload(pcells.data(), 0, pcells.size(), s);
-    if (!big.empty()) {
-      std::vector<double> dm(big.size(), DBL_MAX);
-      d_dmin.reserve(big.size(), s);
-      d_dmin.upload(dm.data(), 0, dm.size(), s);
-      d_scale.reserve(big.size(), s);
-      HCK(cudaMemsetAsync(d_scale.p, 0, big.size() * sizeof(double), s));
-    }
-    const int64_t st_small = (int64_t)status.bump(small.size(), s);
+    std::vector<double> dm(big.size(), DBL_MAX);
+    d_dmin.reserve(big.size(), s);
+    d_dmin.upload(dm.data(), 0, dm.size(), s);
+    d_scale.reserve(big.size(), s);
+    HCK(cudaMemsetAsync(d_scale.p, 0, big.size() * sizeof(double), s));
     const int64_t st_big = (int64_t)status.bump(big.size(), s);
-    if (!big.empty()) HCK(cudaMemsetAsync(status.p + st_big, 0, big.size() * sizeof(int), s));
-    const char* what = is_top ? "top block" : "cell";
-    pending.push_back({st_small, (int64_t)small.size(), tag, what});
-    pending.push_back({st_big, (int64_t)big.size(), tag, what});
-    L.lap("e-uploads");
-    Arenas A = arenas_for(r);
-    if (!small.empty()) {
-      A.status = status.p + st_small;
-      static const int nt128_nf = getenv("HIFDE_ELIM128_NF") ? atoi(getenv("HIFDE_ELIM128_NF")) : 64;
-      const int kl = F->klog.begin(is_top ? "elim_small_kernel(top)" : "elim_small_kernel", tag, 0, L.gb_cls[0],
-                                   L.gf_cls[0], s);
-      launch_elim_small(d_small.p, (int)small.size(), A, smem_small, max_small_nf <= nt128_nf ? 128 : 256, s);
-      F->klog.end(kl, s);
+    HCK(cudaMemsetAsync(status.p + st_big, 0, big.size() * sizeof(int), s));
+    pending.push_back({st_big, (int64_t)big.size(), tag, is_top ? "top block" : "cell"});
+    A.status = status.p + st_big;
+    const int kl = F->klog.begin(is_top ? "elim_blocked_pipeline(top)" : "elim_blocked_pipeline", tag, 0, gb, gf, s);
+    launch_big_assemble(d_big, d_asm.p, (int)asm_work.size(), A, d_scale.p, smem_big, s);
+    ++g_launches;
+    for (int p = 0; p < npanel; ++p) {
+      const int p0 = p * kPanelB;
+      launch_panel_chol(d_big, d_pcells.p + pc_off[(size_t)p], (int)(pc_off[(size_t)p + 1] - pc_off[(size_t)p]), p0,
+                        A, d_dmin.p, s);
+      launch_panel_trsm(d_big, d_ptrsm.p + pt_off[(size_t)p], (int)(pt_off[(size_t)p + 1] - pt_off[(size_t)p]), p0, A,
+                        s);
+      launch_panel_update(d_big, d_pupd.p + pu_off[(size_t)p], (int)(pu_off[(size_t)p + 1] - pu_off[(size_t)p]), p0,
+                          A, s);
+      g_launches += 3;
+    }
+    if (!tiles.empty()) {
+      launch_schur_tiles(d_big, d_tiles.p, (int)tiles.size(), A, s);
       ++g_launches;
     }
-    if (!big.empty()) {
-      A.status = status.p + st_big;
-      const int kl = F->klog.begin(is_top ? "elim_blocked_pipeline(top)" : "elim_blocked_pipeline", tag, 0,
-                                   L.gb_cls[1], L.gf_cls[1], s);
-      launch_big_assemble(d_big.p, d_asm.p, (int)asm_work.size(), A, d_scale.p, smem_big, s);
-      ++g_launches;
-      for (int p = 0; p < npanel; ++p) {
-        const int p0 = p * kPanelB;
-        launch_panel_chol(d_big.p, d_pcells.p + pc_off[(size_t)p], (int)(pc_off[(size_t)p + 1] - pc_off[(size_t)p]),
-                          p0, A, d_dmin.p, s);
-        launch_panel_trsm(d_big.p, d_ptrsm.p + pt_off[(size_t)p], (int)(pt_off[(size_t)p + 1] - pt_off[(size_t)p]),
-                          p0, A, s);
-        launch_panel_update(d_big.p, d_pupd.p + pu_off[(size_t)p], (int)(pu_off[(size_t)p + 1] - pu_off[(size_t)p]),
-                            p0, A, s);
-        g_launches += 3;
-      }
-      if (!tiles.empty()) {
-        launch_schur_tiles(d_big.p, d_tiles.p, (int)tiles.size(), A, s);
-        ++g_launches;
-      }
-      launch_big_finish(d_big.p, (int)big.size(), A, d_dmin.p, d_scale.p, s);
-      g_launches += 1 + inv.launch(d_big.p, A, s);
-      F->klog.end(kl, s);
-    }
-    L.lap("e-launches");
-    d_small.release(s);
-    d_big.release(s);
+    launch_big_finish(d_big, (int)big.size(), A, d_dmin.p, d_scale.p, s);
+    g_launches += 1 + inv.launch(d_big, A, s);
+    F->klog.end(kl, s);
     d_tiles.release(s);
     d_asm.release(s);
     d_ptrsm.release(s);
@@ -1610,22 +1629,6 @@ struct Factorizer {
     d_pcells.release(s);
     d_dmin.release(s);
     d_scale.release(s);
-    };
-    for (int r = rank_lo(); r < rank_hi(); ++r) launch_rank(r);
-    HCK(cudaEventRecord(L.ev1, s));
-    HCK(cudaGetLastError());
-    HTRACE("  launched");
-    if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
-    // (the kernels retire the cells in the device active mask themselves;
-    // real ranks merge the masks)
-    union_state(nullptr, nullptr, 0, 0);
-    L.t_launch = now_s() - tp;
-    L.lap("launch");
-    tp = now_s();
-    if (is_top) check_status();
-    // solve-side reduction structure for the shared neighbour DOFs
-    if (!is_top) build_reduction((size_t)(&L - F->levels.data()), L);
-    L.t_sync = now_s() - tp;
   }
 
   // Solve-side reduction of one elimination level: for every neighbour DOF the
@@ -1753,39 +1756,17 @@ struct Factorizer {
         Sz& z = sz[(size_t)t];
         z.scr = 0;
         z.smem = 0;
-        // index arrays, then the CPQR vectors (kernels_factor.cu skel_group)
-        const size_t ib = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * nc)) + sizeof(double) * 5 * (size_t)nc;
-        const size_t q4 = (size_t)nc * nc / 4 + nc;
-        const size_t lq = (size_t)skel_ldq(nq);  // padded column stride in shared memory
-        const size_t wsd = (size_t)(nc + lq) * nc + 2 * (size_t)nc + 3 * q4 + 2 * (size_t)nc * nc;
-        const size_t mq = lq * nc + 2 * (size_t)nc;
-        if (nc > kMaxSkelNc) {
-          T.mode = 2;  // beyond the one-CTA CPQR
-        } else if (ib + sizeof(double) * wsd <= kSmemCap) {
-          T.mode = 0;
-          z.smem = ib + sizeof(double) * wsd;
-        } else if (ib + sizeof(double) * mq <= kSmemCap) {
-          T.mode = 1;
-          z.scr = 3 * (size_t)nc * nc + 3 * q4 + 8;
-          z.smem = ib + sizeof(double) * mq;
-        } else if (nq > nc && nc <= 160 &&
-                   ib + sizeof(double) * ((size_t)(2 * nc) * nc + 2 * (size_t)nc) <= kSmemCap) {
-          // Mq in global scratch, compressed to R (nc x nc) in shared memory by
-          // chunked Householder QR: column norms and pivots are unchanged
-          T.mode = 3;
-          const size_t avail = (kSmemCap - ib) / sizeof(double) - 2 * (size_t)nc;
-          T.chunk = (int32_t)std::min<size_t>(avail / nc - nc, (size_t)nq);
-          z.scr = wsd + 8;
-          z.smem = ib + sizeof(double) * ((size_t)(nc + T.chunk) * nc + 2 * (size_t)nc);
-        } else {
-          T.mode = 2;  // too large for one CTA: cluster pipeline (kernels_skelbig.cu)
-        }
+        const SkelSizes zz = skel_sizes(nc, nq, T.maxnb);
+        (void)nf;
+        T.mode = zz.mode;
+        T.chunk = zz.chunk;
+        z.scr = zz.scr;
+        z.smem = zz.smem;
         // one-CTA groups the Gram path can take keep room for the large-group
         // record: they join the large-group pipeline in exact batches
         // (promote[] below), where a one-CTA launch per batch would be exposed
         promote[(size_t)t] = (T.mode == 1 || T.mode == 3) && (double)nq * nc * nc >= promote_work && gram_ok(nc, nq);
-        z.fac = (size_t)nc * nc + 2 * q4 +
-                ((T.mode == 2 || promote[(size_t)t]) ? (size_t)nc * (nc + 1) / 2 + nc : 0);
+        z.fac = zz.fac + ((T.mode == 2 || promote[(size_t)t]) ? zz.fac_big : 0);
         const size_t p0 = mypred.size();
         for (int i = 0; i < nq; ++i) {
           const int32_t go = group_of[(size_t)q[i]];
@@ -1971,10 +1952,7 @@ struct Factorizer {
         bool fits = true;
         for (int64_t t = 0; t < nt && fits; ++t) {
           const SkelTask& T = tasks[(size_t)t];
-          const int nf = T.nc + T.nq;
-          const size_t need = align16(sizeof(int32_t) * (size_t)(2 * nf + T.maxnb + 8 * T.nc)) +
-                              sizeof(double) * (6 * (size_t)T.nc + (size_t)T.nq +
-                                                (size_t)skel_ldq(T.nq) * ((T.nc + csz - 1) / csz));
+          const size_t need = skel_cluster_need(T.nc, T.nq, T.maxnb, csz);
           need_max = std::max(need_max, need);
           fits = need <= kSmemCap;
         }
@@ -1994,9 +1972,8 @@ struct Factorizer {
         std::vector<SkelTask> ct(tasks);  // per-group global workspace of the cluster kernel
         size_t tot = 0;
         for (auto& T : ct) {
-          const size_t q4 = (size_t)T.nc * T.nc / 4 + T.nc;
           T.scratch_off = (int64_t)tot;
-          tot += 4 * (size_t)T.nc * T.nc + 3 * q4 + 8;
+          tot += skel_cluster_scratch(T.nc);
         }
         const int64_t base = (int64_t)scratch.bump(tot, s);
         for (auto& T : ct) T.scratch_off += base;
@@ -2750,6 +2727,637 @@ struct Factorizer {
     upload(B, L.bwd_ph);
   }
 
+  // =========================================================================
+  // Device symbolic mode (symbolic.cu): the level's partition, fronts, task
+  // tables and block-table updates run on the GPU; the host only sizes the
+  // arenas (one small readback per level) and launches.  Used from level 0
+  // while the levels are interior / interface partitions; dev_to_host()
+  // hands the state to the host analysis before the first level it cannot
+  // take (adaptive hifde3x cells, large skeleton groups, the terminal block).
+  // =========================================================================
+  struct SymScalars {
+    int64_t nact, nalive, nblk, red_nt;
+    int32_t ng, nretry, fatal, pad;
+  };
+  bool dev_mode = false;
+  SymWork symw;
+  DBuf<int32_t> sy_act, sy_keys, sy_skeys, sy_gmem, sy_head, sy_group_of;
+  DBuf<int64_t> sy_goff;
+  DBuf<uint8_t> sy_alive;  // block alive flags (device mode)
+  DBuf<int32_t> sy_alist, sy_mcnt, sy_mptr, sy_mblk;
+  DBuf<int32_t> sy_nq, sy_nb, sy_maxnb, sy_npred, sy_flag, sy_retry;
+  DBuf<int64_t> sy_inc, sy_exc;  // ElimInc / SkelInc storage (8 words per group)
+  DBuf<int32_t> sy_preds, sy_b0, sy_b1, sy_changed;
+  DBuf<int64_t> sy_pred_ptr, sy_cl_rel;
+  DBuf<ElimTask> sy_small, sy_big;
+  DBuf<SkelTask> sy_tasks;
+  DBuf<int32_t> sy_red_key, sy_red_key2;
+  DBuf<int64_t> sy_red_val;
+  DBuf<double4> sy_cellstat;
+  DBuf<uint8_t> sy_cellcls;
+  DBuf<int2> sy_fin;
+  DBuf<int> sy_done;
+  SymScalars* d_scal = nullptr;
+  LevelTotals* d_tot = nullptr;
+  LevelStat* d_lstat = nullptr;
+  int lstat_cap = 0, nlstat = 0;
+  SymScalars* h_scal = nullptr;  // pinned
+  LevelTotals* h_tot = nullptr;  // pinned
+  int64_t nblk_ub = 0;           // host bound on the device block count
+  int64_t nact_ub = 0;           // host bound on the active count
+  int last_dev_level = -1;       // LevelRec index of the previous device level (its active_after)
+  std::vector<size_t> dev_levels;  // LevelRec indices of the device levels
+
+  void* dev_alloc(size_t bytes) {
+    void* q = nullptr;
+    HCK(cudaMallocAsync(&q, std::max<size_t>(bytes, 16), s));
+    F->dev_allocs.push_back(q);
+    return q;
+  }
+
+  void dev_init() {
+    const int cap = 3 * std::max(g.nlevels, 1) + 8;
+    HCK(cudaMallocAsync((void**)&d_scal, sizeof(SymScalars), s));
+    HCK(cudaMallocAsync((void**)&d_tot, sizeof(LevelTotals), s));
+    HCK(cudaMallocAsync((void**)&d_lstat, sizeof(LevelStat) * (size_t)cap, s));
+    HCK(cudaMemsetAsync(d_scal, 0, sizeof(SymScalars), s));
+    HCK(cudaMemsetAsync(d_lstat, 0, sizeof(LevelStat) * (size_t)cap, s));
+    lstat_cap = cap;
+    static SymScalars* hs = nullptr;
+    static LevelTotals* ht = nullptr;
+    if (!hs) {
+      HCK(cudaHostAlloc((void**)&hs, sizeof(SymScalars), cudaHostAllocDefault));
+      HCK(cudaHostAlloc((void**)&ht, sizeof(LevelTotals), cudaHostAllocDefault));
+    }
+    h_scal = hs;
+    h_tot = ht;
+    sy_group_of.reserve((size_t)N, s);
+    HCK(cudaMemsetAsync(sy_group_of.p, 0xFF, sizeof(int32_t) * (size_t)N, s));
+    nact_ub = N;
+    nblk_ub = 0;
+  }
+
+  void dev_release() {
+    for (auto* b : {&sy_act, &sy_keys, &sy_skeys, &sy_gmem, &sy_head, &sy_group_of, &sy_alist, &sy_mcnt, &sy_mptr,
+                    &sy_mblk, &sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry, &sy_preds, &sy_b0, &sy_b1,
+                    &sy_changed, &sy_red_key, &sy_red_key2})
+      b->release(s);
+    for (auto* b : {&sy_goff, &sy_inc, &sy_exc, &sy_pred_ptr, &sy_cl_rel, &sy_red_val}) b->release(s);
+    sy_alive.release(s);
+    sy_cellcls.release(s);
+    sy_small.release(s);
+    sy_big.release(s);
+    sy_tasks.release(s);
+    sy_cellstat.release(s);
+    sy_fin.release(s);
+    sy_done.release(s);
+    if (symw.cub_tmp) cudaFreeAsync(symw.cub_tmp, s);
+    symw.cub_tmp = nullptr;
+    symw.cub_bytes = 0;
+    for (void** q : {(void**)&d_scal, (void**)&d_tot, (void**)&d_lstat})
+      if (*q) {
+        cudaFreeAsync(*q, s);
+        *q = nullptr;
+      }
+  }
+
+  // block-table capacity for `ub` blocks (new alive flags zero; growth keeps
+  // every existing entry)
+  void dev_blocks_reserve(int64_t ub) {
+    const size_t old = sy_alive.cap;
+    d_blk_dof_off.n = d_blk_dof_off.cap;
+    d_blk_n.n = d_blk_n.cap;
+    d_blk_val_off.n = d_blk_val_off.cap;
+    sy_alive.n = sy_alive.cap;
+    d_blk_dof_off.reserve((size_t)ub, s);
+    d_blk_n.reserve((size_t)ub, s);
+    d_blk_val_off.reserve((size_t)ub, s);
+    sy_alive.reserve((size_t)ub, s);
+    if (sy_alive.cap > old) HCK(cudaMemsetAsync(sy_alive.p + old, 0, sy_alive.cap - old, s));
+  }
+
+  // per-group scratch of the symbolic pass for up to `ng_ub` groups
+  void dev_group_reserve(int64_t ng_ub) {
+    for (auto* b : {&sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry}) b->reserve((size_t)ng_ub + 1, s);
+    sy_inc.reserve((size_t)8 * (ng_ub + 1), s);
+    sy_exc.reserve((size_t)8 * (ng_ub + 1), s);
+    sy_goff.reserve((size_t)ng_ub + 2, s);
+  }
+
+  // pending status words + totals and scalars to the host (the level's sync)
+  void dev_sync_totals() {
+    HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
+    HCK(cudaMemcpyAsync(h_scal, d_scal, sizeof(SymScalars), cudaMemcpyDeviceToHost, s));
+    check_status();  // synchronizes the stream
+  }
+
+  // Partition + membership + count pass of a level.  kind 0 interior cells,
+  // 1 edges, 2 faces.  Returns false when the level overflowed the device
+  // front tiers (the host takes over).
+  bool dev_front_count(int ell, int kind, SymFront& P, int64_t& ng_ub) {
+    a0_ready();
+    const int w = g.m << ell, k = g.n / w;
+    int64_t nkeys = 1;
+    for (int ax = 0; ax < g.dim; ++ax) nkeys *= k;
+    if (kind != 0) nkeys *= g.dim;
+    ng_ub = nkeys;
+    // active list (its count is the previous device level's active_after)
+    sy_act.reserve((size_t)N, s);
+    HCK(sym_active_list(d_active, N, sy_act.p, &d_scal->nact, symw, s));
+    if (last_dev_level >= 0)
+      HCK(sym_copy_count(&d_scal->nact, &d_lstat[F->levels[(size_t)last_dev_level].dev_stat].active_after, s));
+    for (auto* b : {&sy_keys, &sy_skeys, &sy_gmem, &sy_head}) b->reserve((size_t)nact_ub + 1, s);
+    dev_group_reserve(ng_ub);
+    SymPartArgs A;
+    A.act = sy_act.p;
+    A.nact = &d_scal->nact;
+    A.nact_ub = nact_ub;
+    A.dim = g.dim;
+    A.side = g.n - 1;
+    A.w = w;
+    A.k = k;
+    A.kind = kind;
+    A.nkeys = (int32_t)nkeys;
+    A.keys = sy_keys.p;
+    A.skeys = sy_skeys.p;
+    A.gmem = sy_gmem.p;
+    A.head = sy_head.p;
+    A.goff = sy_goff.p;
+    A.ng = &d_scal->ng;
+    A.group_of = kind != 0 ? sy_group_of.p : nullptr;
+    HCK(sym_partition(A, symw, s));
+    // membership of the live blocks over the active DOFs
+    sy_alist.reserve((size_t)std::max<int64_t>(nblk_ub, 1), s);
+    sy_mcnt.reserve((size_t)N + 1, s);
+    sy_mptr.reserve((size_t)N + 1, s);
+    int64_t ment = 0;  // bound on the membership entries: the live blocks' orders
+    ment = std::max<int64_t>(ment, mem_entries_ub);
+    sy_mblk.reserve((size_t)std::max<int64_t>(ment, 1), s);
+    SymMemberArgs M;
+    M.blk_alive = sy_alive.p;
+    M.nblk_ub = nblk_ub;
+    M.alive_list = sy_alist.p;
+    M.nalive = &d_scal->nalive;
+    M.blk_n = d_blk_n.p;
+    M.blk_dof_off = d_blk_dof_off.p;
+    M.idx = F->idx.p;
+    M.active = d_active;
+    M.N = N;
+    M.cnt = sy_mcnt.p;
+    M.mptr = sy_mptr.p;
+    M.mblk = sy_mblk.p;
+    if (nblk_ub > 0) {
+      HCK(sym_membership(M, symw, s));
+    } else {
+      HCK(cudaMemsetAsync(sy_mptr.p, 0, sizeof(int32_t) * ((size_t)N + 1), s));
+    }
+    std::memset(&P, 0, sizeof P);
+    P.goff = sy_goff.p;
+    P.gmem = sy_gmem.p;
+    P.ng = &d_scal->ng;
+    P.mptr = sy_mptr.p;
+    P.mblk = sy_mblk.p;
+    P.blk_n = d_blk_n.p;
+    P.blk_dof_off = d_blk_dof_off.p;
+    P.idx = F->idx.p;
+    P.indptr = d_indptr;
+    P.indices = d_indices;
+    P.active = d_active;
+    P.group_of = kind != 0 ? sy_group_of.p : nullptr;
+    P.nq = sy_nq.p;
+    P.nb = sy_nb.p;
+    P.maxnb = sy_maxnb.p;
+    P.npred = sy_npred.p;
+    P.flag = sy_flag.p;
+    P.retry = sy_retry.p;
+    P.nretry = &d_scal->nretry;
+    P.fatal = &d_scal->fatal;
+    HCK(cudaMemsetAsync(sy_npred.p, 0, sizeof(int32_t) * ((size_t)ng_ub + 1), s));
+    HCK(sym_fronts_count(P, s));
+    return true;
+  }
+  int64_t mem_entries_ub = 0;  // bound on sum of the live blocks' orders
+
+  // register the level's LevelStat slot
+  int dev_stat_slot(LevelRec& L) {
+    if (nlstat >= lstat_cap) throw Fail{HIFDE_INTERNAL, "device level statistics overflow"};
+    L.dev_stat = nlstat++;
+    return L.dev_stat;
+  }
+
+  // ---- elimination level ---------------------------------------------------
+  // returns false if the host must take this level (state handed over)
+  bool dev_elimination_level(int ell, double tag, LevelRec& L) {
+    const double t_begin = now_s();
+    L.kind = 0;
+    L.lap(nullptr);
+    HCK(cudaEventCreate(&L.ev0));
+    HCK(cudaEventCreate(&L.ev1));
+    HCK(cudaEventRecord(L.ev0, s));
+    const int kls = F->klog.begin("symbolic_device", tag, 0, 0, 0, s);
+    SymFront P;
+    int64_t ng_ub = 0;
+    dev_front_count(ell, 0, P, ng_ub);
+    ElimInc* inc = reinterpret_cast<ElimInc*>(sy_inc.p);
+    ElimInc* exc = reinterpret_cast<ElimInc*>(sy_exc.p);
+    HCK(sym_elim_sizes(P, 0, (int)ng_ub, inc, exc, d_tot, symw, s));
+    dev_sync_totals();
+    L.lap("dev-count");
+    if (h_scal->fatal) {
+      F->klog.end(kls, s);
+      HCK(cudaEventRecord(L.ev1, s));
+      return false;
+    }
+    nact_ub = h_scal->nact;
+    const LevelTotals T = *h_tot;
+    const int64_t ng = T.ng;
+    L.ngroups = ng;
+    L.max_front = T.max_front;
+    const int st = dev_stat_slot(L);
+    // arenas
+    const int64_t idx_base = (int64_t)F->idx.bump((size_t)T.sum[0], s);
+    lists.reserve((size_t)std::max<int64_t>(T.sum[1], 1), s);
+    lists.n = (size_t)T.sum[1];
+    const int64_t fac_base = (int64_t)F->fac.bump((size_t)T.sum[2], s);
+    const int64_t bv_base = T.sum[3] ? (int64_t)bvals.bump((size_t)T.sum[3], s) : 0;
+    dev_blocks_reserve(nblk_ub + T.sum[5] + 1);
+    sy_small.reserve((size_t)std::max<int64_t>(T.sum[6], 1), s);
+    sy_big.reserve((size_t)std::max<int64_t>(T.sum[7], 1), s);
+    sy_red_key.reserve((size_t)T.sum[4] + 1, s);
+    sy_red_key2.reserve((size_t)T.sum[4] + 1, s);
+    sy_red_val.reserve((size_t)T.sum[4] + 1, s);
+    sy_cellstat.reserve((size_t)ng + 1, s);
+    sy_cellcls.reserve((size_t)ng + 1, s);
+    SolveRec* recs = (SolveRec*)dev_alloc(sizeof(SolveRec) * (size_t)ng);
+    hifde_record_t* xr = (hifde_record_t*)dev_alloc(sizeof(hifde_record_t) * (size_t)ng);
+    int32_t* red_t = (int32_t*)dev_alloc(sizeof(int32_t) * ((size_t)T.sum[4] + 1));
+    int64_t* red_ptr = (int64_t*)dev_alloc(sizeof(int64_t) * ((size_t)T.sum[4] + 2));
+    int64_t* red_ent = (int64_t*)dev_alloc(sizeof(int64_t) * ((size_t)T.sum[4] + 1));
+    int64_t* red_cnt = reinterpret_cast<int64_t*>(sy_inc.p);  // the increments are no longer needed after the fill
+    // fronts into the arenas
+    P.exc = sy_exc.p;
+    P.exc_stride = kElimIncN;
+    P.o_nf = 0;
+    P.o_nb = 1;
+    P.o_pred = 0;
+    P.idx_base = idx_base;
+    P.idx_out = F->idx.p;
+    P.lists = lists.p;
+    P.preds = nullptr;
+    HCK(sym_fronts_fill(P, s));
+    ElimFillArgs A;
+    A.is_top = 0;
+    A.idx_base = idx_base;
+    A.fac_base = fac_base;
+    A.bv_base = bv_base;
+    A.exc = exc;
+    A.small = sy_small.p;
+    A.big = sy_big.p;
+    A.recs = recs;
+    A.xrec = xr;
+    A.blk_dof_off = d_blk_dof_off.p;
+    A.blk_n = d_blk_n.p;
+    A.blk_val_off = d_blk_val_off.p;
+    A.blk_alive = sy_alive.p;
+    A.nblk = &d_scal->nblk;
+    A.newblk_total = &d_tot->sum[5];
+    A.lists = lists.p;
+    A.idx = F->idx.p;
+    A.red_key = sy_red_key.p;
+    A.red_val = sy_red_val.p;
+    A.red_key2 = sy_red_key2.p;
+    A.red_ent = red_ent;
+    A.red_targets = red_t;
+    A.red_cnt = red_cnt;
+    A.red_ptr = red_ptr;
+    A.red_nt = &d_scal->red_nt;
+    A.N = N;
+    A.cellstat = sy_cellstat.p;
+    A.cellcls = sy_cellcls.p;
+    A.stat = d_lstat + st;
+    sy_inc.reserve((size_t)std::max<int64_t>(8 * (ng_ub + 1), T.sum[4] + 2), s);
+    red_cnt = reinterpret_cast<int64_t*>(sy_inc.p);
+    A.red_cnt = red_cnt;
+    HCK(sym_elim_fill(P, A, T.sum[4], symw, s));
+    HCK(sym_copy_count(&d_scal->red_nt, &d_lstat[st].ntargets, s));
+    F->klog.end(kls, s);
+    nblk_ub += T.sum[5];
+    mem_entries_ub += T.sum[4];
+    L.t_sym = now_s() - t_begin;
+    // numeric launches
+    Arenas Ar = arenas();
+    const int64_t nsmall = T.sum[6], nbig = T.sum[7];
+    if (nsmall) {
+      const int64_t st_small = (int64_t)status.bump((size_t)nsmall, s);
+      pending.push_back({st_small, nsmall, tag, "cell"});
+      Ar.status = status.p + st_small;
+      const int kl = F->klog.begin("elim_small_kernel", tag, 0, 0, 0, s);
+      launch_elim_small(sy_small.p, (int)nsmall, Ar, (size_t)T.smem, T.max_small_nf <= 64 ? 128 : 256, s);
+      F->klog.end(kl, s);
+      ++g_launches;
+    }
+    if (nbig) {  // the blocked path builds its work lists from (nc, nq) on the host
+      std::vector<ElimTask> big((size_t)nbig);
+      HCK(cudaMemcpyAsync(big.data(), sy_big.p, sizeof(ElimTask) * (size_t)nbig, cudaMemcpyDeviceToHost, s));
+      HCK(cudaStreamSynchronize(s));
+      launch_big_cells(big, sy_big.p, (size_t)T.smem_big, Ar, tag, false, 0, 0);
+    }
+    HCK(cudaEventRecord(L.ev1, s));
+    HCK(cudaGetLastError());
+    L.ncontrib = T.sum[4];
+    F->max_contrib = std::max(F->max_contrib, L.ncontrib);
+    L.d_xrec = xr;
+    L.nxrec = ng;
+    L.d_recs = recs;
+    L.d_all = recs;
+    L.d_targets = red_t;
+    L.d_ptr = red_ptr;
+    L.d_ent = red_ent;
+    dev_levels.push_back((size_t)(&L - F->levels.data()));
+    last_dev_level = (int)(&L - F->levels.data());
+    L.lap("dev-launch");
+    return true;
+  }
+
+  // ---- skeletonization level -----------------------------------------------
+  bool dev_skeleton_level(int ell, int kind, double tag, LevelRec& L) {
+    const double t_begin = now_s();
+    L.kind = 1;
+    L.lap(nullptr);
+    HCK(cudaEventCreate(&L.ev0));
+    HCK(cudaEventCreate(&L.ev1));
+    HCK(cudaEventRecord(L.ev0, s));
+    const int kls = F->klog.begin("symbolic_device", tag, 0, 0, 0, s);
+    SymFront P;
+    int64_t ng_ub = 0;
+    dev_front_count(ell, 1 + kind, P, ng_ub);
+    SkelInc* inc = reinterpret_cast<SkelInc*>(sy_inc.p);
+    SkelInc* exc = reinterpret_cast<SkelInc*>(sy_exc.p);
+    const bool gram_eps = opt.eps >= kGramMinEps;
+    HCK(sym_skel_sizes(P, kPromoteWork, gram_eps ? 1 : 0, (int)ng_ub, inc, exc, d_tot, symw, s));
+    dev_sync_totals();
+    L.lap("dev-count");
+    const LevelTotals T = *h_tot;
+    if (h_scal->fatal || T.any_mode2 || (g.dim == 3 && T.any_promote)) {
+      HCK(sym_reset_groups(sy_gmem.p, sy_goff.p, &d_scal->ng, sy_group_of.p, s));
+      F->klog.end(kls, s);
+      HCK(cudaEventRecord(L.ev1, s));
+      return false;
+    }
+    nact_ub = h_scal->nact;
+    const int64_t ng = T.ng;
+    L.ngroups = ng;
+    L.max_front = T.max_front;
+    const int st = dev_stat_slot(L);
+    scratch.n = 0;
+    const int64_t idx_base = (int64_t)F->idx.bump((size_t)(T.sum[0] + T.sum[6]), s);
+    lists.reserve((size_t)std::max<int64_t>(T.sum[1], 1), s);
+    lists.n = (size_t)T.sum[1];
+    const int64_t scr_base = T.sum[2] ? (int64_t)scratch.bump((size_t)T.sum[2], s) : 0;
+    const int64_t fac_base = (int64_t)F->fac.bump((size_t)T.sum[3], s);
+    const int64_t bv_base = (int64_t)bvals.bump((size_t)T.sum[4], s);
+    sy_preds.reserve((size_t)T.sum[5] + 1, s);
+    sy_pred_ptr.reserve((size_t)ng + 2, s);
+    sy_cl_rel.reserve((size_t)ng + 1, s);
+    sy_tasks.reserve((size_t)ng + 1, s);
+    P.exc = sy_exc.p;
+    P.exc_stride = kSkelIncN;
+    P.o_nf = 0;
+    P.o_nb = 1;
+    P.o_pred = 5;
+    P.idx_base = idx_base;
+    P.idx_out = F->idx.p;
+    P.lists = lists.p;
+    P.preds = sy_preds.p;
+    HCK(sym_fronts_fill(P, s));
+    SkelFillArgs A;
+    A.idx_base = idx_base;
+    A.scr_base = scr_base;
+    A.fac_base = fac_base;
+    A.bv_base = bv_base;
+    A.tot_nf = T.sum[0];
+    A.exc = exc;
+    A.tasks = sy_tasks.p;
+    A.pred_ptr = sy_pred_ptr.p;
+    A.cl_rel = sy_cl_rel.p;
+    A.idx = F->idx.p;
+    HCK(sym_skel_fill(P, A, s));
+    HCK(sym_reset_groups(sy_gmem.p, sy_goff.p, &d_scal->ng, sy_group_of.p, s));
+    // exact or snapshot order (the host path's rule)
+    bool exact = opt.order_mode == HIFDE_ORDER_EXACT;
+    int nbatch = 1;
+    if (opt.order_mode != HIFDE_ORDER_SNAPSHOT && ng > 1) {
+      const int iters = opt.exact_max_batches + 1;
+      sy_b0.reserve((size_t)ng + 1, s);
+      sy_b1.reserve((size_t)ng + 1, s);
+      sy_changed.reserve((size_t)iters + 1, s);
+      HCK(sym_skel_chain(sy_pred_ptr.p, sy_preds.p, &d_scal->ng, (int)ng, iters, sy_b0.p, sy_b1.p, sy_changed.p,
+                         d_tot, s));
+      HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
+      HCK(cudaStreamSynchronize(s));
+      nbatch = (int)h_tot->max_chain + 1;
+      if (opt.order_mode == HIFDE_ORDER_AUTO) exact = nbatch <= opt.exact_max_batches;
+    }
+    L.nbatches = exact ? nbatch : 1;
+    F->klog.end(kls, s);
+    L.t_sym = now_s() - t_begin;
+    L.lap("dev-fill");
+    const int64_t st_off = (int64_t)status.bump((size_t)ng, s);
+    HCK(cudaMemsetAsync(status.p + st_off, 0, (size_t)ng * sizeof(int), s));
+    pending.push_back({st_off, ng, tag, "group"});
+    kout.n = 0;
+    kout.bump((size_t)ng, s);
+    Arenas Ar = arenas();
+    Ar.status = status.p + st_off;
+    const bool one_launch = exact && ng > 1;
+    const int nthr = (T.max_nc > 32 || T.max_nq > 128) ? 512 : 128;
+    if (one_launch) {
+      sy_done.reserve((size_t)ng, s);
+      HCK(cudaMemsetAsync(sy_done.p, 0, sizeof(int) * (size_t)ng, s));
+      int cs = 0, ncls = 0;
+      size_t smem_cl = 0;
+      if (T.max_nc >= kClusterMinNc) {
+        for (int csz : {4, 2}) {
+          const size_t need = (size_t)(csz == 4 ? T.cl_need4 : T.cl_need2);
+          if (need > kSmemCap) continue;
+          const int capc = skel_cluster_capacity(need, csz);
+          if (capc >= 1 && ng <= capc) {
+            cs = csz;
+            ncls = (int)std::min<int64_t>(ng, capc);
+            smem_cl = need;
+            break;
+          }
+        }
+      }
+      if (cs > 0) {
+        const int64_t base = (int64_t)scratch.bump((size_t)T.sum[7], s);
+        HCK(sym_skel_cluster_tasks(sy_tasks.p, sy_cl_rel.p, base, &d_scal->ng, (int)ng, s));
+        Ar.scratch = scratch.p;
+        const int kl = F->klog.begin("skel_cluster_kernel", tag, 0, 0, 0, s);
+        HCK(launch_skel_cluster(sy_tasks.p, (int)ng, sy_pred_ptr.p, sy_preds.p, sy_done.p, Ar, opt.eps, smem_cl, ncls,
+                                cs, s));
+        F->klog.end(kl, s);
+      } else {
+        const int cap = skel_ordered_capacity((size_t)T.smem, nthr);
+        if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
+        const int kl = F->klog.begin("skel_ordered_kernel", tag, 0, 0, 0, s);
+        HCK(launch_skel_ordered(sy_tasks.p, (int)ng, sy_pred_ptr.p, sy_preds.p, sy_done.p, Ar, opt.eps,
+                                (size_t)T.smem, nthr, (int)std::min<int64_t>(ng, cap), s));
+        F->klog.end(kl, s);
+      }
+      ++g_launches;
+    } else {
+      const int kl = F->klog.begin("skel_kernel", tag, 0, 0, 0, s);
+      launch_skel(sy_tasks.p, (int)ng, Ar, opt.eps, (size_t)T.smem, nthr, s);
+      F->klog.end(kl, s);
+      launch_apply_rd(sy_tasks.p, (int)ng, Ar, s);
+      g_launches += 2;
+    }
+    // ranks known on the device: delta blocks, solve records, statistics
+    SolveRec* recs = (SolveRec*)dev_alloc(sizeof(SolveRec) * (size_t)ng);
+    hifde_record_t* xr = (hifde_record_t*)dev_alloc(sizeof(hifde_record_t) * (size_t)ng);
+    dev_blocks_reserve(nblk_ub + ng + 1);
+    sy_fin.reserve((size_t)2 * ng + 2, s);
+    SkelFinishArgs Fa;
+    Fa.inc = sy_fin.p;
+    Fa.exc = sy_fin.p + ng + 1;
+    Fa.recs = recs;
+    Fa.xrec = xr;
+    Fa.blk_dof_off = d_blk_dof_off.p;
+    Fa.blk_n = d_blk_n.p;
+    Fa.blk_val_off = d_blk_val_off.p;
+    Fa.blk_alive = sy_alive.p;
+    Fa.nblk = &d_scal->nblk;
+    Fa.stat = d_lstat + st;
+    HCK(sym_skel_finish(sy_tasks.p, kout.p, &d_scal->ng, (int)ng, Fa, symw, s));
+    HCK(cudaEventRecord(L.ev1, s));
+    HCK(cudaGetLastError());
+    nblk_ub += ng;
+    mem_entries_ub += T.sum[6];  // delta blocks: at most the groups' sizes
+    L.d_xrec = xr;
+    L.nxrec = ng;
+    L.d_recs = recs;
+    L.d_all = recs;
+    dev_levels.push_back((size_t)(&L - F->levels.data()));
+    last_dev_level = (int)(&L - F->levels.data());
+    L.lap("dev-launch");
+    return true;
+  }
+
+  // Hand the device state to the host analysis: block table, index-arena
+  // mirror of the live blocks, active mask / list, membership.
+  void dev_to_host() {
+    if (!dev_mode) return;
+    dev_mode = false;
+    HCK(cudaMemcpyAsync(h_scal, d_scal, sizeof(SymScalars), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    const int64_t nb = h_scal->nblk;
+    blk_dof_off.resize((size_t)nb);
+    blk_n.resize((size_t)nb);
+    blk_val_off.resize((size_t)nb);
+    blk_alive.resize((size_t)nb);
+    bf_key.assign((size_t)nb, -2);
+    bf_val.assign((size_t)nb, 0);
+    if (nb) {
+      HCK(cudaMemcpyAsync(blk_dof_off.data(), d_blk_dof_off.p, sizeof(int64_t) * (size_t)nb, cudaMemcpyDeviceToHost, s));
+      HCK(cudaMemcpyAsync(blk_n.data(), d_blk_n.p, sizeof(int32_t) * (size_t)nb, cudaMemcpyDeviceToHost, s));
+      HCK(cudaMemcpyAsync(blk_val_off.data(), d_blk_val_off.p, sizeof(int64_t) * (size_t)nb, cudaMemcpyDeviceToHost, s));
+      HCK(cudaMemcpyAsync(blk_alive.data(), sy_alive.p, (size_t)nb, cudaMemcpyDeviceToHost, s));
+    }
+    HCK(cudaMemcpyAsync(active.data(), d_active, (size_t)N, cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    d_blk_dof_off.n = d_blk_n.n = d_blk_val_off.n = (size_t)nb;
+    blk_uploaded = (size_t)nb;
+    // index-arena mirror: the DOF lists of the live blocks
+    const size_t nidx = F->idx.n;
+    h_idx.resize(nidx);
+    int64_t lo = (int64_t)nidx;
+    for (int64_t b = 0; b < nb; ++b)
+      if (blk_alive[(size_t)b]) lo = std::min(lo, blk_dof_off[(size_t)b]);
+    if (lo < (int64_t)nidx)
+      pinned_xfer().d2h(h_idx.data() + lo, F->idx.p + lo, (nidx - (size_t)lo) * sizeof(int32_t), s);
+    idx_uploaded = nidx;
+    // active list and membership (active DOFs only: the host looks up
+    // membership of active DOFs alone)
+    act.clear();
+    for (int64_t i = 0; i < N; ++i)
+      if (active[(size_t)i]) act.push_back((int32_t)i);
+    if (last_dev_level >= 0) F->levels[(size_t)last_dev_level].active_after = (int64_t)act.size();
+    member.reset();
+    size_t nadd = 0;
+    for (int64_t b = 0; b < nb; ++b)
+      if (blk_alive[(size_t)b]) nadd += (size_t)blk_n[(size_t)b];
+    member.ensure_room(nadd);
+    const int nthu = nthreads;
+#pragma omp parallel num_threads(nthu)
+    {
+      const int tid = omp_get_thread_num(), nth = omp_get_num_threads();
+      const int64_t dlo = N * tid / nth, dhi = N * (tid + 1) / nth;
+      for (int64_t b = 0; b < nb; ++b) {
+        if (!blk_alive[(size_t)b]) continue;
+        const int32_t* d = h_idx.data() + blk_dof_off[(size_t)b];
+        for (int32_t i = 0; i < blk_n[(size_t)b]; ++i)
+          if (d[i] >= dlo && d[i] < dhi && active[(size_t)d[i]]) member.add(d[i], (int32_t)b);
+      }
+    }
+    // the upload cursor of the block table continues from here
+  }
+
+  // Device levels: statistics to the LevelRecs, solve metadata (device tables
+  // when every record is small, else the host plan), kernel-log totals.
+  void dev_finalize() {
+    if (dev_levels.empty()) return;
+    std::vector<LevelStat> st((size_t)nlstat);
+    HCK(cudaMemcpyAsync(st.data(), d_lstat, sizeof(LevelStat) * (size_t)nlstat, cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    for (size_t li : dev_levels) {
+      LevelRec& L = F->levels[li];
+      const LevelStat& S = st[(size_t)L.dev_stat];
+      L.ngroups = S.ngroups;
+      L.nskel = S.nskel;
+      L.nred = S.nred;
+      L.max_front = S.max_front;
+      L.gflop = S.gflop;
+      L.gbytes = S.gbytes;
+      for (int c = 0; c < 2; ++c) {
+        L.gf_cls[c] = S.gf_cls[c];
+        L.gb_cls[c] = S.gb_cls[c];
+      }
+      L.solve_fac = S.solve_fac;
+      L.solve_rows = S.solve_rows;
+      if (L.active_after == 0 && (int)li != last_dev_level) L.active_after = S.active_after;
+      F->m_f_bytes += S.mf_bytes;
+      L.nall = (int)S.nrecs;
+      L.all_max_nc = (int)S.max_nc;
+      L.all_max_nq = (int)S.max_nq;
+      if (L.kind == 0) L.ntargets = (int)S.ntargets;
+      const bool all_small = S.max_nc <= 96 && S.max_nq <= 192;
+      if (all_small) {
+        L.nsmall = (int)S.nrecs;
+        L.max_nc = (int)S.max_nc;
+        L.max_nq = (int)S.max_nq;
+      } else {  // large records: the host plan (tiled phases)
+        L.recs.resize((size_t)S.nrecs);
+        HCK(cudaMemcpy(L.recs.data(), L.d_recs, sizeof(SolveRec) * (size_t)S.nrecs, cudaMemcpyDeviceToHost));
+        L.d_recs = nullptr;
+        L.d_all = nullptr;
+        L.nall = 0;
+        L.all_max_nc = L.all_max_nq = 0;
+        L.solve_fac = L.solve_rows = 0;
+        build_solve_plan(L);
+      }
+      for (auto& E : F->klog.v) {  // kernel log: the level's totals to its main launch
+        if (E.phase != 0 || E.tag != L.tag) continue;
+        if (E.name == "elim_small_kernel") { E.gbytes = L.gb_cls[0]; E.gflop = L.gf_cls[0]; }
+        if (E.name == "elim_blocked_pipeline") { E.gbytes = L.gb_cls[1]; E.gflop = L.gf_cls[1]; }
+        if (E.name == "skel_kernel" || E.name == "skel_ordered_kernel" || E.name == "skel_cluster_kernel") {
+          E.gbytes = L.gbytes;
+          E.gflop = L.gflop;
+        }
+      }
+    }
+  }
+
   // -------------------------------------------------------------------------
   // Thread-safe variant for the wavefront partition: the block verdicts are
   // cached per thread for the cell being processed (owners do not change
@@ -3067,8 +3675,33 @@ struct Factorizer {
       L.active_after = (int64_t)w;
       L.seconds = now_s() - tl;
     };
+    // device symbolic mode from level 0 (not for the sharded sweep, whose
+    // ranks keep the host analysis, nor for verify runs)
+    dev_mode = opt.symbolic == HIFDE_SYMBOLIC_AUTO && !sharded() && !opt.verify && N > 0;
+    if (dev_mode) dev_init();
+    // a device level that cannot run on the device hands over and is redone on the host
+    auto dev_fallback = [&](LevelRec& L, double tag) {
+      if (L.ev0) cudaEventDestroy(L.ev0);
+      if (L.ev1) cudaEventDestroy(L.ev1);
+      L = LevelRec();
+      L.tag = tag;
+      dev_to_host();
+    };
     for (int ell = 0; ell < Lv; ++ell) {
-      {
+      if (dev_mode && opt.variant == HIFDE_VARIANT_HIFDE3X && ell > 0) dev_to_host();  // adaptive cells: host
+      if (dev_mode) {
+        const double tl = now_s();
+        F->levels.emplace_back();
+        LevelRec& L = F->levels.back();
+        L.tag = (double)ell;
+        if (dev_elimination_level(ell, L.tag, L)) {
+          L.seconds = now_s() - tl;
+        } else {
+          dev_fallback(L, (double)ell);
+          F->levels.pop_back();
+        }
+      }
+      if (!dev_mode || F->levels.empty() || F->levels.back().tag != (double)ell) {
         const double tl = now_s();
         Groups gr;
         if (opt.variant == HIFDE_VARIANT_HIFDE3X && ell > 0) {
@@ -3115,6 +3748,18 @@ struct Factorizer {
         helper.post([this, &L]() { build_solve_plan(L); });
       }
       auto skel = [&](double tag, int kind) {
+        if (dev_mode) {
+          const double tl = now_s();
+          F->levels.emplace_back();
+          LevelRec& L = F->levels.back();
+          L.tag = tag;
+          if (dev_skeleton_level(ell, kind, tag, L)) {
+            L.seconds = now_s() - tl;
+            return;
+          }
+          dev_fallback(L, tag);
+          F->levels.pop_back();
+        }
         const double tl = now_s();
         Groups gr = interface_groups(g, X, ell, act, kind);
         F->levels.emplace_back();
@@ -3132,6 +3777,7 @@ struct Factorizer {
         if (ell >= opt.skip_levels) skel(ell + 2.0 / 3.0, 0);
       }
     }
+    dev_to_host();  // the terminal block runs on the host path
     // terminal block: every DOF still active (src/driver.py:152-157)
     {
       const double tl = now_s();
@@ -3162,6 +3808,7 @@ struct Factorizer {
     F->xfer_bytes = xfer_bytes;
     helper.drain();
     build_solve_plan(F->levels.back());  // the terminal block
+    dev_finalize();
     finish_reductions();
     PR.lap("reductions");
     // solve metadata to the device: small records one CTA each, large ones as
@@ -3815,7 +4462,17 @@ int hifde_level_records(const hifde_factor_t* f, int level, hifde_record_t* out,
                         int64_t* count) {
   g_err.clear();
   if (!f || !count || level < 0 || level >= (int)f->levels.size()) { g_err = "bad level"; return HIFDE_BADARG; }
-  const auto& X = f->levels[(size_t)level].xrec;
+  auto& L = const_cast<hifde::LevelRec&>(f->levels[(size_t)level]);
+  if (L.d_xrec && L.xrec.empty() && L.nxrec > 0) {  // device-symbolic level: copy its export view once
+    L.xrec.resize((size_t)L.nxrec);
+    if (cudaSetDevice(f->device) != cudaSuccess ||
+        cudaMemcpy(L.xrec.data(), L.d_xrec, L.nxrec * sizeof(hifde_record_t), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      L.xrec.clear();
+      g_err = "record copy failed";
+      return HIFDE_CUDA;
+    }
+  }
+  const auto& X = L.xrec;
   *count = (int64_t)X.size();
   if (out) {
     if (cap < (int64_t)X.size()) { g_err = "record buffer too small"; return HIFDE_BADARG; }

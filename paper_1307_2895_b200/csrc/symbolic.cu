@@ -1,0 +1,987 @@
+// Device symbolic pass of the level sweep.
+//
+// On the fine levels the host used to spend most of the factorization on
+// integer bookkeeping: the level partition, every cell's neighbour set
+// (src/sparse.py:164-173 on the clique-block store), block membership, task
+// tables and arena offsets.  Here the same steps run on the GPU, on the
+// device-resident structure (active mask, block table, index arena), with
+// results identical to the host path:
+//   * partition: the reference's keys (keys.h), a stable radix sort of the
+//     active DOFs by key (members ascending within a group, groups in key
+//     order, src/partition.py:40-92,108-181);
+//   * membership: per level a DOF -> live-block CSR over the active DOFs;
+//   * fronts: per group the live blocks touching it and its neighbour set q
+//     = active DOFs coupled through a block or A0, not in the group; hashed in
+//     shared memory, then sorted (count pass, then fill pass);
+//   * sizes and offsets: the host's sizing rules (hifde_internal.h) and
+//     prefix sums in the host's task order, so arena offsets, block ids and
+//     therefore every summation order match the host path bit for bit;
+//   * exact-order dependency chains: predecessor CSR and the longest chain by
+//     relaxation (the exact / snapshot choice of the host path).
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+
+#include <cub/cub.cuh>
+
+#include "hifde_internal.h"
+#include "keys.h"
+
+namespace hifde {
+
+namespace {
+
+constexpr int kSymNT = 128;
+constexpr int32_t kEmpty = INT32_MAX;
+
+__device__ __forceinline__ void dof_coords(int64_t d, int dim, int side, int* x) {
+  for (int ax = 0; ax < dim; ++ax) {
+    x[ax] = (int)(d % side) + 1;
+    d /= side;
+  }
+}
+
+__device__ __forceinline__ uint32_t hash_slot(int32_t key, int logh) {
+  return ((uint32_t)key * 2654435761u) >> (32 - logh);
+}
+
+// Insert key into an open-addressing set of 2^logh slots; returns false when
+// the set overflows (more than half full or no free slot within the probes).
+__device__ __forceinline__ bool set_insert(int32_t* t, int logh, int32_t key, int* count, int* ovf) {
+  const uint32_t mask = (1u << logh) - 1;
+  uint32_t h = hash_slot(key, logh);
+  for (int p = 0; p <= (int)mask; ++p) {
+    const int32_t old = atomicCAS(&t[h], kEmpty, key);
+    if (old == kEmpty) {
+      if (atomicAdd(count, 1) >= (int)(mask + 1) / 2) *ovf = 1;
+      return true;
+    }
+    if (old == key) return true;
+    h = (h + 1) & mask;
+  }
+  *ovf = 1;
+  return false;
+}
+
+__device__ __forceinline__ int bsearch_sorted(const int32_t* s, int n, int32_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (s[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return (lo < n && s[lo] == key) ? lo : -1;
+}
+
+// Compact the non-empty slots of t[0, H) into out[0, n) (slot order), n
+// returned to every thread.  One barrier-separated block scan.
+template <int NT>
+__device__ int compact_set(const int32_t* t, int H, int32_t* out) {
+  typedef cub::BlockScan<int, NT> Scan;
+  __shared__ typename Scan::TempStorage ts;
+  __shared__ int total;
+  const int per = (H + NT - 1) / NT;
+  const int lo = threadIdx.x * per, hi = min(lo + per, H);
+  int c = 0;
+  for (int i = lo; i < hi; ++i) c += t[i] != kEmpty;
+  int off = 0, tot = 0;
+  Scan(ts).ExclusiveSum(c, off, tot);
+  for (int i = lo; i < hi; ++i)
+    if (t[i] != kEmpty) out[off++] = t[i];
+  if (threadIdx.x == 0) total = tot;
+  __syncthreads();
+  return total;
+}
+
+// Ascending bitonic sort of s[0, n) in place (s has room for the next power of two).
+template <int NT>
+__device__ void sort_small(int32_t* s, int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  for (int i = n + threadIdx.x; i < p; i += NT) s[i] = kEmpty;
+  __syncthreads();
+  for (int k = 2; k <= p; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < p; i += NT) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int32_t a = s[i], b = s[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            s[i] = b;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Partition
+// ---------------------------------------------------------------------------
+__global__ void sym_keys_kernel(const int32_t* __restrict__ act, const int64_t* __restrict__ nact, int64_t nact_ub,
+                                int dim, int side, int w, int k, int kind, int32_t nkeys, int32_t* __restrict__ keys) {
+  const int64_t na = *nact;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nact_ub; i += (int64_t)gridDim.x * blockDim.x) {
+    int key = -1;
+    if (i < na) {
+      int x[3] = {0, 0, 0};
+      dof_coords(act[i], dim, side, x);
+      key = kind == 0 ? interior_key(x, dim, w, k) : interface_key(x, dim, w, k, kind == 2);
+    }
+    keys[i] = key < 0 ? nkeys : key;  // nkeys: no group (sorts last)
+  }
+}
+
+// Group offsets of the sorted members: goff[g] = first member of group g,
+// goff[ng] = members; group_of[d] = g (skeleton levels; -1 elsewhere).
+__global__ void sym_groups_kernel(const int32_t* __restrict__ skeys, const int32_t* __restrict__ gid,
+                                  const int32_t* __restrict__ gmem, const int64_t* __restrict__ nact, int32_t nkeys,
+                                  int64_t* __restrict__ goff, int32_t* __restrict__ ng, int32_t* group_of) {
+  const int64_t na = *nact;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t key = skeys[i];
+    if (key == nkeys) continue;
+    const int g = gid[i] - 1;  // inclusive scan of the head flags
+    if (i == 0 || skeys[i - 1] != key) goff[g] = i;
+    if (i + 1 == na || skeys[i + 1] == nkeys) {
+      goff[g + 1] = i + 1;
+      *ng = g + 1;
+    }
+    if (group_of) group_of[gmem[i]] = g;
+  }
+}
+
+__global__ void sym_heads_kernel(const int32_t* __restrict__ skeys, int64_t n, int32_t nkeys,
+                                 int32_t* __restrict__ head) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t key = skeys[i];
+    head[i] = key != nkeys && (i == 0 || skeys[i - 1] != key);
+  }
+}
+
+__global__ void sym_reset_group_of(const int32_t* __restrict__ gmem, const int64_t* __restrict__ goff,
+                                   const int32_t* __restrict__ ng, int32_t* __restrict__ group_of) {
+  const int64_t n = goff[*ng];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    group_of[gmem[i]] = -1;
+}
+
+// ---------------------------------------------------------------------------
+// Membership: DOF -> live blocks, over the active DOFs
+// ---------------------------------------------------------------------------
+__global__ void sym_member_count(const int32_t* __restrict__ alive_list, const int64_t* __restrict__ nalive,
+                                 const int32_t* __restrict__ blk_n, const int64_t* __restrict__ blk_dof_off,
+                                 const int32_t* __restrict__ idx, const uint8_t* __restrict__ active,
+                                 int32_t* __restrict__ cnt) {
+  const int64_t nb = *nalive;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = w0; j < nb; j += nw) {
+    const int32_t b = alive_list[j];
+    const int32_t* d = idx + blk_dof_off[b];
+    for (int i = lane; i < blk_n[b]; i += 32)
+      if (active[d[i]]) atomicAdd(&cnt[d[i]], 1);
+  }
+}
+
+__global__ void sym_member_fill(const int32_t* __restrict__ alive_list, const int64_t* __restrict__ nalive,
+                                const int32_t* __restrict__ blk_n, const int64_t* __restrict__ blk_dof_off,
+                                const int32_t* __restrict__ idx, const uint8_t* __restrict__ active,
+                                int32_t* __restrict__ pos, int32_t* __restrict__ mblk) {
+  const int64_t nb = *nalive;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = w0; j < nb; j += nw) {
+    const int32_t b = alive_list[j];
+    const int32_t* d = idx + blk_dof_off[b];
+    for (int i = lane; i < blk_n[b]; i += 32)
+      if (active[d[i]]) mblk[atomicAdd(&pos[d[i]], 1)] = b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fronts: live blocks touching the group, neighbour set q, predecessors
+// ---------------------------------------------------------------------------
+template <int LQ, int LB, int LP, int NCMAX, bool FILL>
+__global__ void __launch_bounds__(kSymNT) sym_front_kernel(SymFront P) {
+  constexpr int HQ = 1 << LQ, HB = 1 << LB, HP = 1 << LP;
+  extern __shared__ __align__(16) int32_t sm[];
+  int32_t* c = sm;                 // NCMAX
+  int32_t* hb = c + NCMAX;         // HB
+  int32_t* hq = hb + HB;           // HQ
+  int32_t* hp = hq + HQ;           // HP
+  int32_t* buf = hp + HP;          // HQ (sort buffer)
+  __shared__ int nbk, nqk, npk, ovf, maxnb;
+  const int ngr = *P.ng;
+  const bool big_tier = LQ > 10;
+  const int nwork = big_tier ? *P.nretry : ngr;
+  for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
+    const int g = big_tier ? P.retry[wi] : wi;
+    if (!big_tier && P.flag[g] && FILL) continue;  // the big tier fills it
+    const int64_t c0 = P.goff[g];
+    const int nc = (int)(P.goff[g + 1] - c0);
+    if (threadIdx.x == 0) { nbk = nqk = npk = ovf = maxnb = 0; }
+    for (int i = threadIdx.x; i < HB; i += kSymNT) hb[i] = kEmpty;
+    for (int i = threadIdx.x; i < HQ; i += kSymNT) hq[i] = kEmpty;
+    for (int i = threadIdx.x; i < HP; i += kSymNT) hp[i] = kEmpty;
+    __syncthreads();
+    if (nc > NCMAX) {
+      if (threadIdx.x == 0) ovf = 1;
+    } else {
+      for (int i = threadIdx.x; i < nc; i += kSymNT) c[i] = P.gmem[c0 + i];
+    }
+    __syncthreads();
+    if (!ovf) {
+      // live blocks touching the group
+      for (int i = threadIdx.x; i < nc; i += kSymNT) {
+        const int32_t d = c[i];
+        for (int32_t t = P.mptr[d]; t < P.mptr[d + 1]; ++t) set_insert(hb, LB, P.mblk[t], &nbk, &ovf);
+      }
+    }
+    __syncthreads();
+    int nb = 0;
+    if (!ovf) nb = compact_set<kSymNT>(hb, HB, buf);  // unique blocks (slot order)
+    __syncthreads();
+    if (!ovf) {
+      // q candidates: the blocks' DOFs (warp per block), then A0 rows of c
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+      for (int j = wid; j < nb; j += kSymNT / 32) {
+        const int32_t b = buf[j];
+        const int n = P.blk_n[b];
+        if (lane == 0) atomicMax(&maxnb, n);
+        const int32_t* d = P.idx + P.blk_dof_off[b];
+        for (int i = lane; i < n; i += 32) {
+          const int32_t e = d[i];
+          if (P.active[e] && bsearch_sorted(c, nc, e) < 0) set_insert(hq, LQ, e, &nqk, &ovf);
+        }
+      }
+      for (int i = threadIdx.x; i < nc; i += kSymNT) {
+        const int32_t d = c[i];
+        for (int64_t t = P.indptr[d]; t < P.indptr[d + 1]; ++t) {
+          const int32_t e = P.indices[t];
+          if (P.active[e] && bsearch_sorted(c, nc, e) < 0) set_insert(hq, LQ, e, &nqk, &ovf);
+        }
+      }
+    }
+    __syncthreads();
+    if (!ovf && P.group_of) {  // predecessors: earlier groups owning a DOF of q
+      for (int i = threadIdx.x; i < HQ; i += kSymNT) {
+        const int32_t e = hq[i];
+        if (e == kEmpty) continue;
+        const int32_t go = P.group_of[e];
+        if (go >= 0 && go < g) set_insert(hp, LP, go, &npk, &ovf);
+      }
+    }
+    __syncthreads();
+    if (ovf) {
+      if (!FILL && threadIdx.x == 0) {
+        if (!big_tier) {
+          P.flag[g] = 1;
+          P.retry[atomicAdd(P.nretry, 1)] = g;
+        } else {
+          atomicExch(P.fatal, 1);
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    if (!FILL) {
+      if (threadIdx.x == 0) {
+        P.nq[g] = nqk;
+        P.nb[g] = nb;
+        P.maxnb[g] = maxnb;
+        P.npred[g] = npk;
+        if (!big_tier) P.flag[g] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    // fill: c, sorted q, sorted blocks, sorted predecessors
+    const int64_t* ex = P.exc + (size_t)g * P.exc_stride;
+    const int64_t doff = P.idx_base + ex[P.o_nf];
+    int32_t* out = P.idx_out + doff;
+    for (int i = threadIdx.x; i < nc; i += kSymNT) out[i] = c[i];
+    sort_small<kSymNT>(buf, nb);
+    int32_t* lo = P.lists + ex[P.o_nb];
+    for (int i = threadIdx.x; i < nb; i += kSymNT) lo[i] = buf[i];
+    __syncthreads();
+    const int nq = compact_set<kSymNT>(hq, HQ, buf);
+    sort_small<kSymNT>(buf, nq);
+    for (int i = threadIdx.x; i < nq; i += kSymNT) out[nc + i] = buf[i];
+    __syncthreads();
+    if (P.group_of) {
+      const int np = compact_set<kSymNT>(hp, HP, buf);
+      sort_small<kSymNT>(buf, np);
+      int32_t* po = P.preds + ex[P.o_pred];
+      for (int i = threadIdx.x; i < np; i += kSymNT) po[i] = buf[i];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Elimination level: sizes, prefix sums, task tables, block table updates
+// ---------------------------------------------------------------------------
+struct ElimIncOp {
+  __device__ __forceinline__ ElimInc operator()(const ElimInc& a, const ElimInc& b) const {
+    ElimInc r;
+#pragma unroll
+    for (int i = 0; i < kElimIncN; ++i) r.v[i] = a.v[i] + b.v[i];
+    return r;
+  }
+};
+struct SkelIncOp {
+  __device__ __forceinline__ SkelInc operator()(const SkelInc& a, const SkelInc& b) const {
+    SkelInc r;
+#pragma unroll
+    for (int i = 0; i < kSkelIncN; ++i) r.v[i] = a.v[i] + b.v[i];
+    return r;
+  }
+};
+
+__device__ __forceinline__ void amax64(int64_t* p, int64_t v) {
+  atomicMax((unsigned long long*)p, (unsigned long long)v);
+}
+
+__global__ void elim_size_kernel(const SymFront P, int is_top, ElimInc* __restrict__ inc, LevelTotals* tot) {
+  const int ng = *P.ng;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g], nb = P.nb[g], mb = P.maxnb[g];
+    const ElimSizes z = elim_sizes(nc, nq, mb, is_top != 0);
+    ElimInc I;
+    I.v[0] = nc + nq;                                                  // idx
+    I.v[1] = nb;                                                       // lists
+    I.v[2] = (int64_t)nc * nc + (z.big ? (int64_t)nc * (nc + 1) / 2 : 0) + (int64_t)nc * nq;  // fac
+    I.v[3] = (int64_t)nq * nq;                                         // block arena
+    I.v[4] = nq;                                                       // contribution rows
+    I.v[5] = nq > 0;                                                   // new blocks
+    I.v[6] = !z.big;                                                   // small cells
+    I.v[7] = z.big;                                                    // big cells
+    inc[g] = I;
+    if (z.big) {
+      amax64(&tot->smem_big, (int64_t)elim_big_smem(nc + nq, mb));
+      amax64(&tot->max_big_nc, nc);
+    } else {
+      amax64(&tot->smem, (int64_t)z.smem);
+      amax64(&tot->max_small_nf, nc + nq);
+    }
+    amax64(&tot->max_front, nc + nq);
+    amax64(&tot->max_nc, nc);
+    amax64(&tot->max_nq, nq);
+  }
+}
+
+__global__ void elim_total_kernel(const int32_t* __restrict__ ng, const ElimInc* __restrict__ inc,
+                                  const ElimInc* __restrict__ exc, LevelTotals* tot) {
+  const int n = *ng;
+  tot->ng = n;
+  for (int i = 0; i < kElimIncN; ++i) tot->sum[i] = n ? exc[n - 1].v[i] + inc[n - 1].v[i] : 0;
+}
+
+__global__ void elim_fill_kernel(const SymFront P, ElimFillArgs A) {
+  const int ng = *P.ng;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g], nb = P.nb[g], mb = P.maxnb[g];
+    const ElimSizes z = elim_sizes(nc, nq, mb, A.is_top != 0);
+    const ElimInc& o = A.exc[g];
+    ElimTask T;
+    T.nc = nc;
+    T.nq = nq;
+    T.nblk = nb;
+    T.maxnb = mb;
+    T.dofs_off = A.idx_base + o.v[0];
+    T.blk_off = o.v[1];
+    T.scratch_off = z.scratch_off;
+    T.C_off = A.fac_base + o.v[2];
+    T.P_off = z.big ? T.C_off + (int64_t)nc * nc : T.C_off;
+    T.W_off = T.C_off + (int64_t)nc * nc + (z.big ? (int64_t)nc * (nc + 1) / 2 : 0);
+    T.U_off = nq > 0 ? A.bv_base + o.v[3] : 0;
+    if (z.big) A.big[o.v[7]] = T;
+    else A.small[o.v[6]] = T;
+    SolveRec R;
+    R.nc = nc;
+    R.nq = nq;
+    R.idx_off = T.dofs_off;
+    R.C_off = T.P_off;  // the solve applies the packed inverse
+    R.W_off = T.W_off;
+    R.T_off = 0;
+    R.contrib_off = o.v[4];
+    R.inv = 1;
+    R.pad = 0;
+    A.recs[g] = R;
+    hifde_record_t X;
+    X.kind = A.is_top ? 2 : 0;
+    X.nc = nc;
+    X.nq = nq;
+    X.nr = 0;
+    X.cell_off = T.dofs_off;
+    X.idx_off = T.dofs_off;
+    X.P_off = T.P_off;
+    X.W_off = T.W_off;
+    X.T_off = 0;
+    A.xrec[g] = X;
+    const int64_t nblk0 = *A.nblk;
+    if (nq > 0) {
+      const int64_t id = nblk0 + o.v[5];
+      A.blk_dof_off[id] = T.dofs_off + nc;
+      A.blk_n[id] = nq;
+      A.blk_val_off[id] = T.U_off;
+      A.blk_alive[id] = 1;
+    }
+    const int32_t* bl = A.lists + T.blk_off;
+    for (int j = 0; j < nb; ++j) A.blk_alive[bl[j]] = 0;  // consumed (a block touches one cell of a level)
+    // solve-side reduction pairs: (neighbour DOF, contribution row)
+    const int32_t* q = A.idx + T.dofs_off + nc;
+    for (int i = 0; i < nq; ++i) {
+      A.red_key[o.v[4] + i] = q[i];
+      A.red_val[o.v[4] + i] = o.v[4] + i;
+    }
+    // level statistics (SURVEY 8(d) work per cell, the reference's m_f accounting)
+    const double dc = nc, dq = nq;
+    const double gf = (dc * dc * dc / 3 + dc * dc * dq + dc * dq + dc * dq * dq) * 1e-9;
+    const double gb = 8.0 * ((dc + dq) * (dc + dq) + dc * dc + dc + dc * dq + 2 * dq * dq) * 1e-9;
+    A.cellstat[g] = make_double4(gf, gb, 8.0 * (dc * dc + dc + dc * dq), dc * (dc + 1) / 2 + dc * dq);
+    A.cellcls[g] = (uint8_t)z.big;
+  }
+}
+
+// per-level statistics of an elimination level (one CTA, fixed order: deterministic)
+__global__ void elim_stats_kernel(const int32_t* __restrict__ ng, const double4* __restrict__ cs,
+                                  const uint8_t* __restrict__ cls, const SymFront P, LevelStat* st,
+                                  const int64_t* __restrict__ nblk_inc, int64_t* nblk) {
+  __shared__ double red[8][256];
+  const int n = *ng;
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t mx_nc = 0, mx_nq = 0, mf = 0, rows = 0, mfront = 0;
+  for (int g = threadIdx.x; g < n; g += 256) {
+    const double4 v = cs[g];
+    const int c = cls[g];
+    a[0] += v.x;
+    a[1] += v.y;
+    a[2 + 2 * c] += v.x;
+    a[3 + 2 * c] += v.y;
+    a[6] += v.w;
+    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g];
+    mf += (int64_t)v.z;
+    rows += nc + nq;
+    mx_nc = max(mx_nc, (int64_t)nc);
+    mx_nq = max(mx_nq, (int64_t)nq);
+    mfront = max(mfront, (int64_t)(nc + nq));
+  }
+  for (int i = 0; i < 7; ++i) red[i][threadIdx.x] = a[i];
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int i = 0; i < 7; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + s];
+    __syncthreads();
+  }
+  typedef cub::BlockReduce<int64_t, 256> R;
+  __shared__ typename R::TempStorage rt;
+  const int64_t s_mf = R(rt).Sum(mf);
+  __syncthreads();
+  const int64_t s_rows = R(rt).Sum(rows);
+  __syncthreads();
+  const int64_t m_nc = R(rt).Reduce(mx_nc, cub::Max());
+  __syncthreads();
+  const int64_t m_nq = R(rt).Reduce(mx_nq, cub::Max());
+  __syncthreads();
+  const int64_t m_front = R(rt).Reduce(mfront, cub::Max());
+  if (threadIdx.x == 0) {
+    st->ngroups = n;
+    st->gflop = red[0][0];
+    st->gbytes = red[1][0];
+    st->gf_cls[0] = red[2][0];
+    st->gb_cls[0] = red[3][0];
+    st->gf_cls[1] = red[4][0];
+    st->gb_cls[1] = red[5][0];
+    st->solve_fac = red[6][0];
+    st->solve_rows = (double)s_rows;
+    st->mf_bytes = s_mf;
+    st->nrecs = n;
+    st->max_nc = m_nc;
+    st->max_nq = m_nq;
+    st->max_front = m_front;
+    *nblk += *nblk_inc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Skeletonization level
+// ---------------------------------------------------------------------------
+__global__ void skel_size_kernel(const SymFront P, double promote_work, int gram_eps_ok, SkelInc* __restrict__ inc,
+                                 LevelTotals* tot) {
+  const int ng = *P.ng;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g], nb = P.nb[g], mb = P.maxnb[g];
+    const SkelSizes z = skel_sizes(nc, nq, mb);
+    const bool promote = (z.mode == 1 || z.mode == 3) && (double)nq * nc * nc >= promote_work && gram_eps_ok &&
+                         nq >= 2 * nc && nc <= 1024;
+    SkelInc I;
+    I.v[0] = nc + nq;                                                  // idx (fronts)
+    I.v[1] = nb;                                                       // lists
+    I.v[2] = (int64_t)z.scr;                                           // scratch
+    I.v[3] = (int64_t)(z.fac + ((z.mode == 2 || promote) ? z.fac_big : 0));  // fac
+    I.v[4] = (int64_t)nc * nc;                                         // delta blocks
+    I.v[5] = P.npred[g];                                               // predecessors
+    I.v[6] = nc;                                                       // sk/rd output lists
+    I.v[7] = (int64_t)skel_cluster_scratch(nc);                        // cluster workspace
+    inc[g] = I;
+    amax64(&tot->smem, (int64_t)z.smem);
+    amax64(&tot->max_nc, nc);
+    amax64(&tot->max_nq, nq);
+    amax64(&tot->max_front, nc + nq);
+    amax64(&tot->cl_need4, (int64_t)skel_cluster_need(nc, nq, mb, 4));
+    amax64(&tot->cl_need2, (int64_t)skel_cluster_need(nc, nq, mb, 2));
+    if (z.mode == 2) amax64(&tot->any_mode2, 1);
+    if (promote && (double)nq * nc * nc >= 4e6) amax64(&tot->any_promote, 1);
+  }
+}
+
+__global__ void skel_total_kernel(const int32_t* __restrict__ ng, const SkelInc* __restrict__ inc,
+                                  const SkelInc* __restrict__ exc, LevelTotals* tot) {
+  const int n = *ng;
+  tot->ng = n;
+  for (int i = 0; i < kSkelIncN; ++i) tot->sum[i] = n ? exc[n - 1].v[i] + inc[n - 1].v[i] : 0;
+}
+
+__global__ void skel_fill_kernel(const SymFront P, SkelFillArgs A) {
+  const int ng = *P.ng;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g], nb = P.nb[g], mb = P.maxnb[g];
+    const SkelSizes z = skel_sizes(nc, nq, mb);
+    const SkelInc& o = A.exc[g];
+    SkelTask T;
+    T.nc = nc;
+    T.nq = nq;
+    T.nblk = nb;
+    T.maxnb = mb;
+    T.dofs_off = A.idx_base + o.v[0];
+    T.blk_off = o.v[1];
+    T.scratch_off = z.scr ? A.scr_base + o.v[2] : -1;
+    T.rec_off = A.fac_base + o.v[3];
+    T.delta_off = A.bv_base + o.v[4];
+    T.out_off = A.idx_base + A.tot_nf + o.v[6];
+    T.group = g;
+    T.mode = z.mode;
+    T.chunk = z.chunk;
+    T.pad2 = 0;
+    A.tasks[g] = T;
+    A.pred_ptr[g] = o.v[5];
+    if (g == ng - 1) A.pred_ptr[ng] = o.v[5] + P.npred[g];
+    A.cl_rel[g] = o.v[7];
+    int32_t* out = A.idx + T.out_off;
+    for (int i = 0; i < nc; ++i) out[i] = 0;
+  }
+}
+
+// cluster path: per-group global workspace in scratch_off
+__global__ void skel_cluster_tasks(SkelTask* __restrict__ tasks, const int64_t* __restrict__ cl_rel, int64_t base,
+                                   const int32_t* __restrict__ ng) {
+  const int n = *ng;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x)
+    tasks[g].scratch_off = base + cl_rel[g];
+}
+
+// Longest dependency chain: b[t] = 1 + max b[p] over predecessors p (Jacobi
+// sweeps from 0; after i sweeps b = min(chain, i)); iteration it stops early
+// once the previous sweep changed nothing.
+__global__ void skel_relax_kernel(const int64_t* __restrict__ pred_ptr, const int32_t* __restrict__ preds,
+                                  const int32_t* __restrict__ ng, const int32_t* __restrict__ bin,
+                                  int32_t* __restrict__ bout, int32_t* changed, int it) {
+  if (it > 0 && changed[it - 1] == 0) return;
+  const int n = *ng;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    int b = 0;
+    for (int64_t p = pred_ptr[t]; p < pred_ptr[t + 1]; ++p) b = max(b, bin[preds[p]] + 1);
+    bout[t] = b;
+    if (b != bin[t]) changed[it] = 1;
+  }
+}
+
+__global__ void skel_chain_kernel(const int32_t* __restrict__ b0, const int32_t* __restrict__ b1,
+                                  const int32_t* __restrict__ changed, int iters, const int32_t* __restrict__ ng,
+                                  LevelTotals* tot) {
+  // the last sweep that ran wrote buffer (it + 1) % 2 ... pick the final one
+  int last = iters - 1;
+  for (int i = 1; i < iters; ++i)
+    if (changed[i - 1] == 0) { last = i - 1; break; }
+  const int32_t* b = (last % 2 == 0) ? b1 : b0;
+  const int n = *ng;
+  int m = 0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) m = max(m, b[t]);
+  typedef cub::BlockReduce<int, 256> R;
+  __shared__ typename R::TempStorage rt;
+  m = R(rt).Reduce(m, cub::Max());
+  if (threadIdx.x == 0) tot->max_chain = m;
+}
+
+// after the level's kernels: ranks known -> delta blocks, solve records, stats
+__global__ void skel_finish_inc(const SkelTask* __restrict__ tasks, const int32_t* __restrict__ kout,
+                                const int32_t* __restrict__ ng, int2* __restrict__ inc) {
+  const int n = *ng;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
+    const int k = kout[g], r = tasks[g].nc - k;
+    inc[g] = make_int2(r > 0 && k > 0, r > 0);
+  }
+}
+
+struct Int2Sum {
+  __device__ __forceinline__ int2 operator()(const int2& a, const int2& b) const {
+    return make_int2(a.x + b.x, a.y + b.y);
+  }
+};
+
+__global__ void skel_finish_fill(const SkelTask* __restrict__ tasks, const int32_t* __restrict__ kout,
+                                 const int32_t* __restrict__ ng, const int2* __restrict__ exc, SkelFinishArgs A) {
+  const int n = *ng;
+  const int64_t nblk0 = *A.nblk;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
+    const SkelTask& T = tasks[g];
+    const int k = kout[g], r = T.nc - k;
+    if (r > 0 && k > 0) {
+      const int64_t id = nblk0 + exc[g].x;
+      A.blk_dof_off[id] = T.out_off;
+      A.blk_n[id] = k;
+      A.blk_val_off[id] = T.delta_off;
+      A.blk_alive[id] = 1;
+    }
+    hifde_record_t X;
+    X.kind = 1;
+    X.nc = T.nc;
+    X.nq = k;
+    X.nr = r;
+    X.cell_off = T.dofs_off;
+    X.idx_off = T.out_off;
+    X.T_off = T.rec_off;
+    X.P_off = T.rec_off + (int64_t)k * r;
+    X.W_off = T.rec_off + (int64_t)k * r + (int64_t)r * r;
+    A.xrec[g] = X;
+    if (r > 0) {
+      SolveRec R;
+      R.nc = r;
+      R.nq = k;
+      R.idx_off = T.out_off;
+      R.T_off = T.rec_off;
+      R.C_off = T.rec_off + (int64_t)k * r;
+      R.W_off = R.C_off + (int64_t)r * r;
+      R.contrib_off = 0;
+      R.inv = 1;
+      R.pad = 0;
+      A.recs[exc[g].y] = R;
+    }
+  }
+}
+
+__global__ void skel_stats_kernel(const SkelTask* __restrict__ tasks, const int32_t* __restrict__ kout,
+                                  const int32_t* __restrict__ ng, const int2* __restrict__ exc,
+                                  const int2* __restrict__ inc, LevelStat* st, int64_t* nblk) {
+  __shared__ double red[4][256];
+  typedef cub::BlockReduce<int64_t, 256> R;
+  __shared__ typename R::TempStorage rt;
+  const int n = *ng;
+  double fl = 0, by = 0, sf = 0, sr = 0;
+  int64_t nsk = 0, nrd = 0, mf = 0, mnc = 0, mnq = 0, mfront = 0;
+  for (int g = threadIdx.x; g < n; g += 256) {
+    const SkelTask& T = tasks[g];
+    const int kk = kout[g], r = T.nc - kk;
+    nsk += kk;
+    nrd += r;
+    mfront = max(mfront, (int64_t)(T.nc + T.nq));
+    const double dc = T.nc, dq = T.nq, dk = kk, dr = r;
+    double f = 4 * dq * dc * dk - 2 * dk * dk * (dq + dc) + 4 * dk * dk * dk / 3 + 2 * dq * dc + dk * dk * dr +
+               2 * dk * dk * dr + 4 * dk * dr * dr;
+    if (r > 0) f += dr * dr * dr / 3 + dr * dr * dk + dk * dk * dr;
+    fl += f * 1e-9;
+    by += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
+    if (r > 0) {
+      mf += 8 * ((int64_t)kk * r + (int64_t)r * r + r + (int64_t)r * kk);
+      sf += dr * (dr + 1) / 2 + 2 * dr * dk;
+      sr += dr + dk;
+      mnc = max(mnc, (int64_t)r);
+      mnq = max(mnq, (int64_t)kk);
+    }
+  }
+  red[0][threadIdx.x] = fl;
+  red[1][threadIdx.x] = by;
+  red[2][threadIdx.x] = sf;
+  red[3][threadIdx.x] = sr;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int i = 0; i < 4; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + s];
+    __syncthreads();
+  }
+  const int64_t s_nsk = R(rt).Sum(nsk);
+  __syncthreads();
+  const int64_t s_nrd = R(rt).Sum(nrd);
+  __syncthreads();
+  const int64_t s_mf = R(rt).Sum(mf);
+  __syncthreads();
+  const int64_t m_nc = R(rt).Reduce(mnc, cub::Max());
+  __syncthreads();
+  const int64_t m_nq = R(rt).Reduce(mnq, cub::Max());
+  __syncthreads();
+  const int64_t m_front = R(rt).Reduce(mfront, cub::Max());
+  if (threadIdx.x == 0) {
+    st->ngroups = n;
+    st->nskel = s_nsk;
+    st->nred = s_nrd;
+    st->gflop = red[0][0];
+    st->gbytes = red[1][0];
+    st->gf_cls[0] = red[0][0];
+    st->gb_cls[0] = red[1][0];
+    st->solve_fac = red[2][0];
+    st->solve_rows = red[3][0];
+    st->mf_bytes = s_mf;
+    st->max_nc = m_nc;
+    st->max_nq = m_nq;
+    st->max_front = m_front;
+    const int2 last = n ? make_int2(exc[n - 1].x + inc[n - 1].x, exc[n - 1].y + inc[n - 1].y) : make_int2(0, 0);
+    st->nrecs = last.y;
+    *nblk += last.x;
+  }
+}
+
+// active DOFs -> ascending list (and the count into the previous level's stats)
+__global__ void count_to(const int64_t* __restrict__ n, int64_t* dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *dst = *n;
+}
+
+// ---------------------------------------------------------------------------
+// Host-side launchers
+// ---------------------------------------------------------------------------
+namespace {
+int sym_grid(int per_sm) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm * per_sm;
+}
+}  // namespace
+
+// temp storage for CUB calls lives at the front of W.cub_tmp; the launcher
+// grows it (stream-ordered) when a call needs more
+static void ensure_tmp(SymWork& W, size_t bytes, cudaStream_t s) {
+  if (bytes <= W.cub_bytes) return;
+  if (W.cub_tmp) cudaFreeAsync(W.cub_tmp, s);
+  W.cub_bytes = bytes + bytes / 2 + (1 << 20);
+  cudaMallocAsync((void**)&W.cub_tmp, W.cub_bytes, s);
+}
+
+cudaError_t sym_active_list(const uint8_t* active, int64_t N, int32_t* act, int64_t* nact, SymWork& W,
+                            cudaStream_t s) {
+  size_t tb = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tb, it, active, act, nact, (int)N, s);
+  ensure_tmp(W, tb, s);
+  return cub::DeviceSelect::Flagged(W.cub_tmp, tb, it, active, act, nact, (int)N, s);
+}
+
+cudaError_t sym_partition(const SymPartArgs& A, SymWork& W, cudaStream_t s) {
+  if (A.nact_ub <= 0) {
+    cudaMemsetAsync(A.ng, 0, sizeof(int32_t), s);
+    cudaMemsetAsync(A.goff, 0, sizeof(int64_t), s);
+    return cudaGetLastError();
+  }
+  const int grid = sym_grid(8);
+  sym_keys_kernel<<<grid, 256, 0, s>>>(A.act, A.nact, A.nact_ub, A.dim, A.side, A.w, A.k, A.kind, A.nkeys, A.keys);
+  int bits = 1;
+  while ((1ll << bits) <= (int64_t)A.nkeys) ++bits;  // keys in [0, nkeys]
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, A.keys, A.skeys, A.act, A.gmem, (int)A.nact_ub, 0, bits, s);
+  ensure_tmp(W, tb, s);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, A.keys, A.skeys, A.act, A.gmem, (int)A.nact_ub,
+                                                  0, bits, s);
+  if (e != cudaSuccess) return e;
+  sym_heads_kernel<<<grid, 256, 0, s>>>(A.skeys, A.nact_ub, A.nkeys, A.head);
+  tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, A.head, A.head, (int)A.nact_ub, s);
+  ensure_tmp(W, tb, s);
+  e = cub::DeviceScan::InclusiveSum(W.cub_tmp, tb, A.head, A.head, (int)A.nact_ub, s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(A.ng, 0, sizeof(int32_t), s);
+  cudaMemsetAsync(A.goff, 0, sizeof(int64_t), s);
+  sym_groups_kernel<<<grid, 256, 0, s>>>(A.skeys, A.head, A.gmem, A.nact, A.nkeys, A.goff, A.ng, A.group_of);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_membership(const SymMemberArgs& A, SymWork& W, cudaStream_t s) {
+  // live blocks
+  size_t tb = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tb, it, A.blk_alive, A.alive_list, A.nalive, (int)A.nblk_ub, s);
+  ensure_tmp(W, tb, s);
+  cudaError_t e = cub::DeviceSelect::Flagged(W.cub_tmp, tb, it, A.blk_alive, A.alive_list, A.nalive,
+                                             (int)A.nblk_ub, s);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(A.cnt, 0, sizeof(int32_t) * (size_t)(A.N + 1), s);
+  const int grid = sym_grid(8);
+  sym_member_count<<<grid, 256, 0, s>>>(A.alive_list, A.nalive, A.blk_n, A.blk_dof_off, A.idx, A.active, A.cnt);
+  tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, A.cnt, A.mptr, (int)(A.N + 1), s);
+  ensure_tmp(W, tb, s);
+  e = cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, A.cnt, A.mptr, (int)(A.N + 1), s);
+  if (e != cudaSuccess) return e;
+  cudaMemcpyAsync(A.cnt, A.mptr, sizeof(int32_t) * (size_t)(A.N + 1), cudaMemcpyDeviceToDevice, s);
+  sym_member_fill<<<grid, 256, 0, s>>>(A.alive_list, A.nalive, A.blk_n, A.blk_dof_off, A.idx, A.active, A.cnt,
+                                       A.mblk);
+  return cudaGetLastError();
+}
+
+namespace {
+constexpr int kSLQ = 10, kSLB = 8, kSLP = 8, kSNC = 512;     // small tier: 1024 / 256 / 256 slots, 512 DOFs
+constexpr int kBLQ = 14, kBLB = 11, kBLP = 11, kBNC = 4096;  // big tier
+constexpr size_t smem_of(int lq, int lb, int lp, int nc) {
+  return sizeof(int32_t) * ((size_t)nc + (1u << lb) + 2 * (1u << lq) + (1u << lp));
+}
+template <bool FILL>
+cudaError_t fronts_pass(const SymFront& P, cudaStream_t s) {
+  auto ks = sym_front_kernel<kSLQ, kSLB, kSLP, kSNC, FILL>;
+  auto kb = sym_front_kernel<kBLQ, kBLB, kBLP, kBNC, FILL>;
+  static bool once = false;
+  const size_t ss = smem_of(kSLQ, kSLB, kSLP, kSNC), sb = smem_of(kBLQ, kBLB, kBLP, kBNC);
+  if (!once) {
+    cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ss);
+    cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    once = true;
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ks, kSymNT, ss);
+  ks<<<sym_grid(std::max(per, 1)), kSymNT, ss, s>>>(P);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kb, kSymNT, sb);
+  kb<<<sym_grid(std::max(per, 1)), kSymNT, sb, s>>>(P);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t sym_fronts_count(const SymFront& P, cudaStream_t s) {
+  cudaMemsetAsync(P.nretry, 0, sizeof(int32_t), s);
+  return fronts_pass<false>(P, s);
+}
+cudaError_t sym_fronts_fill(const SymFront& P, cudaStream_t s) { return fronts_pass<true>(P, s); }
+
+cudaError_t sym_elim_sizes(const SymFront& P, int is_top, int ng_ub, ElimInc* inc, ElimInc* exc, LevelTotals* tot,
+                           SymWork& W, cudaStream_t s) {
+  cudaMemsetAsync(tot, 0, sizeof(LevelTotals), s);
+  cudaMemsetAsync(inc, 0, sizeof(ElimInc) * (size_t)ng_ub, s);
+  elim_size_kernel<<<sym_grid(4), 256, 0, s>>>(P, is_top, inc, tot);
+  size_t tb = 0;
+  ElimInc zero;
+  for (int i = 0; i < kElimIncN; ++i) zero.v[i] = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tb, inc, exc, ElimIncOp(), zero, ng_ub, s);
+  ensure_tmp(W, tb, s);
+  cudaError_t e = cub::DeviceScan::ExclusiveScan(W.cub_tmp, tb, inc, exc, ElimIncOp(), zero, ng_ub, s);
+  if (e != cudaSuccess) return e;
+  elim_total_kernel<<<1, 1, 0, s>>>(P.ng, inc, exc, tot);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_elim_fill(const SymFront& P, const ElimFillArgs& A, int64_t nred_ub, SymWork& W, cudaStream_t s) {
+  elim_fill_kernel<<<sym_grid(4), 256, 0, s>>>(P, A);
+  elim_stats_kernel<<<1, 256, 0, s>>>(P.ng, A.cellstat, A.cellcls, P, A.stat, A.newblk_total, A.nblk);
+  // reduction of the forward sweep: contribution rows grouped by neighbour
+  // DOF in record order (stable radix sort), targets = the distinct DOFs
+  if (nred_ub > 0) {
+    size_t tb = 0;
+    int bits = 1;
+    while ((1ll << bits) < A.N) ++bits;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, A.red_key, A.red_key2, A.red_val, A.red_ent, (int)nred_ub, 0, bits,
+                                    s);
+    ensure_tmp(W, tb, s);
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, A.red_key, A.red_key2, A.red_val, A.red_ent,
+                                                    (int)nred_ub, 0, bits, s);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(A.red_cnt, 0, sizeof(int64_t) * (size_t)(nred_ub + 1), s);
+    tb = 0;
+    cub::DeviceRunLengthEncode::Encode(nullptr, tb, A.red_key2, A.red_targets, A.red_cnt, A.red_nt, (int)nred_ub, s);
+    ensure_tmp(W, tb, s);
+    e = cub::DeviceRunLengthEncode::Encode(W.cub_tmp, tb, A.red_key2, A.red_targets, A.red_cnt, A.red_nt,
+                                           (int)nred_ub, s);
+    if (e != cudaSuccess) return e;
+    tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, A.red_cnt, A.red_ptr, (int)(nred_ub + 1), s);
+    ensure_tmp(W, tb, s);
+    e = cub::DeviceScan::ExclusiveSum(W.cub_tmp, tb, A.red_cnt, A.red_ptr, (int)(nred_ub + 1), s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t sym_skel_sizes(const SymFront& P, double promote_work, int gram_eps_ok, int ng_ub, SkelInc* inc,
+                           SkelInc* exc, LevelTotals* tot, SymWork& W, cudaStream_t s) {
+  cudaMemsetAsync(tot, 0, sizeof(LevelTotals), s);
+  cudaMemsetAsync(inc, 0, sizeof(SkelInc) * (size_t)ng_ub, s);
+  skel_size_kernel<<<sym_grid(4), 256, 0, s>>>(P, promote_work, gram_eps_ok, inc, tot);
+  size_t tb = 0;
+  SkelInc zero;
+  for (int i = 0; i < kSkelIncN; ++i) zero.v[i] = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tb, inc, exc, SkelIncOp(), zero, ng_ub, s);
+  ensure_tmp(W, tb, s);
+  cudaError_t e = cub::DeviceScan::ExclusiveScan(W.cub_tmp, tb, inc, exc, SkelIncOp(), zero, ng_ub, s);
+  if (e != cudaSuccess) return e;
+  skel_total_kernel<<<1, 1, 0, s>>>(P.ng, inc, exc, tot);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t s) {
+  skel_fill_kernel<<<sym_grid(4), 256, 0, s>>>(P, A);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_skel_chain(const int64_t* pred_ptr, const int32_t* preds, const int32_t* ng, int ng_ub, int iters,
+                           int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot, cudaStream_t s) {
+  cudaMemsetAsync(b0, 0, sizeof(int32_t) * (size_t)ng_ub, s);
+  cudaMemsetAsync(changed, 0, sizeof(int32_t) * (size_t)iters, s);
+  const int grid = std::max(1, std::min(sym_grid(4), (ng_ub + 255) / 256));
+  for (int it = 0; it < iters; ++it) {
+    const int32_t* bin = (it % 2 == 0) ? b0 : b1;
+    int32_t* bout = (it % 2 == 0) ? b1 : b0;
+    skel_relax_kernel<<<grid, 256, 0, s>>>(pred_ptr, preds, ng, bin, bout, changed, it);
+  }
+  skel_chain_kernel<<<1, 256, 0, s>>>(b0, b1, changed, iters, ng, tot);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_skel_cluster_tasks(SkelTask* tasks, const int64_t* cl_rel, int64_t base, const int32_t* ng,
+                                   int ng_ub, cudaStream_t s) {
+  skel_cluster_tasks<<<std::max(1, (ng_ub + 255) / 256), 256, 0, s>>>(tasks, cl_rel, base, ng);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_skel_finish(const SkelTask* tasks, const int32_t* kout, const int32_t* ng, int ng_ub,
+                            const SkelFinishArgs& A, SymWork& W, cudaStream_t s) {
+  const int grid = std::max(1, std::min(sym_grid(4), (ng_ub + 255) / 256));
+  int2* inc = A.inc;
+  int2* exc = A.exc;
+  cudaMemsetAsync(inc, 0, sizeof(int2) * (size_t)ng_ub, s);
+  skel_finish_inc<<<grid, 256, 0, s>>>(tasks, kout, ng, inc);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveScan(nullptr, tb, inc, exc, Int2Sum(), make_int2(0, 0), ng_ub, s);
+  ensure_tmp(W, tb, s);
+  cudaError_t e = cub::DeviceScan::ExclusiveScan(W.cub_tmp, tb, inc, exc, Int2Sum(), make_int2(0, 0), ng_ub, s);
+  if (e != cudaSuccess) return e;
+  skel_finish_fill<<<grid, 256, 0, s>>>(tasks, kout, ng, exc, A);
+  skel_stats_kernel<<<1, 256, 0, s>>>(tasks, kout, ng, exc, inc, A.stat, A.nblk);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_reset_groups(const int32_t* gmem, const int64_t* goff, const int32_t* ng, int32_t* group_of,
+                             cudaStream_t s) {
+  sym_reset_group_of<<<sym_grid(4), 256, 0, s>>>(gmem, goff, ng, group_of);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_copy_count(const int64_t* n, int64_t* dst, cudaStream_t s) {
+  count_to<<<1, 32, 0, s>>>(n, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace hifde

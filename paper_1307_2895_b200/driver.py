@@ -183,7 +183,8 @@ class GeneralizedLDL:
 
 def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
             order: str = "auto", exact_max_batches: int = 64, device: Optional[int] = None,
-            stream: Optional[int] = None, comm=None, kernel_log: bool = False) -> GeneralizedLDL:
+            stream: Optional[int] = None, comm=None, kernel_log: bool = False,
+            symbolic: str = "auto") -> GeneralizedLDL:
     lib = L.load()
     if not spd:
         raise NotImplementedError("indefinite (Bunch-Kaufman) mode is outside the GPU hot path")
@@ -205,6 +206,7 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     opt.stream = stream
     opt.comm = comm.handle if comm is not None else None  # distributed.Comm: sharded sweep
     opt.kernel_log = int(bool(kernel_log))
+    opt.symbolic = L.SYMBOLIC[symbolic]  # "host": the host level analysis throughout (A/B tests)
     h = C.c_void_p()
     code = lib.hifde_factor(indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, csr.shape[0],
                             int(grid.dim), int(grid.n), int(grid.m), int(grid.nlevels),
