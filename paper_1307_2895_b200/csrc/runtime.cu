@@ -2848,7 +2848,8 @@ struct Factorizer {
   void dev_sync_totals() {
     HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
     HCK(cudaMemcpyAsync(h_scal, d_scal, sizeof(SymScalars), cudaMemcpyDeviceToHost, s));
-    check_status();  // synchronizes the stream
+    HCK(cudaStreamSynchronize(s));
+    check_status();
   }
 
   // Partition + membership + count pass of a level.  kind 0 interior cells,
@@ -3002,6 +3003,9 @@ struct Factorizer {
     P.o_pred = 0;
     P.idx_base = idx_base;
     P.idx_out = F->idx.p;
+    P.idx = F->idx.p;  // the arenas may have moved since the count pass
+    P.blk_n = d_blk_n.p;
+    P.blk_dof_off = d_blk_dof_off.p;
     P.lists = lists.p;
     P.preds = nullptr;
     HCK(sym_fronts_fill(P, s));
@@ -3127,6 +3131,9 @@ struct Factorizer {
     P.o_pred = 5;
     P.idx_base = idx_base;
     P.idx_out = F->idx.p;
+    P.idx = F->idx.p;  // the arenas may have moved since the count pass
+    P.blk_n = d_blk_n.p;
+    P.blk_dof_off = d_blk_dof_off.p;
     P.lists = lists.p;
     P.preds = sy_preds.p;
     HCK(sym_fronts_fill(P, s));
