@@ -115,6 +115,7 @@ __device__ __forceinline__ double* workspace(double* smem, double* scratch, int6
 // 2 dense row-major (ld lda), 3 dense transposed.
 constexpr int kGKC = 32, kGRB = 16, kGMI = 6;
 constexpr int kGRows = (NT / kGRB) * kGMI;  // rows per pass (96)
+constexpr int kMmaMinRhs = 8;               // small-record kernels: DMMA tiles from 8 right-hand sides
 constexpr int kDmmaMinRhs = 48;             // right-hand sides from which products use DMMA (measured: 16 and 32
                                             // RHS have too few tiles per warp to hide DMMA latency)
 // One right-hand side: a matrix-vector product read straight from global
@@ -498,6 +499,243 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_small_kernel(const SolveRec
     double acc = 0.0;
     for (int k = 0; k < nc; ++k) acc += (k >= i ? sP[k * (k + 1) / 2 + i] : 0.0) * st[k * nrhs + r];
     v[(size_t)c[i] * nrhs + r] = 0.0 + 1.0 * acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Small records on the FP64 tensor cores (8+ right-hand sides): the same
+// single-load phase, then every product D = op(A) X as 8 x 8 DMMA tiles
+// (mma.sync m8n8k4).  Warp w owns the tile pairs p = w, w + 8, ... of
+// (row tile, RHS tile); with 8, 16, 32 or 64 right-hand sides all of a warp's
+// tiles share one RHS tile, so its X fragment is loaded once per k step.
+// Triangular factors skip the k steps outside the triangle.  Products are
+// written in place where the inputs allow (s over x_c, t over x_c), so a
+// level-0 cell of config 3 needs 49 KB (forward) / 65 KB (backward).
+// ---------------------------------------------------------------------------
+constexpr int kMmaMaxJ = 12;  // tile pairs per warp: 96 rows x 64 RHS
+
+__host__ __device__ inline int mma_ld(int nrhs) {  // row stride: >= nrhs, = 8 (mod 16): conflict-free B fragments
+  int ld = (nrhs + 7) / 8 * 8;
+  if (ld % 16 == 0) ld += 8;
+  return ld;
+}
+
+// A(i, k): 0 packed lower P, 1 its transpose, 2 dense row-major, 3 dense transposed
+template <int AM>
+__device__ __forceinline__ double mma_a(const double* __restrict__ A, int lda, int i, int k) {
+  if (AM == 0) return k <= i ? A[i * (i + 1) / 2 + k] : 0.0;
+  if (AM == 1) return k >= i ? A[k * (k + 1) / 2 + i] : 0.0;
+  if (AM == 2) return A[i * lda + k];
+  return A[k * lda + i];
+}
+
+template <int AM, class Out>
+__device__ __forceinline__ void warp_mma(int M, int K, const double* __restrict__ A, int lda, const double* X,
+                                         int ldx, int R, Out out) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int mt = (M + 7) >> 3, ntr = (R + 7) >> 3, npair = mt * ntr;
+  const int ar = lane >> 2, ak = lane & 3;
+  const bool one_rt = NW % ntr == 0;  // every pair of this warp in RHS tile w % ntr
+  double acc[kMmaMaxJ][2];
+#pragma unroll
+  for (int j = 0; j < kMmaMaxJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+  int klo = 0, khi = K;
+  if (w < npair) {
+    const int mlo = w / ntr, mhi = (w + NW * ((npair - 1 - w) / NW)) / ntr;
+    if (AM == 0) khi = min(K, 8 * mhi + 8);
+    if (AM == 1) klo = 8 * mlo;
+  } else {
+    khi = 0;
+  }
+  for (int k0 = klo & ~3; k0 < khi; k0 += 4) {
+    const int k = k0 + ak;
+    double b0 = 0.0;
+    if (one_rt) {
+      const int c = 8 * (w % ntr) + ar;
+      b0 = (k < K && c < R) ? X[k * ldx + c] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kMmaMaxJ; ++j) {
+      const int p = w + NW * j;
+      if (p >= npair) break;
+      const int mi = p / ntr, ri = p - mi * ntr;
+      if (AM == 0 && k0 >= 8 * mi + 8) continue;  // above the diagonal: zero
+      if (AM == 1 && k0 + 4 <= 8 * mi) continue;  // below it (transpose): zero
+      const int i = 8 * mi + ar;
+      const double a = (i < M && k < K) ? mma_a<AM>(A, lda, i, k) : 0.0;
+      double b = b0;
+      if (!one_rt) {
+        const int c = 8 * ri + ar;
+        b = (k < K && c < R) ? X[k * ldx + c] : 0.0;
+      }
+      dmma_8x8x4(acc[j][0], acc[j][1], a, b);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kMmaMaxJ; ++j) {
+    const int p = w + NW * j;
+    if (p >= npair) break;
+    const int mi = p / ntr, ri = p - mi * ntr;
+    const int row = 8 * mi + (lane >> 2);
+    if (row >= M) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = 8 * ri + 2 * (lane & 3) + h;
+      if (col < R) out(row, col, acc[j][h], j, h);
+    }
+  }
+}
+
+// forward: s = P x_c -> v_c ; g = W^T s -> contribution rows
+__global__ void __launch_bounds__(NT) solve_elim_fwd_mma_kernel(const SolveRec* __restrict__ recs,
+                                                                const int32_t* __restrict__ idx,
+                                                                const double* __restrict__ fac,
+                                                                double* __restrict__ v, int R,
+                                                                double* __restrict__ contrib) {
+  extern __shared__ __align__(16) double sm[];
+  const SolveRec rc = recs[blockIdx.x];
+  const int nc = rc.nc, nq = rc.nq, ld = mma_ld(R);
+  const int np = nc * (nc + 1) / 2;
+  double* sP = sm;
+  double* sW = sP + np;
+  double* sx = sW + nc * nq;
+  const int32_t* c = idx + rc.idx_off;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < np; e += NT) sP[e] = P[e];
+  for (int e = threadIdx.x; e < nc * nq; e += NT) sW[e] = W[e];
+  for (int e = threadIdx.x; e < nc * R; e += NT) {
+    const int i = e / R, r = e - i * R;
+    sx[i * ld + r] = v[(size_t)c[i] * R + r];
+  }
+  __syncthreads();
+  // s = P x_c, kept in registers until every warp has read x_c, then in place
+  {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ntr = (R + 7) >> 3, npair = ((nc + 7) >> 3) * ntr;
+    double keep[kMmaMaxJ][2];
+    warp_mma<0>(nc, nc, sP, 0, sx, ld, R, [&](int row, int col, double val, int j_, int h_) {
+      keep[j_][h_] = val;
+      v[(size_t)c[row] * R + col] = val;
+    });
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kMmaMaxJ; ++j) {
+      const int p = w + NW * j;
+      if (p >= npair) break;
+      const int mi = p / ntr, ri = p - mi * ntr, row = 8 * mi + (lane >> 2);
+      if (row >= nc) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * ri + 2 * (lane & 3) + h;
+        if (col < R) sx[row * ld + col] = keep[j][h];
+      }
+    }
+  }
+  __syncthreads();
+  if (nq > 0) {
+    double* g = contrib + (size_t)rc.contrib_off * R;
+    warp_mma<3>(nq, nc, sW, nq, sx, ld, R, [&](int row, int col, double val, int j_, int h_) { g[(size_t)row * R + col] = val; });
+  }
+}
+
+// backward: t = x_c - W x_q (in place) ; v_c = P^T t
+__global__ void __launch_bounds__(NT) solve_elim_bwd_mma_kernel(const SolveRec* __restrict__ recs,
+                                                                const int32_t* __restrict__ idx,
+                                                                const double* __restrict__ fac,
+                                                                double* __restrict__ v, int R) {
+  extern __shared__ __align__(16) double sm[];
+  const SolveRec rc = recs[blockIdx.x];
+  const int nc = rc.nc, nq = rc.nq, ld = mma_ld(R);
+  const int np = nc * (nc + 1) / 2;
+  double* sP = sm;
+  double* sW = sP + np;
+  double* st = sW + nc * nq;
+  double* sq = st + nc * ld;
+  const int32_t* c = idx + rc.idx_off;
+  const int32_t* q = c + nc;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < np; e += NT) sP[e] = P[e];
+  for (int e = threadIdx.x; e < nc * nq; e += NT) sW[e] = W[e];
+  for (int e = threadIdx.x; e < nc * R; e += NT) {
+    const int i = e / R, r = e - i * R;
+    st[i * ld + r] = v[(size_t)c[i] * R + r];
+  }
+  for (int e = threadIdx.x; e < nq * R; e += NT) {
+    const int b = e / R, r = e - b * R;
+    sq[b * ld + r] = v[(size_t)q[b] * R + r];
+  }
+  __syncthreads();
+  if (nq > 0) {
+    warp_mma<2>(nc, nq, sW, nq, sq, ld, R, [&](int row, int col, double val, int j_, int h_) { st[row * ld + col] -= val; });
+    __syncthreads();
+  }
+  warp_mma<1>(nc, nc, sP, 0, st, ld, R, [&](int row, int col, double val, int j_, int h_) { v[(size_t)c[row] * R + col] = val; });
+}
+
+// skeleton record: sk[k] then rd[r]; T (k x r), P (r x r packed), W (r x k)
+__global__ void __launch_bounds__(NT) solve_skel_mma_kernel(const SolveRec* __restrict__ recs,
+                                                            const int32_t* __restrict__ idx,
+                                                            const double* __restrict__ fac,
+                                                            double* __restrict__ v, int R, int forward) {
+  extern __shared__ __align__(16) double sm[];
+  const SolveRec rc = recs[blockIdx.x];
+  const int r = rc.nc, k = rc.nq, ld = mma_ld(R);
+  const int np = r * (r + 1) / 2;
+  double* sT = sm;             // k x r
+  double* sP = sT + k * r;     // packed r x r
+  double* sW = sP + np;        // r x k
+  double* xs = sW + r * k;     // k x ld
+  double* xr = xs + k * ld;    // r x ld
+  double* x2 = xr + r * ld;    // r x ld
+  const int32_t* sk = idx + rc.idx_off;
+  const int32_t* rd = sk + k;
+  const double* T = fac + rc.T_off;
+  const double* P = fac + rc.C_off;
+  const double* W = fac + rc.W_off;
+  for (int e = threadIdx.x; e < k * r; e += NT) sT[e] = T[e];
+  for (int e = threadIdx.x; e < np; e += NT) sP[e] = P[e];
+  for (int e = threadIdx.x; e < r * k; e += NT) sW[e] = W[e];
+  for (int e = threadIdx.x; e < k * R; e += NT) {
+    const int a = e / R, j = e - a * R;
+    xs[a * ld + j] = v[(size_t)sk[a] * R + j];
+  }
+  for (int e = threadIdx.x; e < r * R; e += NT) {
+    const int b = e / R, j = e - b * R;
+    xr[b * ld + j] = v[(size_t)rd[b] * R + j];
+  }
+  __syncthreads();
+  if (forward) {
+    if (k > 0) {  // v_rd -= T^T v_sk
+      warp_mma<3>(r, k, sT, r, xs, ld, R, [&](int row, int col, double val, int j_, int h_) { xr[row * ld + col] -= val; });
+      __syncthreads();
+    }
+    warp_mma<0>(r, r, sP, 0, xr, ld, R, [&](int row, int col, double val, int j_, int h_) {  // s = P v_rd
+      x2[row * ld + col] = val;
+      v[(size_t)rd[row] * R + col] = val;
+    });
+    __syncthreads();
+    if (k > 0)  // v_sk -= W^T s
+      warp_mma<3>(k, r, sW, k, x2, ld, R, [&](int row, int col, double val, int j_, int h_) {
+        v[(size_t)sk[row] * R + col] = xs[row * ld + col] - val;
+      });
+  } else {
+    if (k > 0) {  // v_rd -= W v_sk
+      warp_mma<2>(r, k, sW, k, xs, ld, R, [&](int row, int col, double val, int j_, int h_) { xr[row * ld + col] -= val; });
+      __syncthreads();
+    }
+    warp_mma<1>(r, r, sP, 0, xr, ld, R, [&](int row, int col, double val, int j_, int h_) {  // v_rd = P^T (...)
+      x2[row * ld + col] = val;
+      v[(size_t)rd[row] * R + col] = val;
+    });
+    __syncthreads();
+    if (k > 0)  // v_sk -= T v_rd
+      warp_mma<2>(k, r, sT, r, x2, ld, R, [&](int row, int col, double val, int j_, int h_) {
+        v[(size_t)sk[row] * R + col] = xs[row * ld + col] - val;
+      });
   }
 }
 
@@ -908,6 +1146,9 @@ void launch_solve_elim_fwd(const SolveRec* recs, int nrec, const int32_t* idx, c
 }
 
 size_t solve_small_smem(int max_nc, int max_nq, int nrhs) {
+  if (nrhs >= kMmaMinRhs)  // DMMA kernels: x_c (forward) or x_c and x_q (backward) at stride mma_ld
+    return sizeof(double) * ((size_t)max_nc * (max_nc + 1) / 2 + (size_t)max_nc * max_nq +
+                             (size_t)(max_nc + max_nq) * mma_ld(nrhs));
   return sizeof(double) * ((size_t)max_nc * (max_nc + 1) / 2 + (size_t)max_nc * max_nq + 2 * (size_t)max_nc * nrhs +
                            (size_t)max_nq * nrhs);
 }
@@ -921,13 +1162,25 @@ void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx,
                                            (int)kSmemCapBytes),
                       true);
   (void)once;
+  static bool once2 = (cudaFuncSetAttribute(solve_elim_fwd_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kSmemCapBytes),
+                       cudaFuncSetAttribute(solve_elim_bwd_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kSmemCapBytes),
+                       true);
+  (void)once2;
+  if (nrhs >= kMmaMinRhs) {
+    if (forward) solve_elim_fwd_mma_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib);
+    else solve_elim_bwd_mma_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs);
+    return;
+  }
   if (forward) solve_elim_fwd_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, contrib);
   else solve_elim_bwd_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs);
 }
 
 size_t solve_skel_small_smem(int max_r, int max_k, int nrhs) {
-  return sizeof(double) * (2 * (size_t)max_k * max_r + (size_t)max_r * (max_r + 1) / 2 + (size_t)max_k * nrhs +
-                           2 * (size_t)max_r * nrhs);
+  const size_t ld = nrhs >= kMmaMinRhs ? (size_t)mma_ld(nrhs) : (size_t)nrhs;
+  return sizeof(double) * (2 * (size_t)max_k * max_r + (size_t)max_r * (max_r + 1) / 2 + (size_t)max_k * ld +
+                           2 * (size_t)max_r * ld);
 }
 
 void launch_solve_skel_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
@@ -937,6 +1190,14 @@ void launch_solve_skel_small(const SolveRec* recs, int nrec, const int32_t* idx,
                                            (int)kSmemCapBytes),
                       true);
   (void)once;
+  static bool once2 = (cudaFuncSetAttribute(solve_skel_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)kSmemCapBytes),
+                       true);
+  (void)once2;
+  if (nrhs >= kMmaMinRhs) {
+    solve_skel_mma_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward);
+    return;
+  }
   solve_skel_small_kernel<<<nrec, NT, smem, s>>>(recs, idx, fac, v, nrhs, forward);
 }
 

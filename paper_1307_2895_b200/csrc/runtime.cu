@@ -584,7 +584,7 @@ struct FrontSym {  // result of the symbolic analysis of one cell / group
 // host threads into pinned memory while the previous chunk's DMA runs (a
 // pageable cudaMemcpy stages through the driver at one thread's memcpy speed).
 struct PinnedXfer {
-  static constexpr size_t kChunk = 8u << 20;
+  static constexpr size_t kChunk = 32u << 20;
   char* buf[2] = {nullptr, nullptr};
   cudaEvent_t ev[2] = {nullptr, nullptr};
   int dev = -1;
@@ -599,8 +599,22 @@ struct PinnedXfer {
     dev = device;
     return true;
   }
+  // host memory the driver already has page-locked (cudaHostAlloc'ed or
+  // registered, e.g. a pinned torch tensor): DMA straight from / into it
+  static bool page_locked(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  }
+  static int copy_threads() {
+    static const int n = std::max(1, std::min(16, omp_get_num_procs()));
+    return n;
+  }
   static void pmemcpy(char* d, const char* s, size_t n) {
-    const int nth = n >= (1u << 20) ? 8 : 1;
+    const int nth = n >= (1u << 20) ? copy_threads() : 1;
 #pragma omp parallel for num_threads(nth) schedule(static)
     for (int t = 0; t < nth; ++t) {
       const size_t lo = n * t / nth, hi = n * (t + 1) / nth;
@@ -611,7 +625,7 @@ struct PinnedXfer {
     int device = 0;
     HCK(cudaGetDevice(&device));
     std::lock_guard<std::mutex> lk(m);
-    if (bytes < (1u << 20) || !ready(device)) {
+    if (bytes < (1u << 20) || page_locked(src) || !ready(device)) {
       HCK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
       return;
     }
@@ -630,7 +644,7 @@ struct PinnedXfer {
     int device = 0;
     HCK(cudaGetDevice(&device));
     std::lock_guard<std::mutex> lk(m);
-    if (bytes < (1u << 20) || !ready(device)) {
+    if (bytes < (1u << 20) || page_locked(dst) || !ready(device)) {
       HCK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
       HCK(cudaStreamSynchronize(s));
       return;

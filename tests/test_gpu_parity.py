@@ -375,37 +375,41 @@ def test_api_errors_are_reference_exceptions():
     assert np.isfinite(x).all()
 
 
-_SOLVE_DIGEST = r'''
-import hashlib, sys
+_SOLVE_DUMP = r'''
+import sys
 import numpy as np
 sys.path.insert(0, ".")
 import paper_1307_2895_b200 as H
-out = []
+out = {}
 for dim, n, m, eps, var in [(2, 64, 8, 1e-6, "hifde"), (3, 16, 4, 1e-6, "hifde3x")]:
     g = H.build_grid(dim, n, m)
     a = H.assemble(g, H.gaussian_contrast_field(g, seed=5))
     f = (H.factor_hifde if var == "hifde" else H.factor_hifde3x)(a, g, eps)
-    for nrhs in (2, 3, 17, 48, 64):
+    for nrhs in (2, 3, 8, 17, 48, 64):
         b = np.random.default_rng(nrhs).standard_normal((g.ndof, nrhs))
-        out.append(hashlib.sha256(f.apply_inverse(b).tobytes()).hexdigest()[:16])
-print(" ".join(out))
+        out[f"{dim}_{nrhs}"] = f.apply_inverse(b)
+np.savez(sys.argv[1], **out)
 '''
 
 
 @pytest.mark.gpu
-def test_small_record_solve_kernels_are_bit_identical():
-    """The single-load-phase record kernels sum in the general kernels' order:
-    solutions are byte-identical with them switched off (HIFDE_NO_SOLVE_SMALL,
-    read once per process, hence the subprocesses)."""
+def test_small_record_solve_kernels_match_general(tmp_path):
+    """The fine-level record kernels (single load phase; DMMA tiles from 8
+    right-hand sides) against the general record kernels
+    (HIFDE_NO_SOLVE_SMALL, read once per process, hence the subprocesses):
+    the same solutions to FP64 rounding of a different summation order."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    runs = []
-    for env in ({}, {"HIFDE_NO_SOLVE_SMALL": "1"}):
-        r = subprocess.run([sys.executable, "-c", _SOLVE_DIGEST], capture_output=True, text=True, cwd=root,
+    files = []
+    for i, env in enumerate(({}, {"HIFDE_NO_SOLVE_SMALL": "1"})):
+        fn = str(tmp_path / f"x{i}.npz")
+        r = subprocess.run([sys.executable, "-c", _SOLVE_DUMP, fn], capture_output=True, text=True, cwd=root,
                            env=dict(os.environ, **env), timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
-        runs.append(r.stdout.strip().splitlines()[-1])
-    assert runs[0] == runs[1]
+        files.append(np.load(fn))
+    for k in files[0].files:
+        x, y = files[0][k], files[1][k]
+        assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y), (k, np.linalg.norm(x - y) / np.linalg.norm(y))
