@@ -207,6 +207,185 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// Lower-triangular tile index tt -> (ti, tj), tj <= ti.
+__device__ __forceinline__ void tri_tile(int tt, int& ti, int& tj) {
+  int i = (int)((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= tt) ++i;
+  while (i * (i + 1) / 2 > tt) --i;
+  ti = i;
+  tj = tt - i * (i + 1) / 2;
+}
+
+// Blocked partial Cholesky of a front F (nf x nf, row-major, ld nf; lower
+// triangle used) over its first nc columns, 8-wide panels:
+//   * warp 0 factors the 8 x 8 diagonal block in registers (shuffles, no
+//     block barrier per column);
+//   * every thread solves one row of the panel below the block;
+//   * the trailing lower triangle takes the rank-8 update as 8 x 8 FP64 DMMA
+//     tiles (mma.sync m8n8k4), spread over the warps.
+// Three barriers per panel instead of one per column.  Afterwards F holds C
+// (rows < nc), L_qc = W^T = F_qc C^-T (rows >= nc, columns < nc) and the lower
+// triangle of U = F_qq - W^T W.  Status as chol_1sync: 1 indefinite (a pivot
+// <= 0 or NaN), 2 singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
+template <int NT>
+__device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double* Lp, int* sflag) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (nc == 0) return 0;
+  double sc = 0.0;
+  for (int i = threadIdx.x; i < nc; i += NT) sc = fmax(sc, fabs(F[(size_t)i * nf + i]));
+  double scale = block_max<NT>(sc, red);
+  if (scale == 0.0) {
+    double s2 = 0.0;
+    for (int e = threadIdx.x; e < nc * nc; e += NT) {
+      const int i = e / nc, j = e - i * nc;
+      if (j <= i) s2 = fmax(s2, fabs(F[(size_t)i * nf + j]));
+    }
+    scale = block_max<NT>(s2, red);
+  }
+  double dmin = DBL_MAX;
+  for (int p0 = 0; p0 < nc; p0 += 8) {
+    const int pw = min(8, nc - p0), p1 = p0 + pw;
+    __syncthreads();  // the previous trailing update is complete
+    if (wid == 0) {
+      double r[8];
+      const int l = lane;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = (l < pw && j <= l) ? F[(size_t)(p0 + l) * nf + p0 + j] : 0.0;
+      int bad = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < pw) {  // warp-uniform
+          const double akk = __shfl_sync(0xffffffffu, r[k], k);
+          if (!(akk > 0.0)) bad = 1;
+          dmin = fmin(dmin, akk);
+          const double lkk = sqrt(akk);
+          const double inv = 1.0 / lkk;
+          if (l == k) r[k] = lkk;
+          else if (l > k) r[k] *= inv;
+#pragma unroll
+          for (int j = k + 1; j < 8; ++j) {
+            const double ljk = __shfl_sync(0xffffffffu, r[k], j);
+            if (j <= l && l < pw) r[j] -= r[k] * ljk;
+          }
+        }
+      }
+      if (l < 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool in = l < pw && j <= l;
+          if (in) F[(size_t)(p0 + l) * nf + p0 + j] = r[j];
+          Lp[l * 8 + j] = in ? r[j] : 0.0;
+        }
+        Lp[64 + l] = l < pw ? 1.0 / r[l] : 0.0;  // inverse diagonal
+      }
+      if (lane == 0) *sflag = bad;
+    }
+    __syncthreads();
+    if (*sflag) return 1;
+    // panel below the diagonal block: row i <- row i C_pp^-T
+    for (int i = p1 + threadIdx.x; i < nf; i += NT) {
+      double x[8];
+      double* Fi = F + (size_t)i * nf + p0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = k < pw ? Fi[k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        double sk = x[k];
+#pragma unroll
+        for (int m = 0; m < k; ++m) sk -= x[m] * Lp[k * 8 + m];
+        x[k] = k < pw ? sk * Lp[64 + k] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < pw) Fi[k] = x[k];
+    }
+    __syncthreads();
+    // trailing lower triangle from p1: F[i][j] -= sum_k L[i][p0+k] L[j][p0+k]
+    const int nt = (nf - p1 + 7) / 8;
+    for (int tt = wid; tt < nt * (nt + 1) / 2; tt += NW) {
+      int ti, tj;
+      tri_tile(tt, ti, tj);
+      const int rb = p1 + 8 * ti, cb = p1 + 8 * tj;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 8; ks += 4) {
+        const int k = ks + (lane & 3);
+        const int ra = rb + (lane >> 2), rc = cb + (lane >> 2);
+        const double a = (k < pw && ra < nf) ? F[(size_t)ra * nf + p0 + k] : 0.0;
+        const double b = (k < pw && rc < nf) ? F[(size_t)rc * nf + p0 + k] : 0.0;
+        dmma_8x8x4(c0, c1, a, b);
+      }
+      const int row = rb + (lane >> 2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = cb + 2 * (lane & 3) + h;
+        if (row < nf && col <= row) F[(size_t)row * nf + col] -= h ? c1 : c0;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) red[0] = dmin;  // warp 0 tracked the pivots
+  __syncthreads();
+  dmin = red[0];
+  __syncthreads();
+  if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;
+  return 0;
+}
+
+// X = C^-1 (n x n, row-major ld n, zeros above the diagonal) for the lower C
+// (row-major, ld ldc) by block rows: X_b = C_bb^-1 (I_b - C_b,<b X_<b); the
+// product on DMMA tiles, the 8-row block by one thread per column.
+template <int NT>
+__device__ void tri_inverse_blocked(const double* C, int n, int ldc, double* X, double* Lp) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < n * n; e += NT) X[e] = 0.0;
+  for (int b0 = 0; b0 < n; b0 += 8) {
+    const int bw = min(8, n - b0);
+    __syncthreads();
+    // Y = -C[b0:b0+bw, 0:b0) X[0:b0, 0:b0) into X's block rows (columns < b0)
+    const int nct = (b0 + 7) / 8;
+    for (int ct = wid; ct < nct; ct += NW) {
+      const int j0 = 8 * ct;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k0 = j0 & ~3; k0 < b0; k0 += 4) {  // X[k][j] = 0 for k < j
+        const int k = k0 + (lane & 3);
+        const int ra = b0 + (lane >> 2), jb = j0 + (lane >> 2);
+        const double a = (ra < n && k < b0) ? C[(size_t)ra * ldc + k] : 0.0;
+        const double b = (k < b0 && jb < b0) ? X[(size_t)k * n + jb] : 0.0;
+        dmma_8x8x4(c0, c1, a, b);
+      }
+      const int row = b0 + (lane >> 2);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = j0 + 2 * (lane & 3) + h;
+        if (row < n && col < b0) X[(size_t)row * n + col] = -(h ? c1 : c0);
+      }
+    }
+    if (threadIdx.x < 64) {  // the diagonal block and its inverse diagonal
+      const int i = threadIdx.x >> 3, j = threadIdx.x & 7;
+      Lp[threadIdx.x] = (i < bw && j <= i) ? C[(size_t)(b0 + i) * ldc + b0 + j] : 0.0;
+      if (j == 0) Lp[64 + i] = i < bw ? 1.0 / C[(size_t)(b0 + i) * ldc + b0 + i] : 0.0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < b0 + bw; j += NT) {  // columns of the block rows
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double sacc = (j == b0 + i ? 1.0 : 0.0) + (i < bw && j < b0 ? X[(size_t)(b0 + i) * n + j] : 0.0);
+#pragma unroll
+        for (int m = 0; m < i; ++m) sacc -= Lp[i * 8 + m] * x[m];
+        x[i] = i < bw ? sacc * Lp[64 + i] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < bw) X[(size_t)(b0 + i) * n + j] = (j <= b0 + i) ? x[i] : 0.0;
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -215,7 +394,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // W = C^-1 F_cq; U = F_qq - W^T W.  Also the terminal block (nq == 0).
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
+__global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[NT / 32];
   const ElimTask t = tasks[blockIdx.x];
@@ -258,55 +437,31 @@ __global__ void __launch_bounds__(NT) elim_small_kernel(const ElimTask* __restri
     }
     __syncthreads();
   }
-  const int st = chol_1sync<NT>(F, nc, nf, red);
+  __shared__ double Lp[72];
+  __shared__ int sflag;
+  const int st = front_chol_blocked<NT>(F, nc, nf, red, Lp, &sflag);
   if (st != 0) {
     if (threadIdx.x == 0) A.status[blockIdx.x] = st;
     return;
   }
-  // W = C^-1 F_cq and (with room) X = C^-1 I in ONE barrier-free pass: a
-  // thread per right-hand-side column, forward substitution down the rows.
-  // Each column's sums run in the same order as the row-sweep TRSM
-  // (trsm_1sync), so the results are bit-identical to it; the identity
-  // columns start at their diagonal (the skipped terms are exact zeros).
-  double* X = t.scratch_off == -2 ? F + (size_t)nf * nf : nullptr;
-  const int ncol = nq + (X ? nc : 0);
-  for (int j = threadIdx.x; j < ncol; j += NT) {
-    if (j < nq) {
-      double* B = F + nc + j;
-      for (int i = 0; i < nc; ++i) {
-        const double* Ci = F + (size_t)i * nf;
-        double sacc = B[(size_t)i * nf];
-        for (int l = 0; l < i; ++l) sacc -= Ci[l] * B[(size_t)l * nf];
-        B[(size_t)i * nf] = sacc * (1.0 / Ci[i]);
-      }
-    } else {
-      const int jj = j - nq;
-      for (int i = 0; i < jj; ++i) X[(size_t)i * nc + jj] = 0.0;
-      for (int i = jj; i < nc; ++i) {
-        const double* Ci = F + (size_t)i * nf;
-        double sacc = i == jj ? 1.0 : 0.0;
-        for (int l = jj; l < i; ++l) sacc -= Ci[l] * X[(size_t)l * nc + jj];
-        X[(size_t)i * nc + jj] = sacc * (1.0 / Ci[i]);
-      }
-    }
-  }
-  __syncthreads();
+  // outputs: W = (L_qc)^T row-major nc x nq, U = F_qq - W^T W (symmetric from
+  // its lower triangle), P = C^-1 packed
   if (nq > 0) {
-    double* U = A.bvals + t.U_off;
-    for (int e = threadIdx.x; e < nq * nq; e += NT) {
-      const int a = e / nq, b = e - a * nq;
-      double s = F[(nc + a) * nf + nc + b];
-      for (int k = 0; k < nc; ++k) s -= F[k * nf + nc + a] * F[k * nf + nc + b];
-      U[e] = s;
-    }
     double* W = A.fac + t.W_off;
     for (int e = threadIdx.x; e < nc * nq; e += NT) {
       const int i = e / nq, j = e - i * nq;
-      W[e] = F[i * nf + nc + j];
+      W[e] = F[(size_t)(nc + j) * nf + i];
+    }
+    double* U = A.bvals + t.U_off;
+    for (int e = threadIdx.x; e < nq * nq; e += NT) {
+      const int a = e / nq, b = e - a * nq;
+      const int hi = a > b ? a : b, lo = a > b ? b : a;
+      U[e] = F[(size_t)(nc + hi) * nf + nc + lo];
     }
   }
-  // the solve applies C^-1 as a product: store it packed (lower, row-major)
+  double* X = t.scratch_off == -2 ? F + (size_t)nf * nf : nullptr;
   if (X) {
+    tri_inverse_blocked<NT>(F, nc, nf, X, Lp);
     double* P = A.fac + t.P_off;
     for (int e = threadIdx.x; e < nc * nc; e += NT) {
       const int i = e / nc, j = e - i * nc;
