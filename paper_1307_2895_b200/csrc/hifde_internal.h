@@ -126,7 +126,7 @@ __host__ __device__ inline ElimSizes elim_sizes(int nc, int nq, int maxnb, bool 
   const int nf = nc + nq;
   const size_t ib = hd_align16(sizeof(int32_t) * (size_t)(nf + maxnb));
   const size_t need = ib + sizeof(double) * (size_t)nf * nf;
-  const size_t need_inv = need + sizeof(double) * (size_t)nc * nc;
+  const size_t need_inv = need + sizeof(double) * 8 * (size_t)nc;  // in-place inverse: one 8-row product block
   ElimSizes z;
   if (need <= kSmemCapBytes && (is_top || (nc < kBigCellNc && nf < kBigCellNf))) {
     z.big = 0;

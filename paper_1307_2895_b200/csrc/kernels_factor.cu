@@ -209,7 +209,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 
 // Lower-triangular tile index tt -> (ti, tj), tj <= ti.
 __device__ __forceinline__ void tri_tile(int tt, int& ti, int& tj) {
-  int i = (int)((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
+  int i = (int)((sqrtf(8.0f * (float)tt + 1.0f) - 1.0f) * 0.5f);
   while ((i + 1) * (i + 2) / 2 <= tt) ++i;
   while (i * (i + 1) / 2 > tt) --i;
   ti = i;
@@ -218,17 +218,19 @@ __device__ __forceinline__ void tri_tile(int tt, int& ti, int& tj) {
 
 // Blocked partial Cholesky of a front F (nf x nf, row-major, ld nf; lower
 // triangle used) over its first nc columns, 8-wide panels:
-//   * warp 0 factors the 8 x 8 diagonal block in registers (shuffles, no
-//     block barrier per column);
+//   * every warp factors the 8 x 8 diagonal block itself, in registers with
+//     shuffles (redundantly: no barrier and no idle warps while one warp
+//     factors), and keeps it in its own shared-memory slot;
 //   * every thread solves one row of the panel below the block;
 //   * the trailing lower triangle takes the rank-8 update as 8 x 8 FP64 DMMA
 //     tiles (mma.sync m8n8k4), spread over the warps.
-// Three barriers per panel instead of one per column.  Afterwards F holds C
+// Two barriers per panel instead of one per column.  Afterwards F holds C
 // (rows < nc), L_qc = W^T = F_qc C^-T (rows >= nc, columns < nc) and the lower
 // triangle of U = F_qq - W^T W.  Status as chol_1sync: 1 indefinite (a pivot
 // <= 0 or NaN), 2 singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
+// Lw: NT/32 slots of 72 doubles (the warp's factored block, inverse diagonal).
 template <int NT>
-__device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double* Lp, int* sflag) {
+__device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double* Lw) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (nc == 0) return 0;
@@ -243,11 +245,12 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
     }
     scale = block_max<NT>(s2, red);
   }
+  double* Lp = Lw + wid * 72;
   double dmin = DBL_MAX;
   for (int p0 = 0; p0 < nc; p0 += 8) {
     const int pw = min(8, nc - p0), p1 = p0 + pw;
     __syncthreads();  // the previous trailing update is complete
-    if (wid == 0) {
+    {
       double r[8];
       const int l = lane;
 #pragma unroll
@@ -270,19 +273,14 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
           }
         }
       }
+      if (bad) return 1;  // every warp saw the same pivots
       if (l < 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const bool in = l < pw && j <= l;
-          if (in) F[(size_t)(p0 + l) * nf + p0 + j] = r[j];
-          Lp[l * 8 + j] = in ? r[j] : 0.0;
-        }
+        for (int j = 0; j < 8; ++j) Lp[l * 8 + j] = (l < pw && j <= l) ? r[j] : 0.0;
         Lp[64 + l] = l < pw ? 1.0 / r[l] : 0.0;  // inverse diagonal
       }
-      if (lane == 0) *sflag = bad;
+      __syncwarp();
     }
-    __syncthreads();
-    if (*sflag) return 1;
     // panel below the diagonal block: row i <- row i C_pp^-T
     for (int i = p1 + threadIdx.x; i < nf; i += NT) {
       double x[8];
@@ -301,6 +299,11 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
         if (k < pw) Fi[k] = x[k];
     }
     __syncthreads();
+    if (wid == 0 && lane < pw) {  // the factored diagonal block into place (nobody reads it this panel)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j <= lane) F[(size_t)(p0 + lane) * nf + p0 + j] = Lp[lane * 8 + j];
+    }
     // trailing lower triangle from p1: F[i][j] -= sum_k L[i][p0+k] L[j][p0+k]
     const int nt = (nf - p1 + 7) / 8;
     for (int tt = wid; tt < nt * (nt + 1) / 2; tt += NW) {
@@ -325,26 +328,21 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) red[0] = dmin;  // warp 0 tracked the pivots
-  __syncthreads();
-  dmin = red[0];
-  __syncthreads();
-  if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;
+  if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;  // every warp tracked every pivot
   return 0;
 }
 
-// X = C^-1 (n x n, row-major ld n, zeros above the diagonal) for the lower C
-// (row-major, ld ldc) by block rows: X_b = C_bb^-1 (I_b - C_b,<b X_<b); the
-// product on DMMA tiles, the 8-row block by one thread per column.
+// In place: the lower C (n x n, row-major ld) becomes X = C^-1, block row by
+// block row: X_b,<b = -C_bb^-1 (C_b,<b X_<b) (the product on DMMA tiles into
+// Y, 8 x n), X_bb = C_bb^-1, by one thread per column.  The strictly upper
+// part is not touched.
 template <int NT>
-__device__ void tri_inverse_blocked(const double* C, int n, int ldc, double* X, double* Lp) {
+__device__ void tri_inverse_inplace(double* C, int n, int ld, double* Y, double* Lp) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int e = threadIdx.x; e < n * n; e += NT) X[e] = 0.0;
   for (int b0 = 0; b0 < n; b0 += 8) {
     const int bw = min(8, n - b0);
-    __syncthreads();
-    // Y = -C[b0:b0+bw, 0:b0) X[0:b0, 0:b0) into X's block rows (columns < b0)
+    __syncthreads();  // X_<b complete
     const int nct = (b0 + 7) / 8;
     for (int ct = wid; ct < nct; ct += NW) {
       const int j0 = 8 * ct;
@@ -352,35 +350,35 @@ __device__ void tri_inverse_blocked(const double* C, int n, int ldc, double* X, 
       for (int k0 = j0 & ~3; k0 < b0; k0 += 4) {  // X[k][j] = 0 for k < j
         const int k = k0 + (lane & 3);
         const int ra = b0 + (lane >> 2), jb = j0 + (lane >> 2);
-        const double a = (ra < n && k < b0) ? C[(size_t)ra * ldc + k] : 0.0;
-        const double b = (k < b0 && jb < b0) ? X[(size_t)k * n + jb] : 0.0;
+        const double a = (ra < n && k < b0) ? C[(size_t)ra * ld + k] : 0.0;
+        const double b = (k < b0 && jb <= k) ? C[(size_t)k * ld + jb] : 0.0;  // X, lower part only
         dmma_8x8x4(c0, c1, a, b);
       }
-      const int row = b0 + (lane >> 2);
+      const int row = lane >> 2;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = j0 + 2 * (lane & 3) + h;
-        if (row < n && col < b0) X[(size_t)row * n + col] = -(h ? c1 : c0);
+        if (col < b0) Y[row * n + col] = h ? c1 : c0;
       }
     }
     if (threadIdx.x < 64) {  // the diagonal block and its inverse diagonal
       const int i = threadIdx.x >> 3, j = threadIdx.x & 7;
-      Lp[threadIdx.x] = (i < bw && j <= i) ? C[(size_t)(b0 + i) * ldc + b0 + j] : 0.0;
-      if (j == 0) Lp[64 + i] = i < bw ? 1.0 / C[(size_t)(b0 + i) * ldc + b0 + i] : 0.0;
+      Lp[threadIdx.x] = (i < bw && j <= i) ? C[(size_t)(b0 + i) * ld + b0 + j] : 0.0;
+      if (j == 0) Lp[64 + i] = i < bw ? 1.0 / C[(size_t)(b0 + i) * ld + b0 + i] : 0.0;
     }
     __syncthreads();
-    for (int j = threadIdx.x; j < b0 + bw; j += NT) {  // columns of the block rows
+    for (int j = threadIdx.x; j < b0 + bw; j += NT) {  // columns of the block row
       double x[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        double sacc = (j == b0 + i ? 1.0 : 0.0) + (i < bw && j < b0 ? X[(size_t)(b0 + i) * n + j] : 0.0);
+        double sacc = (j == b0 + i ? 1.0 : 0.0) - (i < bw && j < b0 ? Y[i * n + j] : 0.0);
 #pragma unroll
         for (int m = 0; m < i; ++m) sacc -= Lp[i * 8 + m] * x[m];
         x[i] = i < bw ? sacc * Lp[64 + i] : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (i < bw) X[(size_t)(b0 + i) * n + j] = (j <= b0 + i) ? x[i] : 0.0;
+        if (i < bw && j <= b0 + i) C[(size_t)(b0 + i) * ld + j] = x[i];
     }
   }
   __syncthreads();
@@ -394,7 +392,7 @@ __device__ void tri_inverse_blocked(const double* C, int n, int ldc, double* X, 
 // W = C^-1 F_cq; U = F_qq - W^T W.  Also the terminal block (nq == 0).
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
+__global__ void __launch_bounds__(NT, 1024 / NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[NT / 32];
   const ElimTask t = tasks[blockIdx.x];
@@ -427,19 +425,26 @@ __global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask
     const double* bv = A.bvals + A.blk_val_off[bid];
     for (int k = threadIdx.x; k < nb; k += NT) smap[k] = front_pos(sdofs, nc, nq, bd[k]);
     __syncthreads();
-    for (int k = (int)(threadIdx.x >> 5); k < nb; k += NT / 32) {  // warp per block row
-      const int pk = smap[k];
-      if (pk < 0) continue;
+    // warp per block row, four rows' loads in flight per lane
+    for (int k0 = (int)(threadIdx.x >> 5) * 4; k0 < nb; k0 += NT / 8) {
       for (int l = (int)(threadIdx.x & 31); l < nb; l += 32) {
         const int pl = smap[l];
-        if (pl >= 0) F[pk * nf + pl] += bv[(size_t)k * nb + l];
+        double val[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) val[u] = (k0 + u < nb && pl >= 0) ? bv[(size_t)(k0 + u) * nb + l] : 0.0;
+        if (pl < 0) continue;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k0 + u >= nb) break;
+          const int pk = smap[k0 + u];
+          if (pk >= 0) F[pk * nf + pl] += val[u];
+        }
       }
     }
     __syncthreads();
   }
-  __shared__ double Lp[72];
-  __shared__ int sflag;
-  const int st = front_chol_blocked<NT>(F, nc, nf, red, Lp, &sflag);
+  __shared__ double Lw[NT / 32 * 72];
+  const int st = front_chol_blocked<NT>(F, nc, nf, red, Lw);
   if (st != 0) {
     if (threadIdx.x == 0) A.status[blockIdx.x] = st;
     return;
@@ -459,13 +464,17 @@ __global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask
       U[e] = F[(size_t)(nc + hi) * nf + nc + lo];
     }
   }
-  double* X = t.scratch_off == -2 ? F + (size_t)nf * nf : nullptr;
-  if (X) {
-    tri_inverse_blocked<NT>(F, nc, nf, X, Lp);
+  // packed C^-1 for the solve: inverted in place (Y: the 8 x nc block-row
+  // product, after the front)
+  if (t.scratch_off == -2) {
+    tri_inverse_inplace<NT>(F, nc, nf, F + (size_t)nf * nf, Lw);
     double* P = A.fac + t.P_off;
-    for (int e = threadIdx.x; e < nc * nc; e += NT) {
-      const int i = e / nc, j = e - i * nc;
-      if (j <= i) P[(size_t)i * (i + 1) / 2 + j] = X[e];
+    for (int e = threadIdx.x; e < nc * (nc + 1) / 2; e += NT) {
+      const int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+      int ii = i;
+      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
+      while (ii * (ii + 1) / 2 > e) --ii;
+      P[e] = F[(size_t)ii * nf + (e - ii * (ii + 1) / 2)];
     }
   } else {
     tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
@@ -767,14 +776,23 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       smap[k] = (p >= 0 && salive[p]) ? p : -1;
     }
     __syncthreads();
-    for (int k = (int)(threadIdx.x >> 5); k < nb; k += NT / 32) {  // warp per block row
-      const int pk = smap[k];
-      if (pk < 0) continue;
+    // warp per block row, four rows' loads in flight per lane (each front
+    // entry still takes one add per block: same sums as one row at a time)
+    for (int k0 = (int)(threadIdx.x >> 5) * 4; k0 < nb; k0 += NT / 8) {
       for (int l = (int)(threadIdx.x & 31); l < nb; l += 32) {
         const int pl = smap[l];
+        double val[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) val[u] = (k0 + u < nb && pl >= 0 && pl < nc) ? bv[(size_t)(k0 + u) * nb + l] : 0.0;
         if (pl < 0 || pl >= nc) continue;
-        if (pk < nc) Acc[pk * nc + pl] += bv[(size_t)k * nb + l];
-        else Mq[(pk - nc) + (size_t)pl * ldq] += bv[(size_t)k * nb + l];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k0 + u >= nb) break;
+          const int pk = smap[k0 + u];
+          if (pk < 0) continue;
+          if (pk < nc) Acc[pk * nc + pl] += val[u];
+          else Mq[(pk - nc) + (size_t)pl * ldq] += val[u];
+        }
       }
     }
     __syncthreads();

@@ -537,58 +537,57 @@ __device__ __forceinline__ void warp_mma(int M, int K, const double* __restrict_
   const int mt = (M + 7) >> 3, ntr = (R + 7) >> 3, npair = mt * ntr;
   const int ar = lane >> 2, ak = lane & 3;
   const bool one_rt = NW % ntr == 0;  // every pair of this warp in RHS tile w % ntr
+  // this warp's tile pairs p = w + NW j: with one RHS tile per warp the row
+  // tile is m0 + j * dm (no division in the k loop)
+  const int nj = w < npair ? (npair - 1 - w) / NW + 1 : 0;
+  const int m0 = w / ntr, dm = NW / ntr, r0 = w - m0 * ntr;
+  auto tmj = [&](int j) { return one_rt ? m0 + j * dm : (w + NW * j) / ntr; };
+  auto trj = [&](int j) { return one_rt ? r0 : (w + NW * j) % ntr; };
   double acc[kMmaMaxJ][2];
 #pragma unroll
   for (int j = 0; j < kMmaMaxJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-  int klo = 0, khi = K;
-  if (w < npair) {
-    const int mlo = w / ntr, mhi = (w + NW * ((npair - 1 - w) / NW)) / ntr;
-    if (AM == 0) khi = min(K, 8 * mhi + 8);
-    if (AM == 1) klo = 8 * mlo;
-  } else {
-    khi = 0;
+  int klo = 0, khi = nj ? K : 0;
+  if (nj) {
+    if (AM == 0) khi = min(K, 8 * tmj(nj - 1) + 8);
+    if (AM == 1) klo = 8 * tmj(0);
   }
+  const int cfix = 8 * r0 + ar;
   for (int k0 = klo & ~3; k0 < khi; k0 += 4) {
     const int k = k0 + ak;
+    const bool kin = k < K;
     double b0 = 0.0;
-    if (one_rt) {
-      const int c = 8 * (w % ntr) + ar;
-      b0 = (k < K && c < R) ? X[k * ldx + c] : 0.0;
-    }
+    if (one_rt) b0 = (kin && cfix < R) ? X[k * ldx + cfix] : 0.0;
 #pragma unroll
     for (int j = 0; j < kMmaMaxJ; ++j) {
-      const int p = w + NW * j;
-      if (p >= npair) break;
-      const int mi = p / ntr, ri = p - mi * ntr;
+      if (j >= nj) break;
+      const int mi = tmj(j);
       if (AM == 0 && k0 >= 8 * mi + 8) continue;  // above the diagonal: zero
       if (AM == 1 && k0 + 4 <= 8 * mi) continue;  // below it (transpose): zero
       const int i = 8 * mi + ar;
-      const double a = (i < M && k < K) ? mma_a<AM>(A, lda, i, k) : 0.0;
+      const double a = (i < M && kin) ? mma_a<AM>(A, lda, i, k) : 0.0;
       double b = b0;
       if (!one_rt) {
-        const int c = 8 * ri + ar;
-        b = (k < K && c < R) ? X[k * ldx + c] : 0.0;
+        const int c = 8 * trj(j) + ar;
+        b = (kin && c < R) ? X[k * ldx + c] : 0.0;
       }
       dmma_8x8x4(acc[j][0], acc[j][1], a, b);
     }
   }
 #pragma unroll
   for (int j = 0; j < kMmaMaxJ; ++j) {
-    const int p = w + NW * j;
-    if (p >= npair) break;
-    const int mi = p / ntr, ri = p - mi * ntr;
-    const int row = 8 * mi + (lane >> 2);
+    if (j >= nj) break;
+    const int row = 8 * tmj(j) + (lane >> 2);
     if (row >= M) continue;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int col = 8 * ri + 2 * (lane & 3) + h;
+      const int col = 8 * trj(j) + 2 * (lane & 3) + h;
       if (col < R) out(row, col, acc[j][h], j, h);
     }
   }
 }
 
 // forward: s = P x_c -> v_c ; g = W^T s -> contribution rows
-__global__ void __launch_bounds__(NT) solve_elim_fwd_mma_kernel(const SolveRec* __restrict__ recs,
+__global__ void __launch_bounds__(NT, 3) solve_elim_fwd_mma_kernel(const SolveRec* __restrict__ recs,
                                                                 const int32_t* __restrict__ idx,
                                                                 const double* __restrict__ fac,
                                                                 double* __restrict__ v, int R,
@@ -642,7 +641,7 @@ __global__ void __launch_bounds__(NT) solve_elim_fwd_mma_kernel(const SolveRec* 
 }
 
 // backward: t = x_c - W x_q (in place) ; v_c = P^T t
-__global__ void __launch_bounds__(NT) solve_elim_bwd_mma_kernel(const SolveRec* __restrict__ recs,
+__global__ void __launch_bounds__(NT, 3) solve_elim_bwd_mma_kernel(const SolveRec* __restrict__ recs,
                                                                 const int32_t* __restrict__ idx,
                                                                 const double* __restrict__ fac,
                                                                 double* __restrict__ v, int R) {
@@ -677,7 +676,7 @@ __global__ void __launch_bounds__(NT) solve_elim_bwd_mma_kernel(const SolveRec* 
 }
 
 // skeleton record: sk[k] then rd[r]; T (k x r), P (r x r packed), W (r x k)
-__global__ void __launch_bounds__(NT) solve_skel_mma_kernel(const SolveRec* __restrict__ recs,
+__global__ void __launch_bounds__(NT, 3) solve_skel_mma_kernel(const SolveRec* __restrict__ recs,
                                                             const int32_t* __restrict__ idx,
                                                             const double* __restrict__ fac,
                                                             double* __restrict__ v, int R, int forward) {
