@@ -216,23 +216,63 @@ __device__ __forceinline__ void tri_tile(int tt, int& ti, int& tj) {
   tj = tt - i * (i + 1) / 2;
 }
 
+// 8 x 8 diagonal block at (p0, p0) of F (pw <= 8 rows), factored by one warp
+// in registers, lane l holding row l: right-looking with the scaling deferred
+// (a_ij -= a_ik (a_jk / a_kk) per step, then column k scaled by 1 / sqrt(a_kk)
+// -- chol_1sync's association, and no square root on the step chain).  The
+// factor goes to Lp[l*8 + j] and its inverse diagonal to Lp[64 + l].
+__device__ __forceinline__ void diag_factor_warp(const double* F, int nf, int p0, int pw, double* Lp, int& bad,
+                                                 double& dmin) {
+  const int l = threadIdx.x & 31;
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = (l < pw && j <= l) ? F[(size_t)(p0 + l) * nf + p0 + j] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (k < pw) {  // warp-uniform
+      const double akk = __shfl_sync(0xffffffffu, r[k], k);
+      if (!(akk > 0.0)) bad = 1;
+      dmin = fmin(dmin, akk);
+      const double rakk = __drcp_rn(akk);
+#pragma unroll
+      for (int j = k + 1; j < 8; ++j) {
+        const double tj = __shfl_sync(0xffffffffu, r[k], j) * rakk;
+        if (j <= l && l < pw) r[j] -= r[k] * tj;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // deferred column scaling (off the step chain)
+    const double piv = sqrt(__shfl_sync(0xffffffffu, r[k], k));
+    if (k < pw) {
+      if (l == k) r[k] = piv;
+      else if (l > k) r[k] *= __drcp_rn(piv);
+    }
+  }
+  if (l < 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) Lp[l * 8 + j] = (l < pw && j <= l) ? r[j] : 0.0;
+    Lp[64 + l] = l < pw ? __drcp_rn(r[l]) : 0.0;
+  }
+}
+
 // Blocked partial Cholesky of a front F (nf x nf, row-major, ld nf; lower
 // triangle used) over its first nc columns, 8-wide panels:
-//   * every warp factors the 8 x 8 diagonal block itself, in registers with
-//     shuffles (redundantly: no barrier and no idle warps while one warp
-//     factors), and keeps it in its own shared-memory slot;
-//   * every thread solves one row of the panel below the block;
+//   * every thread solves one row of the panel below the diagonal block;
 //   * the trailing lower triangle takes the rank-8 update as 8 x 8 FP64 DMMA
-//     tiles (mma.sync m8n8k4), spread over the warps.
-// Two barriers per panel instead of one per column.  Afterwards F holds C
-// (rows < nc), L_qc = W^T = F_qc C^-T (rows >= nc, columns < nc) and the lower
-// triangle of U = F_qq - W^T W.  Status as chol_1sync: 1 indefinite (a pivot
-// <= 0 or NaN), 2 singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
-// Lw: NT/32 slots of 72 doubles (the warp's factored block, inverse diagonal).
+//     tiles (mma.sync m8n8k4); warp 0 updates the next diagonal tile first
+//     and factors it (diag_factor_warp) while the other warps update the rest
+//     (look-ahead: the diagonal chain overlaps the trailing update).
+// Two barriers per panel.  Afterwards F holds C (rows < nc), L_qc = W^T =
+// F_qc C^-T (rows >= nc, columns < nc) and the lower triangle of U = F_qq -
+// W^T W.  Status as chol_1sync: 1 indefinite (a pivot <= 0 or NaN), 2
+// singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
+// Lw: 2 x 72 doubles (the factored diagonal block, double-buffered).
 template <int NT>
 __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double* Lw) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ int s_bad;
   if (nc == 0) return 0;
   double sc = 0.0;
   for (int i = threadIdx.x; i < nc; i += NT) sc = fmax(sc, fabs(F[(size_t)i * nf + i]));
@@ -245,42 +285,18 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
     }
     scale = block_max<NT>(s2, red);
   }
-  double* Lp = Lw + wid * 72;
-  double dmin = DBL_MAX;
+  double dmin = DBL_MAX;  // warp 0's
+  int bad = 0;
+  if (wid == 0) {
+    diag_factor_warp(F, nf, 0, min(8, nc), Lw, bad, dmin);
+    if (lane == 0) s_bad = bad;
+  }
+  __syncthreads();
+  int buf = 0;
   for (int p0 = 0; p0 < nc; p0 += 8) {
+    if (s_bad) return 1;
     const int pw = min(8, nc - p0), p1 = p0 + pw;
-    __syncthreads();  // the previous trailing update is complete
-    {
-      double r[8];
-      const int l = lane;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = (l < pw && j <= l) ? F[(size_t)(p0 + l) * nf + p0 + j] : 0.0;
-      int bad = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (k < pw) {  // warp-uniform
-          const double akk = __shfl_sync(0xffffffffu, r[k], k);
-          if (!(akk > 0.0)) bad = 1;
-          dmin = fmin(dmin, akk);
-          const double lkk = sqrt(akk);
-          const double inv = 1.0 / lkk;
-          if (l == k) r[k] = lkk;
-          else if (l > k) r[k] *= inv;
-#pragma unroll
-          for (int j = k + 1; j < 8; ++j) {
-            const double ljk = __shfl_sync(0xffffffffu, r[k], j);
-            if (j <= l && l < pw) r[j] -= r[k] * ljk;
-          }
-        }
-      }
-      if (bad) return 1;  // every warp saw the same pivots
-      if (l < 8) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) Lp[l * 8 + j] = (l < pw && j <= l) ? r[j] : 0.0;
-        Lp[64 + l] = l < pw ? 1.0 / r[l] : 0.0;  // inverse diagonal
-      }
-      __syncwarp();
-    }
+    const double* Lp = Lw + 72 * buf;
     // panel below the diagonal block: row i <- row i C_pp^-T
     for (int i = p1 + threadIdx.x; i < nf; i += NT) {
       double x[8];
@@ -299,14 +315,10 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
         if (k < pw) Fi[k] = x[k];
     }
     __syncthreads();
-    if (wid == 0 && lane < pw) {  // the factored diagonal block into place (nobody reads it this panel)
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j <= lane) F[(size_t)(p0 + lane) * nf + p0 + j] = Lp[lane * 8 + j];
-    }
-    // trailing lower triangle from p1: F[i][j] -= sum_k L[i][p0+k] L[j][p0+k]
-    const int nt = (nf - p1 + 7) / 8;
-    for (int tt = wid; tt < nt * (nt + 1) / 2; tt += NW) {
+    // trailing lower triangle from p1: F[i][j] -= sum_k L[i][p0+k] L[j][p0+k];
+    // tile 0 (the next diagonal block) by warp 0, which then factors it
+    const int nt = (nf - p1 + 7) / 8, ntt = nt * (nt + 1) / 2;
+    auto tile = [&](int tt) {
       int ti, tj;
       tri_tile(tt, ti, tj);
       const int rb = p1 + 8 * ti, cb = p1 + 8 * tj;
@@ -325,10 +337,33 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
         const int col = cb + 2 * (lane & 3) + h;
         if (row < nf && col <= row) F[(size_t)row * nf + col] -= h ? c1 : c0;
       }
+    };
+    if (wid == 0) {
+      if (lane < pw) {  // this panel's factored diagonal block into place
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j <= lane) F[(size_t)(p0 + lane) * nf + p0 + j] = Lp[lane * 8 + j];
+      }
+      if (ntt > 0) {
+        tile(0);
+        __syncwarp();
+        if (p1 < nc) {
+          diag_factor_warp(F, nf, p1, min(8, nc - p1), Lw + 72 * (buf ^ 1), bad, dmin);
+          if (lane == 0) s_bad = bad;
+        }
+      }
+      for (int tt = NW; tt < ntt; tt += NW) tile(tt);  // warp 0's share beyond tile 0
+    } else {
+      for (int tt = wid; tt < ntt; tt += NW) tile(tt);
     }
+    buf ^= 1;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) red[0] = dmin;  // warp 0 factored every diagonal block
   __syncthreads();
-  if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;  // every warp tracked every pivot
+  dmin = red[0];
+  __syncthreads();
+  if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;
   return 0;
 }
 
@@ -392,7 +427,7 @@ __device__ void tri_inverse_inplace(double* C, int n, int ld, double* Y, double*
 // W = C^-1 F_cq; U = F_qq - W^T W.  Also the terminal block (nq == 0).
 // ---------------------------------------------------------------------------
 template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
+__global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask* __restrict__ tasks, Arenas A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ double red[NT / 32];
   const ElimTask t = tasks[blockIdx.x];
@@ -406,9 +441,13 @@ __global__ void __launch_bounds__(NT, 1024 / NT) elim_small_kernel(const ElimTas
   for (int i = threadIdx.x; i < nc; i += NT) A.active[gd[i]] = 0;  // the cell retires
   for (int e = threadIdx.x; e < nf * nf; e += NT) F[e] = 0.0;
   __syncthreads();
-  for (int p = threadIdx.x; p < nc; p += NT) {
+  // A0 rows of c: eight entry slots per row, so the loads of a row's entries
+  // are in flight together (each front entry has one CSR entry: no races)
+  for (int e = threadIdx.x; e < 8 * nc; e += NT) {
+    const int p = e >> 3, slot = e & 7;
     const int g = sdofs[p];
-    for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
+    const int64_t k0 = A.indptr[g], k1 = A.indptr[g + 1];
+    for (int64_t k = k0 + slot; k < k1; k += 8) {
       const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
       if (pj < 0) continue;
       const double v = A.a0[k];
@@ -443,7 +482,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) elim_small_kernel(const ElimTas
     }
     __syncthreads();
   }
-  __shared__ double Lw[NT / 32 * 72];
+  __shared__ double Lw[2 * 72];
   const int st = front_chol_blocked<NT>(F, nc, nf, red, Lw);
   if (st != 0) {
     if (threadIdx.x == 0) A.status[blockIdx.x] = st;

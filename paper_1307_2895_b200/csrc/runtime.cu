@@ -640,6 +640,16 @@ struct PinnedXfer {
     HCK(cudaEventSynchronize(ev[0]));  // the slots may be reused by the next call at once
     HCK(cudaEventSynchronize(ev[1]));
   }
+  // Fault in the pages of a fresh pageable destination on all copy threads,
+  // one write per 4 KiB page (the caller overwrites the buffer anyway): run
+  // while the GPU still computes, the staged copy-out then meets no faults.
+  static void prefault(void* dst, size_t bytes) {
+    if (bytes < (8u << 20) || page_locked(dst)) return;
+    char* d = (char*)dst;
+    const int64_t npg = (int64_t)((bytes + 4095) / 4096);
+#pragma omp parallel for num_threads(copy_threads()) schedule(static)
+    for (int64_t i = 0; i < npg; ++i) d[(size_t)i * 4096] = 0;
+  }
   void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     int device = 0;
     HCK(cudaGetDevice(&device));
@@ -4019,6 +4029,9 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     phases(L.bwd_ph);
   }
   HCK(cudaGetLastError());
+  // host output that is not the input: fault its pages in while the sweep runs
+  if (!dev && ((const char*)x >= (const char*)b + bytes || (const char*)x + bytes <= (const char*)b))
+    PinnedXfer::prefault(x, bytes);
   if (dev) HCK(cudaMemcpyAsync(x, v, bytes, cudaMemcpyDeviceToDevice, s));
   else pinned_xfer().d2h(x, v, bytes, s);
   HCK(cudaFreeAsync(v, s));
