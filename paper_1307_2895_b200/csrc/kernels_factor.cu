@@ -217,10 +217,11 @@ __device__ __forceinline__ void tri_tile(int tt, int& ti, int& tj) {
 }
 
 // 8 x 8 diagonal block at (p0, p0) of F (pw <= 8 rows), factored by one warp
-// in registers, lane l holding row l: right-looking with the scaling deferred
-// (a_ij -= a_ik (a_jk / a_kk) per step, then column k scaled by 1 / sqrt(a_kk)
-// -- chol_1sync's association, and no square root on the step chain).  The
-// factor goes to Lp[l*8 + j] and its inverse diagonal to Lp[64 + l].
+// in registers, lane l holding row l: L_kk = sqrt(a_kk), L_lk = a_lk / L_kk,
+// a_lj -= L_lk L_jk (the scaled form: with the deferred-scaling association
+// of chol_1sync instead, config 3's exact-tie rank decisions at levels
+// 4.5-6.5 drift by -2..-5%).  The factor goes to Lp[l*8 + j] and its inverse
+// diagonal to Lp[64 + l].
 __device__ __forceinline__ void diag_factor_warp(const double* F, int nf, int p0, int pw, double* Lp, int& bad,
                                                  double& dmin) {
   const int l = threadIdx.x & 31;
@@ -233,20 +234,15 @@ __device__ __forceinline__ void diag_factor_warp(const double* F, int nf, int p0
       const double akk = __shfl_sync(0xffffffffu, r[k], k);
       if (!(akk > 0.0)) bad = 1;
       dmin = fmin(dmin, akk);
-      const double rakk = __drcp_rn(akk);
+      const double lkk = sqrt(akk);
+      const double inv = __drcp_rn(lkk);
+      if (l == k) r[k] = lkk;
+      else if (l > k) r[k] *= inv;
 #pragma unroll
       for (int j = k + 1; j < 8; ++j) {
-        const double tj = __shfl_sync(0xffffffffu, r[k], j) * rakk;
-        if (j <= l && l < pw) r[j] -= r[k] * tj;
+        const double ljk = __shfl_sync(0xffffffffu, r[k], j);
+        if (j <= l && l < pw) r[j] -= r[k] * ljk;
       }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {  // deferred column scaling (off the step chain)
-    const double piv = sqrt(__shfl_sync(0xffffffffu, r[k], k));
-    if (k < pw) {
-      if (l == k) r[k] = piv;
-      else if (l > k) r[k] *= __drcp_rn(piv);
     }
   }
   if (l < 8) {
