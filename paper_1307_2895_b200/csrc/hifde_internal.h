@@ -252,17 +252,8 @@ void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, 
 size_t pchol_smem(int nc, int G);
 int pchol_min_ctas(int nc);
 int pchol_coop_capacity(size_t smem);
-// one CTA per group, R in shared memory: groups with pchol_1cta_smem(nc) <= kSmemCapBytes
-size_t pchol_1cta_smem(int nc);
-void launch_pchol_1cta(const SkelBigTask* tasks, int ntasks, size_t smem, const Arenas& A, double eps,
-                       cudaStream_t s);
-// one cl-CTA cluster per group (cl in 2, 4, 8, 16), smem = pchol_smem(max nc, cl)
-cudaError_t launch_pchol_cluster(const SkelBigTask* tasks, int ntasks, int cl, size_t smem, const Arenas& A,
-                                 double eps, cudaStream_t s);
 cudaError_t launch_pchol_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
                               unsigned int* d_bar, size_t smem, const Arenas& A, double eps, cudaStream_t s);
-cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
-                                cudaStream_t s);
 cudaError_t launch_cpqr_coop(const SkelBigTask* tasks, int ntasks, const int* d_gstart, int nblocks,
                              unsigned int* d_bar, int max_nq, const Arenas& A, double eps, cudaStream_t s);
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,

@@ -808,213 +808,6 @@ __global__ void __launch_bounds__(256) pchol_mc_kernel(const SkelBigTask* __rest
   if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
 }
 
-// One-CTA variant for groups whose R fits in shared memory (nc <= ~158):
-// no inter-CTA barrier, one block barrier per pivot step.  Per column the
-// sums are those of pchol_mc_kernel (warp per column, lanes over l, the same
-// butterfly), and the pivot rule is the same, so the results are identical.
-__global__ void __launch_bounds__(256) pchol_1cta_kernel(const SkelBigTask* __restrict__ tasks, Arenas A,
-                                                         double eps) {
-  extern __shared__ __align__(16) double psm[];
-  __shared__ double wbest[2][8];
-  __shared__ int widx[2][8];
-  const SkelBigTask t = tasks[blockIdx.x];
-  const int nc = t.nc, nq = t.nq;
-  const BigWs w = big_ws(t, A);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* Rs = psm;                   // R(l, j) at l * nc + j
-  double* dd = Rs + (size_t)nc * nc;  // Schur diagonal (< 0: pivoted)
-  for (int j = threadIdx.x; j < nc; j += 256) dd[j] = w.G[(size_t)j + (size_t)j * nc];
-  __syncthreads();
-  // warp-level best of this warp's columns (c = wid, wid + 8, ...) -> slot
-  auto post = [&](int slot) {
-    double bv = -1.0;
-    int bi = nc;
-    for (int j = wid + 8 * lane; j < nc; j += 256)
-      if (dd[j] > bv) { bv = dd[j]; bi = j; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) { wbest[slot][wid] = bv; widx[slot][wid] = bi; }
-  };
-  post(0);
-  __syncthreads();
-  double thr = 0.0;
-  int k = nc;
-  for (int i = 0; i < nc; ++i) {
-    const int slot = i & 1;
-    double dP = wbest[slot][0];
-    int P = widx[slot][0];
-    for (int q = 1; q < 8; ++q)
-      if (wbest[slot][q] > dP || (wbest[slot][q] == dP && widx[slot][q] < P)) { dP = wbest[slot][q]; P = widx[slot][q]; }
-    if (i == 0 && !(dP > 0.0)) { k = 0; break; }
-    const double rii = sqrt(dP > 0.0 ? dP : 0.0);
-    if (i == 0) thr = eps * rii;
-    if (rii <= thr || P >= nc) { k = i; break; }
-    if (threadIdx.x == 0) {
-      w.rdiag[i] = rii;
-      w.piv[i] = P;
-    }
-    const double inv = 1.0 / rii;
-    // columns of warp wid: j = wid, wid + 8, ... (the post() ownership)
-    for (int j = wid; j < nc; j += 8) {
-      if (dd[j] < 0.0) continue;
-      if (j == P) {
-        __syncwarp();
-        if (lane == 0) dd[j] = -1.0;
-        continue;
-      }
-      double sacc = 0.0;
-      for (int l = lane; l < i; l += 32) sacc += Rs[(size_t)l * nc + P] * Rs[(size_t)l * nc + j];
-      sacc = warp_sum(sacc);
-      const double rij = (__ldg(w.G + (size_t)j + (size_t)P * nc) - sacc) * inv;
-      __syncwarp();
-      if (lane == 0) {
-        Rs[(size_t)i * nc + j] = rij;
-        w.Mq[(size_t)i + (size_t)j * nq] = rij;
-        const double nd = dd[j] - rij * rij;
-        dd[j] = nd > 0.0 ? nd : 0.0;
-      }
-      __syncwarp();
-    }
-    post(slot ^ 1);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) A.kout[t.group] = k;
-}
-
-size_t pchol_1cta_smem(int nc) { return sizeof(double) * ((size_t)nc * nc + (size_t)nc); }
-
-void launch_pchol_1cta(const SkelBigTask* tasks, int ntasks, size_t smem, const Arenas& A, double eps,
-                       cudaStream_t s) {
-  if (ntasks <= 0) return;
-  static bool once = (cudaFuncSetAttribute(pchol_1cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kSmemCapBytes),
-                      true);
-  (void)once;
-  pchol_1cta_kernel<<<ntasks, 256, smem, s>>>(tasks, A, eps);
-}
-
-// Cluster variant: one CL-CTA cluster per group.  Candidates are exchanged
-// through distributed shared memory and the pivot column's R rows are read
-// from its owner's shared memory; one hardware cluster barrier per step.
-template <int CL>
-__global__ void __launch_bounds__(256) pchol_cl_kernel(const SkelBigTask* __restrict__ tasks, Arenas A, double eps) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ __align__(16) double psm[];
-  __shared__ double cand_v[2];
-  __shared__ int cand_i[2];
-  __shared__ double wbest[8];
-  __shared__ int widx[8];
-  __shared__ double sh_best;
-  __shared__ int sh_pvt;
-  const int rb = (int)cl.block_rank();
-  const int tix = (int)blockIdx.x / CL;
-  const SkelBigTask t = tasks[tix];
-  const int nc = t.nc, nq = t.nq;
-  const BigWs w = big_ws(t, A);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  auto nown_of = [&](int r) { return r < nc ? (nc - r + CL - 1) / CL : 0; };
-  const int nown = nown_of(rb);
-  double* Rs = psm;
-  double* rp = Rs + (size_t)nc * nown;
-  double* dd = rp + nc;
-  for (int c = threadIdx.x; c < nown; c += 256) {
-    const int j = rb + c * CL;
-    dd[c] = w.G[(size_t)j + (size_t)j * nc];
-  }
-  __syncthreads();
-  auto post = [&](int slot) {
-    double bv = -1.0;
-    int bi = nc;
-    for (int c = threadIdx.x; c < nown; c += 256)
-      if (dd[c] > bv) { bv = dd[c]; bi = rb + c * CL; }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) { wbest[wid] = bv; widx[wid] = bi; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b2 = wbest[0];
-      int i2 = widx[0];
-      for (int q = 1; q < 8; ++q)
-        if (wbest[q] > b2 || (wbest[q] == b2 && widx[q] < i2)) { b2 = wbest[q]; i2 = widx[q]; }
-      cand_v[slot] = b2;
-      cand_i[slot] = i2;
-    }
-  };
-  post(0);
-  cl.sync();
-  double thr = 0.0;
-  int k = nc;
-  for (int i = 0; i < nc; ++i) {
-    const int slot = i & 1;
-    if (wid == 0) {
-      double bv = -1.0;
-      int bi = nc;
-      if (lane < CL) {
-        bv = cl.map_shared_rank(cand_v, lane)[slot];
-        bi = cl.map_shared_rank(cand_i, lane)[slot];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-      if (lane == 0) { sh_best = bv; sh_pvt = bi; }
-    }
-    __syncthreads();
-    const int P = sh_pvt;
-    const double dP = sh_best;
-    if (i == 0 && !(dP > 0.0)) { k = 0; break; }
-    const double rii = sqrt(dP > 0.0 ? dP : 0.0);
-    if (i == 0) thr = eps * rii;
-    if (rii <= thr || P >= nc) { k = i; break; }
-    if (rb == 0 && threadIdx.x == 0) {
-      w.rdiag[i] = rii;
-      w.piv[i] = P;
-    }
-    {  // R(0..i-1, P) from the owner's shared memory
-      const int owner = P % CL, cP = P / CL, no = nown_of(owner);
-      const double* Ro = cl.map_shared_rank(Rs, owner);
-      for (int l = threadIdx.x; l < i; l += 256) rp[l] = Ro[(size_t)l * no + cP];
-    }
-    __syncthreads();
-    const double inv = 1.0 / rii;
-    for (int c = wid; c < nown; c += 8) {
-      const int j = rb + c * CL;
-      if (dd[c] < 0.0) continue;
-      if (j == P) {
-        __syncwarp();
-        if (lane == 0) dd[c] = -1.0;
-        continue;
-      }
-      double sacc = 0.0;
-      for (int l = lane; l < i; l += 32) sacc += rp[l] * Rs[(size_t)l * nown + c];
-      sacc = warp_sum(sacc);
-      const double rij = (__ldg(w.G + (size_t)j + (size_t)P * nc) - sacc) * inv;
-      __syncwarp();
-      if (lane == 0) {
-        Rs[(size_t)i * nown + c] = rij;
-        w.Mq[(size_t)i + (size_t)j * nq] = rij;
-        const double nd = dd[c] - rij * rij;
-        dd[c] = nd > 0.0 ? nd : 0.0;
-      }
-    }
-    __syncthreads();
-    post(slot ^ 1);
-    cl.sync();
-  }
-  if (rb == 0 && threadIdx.x == 0) A.kout[t.group] = k;
-  cl.sync();  // peers may still read this CTA's shared memory
-}
 
 // ---------------------------------------------------------------------------
 // sk / rd ascending, output lists, inner elimination task (one CTA per group)
@@ -1410,68 +1203,6 @@ cudaError_t launch_pchol_coop(const SkelBigTask* tasks, int ntasks, const int* d
                                      s);
 }
 
-template <int CL>
-static cudaError_t launch_pchol_cl_t(const SkelBigTask* tasks, int ntasks, size_t smem, const Arenas& A, double eps,
-                                     cudaStream_t s) {
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(pchol_cl_kernel<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(pchol_cl_kernel<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
-    once = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3((unsigned)(ntasks * CL), 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, pchol_cl_kernel<CL>, tasks, A, eps);
-}
-
-cudaError_t launch_pchol_cluster(const SkelBigTask* tasks, int ntasks, int cl, size_t smem, const Arenas& A,
-                                 double eps, cudaStream_t s) {
-  if (ntasks <= 0) return cudaSuccess;
-  switch (cl) {
-    case 2: return launch_pchol_cl_t<2>(tasks, ntasks, smem, A, eps, s);
-    case 4: return launch_pchol_cl_t<4>(tasks, ntasks, smem, A, eps, s);
-    case 8: return launch_pchol_cl_t<8>(tasks, ntasks, smem, A, eps, s);
-    case 16: return launch_pchol_cl_t<16>(tasks, ntasks, smem, A, eps, s);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-cudaError_t launch_cpqr_cluster(const SkelBigTask* tasks, int ntasks, int max_nq, const Arenas& A, double eps,
-                                cudaStream_t s) {
-  if (ntasks <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (size_t)max_nq;
-  static bool once = false;
-  if (!once) {
-    cudaFuncSetAttribute(cpqr_mc_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(cpqr_mc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
-    once = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kCL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.gridDim = dim3((unsigned)(ntasks * kCL), 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const int* gnull = nullptr;
-  unsigned int* bnull = nullptr;
-  return cudaLaunchKernelEx(&cfg, cpqr_mc_kernel<true>, tasks, ntasks, gnull, bnull, A, eps);
-}
 
 void launch_skelbig_sort(const SkelBigTask* tasks, int ntasks, const Arenas& A, ElimTask* inner, double* dmin,
                          double* dscale, cudaStream_t s) {

@@ -926,8 +926,6 @@ struct Factorizer {
   cudaEvent_t ev_id = nullptr, ev_tail = nullptr;
   bool tail_pending = false;
   cudaStream_t tail_stream() {
-    static const bool off = getenv("HIFDE_NO_TAIL_STREAM") != nullptr;
-    if (off) return s;
     if (!tail_s) {
       HCK(cudaStreamCreateWithFlags(&tail_s, cudaStreamNonBlocking));
       HCK(cudaEventCreateWithFlags(&ev_id, cudaEventDisableTiming));
@@ -1755,7 +1753,7 @@ struct Factorizer {
     };
     std::vector<Sz> sz((size_t)nt);
     std::vector<uint8_t> promote((size_t)nt, 0);
-    static const double promote_work = getenv("HIFDE_PROMOTE_WORK") ? atof(getenv("HIFDE_PROMOTE_WORK")) : kPromoteWork;
+    const double promote_work = kPromoteWork;
     std::vector<std::vector<int32_t>> tpred((size_t)nthreads);
     const int nthr = nt >= 256 ? nthreads : 1;
 #pragma omp parallel num_threads(nthr)
@@ -1877,24 +1875,6 @@ struct Factorizer {
       nbatch = 1;
     }
     L.nbatches = nbatch;
-    if (getenv("HIFDE_BIGSHAPES")) {  // debug: workspace modes and shapes of the level's groups
-      int64_t cnt[4] = {0, 0, 0, 0}, mnc[4] = {0, 0, 0, 0}, mnq[4] = {0, 0, 0, 0};
-      double snc[4] = {0, 0, 0, 0}, snq[4] = {0, 0, 0, 0};
-      for (const SkelTask& T : tasks) {
-        const int md = T.mode & 3;
-        ++cnt[md];
-        mnc[md] = std::max<int64_t>(mnc[md], T.nc);
-        mnq[md] = std::max<int64_t>(mnq[md], T.nq);
-        snc[md] += T.nc;
-        snq[md] += T.nq;
-      }
-      fprintf(stderr, "[hifde] tag %.3f modes:", tag);
-      for (int md = 0; md < 4; ++md)
-        if (cnt[md])
-          fprintf(stderr, " m%d n=%lld nc(avg %.0f max %lld) nq(avg %.0f max %lld)", md, (long long)cnt[md],
-                  snc[md] / cnt[md], (long long)mnc[md], snq[md] / cnt[md], (long long)mnq[md]);
-      fprintf(stderr, "\n");
-    }
     L.lap("tasks");
     HTRACE("  symbolic done, %d batches", nbatch);
     double tp = now_s();
@@ -1904,8 +1884,7 @@ struct Factorizer {
     // 3D: an exact level of medium groups alone also takes the pipeline (its
     // batches beat one chained launch of one-CTA groups: config 4 247 -> 216
     // ms GPU); in 2D the one-launch chain stays faster
-    static const int promote_env = getenv("HIFDE_PROMOTE_ANY") ? atoi(getenv("HIFDE_PROMOTE_ANY")) : -1;
-    const bool promote_any = promote_env >= 0 ? promote_env != 0 : g.dim == 3;  // per grid, not per process
+    const bool promote_any = g.dim == 3;  // per grid, not per process
     // (a level whose largest medium group is small keeps the one-launch
     // chain: config 5's level 1.333, nq nc^2 <= 1.3e6, is faster chained)
     bool any_promote = false, big_promote = false;
@@ -1969,7 +1948,7 @@ struct Factorizer {
       // kernel's throughput wins)
       size_t smem_cl = 0;
       int cs = 0, ncls = 0;
-      bool cluster_ok = max_nc >= kClusterMinNc && !getenv("HIFDE_NO_CLUSTER");
+      bool cluster_ok = max_nc >= kClusterMinNc;
       for (int csz : {4, 2}) {
         if (!cluster_ok) break;
         size_t need_max = 0;
@@ -1982,9 +1961,7 @@ struct Factorizer {
         }
         if (!fits) continue;
         const int capc = skel_cluster_capacity(need_max, csz);
-        const char* cf = getenv("HIFDE_CLUSTER_LOAD");  // groups per resident cluster allowed (study)
-        const double load = cf ? atof(cf) : 1.0;
-        if (capc >= 1 && (double)nt <= load * capc) {
+        if (capc >= 1 && nt <= capc) {
           cs = csz;
           ncls = (int)std::min<int64_t>(nt, capc);
           smem_cl = need_max;
@@ -2023,7 +2000,7 @@ struct Factorizer {
         ddone.release(s);
         return;
       }
-      const int nthr = (max_nc > 32 || max_nq > 128 || getenv("HIFDE_SKEL512")) ? 512 : 128;
+      const int nthr = (max_nc > 32 || max_nq > 128) ? 512 : 128;
       const int cap = skel_ordered_capacity(smem, nthr);
       if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
       const int grid = (int)std::min<int64_t>(nt, cap);
@@ -2074,20 +2051,9 @@ struct Factorizer {
     for (int64_t t = 0; t < nt; ++t) order[(size_t)t] = t;
     // (then by owner: a batch's groups are independent, each rank takes a
     // contiguous range)
-    // (and, among the large groups, those whose pivoted Cholesky fits one
-    // CTA first: launch_huge_batch runs them one CTA each)
-    // (the flag only matters for the opt-in one-CTA pivoted Cholesky)
-    static const bool one_cta_env = getenv("HIFDE_PCHOL_1CTA") && atoi(getenv("HIFDE_PCHOL_1CTA")) != 0;
-    std::vector<uint8_t> one_cta_grp((size_t)nt, 0);
-    if (one_cta_env)
-      for (int64_t t = 0; t < nt; ++t) {
-        const SkelTask& T = tasks[(size_t)t];
-        one_cta_grp[(size_t)t] = T.mode == 2 && gram_ok(T.nc, T.nq) && pchol_1cta_smem(T.nc) <= kSmemCapBytes;
-      }
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       if (batch[(size_t)a] != batch[(size_t)b]) return batch[(size_t)a] < batch[(size_t)b];
-      if (own_[(size_t)a] != own_[(size_t)b]) return own_[(size_t)a] < own_[(size_t)b];
-      return one_cta_grp[(size_t)a] > one_cta_grp[(size_t)b];
+      return own_[(size_t)a] < own_[(size_t)b];
     });
     const int PP = sharded() ? P : 1;
     // per batch and rank: small groups (one CTA each) and large groups
@@ -2211,35 +2177,9 @@ struct Factorizer {
       for (int r = rank_lo(); r < rank_hi(); ++r) {
         const int64_t hlo = bh[b0 + r], hhi = bh[b0 + r + 1];
         if (hhi <= hlo) continue;
-        static const bool shapes = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: per-batch shapes and time
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (shapes) {
-          HCK(cudaEventCreate(&e0));
-          HCK(cudaEventCreate(&e1));
-          HCK(cudaEventRecord(e0, s));
-        }
         if (kl_huge < 0) kl_huge = F->klog.begin("skel_large_pipeline", tag, 0, 0, 0, s);
         launch_huge_batch(huge, hlo, hhi, dhuge.p, dinner.p, ddmin.p, dscale.p, arenas_r(r, false),
                           arenas_r(r, true), huge_max_nq, huge_max_nf, huge_max_nb, hl);
-        if (shapes) {
-          HCK(cudaEventRecord(e1, s));
-          std::vector<int32_t> kk((size_t)nt);
-          HCK(cudaMemcpyAsync(kk.data(), kout.p, nt * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-          HCK(cudaStreamSynchronize(s));
-          float ms = 0.f;
-          cudaEventElapsedTime(&ms, e0, e1);
-          double trf = 0;
-          fprintf(stderr, "[hifde] tag %.3f batch %d: %lld large groups, %.3f ms:", tag, b, (long long)(hhi - hlo), ms);
-          for (int64_t i = hlo; i < hhi; ++i) {
-            const SkelBigTask& H = huge[(size_t)i];
-            const int k = kk[(size_t)H.group];
-            fprintf(stderr, " (%d,%d,k%d)", H.nc, H.nq, k);
-            for (int st = 0; st < k; ++st) trf += 24.0 * H.nq * (H.nc - st);
-          }
-          fprintf(stderr, " | cpqr-traffic %.2f GB\n", trf * 1e-9);
-          cudaEventDestroy(e0);
-          cudaEventDestroy(e1);
-        }
       }
       // the large groups retire their rd once every rank's pipeline is done
       for (int r = rank_lo(); r < rank_hi(); ++r) {
@@ -2377,9 +2317,7 @@ struct Factorizer {
   // Large groups whose ID goes through the Gram matrix (kernels_skelbig.cu):
   // loose tolerances only (u / eps^2 << eps, kGramMinEps), tall fronts, R columns in shared memory
   bool gram_ok(int nc, int nq) const {
-    static const bool off = getenv("HIFDE_NO_GRAM") != nullptr;
-    static const double min_eps = getenv("HIFDE_GRAM_MIN_EPS") ? atof(getenv("HIFDE_GRAM_MIN_EPS")) : kGramMinEps;
-    return !off && opt.eps >= min_eps && nq >= 2 * nc && nc <= 1024 && pchol_min_ctas(nc) > 0;
+    return opt.eps >= kGramMinEps && nq >= 2 * nc && nc <= 1024 && pchol_min_ctas(nc) > 0;
   }
 
   // Large-group skeletonization pipeline for huge[lo, hi) (one exact-order batch).
@@ -2484,13 +2422,7 @@ struct Factorizer {
       dm.release(s);
     }
     const size_t smem_asm = align16(sizeof(int32_t) * (size_t)(2 * max_nf));  // front DOFs + alive flags
-    static const bool split_t = getenv("HIFDE_BIGSHAPES") != nullptr;  // debug: phase times
-    cudaEvent_t pe[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (split_t) for (auto& e : pe) HCK(cudaEventCreate(&e));
-    if (split_t) HCK(cudaEventRecord(pe[0], s));
     launch_skelbig_assemble(dtk, d1.p, (int)wasm.size(), A, smem_asm, s);
-    if (split_t) HCK(cudaEventRecord(pe[1], s));
-    static const int cl_min = getenv("HIFDE_CPQR_CLUSTER_MIN") ? atoi(getenv("HIFDE_CPQR_CLUSTER_MIN")) : 1 << 30;
     bool gram = true;
     for (int i = 0; i < n && gram; ++i) gram = gram_ok(huge[(size_t)(lo + i)].nc, huge[(size_t)(lo + i)].nq);
     if (gram) {
@@ -2514,40 +2446,7 @@ struct Factorizer {
       if (!wr.empty()) gpart.reserve(wg.size() * 4096, s);
       launch_skelbig_gram(dtk, dg.p, (int)wg.size(), dr.p, (int)wr.size(), gpart.p, A, s);
       g_launches += wr.empty() ? 1 : 2;
-      // HIFDE_PCHOL_CL = 2/4/8/16 (or -1: smallest fitting >= 4): one cluster
-      // per group, DSMEM candidates and hardware cluster barriers.  Measured
-      // within +-3% of the cooperative path on configs 4 and 5, which stays
-      // the default (0).
-      static const int cl_env = getenv("HIFDE_PCHOL_CL") ? atoi(getenv("HIFDE_PCHOL_CL")) : 0;
-      int maxnc = 0;
-      for (int i = 0; i < n; ++i) maxnc = std::max(maxnc, huge[(size_t)(lo + i)].nc);
-      int clz = 0;
-      if (cl_env != 0)
-        for (int c : {2, 4, 8, 16}) {
-          if (cl_env > 0 && c != cl_env) continue;
-          if (c < (cl_env > 0 ? 2 : 4)) continue;
-          if (pchol_smem(maxnc, c) <= kSmemCapBytes) { clz = c; break; }
-        }
-      // every group's R fits one CTA's shared memory: one CTA per group, no
-      // inter-CTA barriers (HIFDE_PCHOL_1CTA=0 turns it off)
-      // (opt-in, HIFDE_PCHOL_1CTA=1: measured slower on config 5 -- 490 -> 569
-      // ms GPU -- and neutral on config 4; the cooperative kernel spreads each
-      // step's column updates over more SMs)
-      static const bool one_cta_ok = getenv("HIFDE_PCHOL_1CTA") && atoi(getenv("HIFDE_PCHOL_1CTA")) != 0;
-      int n1 = 0, nc1 = 0;  // the leading groups that fit one CTA (sorted first)
-      while (one_cta_ok && clz == 0 && n1 < n && pchol_1cta_smem(huge[(size_t)(lo + n1)].nc) <= kSmemCapBytes) {
-        nc1 = std::max(nc1, huge[(size_t)(lo + n1)].nc);
-        ++n1;
-      }
-      if (n1 > 0) {
-        launch_pchol_1cta(dtk, n1, pchol_1cta_smem(nc1), A, opt.eps, s);
-        ++g_launches;
-      }
-      int c0 = clz ? n : n1;
-      if (clz) {
-        HCK(launch_pchol_cluster(dtk, n, clz, pchol_smem(maxnc, clz), A, opt.eps, s));
-        ++g_launches;
-      }
+      int c0 = 0;
       while (c0 < n) {
         size_t smem0 = 0;
         int cn = 0, need = 0;
@@ -2569,8 +2468,7 @@ struct Factorizer {
           const int nc = huge[(size_t)(lo + c0 + i)].nc;
           const int gm = pchol_min_ctas(nc);
           const int extra = (int)((double)(cap - need) * ((double)nc * nc) / std::max(tot, 1.0));
-          static const int maxg = getenv("HIFDE_PCHOL_MAXG") ? atoi(getenv("HIFDE_PCHOL_MAXG")) : kMaxG;
-          const int g = std::max(gm, std::min({gm + extra, nc, maxg}));
+          const int g = std::max(gm, std::min({gm + extra, nc, kMaxG}));
           gs[(size_t)i + 1] = gs[(size_t)i] + g;
           smem = std::max(smem, pchol_smem(nc, g));
         }
@@ -2588,10 +2486,6 @@ struct Factorizer {
       }
       dg.release(s);
       dr.release(s);
-    } else if (n >= cl_min) {
-      // many groups: 16-CTA clusters per group, scheduled in waves
-      HCK(launch_cpqr_cluster(dtk, n, max_nq, A, opt.eps, s));
-      ++g_launches;
     } else {
       // few groups (exact-order batches): all SMs, split over the groups in
       // proportion to their work (nq * nc), at most one CTA per column; more
@@ -2625,7 +2519,6 @@ struct Factorizer {
         dbar.release(s);
       }
     }
-    if (split_t) HCK(cudaEventRecord(pe[2], s));
     launch_skelbig_sort(dtk, n, AH, inner, dmin, dscale, s);
     // the tail: on the tail stream once the ID, the sort and this batch's
     // uploads (all on the main stream) are done
@@ -2663,17 +2556,6 @@ struct Factorizer {
     if (trace_on()) { HCK(cudaStreamSynchronize(ts)); HTRACE("    huge: inverse done (%zu loc / %zu diag / %zu tiles)", inv.loc.size(), inv.diag.size(), inv.tiles.size()); }
     g_launches += 2;
     HCK(cudaGetLastError());
-    if (split_t) {
-      join_tails();
-      HCK(cudaEventRecord(pe[3], s));
-      HCK(cudaStreamSynchronize(s));
-      float t01 = 0.f, t12 = 0.f, t23 = 0.f;
-      cudaEventElapsedTime(&t01, pe[0], pe[1]);
-      cudaEventElapsedTime(&t12, pe[1], pe[2]);
-      cudaEventElapsedTime(&t23, pe[2], pe[3]);
-      fprintf(stderr, "[hifde]   assemble %.3f cpqr %.3f rest %.3f ms\n", t01, t12, t23);
-      for (auto& e : pe) cudaEventDestroy(e);
-    }
     d1.release(s);
     for (auto* d : {&d2, &d3, &d4, &d5, &d6, &d7, &d8, &d10, &d11}) d->release(ts);  // tail-stream order
     inv.release(ts);
@@ -3593,8 +3475,7 @@ struct Factorizer {
       // the first kernel launch, a0_ready())
       int dev = 0;
       HCK(cudaGetDevice(&dev));
-      static const size_t pin_min = getenv("HIFDE_A0_PIN_MB") ? (size_t)atoi(getenv("HIFDE_A0_PIN_MB")) << 20
-                                                              : (size_t)1 << 20;
+      const size_t pin_min = (size_t)1 << 20;
       const bool big = (size_t)nnz * 12 > pin_min;  // large inputs: pinned staging
       a0_job = helper.post([=]() {
         cudaError_t e = cudaSetDevice(dev);
@@ -3926,10 +3807,8 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
   // fine elimination levels: the single-load-phase kernels
   static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
-  static const int small_max_rhs = getenv("HIFDE_SOLVE_SMALL_RHS") ? atoi(getenv("HIFDE_SOLVE_SMALL_RHS")) : 64;
-  static const int small_max_n = getenv("HIFDE_SOLVE_SMALL_N") ? atoi(getenv("HIFDE_SOLVE_SMALL_N")) : 96;
-  static const size_t small_max_smem = getenv("HIFDE_SOLVE_SMALL_SMEM") ? (size_t)atoi(getenv("HIFDE_SOLVE_SMALL_SMEM")) * 1024
-                                                                          : (size_t)200 * 1024;
+  constexpr int small_max_rhs = 64, small_max_n = 96;
+  constexpr size_t small_max_smem = (size_t)200 * 1024;
   auto small_path = [&](const LevelRec& L) {
     return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
            L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
