@@ -650,6 +650,44 @@ struct PinnedXfer {
 #pragma omp parallel for num_threads(copy_threads()) schedule(static)
     for (int64_t i = 0; i < npg; ++i) d[(size_t)i * 4096] = 0;
   }
+  // Column chunks c (device blocks vb[c], N x (c0[c+1] - c0[c]) row-major)
+  // into the columns [c0[c], c0[c+1]) of the host block x (N x nrhs), each
+  // after its event es[c]: row pieces through the two pinned slots, the
+  // host threads scattering one piece while the next one's DMA runs.
+  void d2h_columns(double* x, int nrhs, const std::vector<double*>& vb, const std::vector<int>& c0, int64_t N,
+                   const std::vector<cudaEvent_t>& es, cudaStream_t s) {
+    int device = 0;
+    HCK(cudaGetDevice(&device));
+    std::lock_guard<std::mutex> lk(m);
+    if (!ready(device)) throw Fail{HIFDE_CUDA, "pinned staging buffers unavailable"};
+    struct Piece { int c; int64_t r0, r1; };
+    std::vector<Piece> pcs;
+    for (size_t c = 0; c + 1 < c0.size(); ++c) {
+      const int w = c0[c + 1] - c0[c];
+      const int64_t rows = std::max<int64_t>(1, (int64_t)(kChunk / ((size_t)w * sizeof(double))));
+      for (int64_t r0 = 0; r0 < N; r0 += rows) pcs.push_back(Piece{(int)c, r0, std::min(N, r0 + rows)});
+    }
+    auto issue = [&](size_t k) {
+      const Piece& P = pcs[k];
+      const int w = c0[(size_t)P.c + 1] - c0[(size_t)P.c];
+      if (k == 0 || pcs[k - 1].c != P.c) HCK(cudaStreamWaitEvent(s, es[(size_t)P.c], 0));
+      HCK(cudaMemcpyAsync(buf[k & 1], vb[(size_t)P.c] + P.r0 * w, (size_t)(P.r1 - P.r0) * w * sizeof(double),
+                          cudaMemcpyDeviceToHost, s));
+      HCK(cudaEventRecord(ev[k & 1], s));
+    };
+    issue(0);
+    for (size_t k = 0; k < pcs.size(); ++k) {
+      HCK(cudaEventSynchronize(ev[k & 1]));
+      if (k + 1 < pcs.size()) issue(k + 1);
+      const Piece& P = pcs[k];
+      const int w = c0[(size_t)P.c + 1] - c0[(size_t)P.c], col = c0[(size_t)P.c];
+      const double* src = (const double*)buf[k & 1];
+      const int64_t nr = P.r1 - P.r0;
+#pragma omp parallel for num_threads(copy_threads()) schedule(static)
+      for (int64_t i = 0; i < nr; ++i)
+        std::memcpy(x + (size_t)(P.r0 + i) * nrhs + col, src + (size_t)i * w, (size_t)w * sizeof(double));
+    }
+  }
   void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     int device = 0;
     HCK(cudaGetDevice(&device));
@@ -3778,13 +3816,8 @@ struct Factorizer {
 // ---------------------------------------------------------------------------
 // Solve sweep
 // ---------------------------------------------------------------------------
-void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, bool dev, cudaStream_t s) {
-  const int64_t N = F->n;
-  const size_t bytes = (size_t)N * nrhs * sizeof(double);
-  double* v = nullptr;
-  HCK(cudaMallocAsync((void**)&v, std::max<size_t>(bytes, 8), s));
-  if (dev) HCK(cudaMemcpyAsync(v, b, bytes, cudaMemcpyDeviceToDevice, s));
-  else pinned_xfer().h2d(v, b, bytes, s);
+// The up/down sweep on the device block v (N x nrhs row-major, in place).
+void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
   double* contrib = nullptr;
   HCK(cudaMallocAsync((void**)&contrib, std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
   double* tscr = nullptr;
@@ -3828,11 +3861,6 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
   const size_t nl = F->levels.size();
   // kernel log: one entry per level and direction; algorithmic bytes = the
   // level's factor entries + one read and one write of every touched row
-  std::unique_lock<std::mutex> klk(F->klog_m, std::defer_lock);
-  if (F->klog.on) {
-    klk.lock();
-    F->klog.clear(1);
-  }
   auto kbegin = [&](const LevelRec& L, bool fwd) {
     if (!F->klog.on || (L.nall == 0 && L.recs.empty())) return -1;
     const char* nm = L.kind == 1 ? (fwd ? "solve_skel_fwd" : "solve_skel_bwd")
@@ -3908,17 +3936,90 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     phases(L.bwd_ph);
   }
   HCK(cudaGetLastError());
-  // host output that is not the input: fault its pages in while the sweep runs
-  if (!dev && ((const char*)x >= (const char*)b + bytes || (const char*)x + bytes <= (const char*)b))
-    PinnedXfer::prefault(x, bytes);
-  if (dev) HCK(cudaMemcpyAsync(x, v, bytes, cudaMemcpyDeviceToDevice, s));
-  else pinned_xfer().d2h(x, v, bytes, s);
-  HCK(cudaFreeAsync(v, s));
   HCK(cudaFreeAsync(contrib, s));
   HCK(cudaFreeAsync(tscr, s));
   HCK(cudaFreeAsync(scratch, s));
+}
+
+// Host right-hand sides already page-locked (a pinned torch tensor, ...) and a
+// large block: column chunks flow through three engines at once -- the H2D
+// copy engine uploads chunk c + 1 (a strided 2D DMA straight from the
+// caller's rows) while the SMs sweep chunk c and the D2H engine returns chunk
+// c - 1 through pinned pieces that host threads scatter into the caller's
+// columns.  Same result as one sweep of the whole block, column by column.
+void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nrhs, cudaStream_t s) {
+  const int64_t N = F->n;
+  const int nch = nrhs >= 64 ? 4 : 2;
+  std::vector<int> c0((size_t)nch + 1, 0);
+  for (int c = 0; c < nch; ++c) c0[(size_t)c + 1] = (int)((int64_t)nrhs * (c + 1) / nch / 8 * 8);
+  c0[(size_t)nch] = nrhs;
+  int wmax = 0;
+  for (int c = 0; c < nch; ++c) wmax = std::max(wmax, c0[(size_t)c + 1] - c0[(size_t)c]);
+  cudaStream_t sh = nullptr, sd = nullptr;
+  HCK(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking));
+  HCK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> eh((size_t)nch), es((size_t)nch);
+  for (int c = 0; c < nch; ++c) {
+    HCK(cudaEventCreateWithFlags(&eh[(size_t)c], cudaEventDisableTiming));
+    HCK(cudaEventCreateWithFlags(&es[(size_t)c], cudaEventDisableTiming));
+  }
+  std::vector<double*> vb((size_t)nch, nullptr);
+  for (int c = 0; c < nch; ++c)
+    HCK(cudaMallocAsync((void**)&vb[(size_t)c], (size_t)N * (c0[(size_t)c + 1] - c0[(size_t)c]) * sizeof(double), s));
+  cudaEvent_t ealloc = nullptr;
+  HCK(cudaEventCreateWithFlags(&ealloc, cudaEventDisableTiming));
+  HCK(cudaEventRecord(ealloc, s));
+  HCK(cudaStreamWaitEvent(sh, ealloc, 0));
+  for (int c = 0; c < nch; ++c) {  // every upload and sweep queued at once
+    const int w = c0[(size_t)c + 1] - c0[(size_t)c];
+    HCK(cudaMemcpy2DAsync(vb[(size_t)c], (size_t)w * sizeof(double), b + c0[(size_t)c], (size_t)nrhs * sizeof(double),
+                          (size_t)w * sizeof(double), (size_t)N, cudaMemcpyHostToDevice, sh));
+    HCK(cudaEventRecord(eh[(size_t)c], sh));
+    HCK(cudaStreamWaitEvent(s, eh[(size_t)c], 0));
+    solve_sweep(F, vb[(size_t)c], w, s);
+    HCK(cudaEventRecord(es[(size_t)c], s));
+  }
+  const size_t total = (size_t)N * nrhs * sizeof(double);
+  PinnedXfer::prefault(x, total);  // while the first chunks upload and sweep
+  pinned_xfer().d2h_columns(x, nrhs, vb, c0, N, es, sd);
+  for (int c = 0; c < nch; ++c) HCK(cudaFreeAsync(vb[(size_t)c], sd));
+  HCK(cudaStreamSynchronize(sd));
+  for (int c = 0; c < nch; ++c) {
+    cudaEventDestroy(eh[(size_t)c]);
+    cudaEventDestroy(es[(size_t)c]);
+  }
+  cudaEventDestroy(ealloc);
+  HCK(cudaStreamSynchronize(s));
+  cudaStreamDestroy(sh);
+  cudaStreamDestroy(sd);
+}
+
+void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, bool dev, cudaStream_t s) {
+  const int64_t N = F->n;
+  const size_t bytes = (size_t)N * nrhs * sizeof(double);
+  std::unique_lock<std::mutex> klk(F->klog_m, std::defer_lock);
+  if (F->klog.on) {
+    klk.lock();
+    F->klog.clear(1);
+  }
+  const bool disjoint = (const char*)x >= (const char*)b + bytes || (const char*)x + bytes <= (const char*)b;
+  if (!dev && nrhs >= 16 && bytes >= ((size_t)64 << 20) && disjoint && PinnedXfer::page_locked(b)) {
+    solve_pipelined(F, b, x, nrhs, s);
+    return;
+  }
+  double* v = nullptr;
+  HCK(cudaMallocAsync((void**)&v, std::max<size_t>(bytes, 8), s));
+  if (dev) HCK(cudaMemcpyAsync(v, b, bytes, cudaMemcpyDeviceToDevice, s));
+  else pinned_xfer().h2d(v, b, bytes, s);
+  solve_sweep(F, v, nrhs, s);
+  // host output that is not the input: fault its pages in while the sweep runs
+  if (!dev && disjoint) PinnedXfer::prefault(x, bytes);
+  if (dev) HCK(cudaMemcpyAsync(x, v, bytes, cudaMemcpyDeviceToDevice, s));
+  else pinned_xfer().d2h(x, v, bytes, s);
+  HCK(cudaFreeAsync(v, s));
   if (!dev) HCK(cudaStreamSynchronize(s));
 }
+
 
 // y = F x: the solve sweep inverted record by record (kernels_solve.cu).
 void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, bool dev, cudaStream_t s) {
