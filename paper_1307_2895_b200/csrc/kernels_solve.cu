@@ -529,7 +529,9 @@ __device__ __forceinline__ double mma_a(const double* __restrict__ A, int lda, i
   return A[k * lda + i];
 }
 
-template <int AM, class Out>
+// kOne: the caller guarantees one batch (M <= 96 rows with 64 RHS), so the
+// pair index handed to `out` is a compile-time register index
+template <int AM, bool kOne = false, class Out>
 __device__ __forceinline__ void warp_mma(int M, int K, const double* __restrict__ A, int lda, const double* X,
                                          int ldx, int R, Out out) {
   constexpr int NW = NT / 32;
@@ -543,45 +545,47 @@ __device__ __forceinline__ void warp_mma(int M, int K, const double* __restrict_
   const int m0 = w / ntr, dm = NW / ntr, r0 = w - m0 * ntr;
   auto tmj = [&](int j) { return one_rt ? m0 + j * dm : (w + NW * j) / ntr; };
   auto trj = [&](int j) { return one_rt ? r0 : (w + NW * j) % ntr; };
-  double acc[kMmaMaxJ][2];
+  // pairs in batches of kMmaMaxJ accumulators (M up to 192 rows: 24 row tiles)
+  for (int jb = 0; jb < (kOne ? min(nj, 1) : nj); jb += kMmaMaxJ) {
+    const int nb = min(kMmaMaxJ, nj - jb);
+    double acc[kMmaMaxJ][2];
 #pragma unroll
-  for (int j = 0; j < kMmaMaxJ; ++j) acc[j][0] = acc[j][1] = 0.0;
-  int klo = 0, khi = nj ? K : 0;
-  if (nj) {
-    if (AM == 0) khi = min(K, 8 * tmj(nj - 1) + 8);
-    if (AM == 1) klo = 8 * tmj(0);
-  }
-  const int cfix = 8 * r0 + ar;
-  for (int k0 = klo & ~3; k0 < khi; k0 += 4) {
-    const int k = k0 + ak;
-    const bool kin = k < K;
-    double b0 = 0.0;
-    if (one_rt) b0 = (kin && cfix < R) ? X[k * ldx + cfix] : 0.0;
+    for (int j = 0; j < kMmaMaxJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+    int klo = 0, khi = K;
+    if (AM == 0) khi = min(K, 8 * tmj(jb + nb - 1) + 8);
+    if (AM == 1) klo = 8 * tmj(jb);
+    const int cfix = 8 * r0 + ar;
+    for (int k0 = klo & ~3; k0 < khi; k0 += 4) {
+      const int k = k0 + ak;
+      const bool kin = k < K;
+      double b0 = 0.0;
+      if (one_rt) b0 = (kin && cfix < R) ? X[k * ldx + cfix] : 0.0;
+#pragma unroll
+      for (int j = 0; j < kMmaMaxJ; ++j) {
+        if (j >= nb) break;
+        const int mi = tmj(jb + j);
+        if (AM == 0 && k0 >= 8 * mi + 8) continue;  // above the diagonal: zero
+        if (AM == 1 && k0 + 4 <= 8 * mi) continue;  // below it (transpose): zero
+        const int i = 8 * mi + ar;
+        const double a = (i < M && kin) ? mma_a<AM>(A, lda, i, k) : 0.0;
+        double b = b0;
+        if (!one_rt) {
+          const int c = 8 * trj(jb + j) + ar;
+          b = (kin && c < R) ? X[k * ldx + c] : 0.0;
+        }
+        dmma_8x8x4(acc[j][0], acc[j][1], a, b);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < kMmaMaxJ; ++j) {
-      if (j >= nj) break;
-      const int mi = tmj(j);
-      if (AM == 0 && k0 >= 8 * mi + 8) continue;  // above the diagonal: zero
-      if (AM == 1 && k0 + 4 <= 8 * mi) continue;  // below it (transpose): zero
-      const int i = 8 * mi + ar;
-      const double a = (i < M && kin) ? mma_a<AM>(A, lda, i, k) : 0.0;
-      double b = b0;
-      if (!one_rt) {
-        const int c = 8 * trj(j) + ar;
-        b = (kin && c < R) ? X[k * ldx + c] : 0.0;
+      if (j >= nb) break;
+      const int row = 8 * tmj(jb + j) + (lane >> 2);
+      if (row >= M) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * trj(jb + j) + 2 * (lane & 3) + h;
+        if (col < R) out(row, col, acc[j][h], kOne ? j : jb + j, h);
       }
-      dmma_8x8x4(acc[j][0], acc[j][1], a, b);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kMmaMaxJ; ++j) {
-    if (j >= nj) break;
-    const int row = 8 * tmj(j) + (lane >> 2);
-    if (row >= M) continue;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int col = 8 * trj(j) + 2 * (lane & 3) + h;
-      if (col < R) out(row, col, acc[j][h], j, h);
     }
   }
 }
@@ -615,7 +619,7 @@ __global__ void __launch_bounds__(NT, 3) solve_elim_fwd_mma_kernel(const SolveRe
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ntr = (R + 7) >> 3, npair = ((nc + 7) >> 3) * ntr;
     double keep[kMmaMaxJ][2];
-    warp_mma<0>(nc, nc, sP, 0, sx, ld, R, [&](int row, int col, double val, int j_, int h_) {
+    warp_mma<0, true>(nc, nc, sP, 0, sx, ld, R, [&](int row, int col, double val, int j_, int h_) {
       keep[j_][h_] = val;
       v[(size_t)c[row] * R + col] = val;
     });

@@ -381,13 +381,14 @@ import numpy as np
 sys.path.insert(0, ".")
 import paper_1307_2895_b200 as H
 out = {}
-for dim, n, m, eps, var in [(2, 64, 8, 1e-6, "hifde"), (3, 16, 4, 1e-6, "hifde3x")]:
+for dim, n, m, eps, var in [(2, 64, 8, 1e-6, "hifde"), (2, 256, 8, 1e-9, "hifde"), (3, 16, 4, 1e-6, "hifde3x"),
+                            (3, 32, 4, 1e-6, "hifde3x")]:
     g = H.build_grid(dim, n, m)
     a = H.assemble(g, H.gaussian_contrast_field(g, seed=5))
     f = (H.factor_hifde if var == "hifde" else H.factor_hifde3x)(a, g, eps)
-    for nrhs in (2, 3, 8, 17, 48, 64):
+    for nrhs in (2, 3, 8, 16, 17, 40, 48, 64):
         b = np.random.default_rng(nrhs).standard_normal((g.ndof, nrhs))
-        out[f"{dim}_{nrhs}"] = f.apply_inverse(b)
+        out[f"{dim}_{n}_{nrhs}"] = f.apply_inverse(b)
 np.savez(sys.argv[1], **out)
 '''
 
