@@ -650,42 +650,36 @@ struct PinnedXfer {
 #pragma omp parallel for num_threads(copy_threads()) schedule(static)
     for (int64_t i = 0; i < npg; ++i) d[(size_t)i * 4096] = 0;
   }
-  // Column chunks c (device blocks vb[c], N x (c0[c+1] - c0[c]) row-major)
-  // into the columns [c0[c], c0[c+1]) of the host block x (N x nrhs), each
-  // after its event es[c]: row pieces through the two pinned slots, the
-  // host threads scattering one piece while the next one's DMA runs.
+  // The column chunks c (device blocks vb[c], N x (c0[c+1] - c0[c]) row-major,
+  // complete after their events es[c]) back into the host block x (N x nrhs):
+  // row pieces gathered from every chunk by strided DMAs into a pinned slot
+  // (whole rows, nrhs wide), copied out contiguously by the host threads
+  // while the other slot's DMAs run.
   void d2h_columns(double* x, int nrhs, const std::vector<double*>& vb, const std::vector<int>& c0, int64_t N,
                    const std::vector<cudaEvent_t>& es, cudaStream_t s) {
     int device = 0;
     HCK(cudaGetDevice(&device));
     std::lock_guard<std::mutex> lk(m);
     if (!ready(device)) throw Fail{HIFDE_CUDA, "pinned staging buffers unavailable"};
-    struct Piece { int c; int64_t r0, r1; };
-    std::vector<Piece> pcs;
-    for (size_t c = 0; c + 1 < c0.size(); ++c) {
-      const int w = c0[c + 1] - c0[c];
-      const int64_t rows = std::max<int64_t>(1, (int64_t)(kChunk / ((size_t)w * sizeof(double))));
-      for (int64_t r0 = 0; r0 < N; r0 += rows) pcs.push_back(Piece{(int)c, r0, std::min(N, r0 + rows)});
-    }
-    auto issue = [&](size_t k) {
-      const Piece& P = pcs[k];
-      const int w = c0[(size_t)P.c + 1] - c0[(size_t)P.c];
-      if (k == 0 || pcs[k - 1].c != P.c) HCK(cudaStreamWaitEvent(s, es[(size_t)P.c], 0));
-      HCK(cudaMemcpyAsync(buf[k & 1], vb[(size_t)P.c] + P.r0 * w, (size_t)(P.r1 - P.r0) * w * sizeof(double),
-                          cudaMemcpyDeviceToHost, s));
+    for (const cudaEvent_t e : es) HCK(cudaStreamWaitEvent(s, e, 0));
+    const int64_t rows = std::max<int64_t>(1, (int64_t)(kChunk / ((size_t)nrhs * sizeof(double))));
+    const int64_t npc = (N + rows - 1) / rows;
+    auto issue = [&](int64_t k) {
+      const int64_t r0 = k * rows, r1 = std::min(N, r0 + rows);
+      for (size_t c = 0; c + 1 < c0.size(); ++c) {
+        const int w = c0[c + 1] - c0[c];
+        HCK(cudaMemcpy2DAsync((double*)buf[k & 1] + c0[c], (size_t)nrhs * sizeof(double), vb[c] + r0 * w,
+                              (size_t)w * sizeof(double), (size_t)w * sizeof(double), (size_t)(r1 - r0),
+                              cudaMemcpyDeviceToHost, s));
+      }
       HCK(cudaEventRecord(ev[k & 1], s));
     };
     issue(0);
-    for (size_t k = 0; k < pcs.size(); ++k) {
+    for (int64_t k = 0; k < npc; ++k) {
       HCK(cudaEventSynchronize(ev[k & 1]));
-      if (k + 1 < pcs.size()) issue(k + 1);
-      const Piece& P = pcs[k];
-      const int w = c0[(size_t)P.c + 1] - c0[(size_t)P.c], col = c0[(size_t)P.c];
-      const double* src = (const double*)buf[k & 1];
-      const int64_t nr = P.r1 - P.r0;
-#pragma omp parallel for num_threads(copy_threads()) schedule(static)
-      for (int64_t i = 0; i < nr; ++i)
-        std::memcpy(x + (size_t)(P.r0 + i) * nrhs + col, src + (size_t)i * w, (size_t)w * sizeof(double));
+      if (k + 1 < npc) issue(k + 1);
+      const int64_t r0 = k * rows, r1 = std::min(N, r0 + rows);
+      pmemcpy((char*)(x + (size_t)r0 * nrhs), buf[k & 1], (size_t)(r1 - r0) * nrhs * sizeof(double));
     }
   }
   void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
