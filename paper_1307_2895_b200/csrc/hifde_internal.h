@@ -231,9 +231,11 @@ int skel_cluster_capacity(size_t smem, int cs);  // resident clusters of cs CTAs
 cudaError_t launch_skel_cluster(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
                                 int* done, const Arenas& A, double eps, size_t smem, int nclusters, int cs,
                                 cudaStream_t s);
+// order: claim order of the groups (topological: by dependency depth, then
+// reference order); done: ntasks + 1 ints, zeroed (the last is the claim counter)
 cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
-                                int* done, const Arenas& A, double eps, size_t smem, int nt, int grid,
-                                cudaStream_t s);
+                                const int32_t* order, int* done, const Arenas& A, double eps, size_t smem, int nt,
+                                int grid, cudaStream_t s);
 
 // work int4 {task, block index, map offset of the block, 0}
 void launch_skelbig_posmap(const SkelBigTask* tasks, const int4* work, int nwork, const Arenas& A, cudaStream_t s);
@@ -457,6 +459,11 @@ cudaError_t sym_skel_sizes(const SymFront& P, double promote_work, int gram_eps_
 cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t s);
 cudaError_t sym_skel_chain(const int64_t* pred_ptr, const int32_t* preds, const int32_t* ng, int ng_ub, int iters,
                            int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot, cudaStream_t s);
+// claim order of an exact level: groups sorted stably by dependency depth
+// (the final relaxation buffer of sym_skel_chain)
+cudaError_t sym_skel_order(const int32_t* b0, const int32_t* b1, const int32_t* changed, int iters,
+                           const int32_t* ng, int ng_ub, int32_t* depth, int32_t* depth_sorted, int32_t* iota,
+                           int32_t* order, SymWork& W, cudaStream_t s);
 cudaError_t sym_skel_cluster_tasks(SkelTask* tasks, const int64_t* cl_rel, int64_t base, const int32_t* ng,
                                    int ng_ub, cudaStream_t s);
 cudaError_t sym_skel_finish(const SkelTask* tasks, const int32_t* kout, const int32_t* ng, int ng_ub,

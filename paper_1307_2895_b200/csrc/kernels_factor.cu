@@ -806,20 +806,24 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     const int nb = A.blk_n[bid];
     const int32_t* bd = A.idx + A.blk_dof_off[bid];
     const double* bv = A.bvals + A.blk_val_off[bid];
+    if (threadIdx.x == 0) sh_k = 0;
+    __syncthreads();
     for (int k = threadIdx.x; k < nb; k += NT) {
       const int p = front_pos(sdofs, nc, nq, bd[k]);
       smap[k] = (p >= 0 && salive[p]) ? p : -1;
+      if (p >= 0 && p < nc && salive[p]) skl[atomicAdd(&sh_k, 1)] = k;  // block columns landing in c
     }
     __syncthreads();
-    // warp per block row, four rows' loads in flight per lane (each front
-    // entry still takes one add per block: same sums as one row at a time)
+    // only the columns of c are assembled (A_cc and Mq = A_qc): warp per
+    // block row over the compact column list, four rows' loads in flight per
+    // lane (each front entry still takes one add per block)
+    const int ncc = sh_k;
     for (int k0 = (int)(threadIdx.x >> 5) * 4; k0 < nb; k0 += NT / 8) {
-      for (int l = (int)(threadIdx.x & 31); l < nb; l += 32) {
-        const int pl = smap[l];
+      for (int j = (int)(threadIdx.x & 31); j < ncc; j += 32) {
+        const int l = skl[j], pl = smap[l];
         double val[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) val[u] = (k0 + u < nb && pl >= 0 && pl < nc) ? bv[(size_t)(k0 + u) * nb + l] : 0.0;
-        if (pl < 0 || pl >= nc) continue;
+        for (int u = 0; u < 4; ++u) val[u] = (k0 + u < nb && smap[k0 + u] >= 0) ? bv[(size_t)(k0 + u) * nb + l] : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (k0 + u >= nb) break;
@@ -1129,18 +1133,26 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
 }
 
 // Exact (reference) order in one launch: co-resident CTAs walk the groups in
-// reference order (task j -> CTA j mod grid); a group starts once every
-// earlier neighbouring group has finished (its redundant DOFs are then
-// retired in the device active mask), exactly the state the reference's
-// sequential loop gives it (src/driver.py:190-194, src/factor_ops.py:208).
-// Deadlock-free: the lowest unfinished group always has all predecessors done
-// and its CTA is not blocked.
+// reference order; a group starts once every earlier neighbouring group has
+// finished (its redundant DOFs are then retired in the device active mask),
+// exactly the state the reference's sequential loop gives it
+// (src/driver.py:190-194, src/factor_ops.py:208).  Deadlock-free: groups are
+// claimed in a topological order, so a claimed group's predecessors are all
+// claimed by running CTAs.
+// Groups are claimed dynamically in `order` (the reference order sorted
+// stably by dependency depth, a topological order): a CTA never holds a group
+// whose predecessors are still unclaimed, so the chain is not delayed behind
+// groups waiting elsewhere (static round-robin assignment was: config 3
+// level 3.5 ran its 62-link chain in 7.4 ms with 3.2 ms of work on it).
+// done[ntasks] is the claim counter.
 template <int NT>
 __global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __restrict__ tasks, int ntasks,
                                                           const int64_t* __restrict__ pred_ptr,
                                                           const int32_t* __restrict__ pred,
+                                                          const int32_t* __restrict__ order,
                                                           int* __restrict__ done, Arenas A, double eps) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_claim;
   auto stamp = [&](int j, int which) {
     if (A.tlog && threadIdx.x == 0) {
       unsigned long long g;
@@ -1148,7 +1160,13 @@ __global__ void __launch_bounds__(NT) skel_ordered_kernel(const SkelTask* __rest
       A.tlog[(size_t)j * 16 + which] = g;
     }
   };
-  for (int j = blockIdx.x; j < ntasks; j += gridDim.x) {
+  for (;;) {
+    if (threadIdx.x == 0) s_claim = atomicAdd(done + ntasks, 1);
+    __syncthreads();
+    const int i = s_claim;
+    __syncthreads();
+    if (i >= ntasks) break;
+    const int j = order[i];
     const SkelTask t = tasks[j];
     stamp(j, 0);
     auto wait = [&]() {
@@ -1569,12 +1587,12 @@ int skel_ordered_capacity(size_t smem, int nt) {
 }
 
 cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64_t* pred_ptr, const int32_t* pred,
-                                int* done, const Arenas& A, double eps, size_t smem, int nt, int grid,
-                                cudaStream_t s) {
+                                const int32_t* order, int* done, const Arenas& A, double eps, size_t smem, int nt,
+                                int grid, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   Arenas Ac = A;
-  void* args[] = {(void*)&d_tasks, (void*)&ntasks, (void*)&pred_ptr, (void*)&pred, (void*)&done, (void*)&Ac,
-                  (void*)&eps};
+  void* args[] = {(void*)&d_tasks, (void*)&ntasks, (void*)&pred_ptr, (void*)&pred, (void*)&order, (void*)&done,
+                  (void*)&Ac, (void*)&eps};
   if (nt <= 128)
     return cudaLaunchCooperativeKernel((const void*)skel_ordered_kernel<128>, dim3((unsigned)grid), dim3(128), args,
                                        smem, s);

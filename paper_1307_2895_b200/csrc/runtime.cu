@@ -1955,7 +1955,7 @@ struct Factorizer {
       lists.upload(hl.data(), 0, hl.size(), s);
       DBuf<SkelTask> dt;
       DBuf<int64_t> dpp;
-      DBuf<int32_t> dpr;
+      DBuf<int32_t> dpr, dord;
       DBuf<int> ddone;
       dt.reserve(tasks.size(), s);
       dt.upload(tasks.data(), 0, tasks.size(), s);
@@ -1963,8 +1963,15 @@ struct Factorizer {
       dpp.upload(pred_ptr.data(), 0, pred_ptr.size(), s);
       dpr.reserve(std::max<size_t>(preds.size(), 1), s);
       dpr.upload(preds.data(), 0, preds.size(), s);
-      ddone.reserve((size_t)nt, s);
-      HCK(cudaMemsetAsync(ddone.p, 0, sizeof(int) * (size_t)nt, s));
+      ddone.reserve((size_t)nt + 1, s);
+      HCK(cudaMemsetAsync(ddone.p, 0, sizeof(int) * ((size_t)nt + 1), s));
+      {  // claim order: by dependency depth, reference order within a depth
+        std::vector<int32_t> ord((size_t)nt);
+        for (int64_t t = 0; t < nt; ++t) ord[(size_t)t] = (int32_t)t;
+        std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return batch[(size_t)a] < batch[(size_t)b]; });
+        dord.reserve((size_t)nt, s);
+        dord.upload(ord.data(), 0, ord.size(), s);
+      }
       const int64_t st_off = (int64_t)status.bump((size_t)nt, s);
       HCK(cudaMemsetAsync(status.p + st_off, 0, (size_t)nt * sizeof(int), s));
       pending.push_back({st_off, nt, tag, "group"});
@@ -2047,7 +2054,7 @@ struct Factorizer {
       }
       if (run_here) {
         const int kl = F->klog.begin("skel_ordered_kernel", tag, 0, 0, 0, s);
-        HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
+        HCK(launch_skel_ordered(dt.p, (int)nt, dpp.p, dpr.p, dord.p, ddone.p, A, opt.eps, smem, nthr, grid, s));
         F->klog.end(kl, s);
         ++g_launches;
       }
@@ -2075,6 +2082,7 @@ struct Factorizer {
       dt.release(s);
       dpp.release(s);
       dpr.release(s);
+      dord.release(s);
       ddone.release(s);
       return;
     }
@@ -2685,7 +2693,7 @@ struct Factorizer {
   DBuf<int32_t> sy_alist, sy_mcnt, sy_mptr, sy_mblk;
   DBuf<int32_t> sy_nq, sy_nb, sy_maxnb, sy_npred, sy_flag, sy_retry;
   DBuf<int64_t> sy_inc, sy_exc;  // ElimInc / SkelInc storage (8 words per group)
-  DBuf<int32_t> sy_preds, sy_b0, sy_b1, sy_changed;
+  DBuf<int32_t> sy_preds, sy_b0, sy_b1, sy_changed, sy_depth, sy_depth2, sy_iota, sy_order;
   DBuf<int64_t> sy_pred_ptr, sy_cl_rel;
   DBuf<ElimTask> sy_small, sy_big;
   DBuf<SkelTask> sy_tasks;
@@ -2738,7 +2746,7 @@ struct Factorizer {
   void dev_release() {
     for (auto* b : {&sy_act, &sy_keys, &sy_skeys, &sy_gmem, &sy_head, &sy_group_of, &sy_alist, &sy_mcnt, &sy_mptr,
                     &sy_mblk, &sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry, &sy_preds, &sy_b0, &sy_b1,
-                    &sy_changed, &sy_red_key, &sy_red_key2})
+                    &sy_changed, &sy_red_key, &sy_red_key2, &sy_depth, &sy_depth2, &sy_iota, &sy_order})
       b->release(s);
     for (auto* b : {&sy_goff, &sy_inc, &sy_exc, &sy_pred_ptr, &sy_cl_rel, &sy_red_val}) b->release(s);
     sy_alive.release(s);
@@ -3117,8 +3125,8 @@ struct Factorizer {
     const bool one_launch = exact && ng > 1;
     const int nthr = (T.max_nc > 32 || T.max_nq > 128) ? 512 : 128;
     if (one_launch) {
-      sy_done.reserve((size_t)ng, s);
-      HCK(cudaMemsetAsync(sy_done.p, 0, sizeof(int) * (size_t)ng, s));
+      sy_done.reserve((size_t)ng + 1, s);
+      HCK(cudaMemsetAsync(sy_done.p, 0, sizeof(int) * ((size_t)ng + 1), s));
       int cs = 0, ncls = 0;
       size_t smem_cl = 0;
       if (T.max_nc >= kClusterMinNc) {
@@ -3145,8 +3153,12 @@ struct Factorizer {
       } else {
         const int cap = skel_ordered_capacity((size_t)T.smem, nthr);
         if (cap < 1) throw Fail{HIFDE_CUDA, "ordered skeleton kernel cannot be resident"};
+        // claim order: stably by dependency depth (the relaxation's result)
+        for (auto* b : {&sy_depth, &sy_depth2, &sy_iota, &sy_order}) b->reserve((size_t)ng + 1, s);
+        HCK(sym_skel_order(sy_b0.p, sy_b1.p, sy_changed.p, opt.exact_max_batches + 1, &d_scal->ng, (int)ng,
+                           sy_depth.p, sy_depth2.p, sy_iota.p, sy_order.p, symw, s));
         const int kl = F->klog.begin("skel_ordered_kernel", tag, 0, 0, 0, s);
-        HCK(launch_skel_ordered(sy_tasks.p, (int)ng, sy_pred_ptr.p, sy_preds.p, sy_done.p, Ar, opt.eps,
+        HCK(launch_skel_ordered(sy_tasks.p, (int)ng, sy_pred_ptr.p, sy_preds.p, sy_order.p, sy_done.p, Ar, opt.eps,
                                 (size_t)T.smem, nthr, (int)std::min<int64_t>(ng, cap), s));
         F->klog.end(kl, s);
       }

@@ -620,6 +620,21 @@ __global__ void skel_chain_kernel(const int32_t* __restrict__ b0, const int32_t*
   if (threadIdx.x == 0) tot->max_chain = m;
 }
 
+// the relaxation's final depths (the buffer the last sweep that ran wrote)
+__global__ void skel_depth_kernel(const int32_t* __restrict__ b0, const int32_t* __restrict__ b1,
+                                  const int32_t* __restrict__ changed, int iters, const int32_t* __restrict__ ng,
+                                  int32_t* __restrict__ depth, int32_t* __restrict__ iota) {
+  int last = iters - 1;
+  for (int i = 1; i < iters; ++i)
+    if (changed[i - 1] == 0) { last = i - 1; break; }
+  const int32_t* b = (last % 2 == 0) ? b1 : b0;
+  const int n = *ng;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    depth[t] = b[t];
+    iota[t] = t;
+  }
+}
+
 // after the level's kernels: ranks known -> delta blocks, solve records, stats
 __global__ void skel_finish_inc(const SkelTask* __restrict__ tasks, const int32_t* __restrict__ kout,
                                 const int32_t* __restrict__ ng, int2* __restrict__ inc) {
@@ -948,6 +963,18 @@ cudaError_t sym_skel_chain(const int64_t* pred_ptr, const int32_t* preds, const 
   }
   skel_chain_kernel<<<1, 256, 0, s>>>(b0, b1, changed, iters, ng, tot);
   return cudaGetLastError();
+}
+
+cudaError_t sym_skel_order(const int32_t* b0, const int32_t* b1, const int32_t* changed, int iters,
+                           const int32_t* ng, int ng_ub, int32_t* depth, int32_t* depth_sorted, int32_t* iota,
+                           int32_t* order, SymWork& W, cudaStream_t s) {
+  skel_depth_kernel<<<std::max(1, (ng_ub + 255) / 256), 256, 0, s>>>(b0, b1, changed, iters, ng, depth, iota);
+  int bits = 1;
+  while ((1 << bits) <= iters) ++bits;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, depth, depth_sorted, iota, order, ng_ub, 0, bits, s);
+  ensure_tmp(W, tb, s);
+  return cub::DeviceRadixSort::SortPairs(W.cub_tmp, tb, depth, depth_sorted, iota, order, ng_ub, 0, bits, s);
 }
 
 cudaError_t sym_skel_cluster_tasks(SkelTask* tasks, const int64_t* cl_rel, int64_t base, const int32_t* ng,
