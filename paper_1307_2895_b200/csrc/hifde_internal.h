@@ -371,6 +371,12 @@ struct SymFront {
   int32_t* retry;           // groups for the large tier
   int32_t* nretry;
   int32_t* fatal;           // even the large tier overflowed (host fallback)
+  // count pass, skeleton levels: unsorted predecessor lists for the chain
+  int32_t* pred_tmp;        // null: not wanted
+  int64_t* pred_start;
+  int64_t* pred_alloc;      // allocation cursor (device scalar, zeroed)
+  int64_t pred_cap;
+  int32_t* pred_ovf;        // the capacity was exceeded
   // fill pass: offsets from the level's prefix sums (int64 words of the
   // per-group increment struct), destinations
   const int64_t* exc;
@@ -457,8 +463,9 @@ cudaError_t sym_elim_fill(const SymFront& P, const ElimFillArgs& A, int64_t nred
 cudaError_t sym_skel_sizes(const SymFront& P, double promote_work, int gram_eps_ok, int ng_ub, SkelInc* inc,
                            SkelInc* exc, LevelTotals* tot, SymWork& W, cudaStream_t s);
 cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t s);
-cudaError_t sym_skel_chain(const int64_t* pred_ptr, const int32_t* preds, const int32_t* ng, int ng_ub, int iters,
-                           int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot, cudaStream_t s);
+cudaError_t sym_skel_chain(const int64_t* pred_start, const int32_t* npred, const int32_t* preds, const int32_t* ng,
+                           int ng_ub, int iters, int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot,
+                           cudaStream_t s);
 // claim order of an exact level: groups sorted stably by dependency depth
 // (the final relaxation buffer of sym_skel_chain)
 cudaError_t sym_skel_order(const int32_t* b0, const int32_t* b1, const int32_t* changed, int iters,

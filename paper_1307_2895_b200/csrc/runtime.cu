@@ -2682,8 +2682,8 @@ struct Factorizer {
   // take (adaptive hifde3x cells, large skeleton groups, the terminal block).
   // =========================================================================
   struct SymScalars {
-    int64_t nact, nalive, nblk, red_nt;
-    int32_t ng, nretry, fatal, pad;
+    int64_t nact, nalive, nblk, red_nt, pred_alloc;
+    int32_t ng, nretry, fatal, pred_ovf;
   };
   bool dev_mode = false;
   SymWork symw;
@@ -2694,7 +2694,8 @@ struct Factorizer {
   DBuf<int32_t> sy_nq, sy_nb, sy_maxnb, sy_npred, sy_flag, sy_retry;
   DBuf<int64_t> sy_inc, sy_exc;  // ElimInc / SkelInc storage (8 words per group)
   DBuf<int32_t> sy_preds, sy_b0, sy_b1, sy_changed, sy_depth, sy_depth2, sy_iota, sy_order;
-  DBuf<int64_t> sy_pred_ptr, sy_cl_rel;
+  DBuf<int64_t> sy_pred_ptr, sy_cl_rel, sy_pred_start;
+  DBuf<int32_t> sy_pred_tmp;
   DBuf<ElimTask> sy_small, sy_big;
   DBuf<SkelTask> sy_tasks;
   DBuf<int32_t> sy_red_key, sy_red_key2;
@@ -2748,7 +2749,8 @@ struct Factorizer {
                     &sy_mblk, &sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry, &sy_preds, &sy_b0, &sy_b1,
                     &sy_changed, &sy_red_key, &sy_red_key2, &sy_depth, &sy_depth2, &sy_iota, &sy_order})
       b->release(s);
-    for (auto* b : {&sy_goff, &sy_inc, &sy_exc, &sy_pred_ptr, &sy_cl_rel, &sy_red_val}) b->release(s);
+    for (auto* b : {&sy_goff, &sy_inc, &sy_exc, &sy_pred_ptr, &sy_cl_rel, &sy_red_val, &sy_pred_start}) b->release(s);
+    sy_pred_tmp.release(s);
     sy_alive.release(s);
     sy_cellcls.release(s);
     sy_small.release(s);
@@ -2879,6 +2881,19 @@ struct Factorizer {
     P.retry = sy_retry.p;
     P.nretry = &d_scal->nretry;
     P.fatal = &d_scal->fatal;
+    P.pred_tmp = nullptr;
+    if (kind != 0 && opt.order_mode != HIFDE_ORDER_SNAPSHOT) {  // predecessor lists for the chain
+      const int64_t cap = 64 * (ng_ub + 1);
+      sy_pred_tmp.reserve((size_t)cap, s);
+      sy_pred_start.reserve((size_t)ng_ub + 1, s);
+      P.pred_tmp = sy_pred_tmp.p;
+      P.pred_start = sy_pred_start.p;
+      P.pred_alloc = &d_scal->pred_alloc;
+      P.pred_cap = cap;
+      P.pred_ovf = &d_scal->pred_ovf;
+      HCK(cudaMemsetAsync(&d_scal->pred_alloc, 0, sizeof(int64_t), s));
+      HCK(cudaMemsetAsync(&d_scal->pred_ovf, 0, sizeof(int32_t), s));
+    }
     HCK(cudaMemsetAsync(sy_npred.p, 0, sizeof(int32_t) * ((size_t)ng_ub + 1), s));
     HCK(sym_fronts_count(P, s));
     return true;
@@ -3045,6 +3060,15 @@ struct Factorizer {
     SkelInc* exc = reinterpret_cast<SkelInc*>(sy_exc.p);
     const bool gram_eps = opt.eps >= kGramMinEps;
     HCK(sym_skel_sizes(P, kPromoteWork, gram_eps ? 1 : 0, (int)ng_ub, inc, exc, d_tot, symw, s));
+    const int iters = opt.exact_max_batches + 1;
+    const bool chain_early = P.pred_tmp != nullptr;
+    if (chain_early) {  // the dependency chain from the count pass's lists: one readback for the level
+      sy_b0.reserve((size_t)ng_ub + 1, s);
+      sy_b1.reserve((size_t)ng_ub + 1, s);
+      sy_changed.reserve((size_t)iters + 1, s);
+      HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_pred_tmp.p, &d_scal->ng, (int)ng_ub, iters, sy_b0.p,
+                         sy_b1.p, sy_changed.p, d_tot, s));
+    }
     dev_sync_totals();
     L.lap("dev-count");
     const LevelTotals T = *h_tot;
@@ -3100,14 +3124,15 @@ struct Factorizer {
     bool exact = opt.order_mode == HIFDE_ORDER_EXACT;
     int nbatch = 1;
     if (opt.order_mode != HIFDE_ORDER_SNAPSHOT && ng > 1) {
-      const int iters = opt.exact_max_batches + 1;
-      sy_b0.reserve((size_t)ng + 1, s);
-      sy_b1.reserve((size_t)ng + 1, s);
-      sy_changed.reserve((size_t)iters + 1, s);
-      HCK(sym_skel_chain(sy_pred_ptr.p, sy_preds.p, &d_scal->ng, (int)ng, iters, sy_b0.p, sy_b1.p, sy_changed.p,
-                         d_tot, s));
-      HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
-      HCK(cudaStreamSynchronize(s));
+      if (h_scal->pred_ovf) {  // the early lists overflowed: the chain over the filled CSR (second readback)
+        sy_npred.reserve((size_t)ng + 1, s);
+        sy_pred_start.reserve((size_t)ng + 1, s);
+        HCK(cudaMemcpyAsync(sy_pred_start.p, sy_pred_ptr.p, sizeof(int64_t) * (size_t)ng, cudaMemcpyDeviceToDevice, s));
+        HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_preds.p, &d_scal->ng, (int)ng, iters, sy_b0.p, sy_b1.p,
+                           sy_changed.p, d_tot, s));
+        HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
+        HCK(cudaStreamSynchronize(s));
+      }
       nbatch = (int)h_tot->max_chain + 1;
       if (opt.order_mode == HIFDE_ORDER_AUTO) exact = nbatch <= opt.exact_max_batches;
     }

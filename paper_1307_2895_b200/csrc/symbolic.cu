@@ -291,6 +291,23 @@ __global__ void __launch_bounds__(kSymNT) sym_front_kernel(SymFront P) {
       continue;
     }
     if (!FILL) {
+      // predecessor lists for the dependency-chain relaxation, right away
+      // (unsorted, at an atomically allocated place: the chain does not need
+      // the arenas, so the level's exact / snapshot choice travels with the
+      // count totals in one readback)
+      __shared__ int64_t pstart;
+      if (P.group_of && P.pred_tmp) {
+        if (threadIdx.x == 0) {
+          pstart = atomicAdd((unsigned long long*)P.pred_alloc, (unsigned long long)npk);
+          if (pstart + npk > P.pred_cap) atomicExch(P.pred_ovf, 1);
+          P.pred_start[g] = pstart;
+        }
+        __syncthreads();
+        if (pstart + npk <= P.pred_cap) {
+          const int np = compact_set<kSymNT>(hp, HP, buf);
+          for (int i = threadIdx.x; i < np; i += kSymNT) P.pred_tmp[pstart + i] = buf[i];
+        }
+      }
       if (threadIdx.x == 0) {
         P.nq[g] = nqk;
         P.nb[g] = nb;
@@ -590,14 +607,16 @@ __global__ void skel_cluster_tasks(SkelTask* __restrict__ tasks, const int64_t* 
 // Longest dependency chain: b[t] = 1 + max b[p] over predecessors p (Jacobi
 // sweeps from 0; after i sweeps b = min(chain, i)); iteration it stops early
 // once the previous sweep changed nothing.
-__global__ void skel_relax_kernel(const int64_t* __restrict__ pred_ptr, const int32_t* __restrict__ preds,
-                                  const int32_t* __restrict__ ng, const int32_t* __restrict__ bin,
-                                  int32_t* __restrict__ bout, int32_t* changed, int it) {
+__global__ void skel_relax_kernel(const int64_t* __restrict__ pred_start, const int32_t* __restrict__ npred,
+                                  const int32_t* __restrict__ preds, const int32_t* __restrict__ ng,
+                                  const int32_t* __restrict__ bin, int32_t* __restrict__ bout, int32_t* changed,
+                                  int it) {
   if (it > 0 && changed[it - 1] == 0) return;
   const int n = *ng;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     int b = 0;
-    for (int64_t p = pred_ptr[t]; p < pred_ptr[t + 1]; ++p) b = max(b, bin[preds[p]] + 1);
+    const int64_t p0 = pred_start[t];
+    for (int64_t p = p0; p < p0 + npred[t]; ++p) b = max(b, bin[preds[p]] + 1);
     bout[t] = b;
     if (b != bin[t]) changed[it] = 1;
   }
@@ -951,15 +970,16 @@ cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t
   return cudaGetLastError();
 }
 
-cudaError_t sym_skel_chain(const int64_t* pred_ptr, const int32_t* preds, const int32_t* ng, int ng_ub, int iters,
-                           int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot, cudaStream_t s) {
+cudaError_t sym_skel_chain(const int64_t* pred_start, const int32_t* npred, const int32_t* preds, const int32_t* ng,
+                           int ng_ub, int iters, int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot,
+                           cudaStream_t s) {
   cudaMemsetAsync(b0, 0, sizeof(int32_t) * (size_t)ng_ub, s);
   cudaMemsetAsync(changed, 0, sizeof(int32_t) * (size_t)iters, s);
   const int grid = std::max(1, std::min(sym_grid(4), (ng_ub + 255) / 256));
   for (int it = 0; it < iters; ++it) {
     const int32_t* bin = (it % 2 == 0) ? b0 : b1;
     int32_t* bout = (it % 2 == 0) ? b1 : b0;
-    skel_relax_kernel<<<grid, 256, 0, s>>>(pred_ptr, preds, ng, bin, bout, changed, it);
+    skel_relax_kernel<<<grid, 256, 0, s>>>(pred_start, npred, preds, ng, bin, bout, changed, it);
   }
   skel_chain_kernel<<<1, 256, 0, s>>>(b0, b1, changed, iters, ng, tot);
   return cudaGetLastError();
