@@ -320,6 +320,7 @@ constexpr int kThreads = 256;
 struct SymWork {           // CUB temporary storage (grown on demand, stream-ordered)
   char* cub_tmp = nullptr;
   size_t cub_bytes = 0;
+  void* stat_part = nullptr;  // per-CTA partials of the level statistics
 };
 struct SymPartArgs {
   const int32_t* act;      // active DOFs, ascending (act[0, *nact))

@@ -2761,6 +2761,8 @@ struct Factorizer {
     sy_done.release(s);
     if (symw.cub_tmp) cudaFreeAsync(symw.cub_tmp, s);
     symw.cub_tmp = nullptr;
+    if (symw.stat_part) cudaFreeAsync(symw.stat_part, s);
+    symw.stat_part = nullptr;
     symw.cub_bytes = 0;
     for (void** q : {(void**)&d_scal, (void**)&d_tot, (void**)&d_lstat})
       if (*q) {

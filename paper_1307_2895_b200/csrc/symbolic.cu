@@ -22,6 +22,7 @@
 #include <climits>
 #include <cstdint>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "hifde_internal.h"
@@ -467,64 +468,94 @@ __global__ void elim_fill_kernel(const SymFront P, ElimFillArgs A) {
   }
 }
 
-// per-level statistics of an elimination level (one CTA, fixed order: deterministic)
-__global__ void elim_stats_kernel(const int32_t* __restrict__ ng, const double4* __restrict__ cs,
-                                  const uint8_t* __restrict__ cls, const SymFront P, LevelStat* st,
-                                  const int64_t* __restrict__ nblk_inc, int64_t* nblk) {
-  __shared__ double red[8][256];
-  const int n = *ng;
-  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int64_t mx_nc = 0, mx_nq = 0, mf = 0, rows = 0, mfront = 0;
-  for (int g = threadIdx.x; g < n; g += 256) {
-    const double4 v = cs[g];
-    const int c = cls[g];
-    a[0] += v.x;
-    a[1] += v.y;
-    a[2 + 2 * c] += v.x;
-    a[3 + 2 * c] += v.y;
-    a[6] += v.w;
-    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g];
-    mf += (int64_t)v.z;
-    rows += nc + nq;
-    mx_nc = max(mx_nc, (int64_t)nc);
-    mx_nq = max(mx_nq, (int64_t)nq);
-    mfront = max(mfront, (int64_t)(nc + nq));
-  }
-  for (int i = 0; i < 7; ++i) red[i][threadIdx.x] = a[i];
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-      for (int i = 0; i < 7; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + s];
+// ---- level statistics: two-stage reduction in a fixed order (deterministic)
+struct StatAcc {
+  double d[8];
+  int64_t sum[4], mx[4];
+};
+constexpr int kStatGrid = 148;
+
+__device__ void stat_block_reduce(StatAcc& a, StatAcc* out) {
+  __shared__ double rd[256];
+  __shared__ int64_t ri[256];
+  for (int i = 0; i < 8; ++i) {
+    rd[threadIdx.x] = a.d[i];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) rd[threadIdx.x] += rd[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out->d[i] = rd[0];
     __syncthreads();
   }
-  typedef cub::BlockReduce<int64_t, 256> R;
-  __shared__ typename R::TempStorage rt;
-  const int64_t s_mf = R(rt).Sum(mf);
-  __syncthreads();
-  const int64_t s_rows = R(rt).Sum(rows);
-  __syncthreads();
-  const int64_t m_nc = R(rt).Reduce(mx_nc, cub::Max());
-  __syncthreads();
-  const int64_t m_nq = R(rt).Reduce(mx_nq, cub::Max());
-  __syncthreads();
-  const int64_t m_front = R(rt).Reduce(mfront, cub::Max());
-  if (threadIdx.x == 0) {
-    st->ngroups = n;
-    st->gflop = red[0][0];
-    st->gbytes = red[1][0];
-    st->gf_cls[0] = red[2][0];
-    st->gb_cls[0] = red[3][0];
-    st->gf_cls[1] = red[4][0];
-    st->gb_cls[1] = red[5][0];
-    st->solve_fac = red[6][0];
-    st->solve_rows = (double)s_rows;
-    st->mf_bytes = s_mf;
-    st->nrecs = n;
-    st->max_nc = m_nc;
-    st->max_nq = m_nq;
-    st->max_front = m_front;
-    *nblk += *nblk_inc;
+  for (int i = 0; i < 8; ++i) {
+    ri[threadIdx.x] = i < 4 ? a.sum[i] : a.mx[i - 4];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) ri[threadIdx.x] = i < 4 ? ri[threadIdx.x] + ri[threadIdx.x + s] : max(ri[threadIdx.x], ri[threadIdx.x + s]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      if (i < 4) out->sum[i] = ri[0];
+      else out->mx[i - 4] = ri[0];
+    }
+    __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(256) elim_stats_part(const int32_t* __restrict__ ng, const double4* __restrict__ cs,
+                                                       const uint8_t* __restrict__ cls, const SymFront P,
+                                                       StatAcc* __restrict__ part) {
+  const int n = *ng;
+  const int lo = (int)((int64_t)n * blockIdx.x / gridDim.x), hi = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
+  StatAcc a;
+  for (int i = 0; i < 8; ++i) a.d[i] = 0.0;
+  for (int i = 0; i < 4; ++i) a.sum[i] = a.mx[i] = 0;
+  for (int g = lo + threadIdx.x; g < hi; g += 256) {
+    const double4 v = cs[g];
+    const int c = cls[g];
+    a.d[0] += v.x;
+    a.d[1] += v.y;
+    a.d[2 + 2 * c] += v.x;
+    a.d[3 + 2 * c] += v.y;
+    a.d[6] += v.w;
+    const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g];
+    a.sum[0] += (int64_t)v.z;
+    a.sum[1] += nc + nq;
+    a.mx[0] = max(a.mx[0], (int64_t)nc);
+    a.mx[1] = max(a.mx[1], (int64_t)nq);
+    a.mx[2] = max(a.mx[2], (int64_t)(nc + nq));
+  }
+  stat_block_reduce(a, part + blockIdx.x);
+}
+
+__global__ void elim_stats_final(const int32_t* __restrict__ ng, const StatAcc* __restrict__ part, int np,
+                                 LevelStat* st, const int64_t* __restrict__ nblk_inc, int64_t* nblk) {
+  if (threadIdx.x != 0) return;
+  StatAcc a = part[0];
+  for (int b = 1; b < np; ++b) {
+    for (int i = 0; i < 8; ++i) a.d[i] += part[b].d[i];
+    for (int i = 0; i < 4; ++i) {
+      a.sum[i] += part[b].sum[i];
+      a.mx[i] = max(a.mx[i], part[b].mx[i]);
+    }
+  }
+  const int n = *ng;
+  st->ngroups = n;
+  st->gflop = a.d[0];
+  st->gbytes = a.d[1];
+  st->gf_cls[0] = a.d[2];
+  st->gb_cls[0] = a.d[3];
+  st->gf_cls[1] = a.d[4];
+  st->gb_cls[1] = a.d[5];
+  st->solve_fac = a.d[6];
+  st->solve_rows = (double)a.sum[1];
+  st->mf_bytes = a.sum[0];
+  st->nrecs = n;
+  st->max_nc = a.mx[0];
+  st->max_nq = a.mx[1];
+  st->max_front = a.mx[2];
+  *nblk += *nblk_inc;
 }
 
 // ---------------------------------------------------------------------------
@@ -622,6 +653,33 @@ __global__ void skel_relax_kernel(const int64_t* __restrict__ pred_start, const 
   }
 }
 
+// The same sweeps in one cooperative launch (grid-wide barrier between
+// sweeps), stopping once a sweep changed nothing: a 2D fine level's 65 sweeps
+// cost one launch instead of 65.
+__global__ void __launch_bounds__(256) skel_relax_coop(const int64_t* __restrict__ pred_start,
+                                                       const int32_t* __restrict__ npred,
+                                                       const int32_t* __restrict__ preds,
+                                                       const int32_t* __restrict__ ng, int32_t* b0, int32_t* b1,
+                                                       int32_t* changed, int iters) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int n = *ng;
+  for (int it = 0; it < iters; ++it) {
+    if (it > 0 && __ldcg(changed + it - 1) == 0) break;  // uniform: read after the barrier
+    const int32_t* bin = (it % 2 == 0) ? b0 : b1;
+    int32_t* bout = (it % 2 == 0) ? b1 : b0;
+    int ch = 0;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+      int b = 0;
+      const int64_t p0 = pred_start[t];
+      for (int64_t p = p0; p < p0 + npred[t]; ++p) b = max(b, __ldcg(bin + preds[p]) + 1);
+      __stcg(bout + t, b);
+      ch |= b != __ldcg(bin + t);
+    }
+    if (__syncthreads_or(ch) && threadIdx.x == 0) atomicExch(changed + it, 1);
+    grid.sync();
+  }
+}
+
 __global__ void skel_chain_kernel(const int32_t* __restrict__ b0, const int32_t* __restrict__ b1,
                                   const int32_t* __restrict__ changed, int iters, const int32_t* __restrict__ ng,
                                   LevelTotals* tot) {
@@ -711,74 +769,66 @@ __global__ void skel_finish_fill(const SkelTask* __restrict__ tasks, const int32
   }
 }
 
-__global__ void skel_stats_kernel(const SkelTask* __restrict__ tasks, const int32_t* __restrict__ kout,
-                                  const int32_t* __restrict__ ng, const int2* __restrict__ exc,
-                                  const int2* __restrict__ inc, LevelStat* st, int64_t* nblk) {
-  __shared__ double red[4][256];
-  typedef cub::BlockReduce<int64_t, 256> R;
-  __shared__ typename R::TempStorage rt;
+__global__ void __launch_bounds__(256) skel_stats_part(const SkelTask* __restrict__ tasks,
+                                                       const int32_t* __restrict__ kout, const int32_t* __restrict__ ng,
+                                                       StatAcc* __restrict__ part) {
   const int n = *ng;
-  double fl = 0, by = 0, sf = 0, sr = 0;
-  int64_t nsk = 0, nrd = 0, mf = 0, mnc = 0, mnq = 0, mfront = 0;
-  for (int g = threadIdx.x; g < n; g += 256) {
+  const int lo = (int)((int64_t)n * blockIdx.x / gridDim.x), hi = (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
+  StatAcc a;
+  for (int i = 0; i < 8; ++i) a.d[i] = 0.0;
+  for (int i = 0; i < 4; ++i) a.sum[i] = a.mx[i] = 0;
+  for (int g = lo + threadIdx.x; g < hi; g += 256) {
     const SkelTask& T = tasks[g];
     const int kk = kout[g], r = T.nc - kk;
-    nsk += kk;
-    nrd += r;
-    mfront = max(mfront, (int64_t)(T.nc + T.nq));
+    a.sum[0] += kk;
+    a.sum[1] += r;
+    a.mx[2] = max(a.mx[2], (int64_t)(T.nc + T.nq));
     const double dc = T.nc, dq = T.nq, dk = kk, dr = r;
     double f = 4 * dq * dc * dk - 2 * dk * dk * (dq + dc) + 4 * dk * dk * dk / 3 + 2 * dq * dc + dk * dk * dr +
                2 * dk * dk * dr + 4 * dk * dr * dr;
     if (r > 0) f += dr * dr * dr / 3 + dr * dr * dk + dk * dk * dr;
-    fl += f * 1e-9;
-    by += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
+    a.d[0] += f * 1e-9;
+    a.d[1] += 8.0 * (dq * dc + dc * dc + dk * dr + dr * dr + dr + dr * dk + 2 * dk * dk) * 1e-9;
     if (r > 0) {
-      mf += 8 * ((int64_t)kk * r + (int64_t)r * r + r + (int64_t)r * kk);
-      sf += dr * (dr + 1) / 2 + 2 * dr * dk;
-      sr += dr + dk;
-      mnc = max(mnc, (int64_t)r);
-      mnq = max(mnq, (int64_t)kk);
+      a.sum[2] += 8 * ((int64_t)kk * r + (int64_t)r * r + r + (int64_t)r * kk);
+      a.d[2] += dr * (dr + 1) / 2 + 2 * dr * dk;
+      a.d[3] += dr + dk;
+      a.mx[0] = max(a.mx[0], (int64_t)r);
+      a.mx[1] = max(a.mx[1], (int64_t)kk);
     }
   }
-  red[0][threadIdx.x] = fl;
-  red[1][threadIdx.x] = by;
-  red[2][threadIdx.x] = sf;
-  red[3][threadIdx.x] = sr;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-      for (int i = 0; i < 4; ++i) red[i][threadIdx.x] += red[i][threadIdx.x + s];
-    __syncthreads();
+  stat_block_reduce(a, part + blockIdx.x);
+}
+
+__global__ void skel_stats_final(const int32_t* __restrict__ ng, const StatAcc* __restrict__ part, int np,
+                                 const int2* __restrict__ exc, const int2* __restrict__ inc, LevelStat* st,
+                                 int64_t* nblk) {
+  if (threadIdx.x != 0) return;
+  StatAcc a = part[0];
+  for (int b = 1; b < np; ++b) {
+    for (int i = 0; i < 8; ++i) a.d[i] += part[b].d[i];
+    for (int i = 0; i < 4; ++i) {
+      a.sum[i] += part[b].sum[i];
+      a.mx[i] = max(a.mx[i], part[b].mx[i]);
+    }
   }
-  const int64_t s_nsk = R(rt).Sum(nsk);
-  __syncthreads();
-  const int64_t s_nrd = R(rt).Sum(nrd);
-  __syncthreads();
-  const int64_t s_mf = R(rt).Sum(mf);
-  __syncthreads();
-  const int64_t m_nc = R(rt).Reduce(mnc, cub::Max());
-  __syncthreads();
-  const int64_t m_nq = R(rt).Reduce(mnq, cub::Max());
-  __syncthreads();
-  const int64_t m_front = R(rt).Reduce(mfront, cub::Max());
-  if (threadIdx.x == 0) {
-    st->ngroups = n;
-    st->nskel = s_nsk;
-    st->nred = s_nrd;
-    st->gflop = red[0][0];
-    st->gbytes = red[1][0];
-    st->gf_cls[0] = red[0][0];
-    st->gb_cls[0] = red[1][0];
-    st->solve_fac = red[2][0];
-    st->solve_rows = red[3][0];
-    st->mf_bytes = s_mf;
-    st->max_nc = m_nc;
-    st->max_nq = m_nq;
-    st->max_front = m_front;
-    const int2 last = n ? make_int2(exc[n - 1].x + inc[n - 1].x, exc[n - 1].y + inc[n - 1].y) : make_int2(0, 0);
-    st->nrecs = last.y;
-    *nblk += last.x;
-  }
+  const int n = *ng;
+  st->ngroups = n;
+  st->nskel = a.sum[0];
+  st->nred = a.sum[1];
+  st->gflop = a.d[0];
+  st->gbytes = a.d[1];
+  st->gf_cls[0] = a.d[0];
+  st->gb_cls[0] = a.d[1];
+  st->solve_fac = a.d[2];
+  st->solve_rows = a.d[3];
+  st->mf_bytes = a.sum[2];
+  st->max_nc = a.mx[0];
+  st->max_nq = a.mx[1];
+  st->max_front = a.mx[2];
+  const int2 last = n ? make_int2(exc[n - 1].x + inc[n - 1].x, exc[n - 1].y + inc[n - 1].y) : make_int2(0, 0);
+  st->nrecs = last.y;
+  *nblk += last.x;
 }
 
 // active DOFs -> ascending list (and the count into the previous level's stats)
@@ -800,6 +850,12 @@ int sym_grid(int per_sm) {
   return nsm * per_sm;
 }
 }  // namespace
+
+// per-CTA partials of the level statistics (persistent, SymWork-owned)
+static StatAcc* stat_parts(SymWork& W, cudaStream_t s) {
+  if (!W.stat_part) cudaMallocAsync(&W.stat_part, sizeof(StatAcc) * kStatGrid, s);
+  return reinterpret_cast<StatAcc*>(W.stat_part);
+}
 
 // temp storage for CUB calls lives at the front of W.cub_tmp; the launcher
 // grows it (stream-ordered) when a call needs more
@@ -920,7 +976,9 @@ cudaError_t sym_elim_sizes(const SymFront& P, int is_top, int ng_ub, ElimInc* in
 
 cudaError_t sym_elim_fill(const SymFront& P, const ElimFillArgs& A, int64_t nred_ub, SymWork& W, cudaStream_t s) {
   elim_fill_kernel<<<sym_grid(4), 256, 0, s>>>(P, A);
-  elim_stats_kernel<<<1, 256, 0, s>>>(P.ng, A.cellstat, A.cellcls, P, A.stat, A.newblk_total, A.nblk);
+  StatAcc* part = stat_parts(W, s);
+  elim_stats_part<<<kStatGrid, 256, 0, s>>>(P.ng, A.cellstat, A.cellcls, P, part);
+  elim_stats_final<<<1, 32, 0, s>>>(P.ng, part, kStatGrid, A.stat, A.newblk_total, A.nblk);
   // reduction of the forward sweep: contribution rows grouped by neighbour
   // DOF in record order (stable radix sort), targets = the distinct DOFs
   if (nred_ub > 0) {
@@ -975,12 +1033,13 @@ cudaError_t sym_skel_chain(const int64_t* pred_start, const int32_t* npred, cons
                            cudaStream_t s) {
   cudaMemsetAsync(b0, 0, sizeof(int32_t) * (size_t)ng_ub, s);
   cudaMemsetAsync(changed, 0, sizeof(int32_t) * (size_t)iters, s);
-  const int grid = std::max(1, std::min(sym_grid(4), (ng_ub + 255) / 256));
-  for (int it = 0; it < iters; ++it) {
-    const int32_t* bin = (it % 2 == 0) ? b0 : b1;
-    int32_t* bout = (it % 2 == 0) ? b1 : b0;
-    skel_relax_kernel<<<grid, 256, 0, s>>>(pred_start, npred, preds, ng, bin, bout, changed, it);
-  }
+  static int per_sm = 0;
+  if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skel_relax_coop, 256, 0);
+  const int grid = std::max(1, std::min(sym_grid(std::max(per_sm, 1)), (ng_ub + 255) / 256));
+  void* args[] = {(void*)&pred_start, (void*)&npred, (void*)&preds, (void*)&ng, (void*)&b0, (void*)&b1,
+                  (void*)&changed, (void*)&iters};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)skel_relax_coop, dim3((unsigned)grid), dim3(256), args, 0, s);
+  if (e != cudaSuccess) return e;
   skel_chain_kernel<<<1, 256, 0, s>>>(b0, b1, changed, iters, ng, tot);
   return cudaGetLastError();
 }
@@ -1016,7 +1075,9 @@ cudaError_t sym_skel_finish(const SkelTask* tasks, const int32_t* kout, const in
   cudaError_t e = cub::DeviceScan::ExclusiveScan(W.cub_tmp, tb, inc, exc, Int2Sum(), make_int2(0, 0), ng_ub, s);
   if (e != cudaSuccess) return e;
   skel_finish_fill<<<grid, 256, 0, s>>>(tasks, kout, ng, exc, A);
-  skel_stats_kernel<<<1, 256, 0, s>>>(tasks, kout, ng, exc, inc, A.stat, A.nblk);
+  StatAcc* part = stat_parts(W, s);
+  skel_stats_part<<<kStatGrid, 256, 0, s>>>(tasks, kout, ng, part);
+  skel_stats_final<<<1, 32, 0, s>>>(ng, part, kStatGrid, exc, inc, A.stat, A.nblk);
   return cudaGetLastError();
 }
 
