@@ -172,6 +172,18 @@ int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n,
                 int nrhs, int device_ptrs, void* stream);
 
 /*
+ * Page-locked host blocks from the library's caching pool, for solve/apply
+ * outputs (and inputs): hifde_solve DMAs a result straight into such a block,
+ * and a freed block is reused by the next request of about its size, so
+ * repeated solves pay neither the pinning nor the page faults of a fresh
+ * multi-GB host array.  No reference counterpart (the reference returns a
+ * fresh numpy array from apply_inverse, src/driver.py:113-129; the Python
+ * shim wraps these blocks in numpy arrays with the same semantics).
+ */
+int hifde_host_alloc(size_t bytes, void** out);
+int hifde_host_free(void* p);
+
+/*
  * y = F x (the factored operator, ~ A x), same layout and pointer rules as
  * hifde_solve; apply(apply_inverse(b)) == b up to rounding.
  */

@@ -90,7 +90,7 @@ class KernelStat(C.Structure):  # hifde_kernel_stat_t
 # every symbol the public header declares
 EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
-    "hifde_solve", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count", "hifde_kernel_stats",
+    "hifde_solve", "hifde_host_alloc", "hifde_host_free", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count", "hifde_kernel_stats",
     "hifde_free", "hifde_last_error", "hifde_partition",
     "hifde_comm_unique_id", "hifde_comm_init", "hifde_comm_emulated", "hifde_comm_host", "hifde_comm_info",
     "hifde_comm_free",
@@ -148,6 +148,10 @@ def load(path: str | None = None):
     lib.hifde_last_launch_count.restype = C.c_int64
     lib.hifde_kernel_stats.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
     lib.hifde_kernel_stats.restype = C.c_int
+    lib.hifde_host_alloc.argtypes = [C.c_size_t, C.POINTER(C.c_void_p)]
+    lib.hifde_host_alloc.restype = C.c_int
+    lib.hifde_host_free.argtypes = [C.c_void_p]
+    lib.hifde_host_free.restype = C.c_int
     lib.hifde_free.argtypes = [C.c_void_p]
     lib.hifde_free.restype = None
     lib.hifde_last_error.restype = C.c_char_p

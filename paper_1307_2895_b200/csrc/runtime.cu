@@ -29,6 +29,7 @@
 #include <deque>
 #include <exception>
 #include <functional>
+#include <unordered_map>
 #include <thread>
 #include <future>
 #include <memory>
@@ -657,6 +658,15 @@ struct PinnedXfer {
   // while the other slot's DMAs run.
   void d2h_columns(double* x, int nrhs, const std::vector<double*>& vb, const std::vector<int>& c0, int64_t N,
                    const std::vector<cudaEvent_t>& es, cudaStream_t s) {
+    if (page_locked(x)) {  // page-locked output: each chunk's columns DMA'd straight into x
+      for (size_t c = 0; c + 1 < c0.size(); ++c) {
+        const int w = c0[c + 1] - c0[c];
+        HCK(cudaStreamWaitEvent(s, es[c], 0));
+        HCK(cudaMemcpy2DAsync(x + c0[c], (size_t)nrhs * sizeof(double), vb[c], (size_t)w * sizeof(double),
+                              (size_t)w * sizeof(double), (size_t)N, cudaMemcpyDeviceToHost, s));
+      }
+      return;
+    }
     int device = 0;
     HCK(cudaGetDevice(&device));
     std::lock_guard<std::mutex> lk(m);
@@ -711,6 +721,75 @@ struct PinnedXfer {
 PinnedXfer& pinned_xfer() {
   static PinnedXfer x;
   return x;
+}
+
+// Caching allocator of page-locked host blocks for solve/apply outputs
+// (hifde_host_alloc / hifde_host_free): the result of a solve is DMA'd
+// straight into its pages, and a freed block serves the next request of about
+// its size, so neither the pinning nor the first-touch faults of a fresh
+// multi-GB host array recur per call.  Free blocks beyond kCacheCap are
+// returned to the driver.
+struct HostPool {
+  static constexpr size_t kGran = (size_t)2 << 20;
+  static constexpr size_t kCacheCap = (size_t)16 << 30;
+  std::mutex m;
+  std::vector<std::pair<size_t, void*>> free_;  // cached blocks, most recently freed last
+  std::unordered_map<void*, size_t> live;       // block -> size
+  size_t cached = 0;
+  void* alloc(size_t bytes) {
+    const size_t want = (std::max<size_t>(bytes, 1) + kGran - 1) / kGran * kGran;
+    {
+      std::lock_guard<std::mutex> lk(m);
+      // the most recently freed block that fits without wasting over a quarter
+      for (size_t i = free_.size(); i-- > 0;) {
+        if (free_[i].first < want || free_[i].first > want + want / 4) continue;
+        void* p = free_[i].second;
+        live[p] = free_[i].first;
+        cached -= free_[i].first;
+        free_.erase(free_.begin() + (std::ptrdiff_t)i);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, want, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      trim(0);  // give the cached blocks back and retry once
+      if (cudaHostAlloc(&p, want, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+    }
+    std::lock_guard<std::mutex> lk(m);
+    live[p] = want;
+    return p;
+  }
+  bool release(void* p) {
+    std::lock_guard<std::mutex> lk(m);
+    auto it = live.find(p);
+    if (it == live.end()) return false;
+    free_.emplace_back(it->second, p);
+    cached += it->second;
+    live.erase(it);
+    trim_locked(kCacheCap);
+    return true;
+  }
+  void trim_locked(size_t keep) {  // least recently freed blocks go first
+    size_t i = 0;
+    while (cached > keep && i < free_.size()) {
+      cudaFreeHost(free_[i].second);
+      cached -= free_[i].first;
+      ++i;
+    }
+    free_.erase(free_.begin(), free_.begin() + (std::ptrdiff_t)i);
+  }
+  void trim(size_t keep) {
+    std::lock_guard<std::mutex> lk(m);
+    trim_locked(keep);
+  }
+};
+HostPool& host_pool() {
+  static HostPool p;
+  return p;
 }
 
 // One background host thread per factorization for work that only the solve
@@ -3978,11 +4057,18 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
 // large block: column chunks flow through three engines at once -- the H2D
 // copy engine uploads chunk c + 1 (a strided 2D DMA straight from the
 // caller's rows) while the SMs sweep chunk c and the D2H engine returns chunk
-// c - 1 through pinned pieces that host threads scatter into the caller's
-// columns.  Same result as one sweep of the whole block, column by column.
+// c - 1, by a strided DMA straight into the caller's columns when the output
+// is page-locked too (hifde_host_alloc blocks), else through pinned pieces
+// that host threads scatter.  Same result as one sweep of the whole block,
+// column by column.
 void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nrhs, cudaStream_t s) {
   const int64_t N = F->n;
-  const int nch = nrhs >= 64 ? 4 : 2;
+  // Two column chunks (one below 32 RHS): strided DMAs of 8-column (64 B)
+  // row pieces run at 24-28 GB/s, 16-column pieces at 47-51 GB/s alone and
+  // 71 GB/s both directions at once, 32-column pieces at 56-57 and 101 GB/s
+  // (tools/dma2d_probe.py).  Config 3, 64 RHS: 4 chunks of 16 columns 83 ms,
+  // 2 of 32 71 ms (H2D 2 x 19.3 + last sweep 10 + last D2H 21).
+  const int nch = nrhs >= 32 ? 2 : 1;
   std::vector<int> c0((size_t)nch + 1, 0);
   for (int c = 0; c < nch; ++c) c0[(size_t)c + 1] = (int)((int64_t)nrhs * (c + 1) / nch / 8 * 8);
   c0[(size_t)nch] = nrhs;
@@ -4438,6 +4524,32 @@ int hifde_import(int64_t n, int dim, double eps, int nlevels, const double* tags
     return HIFDE_INTERNAL;
   }
   *out = F.release();
+  return HIFDE_OK;
+}
+
+int hifde_host_alloc(size_t bytes, void** out) {
+  g_err.clear();
+  if (!out) { g_err = "null argument"; return HIFDE_BADARG; }
+  *out = nullptr;
+  try {
+    *out = host_pool().alloc(bytes);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
+  }
+  if (!*out) { g_err = "page-locked host allocation failed"; return HIFDE_CUDA; }
+  return HIFDE_OK;
+}
+
+int hifde_host_free(void* p) {
+  g_err.clear();
+  if (!p) return HIFDE_OK;
+  try {
+    if (!host_pool().release(p)) { g_err = "not a block of hifde_host_alloc"; return HIFDE_BADARG; }
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
+  }
   return HIFDE_OK;
 }
 

@@ -113,6 +113,18 @@ class GeneralizedLDL:
     def storage_bytes(self) -> int:
         return self.metrics["m_f_bytes"]
 
+    def _out(self, like: np.ndarray) -> np.ndarray:
+        """Output array for a host solve/apply: large results live in a
+        page-locked block of the library's caching pool (DMA'd straight into,
+        recycled when the array is garbage-collected); small ones are plain."""
+        if like.nbytes < _PINNED_MIN:
+            return np.empty_like(like)
+        blk = _PinnedBlock.get(self._lib, like.nbytes)
+        if blk is None:
+            return np.empty_like(like)
+        blk.__array_interface__ = {"shape": like.shape, "typestr": "<f8", "data": (blk.ptr, False), "version": 3}
+        return np.asarray(blk)
+
     def apply_inverse(self, b) -> np.ndarray:
         """x ~= A^{-1} b for b of shape (N,) or (N, nrhs); host arrays."""
         arr = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
@@ -120,7 +132,7 @@ class GeneralizedLDL:
         if arr.shape[0] != self.n:
             raise ValueError("right-hand side has the wrong length")
         nrhs = 1 if vec else arr.shape[1]
-        out = np.empty_like(arr)
+        out = self._out(arr)
         if arr.size:
             code = self._lib.hifde_solve(self._h, arr.ctypes.data, out.ctypes.data, self.n, nrhs, 0, None)
             if code:
@@ -133,7 +145,7 @@ class GeneralizedLDL:
         if arr.shape[0] != self.n:
             raise ValueError("vector has the wrong length")
         nrhs = 1 if arr.ndim == 1 else arr.shape[1]
-        out = np.empty_like(arr)
+        out = self._out(arr)
         if arr.size:
             code = self._lib.hifde_apply(self._h, arr.ctypes.data, out.ctypes.data, self.n, nrhs, 0, None)
             if code:
@@ -177,6 +189,31 @@ class GeneralizedLDL:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+_PINNED_MIN = 8 << 20
+
+
+class _PinnedBlock:
+    """Owner of one hifde_host_alloc block; the numpy array built on it keeps
+    it alive (array base) and the block returns to the pool with it."""
+
+    __slots__ = ("ptr", "lib", "__array_interface__", "__weakref__")
+
+    @classmethod
+    def get(cls, lib, nbytes: int):
+        p = C.c_void_p()
+        if lib.hifde_host_alloc(nbytes, C.byref(p)) or not p.value:
+            return None
+        blk = cls()
+        blk.ptr, blk.lib = p.value, lib
+        return blk
+
+    def __del__(self):
+        try:
+            self.lib.hifde_host_free(C.c_void_p(self.ptr))
         except Exception:
             pass
 

@@ -432,3 +432,36 @@ def test_pipelined_host_solve_matches_one_block_solve():
     y1 = f.apply_inverse(b40.numpy())
     y2 = f.apply_inverse(b40.numpy().copy())
     assert np.linalg.norm(y1 - y2) <= 1e-13 * np.linalg.norm(y2)
+
+
+def test_host_output_paths_agree_and_pool_recycles():
+    """Large host results land in page-locked blocks of the library's pool
+    (hifde_host_alloc): the DMA-straight-in result must equal the staged copy
+    into a pageable caller buffer (hifde_solve on a plain numpy array) and the
+    device-resident solve, and a freed block must serve the next solve."""
+    import ctypes as C
+    import torch
+    g, a, eps, variant, nrhs = H.baseline_problem(2)
+    f = H.factor_hifde(a, g, eps)
+    b = torch.from_numpy(np.random.default_rng(5).standard_normal((g.ndof, 32))).pin_memory()
+    x_pool = f.apply_inverse(b.numpy())
+    assert x_pool.base is not None and x_pool.flags.writeable
+    x_page = np.empty((g.ndof, 32))
+    code = f._lib.hifde_solve(f.handle, b.numpy().ctypes.data, x_page.ctypes.data, g.ndof, 32, 0, None)
+    assert code == 0
+    bd = b.cuda()
+    xd = torch.empty_like(bd)
+    f.apply_inverse_device(bd.data_ptr(), xd.data_ptr(), 32)
+    torch.cuda.synchronize()
+    x_dev = xd.cpu().numpy()
+    for x in (x_pool, x_page):
+        assert np.linalg.norm(x - x_dev) <= 1e-13 * np.linalg.norm(x_dev)
+    ptr = x_pool.ctypes.data
+    del x_pool
+    import gc
+    gc.collect()
+    x_again = f.apply_inverse(b.numpy())
+    assert x_again.ctypes.data == ptr
+    assert np.linalg.norm(x_again - x_dev) <= 1e-13 * np.linalg.norm(x_dev)
+    y = f.apply(x_again)  # apply's output takes the pool as well
+    assert np.linalg.norm(y - b.numpy()) <= 1e-8 * np.linalg.norm(b.numpy())

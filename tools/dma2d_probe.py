@@ -1,24 +1,45 @@
-"""H2D / D2H rate of strided 2D DMA (column chunks of a row-major block) vs 1D."""
+"""PCIe DMA rates for the pipelined host solve: strided 2D copies of column
+chunks of a row-major N x 64 block (widths 8-32 columns), alone and with the
+opposite direction running at the same time, against contiguous 1D copies."""
 import time
-import numpy as np, torch
+import torch
 from cuda.bindings import runtime as rt
 N, R = 4190209, 64
-h = torch.empty((N, R), dtype=torch.float64).pin_memory()
-d = torch.empty((N, 16), dtype=torch.float64, device="cuda")
-d64 = torch.empty((N, R), dtype=torch.float64, device="cuda")
-torch.cuda.synchronize()
-for w in (16, 32):
-    dd = torch.empty((N, w), dtype=torch.float64, device="cuda")
-    for rep in range(2):
-        t = time.perf_counter()
-        err, = rt.cudaMemcpy2D(dd.data_ptr(), w * 8, h.data_ptr(), R * 8, w * 8, N, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter() - t
-        t = time.perf_counter()
-        err, = rt.cudaMemcpy2D(h.data_ptr(), R * 8, dd.data_ptr(), w * 8, w * 8, N, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost)
-        torch.cuda.synchronize()
-        t2 = time.perf_counter() - t
-        gb = N * w * 8 / 1e9
-        print(f"w={w}: 2D H2D {gb/t1:.1f} GB/s  2D D2H {gb/t2:.1f} GB/s", flush=True)
-t = time.perf_counter(); d64.copy_(h, non_blocking=True); torch.cuda.synchronize(); t1 = time.perf_counter() - t
-print(f"1D H2D {N*R*8/1e9/t1:.1f} GB/s")
+H2D, D2H = rt.cudaMemcpyKind.cudaMemcpyHostToDevice, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost
+hi = torch.empty((N, R), dtype=torch.float64).pin_memory()
+ho = torch.empty((N, R), dtype=torch.float64).pin_memory()
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def run(w, both):
+    da = torch.empty((N, R), dtype=torch.float64, device="cuda")
+    db = torch.empty((N, R), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for c in range(0, R, w):
+        rt.cudaMemcpy2DAsync(da.data_ptr() + c * N * 8, w * 8, hi.data_ptr() + c * 8, R * 8, w * 8, N, H2D,
+                             s1.cuda_stream)
+        if both:
+            rt.cudaMemcpy2DAsync(ho.data_ptr() + c * 8, R * 8, db.data_ptr() + c * N * 8, w * 8, w * 8, N, D2H,
+                                 s2.cuda_stream)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t) * 1e3
+
+
+def run_d2h(w):
+    db = torch.empty((N, R), dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for c in range(0, R, w):
+        rt.cudaMemcpy2DAsync(ho.data_ptr() + c * 8, R * 8, db.data_ptr() + c * N * 8, w * 8, w * 8, N, D2H,
+                             s2.cuda_stream)
+    torch.cuda.synchronize()
+    return (time.perf_counter() - t) * 1e3
+
+
+gb = N * R * 8 / 1e9
+for rep in range(2):
+    for w in (8, 16, 32, 64):
+        a, b, c = run(w, False), run_d2h(w), run(w, True)
+        print(f"w={w:2d}: H2D {gb / a * 1e3:5.1f} GB/s ({a:.1f} ms) | D2H {gb / b * 1e3:5.1f} GB/s ({b:.1f} ms) | "
+              f"both at once {c:.1f} ms ({2 * gb / c * 1e3:5.1f} GB/s total)", flush=True)
