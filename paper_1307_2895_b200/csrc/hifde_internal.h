@@ -274,8 +274,9 @@ void launch_skelbig_symm(const SkelBigTask* tasks, const int4* work, int nwork, 
 // solve
 // small elimination records (nc, nq <= 64, 2..16 RHS): one shared-memory load phase
 size_t solve_small_smem(int max_nc, int max_nq, int nrhs);
-void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
-                             int nrhs, double* contrib, size_t smem, int forward, cudaStream_t s);
+void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, int64_t fac_len,
+                             double* v, int nrhs, double* contrib, int max_nc, int max_nq, size_t smem, int forward,
+                             cudaStream_t s);
 size_t solve_skel_small_smem(int max_r, int max_k, int nrhs);
 void launch_solve_skel_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
                              int nrhs, size_t smem, int forward, cudaStream_t s);

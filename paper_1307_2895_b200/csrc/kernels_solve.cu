@@ -14,7 +14,9 @@
 // Fine levels (records up to 96 x 192) use the single-load-phase kernels
 // (solve_*_small_kernel); 48+ right-hand sides take the DMMA products in the
 // general kernels; both sum in cta_gemm's order where they replace it.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "hifde_internal.h"
 
@@ -590,6 +592,99 @@ __device__ __forceinline__ void warp_mma(int M, int K, const double* __restrict_
   }
 }
 
+// warp_mma for the pipelined kernels (registers to spare at one CTA per SM):
+// the per-tile address arithmetic (packed-row bases, row strides, bounds) is
+// hoisted out of the k loop; each DMMA then costs one shared load of A, a
+// compare and the MMA (the loop was issue-bound on index math: ncu, config 3
+// level 0, 56% issue slots busy).  Tile k steps and zero padding are as
+// before, so the sums are unchanged bit for bit.
+struct NoPre {
+  __device__ void operator()() const {}
+};
+template <int AM, bool kOne = false, int MJ = kMmaMaxJ, class Out, class Pre = NoPre>
+__device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double* __restrict__ A, int lda, const double* X,
+                                              int ldx, int R, Out out, Pre pre = Pre{}) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31;
+  const int mt = (M + 7) >> 3, ntr = (R + 7) >> 3, npair = mt * ntr;
+  const int ar = lane >> 2, ak = lane & 3;
+  const bool one_rt = NW % ntr == 0;  // every pair of this warp in RHS tile w % ntr
+  // this warp's tile pairs p = w + NW j: with one RHS tile per warp the row
+  // tile is m0 + j * dm (no division in the k loop)
+  const int nj = w < npair ? (npair - 1 - w) / NW + 1 : 0;
+  const int m0 = w / ntr, dm = NW / ntr, r0 = w - m0 * ntr;
+  auto tmj = [&](int j) { return one_rt ? m0 + j * dm : (w + NW * j) / ntr; };
+  auto trj = [&](int j) { return one_rt ? r0 : (w + NW * j) % ntr; };
+  // pairs in batches of MJ accumulators (M up to 192 rows: 24 row tiles)
+  // kOne: exactly one pass, also for a warp without tiles, so that `pre`
+  // (a group barrier between the k loops and the in-place outputs) is met by
+  // every warp
+  for (int jb = 0; kOne ? jb == 0 : jb < nj; jb += MJ) {
+    const int nb = max(0, min(MJ, nj - jb));
+    double acc[MJ][2];
+    int ibase[MJ];  // per tile: the A offset of (row i, k = 0), or -1 past M
+    int klim[MJ];   // per tile: the k0 bound of its nonzero A columns
+    int irow[MJ];   // per tile: this lane's A row
+    int xcol[MJ];   // per tile (several RHS tiles per warp): its X column
+#pragma unroll
+    for (int j = 0; j < MJ; ++j) {
+      acc[j][0] = acc[j][1] = 0.0;
+      const int mi = j < nb ? tmj(jb + j) : 0;
+      const int i = 8 * mi + ar;
+      int base;
+      if (AM == 0) base = i * (i + 1) / 2;
+      else if (AM == 1) base = i;
+      else if (AM == 2) base = i * lda;
+      else base = i;
+      ibase[j] = (j < nb && i < M) ? base : -1;
+      irow[j] = i;
+      klim[j] = AM == 0 ? 8 * mi + 8 : 8 * mi;  // AM 0: k0 < klim; AM 1: k0 + 4 > klim
+      xcol[j] = j < nb ? 8 * trj(jb + j) + ar : R;
+    }
+    int klo = 0, khi = nb > 0 ? K : 0;
+    if (AM == 0 && nb > 0) khi = min(K, 8 * tmj(jb + nb - 1) + 8);
+    if (AM == 1) klo = 8 * tmj(jb);
+    const int cfix = 8 * r0 + ar;
+    for (int k0 = klo & ~3; k0 < khi; k0 += 4) {
+      const int k = k0 + ak;
+      const bool kin = k < K;
+      double b0 = 0.0;
+      if (one_rt) b0 = (kin && cfix < R) ? X[k * ldx + cfix] : 0.0;
+      int koff;  // the k part of A's offset
+      if (AM == 0) koff = k;
+      else if (AM == 1) koff = k * (k + 1) / 2;
+      else if (AM == 2) koff = k;
+      else koff = k * lda;
+#pragma unroll
+      for (int j = 0; j < MJ; ++j) {
+        if (j >= nb) break;
+        if (AM == 0 && k0 >= klim[j]) continue;      // above the diagonal: zero
+        if (AM == 1 && k0 + 4 <= klim[j]) continue;  // below it (transpose): zero
+        const int i = ibase[j];
+        bool nz = i >= 0 && kin;
+        if (AM == 0) nz = nz && k <= irow[j];  // lower triangle
+        if (AM == 1) nz = nz && k >= irow[j];  // its transpose
+        const double a = nz ? A[i + koff] : 0.0;
+        double b = b0;
+        if (!one_rt) {
+          const int c = xcol[j];
+          b = (kin && c < R) ? X[k * ldx + c] : 0.0;
+        }
+        dmma_8x8x4(acc[j][0], acc[j][1], a, b);
+      }
+    }
+    pre();
+#pragma unroll
+    for (int j = 0; j < MJ; ++j) {
+      if (j >= nb) break;
+      const int row = 8 * tmj(jb + j) + (lane >> 2);
+      if (row >= M) continue;
+      const int col = 8 * trj(jb + j) + 2 * (lane & 3);
+      if (col < R) out(row, col, acc[j][0], acc[j][1]);  // R even: both columns valid
+    }
+  }
+}
+
 // forward: s = P x_c -> v_c ; g = W^T s -> contribution rows
 __global__ void __launch_bounds__(NT, 3) solve_elim_fwd_mma_kernel(const SolveRec* __restrict__ recs,
                                                                 const int32_t* __restrict__ idx,
@@ -678,6 +773,212 @@ __global__ void __launch_bounds__(NT, 3) solve_elim_bwd_mma_kernel(const SolveRe
   }
   warp_mma<1>(nc, nc, sP, 0, st, ld, R, [&](int row, int col, double val, int j_, int h_) { v[(size_t)c[row] * R + col] = val; });
 }
+
+// ---------------------------------------------------------------------------
+// Pipelined elimination-record solve for the fine levels (thousands of
+// records of one small shape, 8+ right-hand sides): one persistent CTA per
+// SM.  A producer warp streams the CTA's next records -- P, W and the
+// gathered rows of v -- into a ring of S shared-memory stages with TMA bulk
+// copies (cp.async.bulk, completion counted on the stage's `full` mbarrier),
+// while eight consumer warps run the current record's DMMA products
+// (warp_mma: the tiles and summation order of the one-record kernels above,
+// so the results are bit-identical) and release the stage on its `empty`
+// mbarrier.  The one-record kernels expose a load phase per record with 3
+// CTAs per SM (ncu, config 3 level 0: long-scoreboard stalls on the gathers,
+// 1.5 TB/s); here the loads of records k+1 .. k+S-1 overlap record k's math.
+// ---------------------------------------------------------------------------
+namespace pipe {
+constexpr int kGroup = 256;     // consumer group: 8 warps (warp_mma's tile assignment)
+constexpr int kMaxStages = 4;
+constexpr int kPipeMJ = 8;      // tile pairs per warp and batch (64 rows x 64 RHS in one batch)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned tx) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok)
+                 : "r"(smem_u32(b)), "r"(parity)
+                 : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void group_sync(int g) { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kGroup) : "memory"); }
+
+// Per-stage layout (doubles, every region 16-byte aligned): P (np + 2),
+// W (nc nq + 2), x_c (nc ld), x_q (nq ld, backward); then ints: c (nc),
+// q (nq), meta (8).
+struct StageGeom {
+  int offW, offX, offQ, offI, doubles;  // offsets in doubles; offI: int region
+  __host__ __device__ static int even(int x) { return (x + 1) & ~1; }
+  __host__ __device__ StageGeom(int max_nc, int max_nq, int ld, bool bwd) {
+    const int np = max_nc * (max_nc + 1) / 2;
+    offW = even(np + 2);
+    offX = offW + even(max_nc * max_nq + 2);
+    offQ = offX + max_nc * ld;
+    offI = offQ + (bwd ? max_nq * ld : 0);
+    doubles = offI + even((max_nc + max_nq + 8 + 1) / 2 + 1);
+  }
+};
+
+// The byte range [src, src + bytes) rounded out to 16-byte granules, if it
+// stays inside the arena; `ph` = doubles of lead-in in the staged copy.
+__device__ __forceinline__ bool granules(const double* src, int n, const double* lo, const double* hi,
+                                         const double*& a0, unsigned& bytes, int& ph) {
+  const uintptr_t s = (uintptr_t)src, e = (uintptr_t)(src + n);
+  const uintptr_t s0 = s & ~(uintptr_t)15, e0 = (e + 15) & ~(uintptr_t)15;
+  a0 = (const double*)s0;
+  bytes = (unsigned)(e0 - s0);
+  ph = (int)((s - s0) >> 3);
+  return s0 >= (uintptr_t)lo && e0 <= (uintptr_t)hi;
+}
+
+// NG consumer groups take the CTA's records in turn (record k: group k % NG).
+template <bool kFwd, int NG>
+__global__ void __launch_bounds__(NG * kGroup + 32, 1)
+    solve_elim_pipe_kernel(const SolveRec* __restrict__ recs, int nrec, const int32_t* __restrict__ idx,
+                           const double* __restrict__ fac, int64_t fac_len, double* __restrict__ v, int R,
+                           double* __restrict__ contrib, int max_nc, int max_nq, int nstages) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  const int ld = mma_ld(R);
+  const StageGeom sg(max_nc, max_nq, ld, !kFwd);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], kGroup / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int nk = blockIdx.x < nrec ? (nrec - 1 - (int)blockIdx.x) / G + 1 : 0;
+  if (w == NG * kGroup / 32) {
+    // ---- producer warp ----
+    const double* fac_end = fac + fac_len;
+    for (int k = 0; k < nk; ++k) {
+      const int s = k % nstages;
+      if (k >= nstages) mbar_wait(&empty[s], (unsigned)((k / nstages) + 1) & 1u);
+      double* st = sm + (size_t)s * sg.doubles;
+      int32_t* si = reinterpret_cast<int32_t*>(st + sg.offI);
+      const SolveRec rc = recs[blockIdx.x + (size_t)k * G];
+      const int nc = rc.nc, nq = rc.nq, np = nc * (nc + 1) / 2;
+      const double *aP, *aW;
+      unsigned bP, bW;
+      int pP, pW;
+      const bool okP = granules(fac + rc.C_off, np, fac, fac_end, aP, bP, pP);
+      const bool okW = granules(fac + rc.W_off, nc * nq, fac, fac_end, aW, bW, pW);
+      const unsigned rowb = (unsigned)R * 8u;
+      const unsigned tx = (okP ? bP : 0u) + (okW ? bW : 0u) + rowb * (unsigned)(nc + (kFwd ? 0 : nq));
+      if (lane == 0) mbar_expect_tx(&full[s], tx);
+      __syncwarp();
+      if (lane == 0) {
+        if (okP) bulk_g2s(st, aP, bP, &full[s]);
+        if (okW) bulk_g2s(st + sg.offW, aW, bW, &full[s]);
+      }
+      if (!okP) for (int e = lane; e < np; e += 32) st[e] = fac[rc.C_off + e];  // arena edge: plain copies
+      if (!okW) for (int e = lane; e < nc * nq; e += 32) st[sg.offW + e] = fac[rc.W_off + e];
+      const int32_t* cg = idx + rc.idx_off;
+      for (int i = lane; i < nc; i += 32) {
+        const int g = cg[i];
+        si[i] = g;
+        bulk_g2s(st + sg.offX + (size_t)i * ld, v + (size_t)g * R, rowb, &full[s]);
+      }
+      if (!kFwd)
+        for (int b = lane; b < nq; b += 32) {
+          const int g = cg[nc + b];
+          si[max_nc + b] = g;
+          bulk_g2s(st + sg.offQ + (size_t)b * ld, v + (size_t)g * R, rowb, &full[s]);
+        }
+      if (lane == 0) {
+        int32_t* meta = si + max_nc + max_nq;
+        meta[0] = nc;
+        meta[1] = nq;
+        meta[2] = okP ? pP : 0;
+        meta[3] = okW ? pW : 0;
+        meta[4] = (int32_t)(rc.contrib_off & 0xffffffff);
+        meta[5] = (int32_t)(rc.contrib_off >> 32);
+      }
+      __syncwarp();
+      mbar_arrive(&full[s]);
+    }
+    return;
+  }
+  // ---- consumer warps ----
+  // Every product keeps one RHS tile per warp (R = 8, 16, 32, 64: NW % ntr
+  // == 0), so a warp reads and writes only its RHS tile's 8-column slice of
+  // the staged rows.  At 64 RHS the slice is the warp's alone: results go in
+  // place after its k loops, with no barrier between the products; with
+  // fewer RHS the warps sharing a slice meet at a group barrier first.
+  constexpr int NW = kGroup / 32;
+  const int grp = w / NW;
+  const int lw = w - grp * NW;  // warp within the group
+  for (int k = grp; k < nk; k += NG) {
+    const int s = k % nstages;
+    mbar_wait(&full[s], (unsigned)(k / nstages) & 1u);
+    double* st = sm + (size_t)s * sg.doubles;
+    const int32_t* si = reinterpret_cast<const int32_t*>(st + sg.offI);
+    const int32_t* meta = si + max_nc + max_nq;
+    const int nc = meta[0], nq = meta[1];
+    const double* sP = st + meta[2];
+    const double* sW = st + sg.offW + meta[3];
+    double* sx = st + sg.offX;
+    const int32_t* c = si;
+    const bool own = (R >> 3) == NW;
+    auto gsync = [&]() {
+      if (!own) group_sync(grp);
+    };
+    if (kFwd) {
+      const int64_t coff = (int64_t)(uint32_t)meta[4] | ((int64_t)meta[5] << 32);
+      // s = P x_c -> v_c and in place
+      warp_mma_lean<0, true, kPipeMJ>(lw, nc, nc, sP, 0, sx, ld, R, [&](int row, int col, double a, double b) {
+        *reinterpret_cast<double2*>(sx + row * ld + col) = make_double2(a, b);
+        *reinterpret_cast<double2*>(v + (size_t)c[row] * R + col) = make_double2(a, b);
+      }, gsync);
+      __syncwarp();
+      gsync();
+      if (nq > 0) {  // g = W^T s -> contribution rows
+        double* g = contrib + (size_t)coff * R;
+        warp_mma_lean<3, false, kPipeMJ>(lw, nq, nc, sW, nq, sx, ld, R, [&](int row, int col, double a, double b) {
+          *reinterpret_cast<double2*>(g + (size_t)row * R + col) = make_double2(a, b);
+        });
+      }
+    } else {
+      double* sq = st + sg.offQ;
+      if (nq > 0) {  // t = x_c - W x_q, in place
+        warp_mma_lean<2, false, kPipeMJ>(lw, nc, nq, sW, nq, sq, ld, R, [&](int row, int col, double a, double b) {
+          double2* t = reinterpret_cast<double2*>(sx + row * ld + col);
+          const double2 o = *t;
+          *t = make_double2(o.x - a, o.y - b);
+        });
+        __syncwarp();
+        gsync();
+      }
+      // v_c = P^T t
+      warp_mma_lean<1, false, kPipeMJ>(lw, nc, nc, sP, 0, sx, ld, R, [&](int row, int col, double a, double b) {
+        *reinterpret_cast<double2*>(v + (size_t)c[row] * R + col) = make_double2(a, b);
+      });
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+}  // namespace pipe
 
 // skeleton record: sk[k] then rd[r]; T (k x r), P (r x r packed), W (r x k)
 __global__ void __launch_bounds__(NT, 3) solve_skel_mma_kernel(const SolveRec* __restrict__ recs,
@@ -1156,9 +1457,51 @@ size_t solve_small_smem(int max_nc, int max_nq, int nrhs) {
                            (size_t)max_nq * nrhs);
 }
 
-void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, double* v,
-                             int nrhs, double* contrib, size_t smem, int forward, cudaStream_t s) {
+// Shared memory of the pipelined kernel with `stages` stages (0: the level
+// does not fit two stages).
+static size_t pipe_smem(int max_nc, int max_nq, int nrhs, bool fwd, int& stages) {
+  const pipe::StageGeom sg(max_nc, max_nq, mma_ld(nrhs), !fwd);
+  const size_t per = sizeof(double) * (size_t)sg.doubles;
+  stages = (int)std::min<size_t>(pipe::kMaxStages, (kSmemCapBytes - 1024) / per);
+  return stages >= 2 ? per * stages : 0;
+}
+
+void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, int64_t fac_len,
+                             double* v, int nrhs, double* contrib, int max_nc, int max_nq, size_t smem, int forward,
+                             cudaStream_t s) {
   if (nrec <= 0) return;
+  static int nsm = [] {
+    int d = 0, n = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    return n > 0 ? n : 1;
+  }();
+  // many records of a small shape, an even RHS count (16-byte rows): the
+  // persistent pipelined kernels
+  // (HIFDE_NO_SOLVE_PIPE: the one-record kernels instead -- the tests' A/B of
+  // the two, which must agree bit for bit)
+  static const bool no_pipe = getenv("HIFDE_NO_SOLVE_PIPE") != nullptr;
+  if (!no_pipe && (nrhs == 8 || nrhs == 16 || nrhs == 32 || nrhs == 64) && max_nc <= 64 && nrec >= 4 * nsm) {
+    int stages = 0;
+    const size_t psm = pipe_smem(max_nc, max_nq, nrhs, forward != 0, stages);
+    if (psm) {
+      static bool once3 = (cudaFuncSetAttribute(pipe::solve_elim_pipe_kernel<true, 2>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes),
+                           cudaFuncSetAttribute(pipe::solve_elim_pipe_kernel<false, 2>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes),
+                           true);
+      (void)once3;
+      const int grid = std::min(nrec, nsm);
+      constexpr int nthr = 2 * pipe::kGroup + 32;
+      if (forward)
+        pipe::solve_elim_pipe_kernel<true, 2><<<grid, nthr, psm, s>>>(recs, nrec, idx, fac, fac_len, v, nrhs, contrib,
+                                                                      max_nc, max_nq, stages);
+      else
+        pipe::solve_elim_pipe_kernel<false, 2><<<grid, nthr, psm, s>>>(recs, nrec, idx, fac, fac_len, v, nrhs,
+                                                                       contrib, max_nc, max_nq, stages);
+      return;
+    }
+  }
   static bool once = (cudaFuncSetAttribute(solve_elim_fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)kSmemCapBytes),
                       cudaFuncSetAttribute(solve_elim_bwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -4002,8 +4002,8 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
       phases(L.fwd_ph);
     } else {
       if (nr && small_path(L)) {
-        launch_solve_elim_small(L.d_recs, nr, idx, fac, v, nrhs, contrib, solve_small_smem(L.max_nc, L.max_nq, nrhs),
-                                1, s);
+        launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, v, nrhs, contrib, L.max_nc, L.max_nq,
+                                solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
         ++g_launches;
       } else if (nr) {
         launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s);
@@ -4037,8 +4037,8 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
       }
     } else {
       if (nr && small_path(L)) {
-        launch_solve_elim_small(L.d_recs, nr, idx, fac, v, nrhs, nullptr, solve_small_smem(L.max_nc, L.max_nq, nrhs),
-                                0, s);
+        launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, v, nrhs, nullptr, L.max_nc, L.max_nq,
+                                solve_small_smem(L.max_nc, L.max_nq, nrhs), 0, s);
         ++g_launches;
       } else if (nr) {
         launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s);
