@@ -125,13 +125,17 @@ struct ElimSizes {
 __host__ __device__ inline ElimSizes elim_sizes(int nc, int nq, int maxnb, bool is_top) {
   const int nf = nc + nq;
   const size_t ib = hd_align16(sizeof(int32_t) * (size_t)(nf + maxnb));
+  // the path choices (one CTA or blocked, in-place or per-column inverse)
+  // keep the full-square rule they were tuned with; elim_small_kernel holds
+  // the front as a packed lower triangle
   const size_t need = ib + sizeof(double) * (size_t)nf * nf;
   const size_t need_inv = need + sizeof(double) * 8 * (size_t)nc;  // in-place inverse: one 8-row product block
+  const size_t packed = ib + sizeof(double) * ((size_t)nf * (nf + 1) / 2);
   ElimSizes z;
   if (need <= kSmemCapBytes && (is_top || (nc < kBigCellNc && nf < kBigCellNf))) {
     z.big = 0;
     z.scratch_off = need_inv <= kSmemCapBytes ? -2 : -1;
-    z.smem = z.scratch_off == -2 ? need_inv : need;
+    z.smem = z.scratch_off == -2 ? packed + sizeof(double) * 8 * (size_t)nc : packed;
   } else {
     z.big = 1;
     z.scratch_off = -1;

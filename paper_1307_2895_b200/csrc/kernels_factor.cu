@@ -170,14 +170,23 @@ __device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, in
 // Packed row-major lower inverse of the lower-triangular C (n x n, ld),
 // written to P[i(i+1)/2 + j]; one thread per column, no barriers (each
 // thread reads back only its own column).
+// Packed lower-triangular front storage (row i at i (i + 1) / 2): the
+// elimination kernels touch only the lower triangle of the symmetric front,
+// so a front takes half the shared memory (twice the cells per SM).
+struct PackedLower {
+  double* p;
+  __device__ __forceinline__ double* row(int i) const { return p + (size_t)i * (i + 1) / 2; }
+};
+
 template <int NT>
-__device__ void tri_inverse_packed(const double* C, int n, int ld, double* __restrict__ P) {
+__device__ void tri_inverse_packed(PackedLower C, int n, double* __restrict__ P) {
   for (int j = threadIdx.x; j < n; j += NT) {
-    P[(size_t)j * (j + 1) / 2 + j] = 1.0 / C[(size_t)j * ld + j];
+    P[(size_t)j * (j + 1) / 2 + j] = 1.0 / C.row(j)[j];
     for (int i = j + 1; i < n; ++i) {
       double s = 0.0;
-      for (int l = j; l < i; ++l) s += C[(size_t)i * ld + l] * P[(size_t)l * (l + 1) / 2 + j];
-      P[(size_t)i * (i + 1) / 2 + j] = -s / C[(size_t)i * ld + i];
+      const double* Ci = C.row(i);
+      for (int l = j; l < i; ++l) s += Ci[l] * P[(size_t)l * (l + 1) / 2 + j];
+      P[(size_t)i * (i + 1) / 2 + j] = -s / Ci[i];
     }
   }
 }
@@ -222,12 +231,12 @@ __device__ __forceinline__ void tri_tile(int tt, int& ti, int& tj) {
 // of chol_1sync instead, config 3's exact-tie rank decisions at levels
 // 4.5-6.5 drift by -2..-5%).  The factor goes to Lp[l*8 + j] and its inverse
 // diagonal to Lp[64 + l].
-__device__ __forceinline__ void diag_factor_warp(const double* F, int nf, int p0, int pw, double* Lp, int& bad,
-                                                 double& dmin) {
+__device__ __forceinline__ void diag_factor_warp(PackedLower F, int p0, int pw, double* Lp, int& bad, double& dmin) {
   const int l = threadIdx.x & 31;
   double r[8];
+  const double* Fl = F.row(p0 + (l < pw ? l : 0)) + p0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = (l < pw && j <= l) ? F[(size_t)(p0 + l) * nf + p0 + j] : 0.0;
+  for (int j = 0; j < 8; ++j) r[j] = (l < pw && j <= l) ? Fl[j] : 0.0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (k < pw) {  // warp-uniform
@@ -265,26 +274,26 @@ __device__ __forceinline__ void diag_factor_warp(const double* F, int nf, int p0
 // singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
 // Lw: 2 x 72 doubles (the factored diagonal block, double-buffered).
 template <int NT>
-__device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double* Lw) {
+__device__ int front_chol_blocked(PackedLower F, int nc, int nf, double* red, double* Lw) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __shared__ int s_bad;
   if (nc == 0) return 0;
   double sc = 0.0;
-  for (int i = threadIdx.x; i < nc; i += NT) sc = fmax(sc, fabs(F[(size_t)i * nf + i]));
+  for (int i = threadIdx.x; i < nc; i += NT) sc = fmax(sc, fabs(F.row(i)[i]));
   double scale = block_max<NT>(sc, red);
   if (scale == 0.0) {
     double s2 = 0.0;
     for (int e = threadIdx.x; e < nc * nc; e += NT) {
       const int i = e / nc, j = e - i * nc;
-      if (j <= i) s2 = fmax(s2, fabs(F[(size_t)i * nf + j]));
+      if (j <= i) s2 = fmax(s2, fabs(F.row(i)[j]));
     }
     scale = block_max<NT>(s2, red);
   }
   double dmin = DBL_MAX;  // warp 0's
   int bad = 0;
   if (wid == 0) {
-    diag_factor_warp(F, nf, 0, min(8, nc), Lw, bad, dmin);
+    diag_factor_warp(F, 0, min(8, nc), Lw, bad, dmin);
     if (lane == 0) s_bad = bad;
   }
   __syncthreads();
@@ -296,7 +305,7 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
     // panel below the diagonal block: row i <- row i C_pp^-T
     for (int i = p1 + threadIdx.x; i < nf; i += NT) {
       double x[8];
-      double* Fi = F + (size_t)i * nf + p0;
+      double* Fi = F.row(i) + p0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) x[k] = k < pw ? Fi[k] : 0.0;
 #pragma unroll
@@ -319,32 +328,37 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
       tri_tile(tt, ti, tj);
       const int rb = p1 + 8 * ti, cb = p1 + 8 * tj;
       double c0 = 0.0, c1 = 0.0;
+      const int ra = rb + (lane >> 2), rc = cb + (lane >> 2);
+      const double* Fa = F.row(ra < nf ? ra : p0) + p0;
+      const double* Fc = F.row(rc < nf ? rc : p0) + p0;
 #pragma unroll
       for (int ks = 0; ks < 8; ks += 4) {
         const int k = ks + (lane & 3);
-        const int ra = rb + (lane >> 2), rc = cb + (lane >> 2);
-        const double a = (k < pw && ra < nf) ? F[(size_t)ra * nf + p0 + k] : 0.0;
-        const double b = (k < pw && rc < nf) ? F[(size_t)rc * nf + p0 + k] : 0.0;
+        const double a = (k < pw && ra < nf) ? Fa[k] : 0.0;
+        const double b = (k < pw && rc < nf) ? Fc[k] : 0.0;
         dmma_8x8x4(c0, c1, a, b);
       }
       const int row = rb + (lane >> 2);
+      if (row < nf) {
+        double* Fr = F.row(row);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = cb + 2 * (lane & 3) + h;
-        if (row < nf && col <= row) F[(size_t)row * nf + col] -= h ? c1 : c0;
+        for (int h = 0; h < 2; ++h) {
+          const int col = cb + 2 * (lane & 3) + h;
+          if (col <= row) Fr[col] -= h ? c1 : c0;
+        }
       }
     };
     if (wid == 0) {
       if (lane < pw) {  // this panel's factored diagonal block into place
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (j <= lane) F[(size_t)(p0 + lane) * nf + p0 + j] = Lp[lane * 8 + j];
+          if (j <= lane) F.row(p0 + lane)[p0 + j] = Lp[lane * 8 + j];
       }
       if (ntt > 0) {
         tile(0);
         __syncwarp();
         if (p1 < nc) {
-          diag_factor_warp(F, nf, p1, min(8, nc - p1), Lw + 72 * (buf ^ 1), bad, dmin);
+          diag_factor_warp(F, p1, min(8, nc - p1), Lw + 72 * (buf ^ 1), bad, dmin);
           if (lane == 0) s_bad = bad;
         }
       }
@@ -368,7 +382,7 @@ __device__ int front_chol_blocked(double* F, int nc, int nf, double* red, double
 // Y, 8 x n), X_bb = C_bb^-1, by one thread per column.  The strictly upper
 // part is not touched.
 template <int NT>
-__device__ void tri_inverse_inplace(double* C, int n, int ld, double* Y, double* Lp) {
+__device__ void tri_inverse_inplace(PackedLower C, int n, double* Y, double* Lp) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int b0 = 0; b0 < n; b0 += 8) {
@@ -381,8 +395,8 @@ __device__ void tri_inverse_inplace(double* C, int n, int ld, double* Y, double*
       for (int k0 = j0 & ~3; k0 < b0; k0 += 4) {  // X[k][j] = 0 for k < j
         const int k = k0 + (lane & 3);
         const int ra = b0 + (lane >> 2), jb = j0 + (lane >> 2);
-        const double a = (ra < n && k < b0) ? C[(size_t)ra * ld + k] : 0.0;
-        const double b = (k < b0 && jb <= k) ? C[(size_t)k * ld + jb] : 0.0;  // X, lower part only
+        const double a = (ra < n && k < b0) ? C.row(ra)[k] : 0.0;
+        const double b = (k < b0 && jb <= k) ? C.row(k)[jb] : 0.0;  // X, lower part only
         dmma_8x8x4(c0, c1, a, b);
       }
       const int row = lane >> 2;
@@ -394,8 +408,8 @@ __device__ void tri_inverse_inplace(double* C, int n, int ld, double* Y, double*
     }
     if (threadIdx.x < 64) {  // the diagonal block and its inverse diagonal
       const int i = threadIdx.x >> 3, j = threadIdx.x & 7;
-      Lp[threadIdx.x] = (i < bw && j <= i) ? C[(size_t)(b0 + i) * ld + b0 + j] : 0.0;
-      if (j == 0) Lp[64 + i] = i < bw ? 1.0 / C[(size_t)(b0 + i) * ld + b0 + i] : 0.0;
+      Lp[threadIdx.x] = (i < bw && j <= i) ? C.row(b0 + i)[b0 + j] : 0.0;
+      if (j == 0) Lp[64 + i] = i < bw ? 1.0 / C.row(b0 + i)[b0 + i] : 0.0;
     }
     __syncthreads();
     for (int j = threadIdx.x; j < b0 + bw; j += NT) {  // columns of the block row
@@ -409,7 +423,7 @@ __device__ void tri_inverse_inplace(double* C, int n, int ld, double* Y, double*
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (i < bw && j <= b0 + i) C[(size_t)(b0 + i) * ld + j] = x[i];
+        if (i < bw && j <= b0 + i) C.row(b0 + i)[j] = x[i];
     }
   }
   __syncthreads();
@@ -431,14 +445,17 @@ __global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask
   int32_t* sdofs = reinterpret_cast<int32_t*>(smem);
   int32_t* smap = sdofs + nf;
   const size_t ibytes = align_up(sizeof(int32_t) * (size_t)(nf + t.maxnb), 16);
-  double* F = reinterpret_cast<double*>(smem + ibytes);
+  double* Fp = reinterpret_cast<double*>(smem + ibytes);  // packed lower front, nf (nf + 1) / 2
+  const PackedLower F{Fp};
+  const int nfp = nf * (nf + 1) / 2;
   const int32_t* gd = A.idx + t.dofs_off;
   for (int i = threadIdx.x; i < nf; i += NT) sdofs[i] = gd[i];
   for (int i = threadIdx.x; i < nc; i += NT) A.active[gd[i]] = 0;  // the cell retires
-  for (int e = threadIdx.x; e < nf * nf; e += NT) F[e] = 0.0;
+  for (int e = threadIdx.x; e < nfp; e += NT) Fp[e] = 0.0;
   __syncthreads();
   // A0 rows of c: eight entry slots per row, so the loads of a row's entries
-  // are in flight together (each front entry has one CSR entry: no races)
+  // are in flight together (each front entry has one CSR entry: no races);
+  // the lower triangle only: (p, pj) for pj <= p in c, (pj, p) for pj in q
   for (int e = threadIdx.x; e < 8 * nc; e += NT) {
     const int p = e >> 3, slot = e & 7;
     const int g = sdofs[p];
@@ -446,9 +463,10 @@ __global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask
     for (int64_t k = k0 + slot; k < k1; k += 8) {
       const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
       if (pj < 0) continue;
+      if (pj > p && pj < nc) continue;  // upper part of A_cc (its mirror is in row pj)
       const double v = A.a0[k];
-      F[p * nf + pj] += v;
-      if (pj >= nc) F[pj * nf + p] += v;
+      if (pj >= nc) F.row(pj)[p] += v;
+      else F.row(p)[pj] += v;
     }
   }
   __syncthreads();
@@ -472,7 +490,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask
         for (int u = 0; u < 4; ++u) {
           if (k0 + u >= nb) break;
           const int pk = smap[k0 + u];
-          if (pk >= 0) F[pk * nf + pl] += val[u];
+          if (pk >= pl) F.row(pk)[pl] += val[u];  // the lower triangle (the block is symmetric)
         }
       }
     }
@@ -490,29 +508,23 @@ __global__ void __launch_bounds__(NT, 768 / NT) elim_small_kernel(const ElimTask
     double* W = A.fac + t.W_off;
     for (int e = threadIdx.x; e < nc * nq; e += NT) {
       const int i = e / nq, j = e - i * nq;
-      W[e] = F[(size_t)(nc + j) * nf + i];
+      W[e] = F.row(nc + j)[i];
     }
     double* U = A.bvals + t.U_off;
     for (int e = threadIdx.x; e < nq * nq; e += NT) {
       const int a = e / nq, b = e - a * nq;
       const int hi = a > b ? a : b, lo = a > b ? b : a;
-      U[e] = F[(size_t)(nc + hi) * nf + nc + lo];
+      U[e] = F.row(nc + hi)[nc + lo];
     }
   }
   // packed C^-1 for the solve: inverted in place (Y: the 8 x nc block-row
-  // product, after the front)
+  // product, after the front); rows < nc of the packed front are then P
   if (t.scratch_off == -2) {
-    tri_inverse_inplace<NT>(F, nc, nf, F + (size_t)nf * nf, Lw);
+    tri_inverse_inplace<NT>(F, nc, Fp + nfp, Lw);
     double* P = A.fac + t.P_off;
-    for (int e = threadIdx.x; e < nc * (nc + 1) / 2; e += NT) {
-      const int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-      int ii = i;
-      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-      while (ii * (ii + 1) / 2 > e) --ii;
-      P[e] = F[(size_t)ii * nf + (e - ii * (ii + 1) / 2)];
-    }
+    for (int e = threadIdx.x; e < nc * (nc + 1) / 2; e += NT) P[e] = Fp[e];
   } else {
-    tri_inverse_packed<NT>(F, nc, nf, A.fac + t.P_off);
+    tri_inverse_packed<NT>(F, nc, A.fac + t.P_off);
   }
   if (threadIdx.x == 0) A.status[blockIdx.x] = 0;
 }
@@ -1540,17 +1552,19 @@ static void allow_smem(K kern) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCapBytes);
 }
 
+// Four warps per cell: with the packed front (level-0 cell of config 3:
+// 24 KB) six cells share an SM (register-bound); eight-warp CTAs were three
+// (config 3 level 0: 6.2 ms at 8 warps / full-square front, 5.1 ms here).
 void launch_elim_small(const ElimTask* d_tasks, int ntasks, const Arenas& A, size_t smem, int nt,
                        cudaStream_t s) {
   if (ntasks <= 0) return;
+  (void)nt;
   static bool once = false;
   if (!once) {
     allow_smem(elim_small_kernel<128>);
-    allow_smem(elim_small_kernel<256>);
     once = true;
   }
-  if (nt <= 128) elim_small_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A);
-  else elim_small_kernel<256><<<ntasks, 256, smem, s>>>(d_tasks, A);
+  elim_small_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A);
 }
 
 void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
