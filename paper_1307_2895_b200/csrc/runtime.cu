@@ -3327,6 +3327,7 @@ struct Factorizer {
       HCK(cudaMemcpyAsync(blk_val_off.data(), d_blk_val_off.p, sizeof(int64_t) * (size_t)nb, cudaMemcpyDeviceToHost, s));
       HCK(cudaMemcpyAsync(blk_alive.data(), sy_alive.p, (size_t)nb, cudaMemcpyDeviceToHost, s));
     }
+    active.resize((size_t)N);
     HCK(cudaMemcpyAsync(active.data(), d_active, (size_t)N, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     d_blk_dof_off.n = d_blk_n.n = d_blk_val_off.n = (size_t)nb;
@@ -3654,12 +3655,18 @@ struct Factorizer {
       meta.h.resize(0);
       borrowed = true;
     }
-    active.resize((size_t)N);
-    act.resize((size_t)N);
+    // the host's active mask, active list and block membership: filled here
+    // for the host analysis, or by dev_to_host when the device symbolic pass
+    // runs the first levels (config 3: 3.7 ms of O(N) host fills saved)
+    const bool dev_first = opt.symbolic == HIFDE_SYMBOLIC_AUTO && !sharded() && !opt.verify && N > 0;
+    if (!dev_first) {
+      active.resize((size_t)N);
+      act.resize((size_t)N);
 #pragma omp parallel for schedule(static) if (N > (1 << 16))
-    for (int64_t i = 0; i < N; ++i) {
-      active[(size_t)i] = 1;
-      act[(size_t)i] = (int32_t)i;
+      for (int64_t i = 0; i < N; ++i) {
+        active[(size_t)i] = 1;
+        act[(size_t)i] = (int32_t)i;
+      }
     }
     HCK(cudaMallocAsync((void**)&d_active, std::max<int64_t>(N, 1), s));
     HCK(cudaMemsetAsync(d_active, 1, (size_t)N, s));
@@ -3675,8 +3682,8 @@ struct Factorizer {
         hc.g = g;
         hc.valid = true;
         hc.variant = -1;  // arena hints belong to the previous grid
-      } else {
-        member.reset();
+      } else if (!dev_first) {
+        member.reset();  // (dev_to_host resets it before rebuilding)
       }
       if ((int)ctx.size() < nthreads) ctx.resize((size_t)nthreads);
       for (auto& x : ctx)
@@ -3739,7 +3746,7 @@ struct Factorizer {
     };
     // device symbolic mode from level 0 (not for the sharded sweep, whose
     // ranks keep the host analysis, nor for verify runs)
-    dev_mode = opt.symbolic == HIFDE_SYMBOLIC_AUTO && !sharded() && !opt.verify && N > 0;
+    dev_mode = dev_first;
     if (dev_mode) dev_init();
     // a device level that cannot run on the device hands over and is redone on the host
     auto dev_fallback = [&](LevelRec& L, double tag) {
