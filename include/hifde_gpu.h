@@ -86,6 +86,9 @@ typedef struct hifde_options {
   hifde_comm_t* comm;   /* NULL: one GPU; else shard over comm's ranks      */
   int kernel_log;       /* 1: time the main launches (hifde_kernel_stats)   */
   int symbolic;         /* HIFDE_SYMBOLIC_*: where the level analysis runs  */
+  int indptr_int32;     /* 1: indptr points to n + 1 int32 offsets (scipy's
+                           default index type), host arrays only; widened
+                           by the library instead of by the caller          */
 } hifde_options_t;
 
 typedef struct hifde_factor hifde_factor_t;

@@ -32,6 +32,7 @@ class Options(C.Structure):
         ("comm", C.c_void_p),
         ("kernel_log", C.c_int),
         ("symbolic", C.c_int),
+        ("indptr_int32", C.c_int),
     ]
 
 

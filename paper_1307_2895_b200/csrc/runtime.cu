@@ -558,7 +558,7 @@ struct HostCache {
       }
       return p;
     }
-  } pat_ip, pat_ix;
+  } pat_ip, pat_ix, wide_ip;  // wide_ip: int64 copy of an int32 indptr (options.indptr_int32)
   // host mirror of the index arena and the solve-metadata staging buffer,
   // lent to each factorization: their pages stay mapped (a fresh multi-100 MB
   // buffer per factorization costs its page faults on first touch)
@@ -4480,10 +4480,23 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
     fz.F_ = F.get();
     fz.s = F->stream;
     F->klog.on = opt->kernel_log != 0;
-    const int64_t nnz = opt->input_on_device ? 0 : indptr[n];
+    // int32 offsets from the caller: widened here on the host threads into
+    // a cached buffer (its pages stay mapped across factorizations)
+    const int64_t* ip64 = indptr;
+    if (opt->indptr_int32) {
+      if (opt->input_on_device) throw Fail{HIFDE_BADARG, "indptr_int32 needs host arrays"};
+      const int32_t* ip32 = reinterpret_cast<const int32_t*>(indptr);
+      int64_t* w = (int64_t*)host_cache().wide_ip.get((size_t)(n + 1) * sizeof(int64_t));
+      if (!w) throw Fail{HIFDE_CUDA, "page-locked host allocation failed"};
+      const int nth = n > (1 << 20) ? PinnedXfer::copy_threads() : 1;
+#pragma omp parallel for num_threads(nth) schedule(static)
+      for (int64_t i = 0; i <= n; ++i) w[i] = ip32[i];
+      ip64 = w;
+    }
+    const int64_t nnz = opt->input_on_device ? 0 : ip64[n];
     const char* sample = getenv("HIFDE_SAMPLE");  // host sampling profile (diagnostics)
     if (sample) host_sampler_start();
-    fz.run(indptr, indices, vals, nnz);
+    fz.run(ip64, indices, vals, nnz);
     if (sample) host_sampler_stop(sample);
   } catch (const Fail& f) {
     return fail_to_status(f);

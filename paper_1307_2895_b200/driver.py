@@ -226,7 +226,10 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     if not spd:
         raise NotImplementedError("indefinite (Bunch-Kaufman) mode is outside the GPU hot path")
     csr = _as_csr(a)
-    indptr = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+    # scipy's int32 offsets go to the library as they are (it widens them on
+    # its host threads); int64 ones as well
+    ip32 = csr.indptr.dtype == np.int32
+    indptr = np.ascontiguousarray(csr.indptr, dtype=np.int32 if ip32 else np.int64)
     indices = np.ascontiguousarray(csr.indices, dtype=np.int32)
     data = np.ascontiguousarray(csr.data, dtype=np.float64)
     opt = L.Options()
@@ -244,6 +247,7 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     opt.comm = comm.handle if comm is not None else None  # distributed.Comm: sharded sweep
     opt.kernel_log = int(bool(kernel_log))
     opt.symbolic = L.SYMBOLIC[symbolic]  # "host": the host level analysis throughout (A/B tests)
+    opt.indptr_int32 = int(ip32)
     h = C.c_void_p()
     code = lib.hifde_factor(indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, csr.shape[0],
                             int(grid.dim), int(grid.n), int(grid.m), int(grid.nlevels),
