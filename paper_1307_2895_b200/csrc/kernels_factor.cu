@@ -20,7 +20,9 @@
 //   elimination   src/factor_ops.py:138-159, src/dense.py:187-219
 //   skeletonize   src/factor_ops.py:162-214
 //   CPQR / ID     src/dense.py:239-264
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 #include <cooperative_groups.h>
 #include <cuda/atomic>
@@ -62,19 +64,39 @@ __device__ __forceinline__ double group_sum(double v, int G) {
   return v;
 }
 
-template <int NT>
-__device__ double block_max(double v, double* red) {
+// Thread teams of the one-group device code: a whole CTA (the one-CTA
+// kernels) or one warp of a multi-warp CTA that works on its own group
+// (skel_warp_kernel); `sync` is the team's barrier.
+template <int NT_>
+struct CtaTeam {
+  static constexpr int NT = NT_;
+  __device__ __forceinline__ static int tid() { return (int)threadIdx.x; }
+  __device__ __forceinline__ static void sync() { __syncthreads(); }
+};
+struct WarpTeam {
+  static constexpr int NT = 32;
+  __device__ __forceinline__ static int tid() { return (int)(threadIdx.x & 31); }
+  __device__ __forceinline__ static void sync() { __syncwarp(); }
+};
+
+template <class Tm>
+__device__ double block_max_t(double v, double* red) {
+  constexpr int NT = Tm::NT;
   constexpr int NW = NT / 32;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = Tm::tid() & 31, wid = Tm::tid() >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  __syncthreads();
+  Tm::sync();
   if (lane == 0) red[wid] = v;
-  __syncthreads();
+  Tm::sync();
   double s = red[0];
 #pragma unroll
   for (int w = 1; w < NW; ++w) s = fmax(s, red[w]);
   return s;
+}
+template <int NT>
+__device__ double block_max(double v, double* red) {
+  return block_max_t<CtaTeam<NT>>(v, red);
 }
 
 __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -83,36 +105,37 @@ __device__ __forceinline__ size_t align_up(size_t x, size_t a) { return (x + a -
 // Right-looking with the column scaling deferred by one step, so every step
 // needs a single barrier.  Status: 1 indefinite (pivot <= 0 or NaN, dpotrf
 // info > 0), 2 singular (min D <= 1e-14 max|diag A|, src/dense.py:102-113).
-template <int NT>
-__device__ int chol_1sync(double* A, int n, int ld, double* red) {
+template <class Tm>
+__device__ int chol_1sync_t(double* A, int n, int ld, double* red) {
+  constexpr int NT = Tm::NT;
   if (n == 0) return 0;
   double sc = 0.0;
-  for (int i = threadIdx.x; i < n; i += NT) sc = fmax(sc, fabs(A[(size_t)i * ld + i]));
-  double scale = block_max<NT>(sc, red);
+  for (int i = Tm::tid(); i < n; i += NT) sc = fmax(sc, fabs(A[(size_t)i * ld + i]));
+  double scale = block_max_t<Tm>(sc, red);
   if (scale == 0.0) {
     double s2 = 0.0;
-    for (int e = threadIdx.x; e < n * n; e += NT) {
+    for (int e = Tm::tid(); e < n * n; e += NT) {
       const int i = e / n, j = e - i * n;
       if (j <= i) s2 = fmax(s2, fabs(A[(size_t)i * ld + j]));
     }
-    scale = block_max<NT>(s2, red);
+    scale = block_max_t<Tm>(s2, red);
   }
   double dmin = DBL_MAX, prev_piv = 0.0, prev_inv = 0.0;
   for (int k = 0; k < n; ++k) {
-    __syncthreads();
+    Tm::sync();
     const double akk = A[(size_t)k * ld + k];
     if (!(akk > 0.0)) return 1;
     const double piv = sqrt(akk);
     const double rakk = 1.0 / akk;
     dmin = fmin(dmin, akk);
     if (k > 0) {  // finish column k-1 (no longer read by anyone)
-      for (int i = k + threadIdx.x; i < n; i += NT) A[(size_t)i * ld + k - 1] *= prev_inv;
-      if (threadIdx.x == 0) A[(size_t)(k - 1) * ld + k - 1] = prev_piv;
+      for (int i = k + Tm::tid(); i < n; i += NT) A[(size_t)i * ld + k - 1] *= prev_inv;
+      if (Tm::tid() == 0) A[(size_t)(k - 1) * ld + k - 1] = prev_piv;
     }
     // trailing update, lower triangle: warp per row, lanes over columns.
     // A lane's column factors A[j][k] / akk are formed once per step (same
     // rounding as forming them per row) and kept in registers.
-    const int lane = (int)(threadIdx.x & 31);
+    const int lane = (int)(Tm::tid() & 31);
     if (n - k - 1 <= 128) {
       double tj[4];
 #pragma unroll
@@ -120,7 +143,7 @@ __device__ int chol_1sync(double* A, int n, int ld, double* red) {
         const int j = k + 1 + lane + 32 * m;
         tj[m] = j < n ? A[(size_t)j * ld + k] * rakk : 0.0;
       }
-      for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
+      for (int i = k + 1 + (int)(Tm::tid() >> 5); i < n; i += NT / 32) {
         const double aik = A[(size_t)i * ld + k];
         double* Ai = A + (size_t)i * ld;
 #pragma unroll
@@ -130,7 +153,7 @@ __device__ int chol_1sync(double* A, int n, int ld, double* red) {
         }
       }
     } else {
-      for (int i = k + 1 + (int)(threadIdx.x >> 5); i < n; i += NT / 32) {
+      for (int i = k + 1 + (int)(Tm::tid() >> 5); i < n; i += NT / 32) {
         const double aik = A[(size_t)i * ld + k];
         for (int j = k + 1 + lane; j <= i; j += 32) A[(size_t)i * ld + j] -= aik * (A[(size_t)j * ld + k] * rakk);
       }
@@ -138,33 +161,42 @@ __device__ int chol_1sync(double* A, int n, int ld, double* red) {
     prev_piv = piv;
     prev_inv = 1.0 / piv;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) A[(size_t)(n - 1) * ld + n - 1] = prev_piv;
-  __syncthreads();
+  Tm::sync();
+  if (Tm::tid() == 0) A[(size_t)(n - 1) * ld + n - 1] = prev_piv;
+  Tm::sync();
   if (dmin <= kSingularRtol * fmax(scale, 1e-300)) return 2;
   return 0;
+}
+template <int NT>
+__device__ int chol_1sync(double* A, int n, int ld, double* red) {
+  return chol_1sync_t<CtaTeam<NT>>(A, n, ld, red);
 }
 
 // B (n x m, row-major, ldb) <- C^{-1} B, C lower (row-major, ldc); one barrier
 // per row (row scaling deferred by one step).
-template <int NT>
-__device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, int ldb) {
+template <class Tm>
+__device__ void trsm_1sync_t(const double* C, int n, int ldc, double* B, int m, int ldb) {
+  constexpr int NT = Tm::NT;
   double prev = 0.0;
   for (int i = 0; i < n; ++i) {
-    __syncthreads();
+    Tm::sync();
     const double cinv = 1.0 / C[(size_t)i * ldc + i];
     if (i > 0)
-      for (int j = threadIdx.x; j < m; j += NT) B[(size_t)(i - 1) * ldb + j] *= prev;
-    for (int l = i + 1 + (int)(threadIdx.x >> 5); l < n; l += NT / 32) {  // warp per row
+      for (int j = Tm::tid(); j < m; j += NT) B[(size_t)(i - 1) * ldb + j] *= prev;
+    for (int l = i + 1 + (int)(Tm::tid() >> 5); l < n; l += NT / 32) {  // warp per row
       const double c = C[(size_t)l * ldc + i];
-      for (int j = (int)(threadIdx.x & 31); j < m; j += 32) B[(size_t)l * ldb + j] -= c * (B[(size_t)i * ldb + j] * cinv);
+      for (int j = (int)(Tm::tid() & 31); j < m; j += 32) B[(size_t)l * ldb + j] -= c * (B[(size_t)i * ldb + j] * cinv);
     }
     prev = cinv;
   }
-  __syncthreads();
+  Tm::sync();
   if (n > 0)
-    for (int j = threadIdx.x; j < m; j += NT) B[(size_t)(n - 1) * ldb + j] *= prev;
-  __syncthreads();
+    for (int j = Tm::tid(); j < m; j += NT) B[(size_t)(n - 1) * ldb + j] *= prev;
+  Tm::sync();
+}
+template <int NT>
+__device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, int ldb) {
+  trsm_1sync_t<CtaTeam<NT>>(C, n, ldc, B, m, ldb);
 }
 
 // Packed row-major lower inverse of the lower-triangular C (n x n, ld),
@@ -196,18 +228,23 @@ __device__ void trsm_1sync(const double* C, int n, int ldc, double* B, int m, in
 
 // Packed lower inverse via B = C^-1 I in the workspace X (n x n), then a
 // coalesced packed store.  All threads busy, one barrier per row.
-template <int NT>
-__device__ void tri_inverse_packed_ws(const double* C, int n, int ld, double* X, double* __restrict__ P) {
-  __syncthreads();
-  for (int e = threadIdx.x; e < n * n; e += NT) {
+template <class Tm>
+__device__ void tri_inverse_packed_ws_t(const double* C, int n, int ld, double* X, double* __restrict__ P) {
+  constexpr int NT = Tm::NT;
+  Tm::sync();
+  for (int e = Tm::tid(); e < n * n; e += NT) {
     const int i = e / n, j = e - i * n;
     X[e] = (i == j) ? 1.0 : 0.0;
   }
-  trsm_1sync<NT>(C, n, ld, X, n, n);
-  for (int e = threadIdx.x; e < n * n; e += NT) {
+  trsm_1sync_t<Tm>(C, n, ld, X, n, n);
+  for (int e = Tm::tid(); e < n * n; e += NT) {
     const int i = e / n, j = e - i * n;
     if (j <= i) P[(size_t)i * (i + 1) / 2 + j] = X[e];
   }
+}
+template <int NT>
+__device__ void tri_inverse_packed_ws(const double* C, int n, int ld, double* X, double* __restrict__ P) {
+  tri_inverse_packed_ws_t<CtaTeam<NT>>(C, n, ld, X, P);
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -628,10 +665,11 @@ struct NoPublish {
 // congruence B_sr / B_rr from A_cc, the inner Cholesky, W, the delta block
 // and the record (T | packed C^-1 | W).  Z is the post-CPQR workspace
 // (3 q4 + 2 nc^2 doubles); red holds NT/32 partials.
-template <int NT>
-__device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, double* Mq, int ldm,
+template <class Tm>
+__device__ void skel_tail_t(const SkelTask& t, const Arenas& A, int nc, int k, double* Mq, int ldm,
                           const int32_t* perm, int32_t* skl, int32_t* rdl, int32_t* sko, int32_t* rdo,
                           const int32_t* sdofs, const double* Acc, double* Z, double* red) {
+  constexpr int NT = Tm::NT;
   const int r = nc - k;
   const size_t q4 = (size_t)nc * nc / 4 + nc;
   double* Ts = Z;                                      // k x r
@@ -639,7 +677,7 @@ __device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, dou
   double* Wm = Bsr + q4;                               // r x k
   double* Brr = Wm + q4;                               // r x r
   // T = R11^-1 R12 (back substitution, one thread per column of R12)
-  for (int j = threadIdx.x; j < r; j += NT) {
+  for (int j = Tm::tid(); j < r; j += NT) {
     double* col = Mq + (size_t)perm[k + j] * ldm;
     for (int i = k - 1; i >= 0; --i) {
       double s = col[i];
@@ -648,7 +686,7 @@ __device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, dou
     }
   }
   // ascending sk / rd with their pivot positions
-  for (int a = threadIdx.x; a < nc; a += NT) {
+  for (int a = Tm::tid(); a < nc; a += NT) {
     const int pv = perm[a];
     int rank = 0;
     if (a < k) {
@@ -661,39 +699,39 @@ __device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, dou
       rdo[rank] = a - k;
     }
   }
-  __syncthreads();
+  Tm::sync();
   int32_t* out = A.idx + t.out_off;
-  for (int a = threadIdx.x; a < k; a += NT) out[a] = sdofs[skl[a]];
-  for (int a = threadIdx.x; a < r; a += NT) out[k + a] = sdofs[rdl[a]];
-  if (threadIdx.x == 0) A.kout[t.group] = k;
+  for (int a = Tm::tid(); a < k; a += NT) out[a] = sdofs[skl[a]];
+  for (int a = Tm::tid(); a < r; a += NT) out[k + a] = sdofs[rdl[a]];
+  if (Tm::tid() == 0) A.kout[t.group] = k;
   if (r == 0) {
-    if (threadIdx.x == 0) A.status[t.group] = 0;
+    if (Tm::tid() == 0) A.status[t.group] = 0;
     return;
   }
-  for (int e = threadIdx.x; e < k * r; e += NT) {
+  for (int e = Tm::tid(); e < k * r; e += NT) {
     const int a = e / r, b = e - a * r;
     Ts[e] = Mq[sko[a] + (size_t)perm[k + rdo[b]] * ldm];
   }
-  __syncthreads();
+  Tm::sync();
   // B_sr = A_sr - A_ss T
-  for (int e = threadIdx.x; e < k * r; e += NT) {
+  for (int e = Tm::tid(); e < k * r; e += NT) {
     const int a = e / r, b = e - a * r;
     const double* arow = Acc + skl[a] * nc;
     double s = arow[rdl[b]];
     for (int l = 0; l < k; ++l) s -= arow[skl[l]] * Ts[l * r + b];
     Bsr[e] = s;
   }
-  __syncthreads();
+  Tm::sync();
   // B_rr = A_rr - A_sr^T T - T^T B_sr  (then symmetrized)
-  for (int e = threadIdx.x; e < r * r; e += NT) {
+  for (int e = Tm::tid(); e < r * r; e += NT) {
     const int a = e / r, b = e - a * r;
     double s = Acc[rdl[a] * nc + rdl[b]];
     for (int l = 0; l < k; ++l)
       s -= Acc[skl[l] * nc + rdl[a]] * Ts[l * r + b] + Ts[l * r + a] * Bsr[l * r + b];
     Brr[e] = s;
   }
-  __syncthreads();
-  for (int e = threadIdx.x; e < r * r; e += NT) {
+  Tm::sync();
+  for (int e = Tm::tid(); e < r * r; e += NT) {
     const int a = e / r, b = e - a * r;
     if (a < b) {
       const double m = 0.5 * (Brr[e] + Brr[b * r + a]);
@@ -701,49 +739,57 @@ __device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, dou
       Brr[b * r + a] = m;
     }
   }
-  __syncthreads();
-  const int st = chol_1sync<NT>(Brr, r, r, red);
+  Tm::sync();
+  const int st = chol_1sync_t<Tm>(Brr, r, r, red);
   if (st != 0) {
-    if (threadIdx.x == 0) A.status[t.group] = st;
+    if (Tm::tid() == 0) A.status[t.group] = st;
     return;
   }
-  for (int e = threadIdx.x; e < r * k; e += NT) {
+  for (int e = Tm::tid(); e < r * k; e += NT) {
     const int a = e / k, b = e - a * k;
     Wm[e] = Bsr[b * r + a];
   }
-  if (k > 0) trsm_1sync<NT>(Brr, r, r, Wm, k, k);
-  __syncthreads();
+  if (k > 0) trsm_1sync_t<Tm>(Brr, r, r, Wm, k, k);
+  Tm::sync();
   double* dl = A.bvals + t.delta_off;
-  for (int e = threadIdx.x; e < k * k; e += NT) {
+  for (int e = Tm::tid(); e < k * k; e += NT) {
     const int a = e / k, b = e - a * k;
     double s = 0.0;
     for (int l = 0; l < r; ++l) s -= Wm[l * k + a] * Wm[l * k + b];
     dl[e] = s;
   }
   double* rec = A.fac + t.rec_off;
-  for (int e = threadIdx.x; e < k * r; e += NT) rec[e] = Ts[e];
+  for (int e = Tm::tid(); e < k * r; e += NT) rec[e] = Ts[e];
   double* C = rec + (size_t)k * r;
-  tri_inverse_packed_ws<NT>(Brr, r, r, Brr + (size_t)nc * nc, C);  // packed C^-1 for the solve
+  tri_inverse_packed_ws_t<Tm>(Brr, r, r, Brr + (size_t)nc * nc, C);  // packed C^-1 for the solve
   double* Wo = C + (size_t)r * r;
-  for (int e = threadIdx.x; e < r * k; e += NT) Wo[e] = Wm[e];
-  if (threadIdx.x == 0) A.status[t.group] = 0;
+  for (int e = Tm::tid(); e < r * k; e += NT) Wo[e] = Wm[e];
+  if (Tm::tid() == 0) A.status[t.group] = 0;
+}
+template <int NT>
+__device__ void skel_tail(const SkelTask& t, const Arenas& A, int nc, int k, double* Mq, int ldm,
+                          const int32_t* perm, int32_t* skl, int32_t* rdl, int32_t* sko, int32_t* rdo,
+                          const int32_t* sdofs, const double* Acc, double* Z, double* red) {
+  skel_tail_t<CtaTeam<NT>>(t, A, nc, k, Mq, ldm, perm, skl, rdl, sko, rdo, sdofs, Acc, Z, red);
 }
 
 // One skeletonization group.  The front is assembled assuming every neighbour
 // row is alive, then `wait()` runs (exact order: until the earlier
 // neighbouring groups are done), then rows of DOFs retired meanwhile are
 // zeroed -- so the assembly is off the dependency chain's critical path.
-template <int NT, class Wait, class Publish = NoPublish>
-__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem, const Wait& wait,
-                           const Publish& publish = Publish{}) {
+// red: NT / 32 doubles, shk: one int -- the team's shared scalars.
+// GNT: the CTA size whose lane split (lanes per column) the CPQR uses, so a
+// warp team reproduces the GNT-thread CTA's sums exactly.
+template <class Tm, int GNT, class Wait, class Publish = NoPublish>
+__device__ void skel_group_t(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem, const Wait& wait,
+                             const Publish& publish, double* red, int* shk) {
+  constexpr int NT = Tm::NT;
   constexpr int NW = NT / 32;
-  __shared__ double red[NW];
-  __shared__ double sh_beta, sh_tau, sh_scal;
-  __shared__ int sh_k;
+  int& sh_k = *shk;
   const int nc = t.nc, nq = t.nq, nf = nc + nq;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = Tm::tid() & 31, wid = Tm::tid() >> 5;
   auto mark = [&](int which) {  // debug timestamps (HIFDE_SKEL_TLOG)
-    if (A.tlog && threadIdx.x == 0) {
+    if (A.tlog && Tm::tid() == 0) {
       unsigned long long g;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
       A.tlog[(size_t)t.group * 16 + which] = g;
@@ -792,16 +838,16 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   }
 
   const int32_t* gd = A.idx + t.dofs_off;
-  for (int i = threadIdx.x; i < nf; i += NT) {
+  for (int i = Tm::tid(); i < nf; i += NT) {
     const int g = gd[i];
     sdofs[i] = g;
     salive[i] = 1;
   }
-  for (int i = threadIdx.x; i < nc; i += NT) perm[i] = i;
-  for (int e = threadIdx.x; e < nc * nc; e += NT) Acc[e] = 0.0;
-  for (size_t e = threadIdx.x; e < (size_t)ldq * nc; e += NT) Mq[e] = 0.0;
-  __syncthreads();
-  for (int p = threadIdx.x; p < nc; p += NT) {
+  for (int i = Tm::tid(); i < nc; i += NT) perm[i] = i;
+  for (int e = Tm::tid(); e < nc * nc; e += NT) Acc[e] = 0.0;
+  for (size_t e = Tm::tid(); e < (size_t)ldq * nc; e += NT) Mq[e] = 0.0;
+  Tm::sync();
+  for (int p = Tm::tid(); p < nc; p += NT) {
     const int g = sdofs[p];
     for (int64_t k = A.indptr[g]; k < A.indptr[g + 1]; ++k) {
       const int pj = front_pos(sdofs, nc, nq, A.indices[k]);
@@ -811,27 +857,27 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       else Mq[(pj - nc) + (size_t)p * ldq] += v;
     }
   }
-  __syncthreads();
+  Tm::sync();
   const int32_t* bl = A.lists + t.blk_off;
   for (int b = 0; b < t.nblk; ++b) {
     const int bid = bl[b];
     const int nb = A.blk_n[bid];
     const int32_t* bd = A.idx + A.blk_dof_off[bid];
     const double* bv = A.bvals + A.blk_val_off[bid];
-    if (threadIdx.x == 0) sh_k = 0;
-    __syncthreads();
-    for (int k = threadIdx.x; k < nb; k += NT) {
+    if (Tm::tid() == 0) sh_k = 0;
+    Tm::sync();
+    for (int k = Tm::tid(); k < nb; k += NT) {
       const int p = front_pos(sdofs, nc, nq, bd[k]);
       smap[k] = (p >= 0 && salive[p]) ? p : -1;
       if (p >= 0 && p < nc && salive[p]) skl[atomicAdd(&sh_k, 1)] = k;  // block columns landing in c
     }
-    __syncthreads();
+    Tm::sync();
     // only the columns of c are assembled (A_cc and Mq = A_qc): warp per
     // block row over the compact column list, four rows' loads in flight per
     // lane (each front entry still takes one add per block)
     const int ncc = sh_k;
-    for (int k0 = (int)(threadIdx.x >> 5) * 4; k0 < nb; k0 += NT / 8) {
-      for (int j = (int)(threadIdx.x & 31); j < ncc; j += 32) {
+    for (int k0 = (int)(Tm::tid() >> 5) * 4; k0 < nb; k0 += NT / 8) {
+      for (int j = (int)(Tm::tid() & 31); j < ncc; j += 32) {
         const int l = skl[j], pl = smap[l];
         double val[4];
 #pragma unroll
@@ -846,19 +892,19 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         }
       }
     }
-    __syncthreads();
+    Tm::sync();
   }
 
   wait();
-  __syncthreads();
+  Tm::sync();
   // rows of DOFs retired by earlier groups (written by other CTAs)
-  for (int i = nc + threadIdx.x; i < nf; i += NT) {
+  for (int i = nc + Tm::tid(); i < nf; i += NT) {
     if (!__ldcg(A.active + sdofs[i])) {
       salive[i] = 0;
       for (int j = 0; j < nc; ++j) Mq[(size_t)(i - nc) + (size_t)j * ldq] = 0.0;
     }
   }
-  __syncthreads();
+  Tm::sync();
   mark(4);
 
   // ---- mode 3: R factor of Mq by chunked Householder QR in shared memory --
@@ -872,17 +918,17 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     double* S = wsh;
     double* cn2 = cq;  // chunk-part squared norms (the CPQR vectors are not live yet)
     int Gq = 32;
-    while (Gq > 8 && NT / Gq < nc) Gq >>= 1;
+    while (Gq > 8 && GNT / Gq < nc) Gq >>= 1;  // the lane split of a GNT-thread CTA (same sums)
     const int nsq = NT / Gq, slq = lane & (Gq - 1), slotq = wid * (32 / Gq) + lane / Gq;
-    for (int e = threadIdx.x; e < lds * nc; e += NT) S[e] = 0.0;
+    for (int e = Tm::tid(); e < lds * nc; e += NT) S[e] = 0.0;
     for (int r0 = 0; r0 < nq; r0 += h) {
       const int hh = min(h, nq - r0);
-      __syncthreads();
-      for (int e = threadIdx.x; e < h * nc; e += NT) {
+      Tm::sync();
+      for (int e = Tm::tid(); e < h * nc; e += NT) {
         const int j = e / h, rr = e - j * h;
         S[nc + rr + (size_t)j * lds] = rr < hh ? Mq[(size_t)(r0 + rr) + (size_t)j * ldq] : 0.0;
       }
-      __syncthreads();
+      Tm::sync();
       for (int base = 0; base < nc; base += nsq) {
         const int j = base + slotq;
         const double* col = S + (size_t)min(j, nc - 1) * lds;
@@ -891,7 +937,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         a = group_sum(a, Gq);
         if (j < nc && slq == 0) cn2[j] = a;
       }
-      __syncthreads();
+      Tm::sync();
       for (int i = 0; i < nc; ++i) {
         // x = [S_ii ; chunk rows of column i]; the R rows below i are zero
         const double* v = S + (size_t)i * lds;
@@ -946,11 +992,11 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
             }
           }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) S[i + (size_t)i * lds] = beta;
+        Tm::sync();
+        if (Tm::tid() == 0) S[i + (size_t)i * lds] = beta;
       }
     }
-    __syncthreads();
+    Tm::sync();
     Mq = S;      // the CPQR runs on R (nc x nc, column-major, ld lds)
     nqm = nc;
     ldm = lds;
@@ -965,7 +1011,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
   double* Mc = t.mode == 0 ? wsh + (size_t)nc * nc : wsh;
   if (t.mode != 3) { nqm = nq; ldm = ldq; }
   int nq_alive = 0;
-  if (threadIdx.x == 0) {
+  if (Tm::tid() == 0) {
     for (int i = nc; i < nf; ++i) nq_alive += salive[i];
     sh_k = nq_alive;
   }
@@ -984,13 +1030,13 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
       cpos[j] = j;
     }
   }
-  __syncthreads();
+  Tm::sync();
   mark(5);
   nq_alive = sh_k;
   const int kmax = nqm < nc ? nqm : nc;
   const double tol3z = sqrt(DBL_EPSILON * 0.5);  // sqrt(dlamch('E'))
   int G = 32;  // lanes per trailing column
-  while (G > 8 && NT / G < nc) G >>= 1;
+  while (G > 8 && GNT / G < nc) G >>= 1;  // the lane split of a GNT-thread CTA (same sums)
   const int nslots = NT / G, sl = lane & (G - 1), slot = wid * (32 / G) + lane / G;
   double thr = 0.0;
   int k = kmax;
@@ -1036,7 +1082,7 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
     const double rii = fabs(beta);
     if (i == 0) thr = eps > 0.0 ? eps * rii : (double)(nq_alive > nc ? nq_alive : nc) * DBL_EPSILON * rii;
     if (rii <= thr) { k = i; break; }
-    if (threadIdx.x == 0) { rdiag[i] = beta; dcol[p] = 1; }
+    if (Tm::tid() == 0) { rdiag[i] = beta; dcol[p] = 1; }
     // trailing columns: G lanes per column, NT / G columns at once (the
     // step's latency is one column's dependency chain, not NW of them)
     for (int base = 0; base < nc; base += nslots) {
@@ -1118,23 +1164,30 @@ __device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsig
         if (sl == 0) { vn1o[j] = nv; xno[j] = sqrt(acc); }
       }
     }
-    __syncthreads();
+    Tm::sync();
   }
   mark(6);
   // LAPACK order of the columns (the redundant ones as of step k), R_ii into place
   {
     const int32_t* cat = cpos + (k & 1) * nc;
-    for (int pos = threadIdx.x; pos < nc; pos += NT) perm[pos] = cat[pos];
+    for (int pos = Tm::tid(); pos < nc; pos += NT) perm[pos] = cat[pos];
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < k; i += NT) Mc[i + (size_t)perm[i] * ldm] = rdiag[i];
+  Tm::sync();
+  for (int i = Tm::tid(); i < k; i += NT) Mc[i + (size_t)perm[i] * ldm] = rdiag[i];
   Mq = Mc;
-  __syncthreads();
+  Tm::sync();
   // the redundant set is known: later groups may start (exact order) while
   // this one finishes its interpolation and elimination off the chain
   publish(k, perm, sdofs, nc);
 
-  skel_tail<NT>(t, A, nc, k, Mq, ldm, perm, skl, rdl, sko, rdo, sdofs, Acc, Z, red);
+  skel_tail_t<Tm>(t, A, nc, k, Mq, ldm, perm, skl, rdl, sko, rdo, sdofs, Acc, Z, red);
+}
+template <int NT, class Wait, class Publish = NoPublish>
+__device__ void skel_group(const SkelTask& t, const Arenas& A, double eps, unsigned char* smem, const Wait& wait,
+                           const Publish& publish = Publish{}) {
+  __shared__ double red[NT / 32];
+  __shared__ int sh_k;
+  skel_group_t<CtaTeam<NT>, NT>(t, A, eps, smem, wait, publish, red, &sh_k);
 }
 
 template <int NT>
@@ -1142,6 +1195,25 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   extern __shared__ __align__(16) unsigned char smem[];
   const SkelTask t = tasks[blockIdx.x];
   skel_group<NT>(t, A, eps, smem, NoWait{});
+}
+
+// Snapshot levels of many small groups (those the 128-thread skel_kernel
+// takes): one warp per group, W groups per CTA, each warp with its own slice
+// of the dynamic shared memory and only warp barriers.  The CPQR keeps the
+// 128-thread CTA's lane split (GNT = 128), so every sum -- and every rank
+// decision -- is the one-CTA kernel's; the pivot search, reflector scalars
+// and bookkeeping a 4-warp CTA ran four times over run once.
+template <int W>
+__global__ void __launch_bounds__(32 * W) skel_warp_kernel(const SkelTask* __restrict__ tasks, int ntasks, Arenas A,
+                                                           double eps, int per_group) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[W];
+  __shared__ int shk[W];
+  const int w = (int)(threadIdx.x >> 5);
+  const int g = (int)blockIdx.x * W + w;
+  if (g >= ntasks) return;  // warp-uniform: no CTA-wide barrier follows
+  const SkelTask t = tasks[g];
+  skel_group_t<WarpTeam, 128>(t, A, eps, smem + (size_t)w * per_group, NoWait{}, NoPublish{}, red + w, shk + w);
 }
 
 // Exact (reference) order in one launch: co-resident CTAs walk the groups in
@@ -1573,7 +1645,7 @@ void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles
   schur_tile_kernel<<<ntiles, 128, 0, s>>>(d_tasks, d_tiles, A);
 }
 
-void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt,
+void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt, int max_nc,
                  cudaStream_t s) {
   if (ntasks <= 0) return;
   static bool once = false;
@@ -1581,6 +1653,22 @@ void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double ep
     allow_smem(skel_kernel<128>);
     allow_smem(skel_kernel<512>);
     once = true;
+  }
+  // (HIFDE_NO_SKEL_WARP: the one-CTA kernel instead -- the tests' A/B, which
+  // must agree bit for bit)
+  static const bool no_warp = getenv("HIFDE_NO_SKEL_WARP") != nullptr;
+  // many tiny groups (config 3 level 0.5: 7 x 44, 4.4 -> 2.6 ms; config 5
+  // level 1/3: 9 x 92, 5.7 -> 4.1 ms; the 15-column groups of config 3 level
+  // 1.5 are slower by warp, 2.7 -> 3.9 ms): a warp each (bit-identical)
+  if (!no_warp && nt <= 128 && max_nc <= 12 && ntasks >= 4096) {
+    static bool once_w = (allow_smem(skel_warp_kernel<8>), true);
+    (void)once_w;
+    const size_t per = (smem + 15) / 16 * 16;
+    const int W = (int)std::min<size_t>(8, std::max<size_t>(1, (kSmemCapBytes - 2048) / std::max<size_t>(per, 16)));
+    if (W == 8) {
+      skel_warp_kernel<8><<<(ntasks + 7) / 8, 256, per * 8, s>>>(d_tasks, ntasks, A, eps, (int)per);
+      return;
+    }
   }
   if (nt <= 128) skel_kernel<128><<<ntasks, 128, smem, s>>>(d_tasks, A, eps);
   else skel_kernel<512><<<ntasks, 512, smem, s>>>(d_tasks, A, eps);

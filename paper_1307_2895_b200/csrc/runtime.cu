@@ -2280,7 +2280,7 @@ struct Factorizer {
         if (hi > lo) {
           const int kl = F->klog.begin("skel_kernel", tag, 0, 0, 0, s);
           launch_skel(dt.p + lo, (int)(hi - lo), arenas_r(r, false), opt.eps, smem,
-                      (max_nc > 32 || max_nq > 128) ? 512 : 128, s);
+                      (max_nc > 32 || max_nq > 128) ? 512 : 128, (int)max_nc, s);
           F->klog.end(kl, s);
           ++g_launches;
         }
@@ -3271,7 +3271,7 @@ struct Factorizer {
       ++g_launches;
     } else {
       const int kl = F->klog.begin("skel_kernel", tag, 0, 0, 0, s);
-      launch_skel(sy_tasks.p, (int)ng, Ar, opt.eps, (size_t)T.smem, nthr, s);
+      launch_skel(sy_tasks.p, (int)ng, Ar, opt.eps, (size_t)T.smem, nthr, (int)T.max_nc, s);
       F->klog.end(kl, s);
       launch_apply_rd(sy_tasks.p, (int)ng, Ar, s);
       g_launches += 2;

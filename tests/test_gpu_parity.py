@@ -438,6 +438,46 @@ def test_pipelined_record_kernels_bit_identical(tmp_path):
         assert np.array_equal(files[0][k], files[1][k]), k
 
 
+_FACTOR_DUMP = r'''
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+import paper_1307_2895_b200 as H
+out = {}
+for dim, n, m, eps, var, seed in [(2, 512, 8, 1e-9, "hifde", 5), (2, 1024, 8, 1e-6, "hifde", 0),
+                                  (3, 64, 4, 1e-3, "hifde3x", 2)]:
+    g = H.build_grid(dim, n, m)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=seed))
+    f = (H.factor_hifde if var == "hifde" else H.factor_hifde3x)(a, g, eps)
+    b = np.random.default_rng(7).standard_normal((g.ndof, 3))
+    out[f"{dim}_{n}_x"] = f.apply_inverse(b)
+    out[f"{dim}_{n}_k"] = np.array([c for _, c in f.metrics["skeleton_counts"]])
+np.savez(sys.argv[1], **out)
+'''
+
+
+def test_warp_skeleton_kernel_bit_identical(tmp_path):
+    """Snapshot levels of 4096+ small groups run one warp per group
+    (skel_warp_kernel) with the 128-thread CTA's lane split: ranks and
+    solutions identical bit for bit to the one-CTA kernel's
+    (HIFDE_NO_SKEL_WARP), on random-coefficient problems whose fine levels
+    drop DOFs (2D eps 1e-9 / 1e-6, 3D eps 1e-3)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    files = []
+    for i, env in enumerate(({}, {"HIFDE_NO_SKEL_WARP": "1"})):
+        fn = str(tmp_path / f"w{i}.npz")
+        r = subprocess.run([sys.executable, "-c", _FACTOR_DUMP, fn], capture_output=True, text=True, cwd=root,
+                           env=dict(os.environ, **env), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        files.append(np.load(fn))
+    for k in files[0].files:
+        assert np.array_equal(files[0][k], files[1][k]), k
+
+
 def test_pipelined_host_solve_matches_one_block_solve():
     """Page-locked host right-hand sides take the pipelined solve (column
     chunks: strided H2D DMA, sweep, D2H pieces scattered into the caller's
