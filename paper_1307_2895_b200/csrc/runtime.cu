@@ -102,11 +102,12 @@ struct PinnedStage {
   void begin(cudaStream_t st) {
     s = st;
     n = 0;
-    // grow (geometrically, to the cap) only when the last factorization
-    // needed more; a pinned allocation is tens of ms at these sizes, so a
-    // failed size is never retried
+    // grow only when the last factorization needed more, and then in one
+    // step (a pinned allocation runs at ~2.3 GB/s on this host: 256 MB is
+    // ~110 ms, so a geometric series of growths costs the repeated calls of
+    // a fixed problem twice); a failed size is never retried
     if (peak > cap && cap < kMaxCap) {
-      const size_t want = std::min(std::max(4 * peak, 2 * cap), kMaxCap);
+      const size_t want = peak > ((size_t)16 << 20) ? kMaxCap : std::min(std::max(4 * peak, 2 * cap), kMaxCap);
       if (want < failed) {
         char* q = nullptr;
         if (cudaHostAlloc((void**)&q, want, cudaHostAllocDefault) == cudaSuccess) {

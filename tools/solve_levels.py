@@ -12,6 +12,7 @@ phase = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 g, a, eps, variant, nrhs = H.baseline_problem(cfg)
 nrhs = nrhs_over or nrhs
 fac = H.factor_hifde if variant == "hifde" else H.factor_hifde3x
+fac(a, g, eps, kernel_log=True).close()  # warm-up (first-call allocations, page faults)
 f = fac(a, g, eps, kernel_log=True)
 b = torch.from_numpy(np.random.default_rng(1).standard_normal((g.ndof, nrhs))).cuda()
 x = torch.empty_like(b)
