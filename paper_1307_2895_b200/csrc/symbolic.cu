@@ -366,8 +366,45 @@ __device__ __forceinline__ void amax64(int64_t* p, int64_t v) {
   atomicMax((unsigned long long*)p, (unsigned long long)v);
 }
 
+
+// Maxima of a grid-stride loop: per thread over its items, then per block
+// (warp shuffles, shared memory), then one atomic per block and field -- the
+// per-item atomics on the few LevelTotals words serialized at L2 (config 3
+// level 0.5: 130,560 groups x 8 fields, 0.47 ms).  Values are >= 0.
+template <int NF>
+struct BlockMax {
+  int64_t v[NF];
+  __device__ BlockMax() {
+#pragma unroll
+    for (int i = 0; i < NF; ++i) v[i] = 0;
+  }
+  __device__ void put(int i, int64_t x) { v[i] = x > v[i] ? x : v[i]; }
+  // every thread of the block calls it (blockDim.x <= 1024, a multiple of 32)
+  __device__ void commit(int64_t* const (&dst)[NF]) {
+    __shared__ int64_t sh[32][NF];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+      int64_t x = v[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t y = __shfl_xor_sync(0xffffffffu, x, o);
+        x = y > x ? y : x;
+      }
+      if (lane == 0) sh[w][i] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < NF) {
+      int64_t x = 0;
+      for (int k = 0; k < nw; ++k) x = sh[k][threadIdx.x] > x ? sh[k][threadIdx.x] : x;
+      if (x > 0) amax64(dst[threadIdx.x], x);
+    }
+  }
+};
+
 __global__ void elim_size_kernel(const SymFront P, int is_top, ElimInc* __restrict__ inc, LevelTotals* tot) {
   const int ng = *P.ng;
+  BlockMax<7> m;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
     const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g], nb = P.nb[g], mb = P.maxnb[g];
     const ElimSizes z = elim_sizes(nc, nq, mb, is_top != 0);
@@ -382,16 +419,19 @@ __global__ void elim_size_kernel(const SymFront P, int is_top, ElimInc* __restri
     I.v[7] = z.big;                                                    // big cells
     inc[g] = I;
     if (z.big) {
-      amax64(&tot->smem_big, (int64_t)elim_big_smem(nc + nq, mb));
-      amax64(&tot->max_big_nc, nc);
+      m.put(0, (int64_t)elim_big_smem(nc + nq, mb));
+      m.put(1, nc);
     } else {
-      amax64(&tot->smem, (int64_t)z.smem);
-      amax64(&tot->max_small_nf, nc + nq);
+      m.put(2, (int64_t)z.smem);
+      m.put(3, nc + nq);
     }
-    amax64(&tot->max_front, nc + nq);
-    amax64(&tot->max_nc, nc);
-    amax64(&tot->max_nq, nq);
+    m.put(4, nc + nq);
+    m.put(5, nc);
+    m.put(6, nq);
   }
+  int64_t* const dst[7] = {&tot->smem_big, &tot->max_big_nc, &tot->smem, &tot->max_small_nf, &tot->max_front,
+                           &tot->max_nc, &tot->max_nq};
+  m.commit(dst);
 }
 
 __global__ void elim_total_kernel(const int32_t* __restrict__ ng, const ElimInc* __restrict__ inc,
@@ -529,17 +569,25 @@ __global__ void __launch_bounds__(256) elim_stats_part(const int32_t* __restrict
   stat_block_reduce(a, part + blockIdx.x);
 }
 
-__global__ void elim_stats_final(const int32_t* __restrict__ ng, const StatAcc* __restrict__ part, int np,
-                                 LevelStat* st, const int64_t* __restrict__ nblk_inc, int64_t* nblk) {
+// Second stage of the fixed-order level statistics: the kStatGrid partials
+// reduced by one 256-thread block as a tree (a single thread summing them
+// in a row took ~40 us per level on the factor's critical path).
+__device__ StatAcc stat_partials(const StatAcc* __restrict__ part, int np) {
+  StatAcc a;
+  for (int i = 0; i < 8; ++i) a.d[i] = 0.0;
+  for (int i = 0; i < 4; ++i) a.sum[i] = a.mx[i] = 0;
+  if ((int)threadIdx.x < np) a = part[threadIdx.x];
+  __shared__ StatAcc r;
+  stat_block_reduce(a, &r);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) elim_stats_final(const int32_t* __restrict__ ng,
+                                                        const StatAcc* __restrict__ part, int np, LevelStat* st,
+                                                        const int64_t* __restrict__ nblk_inc, int64_t* nblk) {
+  const StatAcc a = stat_partials(part, np);
   if (threadIdx.x != 0) return;
-  StatAcc a = part[0];
-  for (int b = 1; b < np; ++b) {
-    for (int i = 0; i < 8; ++i) a.d[i] += part[b].d[i];
-    for (int i = 0; i < 4; ++i) {
-      a.sum[i] += part[b].sum[i];
-      a.mx[i] = max(a.mx[i], part[b].mx[i]);
-    }
-  }
   const int n = *ng;
   st->ngroups = n;
   st->gflop = a.d[0];
@@ -564,6 +612,7 @@ __global__ void elim_stats_final(const int32_t* __restrict__ ng, const StatAcc* 
 __global__ void skel_size_kernel(const SymFront P, double promote_work, int gram_eps_ok, SkelInc* __restrict__ inc,
                                  LevelTotals* tot) {
   const int ng = *P.ng;
+  BlockMax<8> m;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
     const int nc = (int)(P.goff[g + 1] - P.goff[g]), nq = P.nq[g], nb = P.nb[g], mb = P.maxnb[g];
     const SkelSizes z = skel_sizes(nc, nq, mb);
@@ -579,15 +628,18 @@ __global__ void skel_size_kernel(const SymFront P, double promote_work, int gram
     I.v[6] = nc;                                                       // sk/rd output lists
     I.v[7] = (int64_t)skel_cluster_scratch(nc);                        // cluster workspace
     inc[g] = I;
-    amax64(&tot->smem, (int64_t)z.smem);
-    amax64(&tot->max_nc, nc);
-    amax64(&tot->max_nq, nq);
-    amax64(&tot->max_front, nc + nq);
-    amax64(&tot->cl_need4, (int64_t)skel_cluster_need(nc, nq, mb, 4));
-    amax64(&tot->cl_need2, (int64_t)skel_cluster_need(nc, nq, mb, 2));
-    if (z.mode == 2) amax64(&tot->any_mode2, 1);
-    if (promote && (double)nq * nc * nc >= 4e6) amax64(&tot->any_promote, 1);
+    m.put(0, (int64_t)z.smem);
+    m.put(1, nc);
+    m.put(2, nq);
+    m.put(3, nc + nq);
+    m.put(4, (int64_t)skel_cluster_need(nc, nq, mb, 4));
+    m.put(5, (int64_t)skel_cluster_need(nc, nq, mb, 2));
+    if (z.mode == 2) m.put(6, 1);
+    if (promote && (double)nq * nc * nc >= 4e6) m.put(7, 1);
   }
+  int64_t* const dst[8] = {&tot->smem, &tot->max_nc, &tot->max_nq, &tot->max_front, &tot->cl_need4, &tot->cl_need2,
+                           &tot->any_mode2, &tot->any_promote};
+  m.commit(dst);
 }
 
 __global__ void skel_total_kernel(const int32_t* __restrict__ ng, const SkelInc* __restrict__ inc,
@@ -800,18 +852,12 @@ __global__ void __launch_bounds__(256) skel_stats_part(const SkelTask* __restric
   stat_block_reduce(a, part + blockIdx.x);
 }
 
-__global__ void skel_stats_final(const int32_t* __restrict__ ng, const StatAcc* __restrict__ part, int np,
-                                 const int2* __restrict__ exc, const int2* __restrict__ inc, LevelStat* st,
-                                 int64_t* nblk) {
+__global__ void __launch_bounds__(256) skel_stats_final(const int32_t* __restrict__ ng,
+                                                        const StatAcc* __restrict__ part, int np,
+                                                        const int2* __restrict__ exc, const int2* __restrict__ inc,
+                                                        LevelStat* st, int64_t* nblk) {
+  const StatAcc a = stat_partials(part, np);
   if (threadIdx.x != 0) return;
-  StatAcc a = part[0];
-  for (int b = 1; b < np; ++b) {
-    for (int i = 0; i < 8; ++i) a.d[i] += part[b].d[i];
-    for (int i = 0; i < 4; ++i) {
-      a.sum[i] += part[b].sum[i];
-      a.mx[i] = max(a.mx[i], part[b].mx[i]);
-    }
-  }
   const int n = *ng;
   st->ngroups = n;
   st->nskel = a.sum[0];
@@ -978,7 +1024,7 @@ cudaError_t sym_elim_fill(const SymFront& P, const ElimFillArgs& A, int64_t nred
   elim_fill_kernel<<<sym_grid(4), 256, 0, s>>>(P, A);
   StatAcc* part = stat_parts(W, s);
   elim_stats_part<<<kStatGrid, 256, 0, s>>>(P.ng, A.cellstat, A.cellcls, P, part);
-  elim_stats_final<<<1, 32, 0, s>>>(P.ng, part, kStatGrid, A.stat, A.newblk_total, A.nblk);
+  elim_stats_final<<<1, 256, 0, s>>>(P.ng, part, kStatGrid, A.stat, A.newblk_total, A.nblk);
   // reduction of the forward sweep: contribution rows grouped by neighbour
   // DOF in record order (stable radix sort), targets = the distinct DOFs
   if (nred_ub > 0) {
@@ -1077,7 +1123,7 @@ cudaError_t sym_skel_finish(const SkelTask* tasks, const int32_t* kout, const in
   skel_finish_fill<<<grid, 256, 0, s>>>(tasks, kout, ng, exc, A);
   StatAcc* part = stat_parts(W, s);
   skel_stats_part<<<kStatGrid, 256, 0, s>>>(tasks, kout, ng, part);
-  skel_stats_final<<<1, 32, 0, s>>>(ng, part, kStatGrid, exc, inc, A.stat, A.nblk);
+  skel_stats_final<<<1, 256, 0, s>>>(ng, part, kStatGrid, exc, inc, A.stat, A.nblk);
   return cudaGetLastError();
 }
 
