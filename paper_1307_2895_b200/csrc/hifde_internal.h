@@ -481,6 +481,8 @@ cudaError_t sym_skel_cluster_tasks(SkelTask* tasks, const int64_t* cl_rel, int64
                                    int ng_ub, cudaStream_t s);
 cudaError_t sym_skel_finish(const SkelTask* tasks, const int32_t* kout, const int32_t* ng, int ng_ub,
                             const SkelFinishArgs& A, SymWork& W, cudaStream_t s);
+cudaError_t sym_retire_cells(const int32_t* gmem, const int64_t* goff, const int32_t* ng, uint8_t* active,
+                             cudaStream_t s);
 cudaError_t sym_reset_groups(const int32_t* gmem, const int64_t* goff, const int32_t* ng, int32_t* group_of,
                              cudaStream_t s);
 cudaError_t sym_copy_count(const int64_t* n, int64_t* dst, cudaStream_t s);

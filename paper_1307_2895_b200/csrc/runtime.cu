@@ -909,6 +909,12 @@ struct Factorizer {
       cudaEventDestroy(ev_id);
       cudaEventDestroy(ev_tail);
     }
+    if (sym_s) {
+      cudaStreamSynchronize(sym_s);
+      cudaStreamDestroy(sym_s);
+      cudaEventDestroy(ev_symdone);
+      cudaEventDestroy(ev_symjoin);
+    }
   }
   // Frees every working buffer of the factorization (stream-ordered) and
   // hands the borrowed host buffers back to the cache; idempotent.
@@ -932,6 +938,7 @@ struct Factorizer {
     gpart.release(s);
     scratch.release(s);
     lists.release(s);
+    lists_alt.release(s);
     status.release(s);
     kout.release(s);
     iscratch.release(s);
@@ -1036,6 +1043,23 @@ struct Factorizer {
   // the ranks and the retired rows, not on the tail.
   cudaStream_t tail_s = nullptr;
   cudaEvent_t ev_id = nullptr, ev_tail = nullptr;
+  // Device symbolic of a skeleton level overlapped with the numeric kernels
+  // of the elimination level before it (structure only: partition, fronts,
+  // tables -- nothing of the factor's values): run on sym_s after
+  // ev_symdone (the elimination's symbolic fill and cell retirement), joined
+  // back into the main stream before the level's numeric launches.
+  cudaStream_t sym_s = nullptr;
+  cudaEvent_t ev_symdone = nullptr, ev_symjoin = nullptr;
+  bool symdone_ok = false;
+  DBuf<int32_t> lists_alt;  // the skeleton symbolic's block lists while the elimination reads `lists`
+  cudaStream_t sym_stream() {
+    if (!sym_s) {
+      HCK(cudaStreamCreateWithFlags(&sym_s, cudaStreamNonBlocking));
+      HCK(cudaEventCreateWithFlags(&ev_symdone, cudaEventDisableTiming));
+      HCK(cudaEventCreateWithFlags(&ev_symjoin, cudaEventDisableTiming));
+    }
+    return sym_s;
+  }
   bool tail_pending = false;
   cudaStream_t tail_stream() {
     if (!tail_s) {
@@ -2875,11 +2899,11 @@ struct Factorizer {
   }
 
   // pending status words + totals and scalars to the host (the level's sync)
-  void dev_sync_totals() {
+  void dev_sync_totals(bool statuses = true) {
     HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
     HCK(cudaMemcpyAsync(h_scal, d_scal, sizeof(SymScalars), cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
-    check_status();
+    if (statuses) check_status();  // (not while numeric kernels may still run on the other stream)
   }
 
   // Partition + membership + count pass of a level.  kind 0 interior cells,
@@ -3087,6 +3111,12 @@ struct Factorizer {
     A.red_cnt = red_cnt;
     HCK(sym_elim_fill(P, A, T.sum[4], symw, s));
     HCK(sym_copy_count(&d_scal->red_nt, &d_lstat[st].ntargets, s));
+    HCK(sym_retire_cells(sy_gmem.p, sy_goff.p, &d_scal->ng, d_active, s));
+    if (!sharded()) {  // the next skeleton level's analysis may start from here
+      sym_stream();
+      HCK(cudaEventRecord(ev_symdone, s));
+      symdone_ok = true;
+    }
     F->klog.end(kls, s);
     nblk_ub += T.sum[5];
     mem_entries_ub += T.sum[4];
@@ -3134,6 +3164,21 @@ struct Factorizer {
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
     HCK(cudaEventRecord(L.ev0, s));
+    // overlap with the previous elimination's numeric kernels: the analysis
+    // below runs on sym_s (swapped into `s`) from ev_symdone on
+    const bool ovl = symdone_ok;
+    symdone_ok = false;
+    if (ovl) {
+      HCK(cudaStreamWaitEvent(sym_s, ev_symdone, 0));
+      std::swap(s, sym_s);
+      std::swap(lists, lists_alt);
+    }
+    auto join = [&]() {  // back to the main stream, after the analysis
+      if (!ovl) return;
+      HCK(cudaEventRecord(ev_symjoin, s));
+      std::swap(s, sym_s);
+      HCK(cudaStreamWaitEvent(s, ev_symjoin, 0));
+    };
     const int kls = F->klog.begin("symbolic_device", tag, 0, 0, 0, s);
     SymFront P;
     int64_t ng_ub = 0;
@@ -3151,14 +3196,24 @@ struct Factorizer {
       HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_pred_tmp.p, &d_scal->ng, (int)ng_ub, iters, sy_b0.p,
                          sy_b1.p, sy_changed.p, d_tot, s));
     }
-    dev_sync_totals();
+    dev_sync_totals(!ovl);
     L.lap("dev-count");
     const LevelTotals T = *h_tot;
     if (h_scal->fatal || T.any_mode2 || (g.dim == 3 && T.any_promote)) {
       HCK(sym_reset_groups(sy_gmem.p, sy_goff.p, &d_scal->ng, sy_group_of.p, s));
       F->klog.end(kls, s);
+      join();
       HCK(cudaEventRecord(L.ev1, s));
       return false;
+    }
+    if (ovl) {  // an arena that must grow moves its contents: not while the elimination writes them
+      const bool grow = F->idx.n + (size_t)(T.sum[0] + T.sum[6]) > F->idx.cap ||
+                        F->fac.n + (size_t)T.sum[3] > F->fac.cap || bvals.n + (size_t)T.sum[4] > bvals.cap ||
+                        (size_t)T.sum[2] > scratch.cap;
+      if (grow) {
+        HCK(cudaEventRecord(ev_symjoin, sym_s));
+        HCK(cudaStreamWaitEvent(s, ev_symjoin, 0));
+      }
     }
     nact_ub = h_scal->nact;
     const int64_t ng = T.ng;
@@ -3220,6 +3275,7 @@ struct Factorizer {
     }
     L.nbatches = exact ? nbatch : 1;
     F->klog.end(kls, s);
+    join();
     L.t_sym = now_s() - t_begin;
     L.lap("dev-fill");
     const int64_t st_off = (int64_t)status.bump((size_t)ng, s);

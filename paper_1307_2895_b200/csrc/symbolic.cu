@@ -1133,6 +1133,21 @@ cudaError_t sym_reset_groups(const int32_t* gmem, const int64_t* goff, const int
   return cudaGetLastError();
 }
 
+// Elimination levels: every member of every cell retires (the structural
+// part of the elimination, so the next level's analysis need not wait for
+// the numeric kernels, which clear the same bytes again).
+__global__ void sym_retire_members(const int32_t* __restrict__ gmem, const int64_t* __restrict__ goff,
+                                   const int32_t* __restrict__ ng, uint8_t* __restrict__ active) {
+  const int64_t n = goff[*ng];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    active[gmem[i]] = 0;
+}
+cudaError_t sym_retire_cells(const int32_t* gmem, const int64_t* goff, const int32_t* ng, uint8_t* active,
+                             cudaStream_t s) {
+  sym_retire_members<<<sym_grid(4), 256, 0, s>>>(gmem, goff, ng, active);
+  return cudaGetLastError();
+}
+
 cudaError_t sym_copy_count(const int64_t* n, int64_t* dst, cudaStream_t s) {
   count_to<<<1, 32, 0, s>>>(n, dst);
   return cudaGetLastError();
