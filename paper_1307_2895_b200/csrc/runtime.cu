@@ -880,9 +880,21 @@ Helper& helper_thread() {
 }
 
 struct Factorizer {
-  uint64_t a0_job = 0;  // host CSR upload in flight on the helper thread
+  // host CSR upload in flight on the helper thread: the pattern (which the
+  // symbolic analysis needs) first, then the values on their own copy
+  // stream (needed by the numeric kernels only), overlapping the level-0
+  // analysis
+  uint64_t a0_job = 0, a0_pat_job = 0;
   cudaError_t a0_err = cudaSuccess;
+  cudaStream_t a0_s = nullptr;
+  void a0_pattern_ready() {
+    if (a0_pat_job) {
+      helper.wait(a0_pat_job);
+      a0_pat_job = 0;
+    }
+  }
   void a0_ready() {
+    a0_pattern_ready();
     if (a0_job) {
       helper.wait(a0_job);
       a0_job = 0;
@@ -908,6 +920,10 @@ struct Factorizer {
       cudaStreamDestroy(tail_s);
       cudaEventDestroy(ev_id);
       cudaEventDestroy(ev_tail);
+    }
+    if (a0_s) {
+      cudaStreamSynchronize(a0_s);
+      cudaStreamDestroy(a0_s);
     }
     if (sym_s) {
       cudaStreamSynchronize(sym_s);
@@ -2910,7 +2926,7 @@ struct Factorizer {
   // 1 edges, 2 faces.  Returns false when the level overflowed the device
   // front tiers (the host takes over).
   bool dev_front_count(int ell, int kind, SymFront& P, int64_t& ng_ub) {
-    a0_ready();
+    a0_pattern_ready();  // (the values are the numeric kernels' -- arenas())
     const int w = g.m << ell, k = g.n / w;
     int64_t nkeys = 1;
     for (int ax = 0; ax < g.dim; ++ax) nkeys *= k;
@@ -3685,22 +3701,44 @@ struct Factorizer {
       HCK(cudaGetDevice(&dev));
       const size_t pin_min = (size_t)1 << 20;
       const bool big = (size_t)nnz * 12 > pin_min;  // large inputs: pinned staging
-      a0_job = helper.post([=]() {
+      HCK(cudaStreamCreateWithFlags(&a0_s, cudaStreamNonBlocking));
+      {  // the values' copy follows the allocations
+        cudaEvent_t e0;
+        HCK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+        HCK(cudaEventRecord(e0, s));
+        HCK(cudaStreamWaitEvent(a0_s, e0, 0));
+        HCK(cudaEventDestroy(e0));
+      }
+      const cudaStream_t vs = a0_s;
+      a0_pat_job = helper.post([=]() {
         cudaError_t e = cudaSetDevice(dev);
         if (e == cudaSuccess && big) {
           try {
             pinned_xfer().h2d(d_indptr, ip, (N + 1) * sizeof(int64_t), s);
             pinned_xfer().h2d(d_indices, ix, nnz * sizeof(int32_t), s);
-            pinned_xfer().h2d(d_a0, va, nnz * sizeof(double), s);
           } catch (const Fail&) {
             e = cudaErrorUnknown;
           }
         } else {
           if (e == cudaSuccess) e = cudaMemcpyAsync(d_indptr, ip, (N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
           if (e == cudaSuccess) e = cudaMemcpyAsync(d_indices, ix, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
-          if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, s);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         }
-        a0_err = e;
+        if (e != cudaSuccess) a0_err = e;
+      });
+      a0_job = helper.post([=]() {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess && big) {
+          try {
+            pinned_xfer().h2d(d_a0, va, nnz * sizeof(double), vs);
+          } catch (const Fail&) {
+            e = cudaErrorUnknown;
+          }
+        } else {
+          if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, vs);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(vs);
+        if (e != cudaSuccess) a0_err = e;
       });
     }
     PR.lap("A0");
