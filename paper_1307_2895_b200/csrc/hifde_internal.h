@@ -226,7 +226,7 @@ void launch_inv_tiles(const ElimTask* tasks, const int4* work, int nwork, int p0
 void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles, const Arenas& A,
                         cudaStream_t s);
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt, int max_nc,
-                 cudaStream_t s);
+                 int max_nq, cudaStream_t s);
 void launch_apply_rd(const SkelTask* d_tasks, int ntasks, const Arenas& A, cudaStream_t s);
 int skel_ordered_capacity(size_t smem, int nt);
 constexpr int kClusterThreads = 256;           // threads per CTA of the cluster skeleton kernel

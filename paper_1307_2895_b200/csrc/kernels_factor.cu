@@ -1197,6 +1197,17 @@ __global__ void __launch_bounds__(NT) skel_kernel(const SkelTask* __restrict__ t
   skel_group<NT>(t, A, eps, smem, NoWait{});
 }
 
+// A group per CTA of NTC threads with the lane split of a GNT-thread CTA
+// (bit-identical to skel_kernel<GNT>): smaller CTAs, more groups per SM.
+template <int NTC, int GNT>
+__global__ void __launch_bounds__(NTC) skel_team_kernel(const SkelTask* __restrict__ tasks, Arenas A, double eps) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red[NTC / 32];
+  __shared__ int shk;
+  const SkelTask t = tasks[blockIdx.x];
+  skel_group_t<CtaTeam<NTC>, GNT>(t, A, eps, smem, NoWait{}, NoPublish{}, red, &shk);
+}
+
 // Snapshot levels of many small groups (those the 128-thread skel_kernel
 // takes): one warp per group, W groups per CTA, each warp with its own slice
 // of the dynamic shared memory and only warp barriers.  The CPQR keeps the
@@ -1646,7 +1657,7 @@ void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles
 }
 
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt, int max_nc,
-                 cudaStream_t s) {
+                 int max_nq, cudaStream_t s) {
   if (ntasks <= 0) return;
   static bool once = false;
   if (!once) {
@@ -1654,8 +1665,8 @@ void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double ep
     allow_smem(skel_kernel<512>);
     once = true;
   }
-  // (HIFDE_NO_SKEL_WARP: the one-CTA kernel instead -- the tests' A/B, which
-  // must agree bit for bit)
+  // (HIFDE_NO_SKEL_WARP: the one-CTA kernels of the level's lane split
+  // instead -- the tests' A/B, which must agree bit for bit)
   static const bool no_warp = getenv("HIFDE_NO_SKEL_WARP") != nullptr;
   // many tiny groups (config 3 level 0.5: 7 x 44, 4.4 -> 2.6 ms; config 5
   // level 1/3: 9 x 92, 5.7 -> 4.1 ms; the 15-column groups of config 3 level
@@ -1667,6 +1678,23 @@ void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double ep
     const int W = (int)std::min<size_t>(8, std::max<size_t>(1, (kSmemCapBytes - 2048) / std::max<size_t>(per, 16)));
     if (W == 8) {
       skel_warp_kernel<8><<<(ntasks + 7) / 8, 256, per * 8, s>>>(d_tasks, ntasks, A, eps, (int)per);
+      return;
+    }
+  }
+  // half-size CTAs with the full-size CTA's lane split (bit-identical),
+  // more groups per SM: 15-column groups (config 3 level 1.5: 2.71 -> 2.40
+  // ms on 64 threads) and 512-thread groups with short neighbour blocks
+  // (config 3 level 2.5: 3.16 -> 2.56 ms on 256 threads; the tall ones of
+  // config 5 level 1 2/3 are slower: 30 -> 36 ms)
+  if (!no_warp) {
+    static bool once_t = (allow_smem(skel_team_kernel<64, 128>), allow_smem(skel_team_kernel<256, 512>), true);
+    (void)once_t;
+    if (nt <= 128) {
+      skel_team_kernel<64, 128><<<ntasks, 64, smem, s>>>(d_tasks, A, eps);
+      return;
+    }
+    if (max_nq <= 256) {
+      skel_team_kernel<256, 512><<<ntasks, 256, smem, s>>>(d_tasks, A, eps);
       return;
     }
   }

@@ -2321,7 +2321,7 @@ struct Factorizer {
         if (hi > lo) {
           const int kl = F->klog.begin("skel_kernel", tag, 0, 0, 0, s);
           launch_skel(dt.p + lo, (int)(hi - lo), arenas_r(r, false), opt.eps, smem,
-                      (max_nc > 32 || max_nq > 128) ? 512 : 128, (int)max_nc, s);
+                      (max_nc > 32 || max_nq > 128) ? 512 : 128, (int)max_nc, (int)max_nq, s);
           F->klog.end(kl, s);
           ++g_launches;
         }
@@ -3344,7 +3344,7 @@ struct Factorizer {
       ++g_launches;
     } else {
       const int kl = F->klog.begin("skel_kernel", tag, 0, 0, 0, s);
-      launch_skel(sy_tasks.p, (int)ng, Ar, opt.eps, (size_t)T.smem, nthr, (int)T.max_nc, s);
+      launch_skel(sy_tasks.p, (int)ng, Ar, opt.eps, (size_t)T.smem, nthr, (int)T.max_nc, (int)T.max_nq, s);
       F->klog.end(kl, s);
       launch_apply_rd(sy_tasks.p, (int)ng, Ar, s);
       g_launches += 2;

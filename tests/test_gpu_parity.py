@@ -444,7 +444,7 @@ import numpy as np
 sys.path.insert(0, ".")
 import paper_1307_2895_b200 as H
 out = {}
-for dim, n, m, eps, var, seed in [(2, 512, 8, 1e-9, "hifde", 5), (2, 1024, 8, 1e-6, "hifde", 0),
+for dim, n, m, eps, var, seed in [(2, 512, 8, 1e-9, "hifde", 5), (2, 2048, 8, 1e-9, "hifde", 0),
                                   (3, 64, 4, 1e-3, "hifde3x", 2)]:
     g = H.build_grid(dim, n, m)
     a = H.assemble(g, H.gaussian_contrast_field(g, seed=seed))
@@ -457,11 +457,13 @@ np.savez(sys.argv[1], **out)
 
 
 def test_warp_skeleton_kernel_bit_identical(tmp_path):
-    """Snapshot levels of 4096+ small groups run one warp per group
-    (skel_warp_kernel) with the 128-thread CTA's lane split: ranks and
-    solutions identical bit for bit to the one-CTA kernel's
-    (HIFDE_NO_SKEL_WARP), on random-coefficient problems whose fine levels
-    drop DOFs (2D eps 1e-9 / 1e-6, 3D eps 1e-3)."""
+    """Snapshot levels run their groups on smaller thread teams than the
+    lane split they keep -- one warp per tiny group (skel_warp_kernel),
+    64-thread CTAs for the 128-thread split, 256 for the 512-thread one
+    (skel_team_kernel): ranks and solutions identical bit for bit to the
+    full-size CTAs' (HIFDE_NO_SKEL_WARP), on random-coefficient problems
+    whose fine levels drop DOFs (2D 511^2 and 2047^2 at eps 1e-9, 3D 63^3
+    at eps 1e-3; the 2047^2 grid's levels 0.5-2.5 are snapshot levels)."""
     import os
     import subprocess
     import sys
