@@ -608,13 +608,13 @@ __device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double*
   const int lane = threadIdx.x & 31;
   const int mt = (M + 7) >> 3, ntr = (R + 7) >> 3, npair = mt * ntr;
   const int ar = lane >> 2, ak = lane & 3;
-  const bool one_rt = NW % ntr == 0;  // every pair of this warp in RHS tile w % ntr
+  // the pipelined kernels' RHS counts (8, 16, 32, 64) divide the warps: every
+  // pair of a warp is in RHS tile w % ntr
   // this warp's tile pairs p = w + NW j: with one RHS tile per warp the row
   // tile is m0 + j * dm (no division in the k loop)
   const int nj = w < npair ? (npair - 1 - w) / NW + 1 : 0;
   const int m0 = w / ntr, dm = NW / ntr, r0 = w - m0 * ntr;
-  auto tmj = [&](int j) { return one_rt ? m0 + j * dm : (w + NW * j) / ntr; };
-  auto trj = [&](int j) { return one_rt ? r0 : (w + NW * j) % ntr; };
+  auto tmj = [&](int j) { return m0 + j * dm; };
   // pairs in batches of MJ accumulators (M up to 192 rows: 24 row tiles)
   // kOne: exactly one pass, also for a warp without tiles, so that `pre`
   // (a group barrier between the k loops and the in-place outputs) is met by
@@ -625,7 +625,6 @@ __device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double*
     int ibase[MJ];  // per tile: the A offset of (row i, k = 0), or -1 past M
     int klim[MJ];   // per tile: the k0 bound of its nonzero A columns
     int irow[MJ];   // per tile: this lane's A row
-    int xcol[MJ];   // per tile (several RHS tiles per warp): its X column
 #pragma unroll
     for (int j = 0; j < MJ; ++j) {
       acc[j][0] = acc[j][1] = 0.0;
@@ -639,7 +638,6 @@ __device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double*
       ibase[j] = (j < nb && i < M) ? base : -1;
       irow[j] = i;
       klim[j] = AM == 0 ? 8 * mi + 8 : 8 * mi;  // AM 0: k0 < klim; AM 1: k0 + 4 > klim
-      xcol[j] = j < nb ? 8 * trj(jb + j) + ar : R;
     }
     int klo = 0, khi = nb > 0 ? K : 0;
     if (AM == 0 && nb > 0) khi = min(K, 8 * tmj(jb + nb - 1) + 8);
@@ -648,8 +646,7 @@ __device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double*
     for (int k0 = klo & ~3; k0 < khi; k0 += 4) {
       const int k = k0 + ak;
       const bool kin = k < K;
-      double b0 = 0.0;
-      if (one_rt) b0 = (kin && cfix < R) ? X[k * ldx + cfix] : 0.0;
+      const double b = (kin && cfix < R) ? X[k * ldx + cfix] : 0.0;
       int koff;  // the k part of A's offset
       if (AM == 0) koff = k;
       else if (AM == 1) koff = k * (k + 1) / 2;
@@ -665,11 +662,6 @@ __device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double*
         if (AM == 0) nz = nz && k <= irow[j];  // lower triangle
         if (AM == 1) nz = nz && k >= irow[j];  // its transpose
         const double a = nz ? A[i + koff] : 0.0;
-        double b = b0;
-        if (!one_rt) {
-          const int c = xcol[j];
-          b = (kin && c < R) ? X[k * ldx + c] : 0.0;
-        }
         dmma_8x8x4(acc[j][0], acc[j][1], a, b);
       }
     }
@@ -679,7 +671,7 @@ __device__ __forceinline__ void warp_mma_lean(int w, int M, int K, const double*
       if (j >= nb) break;
       const int row = 8 * tmj(jb + j) + (lane >> 2);
       if (row >= M) continue;
-      const int col = 8 * trj(jb + j) + 2 * (lane & 3);
+      const int col = 8 * r0 + 2 * (lane & 3);
       if (col < R) out(row, col, acc[j][0], acc[j][1]);  // R even: both columns valid
     }
   }
