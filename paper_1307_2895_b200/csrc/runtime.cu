@@ -4055,7 +4055,7 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
   // fine elimination levels: the single-load-phase kernels
   static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
   constexpr int small_max_rhs = 64, small_max_n = 96;
-  constexpr size_t small_max_smem = (size_t)200 * 1024;
+  constexpr size_t small_max_smem = kSmemCapBytes;  // (200 KB kept config 3 level 3, 208 KB, on the streaming kernels: 2x slower)
   auto small_path = [&](const LevelRec& L) {
     return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
            L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
