@@ -920,6 +920,7 @@ struct Factorizer {
       cudaStreamDestroy(tail_s);
       cudaEventDestroy(ev_id);
       cudaEventDestroy(ev_tail);
+      cudaEventDestroy(ev_inv);
     }
     if (a0_s) {
       cudaStreamSynchronize(a0_s);
@@ -938,6 +939,7 @@ struct Factorizer {
   void release_all() {
     if (released) return;
     released = true;
+    if (tail_s) join_inv();  // the deferred inverses read buffers freed here
     if (borrowed) {
       HostCache& hc = host_cache();
       hc.idx_buf.swap(h_idx);
@@ -1082,8 +1084,22 @@ struct Factorizer {
       HCK(cudaStreamCreateWithFlags(&tail_s, cudaStreamNonBlocking));
       HCK(cudaEventCreateWithFlags(&ev_id, cudaEventDisableTiming));
       HCK(cudaEventCreateWithFlags(&ev_tail, cudaEventDisableTiming));
+      HCK(cudaEventCreateWithFlags(&ev_inv, cudaEventDisableTiming));
     }
     return tail_s;
+  }
+  // Packed inverses of a device elimination level's blocked cells run on the
+  // tail stream (only the solve reads them), under the next skeleton level;
+  // joined before anything they read or write can move: the next
+  // elimination's analysis (it rewrites the big-cell task table), a growth of
+  // the factor or status arenas, the hand-over to the host, the end.
+  cudaEvent_t ev_inv = nullptr;
+  bool inv_pending = false;
+  void join_inv() {
+    if (!inv_pending) return;
+    HCK(cudaEventRecord(ev_inv, tail_s));
+    HCK(cudaStreamWaitEvent(s, ev_inv, 0));
+    inv_pending = false;
   }
   // main stream waits for every tail issued so far
   void join_tails() {
@@ -1713,7 +1729,7 @@ struct Factorizer {
   // (kernels_big.cu): per-cell work lists on the host from (nc, nq), the
   // cells' ElimTasks already on the device at d_big.
   void launch_big_cells(const std::vector<ElimTask>& big, const ElimTask* d_big, size_t smem_big, Arenas A,
-                        double tag, bool is_top, double gb, double gf) {
+                        double tag, bool is_top, double gb, double gf, bool defer_inverse = false) {
     if (big.empty()) return;
     std::vector<int4> tiles, asm_work;
     int max_big_nc = 0;
@@ -1793,13 +1809,22 @@ struct Factorizer {
       ++g_launches;
     }
     launch_big_finish(d_big, (int)big.size(), A, d_dmin.p, d_scale.p, s);
-    g_launches += 1 + inv.launch(d_big, A, s);
+    if (defer_inverse) {
+      const cudaStream_t ts = tail_stream();
+      HCK(cudaEventRecord(ev_id, s));
+      HCK(cudaStreamWaitEvent(ts, ev_id, 0));
+      g_launches += 1 + inv.launch(d_big, A, ts);
+      inv.release(ts);
+      inv_pending = true;
+    } else {
+      g_launches += 1 + inv.launch(d_big, A, s);
+      inv.release(s);
+    }
     F->klog.end(kl, s);
     d_tiles.release(s);
     d_asm.release(s);
     d_ptrsm.release(s);
     d_pupd.release(s);
-    inv.release(s);
     d_pcells.release(s);
     d_dmin.release(s);
     d_scale.release(s);
@@ -3033,6 +3058,7 @@ struct Factorizer {
   // returns false if the host must take this level (state handed over)
   bool dev_elimination_level(int ell, double tag, LevelRec& L) {
     const double t_begin = now_s();
+    join_inv();  // its analysis rewrites the big-cell task table
     L.kind = 0;
     L.lap(nullptr);
     HCK(cudaEventCreate(&L.ev0));
@@ -3153,7 +3179,7 @@ struct Factorizer {
       std::vector<ElimTask> big((size_t)nbig);
       HCK(cudaMemcpyAsync(big.data(), sy_big.p, sizeof(ElimTask) * (size_t)nbig, cudaMemcpyDeviceToHost, s));
       HCK(cudaStreamSynchronize(s));
-      launch_big_cells(big, sy_big.p, (size_t)T.smem_big, Ar, tag, false, 0, 0);
+      launch_big_cells(big, sy_big.p, (size_t)T.smem_big, Ar, tag, false, 0, 0, !sharded());
     }
     HCK(cudaEventRecord(L.ev1, s));
     HCK(cudaGetLastError());
@@ -3222,14 +3248,16 @@ struct Factorizer {
       HCK(cudaEventRecord(L.ev1, s));
       return false;
     }
-    if (ovl) {  // an arena that must grow moves its contents: not while the elimination writes them
+    {  // an arena that must grow moves its contents: not while the elimination
+       // (overlapped) or the deferred inverses write them
       const bool grow = F->idx.n + (size_t)(T.sum[0] + T.sum[6]) > F->idx.cap ||
                         F->fac.n + (size_t)T.sum[3] > F->fac.cap || bvals.n + (size_t)T.sum[4] > bvals.cap ||
                         (size_t)T.sum[2] > scratch.cap;
-      if (grow) {
+      if (grow && ovl) {
         HCK(cudaEventRecord(ev_symjoin, sym_s));
         HCK(cudaStreamWaitEvent(s, ev_symjoin, 0));
       }
+      if (grow) join_inv();
     }
     nact_ub = h_scal->nact;
     const int64_t ng = T.ng;
@@ -3294,6 +3322,7 @@ struct Factorizer {
     join();
     L.t_sym = now_s() - t_begin;
     L.lap("dev-fill");
+    if (status.n + (size_t)ng > status.cap) join_inv();  // (the deferred inverses read their statuses)
     const int64_t st_off = (int64_t)status.bump((size_t)ng, s);
     HCK(cudaMemsetAsync(status.p + st_off, 0, (size_t)ng * sizeof(int), s));
     pending.push_back({st_off, ng, tag, "group"});
@@ -3385,6 +3414,7 @@ struct Factorizer {
   void dev_to_host() {
     if (!dev_mode) return;
     dev_mode = false;
+    join_inv();
     HCK(cudaMemcpyAsync(h_scal, d_scal, sizeof(SymScalars), cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const int64_t nb = h_scal->nblk;
