@@ -253,6 +253,28 @@ def test_indefinite_block_raises():
         H.factor_mf(a, g)
 
 
+def test_failed_factorizations_release_device_memory():
+    """A factorization that raises (IndefiniteBlockError from the level-0
+    cells of a large grid) frees its working buffers (Factorizer::release_all):
+    repeated failures leave the device's free memory flat, so a caller that
+    catches the error and retries does not run out of HBM."""
+    import torch
+    g = H.build_grid(2, 512, 8)
+    fld = H.constant_field(g)
+    fld.b[100:140, 100:140] = -1e4
+    a = H.assemble(g, fld)
+    with pytest.raises(H.IndefiniteBlockError):
+        H.factor_hifde(a, g, 1e-6)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(4):
+        with pytest.raises(H.IndefiniteBlockError):
+            H.factor_hifde(a, g, 1e-6)
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 <= 64 << 20, (free0 - free1) / 2**20
+
+
 def test_hifde3x_rejects_2d():
     g = H.build_grid(2, 8, 2)
     a = H.assemble(g, H.constant_field(g))
