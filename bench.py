@@ -362,7 +362,7 @@ class Runner:
 
 def roofline(kstats, steps, pk, pk_kind):
     """Dominant kernel of the step by CUDA-event time (the kernel log of the
-    library: every main launch bracketed by events on the library's stream).
+    library: every main launch bracketed by events on the stream it runs on).
     achieved = its algorithmic bytes (or FLOPs) per launch over its average
     launch duration; bound = FP64 tensor pipe when the work's arithmetic
     intensity is above the ridge (measured DGEMM / measured copy), else HBM."""
@@ -374,7 +374,11 @@ def roofline(kstats, steps, pk, pk_kind):
         for f in ("launches", "seconds", "gbytes", "gflop"):
             a[f] += k[f]
     total = sum(a["seconds"] for a in agg.values())
-    dom = max(agg.values(), key=lambda a: a["seconds"])
+    # the roofline's kernel: the one with the most time among those with
+    # algorithmic work (the device symbolic pass is integer bookkeeping with
+    # no bytes/FLOPs model, and its interval on the second stream spans the
+    # elimination kernels it overlaps)
+    dom = max((a for a in agg.values() if a["gbytes"] > 0 or a["gflop"] > 0), key=lambda a: a["seconds"])
     per_launch_s = dom["seconds"] / max(dom["launches"], 1)
     gb_l = dom["gbytes"] / max(dom["launches"], 1)
     gf_l = dom["gflop"] / max(dom["launches"], 1)
