@@ -274,12 +274,14 @@ __device__ __forceinline__ void diag_factor_warp(PackedLower F, int p0, int pw, 
   const double* Fl = F.row(p0 + (l < pw ? l : 0)) + p0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) r[j] = (l < pw && j <= l) ? Fl[j] : 0.0;
+  bool ok = true;  // (locals: the reference parameters were kept in local memory across the steps)
+  double dm = dmin;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     if (k < pw) {  // warp-uniform
       const double akk = __shfl_sync(0xffffffffu, r[k], k);
-      if (!(akk > 0.0)) bad = 1;
-      dmin = fmin(dmin, akk);
+      ok = ok && akk > 0.0;
+      dm = fmin(dm, akk);
       const double lkk = sqrt(akk);
       const double inv = __drcp_rn(lkk);
       if (l == k) r[k] = lkk;
@@ -291,10 +293,16 @@ __device__ __forceinline__ void diag_factor_warp(PackedLower F, int p0, int pw, 
       }
     }
   }
+  if (!ok) bad = 1;
+  dmin = dm;
   if (l < 8) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) Lp[l * 8 + j] = (l < pw && j <= l) ? r[j] : 0.0;
-    Lp[64 + l] = l < pw ? __drcp_rn(r[l]) : 0.0;
+    double rl = r[0];  // r[l] without a dynamic register index (which sends r to local memory)
+#pragma unroll
+    for (int j = 1; j < 8; ++j)
+      if (j == l) rl = r[j];
+    Lp[64 + l] = l < pw ? __drcp_rn(rl) : 0.0;
   }
 }
 
@@ -360,9 +368,7 @@ __device__ int front_chol_blocked(PackedLower F, int nc, int nf, double* red, do
     // trailing lower triangle from p1: F[i][j] -= sum_k L[i][p0+k] L[j][p0+k];
     // tile 0 (the next diagonal block) by warp 0, which then factors it
     const int nt = (nf - p1 + 7) / 8, ntt = nt * (nt + 1) / 2;
-    auto tile = [&](int tt) {
-      int ti, tj;
-      tri_tile(tt, ti, tj);
+    auto tile = [&](int ti, int tj) {
       const int rb = p1 + 8 * ti, cb = p1 + 8 * tj;
       double c0 = 0.0, c1 = 0.0;
       const int ra = rb + (lane >> 2), rc = cb + (lane >> 2);
@@ -392,16 +398,30 @@ __device__ int front_chol_blocked(PackedLower F, int nc, int nf, double* red, do
           if (j <= lane) F.row(p0 + lane)[p0 + j] = Lp[lane * 8 + j];
       }
       if (ntt > 0) {
-        tile(0);
+        tile(0, 0);
         __syncwarp();
         if (p1 < nc) {
           diag_factor_warp(F, p1, min(8, nc - p1), Lw + 72 * (buf ^ 1), bad, dmin);
           if (lane == 0) s_bad = bad;
         }
       }
-      for (int tt = NW; tt < ntt; tt += NW) tile(tt);  // warp 0's share beyond tile 0
+      // warp 0's share beyond tile 0; (ti, tj) of tile tt = ti (ti + 1) / 2 + tj
+      // advanced incrementally (tri_tile's float sqrt per tile was ~8% of the
+      // samples)
+      int ti = 0, tj = 0;
+      for (int tt = NW; tt < ntt; tt += NW) {
+        tj += NW;
+        while (tj > ti) { tj -= ti + 1; ++ti; }
+        tile(ti, tj);
+      }
     } else {
-      for (int tt = wid; tt < ntt; tt += NW) tile(tt);
+      int ti, tj;
+      tri_tile(wid, ti, tj);
+      for (int tt = wid; tt < ntt; tt += NW) {
+        tile(ti, tj);
+        tj += NW;
+        while (tj > ti) { tj -= ti + 1; ++ti; }
+      }
     }
     buf ^= 1;
     __syncthreads();
