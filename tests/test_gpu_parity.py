@@ -275,6 +275,34 @@ def test_failed_factorizations_release_device_memory():
     assert free0 - free1 <= 64 << 20, (free0 - free1) / 2**20
 
 
+def test_int32_and_int64_csr_offsets_agree():
+    """options.indptr_int32: scipy's int32 offsets go in as they are and are
+    widened by the library; the factor is bit-identical to the one from
+    int64 offsets (both through the C ABI)."""
+    import ctypes as C
+    from paper_1307_2895_b200 import _lib as L
+    lib = L.load()
+    g = H.build_grid(2, 256, 8)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=3))
+    ix = np.ascontiguousarray(a.indices, dtype=np.int32)
+    va = np.ascontiguousarray(a.data, dtype=np.float64)
+    b = np.random.default_rng(2).standard_normal((g.ndof, 3))
+    out = []
+    for ip in (np.ascontiguousarray(a.indptr, dtype=np.int32), np.ascontiguousarray(a.indptr, dtype=np.int64)):
+        opt = L.Options()
+        lib.hifde_default_options(C.byref(opt), L.VARIANT_HIFDE)
+        opt.eps = 1e-9
+        opt.indptr_int32 = int(ip.dtype == np.int32)
+        h = C.c_void_p()
+        assert lib.hifde_factor(ip.ctypes.data, ix.ctypes.data, va.ctypes.data, g.ndof, g.dim, g.n, g.m,
+                                g.nlevels, C.byref(opt), C.byref(h)) == 0
+        f = H.GeneralizedLDL(h.value, lib, True)
+        out.append((f.metrics["skeleton_counts"], f.apply_inverse(b)))
+        f.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+
+
 def test_hifde3x_rejects_2d():
     g = H.build_grid(2, 8, 2)
     a = H.assemble(g, H.constant_field(g))
