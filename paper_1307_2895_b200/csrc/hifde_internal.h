@@ -278,6 +278,8 @@ void launch_skelbig_symm(const SkelBigTask* tasks, const int4* work, int nwork, 
 // solve
 // small elimination records (nc, nq <= 64, 2..16 RHS): one shared-memory load phase
 size_t solve_small_smem(int max_nc, int max_nq, int nrhs);
+void launch_solve_rec_rows(const SolveRec* recs, int nrec, const int32_t* idx, int32_t* cmin, int32_t* cmax,
+                           cudaStream_t s);
 void launch_solve_elim_small(const SolveRec* recs, int nrec, const int32_t* idx, const double* fac, int64_t fac_len,
                              double* v, int nrhs, double* contrib, int max_nc, int max_nq, size_t smem, int forward,
                              cudaStream_t s);

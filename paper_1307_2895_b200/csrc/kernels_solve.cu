@@ -1449,6 +1449,21 @@ size_t solve_small_smem(int max_nc, int max_nq, int nrhs) {
                            (size_t)max_nq * nrhs);
 }
 
+// Per record of an elimination level: its smallest and largest cell DOF
+// (cells ascending in the index arena), for the banded host solve.
+__global__ void solve_rec_rows_kernel(const SolveRec* __restrict__ recs, int nrec, const int32_t* __restrict__ idx,
+                                      int32_t* __restrict__ cmin, int32_t* __restrict__ cmax) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrec) return;
+  const SolveRec rc = recs[r];
+  cmin[r] = rc.nc > 0 ? idx[rc.idx_off] : 0x7fffffff;
+  cmax[r] = rc.nc > 0 ? idx[rc.idx_off + rc.nc - 1] : -1;
+}
+void launch_solve_rec_rows(const SolveRec* recs, int nrec, const int32_t* idx, int32_t* cmin, int32_t* cmax,
+                           cudaStream_t s) {
+  if (nrec > 0) solve_rec_rows_kernel<<<(nrec + 255) / 256, 256, 0, s>>>(recs, nrec, idx, cmin, cmax);
+}
+
 // Shared memory of the pipelined kernel with `stages` stages (0: the level
 // does not fit two stages).
 static size_t pipe_smem(int max_nc, int max_nq, int nrhs, bool fwd, int& stages) {

@@ -369,6 +369,11 @@ struct hifde_factor {
   int64_t tile_rows = 0;  // solve scratch rows of the tiled phases
   char* meta = nullptr;  // every level's solve metadata (one allocation)
   mutable hifde::KLog klog;  // options.kernel_log (the solve appends its launches)
+  // banded host solve (solve_pipelined): per level-0 record, the prefix max
+  // of its largest cell DOF and the suffix min of its smallest, built once
+  mutable std::mutex band_m;
+  mutable bool band_done = false;
+  mutable std::vector<int32_t> band_pmax, band_smin;
   std::vector<void*> dev_allocs;  // device-symbolic levels' solve / export tables
   mutable std::mutex klog_m;
   ~hifde_factor() {
@@ -4061,7 +4066,23 @@ struct Factorizer {
 // Solve sweep
 // ---------------------------------------------------------------------------
 // The up/down sweep on the device block v (N x nrhs row-major, in place).
-void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
+// Level 0 of the sweep in record bands (solve_pipelined): the forward band
+// b waits on fwd_wait[b] (the upload of the rows it reads), the backward
+// band b records bwd_done[b] (its rows may leave).
+struct SweepBands {
+  std::vector<std::pair<int, int>> fwd, bwd;
+  std::vector<cudaEvent_t> fwd_wait, bwd_done;
+};
+
+// Whether level 0 can run banded: every record on the one-CTA kernels.
+bool level0_bandable(const hifde_factor_t* F) {
+  if (F->levels.empty()) return false;
+  const LevelRec& L = F->levels[0];
+  return L.kind == 0 && L.d_recs && L.nsmall > 0 && L.nsmall == L.nall && L.fwd_ph.empty() && L.bwd_ph.empty() &&
+         L.max_nc <= 96 && L.max_nq <= 192;
+}
+
+void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s, const SweepBands* bands = nullptr) {
   double* contrib = nullptr;
   HCK(cudaMallocAsync((void**)&contrib, std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
   double* tscr = nullptr;
@@ -4133,7 +4154,19 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
       }
       phases(L.fwd_ph);
     } else {
-      if (nr && small_path(L)) {
+      if (li == 0 && bands && !(nr && small_path(L)))  // (not banded after all: wait for the whole upload)
+        for (cudaEvent_t e : bands->fwd_wait) HCK(cudaStreamWaitEvent(s, e, 0));
+      if (li == 0 && bands && nr && small_path(L)) {  // upload bands as they land
+        for (size_t b = 0; b < bands->fwd.size(); ++b) {
+          HCK(cudaStreamWaitEvent(s, bands->fwd_wait[b], 0));
+          const int lo = bands->fwd[b].first, hi = bands->fwd[b].second;
+          if (hi > lo) {
+            launch_solve_elim_small(L.d_recs + lo, hi - lo, idx, fac, (int64_t)F->fac.cap, v, nrhs, contrib, L.max_nc,
+                                    L.max_nq, solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
+            ++g_launches;
+          }
+        }
+      } else if (nr && small_path(L)) {
         launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, v, nrhs, contrib, L.max_nc, L.max_nq,
                                 solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
         ++g_launches;
@@ -4168,7 +4201,17 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
         ++g_launches;
       }
     } else {
-      if (nr && small_path(L)) {
+      if (li == 0 && bands && nr && small_path(L)) {  // rows leave as their bands finish
+        for (size_t b = 0; b < bands->bwd.size(); ++b) {
+          const int lo = bands->bwd[b].first, hi = bands->bwd[b].second;
+          if (hi > lo) {
+            launch_solve_elim_small(L.d_recs + lo, hi - lo, idx, fac, (int64_t)F->fac.cap, v, nrhs, nullptr,
+                                    L.max_nc, L.max_nq, solve_small_smem(L.max_nc, L.max_nq, nrhs), 0, s);
+            ++g_launches;
+          }
+          HCK(cudaEventRecord(bands->bwd_done[b], s));
+        }
+      } else if (nr && small_path(L)) {
         launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, v, nrhs, nullptr, L.max_nc, L.max_nq,
                                 solve_small_smem(L.max_nc, L.max_nq, nrhs), 0, s);
         ++g_launches;
@@ -4178,11 +4221,38 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s) {
       }
     }
     phases(L.bwd_ph);
+    if (li == 0 && bands && !(nr && small_path(L)))  // (not banded after all: every band done here)
+      for (cudaEvent_t e : bands->bwd_done) HCK(cudaEventRecord(e, s));
   }
   HCK(cudaGetLastError());
   HCK(cudaFreeAsync(contrib, s));
   HCK(cudaFreeAsync(tscr, s));
   HCK(cudaFreeAsync(scratch, s));
+}
+
+// The level-0 record bounds of the banded host solve, computed once per
+// factor: prefix max of the records' largest cell DOF (pmax[j] = over
+// records < j) and suffix min of their smallest (smin[j] = over records >= j).
+bool level0_bands(const hifde_factor_t* F, cudaStream_t s) {
+  if (!level0_bandable(F)) return false;
+  std::lock_guard<std::mutex> lk(F->band_m);
+  if (!F->band_done) {
+    const LevelRec& L = F->levels[0];
+    const int nrec = L.nsmall;
+    int32_t* d = nullptr;
+    HCK(cudaMallocAsync((void**)&d, sizeof(int32_t) * 2 * (size_t)nrec, s));
+    launch_solve_rec_rows(L.d_recs, nrec, F->idx.p, d, d + nrec, s);
+    std::vector<int32_t> h((size_t)2 * nrec);
+    HCK(cudaMemcpyAsync(h.data(), d, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, s));
+    HCK(cudaFreeAsync(d, s));
+    HCK(cudaStreamSynchronize(s));
+    F->band_pmax.assign((size_t)nrec + 1, -1);
+    F->band_smin.assign((size_t)nrec + 1, (int32_t)F->n);
+    for (int j = 0; j < nrec; ++j) F->band_pmax[(size_t)j + 1] = std::max(F->band_pmax[(size_t)j], h[(size_t)nrec + j]);
+    for (int j = nrec; j-- > 0;) F->band_smin[(size_t)j] = std::min(F->band_smin[(size_t)j + 1], h[(size_t)j]);
+    F->band_done = true;
+  }
+  return true;
 }
 
 // Host right-hand sides already page-locked (a pinned torch tensor, ...) and a
@@ -4221,14 +4291,105 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
   HCK(cudaEventCreateWithFlags(&ealloc, cudaEventDisableTiming));
   HCK(cudaEventRecord(ealloc, s));
   HCK(cudaStreamWaitEvent(sh, ealloc, 0));
+  // Banded level 0 (page-locked output, a level 0 of one-CTA records): each
+  // chunk uploads in row bands and its level-0 forward records run as the
+  // rows they read land; its level-0 backward runs in record bands and the
+  // rows they finish leave at once -- the first and last level of every
+  // chunk's sweep overlap its own transfers (config 3, 64 RHS: the last
+  // chunk's tail was sweep 8 + D2H 19 ms after its upload).
+  const bool banded = PinnedXfer::page_locked(x) && level0_bands(F, s);
+  constexpr int kBands = 8;
+  std::vector<SweepBands> sb((size_t)nch);
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> d2h_rows((size_t)nch);
+  std::vector<cudaEvent_t> band_events;
+  auto new_event = [&]() {
+    cudaEvent_t e;
+    HCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    band_events.push_back(e);
+    return e;
+  };
+  if (banded) {
+    const int nrec = (int)F->band_pmax.size() - 1;
+    for (int c = 0; c < nch; ++c) {
+      SweepBands& B = sb[(size_t)c];
+      // forward: band k = records whose cells lie below upload row bound k + 1
+      int j = 0;
+      for (int k = 0; k < kBands; ++k) {
+        const int64_t ub = k + 1 == kBands ? N : N * (k + 1) / kBands;
+        int j1 = j;
+        if (k + 1 == kBands) j1 = nrec;
+        else
+          while (j1 < nrec && F->band_pmax[(size_t)j1 + 1] < ub) ++j1;  // pmax[j1+1]: max cell DOF of records < j1+1
+        B.fwd.emplace_back(j, j1);
+        B.fwd_wait.push_back(new_event());
+        j = j1;
+      }
+      // backward: equal record bands; rows below the smallest cell DOF of the
+      // records still to come are final
+      int64_t done = 0;
+      for (int k = 0; k < kBands; ++k) {
+        const int lo = (int)((int64_t)nrec * k / kBands), hi = (int)((int64_t)nrec * (k + 1) / kBands);
+        B.bwd.emplace_back(lo, hi);
+        B.bwd_done.push_back(new_event());
+        const int64_t fin = hi >= nrec ? N : std::min<int64_t>(N, F->band_smin[(size_t)hi]);
+        d2h_rows[(size_t)c].emplace_back(done, std::max(done, fin));
+        done = std::max(done, fin);
+      }
+    }
+  }
   for (int c = 0; c < nch; ++c) {  // every upload and sweep queued at once
     const int w = c0[(size_t)c + 1] - c0[(size_t)c];
-    HCK(cudaMemcpy2DAsync(vb[(size_t)c], (size_t)w * sizeof(double), b + c0[(size_t)c], (size_t)nrhs * sizeof(double),
-                          (size_t)w * sizeof(double), (size_t)N, cudaMemcpyHostToDevice, sh));
-    HCK(cudaEventRecord(eh[(size_t)c], sh));
-    HCK(cudaStreamWaitEvent(s, eh[(size_t)c], 0));
-    solve_sweep(F, vb[(size_t)c], w, s);
+    if (banded) {
+      for (int k = 0; k < kBands; ++k) {
+        const int64_t r0 = N * k / kBands, r1 = k + 1 == kBands ? N : N * (k + 1) / kBands;
+        if (r1 > r0)
+          HCK(cudaMemcpy2DAsync(vb[(size_t)c] + (size_t)r0 * w, (size_t)w * sizeof(double),
+                                b + (size_t)r0 * nrhs + c0[(size_t)c], (size_t)nrhs * sizeof(double),
+                                (size_t)w * sizeof(double), (size_t)(r1 - r0), cudaMemcpyHostToDevice, sh));
+        HCK(cudaEventRecord(sb[(size_t)c].fwd_wait[(size_t)k], sh));
+      }
+      HCK(cudaEventRecord(eh[(size_t)c], sh));
+      solve_sweep(F, vb[(size_t)c], w, s, &sb[(size_t)c]);
+    } else {
+      HCK(cudaMemcpy2DAsync(vb[(size_t)c], (size_t)w * sizeof(double), b + c0[(size_t)c],
+                            (size_t)nrhs * sizeof(double), (size_t)w * sizeof(double), (size_t)N,
+                            cudaMemcpyHostToDevice, sh));
+      HCK(cudaEventRecord(eh[(size_t)c], sh));
+      HCK(cudaStreamWaitEvent(s, eh[(size_t)c], 0));
+      solve_sweep(F, vb[(size_t)c], w, s);
+    }
     HCK(cudaEventRecord(es[(size_t)c], s));
+  }
+  if (banded) {  // each chunk's finished row bands straight into the caller's columns
+    for (int c = 0; c < nch; ++c) {
+      const int w = c0[(size_t)c + 1] - c0[(size_t)c];
+      for (int k = 0; k < kBands; ++k) {
+        HCK(cudaStreamWaitEvent(sd, sb[(size_t)c].bwd_done[(size_t)k], 0));
+        const int64_t r0 = d2h_rows[(size_t)c][(size_t)k].first, r1 = d2h_rows[(size_t)c][(size_t)k].second;
+        if (r1 > r0)
+          HCK(cudaMemcpy2DAsync(x + (size_t)r0 * nrhs + c0[(size_t)c], (size_t)nrhs * sizeof(double),
+                                vb[(size_t)c] + (size_t)r0 * w, (size_t)w * sizeof(double), (size_t)w * sizeof(double),
+                                (size_t)(r1 - r0), cudaMemcpyDeviceToHost, sd));
+      }
+      HCK(cudaStreamWaitEvent(sd, es[(size_t)c], 0));  // (rows past the last band bound: none; the sweep's end)
+      const int64_t rdone = d2h_rows[(size_t)c].back().second;
+      if (rdone < N)
+        HCK(cudaMemcpy2DAsync(x + (size_t)rdone * nrhs + c0[(size_t)c], (size_t)nrhs * sizeof(double),
+                              vb[(size_t)c] + (size_t)rdone * w, (size_t)w * sizeof(double), (size_t)w * sizeof(double),
+                              (size_t)(N - rdone), cudaMemcpyDeviceToHost, sd));
+    }
+    for (int c = 0; c < nch; ++c) HCK(cudaFreeAsync(vb[(size_t)c], sd));
+    HCK(cudaStreamSynchronize(sd));
+    for (cudaEvent_t e : band_events) cudaEventDestroy(e);
+    for (int c = 0; c < nch; ++c) {
+      cudaEventDestroy(eh[(size_t)c]);
+      cudaEventDestroy(es[(size_t)c]);
+    }
+    cudaEventDestroy(ealloc);
+    HCK(cudaStreamSynchronize(s));
+    cudaStreamDestroy(sh);
+    cudaStreamDestroy(sd);
+    return;
   }
   const size_t total = (size_t)N * nrhs * sizeof(double);
   PinnedXfer::prefault(x, total);  // while the first chunks upload and sweep
