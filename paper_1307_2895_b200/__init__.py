@@ -11,7 +11,7 @@ _os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")  # before libgomp initializ
 
 from .driver import (FactorizationError, GeneralizedLDL, IndefiniteBlockError,
                      SingularBlockError, apply_inverse, densify, device_count, factor_hifde,
-                     factor_hifde3x, factor_mf)
+                     factor_hifde3x, factor_mf, pinned_csr, pinned_empty)
 from .problems import (CoeffField, GridConfig, assemble, baseline_problem, build_grid,
                        constant_field, gaussian_contrast_field, high_contrast_field)
 from .gldl import export_factor, import_factor, load_factor, read_gldl, save_factor, write_gldl

@@ -375,9 +375,11 @@ struct SymFront {
   int32_t* nb;
   int32_t* maxnb;
   int32_t* npred;
-  int32_t* flag;            // 1: the small shared-memory tier overflowed
+  int32_t* flag;            // tier of the group: 0 warp, 1 shared-memory CTA, 2 large CTA
   int32_t* retry;           // groups for the large tier
   int32_t* nretry;
+  int32_t* retry2;          // groups for the shared-memory CTA tier (too large for a warp)
+  int32_t* nretry2;
   int32_t* fatal;           // even the large tier overflowed (host fallback)
   // count pass, skeleton levels: unsorted predecessor lists for the chain
   int32_t* pred_tmp;        // null: not wanted

@@ -934,6 +934,8 @@ struct Factorizer {
     if (sym_s) {
       cudaStreamSynchronize(sym_s);
       cudaStreamDestroy(sym_s);
+      cudaStreamSynchronize(sym_hi);
+      cudaStreamDestroy(sym_hi);
       cudaEventDestroy(ev_symdone);
       cudaEventDestroy(ev_symjoin);
     }
@@ -1075,9 +1077,20 @@ struct Factorizer {
   cudaEvent_t ev_symdone = nullptr, ev_symjoin = nullptr;
   bool symdone_ok = false;
   DBuf<int32_t> lists_alt;  // the skeleton symbolic's block lists while the elimination reads `lists`
+  // From the second overlap on, the analysis runs on a high-priority stream
+  // (sym_hi swapped in): next to the blocked eliminations it is a latency-
+  // bound chain whose CTAs should go first as the elimination's retire.  The
+  // first overlap (the level-0 elimination, which fills the GPU, against the
+  // level-0.5 analysis, which would too) keeps normal priority: reordering
+  // two saturating kernels gains nothing there.
+  cudaStream_t sym_hi = nullptr;
+  int sym_overlaps = 0;
   cudaStream_t sym_stream() {
     if (!sym_s) {
+      int lo = 0, hi = 0;
+      HCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       HCK(cudaStreamCreateWithFlags(&sym_s, cudaStreamNonBlocking));
+      HCK(cudaStreamCreateWithPriority(&sym_hi, cudaStreamNonBlocking, hi));
       HCK(cudaEventCreateWithFlags(&ev_symdone, cudaEventDisableTiming));
       HCK(cudaEventCreateWithFlags(&ev_symjoin, cudaEventDisableTiming));
     }
@@ -2833,7 +2846,7 @@ struct Factorizer {
   // =========================================================================
   struct SymScalars {
     int64_t nact, nalive, nblk, red_nt, pred_alloc;
-    int32_t ng, nretry, fatal, pred_ovf;
+    int32_t ng, nretry, fatal, pred_ovf, nretry2, pad_;
   };
   bool dev_mode = false;
   SymWork symw;
@@ -2841,7 +2854,7 @@ struct Factorizer {
   DBuf<int64_t> sy_goff;
   DBuf<uint8_t> sy_alive;  // block alive flags (device mode)
   DBuf<int32_t> sy_alist, sy_mcnt, sy_mptr, sy_mblk;
-  DBuf<int32_t> sy_nq, sy_nb, sy_maxnb, sy_npred, sy_flag, sy_retry;
+  DBuf<int32_t> sy_nq, sy_nb, sy_maxnb, sy_npred, sy_flag, sy_retry, sy_retry2;
   DBuf<int64_t> sy_inc, sy_exc;  // ElimInc / SkelInc storage (8 words per group)
   DBuf<int32_t> sy_preds, sy_b0, sy_b1, sy_changed, sy_depth, sy_depth2, sy_iota, sy_order;
   DBuf<int64_t> sy_pred_ptr, sy_cl_rel, sy_pred_start;
@@ -2896,7 +2909,7 @@ struct Factorizer {
 
   void dev_release() {
     for (auto* b : {&sy_act, &sy_keys, &sy_skeys, &sy_gmem, &sy_head, &sy_group_of, &sy_alist, &sy_mcnt, &sy_mptr,
-                    &sy_mblk, &sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry, &sy_preds, &sy_b0, &sy_b1,
+                    &sy_mblk, &sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry, &sy_retry2, &sy_preds, &sy_b0, &sy_b1,
                     &sy_changed, &sy_red_key, &sy_red_key2, &sy_depth, &sy_depth2, &sy_iota, &sy_order})
       b->release(s);
     for (auto* b : {&sy_goff, &sy_inc, &sy_exc, &sy_pred_ptr, &sy_cl_rel, &sy_red_val, &sy_pred_start}) b->release(s);
@@ -2938,7 +2951,8 @@ struct Factorizer {
 
   // per-group scratch of the symbolic pass for up to `ng_ub` groups
   void dev_group_reserve(int64_t ng_ub) {
-    for (auto* b : {&sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry}) b->reserve((size_t)ng_ub + 1, s);
+    for (auto* b : {&sy_nq, &sy_nb, &sy_maxnb, &sy_npred, &sy_flag, &sy_retry, &sy_retry2})
+      b->reserve((size_t)ng_ub + 1, s);
     sy_inc.reserve((size_t)8 * (ng_ub + 1), s);
     sy_exc.reserve((size_t)8 * (ng_ub + 1), s);
     sy_goff.reserve((size_t)ng_ub + 2, s);
@@ -3032,6 +3046,8 @@ struct Factorizer {
     P.flag = sy_flag.p;
     P.retry = sy_retry.p;
     P.nretry = &d_scal->nretry;
+    P.retry2 = sy_retry2.p;
+    P.nretry2 = &d_scal->nretry2;
     P.fatal = &d_scal->fatal;
     P.pred_tmp = nullptr;
     if (kind != 0 && opt.order_mode != HIFDE_ORDER_SNAPSHOT) {  // predecessor lists for the chain
@@ -3216,6 +3232,7 @@ struct Factorizer {
     const bool ovl = symdone_ok;
     symdone_ok = false;
     if (ovl) {
+      if (++sym_overlaps == 2) std::swap(sym_s, sym_hi);
       HCK(cudaStreamWaitEvent(sym_s, ev_symdone, 0));
       std::swap(s, sym_s);
       std::swap(lists, lists_alt);
@@ -4057,6 +4074,17 @@ struct Factorizer {
         fprintf(stderr, "[hifde]   tag %6.3f sub:", L.tag);
         for (const auto& p : L.sub) fprintf(stderr, " %s %.3f", p.first, p.second * 1e3);
         fprintf(stderr, "\n");
+      }
+      if (F->klog.on && !F->klog.v.empty()) {  // device timeline of the logged launches (ms from the first)
+        HCK(cudaDeviceSynchronize());
+        const cudaEvent_t t0e = F->klog.v.front().e0;
+        for (const auto& E : F->klog.v) {
+          if (E.phase != 0) continue;
+          float a = 0.f, b = 0.f;
+          cudaEventElapsedTime(&a, t0e, E.e0);
+          cudaEventElapsedTime(&b, t0e, E.e1);
+          fprintf(stderr, "[hifde] tl %8.3f %8.3f %7.3f  %-28s tag %.3f\n", a, b, b - a, E.name.c_str(), E.tag);
+        }
       }
     }
   }

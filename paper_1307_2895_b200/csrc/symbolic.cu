@@ -208,6 +208,157 @@ __global__ void sym_member_fill(const int32_t* __restrict__ alive_list, const in
 // ---------------------------------------------------------------------------
 // Fronts: live blocks touching the group, neighbour set q, predecessors
 // ---------------------------------------------------------------------------
+// Warp tier (kWarpTier below): one warp per group of at most 32 DOFs with
+// per-warp sets of 32 blocks / 128 neighbours / 64 predecessors; config 3's
+// 130,560 edge groups of level 0.5 (7 DOFs, ~50 neighbours) took one
+// 128-thread CTA each, whose barriers and dependent loads (a chain of ~10
+// global reads per phase) left the pass latency-bound at 16 groups per SM.
+// The sets and the sorted outputs are those of the CTA tiers (they do not
+// depend on insertion order); a group whose sets outgrow the warp's goes to
+// the CTA tier's list (flag 1).
+__device__ __forceinline__ int warp_compact(const int32_t* t, int H, int32_t* out, int lane) {
+  int base = 0;
+  for (int i0 = 0; i0 < H; i0 += 32) {
+    const int32_t v = t[i0 + lane];
+    const unsigned m = __ballot_sync(0xffffffffu, v != kEmpty);
+    if (v != kEmpty) out[base + __popc(m & ((1u << lane) - 1u))] = v;
+    base += __popc(m);
+  }
+  __syncwarp();
+  return base;
+}
+// dst[rank(v)] = v for the n distinct values of src (rank = number smaller)
+__device__ __forceinline__ void warp_rank_sort(const int32_t* src, int n, int32_t* dst, int lane) {
+  for (int i = lane; i < n; i += 32) {
+    const int32_t v = src[i];
+    int r = 0;
+    for (int k = 0; k < n; ++k) r += src[k] < v;
+    dst[r] = v;
+  }
+}
+
+constexpr int kWLQ = 7, kWLB = 5, kWLP = 6, kWNC = 32, kWarpTierW = 8;
+
+template <bool FILL>
+__global__ void __launch_bounds__(32 * kWarpTierW) sym_front_warp_kernel(SymFront P) {
+  constexpr int HQ = 1 << kWLQ, HB = 1 << kWLB, HP = 1 << kWLP;
+  constexpr int kPer = kWNC + HB + HQ + HP + HQ;
+  __shared__ __align__(16) int32_t sh[kWarpTierW][kPer];
+  __shared__ int cnt[kWarpTierW][4];  // blocks, neighbours, predecessors, overflow
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t* c = sh[w];
+  int32_t* hb = c + kWNC;
+  int32_t* hq = hb + HB;
+  int32_t* hp = hq + HQ;
+  int32_t* buf = hp + HP;
+  int* ct = cnt[w];
+  const int ngr = *P.ng;
+  for (int g = blockIdx.x * kWarpTierW + w; g < ngr; g += gridDim.x * kWarpTierW) {
+    if (FILL && P.flag[g] != 0) continue;
+    const int64_t c0 = P.goff[g];
+    const int nc = (int)(P.goff[g + 1] - c0);
+    if (nc > kWNC) {  // count pass only (the fill sees flag 1)
+      if (lane == 0) {
+        P.flag[g] = 1;
+        P.retry2[atomicAdd(P.nretry2, 1)] = g;
+      }
+      continue;
+    }
+    for (int i = lane; i < HB; i += 32) hb[i] = kEmpty;
+    for (int i = lane; i < HQ; i += 32) hq[i] = kEmpty;
+    for (int i = lane; i < HP; i += 32) hp[i] = kEmpty;
+    if (lane < 4) ct[lane] = 0;
+    if (lane < nc) c[lane] = P.gmem[c0 + lane];
+    __syncwarp();
+    if (lane < nc) {  // live blocks touching the group
+      const int32_t d = c[lane];
+      for (int32_t t = P.mptr[d]; t < P.mptr[d + 1]; ++t) set_insert(hb, kWLB, P.mblk[t], &ct[0], &ct[3]);
+    }
+    __syncwarp();
+    int nb = 0, maxnb = 0;
+    if (!ct[3]) {
+      nb = warp_compact(hb, HB, buf, lane);
+      for (int j = 0; j < nb; ++j) {  // q candidates: the blocks' DOFs, then A0 rows of c
+        const int32_t b = buf[j];
+        const int n = P.blk_n[b];
+        maxnb = max(maxnb, n);
+        const int32_t* d = P.idx + P.blk_dof_off[b];
+        for (int i = lane; i < n; i += 32) {
+          const int32_t e = d[i];
+          if (P.active[e] && bsearch_sorted(c, nc, e) < 0) set_insert(hq, kWLQ, e, &ct[1], &ct[3]);
+        }
+      }
+      if (lane < nc) {
+        const int32_t d = c[lane];
+        for (int64_t t = P.indptr[d]; t < P.indptr[d + 1]; ++t) {
+          const int32_t e = P.indices[t];
+          if (P.active[e] && bsearch_sorted(c, nc, e) < 0) set_insert(hq, kWLQ, e, &ct[1], &ct[3]);
+        }
+      }
+    }
+    __syncwarp();
+    if (!ct[3] && P.group_of) {  // predecessors: earlier groups owning a DOF of q
+      for (int i = lane; i < HQ; i += 32) {
+        const int32_t e = hq[i];
+        if (e == kEmpty) continue;
+        const int32_t go = P.group_of[e];
+        if (go >= 0 && go < g) set_insert(hp, kWLP, go, &ct[2], &ct[3]);
+      }
+    }
+    __syncwarp();
+    if (ct[3]) {
+      if (lane == 0) {
+        if (!FILL) {
+          P.flag[g] = 1;
+          P.retry2[atomicAdd(P.nretry2, 1)] = g;
+        } else {
+          atomicExch(P.fatal, 1);  // the count pass fitted these sets
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    const int nqk = ct[1], npk = ct[2];
+    if (!FILL) {
+      if (P.group_of && P.pred_tmp) {  // unsorted predecessor lists for the chain
+        int64_t pstart = 0;
+        if (lane == 0) {
+          pstart = (int64_t)atomicAdd((unsigned long long*)P.pred_alloc, (unsigned long long)npk);
+          if (pstart + npk > P.pred_cap) atomicExch(P.pred_ovf, 1);
+          P.pred_start[g] = pstart;
+        }
+        pstart = __shfl_sync(0xffffffffu, pstart, 0);
+        if (pstart + npk <= P.pred_cap) warp_compact(hp, HP, P.pred_tmp + pstart, lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) maxnb = max(maxnb, __shfl_xor_sync(0xffffffffu, maxnb, o));
+      if (lane == 0) {
+        P.nq[g] = nqk;
+        P.nb[g] = nb;
+        P.maxnb[g] = maxnb;
+        P.npred[g] = npk;
+        P.flag[g] = 0;
+      }
+      __syncwarp();
+      continue;
+    }
+    // fill: c, sorted blocks, sorted q, sorted predecessors
+    const int64_t* ex = P.exc + (size_t)g * P.exc_stride;
+    int32_t* out = P.idx_out + P.idx_base + ex[P.o_nf];
+    if (lane < nc) out[lane] = c[lane];
+    warp_rank_sort(buf, nb, P.lists + ex[P.o_nb], lane);
+    __syncwarp();
+    const int nq = warp_compact(hq, HQ, buf, lane);
+    warp_rank_sort(buf, nq, out + nc, lane);
+    __syncwarp();
+    if (P.group_of) {
+      const int np = warp_compact(hp, HP, buf, lane);
+      warp_rank_sort(buf, np, P.preds + ex[P.o_pred], lane);
+    }
+    __syncwarp();
+  }
+}
+
 template <int LQ, int LB, int LP, int NCMAX, bool FILL>
 __global__ void __launch_bounds__(kSymNT) sym_front_kernel(SymFront P) {
   constexpr int HQ = 1 << LQ, HB = 1 << LB, HP = 1 << LP;
@@ -218,12 +369,11 @@ __global__ void __launch_bounds__(kSymNT) sym_front_kernel(SymFront P) {
   int32_t* hp = hq + HQ;           // HP
   int32_t* buf = hp + HP;          // HQ (sort buffer)
   __shared__ int nbk, nqk, npk, ovf, maxnb;
-  const int ngr = *P.ng;
   const bool big_tier = LQ > 10;
-  const int nwork = big_tier ? *P.nretry : ngr;
+  const int nwork = big_tier ? *P.nretry : *P.nretry2;  // groups the tier before could not take
   for (int wi = blockIdx.x; wi < nwork; wi += gridDim.x) {
-    const int g = big_tier ? P.retry[wi] : wi;
-    if (!big_tier && P.flag[g] && FILL) continue;  // the big tier fills it
+    const int g = big_tier ? P.retry[wi] : P.retry2[wi];
+    if (!big_tier && P.flag[g] != 1 && FILL) continue;  // the big tier fills it
     const int64_t c0 = P.goff[g];
     const int nc = (int)(P.goff[g + 1] - c0);
     if (threadIdx.x == 0) { nbk = nqk = npk = ovf = maxnb = 0; }
@@ -282,7 +432,7 @@ __global__ void __launch_bounds__(kSymNT) sym_front_kernel(SymFront P) {
     if (ovf) {
       if (!FILL && threadIdx.x == 0) {
         if (!big_tier) {
-          P.flag[g] = 1;
+          P.flag[g] = 2;
           P.retry[atomicAdd(P.nretry, 1)] = g;
         } else {
           atomicExch(P.fatal, 1);
@@ -314,7 +464,6 @@ __global__ void __launch_bounds__(kSymNT) sym_front_kernel(SymFront P) {
         P.nb[g] = nb;
         P.maxnb[g] = maxnb;
         P.npred[g] = npk;
-        if (!big_tier) P.flag[g] = 0;
       }
       __syncthreads();
       continue;
@@ -980,6 +1129,9 @@ constexpr size_t smem_of(int lq, int lb, int lp, int nc) {
 }
 template <bool FILL>
 cudaError_t fronts_pass(const SymFront& P, cudaStream_t s) {
+  int wper = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, sym_front_warp_kernel<FILL>, 32 * kWarpTierW, 0);
+  sym_front_warp_kernel<FILL><<<sym_grid(std::max(wper, 1)), 32 * kWarpTierW, 0, s>>>(P);
   auto ks = sym_front_kernel<kSLQ, kSLB, kSLP, kSNC, FILL>;
   auto kb = sym_front_kernel<kBLQ, kBLB, kBLP, kBNC, FILL>;
   static bool once = false;
@@ -1000,6 +1152,7 @@ cudaError_t fronts_pass(const SymFront& P, cudaStream_t s) {
 
 cudaError_t sym_fronts_count(const SymFront& P, cudaStream_t s) {
   cudaMemsetAsync(P.nretry, 0, sizeof(int32_t), s);
+  cudaMemsetAsync(P.nretry2, 0, sizeof(int32_t), s);
   return fronts_pass<false>(P, s);
 }
 cudaError_t sym_fronts_fill(const SymFront& P, cudaStream_t s) { return fronts_pass<true>(P, s); }

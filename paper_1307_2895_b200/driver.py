@@ -218,6 +218,48 @@ class _PinnedBlock:
             pass
 
 
+def _pinned_array(lib, shape, dtype) -> np.ndarray:
+    dtype = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    blk = _PinnedBlock.get(lib, max(nbytes, 1))
+    if blk is None:
+        raise MemoryError("page-locked host allocation failed")
+    blk.__array_interface__ = {"shape": tuple(shape), "typestr": dtype.str, "data": (blk.ptr, False),
+                               "version": 3}
+    return np.asarray(blk)
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """Uninitialized host array in a page-locked block of the library's
+    caching pool (returned to the pool when the array is collected).
+    Right-hand sides and matrices built in such arrays move by direct DMA,
+    with no staging copy on the host."""
+    return _pinned_array(L.load(), shape if isinstance(shape, tuple) else (int(shape),), dtype)
+
+
+def pinned_csr(a) -> sp.csr_matrix:
+    """A copy of the CSR matrix ``a`` whose offsets, column indices and values
+    live in page-locked host memory (``pinned_empty``): ``factor_hifde`` of it
+    uploads the three arrays by direct DMA while the level-0 analysis runs,
+    instead of staging them through the library's pinned buffers.  Offsets
+    keep scipy's int32 when they fit."""
+    csr = _as_csr(a)
+    lib = L.load()
+    ipt = np.int32 if csr.indptr.dtype == np.int32 else np.int64
+    ip = _pinned_array(lib, csr.indptr.shape, ipt)
+    ix = _pinned_array(lib, csr.indices.shape, np.int32)
+    va = _pinned_array(lib, csr.data.shape, np.float64)
+    ip[...] = csr.indptr
+    ix[...] = csr.indices
+    va[...] = csr.data
+    m = sp.csr_matrix((va, ix, ip), shape=csr.shape, copy=False)
+    if any(x.ctypes.data != y.ctypes.data for x, y in ((m.data, va), (m.indices, ix), (m.indptr, ip))):
+        raise RuntimeError("scipy copied the page-locked CSR arrays")
+    m.has_sorted_indices = True
+    m.has_canonical_format = True
+    return m
+
+
 def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
             order: str = "auto", exact_max_batches: int = 64, device: Optional[int] = None,
             stream: Optional[int] = None, comm=None, kernel_log: bool = False,

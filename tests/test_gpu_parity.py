@@ -548,6 +548,24 @@ def test_pipelined_host_solve_matches_one_block_solve():
     assert np.linalg.norm(y1 - y2) <= 1e-13 * np.linalg.norm(y2)
 
 
+def test_pinned_csr_factor_bit_identical():
+    """pinned_csr: the CSR's arrays in page-locked pool blocks (direct DMA in
+    factor_hifde, no host staging) give the same factor as scipy's pageable
+    arrays, bit for bit; pinned_empty arrays feed the host solve."""
+    g, a, eps, variant, nrhs = H.baseline_problem(2)
+    ap = H.pinned_csr(a)
+    assert ap.indptr.dtype == a.indptr.dtype and (ap != a).nnz == 0
+    f0 = H.factor_hifde(a, g, eps)
+    f1 = H.factor_hifde(ap, g, eps)
+    assert f0.metrics["skeleton_counts"] == f1.metrics["skeleton_counts"]
+    b = H.pinned_empty((g.ndof, 16))
+    b[...] = np.random.default_rng(9).standard_normal((g.ndof, 16))
+    x0, x1 = f0.apply_inverse(b), f1.apply_inverse(b)
+    assert np.array_equal(x0, x1)
+    f0.close()
+    f1.close()
+
+
 def test_host_output_paths_agree_and_pool_recycles():
     """Large host results land in page-locked blocks of the library's pool
     (hifde_host_alloc): the DMA-straight-in result must equal the staged copy
