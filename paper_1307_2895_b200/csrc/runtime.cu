@@ -2971,10 +2971,13 @@ struct Factorizer {
   // front tiers (the host takes over).
   bool dev_front_count(int ell, int kind, SymFront& P, int64_t& ng_ub) {
     a0_pattern_ready();  // (the values are the numeric kernels' -- arenas())
-    const int w = g.m << ell, k = g.n / w;
+    // kind 0 cells, 1/2 interfaces, 3 the terminal block (every active DOF, key 0)
+    const bool iface = kind == 1 || kind == 2;
+    const int w = g.m << std::min(ell, 30), k = kind == 3 ? 0 : g.n / w;
     int64_t nkeys = 1;
-    for (int ax = 0; ax < g.dim; ++ax) nkeys *= k;
-    if (kind != 0) nkeys *= g.dim;
+    if (kind != 3)
+      for (int ax = 0; ax < g.dim; ++ax) nkeys *= k;
+    if (iface) nkeys *= g.dim;
     ng_ub = nkeys;
     // active list (its count is the previous device level's active_after)
     sy_act.reserve((size_t)N, s);
@@ -2999,7 +3002,7 @@ struct Factorizer {
     A.head = sy_head.p;
     A.goff = sy_goff.p;
     A.ng = &d_scal->ng;
-    A.group_of = kind != 0 ? sy_group_of.p : nullptr;
+    A.group_of = iface ? sy_group_of.p : nullptr;
     HCK(sym_partition(A, symw, s));
     // membership of the live blocks over the active DOFs
     sy_alist.reserve((size_t)std::max<int64_t>(nblk_ub, 1), s);
@@ -3038,7 +3041,7 @@ struct Factorizer {
     P.indptr = d_indptr;
     P.indices = d_indices;
     P.active = d_active;
-    P.group_of = kind != 0 ? sy_group_of.p : nullptr;
+    P.group_of = iface ? sy_group_of.p : nullptr;
     P.nq = sy_nq.p;
     P.nb = sy_nb.p;
     P.maxnb = sy_maxnb.p;
@@ -3050,7 +3053,7 @@ struct Factorizer {
     P.nretry2 = &d_scal->nretry2;
     P.fatal = &d_scal->fatal;
     P.pred_tmp = nullptr;
-    if (kind != 0 && opt.order_mode != HIFDE_ORDER_SNAPSHOT) {  // predecessor lists for the chain
+    if (iface && opt.order_mode != HIFDE_ORDER_SNAPSHOT) {  // predecessor lists for the chain
       const int64_t cap = 64 * (ng_ub + 1);
       sy_pred_tmp.reserve((size_t)cap, s);
       sy_pred_start.reserve((size_t)ng_ub + 1, s);
@@ -3077,10 +3080,10 @@ struct Factorizer {
 
   // ---- elimination level ---------------------------------------------------
   // returns false if the host must take this level (state handed over)
-  bool dev_elimination_level(int ell, double tag, LevelRec& L) {
+  bool dev_elimination_level(int ell, double tag, LevelRec& L, bool top = false) {
     const double t_begin = now_s();
     join_inv();  // its analysis rewrites the big-cell task table
-    L.kind = 0;
+    L.kind = top ? 2 : 0;
     L.lap(nullptr);
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));
@@ -3088,10 +3091,10 @@ struct Factorizer {
     const int kls = F->klog.begin("symbolic_device", tag, 0, 0, 0, s);
     SymFront P;
     int64_t ng_ub = 0;
-    dev_front_count(ell, 0, P, ng_ub);
+    dev_front_count(ell, top ? 3 : 0, P, ng_ub);
     ElimInc* inc = reinterpret_cast<ElimInc*>(sy_inc.p);
     ElimInc* exc = reinterpret_cast<ElimInc*>(sy_exc.p);
-    HCK(sym_elim_sizes(P, 0, (int)ng_ub, inc, exc, d_tot, symw, s));
+    HCK(sym_elim_sizes(P, top ? 1 : 0, (int)ng_ub, inc, exc, d_tot, symw, s));
     dev_sync_totals();
     L.lap("dev-count");
     if (h_scal->fatal) {
@@ -3140,7 +3143,7 @@ struct Factorizer {
     P.preds = nullptr;
     HCK(sym_fronts_fill(P, s));
     ElimFillArgs A;
-    A.is_top = 0;
+    A.is_top = top ? 1 : 0;
     A.idx_base = idx_base;
     A.fac_base = fac_base;
     A.bv_base = bv_base;
@@ -3189,9 +3192,9 @@ struct Factorizer {
     const int64_t nsmall = T.sum[6], nbig = T.sum[7];
     if (nsmall) {
       const int64_t st_small = (int64_t)status.bump((size_t)nsmall, s);
-      pending.push_back({st_small, nsmall, tag, "cell"});
+      pending.push_back({st_small, nsmall, tag, top ? "top block" : "cell"});
       Ar.status = status.p + st_small;
-      const int kl = F->klog.begin("elim_small_kernel", tag, 0, 0, 0, s);
+      const int kl = F->klog.begin(top ? "elim_small_kernel(top)" : "elim_small_kernel", tag, 0, 0, 0, s);
       launch_elim_small(sy_small.p, (int)nsmall, Ar, (size_t)T.smem, T.max_small_nf <= 64 ? 128 : 256, s);
       F->klog.end(kl, s);
       ++g_launches;
@@ -3200,9 +3203,10 @@ struct Factorizer {
       std::vector<ElimTask> big((size_t)nbig);
       HCK(cudaMemcpyAsync(big.data(), sy_big.p, sizeof(ElimTask) * (size_t)nbig, cudaMemcpyDeviceToHost, s));
       HCK(cudaStreamSynchronize(s));
-      launch_big_cells(big, sy_big.p, (size_t)T.smem_big, Ar, tag, false, 0, 0, !sharded());
+      launch_big_cells(big, sy_big.p, (size_t)T.smem_big, Ar, tag, top, 0, 0, !sharded() && !top);
     }
     HCK(cudaEventRecord(L.ev1, s));
+    if (top) F->s_top = nact_ub;
     HCK(cudaGetLastError());
     L.ncontrib = T.sum[4];
     F->max_contrib = std::max(F->max_contrib, L.ncontrib);
@@ -3437,9 +3441,16 @@ struct Factorizer {
     if (!dev_mode) return;
     dev_mode = false;
     join_inv();
+    // the active list compacted on the device (an O(N) host scan of the mask
+    // was ~3 ms at the end of config 3's factorization)
+    sy_act.reserve((size_t)N + 1, s);
+    HCK(sym_active_list(d_active, N, sy_act.p, &d_scal->nact, symw, s));
     HCK(cudaMemcpyAsync(h_scal, d_scal, sizeof(SymScalars), cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
     const int64_t nb = h_scal->nblk;
+    act.resize((size_t)h_scal->nact);
+    if (!act.empty())
+      HCK(cudaMemcpyAsync(act.data(), sy_act.p, sizeof(int32_t) * act.size(), cudaMemcpyDeviceToHost, s));
     blk_dof_off.resize((size_t)nb);
     blk_n.resize((size_t)nb);
     blk_val_off.resize((size_t)nb);
@@ -3455,6 +3466,7 @@ struct Factorizer {
     active.resize((size_t)N);
     HCK(cudaMemcpyAsync(active.data(), d_active, (size_t)N, cudaMemcpyDeviceToHost, s));
     HCK(cudaStreamSynchronize(s));
+    prof.lap("h-tables");
     d_blk_dof_off.n = d_blk_n.n = d_blk_val_off.n = (size_t)nb;
     blk_uploaded = (size_t)nb;
     // index-arena mirror: the DOF lists of the live blocks
@@ -3466,12 +3478,11 @@ struct Factorizer {
     if (lo < (int64_t)nidx)
       pinned_xfer().d2h(h_idx.data() + lo, F->idx.p + lo, (nidx - (size_t)lo) * sizeof(int32_t), s);
     idx_uploaded = nidx;
+    prof.lap("h-idx");
     // active list and membership (active DOFs only: the host looks up
     // membership of active DOFs alone)
-    act.clear();
-    for (int64_t i = 0; i < N; ++i)
-      if (active[(size_t)i]) act.push_back((int32_t)i);
     if (last_dev_level >= 0) F->levels[(size_t)last_dev_level].active_after = (int64_t)act.size();
+    prof.lap("h-act");
     member.reset();
     size_t nadd = 0;
     for (int64_t b = 0; b < nb; ++b)
@@ -3489,6 +3500,7 @@ struct Factorizer {
           if (d[i] >= dlo && d[i] < dhi && active[(size_t)d[i]]) member.add(d[i], (int32_t)b);
       }
     }
+    prof.lap("h-member");
     // the upload cursor of the block table continues from here
   }
 
@@ -3537,8 +3549,14 @@ struct Factorizer {
       }
       for (auto& E : F->klog.v) {  // kernel log: the level's totals to its main launch
         if (E.phase != 0 || E.tag != L.tag) continue;
-        if (E.name == "elim_small_kernel") { E.gbytes = L.gb_cls[0]; E.gflop = L.gf_cls[0]; }
-        if (E.name == "elim_blocked_pipeline") { E.gbytes = L.gb_cls[1]; E.gflop = L.gf_cls[1]; }
+        if (E.name == "elim_small_kernel" || E.name == "elim_small_kernel(top)") {
+          E.gbytes = L.gb_cls[0];
+          E.gflop = L.gf_cls[0];
+        }
+        if (E.name == "elim_blocked_pipeline" || E.name == "elim_blocked_pipeline(top)") {
+          E.gbytes = L.gb_cls[1];
+          E.gflop = L.gf_cls[1];
+        }
         if (E.name == "skel_kernel" || E.name == "skel_ordered_kernel" || E.name == "skel_cluster_kernel") {
           E.gbytes = L.gbytes;
           E.gflop = L.gflop;
@@ -3993,26 +4011,46 @@ struct Factorizer {
         if (ell >= opt.skip_levels) skel(ell + 2.0 / 3.0, 0);
       }
     }
-    dev_to_host();  // the terminal block runs on the host path
-    // terminal block: every DOF still active (src/driver.py:152-157)
-    {
+    prof.lap("levels");
+    // terminal block: every DOF still active (src/driver.py:152-157); on the
+    // device path when the levels ran there (one cell of every active DOF,
+    // no neighbours), else on the host path after the hand-over
+    bool top_dev = false;
+    if (dev_mode) {
       const double tl = now_s();
-      Groups top;
-      top.members = act;
-      F->s_top = (int64_t)top.members.size();
       F->levels.emplace_back();
       LevelRec& L = F->levels.back();
       L.tag = (double)Lv;
-      if (!top.members.empty()) {
-        top.offsets.push_back((int64_t)top.members.size());
-        elimination_level(top, L.tag, L, true);
-        L.gflop = std::pow((double)F->s_top, 3) / 3 * 1e-9;
-        L.gbytes = 16.0 * F->s_top * F->s_top * 1e-9;
+      if (dev_elimination_level(Lv, L.tag, L, true)) {
+        check_status();
+        L.seconds = now_s() - tl;
+        top_dev = true;
+      } else {
+        dev_fallback(L, (double)Lv);
+        F->levels.pop_back();
       }
-      L.kind = 2;
-      record_trace(L, tl);
     }
-    PR.lap(nullptr);
+    if (!top_dev) {
+      dev_to_host();
+      {
+        const double tl = now_s();
+        Groups top;
+        top.members = act;
+        F->s_top = (int64_t)top.members.size();
+        F->levels.emplace_back();
+        LevelRec& L = F->levels.back();
+        L.tag = (double)Lv;
+        if (!top.members.empty()) {
+          top.offsets.push_back((int64_t)top.members.size());
+          elimination_level(top, L.tag, L, true);
+          L.gflop = std::pow((double)F->s_top, 3) / 3 * 1e-9;
+          L.gbytes = 16.0 * F->s_top * F->s_top * 1e-9;
+        }
+        L.kind = 2;
+        record_trace(L, tl);
+      }
+    }
+    PR.lap("top");
     if (real) {  // every record lives on its owner, zeros elsewhere: sum
       try {
         comm_allreduce(comm, F->fac.p, F->fac.n, kF64, kSum, s);
@@ -4023,7 +4061,7 @@ struct Factorizer {
     F->nranks = sharded() ? P : 1;
     F->xfer_bytes = xfer_bytes;
     helper.drain();
-    build_solve_plan(F->levels.back());  // the terminal block
+    if (!top_dev) build_solve_plan(F->levels.back());  // the terminal block
     dev_finalize();
     finish_reductions();
     PR.lap("reductions");

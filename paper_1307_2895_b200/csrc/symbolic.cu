@@ -130,7 +130,7 @@ __global__ void sym_keys_kernel(const int32_t* __restrict__ act, const int64_t* 
     if (i < na) {
       int x[3] = {0, 0, 0};
       dof_coords(act[i], dim, side, x);
-      key = kind == 0 ? interior_key(x, dim, w, k) : interface_key(x, dim, w, k, kind == 2);
+      key = kind == 3 ? 0 : kind == 0 ? interior_key(x, dim, w, k) : interface_key(x, dim, w, k, kind == 2);
     }
     keys[i] = key < 0 ? nkeys : key;  // nkeys: no group (sorts last)
   }
@@ -208,7 +208,7 @@ __global__ void sym_member_fill(const int32_t* __restrict__ alive_list, const in
 // ---------------------------------------------------------------------------
 // Fronts: live blocks touching the group, neighbour set q, predecessors
 // ---------------------------------------------------------------------------
-// Warp tier (kWarpTier below): one warp per group of at most 32 DOFs with
+// Warp tier (kWarpTierW below): one warp per group of at most 64 DOFs with
 // per-warp sets of 32 blocks / 128 neighbours / 64 predecessors; config 3's
 // 130,560 edge groups of level 0.5 (7 DOFs, ~50 neighbours) took one
 // 128-thread CTA each, whose barriers and dependent loads (a chain of ~10
@@ -237,7 +237,7 @@ __device__ __forceinline__ void warp_rank_sort(const int32_t* src, int n, int32_
   }
 }
 
-constexpr int kWLQ = 7, kWLB = 5, kWLP = 6, kWNC = 32, kWarpTierW = 8;
+constexpr int kWLQ = 7, kWLB = 5, kWLP = 6, kWNC = 64, kWarpTierW = 8;
 
 template <bool FILL>
 __global__ void __launch_bounds__(32 * kWarpTierW) sym_front_warp_kernel(SymFront P) {
@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(32 * kWarpTierW) sym_front_warp_kernel(SymFron
     for (int i = lane; i < HQ; i += 32) hq[i] = kEmpty;
     for (int i = lane; i < HP; i += 32) hp[i] = kEmpty;
     if (lane < 4) ct[lane] = 0;
-    if (lane < nc) c[lane] = P.gmem[c0 + lane];
+    for (int i = lane; i < nc; i += 32) c[i] = P.gmem[c0 + i];
     __syncwarp();
-    if (lane < nc) {  // live blocks touching the group
-      const int32_t d = c[lane];
+    for (int i = lane; i < nc; i += 32) {  // live blocks touching the group
+      const int32_t d = c[i];
       for (int32_t t = P.mptr[d]; t < P.mptr[d + 1]; ++t) set_insert(hb, kWLB, P.mblk[t], &ct[0], &ct[3]);
     }
     __syncwarp();
@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(32 * kWarpTierW) sym_front_warp_kernel(SymFron
           if (P.active[e] && bsearch_sorted(c, nc, e) < 0) set_insert(hq, kWLQ, e, &ct[1], &ct[3]);
         }
       }
-      if (lane < nc) {
-        const int32_t d = c[lane];
+      for (int i = lane; i < nc; i += 32) {
+        const int32_t d = c[i];
         for (int64_t t = P.indptr[d]; t < P.indptr[d + 1]; ++t) {
           const int32_t e = P.indices[t];
           if (P.active[e] && bsearch_sorted(c, nc, e) < 0) set_insert(hq, kWLQ, e, &ct[1], &ct[3]);
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(32 * kWarpTierW) sym_front_warp_kernel(SymFron
     // fill: c, sorted blocks, sorted q, sorted predecessors
     const int64_t* ex = P.exc + (size_t)g * P.exc_stride;
     int32_t* out = P.idx_out + P.idx_base + ex[P.o_nf];
-    if (lane < nc) out[lane] = c[lane];
+    for (int i = lane; i < nc; i += 32) out[i] = c[i];
     warp_rank_sort(buf, nb, P.lists + ex[P.o_nb], lane);
     __syncwarp();
     const int nq = warp_compact(hq, HQ, buf, lane);
@@ -861,41 +861,33 @@ __global__ void __launch_bounds__(256) skel_relax_coop(const int64_t* __restrict
                                                        const int32_t* __restrict__ npred,
                                                        const int32_t* __restrict__ preds,
                                                        const int32_t* __restrict__ ng, int32_t* b0, int32_t* b1,
-                                                       int32_t* changed, int iters) {
+                                                       int32_t* changed, int iters, LevelTotals* tot) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const int n = *ng;
+  int m = 0;  // max depth this thread wrote in the last sweep that ran
   for (int it = 0; it < iters; ++it) {
     if (it > 0 && __ldcg(changed + it - 1) == 0) break;  // uniform: read after the barrier
     const int32_t* bin = (it % 2 == 0) ? b0 : b1;
     int32_t* bout = (it % 2 == 0) ? b1 : b0;
     int ch = 0;
+    m = 0;
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
       int b = 0;
       const int64_t p0 = pred_start[t];
       for (int64_t p = p0; p < p0 + npred[t]; ++p) b = max(b, __ldcg(bin + preds[p]) + 1);
       __stcg(bout + t, b);
       ch |= b != __ldcg(bin + t);
+      m = max(m, b);
     }
     if (__syncthreads_or(ch) && threadIdx.x == 0) atomicExch(changed + it, 1);
     grid.sync();
   }
-}
-
-__global__ void skel_chain_kernel(const int32_t* __restrict__ b0, const int32_t* __restrict__ b1,
-                                  const int32_t* __restrict__ changed, int iters, const int32_t* __restrict__ ng,
-                                  LevelTotals* tot) {
-  // the last sweep that ran wrote buffer (it + 1) % 2 ... pick the final one
-  int last = iters - 1;
-  for (int i = 1; i < iters; ++i)
-    if (changed[i - 1] == 0) { last = i - 1; break; }
-  const int32_t* b = (last % 2 == 0) ? b1 : b0;
-  const int n = *ng;
-  int m = 0;
-  for (int t = threadIdx.x; t < n; t += blockDim.x) m = max(m, b[t]);
+  // the longest chain (was a one-block reduction over every group's depth
+  // after the sweeps: 0.23 ms at config 3 level 0.5)
   typedef cub::BlockReduce<int, 256> R;
   __shared__ typename R::TempStorage rt;
   m = R(rt).Reduce(m, cub::Max());
-  if (threadIdx.x == 0) tot->max_chain = m;
+  if (threadIdx.x == 0 && m > 0) amax64(&tot->max_chain, m);
 }
 
 // the relaxation's final depths (the buffer the last sweep that ran wrote)
@@ -1232,14 +1224,14 @@ cudaError_t sym_skel_chain(const int64_t* pred_start, const int32_t* npred, cons
                            cudaStream_t s) {
   cudaMemsetAsync(b0, 0, sizeof(int32_t) * (size_t)ng_ub, s);
   cudaMemsetAsync(changed, 0, sizeof(int32_t) * (size_t)iters, s);
+  cudaMemsetAsync(&tot->max_chain, 0, sizeof(int64_t), s);
   static int per_sm = 0;
   if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skel_relax_coop, 256, 0);
   const int grid = std::max(1, std::min(sym_grid(std::max(per_sm, 1)), (ng_ub + 255) / 256));
   void* args[] = {(void*)&pred_start, (void*)&npred, (void*)&preds, (void*)&ng, (void*)&b0, (void*)&b1,
-                  (void*)&changed, (void*)&iters};
+                  (void*)&changed, (void*)&iters, (void*)&tot};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)skel_relax_coop, dim3((unsigned)grid), dim3(256), args, 0, s);
   if (e != cudaSuccess) return e;
-  skel_chain_kernel<<<1, 256, 0, s>>>(b0, b1, changed, iters, ng, tot);
   return cudaGetLastError();
 }
 
