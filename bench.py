@@ -358,6 +358,7 @@ class Runner:
             fe.close()
             if i > 0:  # first call warms the host caches of the public path
                 ts.append(t)
+        self.e2e_steps_ms = [round(t * 1e3, 2) for t in ts]
         return float(np.mean(ts))
 
 
@@ -476,7 +477,8 @@ def run_gpu(args, world, rank, local):
                 "d2h_bytes_per_step": int(R.b_host.nbytes),
                 "note": "public API (factor_hifde + apply_inverse) with the host CSR and RHS in page-locked "
                         "memory (pinned_csr / pin_memory, outside the timed region), "
-                        f"mean of {max(1, min(args.steps, 5))} steps after one warm-up"},
+                        f"mean of {max(1, min(args.steps, 5))} steps after one warm-up",
+                "steps_ms": R.e2e_steps_ms},
         "gpu_launches": int(launches // max(args.steps, 1)),
         "gpu_launches_note": "kernel launches of this library per step (factor + solve)",
         "clocks": clk.summary(),

@@ -892,6 +892,7 @@ struct Factorizer {
   uint64_t a0_job = 0, a0_pat_job = 0;
   cudaError_t a0_err = cudaSuccess;
   cudaStream_t a0_s = nullptr;
+  cudaEvent_t ev_a0 = nullptr;  // the values' copy is done (device-side wait)
   void a0_pattern_ready() {
     if (a0_pat_job) {
       helper.wait(a0_pat_job);
@@ -900,9 +901,10 @@ struct Factorizer {
   }
   void a0_ready() {
     a0_pattern_ready();
-    if (a0_job) {
+    if (a0_job) {  // the copy is issued (and, from pageable memory, done): the stream waits for it
       helper.wait(a0_job);
       a0_job = 0;
+      if (a0_err == cudaSuccess && ev_a0) HCK(cudaStreamWaitEvent(s, ev_a0, 0));
     }
     if (a0_err != cudaSuccess) {
       const cudaError_t e = a0_err;
@@ -930,6 +932,7 @@ struct Factorizer {
     if (a0_s) {
       cudaStreamSynchronize(a0_s);
       cudaStreamDestroy(a0_s);
+      if (ev_a0) cudaEventDestroy(ev_a0);
     }
     if (sym_s) {
       cudaStreamSynchronize(sym_s);
@@ -3779,7 +3782,9 @@ struct Factorizer {
         HCK(cudaStreamWaitEvent(a0_s, e0, 0));
         HCK(cudaEventDestroy(e0));
       }
+      HCK(cudaEventCreateWithFlags(&ev_a0, cudaEventDisableTiming));
       const cudaStream_t vs = a0_s;
+      const cudaEvent_t ev_v = ev_a0;
       a0_pat_job = helper.post([=]() {
         cudaError_t e = cudaSetDevice(dev);
         if (e == cudaSuccess && big) {
@@ -3807,7 +3812,10 @@ struct Factorizer {
         } else {
           if (e == cudaSuccess) e = cudaMemcpyAsync(d_a0, va, nnz * sizeof(double), cudaMemcpyHostToDevice, vs);
         }
-        if (e == cudaSuccess) e = cudaStreamSynchronize(vs);
+        // page-locked values: only issued here, the numeric launches' stream
+        // waits for ev_a0 on the device (the host runs on into the next
+        // level's analysis meanwhile)
+        if (e == cudaSuccess) e = cudaEventRecord(ev_v, vs);
         if (e != cudaSuccess) a0_err = e;
       });
     }
