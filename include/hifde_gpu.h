@@ -107,8 +107,12 @@ typedef struct hifde_info {
   int64_t fac_len;      /* doubles in the factor arena (hifde_copy_arenas)  */
   int64_t idx_len;      /* int32 entries in the index arena                 */
   int32_t nranks;       /* ranks the factorization was sharded over (1)     */
-  int32_t pad;
+  int32_t factor_whole; /* 1: the factor arena holds every record; 0: real
+                           ranks before the first operation that sums them
+                           (apply, export, power): each rank holds its own */
   int64_t xfer_bytes;   /* block bytes this rank exchanged with its peers   */
+  int64_t solve_xfer_bytes; /* vector bytes the partitioned solves of this
+                           rank exchanged; 0 unsharded         */
 } hifde_info_t;
 
 /*

@@ -51,8 +51,9 @@ class Info(C.Structure):
         ("fac_len", C.c_int64),
         ("idx_len", C.c_int64),
         ("nranks", C.c_int32),
-        ("pad", C.c_int32),
+        ("factor_whole", C.c_int32),
         ("xfer_bytes", C.c_int64),
+        ("solve_xfer_bytes", C.c_int64),
     ]
 
 

@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -100,6 +101,33 @@ __global__ void seg_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, 
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) b[j] = a[j];
 }
 
+// Rows of an N x nrhs row-major block (the solve vectors): gather the listed
+// rows into a packed buffer, scatter a packed buffer into the listed rows, or
+// zero every row another rank holds.  One thread per double.
+__global__ void rows_gather_kernel(const double* __restrict__ src, const int32_t* __restrict__ rows, int64_t nrows,
+                                   int nrhs, double* __restrict__ dst) {
+  const int64_t tot = nrows * nrhs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nrhs;
+    dst[i] = src[(int64_t)rows[r] * nrhs + (i - r * nrhs)];
+  }
+}
+__global__ void rows_scatter_kernel(const double* __restrict__ src, const int32_t* __restrict__ rows, int64_t nrows,
+                                    int nrhs, double* __restrict__ dst) {
+  const int64_t tot = nrows * nrhs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nrhs;
+    dst[(int64_t)rows[r] * nrhs + (i - r * nrhs)] = src[i];
+  }
+}
+__global__ void rows_zero_unheld_kernel(double* __restrict__ v, const uint8_t* __restrict__ holder, int me, int64_t n,
+                                        int nrhs) {
+  const int64_t tot = n * nrhs;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x)
+    if (holder[i / nrhs] != me) v[i] = 0.0;
+}
+int rows_grid(int64_t tot) { return (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 16)); }
+
 }  // namespace
 
 namespace {
@@ -174,6 +202,20 @@ void launch_seg_copy_i32(const int32_t* src, int32_t* dst, const int64_t* src_of
                          const int64_t* len, int nseg, cudaStream_t s) {
   if (nseg <= 0) return;
   seg_copy_kernel<int32_t><<<nseg, 128, 0, s>>>(src, dst, src_off, dst_off, len);
+}
+
+void launch_rows_gather(const double* src, const int32_t* rows, int64_t nrows, int nrhs, double* dst, cudaStream_t s) {
+  if (nrows <= 0) return;
+  rows_gather_kernel<<<rows_grid(nrows * nrhs), 256, 0, s>>>(src, rows, nrows, nrhs, dst);
+}
+void launch_rows_scatter(const double* src, const int32_t* rows, int64_t nrows, int nrhs, double* dst,
+                         cudaStream_t s) {
+  if (nrows <= 0) return;
+  rows_scatter_kernel<<<rows_grid(nrows * nrhs), 256, 0, s>>>(src, rows, nrows, nrhs, dst);
+}
+void launch_rows_zero_unheld(double* v, const uint8_t* holder, int me, int64_t n, int nrhs, cudaStream_t s) {
+  if (n <= 0) return;
+  rows_zero_unheld_kernel<<<rows_grid(n * nrhs), 256, 0, s>>>(v, holder, me, n, nrhs);
 }
 
 }  // namespace hifde

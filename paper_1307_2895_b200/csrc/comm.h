@@ -55,4 +55,12 @@ void launch_seg_copy(const double* src, double* dst, const int64_t* src_off, con
 void launch_seg_copy_i32(const int32_t* src, int32_t* dst, const int64_t* src_off, const int64_t* dst_off,
                          const int64_t* len, int nseg, cudaStream_t s);
 
+// Rows of an N x nrhs row-major block (partitioned solve exchanges):
+// dst[i, :] = src[rows[i], :]  /  dst[rows[i], :] = src[i, :]  /  v[d, :] = 0
+// wherever holder[d] != me.
+void launch_rows_gather(const double* src, const int32_t* rows, int64_t nrows, int nrhs, double* dst, cudaStream_t s);
+void launch_rows_scatter(const double* src, const int32_t* rows, int64_t nrows, int nrhs, double* dst,
+                         cudaStream_t s);
+void launch_rows_zero_unheld(double* v, const uint8_t* holder, int me, int64_t n, int nrhs, cudaStream_t s);
+
 }  // namespace hifde

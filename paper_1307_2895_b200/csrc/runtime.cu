@@ -290,6 +290,22 @@ struct LevelRec {
   double gb_cls[2] = {0, 0}, gf_cls[2] = {0, 0};
   // solve sweep: factor doubles and touched vector rows of the level's records
   double solve_fac = 0, solve_rows = 0;
+  // sharded factorization: owner rank of each record of `recs`
+  std::vector<uint8_t> rec_own;
+  // partitioned solve: the level's records and reduction
+  // targets of each rank (real ranks: only this process's entry is filled),
+  // and the row exchanges before the forward records [0], before the forward
+  // reduction (contribution rows) [1] and before the backward records [2]
+  std::vector<LevelRec> rank_view;
+  struct XPair {
+    int src, dst;
+    int64_t off, cnt;  // rows [off, off + cnt) of the step's row list
+  };
+  struct XStep {
+    std::vector<XPair> pairs;
+    int32_t* d_rows = nullptr;
+  };
+  XStep xs[3];
 };
 
 // Kernel log (options.kernel_log): CUDA events around the main launches of
@@ -376,6 +392,20 @@ struct hifde_factor {
   mutable std::vector<int32_t> band_pmax, band_smin;
   std::vector<void*> dev_allocs;  // device-symbolic levels' solve / export tables
   mutable std::mutex klog_m;
+  // Partitioned solve of a sharded factorization: every rank
+  // runs only its own records; vector rows and contribution rows cross ranks
+  // as the per-level plans say (LevelRec::xs).  Real ranks hold only their
+  // records' factor values until an operation that needs the whole factor
+  // (apply, export, power iteration) sums the arenas once (ensure_whole).
+  const hifde_comm* comm = nullptr;  // the factorization's communicator (must outlive the solves)
+  bool part = false;                 // partitioned solve plans built
+  bool emu = false;                  // virtual ranks in this process
+  int me = 0;
+  uint8_t* d_holder = nullptr;       // rank holding each solved row after the backward sweep
+  hifde::LevelRec::XStep gather;     // emulated: rows of ranks 1.. into rank 0's vector
+  mutable bool whole = true;         // factor arena holds every record
+  mutable std::mutex whole_m;
+  mutable std::atomic<int64_t> solve_xfer_bytes{0};  // vector bytes this rank exchanged in solves
   ~hifde_factor() {
     // stream-ordered frees: no device-wide synchronization on release
     cudaSetDevice(device);
@@ -1598,6 +1628,7 @@ struct Factorizer {
     own_.assign((size_t)nt, 0);
     if (sharded())
       for (int64_t t = 0; t < nt; ++t) own_[(size_t)t] = owner_of(gr.begin(t));
+    if (sharded()) L.rec_own = own_;
 #pragma omp parallel for num_threads(nthr) schedule(dynamic, 64)
     for (int64_t t = 0; t < nt; ++t) {
       ElimTask& T = tasks[(size_t)t];
@@ -2476,6 +2507,7 @@ struct Factorizer {
         R.inv = 1;
         R.pad = 0;
         L.recs.push_back(R);
+        if (sharded()) L.rec_own.push_back(own_[(size_t)t]);
         L.max_nc = std::max(L.max_nc, r);
         L.max_nq = std::max(L.max_nq, kk);
         F->m_f_bytes += 8 * ((int64_t)kk * r + (int64_t)r * r + r + (int64_t)r * kk);
@@ -2837,6 +2869,181 @@ struct Factorizer {
     };
     upload(F, L.fwd_ph);
     upload(B, L.bwd_ph);
+  }
+
+  // Partitioned solve plans of a sharded factorization (the
+  // solve "same partition"): each rank runs the records it owns, and a row
+  // of the solve vector moves only when a rank is about to read it while
+  // its current value lives elsewhere.  The plan replays both sweeps over
+  // the (replicated) record structure with a bitmask of the ranks holding
+  // each row's current value:
+  //  - forward elimination: a record reads v_c on its owner; the reduction
+  //    of a neighbour row q runs on the rank that next reads q in the forward
+  //    sweep (its contribution rows from other ranks' records travel there,
+  //    and the reduction sums them in record order -- the single-GPU sums);
+  //  - forward skeleton / backward: a record reads (and writes) its rows on
+  //    its owner; backward eliminations read their neighbour rows too.
+  // After the backward sweep each row's holder supplies it to the result.
+  void build_shard_solve() {
+    const size_t nl = F->levels.size();
+    if (P > 32) throw Fail{HIFDE_BADARG, "partitioned solve: more than 32 ranks"};
+    std::vector<const Reduction*> red(nl, nullptr);
+    for (auto& pr : reductions) red[pr.first] = &pr.second;
+    for (const LevelRec& L : F->levels)
+      if (L.rec_own.size() != L.recs.size()) throw Fail{HIFDE_INTERNAL, "partitioned solve: record owners missing"};
+    // the index arena as the kernels left it (sk / rd lists of every group)
+    std::vector<int32_t> hidx(F->idx.n);
+    HCK(cudaMemcpyAsync(hidx.data(), F->idx.p, F->idx.n * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));
+    const int32_t* hx = hidx.data();
+    auto rows_of = [&](const LevelRec& L, const SolveRec& R, bool with_q) {
+      // kind 1: sk[k] then rd[r] (all read); else the cell, then its neighbours
+      const int64_t n = L.kind == 1 ? (int64_t)R.nc + R.nq : (with_q ? (int64_t)R.nc + R.nq : (int64_t)R.nc);
+      return std::make_pair(hx + R.idx_off, n);
+    };
+    // next forward reader of each row -> the rank reducing it at each level
+    std::vector<uint8_t> nxt((size_t)N, 0);
+    std::vector<std::vector<uint8_t>> ered(nl);
+    for (size_t li = nl; li-- > 0;) {
+      const LevelRec& L = F->levels[li];
+      if (red[li]) {
+        ered[li].resize(red[li]->targets.size());
+        for (size_t i = 0; i < red[li]->targets.size(); ++i) ered[li][i] = nxt[(size_t)red[li]->targets[i]];
+      }
+      for (size_t t = 0; t < L.recs.size(); ++t) {
+        const auto rr = rows_of(L, L.recs[t], false);
+        for (int64_t j = 0; j < rr.second; ++j) nxt[(size_t)rr.first[j]] = L.rec_own[t];
+      }
+    }
+    const uint32_t all = P == 32 ? 0xFFFFFFFFu : ((1u << P) - 1);
+    std::vector<uint32_t> valid((size_t)N, all);
+    // ranks receiving a row in the current exchange: not a source before it lands
+    std::vector<uint32_t> adding((size_t)N, 0);
+    std::vector<int32_t> touched;
+    std::vector<std::vector<int32_t>> pend((size_t)P * P);
+    auto need = [&](int o, int32_t d) {
+      const uint32_t m = valid[(size_t)d];
+      uint32_t& a = adding[(size_t)d];
+      if ((m | a) >> o & 1u) return;
+      pend[(size_t)__builtin_ctz(m) * P + o].push_back(d);
+      if (a == 0) touched.push_back(d);
+      a |= 1u << o;
+    };
+    auto flush = [&](LevelRec::XStep& X) {
+      for (int32_t d : touched) {
+        valid[(size_t)d] |= adding[(size_t)d];
+        adding[(size_t)d] = 0;
+      }
+      touched.clear();
+      std::vector<int32_t> rows;
+      for (int a = 0; a < P; ++a)
+        for (int b = 0; b < P; ++b) {
+          std::vector<int32_t>& v = pend[(size_t)a * P + b];
+          if (v.empty()) continue;
+          X.pairs.push_back(LevelRec::XPair{a, b, (int64_t)rows.size(), (int64_t)v.size()});
+          rows.insert(rows.end(), v.begin(), v.end());
+          v.clear();
+        }
+      meta.add(&X.d_rows, rows);
+    };
+    for (size_t li = 0; li < nl; ++li) {  // forward sweep
+      LevelRec& L = F->levels[li];
+      for (size_t t = 0; t < L.recs.size(); ++t) {
+        const auto rr = rows_of(L, L.recs[t], false);
+        for (int64_t j = 0; j < rr.second; ++j) need(L.rec_own[t], rr.first[j]);
+      }
+      const Reduction* R = red[li];
+      if (R)
+        for (size_t i = 0; i < R->targets.size(); ++i) need(ered[li][i], R->targets[i]);
+      flush(L.xs[0]);
+      if (R) {  // contribution rows to the reducing rank
+        std::vector<uint8_t> cown((size_t)L.ncontrib, 0);
+        for (size_t t = 0; t < L.recs.size(); ++t)
+          std::fill_n(cown.begin() + L.recs[t].contrib_off, L.recs[t].nq, L.rec_own[t]);
+        for (size_t i = 0; i < R->targets.size(); ++i)
+          for (int64_t e = R->ptr[i]; e < R->ptr[i + 1]; ++e) {
+            const int64_t row = R->ent[(size_t)e];
+            if (cown[(size_t)row] != ered[li][i]) pend[(size_t)cown[(size_t)row] * P + ered[li][i]].push_back((int32_t)row);
+          }
+      }
+      flush(L.xs[1]);
+      for (size_t t = 0; t < L.recs.size(); ++t) {
+        const auto rr = rows_of(L, L.recs[t], false);
+        for (int64_t j = 0; j < rr.second; ++j) valid[(size_t)rr.first[j]] = 1u << L.rec_own[t];
+      }
+      if (R)
+        for (size_t i = 0; i < R->targets.size(); ++i) valid[(size_t)R->targets[i]] = 1u << ered[li][i];
+    }
+    for (size_t li = nl; li-- > 0;) {  // backward sweep
+      LevelRec& L = F->levels[li];
+      for (size_t t = 0; t < L.recs.size(); ++t) {
+        const auto rr = rows_of(L, L.recs[t], true);
+        for (int64_t j = 0; j < rr.second; ++j) need(L.rec_own[t], rr.first[j]);
+      }
+      flush(L.xs[2]);
+      for (size_t t = 0; t < L.recs.size(); ++t) {
+        const auto rr = rows_of(L, L.recs[t], false);
+        for (int64_t j = 0; j < rr.second; ++j) valid[(size_t)rr.first[j]] = 1u << L.rec_own[t];
+      }
+    }
+    std::vector<uint8_t> holder((size_t)N);
+    for (int64_t d = 0; d < N; ++d) {
+      holder[(size_t)d] = (uint8_t)__builtin_ctz(valid[(size_t)d]);
+      if (emu && holder[(size_t)d] != 0) pend[(size_t)holder[(size_t)d] * P].push_back((int32_t)d);
+    }
+    meta.add(&F->d_holder, holder);
+    flush(F->gather);
+    // each rank's records and reduction targets
+    for (size_t li = 0; li < nl; ++li) {
+      LevelRec& L = F->levels[li];
+      L.rank_view.resize((size_t)P);
+      for (int r = rank_lo(); r < rank_hi(); ++r) {
+        LevelRec& V = L.rank_view[(size_t)r];
+        V.kind = L.kind;
+        V.tag = L.tag;
+        V.ncontrib = L.ncontrib;
+        for (size_t t = 0; t < L.recs.size(); ++t)
+          if (L.rec_own[t] == r) V.recs.push_back(L.recs[t]);
+        build_solve_plan(V);
+        // the whole level's kernel choice (the same arithmetic as its single sweep)
+        V.max_nc = L.max_nc;
+        V.max_nq = L.max_nq;
+        V.recs.clear();
+        V.recs.shrink_to_fit();
+        if (const Reduction* R = red[li]) {
+          std::vector<int32_t> tg;
+          std::vector<int64_t> ptr{0}, ent;
+          for (size_t i = 0; i < R->targets.size(); ++i) {
+            if (ered[li][i] != r) continue;
+            tg.push_back(R->targets[i]);
+            ent.insert(ent.end(), R->ent.begin() + R->ptr[i], R->ent.begin() + R->ptr[i + 1]);
+            ptr.push_back((int64_t)ent.size());
+          }
+          V.ntargets = (int)tg.size();
+          meta.add(&V.d_targets, tg);
+          meta.add(&V.d_ptr, ptr);
+          meta.add(&V.d_ent, ent);
+        }
+      }
+    }
+    if (trace_on())
+      for (size_t li = 0; li < nl; ++li) {
+        const LevelRec& L = F->levels[li];
+        std::string o;
+        for (int k = 0; k < 3; ++k) {
+          o += " |";
+          for (const auto& p : L.xs[k].pairs) o += " " + std::to_string(p.src) + ">" + std::to_string(p.dst) + ":" + std::to_string(p.cnt);
+        }
+        o += " | views";
+        for (const LevelRec& V : L.rank_view)
+          o += " " + std::to_string(V.nsmall) + "/" + std::to_string(V.nall) + "/" + std::to_string(V.fwd_ph.size()) + "/" + std::to_string(V.ntargets);
+        HTRACE("part level %g kind %d recs %zu:%s", L.tag, L.kind, L.recs.size(), o.c_str());
+      }
+    F->part = true;
+    F->emu = emu;
+    F->me = me;
+    F->comm = comm;
+    F->whole = !real;
   }
 
   // =========================================================================
@@ -4059,18 +4266,15 @@ struct Factorizer {
       }
     }
     PR.lap("top");
-    if (real) {  // every record lives on its owner, zeros elsewhere: sum
-      try {
-        comm_allreduce(comm, F->fac.p, F->fac.n, kF64, kSum, s);
-      } catch (const std::exception& e) {
-        throw Fail{HIFDE_CUDA, e.what()};
-      }
-    }
+    // real ranks: every record lives on its owner (zeros elsewhere) -- the
+    // partitioned solve needs nothing else; ensure_whole() sums the arenas
+    // the first time an operation needs every record
     F->nranks = sharded() ? P : 1;
     F->xfer_bytes = xfer_bytes;
     helper.drain();
     if (!top_dev) build_solve_plan(F->levels.back());  // the terminal block
     dev_finalize();
+    if (sharded()) build_shard_solve();
     finish_reductions();
     PR.lap("reductions");
     // solve metadata to the device: small records one CTA each, large ones as
@@ -4156,6 +4360,19 @@ bool level0_bandable(const hifde_factor_t* F) {
          L.max_nc <= 96 && L.max_nq <= 192;
 }
 
+// Sums the real ranks' factor arenas once (each holds its own records, zeros
+// elsewhere) before an operation that reads every record.
+void ensure_whole(const hifde_factor_t* F, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(F->whole_m);
+  if (F->whole) return;
+  try {
+    comm_allreduce(F->comm, F->fac.p, F->fac.n, kF64, kSum, s);
+  } catch (const std::exception& e) {
+    throw Fail{HIFDE_CUDA, e.what()};
+  }
+  F->whole = true;
+}
+
 void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s, const SweepBands* bands = nullptr) {
   double* contrib = nullptr;
   HCK(cudaMallocAsync((void**)&contrib, std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
@@ -4174,129 +4391,251 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s, c
   for (const auto& L : F->levels) {
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
+    for (const auto& V : L.rank_view) ws_plan(V, ws_of(V), sm, pr);
   }
   double* scratch = nullptr;
   HCK(cudaMallocAsync((void**)&scratch, std::max<size_t>(scratch_need * sizeof(double), 8), s));
   // fine elimination levels: the single-load-phase kernels
-  static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
   constexpr int small_max_rhs = 64, small_max_n = 96;
   constexpr size_t small_max_smem = kSmemCapBytes;  // (200 KB kept config 3 level 3, 208 KB, on the streaming kernels: 2x slower)
   auto small_path = [&](const LevelRec& L) {
-    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+    return L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
            L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   auto small_skel = [&](const LevelRec& L) {
-    return !no_small && L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+    return L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
            L.max_nq <= 2 * small_max_n && solve_skel_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   const int32_t* idx = F->idx.p;
   const double* fac = F->fac.p;
-  auto phases = [&](const std::vector<LevelRec::Phase>& ph) {
+  auto phases = [&](const std::vector<LevelRec::Phase>& ph, double* vv, double* cc) {
     for (const auto& P : ph) {
-      launch_solve_tiles(P.d_ops, P.d_work, P.nwork, idx, fac, v, nrhs, tscr, contrib, s);
+      launch_solve_tiles(P.d_ops, P.d_work, P.nwork, idx, fac, vv, nrhs, tscr, cc, s);
       ++g_launches;
     }
   };
-  const size_t nl = F->levels.size();
-  // kernel log: one entry per level and direction; algorithmic bytes = the
-  // level's factor entries + one read and one write of every touched row
-  auto kbegin = [&](const LevelRec& L, bool fwd) {
-    if (!F->klog.on || (L.nall == 0 && L.recs.empty())) return -1;
-    const char* nm = L.kind == 1 ? (fwd ? "solve_skel_fwd" : "solve_skel_bwd")
-                                 : (fwd ? "solve_elim_fwd" : "solve_elim_bwd");
-    return F->klog.begin(nm, L.tag, 1, 8.0 * (L.solve_fac + 2.0 * L.solve_rows * nrhs) * 1e-9,
-                         2.0 * L.solve_fac * nrhs * 1e-9, s);
-  };
-  for (size_t li = 0; li < nl; ++li) {
-    const LevelRec& L = F->levels[li];
+  // Forward records of a level (or of one rank's share of it): v_c = P v_c
+  // and the contribution rows W^T v_c (elimination), or the skeleton record
+  // in place.  `band0`: level 0 of the banded host solve.
+  auto fwd_records = [&](const LevelRec& L, double* vv, double* cc, bool band0) {
     const int nr = L.nsmall;
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
-    const int kl = kbegin(L, true);
-    struct KEnd {
-      const hifde_factor_t* F; int kl; cudaStream_t s;
-      ~KEnd() { F->klog.end(kl, s); }
-    } kend{F, kl, s};
     if (L.kind == 1) {
       if (nr && small_skel(L)) {
-        launch_solve_skel_small(L.d_recs, nr, idx, fac, v, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 1,
+        launch_solve_skel_small(L.d_recs, nr, idx, fac, vv, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 1,
                                 s);
         ++g_launches;
       } else if (nr) {
-        launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 1, scratch, pr, sm, s);
+        launch_solve_skel(L.d_recs, nr, idx, fac, vv, nrhs, 1, scratch, pr, sm, s);
         ++g_launches;
       }
-      phases(L.fwd_ph);
-    } else {
-      if (li == 0 && bands && !(nr && small_path(L)))  // (not banded after all: wait for the whole upload)
-        for (cudaEvent_t e : bands->fwd_wait) HCK(cudaStreamWaitEvent(s, e, 0));
-      if (li == 0 && bands && nr && small_path(L)) {  // upload bands as they land
-        for (size_t b = 0; b < bands->fwd.size(); ++b) {
-          HCK(cudaStreamWaitEvent(s, bands->fwd_wait[b], 0));
-          const int lo = bands->fwd[b].first, hi = bands->fwd[b].second;
-          if (hi > lo) {
-            launch_solve_elim_small(L.d_recs + lo, hi - lo, idx, fac, (int64_t)F->fac.cap, v, nrhs, contrib, L.max_nc,
-                                    L.max_nq, solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
-            ++g_launches;
-          }
-        }
-      } else if (nr && small_path(L)) {
-        launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, v, nrhs, contrib, L.max_nc, L.max_nq,
-                                solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
-        ++g_launches;
-      } else if (nr) {
-        launch_solve_elim_fwd(L.d_recs, nr, idx, fac, v, nrhs, contrib, scratch, pr, sm, s);
-        ++g_launches;
-      }
-      phases(L.fwd_ph);
-      if (L.kind == 0 && L.ntargets) {
-        launch_solve_reduce(L.d_targets, L.d_ptr, L.d_ent, L.ntargets, contrib, v, nrhs, s);
-        ++g_launches;
-      }
+      phases(L.fwd_ph, vv, cc);
+      return;
     }
-  }
-  for (size_t li = nl; li-- > 0;) {
-    const LevelRec& L = F->levels[li];
+    if (band0 && !(nr && small_path(L)))  // (not banded after all: wait for the whole upload)
+      for (cudaEvent_t e : bands->fwd_wait) HCK(cudaStreamWaitEvent(s, e, 0));
+    if (band0 && nr && small_path(L)) {  // upload bands as they land
+      for (size_t b = 0; b < bands->fwd.size(); ++b) {
+        HCK(cudaStreamWaitEvent(s, bands->fwd_wait[b], 0));
+        const int lo = bands->fwd[b].first, hi = bands->fwd[b].second;
+        if (hi > lo) {
+          launch_solve_elim_small(L.d_recs + lo, hi - lo, idx, fac, (int64_t)F->fac.cap, vv, nrhs, cc, L.max_nc,
+                                  L.max_nq, solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
+          ++g_launches;
+        }
+      }
+    } else if (nr && small_path(L)) {
+      launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, vv, nrhs, cc, L.max_nc, L.max_nq,
+                              solve_small_smem(L.max_nc, L.max_nq, nrhs), 1, s);
+      ++g_launches;
+    } else if (nr) {
+      launch_solve_elim_fwd(L.d_recs, nr, idx, fac, vv, nrhs, cc, scratch, pr, sm, s);
+      ++g_launches;
+    }
+    phases(L.fwd_ph, vv, cc);
+  };
+  // the elimination's neighbour rows: v_q -= the contribution rows, summed in record order
+  auto fwd_reduce = [&](const LevelRec& L, double* vv, double* cc) {
+    if (L.kind == 0 && L.ntargets) {
+      launch_solve_reduce(L.d_targets, L.d_ptr, L.d_ent, L.ntargets, cc, vv, nrhs, s);
+      ++g_launches;
+    }
+  };
+  auto bwd_records = [&](const LevelRec& L, double* vv, bool band0) {
     const int nr = L.nsmall;
     size_t sm; int64_t pr;
     ws_plan(L, ws_of(L), sm, pr);
-    const int kl = kbegin(L, false);
-    struct KEnd {
-      const hifde_factor_t* F; int kl; cudaStream_t s;
-      ~KEnd() { F->klog.end(kl, s); }
-    } kend{F, kl, s};
     if (L.kind == 1) {
       if (nr && small_skel(L)) {
-        launch_solve_skel_small(L.d_recs, nr, idx, fac, v, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 0,
+        launch_solve_skel_small(L.d_recs, nr, idx, fac, vv, nrhs, solve_skel_small_smem(L.max_nc, L.max_nq, nrhs), 0,
                                 s);
         ++g_launches;
       } else if (nr) {
-        launch_solve_skel(L.d_recs, nr, idx, fac, v, nrhs, 0, scratch, pr, sm, s);
+        launch_solve_skel(L.d_recs, nr, idx, fac, vv, nrhs, 0, scratch, pr, sm, s);
         ++g_launches;
       }
     } else {
-      if (li == 0 && bands && nr && small_path(L)) {  // rows leave as their bands finish
+      if (band0 && nr && small_path(L)) {  // rows leave as their bands finish
         for (size_t b = 0; b < bands->bwd.size(); ++b) {
           const int lo = bands->bwd[b].first, hi = bands->bwd[b].second;
           if (hi > lo) {
-            launch_solve_elim_small(L.d_recs + lo, hi - lo, idx, fac, (int64_t)F->fac.cap, v, nrhs, nullptr,
+            launch_solve_elim_small(L.d_recs + lo, hi - lo, idx, fac, (int64_t)F->fac.cap, vv, nrhs, nullptr,
                                     L.max_nc, L.max_nq, solve_small_smem(L.max_nc, L.max_nq, nrhs), 0, s);
             ++g_launches;
           }
           HCK(cudaEventRecord(bands->bwd_done[b], s));
         }
       } else if (nr && small_path(L)) {
-        launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, v, nrhs, nullptr, L.max_nc, L.max_nq,
+        launch_solve_elim_small(L.d_recs, nr, idx, fac, (int64_t)F->fac.cap, vv, nrhs, nullptr, L.max_nc, L.max_nq,
                                 solve_small_smem(L.max_nc, L.max_nq, nrhs), 0, s);
         ++g_launches;
       } else if (nr) {
-        launch_solve_elim_bwd(L.d_recs, nr, idx, fac, v, nrhs, scratch, pr, sm, s);
+        launch_solve_elim_bwd(L.d_recs, nr, idx, fac, vv, nrhs, scratch, pr, sm, s);
         ++g_launches;
       }
     }
-    phases(L.bwd_ph);
-    if (li == 0 && bands && !(nr && small_path(L)))  // (not banded after all: every band done here)
+    phases(L.bwd_ph, vv, nullptr);
+    if (band0 && !(nr && small_path(L)))  // (not banded after all: every band done here)
       for (cudaEvent_t e : bands->bwd_done) HCK(cudaEventRecord(e, s));
+  };
+  const size_t nl = F->levels.size();
+  if (F->part) {
+    // Partitioned sweep (build_shard_solve): this process's ranks run their
+    // own records on their own copy of v; the planned rows move in between.
+    const int P = F->nranks;
+    const int lo = F->emu ? 0 : F->me, hi = F->emu ? P : F->me + 1;
+    std::vector<double*> vr((size_t)P, nullptr), cr((size_t)P, nullptr);
+    std::vector<void*> owned;
+    const size_t vbytes = (size_t)F->n * nrhs * sizeof(double);
+    for (int r = lo; r < hi; ++r) {
+      if (r == lo) {
+        vr[(size_t)r] = v;
+        cr[(size_t)r] = contrib;
+        continue;
+      }
+      HCK(cudaMallocAsync((void**)&vr[(size_t)r], std::max<size_t>(vbytes, 8), s));
+      HCK(cudaMemcpyAsync(vr[(size_t)r], v, vbytes, cudaMemcpyDeviceToDevice, s));
+      HCK(cudaMallocAsync((void**)&cr[(size_t)r], std::max<size_t>(F->max_contrib * nrhs * sizeof(double), 8), s));
+      owned.push_back(vr[(size_t)r]);
+      owned.push_back(cr[(size_t)r]);
+    }
+    int64_t xmax = 0;
+    auto step_rows = [&](const LevelRec::XStep& X, bool mine_only) {
+      int64_t sn = 0, rn = 0;
+      for (const auto& p : X.pairs) {
+        if (!F->emu && mine_only) {
+          if (p.src == F->me) sn += p.cnt;
+          if (p.dst == F->me) rn += p.cnt;
+        } else {
+          sn = std::max(sn, p.cnt);
+        }
+      }
+      return F->emu ? sn : sn + rn;
+    };
+    for (const auto& L : F->levels)
+      for (const auto& X : L.xs) xmax = std::max(xmax, step_rows(X, true));
+    xmax = std::max(xmax, step_rows(F->gather, true));
+    double* xbuf = nullptr;
+    HCK(cudaMallocAsync((void**)&xbuf, std::max<size_t>((size_t)xmax * nrhs * sizeof(double), 8), s));
+    owned.push_back(xbuf);
+    int64_t moved = 0;
+    // rows listed by X from bufs[src] to bufs[dst] (vector rows or contribution rows)
+    auto exchange = [&](const LevelRec::XStep& X, std::vector<double*>& bufs) {
+      if (X.pairs.empty()) return;
+      if (F->emu) {
+        for (const auto& p : X.pairs) {
+          launch_rows_gather(bufs[(size_t)p.src], X.d_rows + p.off, p.cnt, nrhs, xbuf, s);
+          launch_rows_scatter(xbuf, X.d_rows + p.off, p.cnt, nrhs, bufs[(size_t)p.dst], s);
+          g_launches += 2;
+          moved += p.cnt;
+        }
+        return;
+      }
+      std::vector<P2P> sends, recvs;
+      std::vector<const LevelRec::XPair*> unpack;
+      int64_t o = 0;
+      for (const auto& p : X.pairs) {
+        if (p.src == F->me) {
+          launch_rows_gather(bufs[(size_t)F->me], X.d_rows + p.off, p.cnt, nrhs, xbuf + o * nrhs, s);
+          ++g_launches;
+          sends.push_back(P2P{p.dst, xbuf + o * nrhs, (size_t)p.cnt * nrhs * sizeof(double)});
+          o += p.cnt;
+          moved += p.cnt;
+        }
+      }
+      const int64_t rbase = o;
+      for (const auto& p : X.pairs) {
+        if (p.dst == F->me) {
+          recvs.push_back(P2P{p.src, xbuf + o * nrhs, (size_t)p.cnt * nrhs * sizeof(double)});
+          unpack.push_back(&p);
+          o += p.cnt;
+          moved += p.cnt;
+        }
+      }
+      if (sends.empty() && recvs.empty()) return;
+      try {
+        comm_sendrecv(F->comm, sends.data(), (int)sends.size(), recvs.data(), (int)recvs.size(), s);
+      } catch (const std::exception& e) {
+        throw Fail{HIFDE_CUDA, e.what()};
+      }
+      o = rbase;
+      for (const auto* p : unpack) {
+        launch_rows_scatter(xbuf + o * nrhs, X.d_rows + p->off, p->cnt, nrhs, bufs[(size_t)F->me], s);
+        ++g_launches;
+        o += p->cnt;
+      }
+    };
+    for (size_t li = 0; li < nl; ++li) {
+      const LevelRec& L = F->levels[li];
+      exchange(L.xs[0], vr);
+      for (int r = lo; r < hi; ++r) fwd_records(L.rank_view[(size_t)r], vr[(size_t)r], cr[(size_t)r], false);
+      exchange(L.xs[1], cr);
+      for (int r = lo; r < hi; ++r) fwd_reduce(L.rank_view[(size_t)r], vr[(size_t)r], cr[(size_t)r]);
+    }
+    for (size_t li = nl; li-- > 0;) {
+      const LevelRec& L = F->levels[li];
+      exchange(L.xs[2], vr);
+      for (int r = lo; r < hi; ++r) bwd_records(L.rank_view[(size_t)r], vr[(size_t)r], false);
+    }
+    if (F->emu) {  // rows held by virtual ranks 1.. into rank 0's vector
+      exchange(F->gather, vr);
+    } else {  // every rank returns the whole solution: zeros where another rank holds the row, summed
+      launch_rows_zero_unheld(v, F->d_holder, F->me, F->n, nrhs, s);
+      ++g_launches;
+      try {
+        comm_allreduce(F->comm, v, (size_t)F->n * nrhs, kF64, kSum, s);
+      } catch (const std::exception& e) {
+        throw Fail{HIFDE_CUDA, e.what()};
+      }
+    }
+    F->solve_xfer_bytes += moved * nrhs * (int64_t)sizeof(double);
+    for (void* q : owned) HCK(cudaFreeAsync(q, s));
+  } else {
+    // kernel log: one entry per level and direction; algorithmic bytes = the
+    // level's factor entries + one read and one write of every touched row
+    auto kbegin = [&](const LevelRec& L, bool fwd) {
+      if (!F->klog.on || (L.nall == 0 && L.recs.empty())) return -1;
+      const char* nm = L.kind == 1 ? (fwd ? "solve_skel_fwd" : "solve_skel_bwd")
+                                   : (fwd ? "solve_elim_fwd" : "solve_elim_bwd");
+      return F->klog.begin(nm, L.tag, 1, 8.0 * (L.solve_fac + 2.0 * L.solve_rows * nrhs) * 1e-9,
+                           2.0 * L.solve_fac * nrhs * 1e-9, s);
+    };
+    struct KEnd {
+      const hifde_factor_t* F; int kl; cudaStream_t s;
+      ~KEnd() { F->klog.end(kl, s); }
+    };
+    for (size_t li = 0; li < nl; ++li) {
+      const LevelRec& L = F->levels[li];
+      KEnd kend{F, kbegin(L, true), s};
+      fwd_records(L, v, contrib, li == 0 && bands);
+      fwd_reduce(L, v, contrib);
+    }
+    for (size_t li = nl; li-- > 0;) {
+      const LevelRec& L = F->levels[li];
+      KEnd kend{F, kbegin(L, false), s};
+      bwd_records(L, v, li == 0 && bands);
+    }
   }
   HCK(cudaGetLastError());
   HCK(cudaFreeAsync(contrib, s));
@@ -4489,7 +4828,7 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
     F->klog.clear(1);
   }
   const bool disjoint = (const char*)x >= (const char*)b + bytes || (const char*)x + bytes <= (const char*)b;
-  if (!dev && nrhs >= 16 && bytes >= ((size_t)64 << 20) && disjoint && PinnedXfer::page_locked(b)) {
+  if (!dev && !F->part && nrhs >= 16 && bytes >= ((size_t)64 << 20) && disjoint && PinnedXfer::page_locked(b)) {
     solve_pipelined(F, b, x, nrhs, s);
     return;
   }
@@ -4509,6 +4848,7 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
 
 // y = F x: the solve sweep inverted record by record (kernels_solve.cu).
 void do_apply(const hifde_factor_t* F, const double* x, double* y, int nrhs, bool dev, cudaStream_t s) {
+  ensure_whole(F, s);
   const int64_t N = F->n;
   const size_t bytes = (size_t)N * nrhs * sizeof(double);
   double* v = nullptr;
@@ -5029,6 +5369,10 @@ int hifde_copy_arenas(const hifde_factor_t* f, double* fac, int64_t fac_len, int
   }
   try {
     HCK(cudaSetDevice(f->device));
+    if (fac && fac_len && !f->whole) {  // sharded over real ranks: every rank calls this (a collective)
+      ensure_whole(f, f->stream);
+      HCK(cudaStreamSynchronize(f->stream));
+    }
     if (fac && fac_len) HCK(cudaMemcpy(fac, f->fac.p, (size_t)fac_len * sizeof(double), cudaMemcpyDeviceToHost));
     if (idx && idx_len) HCK(cudaMemcpy(idx, f->idx.p, (size_t)idx_len * sizeof(int32_t), cudaMemcpyDeviceToHost));
   } catch (const Fail& e) {
@@ -5079,6 +5423,8 @@ int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
   info->idx_len = (int64_t)f->idx.n;
   info->nranks = f->nranks;
   info->xfer_bytes = f->xfer_bytes;
+  info->factor_whole = f->whole ? 1 : 0;
+  info->solve_xfer_bytes = f->solve_xfer_bytes.load();
   return HIFDE_OK;
 }
 

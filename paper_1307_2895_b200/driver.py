@@ -113,6 +113,16 @@ class GeneralizedLDL:
     def storage_bytes(self) -> int:
         return self.metrics["m_f_bytes"]
 
+    def shard_info(self) -> dict:
+        """Live state of a sharded factor: whether this rank's
+        arena holds every record yet (real ranks hold their own until apply /
+        export / power sum them) and the vector bytes its partitioned solves
+        exchanged with the other ranks."""
+        info = L.Info()
+        self._lib.hifde_get_info(self._h, C.byref(info))
+        return {"nranks": int(info.nranks), "factor_whole": bool(info.factor_whole),
+                "solve_xfer_bytes": int(info.solve_xfer_bytes)}
+
     def _out(self, like: np.ndarray) -> np.ndarray:
         """Output array for a host solve/apply: large results live in a
         page-locked block of the library's caching pool (DMA'd straight into,
