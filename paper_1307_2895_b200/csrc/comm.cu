@@ -126,6 +126,17 @@ __global__ void rows_zero_unheld_kernel(double* __restrict__ v, const uint8_t* _
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x)
     if (holder[i / nrhs] != me) v[i] = 0.0;
 }
+// Retire the DOFs of merged index-arena regions in the active mask: region i
+// is idx[off[i], off[i] + len[i]); its first kout[kid[i]] entries stay
+// active (a skeleton group's sk; kid < 0: none, a whole cell).  One CTA per
+// region.
+__global__ void retire_regions_kernel(const int32_t* __restrict__ idx, const int64_t* __restrict__ off,
+                                      const int64_t* __restrict__ len, const int64_t* __restrict__ kid,
+                                      const int32_t* __restrict__ kout, uint8_t* __restrict__ active) {
+  const int i = blockIdx.x;
+  const int64_t k = kid[i] >= 0 ? kout[kid[i]] : 0;
+  for (int64_t a = k + threadIdx.x; a < len[i]; a += blockDim.x) active[idx[off[i] + a]] = 0;
+}
 int rows_grid(int64_t tot) { return (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 16)); }
 
 }  // namespace
@@ -212,6 +223,11 @@ void launch_rows_scatter(const double* src, const int32_t* rows, int64_t nrows, 
                          cudaStream_t s) {
   if (nrows <= 0) return;
   rows_scatter_kernel<<<rows_grid(nrows * nrhs), 256, 0, s>>>(src, rows, nrows, nrhs, dst);
+}
+void launch_retire_regions(const int32_t* idx, const int64_t* off, const int64_t* len, const int64_t* kid,
+                           const int32_t* kout, int nreg, uint8_t* active, cudaStream_t s) {
+  if (nreg <= 0) return;
+  retire_regions_kernel<<<nreg, 128, 0, s>>>(idx, off, len, kid, kout, active);
 }
 void launch_rows_zero_unheld(double* v, const uint8_t* holder, int me, int64_t n, int nrhs, cudaStream_t s) {
   if (n <= 0) return;

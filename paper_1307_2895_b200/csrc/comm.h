@@ -61,6 +61,9 @@ void launch_seg_copy_i32(const int32_t* src, int32_t* dst, const int64_t* src_of
 void launch_rows_gather(const double* src, const int32_t* rows, int64_t nrows, int nrhs, double* dst, cudaStream_t s);
 void launch_rows_scatter(const double* src, const int32_t* rows, int64_t nrows, int nrhs, double* dst,
                          cudaStream_t s);
+// active[idx[off[i] + a]] = 0 for a in [kout[kid[i]] (0 if kid[i] < 0), len[i])
+void launch_retire_regions(const int32_t* idx, const int64_t* off, const int64_t* len, const int64_t* kid,
+                           const int32_t* kout, int nreg, uint8_t* active, cudaStream_t s);
 void launch_rows_zero_unheld(double* v, const uint8_t* holder, int me, int64_t n, int nrhs, cudaStream_t s);
 
 }  // namespace hifde

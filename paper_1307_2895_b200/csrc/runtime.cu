@@ -14,7 +14,7 @@
 // Sharding (options.comm, shard.h / comm.h): every rank runs this host
 // analysis; a group's kernels run on its owner, consumed blocks are exchanged
 // before each level and the state every rank reads is merged after each
-// launch.  Exact-order 3D batches queue each large-group tail on a second
+// launch; the solve runs each rank's own records, exchanging vector rows.  Exact-order 3D batches queue each large-group tail on a second
 // stream so it overlaps the next batch's assembly and ID.
 #include <algorithm>
 #include <atomic>
@@ -991,6 +991,7 @@ struct Factorizer {
     for (auto* d : {&xsend, &xrecv}) d->release(s);
     xseg.release(s);
     xiseg.release(s);
+    xret.release(s);
     xi32.release(s);
     agree.release(s);
     gpart.release(s);
@@ -1078,12 +1079,13 @@ struct Factorizer {
   // --- sharding over ranks (opt.comm, shard.h) -------------------------------
   // Every rank runs this host analysis identically; a group's kernels run on
   // its owner only.  Real ranks (NCCL): the blocks a rank's groups consume
-  // from other ranks arrive before the launch, and the state every rank reads
-  // (active mask, ranks, sk/rd lists) is merged after each launch by
-  // whole-slice all-reduces (min / max over slices the non-owners left at
-  // 1 / 0); the factor arena is summed once at the end (non-owners hold
-  // zeros).  Emulated ranks: one process launches every virtual rank's groups
-  // with that rank's private block arena.
+  // from other ranks arrive before the launch; after each launch the ranks
+  // and sk/rd lists are merged by all-reduces over the level's slices (max
+  // over slices the non-owners left at 0) and every rank retires the other
+  // ranks' DOFs in its own active mask.  Each rank keeps only its records'
+  // factor values: the solve is partitioned the same way (build_shard_solve).
+  // Emulated ranks: one process launches every virtual rank's groups with
+  // that rank's private block arena.
   const hifde_comm* comm = nullptr;
   int P = 1, me = 0;
   bool emu = false, real = false;
@@ -1189,16 +1191,19 @@ struct Factorizer {
   void fac_grown(size_t off, size_t cnt) {
     if (real && cnt) HCK(cudaMemsetAsync(F->fac.p + off, 0, cnt * sizeof(double), s));
   }
-  // Real ranks: merge the ranks kout[0, nk), the index-arena regions
+  // Real ranks: merge the ranks kout[0, nk) and the index-arena regions
   // [off[i], off[i] + len[i]) (sk/rd lists, zero on non-owners: packed,
-  // max-reduced, scattered back) and the active masks (min).
+  // max-reduced, scattered back), then retire every region's DOFs past its
+  // rank kout[kid[i]] (kid == nullptr: cells, all of them) in the local active
+  // mask -- the owners' kernels retired theirs already; no rank exchanges the
+  // N-byte mask.
   DBuf<int32_t> xi32;
-  DBuf<int64_t> xiseg;
-  void union_state(const int64_t* off, const int* len, int nreg, int64_t nk) {
+  DBuf<int64_t> xiseg, xret;
+  void union_state(const int64_t* off, const int* len, const int32_t* kid, int nreg, int64_t nk) {
     if (!real) return;
     try {
       if (nk > 0) comm_allreduce(comm, kout.p, (size_t)nk, kI32, kMax, s);
-      if (nreg > 0) {
+      if (nreg > 0 && kid) {
         std::vector<int64_t> seg((size_t)3 * nreg);
         int64_t tot = 0;
         for (int i = 0; i < nreg; ++i) {
@@ -1217,7 +1222,18 @@ struct Factorizer {
           g_launches += 2;
         }
       }
-      comm_allreduce(comm, d_active, (size_t)N, kU8, kMin, s);
+      if (nreg > 0) {
+        std::vector<int64_t> ret((size_t)3 * nreg);
+        for (int i = 0; i < nreg; ++i) {
+          ret[(size_t)i] = off[i];
+          ret[(size_t)nreg + i] = len[i];
+          ret[(size_t)2 * nreg + i] = kid ? kid[i] : -1;
+        }
+        xret.reserve(ret.size(), s);
+        xret.upload(ret.data(), 0, ret.size(), s);
+        launch_retire_regions(F->idx.p, xret.p, xret.p + nreg, xret.p + 2 * nreg, kout.p, nreg, d_active, s);
+        ++g_launches;
+      }
     } catch (const std::exception& e) {
       throw Fail{HIFDE_CUDA, e.what()};
     }
@@ -1226,11 +1242,13 @@ struct Factorizer {
     if (!real) return;
     std::vector<int64_t> off((size_t)nt);
     std::vector<int> len((size_t)nt);
+    std::vector<int32_t> kid((size_t)nt);
     for (int64_t t = 0; t < nt; ++t) {
       off[(size_t)t] = tasks[(size_t)t].out_off;
       len[(size_t)t] = tasks[(size_t)t].nc;
+      kid[(size_t)t] = (int32_t)t;
     }
-    union_state(off.data(), len.data(), (int)nt, nt);
+    union_state(off.data(), len.data(), kid.data(), (int)nt, nt);
   }
   // Make every block listed by the tasks resident on the task's owner.
   void exchange_blocks(int64_t nt, const uint8_t* owner, const int64_t* ptr, const int32_t* cnt,
@@ -1766,8 +1784,16 @@ struct Factorizer {
     HTRACE("  launched");
     if (trace_on()) { HCK(cudaStreamSynchronize(s)); HTRACE("  kernels done"); }
     // (the kernels retire the cells in the device active mask themselves;
-    // real ranks merge the masks)
-    union_state(nullptr, nullptr, 0, 0);
+    // real ranks retire the other ranks' cells locally)
+    if (real) {
+      std::vector<int64_t> off((size_t)nt);
+      std::vector<int> len((size_t)nt);
+      for (int64_t t = 0; t < nt; ++t) {
+        off[(size_t)t] = tasks[(size_t)t].dofs_off;
+        len[(size_t)t] = tasks[(size_t)t].nc;
+      }
+      union_state(off.data(), len.data(), nullptr, (int)nt, 0);
+    }
     L.t_launch = now_s() - tp;
     L.lap("launch");
     tp = now_s();
@@ -2381,11 +2407,13 @@ struct Factorizer {
       if (!real || hi <= lo) return;
       std::vector<int64_t> off;
       std::vector<int> len;
+      std::vector<int32_t> kid;
       for (int64_t i = lo; i < hi; ++i) {
         off.push_back(v[(size_t)i].out_off);
         len.push_back(v[(size_t)i].nc);
+        kid.push_back(v[(size_t)i].group);
       }
-      union_state(off.data(), len.data(), (int)off.size(), nt);
+      union_state(off.data(), len.data(), kid.data(), (int)off.size(), nt);
     };
     HCK(cudaEventCreate(&L.ev0));
     HCK(cudaEventCreate(&L.ev1));

@@ -7,10 +7,17 @@ communicator to ``factor_hifde`` / ``factor_hifde3x`` / ``factor_mf``
 (``comm=``) partitions the level sweep spatially: each group is factored by the
 rank owning its subdomain box, the blocks a rank's groups consume from its
 neighbours travel as grouped ``ncclSend/ncclRecv`` before the level, and the
-coarse exact-order levels run on rank 0.  Every rank returns the whole factor
-(the records are summed once at the end), so ``apply_inverse`` on any rank is
-the single-GPU solve; ``rhs_columns`` splits a block of right-hand sides over
-the ranks.
+coarse exact-order levels run on rank 0.  Each rank keeps the factor values
+of its own records only, and ``apply_inverse`` (and ``pcg_gpu``) is the
+partitioned solve: every rank runs its records level by level, and the vector
+rows a rank is about to read while another holds their current value move by
+grouped ``ncclSend/ncclRecv`` (neighbour-row reductions run on the rank that
+reads the row next, so the result is bit-identical to the single sweep); every
+rank returns the whole solution.  The communicator must outlive the factor's
+solves.  ``apply``, the export and the power estimators sum the ranks' factor
+arenas once, on first use (a collective: every rank calls them).
+``rhs_columns`` splits a block of right-hand sides over the ranks when
+independent solves are wanted instead.
 
 The reference (``src/driver.py:183``) is single-threaded and has no
 multi-process path; this module has no reference counterpart beyond the
