@@ -251,6 +251,12 @@ int cpqr_coop_capacity(size_t smem);
 // Used only when u cond(G11) ~ u / eps^2 <= 1e-8 << eps (T = R11^-1 R12 from
 // the Cholesky factor of G loses u cond(G11)); the rank cut eps^2 |G| >> u |G|
 constexpr double kGramMinEps = 1e-4;
+// Full-rank certificate of a small skeletonization group (skel_group_t): groups
+// of at most kCertMaxNc DOFs, tolerances from kCertMinEps up (so that
+// (kCertSafety eps)^2 >= 1e-11 stays far above the rounding of the Gram matrix).
+constexpr int kCertMaxNc = 12;
+constexpr double kCertMinEps = 2e-7;
+constexpr double kCertSafety = 16.0;
 constexpr double kPromoteWork = 2.5e5;  // nq nc^2 above which a one-CTA group joins the pipeline
 constexpr int kGramRows = 1024;  // rows per split of a Gram tile
 void launch_skelbig_gram(const SkelBigTask* tasks, const int4* work, int nwork, const int4* tiles, int ntiles,

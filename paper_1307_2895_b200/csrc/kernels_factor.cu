@@ -676,6 +676,19 @@ __global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restr
 struct NoWait {
   __device__ void operator()() const {}
 };
+// Full-rank certificate on / off (HIFDE_NO_RANK_CERT clears it: the tests'
+// A/B against the plain pivoted QR, which must give the same records).
+__device__ int d_rank_cert = 1;
+static void rank_cert_init() {
+  static const bool once = [] {
+    if (getenv("HIFDE_NO_RANK_CERT")) {
+      const int z = 0;
+      cudaMemcpyToSymbol(d_rank_cert, &z, sizeof z);
+    }
+    return true;
+  }();
+  (void)once;
+}
 struct NoPublish {
   __device__ void operator()(int, const int32_t*, const int32_t*, int) const {}
 };
@@ -1030,12 +1043,63 @@ __device__ void skel_group_t(const SkelTask& t, const Arenas& A, double eps, uns
   // per step.
   double* Mc = t.mode == 0 ? wsh + (size_t)nc * nc : wsh;
   if (t.mode != 3) { nqm = nq; ldm = ldq; }
+  // ---- full-rank certificate (small groups, eps well above rounding) ------
+  // Every |R_ii| of the pivoted QR is at least sigma_min(Mq), and R_11 is the
+  // largest column norm.  If G - tau^2 I (G = Mq^T Mq, tau = kCertSafety eps
+  // max_j |Mq e_j|) has an LDL^T with pivots above tau^2, then sigma_min > tau
+  // and no pivot can reach the cut eps |R_11| (tau^2 is >= 1e-11 |G|, five
+  // orders above the rounding of G and of its factorization): the rank is nc,
+  // sk = c, nothing is eliminated -- the same record the QR ends in, without
+  // its nc dependent pivot steps.  A group that fails the test takes the QR.
+  bool certified = false;
+  if (t.mode == 0 && nc <= kCertMaxNc && nqm >= nc && eps >= kCertMinEps && d_rank_cert) {
+    double* Gm = Z;  // nc x nc (lower triangle used); Z is idle until the tail
+    const int npair = nc * (nc + 1) / 2;
+    for (int e = Tm::tid(); e < npair; e += NT) {
+      int a = 0;
+      while ((a + 1) * (a + 2) / 2 <= e) ++a;
+      const int b = e - a * (a + 1) / 2;  // b <= a
+      const double* ca = Mc + (size_t)a * ldm;
+      const double* cb = Mc + (size_t)b * ldm;
+      double s0 = 0.0, s1 = 0.0;
+      int r = 0;
+      for (; r + 1 < nqm; r += 2) {
+        s0 += ca[r] * cb[r];
+        s1 += ca[r + 1] * cb[r + 1];
+      }
+      if (r < nqm) s0 += ca[r] * cb[r];
+      Gm[a * nc + b] = s0 + s1;
+    }
+    Tm::sync();
+    double gmax = 0.0;
+    for (int j = 0; j < nc; ++j) gmax = fmax(gmax, Gm[j * nc + j]);
+    const double tau2 = (kCertSafety * eps) * (kCertSafety * eps) * gmax;
+    certified = gmax > 0.0;
+    for (int j = 0; j < nc && certified; ++j) {
+      const double d = Gm[j * nc + j] - tau2;  // the same value in every thread
+      if (!(d > tau2)) { certified = false; break; }
+      const double dinv = 1.0 / d;
+      const int m = nc - 1 - j, mp = m * (m + 1) / 2;
+      for (int e = Tm::tid(); e < mp; e += NT) {
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= e) ++a;
+        const int b = e - a * (a + 1) / 2;
+        const int ia = j + 1 + a, ib = j + 1 + b;
+        Gm[ia * nc + ib] -= Gm[ia * nc + j] * Gm[ib * nc + j] * dinv;
+      }
+      Tm::sync();
+    }
+    if (certified) {
+      for (int pos = Tm::tid(); pos < 2 * nc; pos += NT) cpos[pos] = pos < nc ? pos : pos - nc;
+      Tm::sync();
+    }
+  }
   int nq_alive = 0;
-  if (Tm::tid() == 0) {
+  if (Tm::tid() == 0 && !certified) {
     for (int i = nc; i < nf; ++i) nq_alive += salive[i];
     sh_k = nq_alive;
   }
-  for (int j = wid; j < nc; j += NW) {
+  for (int j = wid; j < nc && !certified; j += NW) {
     const double* col = Mc + (size_t)j * ldm;
     double s1 = 0.0;
     for (int r = 1 + lane; r < nqm; r += 32) s1 += col[r] * col[r];
@@ -1060,7 +1124,7 @@ __device__ void skel_group_t(const SkelTask& t, const Arenas& A, double eps, uns
   const int nslots = NT / G, sl = lane & (G - 1), slot = wid * (32 / G) + lane / G;
   double thr = 0.0;
   int k = kmax;
-  for (int i = 0; i < kmax; ++i) {
+  for (int i = 0; i < kmax && !certified; ++i) {
     const int cur = (i & 1) * nc, nxt = nc - cur;
     const double* vn1 = cq + cur;
     double* vn1o = cq + nxt;
@@ -1193,7 +1257,8 @@ __device__ void skel_group_t(const SkelTask& t, const Arenas& A, double eps, uns
     for (int pos = Tm::tid(); pos < nc; pos += NT) perm[pos] = cat[pos];
   }
   Tm::sync();
-  for (int i = Tm::tid(); i < k; i += NT) Mc[i + (size_t)perm[i] * ldm] = rdiag[i];
+  if (!certified)
+    for (int i = Tm::tid(); i < k; i += NT) Mc[i + (size_t)perm[i] * ldm] = rdiag[i];
   Mq = Mc;
   Tm::sync();
   // the redundant set is known: later groups may start (exact order) while
@@ -1679,6 +1744,7 @@ void launch_schur_tiles(const ElimTask* d_tasks, const int4* d_tiles, int ntiles
 void launch_skel(const SkelTask* d_tasks, int ntasks, const Arenas& A, double eps, size_t smem, int nt, int max_nc,
                  int max_nq, cudaStream_t s) {
   if (ntasks <= 0) return;
+  rank_cert_init();
   static bool once = false;
   if (!once) {
     allow_smem(skel_kernel<128>);
@@ -1740,6 +1806,7 @@ cudaError_t launch_skel_ordered(const SkelTask* d_tasks, int ntasks, const int64
                                 const int32_t* order, int* done, const Arenas& A, double eps, size_t smem, int nt,
                                 int grid, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
+  rank_cert_init();
   Arenas Ac = A;
   void* args[] = {(void*)&d_tasks, (void*)&ntasks, (void*)&pred_ptr, (void*)&pred, (void*)&order, (void*)&done,
                   (void*)&Ac, (void*)&eps};

@@ -530,6 +530,48 @@ def test_warp_skeleton_kernel_bit_identical(tmp_path):
         assert np.array_equal(files[0][k], files[1][k]), k
 
 
+_CERT_DUMP = r'''
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+import paper_1307_2895_b200 as H
+out = {}
+for dim, n, m, eps, var, seed in [(2, 512, 8, 1e-6, "hifde", 5), (2, 1024, 8, 1e-5, "hifde", 1),
+                                  (2, 256, 4, 1e-3, "hifde", 3), (3, 32, 4, 1e-3, "hifde3x", 2),
+                                  (3, 32, 2, 1e-2, "hifde", 4)]:
+    g = H.build_grid(dim, n, m)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=seed))
+    f = (H.factor_hifde if var == "hifde" else H.factor_hifde3x)(a, g, eps)
+    b = np.random.default_rng(7).standard_normal((g.ndof, 3))
+    out[f"{dim}_{n}_{eps}_x"] = f.apply_inverse(b)
+    out[f"{dim}_{n}_{eps}_k"] = np.array([c for _, c in f.metrics["skeleton_counts"]])
+np.savez(sys.argv[1], **out)
+'''
+
+
+def test_full_rank_certificate_changes_nothing(tmp_path):
+    """Small groups whose neighbour block is certified full rank (Gram
+    matrix minus (16 eps |R_11|)^2 I positive definite) skip the pivoted QR:
+    the record is the one the QR ends in (rank nc, nothing eliminated), so
+    ranks and solutions are identical bit for bit to HIFDE_NO_RANK_CERT, on
+    random-coefficient problems from eps 1e-6 (config 3's) to eps 1e-2,
+    where small groups do drop DOFs and must fail the certificate."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    files = []
+    for i, env in enumerate(({}, {"HIFDE_NO_RANK_CERT": "1"})):
+        fn = str(tmp_path / f"c{i}.npz")
+        r = subprocess.run([sys.executable, "-c", _CERT_DUMP, fn], capture_output=True, text=True, cwd=root,
+                           env=dict(os.environ, **env), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        files.append(np.load(fn))
+    for k in files[0].files:
+        assert np.array_equal(files[0][k], files[1][k]), k
+
+
 def test_pipelined_host_solve_matches_one_block_solve():
     """Page-locked host right-hand sides take the pipelined solve (column
     chunks: strided H2D DMA, sweep, D2H pieces scattered into the caller's
