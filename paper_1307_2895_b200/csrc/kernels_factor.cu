@@ -909,6 +909,39 @@ __device__ void skel_group_t(const SkelTask& t, const Arenas& A, double eps, uns
     // block row over the compact column list, four rows' loads in flight per
     // lane (each front entry still takes one add per block)
     const int ncc = sh_k;
+    if (ncc <= 16) {
+      // few columns land in c (the small groups): a warp per block row would
+      // leave most lanes idle, so the (row, column) pairs are dealt to the
+      // threads instead, four loads in flight per thread
+      const int total = nb * ncc;
+      const float rcc = 1.0f / (float)ncc;
+      for (int e0 = (int)Tm::tid(); e0 < total; e0 += 4 * NT) {
+        double val[4];
+        int pk[4], pl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int e = e0 + u * NT;
+          pk[u] = -1;
+          pl[u] = 0;
+          val[u] = 0.0;
+          if (e < total) {
+            int kr = (int)((float)e * rcc);
+            if (kr * ncc > e) --kr;
+            else if ((kr + 1) * ncc <= e) ++kr;
+            const int l = skl[e - kr * ncc];
+            pl[u] = smap[l];
+            pk[u] = smap[kr];
+            if (pk[u] >= 0) val[u] = bv[(size_t)kr * nb + l];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (pk[u] < 0) continue;
+          if (pk[u] < nc) Acc[pk[u] * nc + pl[u]] += val[u];
+          else Mq[(pk[u] - nc) + (size_t)pl[u] * ldq] += val[u];
+        }
+      }
+    } else
     for (int k0 = (int)(Tm::tid() >> 5) * 4; k0 < nb; k0 += NT / 8) {
       for (int j = (int)(Tm::tid() & 31); j < ncc; j += 32) {
         const int l = skl[j], pl = smap[l];
