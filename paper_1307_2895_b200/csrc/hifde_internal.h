@@ -480,8 +480,8 @@ cudaError_t sym_skel_sizes(const SymFront& P, double promote_work, int gram_eps_
                            SkelInc* exc, LevelTotals* tot, SymWork& W, cudaStream_t s);
 cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t s);
 cudaError_t sym_skel_chain(const int64_t* pred_start, const int32_t* npred, const int32_t* preds, const int32_t* ng,
-                           int ng_ub, int iters, int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot,
-                           cudaStream_t s);
+                           int ng_ub, int iters, int cap, int32_t* b0, int32_t* b1, int32_t* changed,
+                           LevelTotals* tot, cudaStream_t s);
 // claim order of an exact level: groups sorted stably by dependency depth
 // (the final relaxation buffer of sym_skel_chain)
 cudaError_t sym_skel_order(const int32_t* b0, const int32_t* b1, const int32_t* changed, int iters,

@@ -1112,12 +1112,12 @@ struct Factorizer {
   cudaEvent_t ev_symdone = nullptr, ev_symjoin = nullptr;
   bool symdone_ok = false;
   DBuf<int32_t> lists_alt;  // the skeleton symbolic's block lists while the elimination reads `lists`
-  // From the second overlap on, the analysis runs on a high-priority stream
-  // (sym_hi swapped in): next to the blocked eliminations it is a latency-
-  // bound chain whose CTAs should go first as the elimination's retire.  The
-  // first overlap (the level-0 elimination, which fills the GPU, against the
-  // level-0.5 analysis, which would too) keeps normal priority: reordering
-  // two saturating kernels gains nothing there.
+  // The overlapped analysis runs on a high-priority stream (sym_hi swapped
+  // in at the first overlap): it is a chain of ~40 small launches with a
+  // readback in the middle, and at normal priority its CTAs queue behind the
+  // elimination's (config 3: the level-0.5 analysis then ran in the tail of
+  // the level-0 elimination, 1.1 ms of mostly idle SMs; at high priority it
+  // ends 3 ms before the elimination does and the pair takes 0.3 ms less).
   cudaStream_t sym_hi = nullptr;
   int sym_overlaps = 0;
   cudaStream_t sym_stream() {
@@ -3474,7 +3474,7 @@ struct Factorizer {
     const bool ovl = symdone_ok;
     symdone_ok = false;
     if (ovl) {
-      if (++sym_overlaps == 2) std::swap(sym_s, sym_hi);
+      if (++sym_overlaps == 1) std::swap(sym_s, sym_hi);
       HCK(cudaStreamWaitEvent(sym_s, ev_symdone, 0));
       std::swap(s, sym_s);
       std::swap(lists, lists_alt);
@@ -3494,13 +3494,15 @@ struct Factorizer {
     const bool gram_eps = opt.eps >= kGramMinEps;
     HCK(sym_skel_sizes(P, kPromoteWork, gram_eps ? 1 : 0, (int)ng_ub, inc, exc, d_tot, symw, s));
     const int iters = opt.exact_max_batches + 1;
+    // AUTO: only whether the chain passes exact_max_batches matters (early exit of the relaxation)
+    const int chain_cap = opt.order_mode == HIFDE_ORDER_AUTO ? opt.exact_max_batches : 0;
     const bool chain_early = P.pred_tmp != nullptr;
     if (chain_early) {  // the dependency chain from the count pass's lists: one readback for the level
       sy_b0.reserve((size_t)ng_ub + 1, s);
       sy_b1.reserve((size_t)ng_ub + 1, s);
       sy_changed.reserve((size_t)iters + 1, s);
-      HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_pred_tmp.p, &d_scal->ng, (int)ng_ub, iters, sy_b0.p,
-                         sy_b1.p, sy_changed.p, d_tot, s));
+      HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_pred_tmp.p, &d_scal->ng, (int)ng_ub, iters, chain_cap,
+                         sy_b0.p, sy_b1.p, sy_changed.p, d_tot, s));
     }
     dev_sync_totals(!ovl);
     L.lap("dev-count");
@@ -3573,8 +3575,8 @@ struct Factorizer {
         sy_npred.reserve((size_t)ng + 1, s);
         sy_pred_start.reserve((size_t)ng + 1, s);
         HCK(cudaMemcpyAsync(sy_pred_start.p, sy_pred_ptr.p, sizeof(int64_t) * (size_t)ng, cudaMemcpyDeviceToDevice, s));
-        HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_preds.p, &d_scal->ng, (int)ng, iters, sy_b0.p, sy_b1.p,
-                           sy_changed.p, d_tot, s));
+        HCK(sym_skel_chain(sy_pred_start.p, sy_npred.p, sy_preds.p, &d_scal->ng, (int)ng, iters, chain_cap, sy_b0.p,
+                           sy_b1.p, sy_changed.p, d_tot, s));
         HCK(cudaMemcpyAsync(h_tot, d_tot, sizeof(LevelTotals), cudaMemcpyDeviceToHost, s));
         HCK(cudaStreamSynchronize(s));
       }

@@ -861,10 +861,45 @@ __global__ void __launch_bounds__(256) skel_relax_coop(const int64_t* __restrict
                                                        const int32_t* __restrict__ npred,
                                                        const int32_t* __restrict__ preds,
                                                        const int32_t* __restrict__ ng, int32_t* b0, int32_t* b1,
-                                                       int32_t* changed, int iters, LevelTotals* tot) {
+                                                       int32_t* changed, int iters, int cap, LevelTotals* tot) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const int n = *ng;
   int m = 0;  // max depth this thread wrote in the last sweep that ran
+  if (cap > 0) {
+    // AUTO order only asks whether the chain exceeds `cap`: relax in place
+    // (every value stays a lower bound of its depth and only grows, so the
+    // fixed point is the Jacobi sweeps' and is reached no later) and stop as
+    // soon as any depth passes the cap -- a fine level's chain of thousands
+    // shows after a few sweeps instead of cap + 1.  The level then runs in
+    // snapshot order and its depths are not used; a chain within the cap
+    // converges to the exact depths as before.
+    for (int it = 0; it < iters; ++it) {
+      int ch = 0;
+      for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        int b = 0;
+        const int64_t p0 = pred_start[t];
+        for (int64_t p = p0; p < p0 + npred[t]; ++p) b = max(b, __ldcg(b0 + preds[p]) + 1);
+        if (b > __ldcg(b0 + t)) {
+          __stcg(b0 + t, b);
+          ch = 1;
+        }
+        m = max(m, b);
+      }
+      const int any = __syncthreads_or(ch | (m > cap ? 2 : 0));
+      if (threadIdx.x == 0) {
+        if (any & 1) atomicExch(changed + it, 1);
+        if (any & 2) atomicExch(changed + iters, 1);  // past the cap
+      }
+      grid.sync();
+      if (__ldcg(changed + it) == 0 || __ldcg(changed + iters) != 0) break;  // uniform: read after the barrier
+    }
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) b1[t] = __ldcg(b0 + t);
+    typedef cub::BlockReduce<int, 256> R0;
+    __shared__ typename R0::TempStorage rt0;
+    m = R0(rt0).Reduce(m, cub::Max());
+    if (threadIdx.x == 0 && m > 0) amax64(&tot->max_chain, m);
+    return;
+  }
   for (int it = 0; it < iters; ++it) {
     if (it > 0 && __ldcg(changed + it - 1) == 0) break;  // uniform: read after the barrier
     const int32_t* bin = (it % 2 == 0) ? b0 : b1;
@@ -1220,16 +1255,16 @@ cudaError_t sym_skel_fill(const SymFront& P, const SkelFillArgs& A, cudaStream_t
 }
 
 cudaError_t sym_skel_chain(const int64_t* pred_start, const int32_t* npred, const int32_t* preds, const int32_t* ng,
-                           int ng_ub, int iters, int32_t* b0, int32_t* b1, int32_t* changed, LevelTotals* tot,
-                           cudaStream_t s) {
+                           int ng_ub, int iters, int cap, int32_t* b0, int32_t* b1, int32_t* changed,
+                           LevelTotals* tot, cudaStream_t s) {
   cudaMemsetAsync(b0, 0, sizeof(int32_t) * (size_t)ng_ub, s);
-  cudaMemsetAsync(changed, 0, sizeof(int32_t) * (size_t)iters, s);
+  cudaMemsetAsync(changed, 0, sizeof(int32_t) * ((size_t)iters + 1), s);
   cudaMemsetAsync(&tot->max_chain, 0, sizeof(int64_t), s);
   static int per_sm = 0;
   if (!per_sm) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, skel_relax_coop, 256, 0);
   const int grid = std::max(1, std::min(sym_grid(std::max(per_sm, 1)), (ng_ub + 255) / 256));
   void* args[] = {(void*)&pred_start, (void*)&npred, (void*)&preds, (void*)&ng, (void*)&b0, (void*)&b1,
-                  (void*)&changed, (void*)&iters, (void*)&tot};
+                  (void*)&changed, (void*)&iters, (void*)&cap, (void*)&tot};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)skel_relax_coop, dim3((unsigned)grid), dim3(256), args, 0, s);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
