@@ -407,6 +407,11 @@ def roofline(kstats, steps, pk, pk_kind):
             "launches_per_step": dom["launches"] / steps, "launch_seconds": per_launch_s,
             "algorithmic_gbytes_per_launch": gb_l, "algorithmic_gflop_per_launch": gf_l,
             "share_of_logged_time": dom["seconds"] / total if total else None,
+            "launch_seconds_note": ("CUDA events around the launch inside the timed step; the level-0 elimination's "
+                                    "interval includes the level-0.5 symbolic analysis, which runs on a high-priority "
+                                    "stream on the same SMs (the kernel alone under ncu: profiles/r02_ncu_final.txt)"
+                                    if dom["name"] == "elim_small_kernel" and dom["tag"] == 0.0 else
+                                    "CUDA events around the launch inside the timed step"),
             "peak_kind": peak_kind,
             "top_kernels": [{"kernel": a["name"], "level": a["tag"], "phase": a["phase"],
                              "ms_per_step": a["seconds"] / steps * 1e3,
