@@ -595,7 +595,7 @@ constexpr int kTile = kSchurTile, kKc = 32, kLdS = 68;
 
 // Rows of W are staged 32 at a time; the next stage is prefetched into
 // registers while the DMMA loop runs on the current one.
-__global__ void __launch_bounds__(128) schur_tile_kernel(const ElimTask* __restrict__ tasks,
+__global__ void __launch_bounds__(128, 3) schur_tile_kernel(const ElimTask* __restrict__ tasks,
                                                          const int4* __restrict__ tiles, Arenas A) {
   __shared__ double Wa[kKc][kLdS];
   __shared__ double Wb[kKc][kLdS];
