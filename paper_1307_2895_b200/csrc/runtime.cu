@@ -964,6 +964,11 @@ struct Factorizer {
       cudaStreamDestroy(a0_s);
       if (ev_a0) cudaEventDestroy(ev_a0);
     }
+    if (pat_s) {
+      cudaStreamSynchronize(pat_s);
+      cudaStreamDestroy(pat_s);
+      cudaEventDestroy(ev_pat);
+    }
     if (sym_s) {
       cudaStreamSynchronize(sym_s);
       cudaStreamDestroy(sym_s);
@@ -979,6 +984,10 @@ struct Factorizer {
   void release_all() {
     if (released) return;
     released = true;
+    if (pat_pending) {  // (not pat_wait: release_all also runs on error paths and must not throw)
+      pat_pending = false;
+      cudaEventSynchronize(ev_pat);
+    }
     if (tail_s) join_inv();  // the deferred inverses read buffers freed here
     if (borrowed) {
       HostCache& hc = host_cache();
@@ -1120,6 +1129,19 @@ struct Factorizer {
   // ends 3 ms before the elimination does and the pair takes 0.3 ms less).
   cudaStream_t sym_hi = nullptr;
   int sym_overlaps = 0;
+  // Device-resident input: the host copy of the CSR pattern is only read by
+  // the host analysis.  While the device symbolic pass runs the levels the
+  // copy (117 MB on config 3: 2.1 ms of a 41 ms factorization when waited for
+  // up front) goes over a copy engine on its own stream; the hand-over to the
+  // host analysis and the end of the run wait for it.
+  cudaStream_t pat_s = nullptr;
+  cudaEvent_t ev_pat = nullptr;
+  bool pat_pending = false;
+  void pat_wait() {
+    if (!pat_pending) return;
+    pat_pending = false;
+    HCK(cudaEventSynchronize(ev_pat));
+  }
   cudaStream_t sym_stream() {
     if (!sym_s) {
       int lo = 0, hi = 0;
@@ -3680,6 +3702,7 @@ struct Factorizer {
   void dev_to_host() {
     if (!dev_mode) return;
     dev_mode = false;
+    pat_wait();  // the host analysis reads the pattern
     join_inv();
     // the active list compacted on the device (an O(N) host scan of the mask
     // was ~3 ms at the end of config 3's factorization)
@@ -3945,6 +3968,34 @@ struct Factorizer {
     HCK(cudaStreamSynchronize(s));
   }
 
+  // Starts the device-to-host copy of a device-resident pattern on pat_s;
+  // false (nothing started) when the pinned cache buffers are not available.
+  bool pat_async(const int64_t* ip, const int32_t* ix, const double* va, int64_t& nnz_out) {
+    HostCache& hc = host_cache();
+    int64_t* hip = (int64_t*)hc.pat_ip.get((N + 1) * sizeof(int64_t));
+    if (!hip) return false;
+    int64_t nz = 0;
+    HCK(cudaMemcpyAsync(&nz, ip + N, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    HCK(cudaStreamSynchronize(s));  // (also: the caller's arrays are complete on s)
+    int32_t* hix = (int32_t*)hc.pat_ix.get((size_t)std::max<int64_t>(nz, 1) * sizeof(int32_t));
+    if (!hix) return false;
+    if (!pat_s) {
+      HCK(cudaStreamCreateWithFlags(&pat_s, cudaStreamNonBlocking));
+      HCK(cudaEventCreateWithFlags(&ev_pat, cudaEventDisableTiming));
+    }
+    HCK(cudaMemcpyAsync(hip, ip, (N + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, pat_s));
+    HCK(cudaMemcpyAsync(hix, ix, nz * sizeof(int32_t), cudaMemcpyDeviceToHost, pat_s));
+    HCK(cudaEventRecord(ev_pat, pat_s));
+    pat_pending = true;
+    nnz_out = nz;
+    indptr = hip;
+    indices = hix;
+    d_indptr = const_cast<int64_t*>(ip);
+    d_indices = const_cast<int32_t*>(ix);
+    d_a0 = const_cast<double*>(va);
+    return true;
+  }
+
   void run(const int64_t* ip, const int32_t* ix, const double* va, int64_t nnz) {
     const double t0 = now_s();
     N = g.ndof();
@@ -3970,7 +4021,10 @@ struct Factorizer {
       ~StageOff() { g_stage = nullptr; }
     } stage_off;
     // A0: the symbolic analysis needs the pattern on the host
-    if (opt.input_on_device) {
+    const bool dev_first = opt.symbolic == HIFDE_SYMBOLIC_AUTO && !sharded() && !opt.verify && N > 0;
+    if (opt.input_on_device && dev_first && pat_async(ip, ix, va, nnz)) {
+      // (pattern copy in flight on pat_s)
+    } else if (opt.input_on_device) {
       HostCache& hc = host_cache();
       int64_t* hip = (int64_t*)hc.pat_ip.get((N + 1) * sizeof(int64_t));
       if (hip) {
@@ -4068,7 +4122,6 @@ struct Factorizer {
     // the host's active mask, active list and block membership: filled here
     // for the host analysis, or by dev_to_host when the device symbolic pass
     // runs the first levels (config 3: 3.7 ms of O(N) host fills saved)
-    const bool dev_first = opt.symbolic == HIFDE_SYMBOLIC_AUTO && !sharded() && !opt.verify && N > 0;
     if (!dev_first) {
       active.resize((size_t)N);
       act.resize((size_t)N);
