@@ -89,6 +89,13 @@ typedef struct hifde_options {
   int indptr_int32;     /* 1: indptr points to n + 1 int32 offsets (scipy's
                            default index type), host arrays only; widened
                            by the library instead of by the caller          */
+  int async_factor;     /* 1: hifde_factor returns the handle at once and the
+                           factorization runs on a library thread (one GPU
+                           only; the input arrays must stay valid until
+                           hifde_wait or the first call that uses the handle,
+                           which wait for it and report its status).  A
+                           hifde_solve of page-locked host right-hand sides
+                           uploads them while the factorization still runs. */
 } hifde_options_t;
 
 typedef struct hifde_factor hifde_factor_t;
@@ -271,6 +278,10 @@ typedef struct hifde_kernel_stat {
 int hifde_kernel_stats(const hifde_factor_t* f, int phase, hifde_kernel_stat_t* out, int64_t cap,
                        int64_t* count);
 void hifde_free(hifde_factor_t* f);
+/* Waits for an options.async_factor factorization; returns its status (0 at
+ * once for a handle that is complete).  Reference: none (factor_hifde,
+ * src/driver.py:212-225, returns when the factor is complete). */
+int hifde_wait(const hifde_factor_t* f);
 
 /* Thread-local message describing the last non-zero status. */
 const char* hifde_last_error(void);

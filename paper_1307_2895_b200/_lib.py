@@ -33,6 +33,7 @@ class Options(C.Structure):
         ("kernel_log", C.c_int),
         ("symbolic", C.c_int),
         ("indptr_int32", C.c_int),
+        ("async_factor", C.c_int),
     ]
 
 
@@ -93,7 +94,7 @@ class KernelStat(C.Structure):  # hifde_kernel_stat_t
 EXPORTS = [
     "hifde_version", "hifde_device_count", "hifde_default_options", "hifde_factor",
     "hifde_solve", "hifde_host_alloc", "hifde_host_free", "hifde_apply", "hifde_pcg", "hifde_level_records", "hifde_copy_arenas", "hifde_import", "hifde_power_norm", "hifde_get_info", "hifde_get_level", "hifde_last_launch_count", "hifde_kernel_stats",
-    "hifde_free", "hifde_last_error", "hifde_partition",
+    "hifde_free", "hifde_wait", "hifde_last_error", "hifde_partition",
     "hifde_comm_unique_id", "hifde_comm_init", "hifde_comm_emulated", "hifde_comm_host", "hifde_comm_info",
     "hifde_comm_free",
     "hifde_comm_last_error", "hifde_shard_owner", "hifde_shard_plan",
@@ -156,6 +157,8 @@ def load(path: str | None = None):
     lib.hifde_host_free.restype = C.c_int
     lib.hifde_free.argtypes = [C.c_void_p]
     lib.hifde_free.restype = None
+    lib.hifde_wait.argtypes = [C.c_void_p]
+    lib.hifde_wait.restype = C.c_int
     lib.hifde_last_error.restype = C.c_char_p
     lib.hifde_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                     C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]

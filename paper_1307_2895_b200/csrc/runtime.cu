@@ -406,7 +406,18 @@ struct hifde_factor {
   mutable bool whole = true;         // factor arena holds every record
   mutable std::mutex whole_m;
   mutable std::atomic<int64_t> solve_xfer_bytes{0};  // vector bytes this rank exchanged in solves
+  // options.async_factor: the factorization runs on `worker`; every entry
+  // point that reads the factor joins it first (async_done)
+  mutable std::thread worker;
+  mutable std::mutex async_m;
+  int async_status = 0;
+  std::string async_err;
+  std::atomic<int> inputs_issued{1};  // 0 until the worker has queued its own uploads
+  mutable std::atomic<int> async_pending{0};  // 1 from the worker's start to its join
+  std::mutex ev_m;
+  cudaEvent_t ev_inputs = nullptr;  // the matrix values' upload (while the factorization owns it)
   ~hifde_factor() {
+    if (worker.joinable()) worker.join();
     // stream-ordered frees: no device-wide synchronization on release
     cudaSetDevice(device);
     if (meta) cudaFreeAsync(meta, stream);
@@ -962,6 +973,10 @@ struct Factorizer {
     if (a0_s) {
       cudaStreamSynchronize(a0_s);
       cudaStreamDestroy(a0_s);
+      if (F) {
+        std::lock_guard<std::mutex> lk(F->ev_m);
+        F->ev_inputs = nullptr;
+      }
       if (ev_a0) cudaEventDestroy(ev_a0);
     }
     if (pat_s) {
@@ -4092,6 +4107,7 @@ struct Factorizer {
         }
         if (e != cudaSuccess) a0_err = e;
       });
+      hifde_factor_t* const Fq = F;
       a0_job = helper.post([=]() {
         cudaError_t e = cudaSetDevice(dev);
         if (e == cudaSuccess && big) {
@@ -4108,9 +4124,17 @@ struct Factorizer {
         // level's analysis meanwhile)
         if (e == cudaSuccess) e = cudaEventRecord(ev_v, vs);
         if (e != cudaSuccess) a0_err = e;
+        // (an asynchronous factorization: a waiting solve may queue its own
+        // uploads behind the matrix's now)
+        {
+          std::lock_guard<std::mutex> lk(Fq->ev_m);
+          Fq->ev_inputs = e == cudaSuccess ? ev_v : nullptr;
+        }
+        Fq->inputs_issued.store(1);
       });
     }
     PR.lap("A0");
+    if (!own_a0) F->inputs_issued.store(1);
     {  // borrow the persistent host buffers (returned at the end of run)
       HostCache& hc = host_cache();
       h_idx.swap(hc.idx_buf);
@@ -4759,8 +4783,13 @@ bool level0_bands(const hifde_factor_t* F, cudaStream_t s) {
 // is page-locked too (hifde_host_alloc blocks), else through pinned pieces
 // that host threads scatter.  Same result as one sweep of the whole block,
 // column by column.
-void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nrhs, cudaStream_t s) {
+// `ready` (may be empty) runs once every upload is queued and before the
+// factor is read: an options.async_factor factorization is waited for there,
+// so the right-hand sides cross PCIe while it still runs.
+void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nrhs, cudaStream_t s,
+                     const std::function<void()>& ready = {}) {
   const int64_t N = F->n;
+  const bool early = (bool)ready;
   // Two column chunks (one below 32 RHS): strided DMAs of 8-column (64 B)
   // row pieces run at 24-28 GB/s, 16-column pieces at 47-51 GB/s alone and
   // 71 GB/s both directions at once, 32-column pieces at 56-57 and 101 GB/s
@@ -4781,22 +4810,19 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
     HCK(cudaEventCreateWithFlags(&es[(size_t)c], cudaEventDisableTiming));
   }
   std::vector<double*> vb((size_t)nch, nullptr);
+  // (early: on the upload stream -- `s` is busy with the factorization, and an
+  // allocation ordered on it would hold the uploads back until it ends)
   for (int c = 0; c < nch; ++c)
-    HCK(cudaMallocAsync((void**)&vb[(size_t)c], (size_t)N * (c0[(size_t)c + 1] - c0[(size_t)c]) * sizeof(double), s));
+    HCK(cudaMallocAsync((void**)&vb[(size_t)c], (size_t)N * (c0[(size_t)c + 1] - c0[(size_t)c]) * sizeof(double),
+                        early ? sh : s));
   cudaEvent_t ealloc = nullptr;
   HCK(cudaEventCreateWithFlags(&ealloc, cudaEventDisableTiming));
-  HCK(cudaEventRecord(ealloc, s));
-  HCK(cudaStreamWaitEvent(sh, ealloc, 0));
-  // Banded level 0 (page-locked output, a level 0 of one-CTA records): each
-  // chunk uploads in row bands and its level-0 forward records run as the
-  // rows they read land; its level-0 backward runs in record bands and the
-  // rows they finish leave at once -- the first and last level of every
-  // chunk's sweep overlap its own transfers (config 3, 64 RHS: the last
-  // chunk's tail was sweep 8 + D2H 19 ms after its upload).
-  const bool banded = PinnedXfer::page_locked(x) && level0_bands(F, s);
+  if (!early) {
+    HCK(cudaEventRecord(ealloc, s));
+    HCK(cudaStreamWaitEvent(sh, ealloc, 0));
+  }
+  // every chunk's upload in kBands row bands, an event per band
   constexpr int kBands = 8;
-  std::vector<SweepBands> sb((size_t)nch);
-  std::vector<std::vector<std::pair<int64_t, int64_t>>> d2h_rows((size_t)nch);
   std::vector<cudaEvent_t> band_events;
   auto new_event = [&]() {
     cudaEvent_t e;
@@ -4804,6 +4830,71 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
     band_events.push_back(e);
     return e;
   };
+  std::vector<std::vector<cudaEvent_t>> up_ev((size_t)nch);
+  if (early) {  // the factorization's own uploads (the CSR) go first
+    while (!F->inputs_issued.load()) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    hifde_factor_t* Fm = const_cast<hifde_factor_t*>(F);
+    std::lock_guard<std::mutex> lk(Fm->ev_m);
+    if (Fm->ev_inputs) HCK(cudaStreamWaitEvent(sh, Fm->ev_inputs, 0));
+  }
+  // early: the factorization's own host-to-device copies (the task tables of
+  // the blocked levels) share the copy engine with these uploads, and with
+  // upload work always queued they were starved until the last band had
+  // gone (config 3: level 2's blocked elimination began 27 ms late; three
+  // 4 MB pieces in flight did the same).  So the bands go in 8 MB pieces,
+  // ONE in flight: this thread waits for a piece before it queues the next
+  // (it has nothing else to do until the factor is complete), and the gap
+  // lets the other stream's copy in.  Piece sizes from 4 to 64 MB measure
+  // the same step time.
+  cudaEvent_t fc[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (early)
+    for (auto& e : fc) e = new_event();
+  int64_t issued = 0;
+  for (int c = 0; c < nch; ++c) {
+    const int w = c0[(size_t)c + 1] - c0[(size_t)c];
+    const int64_t piece = early ? std::max<int64_t>(1024, ((int64_t)8 << 20) / ((int64_t)w * 8)) : N;
+    for (int k = 0; k < kBands; ++k) {
+      const int64_t r0 = N * k / kBands, r1 = k + 1 == kBands ? N : N * (k + 1) / kBands;
+      for (int64_t q0 = r0; q0 < r1; q0 += piece) {
+        const int64_t q1 = std::min(r1, q0 + piece);
+        if (early && issued >= 1) HCK(cudaEventSynchronize(fc[(issued - 1) & 3]));
+        HCK(cudaMemcpy2DAsync(vb[(size_t)c] + (size_t)q0 * w, (size_t)w * sizeof(double),
+                              b + (size_t)q0 * nrhs + c0[(size_t)c], (size_t)nrhs * sizeof(double),
+                              (size_t)w * sizeof(double), (size_t)(q1 - q0), cudaMemcpyHostToDevice, sh));
+        if (early) HCK(cudaEventRecord(fc[issued & 3], sh));
+        ++issued;
+      }
+      up_ev[(size_t)c].push_back(new_event());
+      HCK(cudaEventRecord(up_ev[(size_t)c].back(), sh));
+    }
+    HCK(cudaEventRecord(eh[(size_t)c], sh));
+  }
+  if (early) {
+    try {
+      ready();
+    } catch (...) {  // the factorization failed: nothing of it may be read
+      for (int c = 0; c < nch; ++c) cudaFreeAsync(vb[(size_t)c], sh);
+      cudaStreamSynchronize(sh);
+      for (cudaEvent_t e : band_events) cudaEventDestroy(e);
+      for (int c = 0; c < nch; ++c) {
+        cudaEventDestroy(eh[(size_t)c]);
+        cudaEventDestroy(es[(size_t)c]);
+      }
+      cudaEventDestroy(ealloc);
+      cudaStreamDestroy(sh);
+      cudaStreamDestroy(sd);
+      throw;
+    }
+  }
+  // Banded level 0 (page-locked output, a level 0 of one-CTA records): each
+  // chunk uploads in row bands and its level-0 forward records run as the
+  // rows they read land; its level-0 backward runs in record bands and the
+  // rows they finish leave at once -- the first and last level of every
+  // chunk's sweep overlap its own transfers (config 3, 64 RHS: the last
+  // chunk's tail was sweep 8 + D2H 19 ms after its upload).
+  const bool banded = PinnedXfer::page_locked(x) && level0_bands(F, s);
+  std::vector<SweepBands> sb((size_t)nch);
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> d2h_rows((size_t)nch);
   if (banded) {
     const int nrec = (int)F->band_pmax.size() - 1;
     for (int c = 0; c < nch; ++c) {
@@ -4817,7 +4908,7 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
         else
           while (j1 < nrec && F->band_pmax[(size_t)j1 + 1] < ub) ++j1;  // pmax[j1+1]: max cell DOF of records < j1+1
         B.fwd.emplace_back(j, j1);
-        B.fwd_wait.push_back(new_event());
+        B.fwd_wait.push_back(up_ev[(size_t)c][(size_t)k]);
         j = j1;
       }
       // backward: equal record bands; rows below the smallest cell DOF of the
@@ -4833,24 +4924,11 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
       }
     }
   }
-  for (int c = 0; c < nch; ++c) {  // every upload and sweep queued at once
+  for (int c = 0; c < nch; ++c) {  // every sweep queued at once (the uploads are)
     const int w = c0[(size_t)c + 1] - c0[(size_t)c];
     if (banded) {
-      for (int k = 0; k < kBands; ++k) {
-        const int64_t r0 = N * k / kBands, r1 = k + 1 == kBands ? N : N * (k + 1) / kBands;
-        if (r1 > r0)
-          HCK(cudaMemcpy2DAsync(vb[(size_t)c] + (size_t)r0 * w, (size_t)w * sizeof(double),
-                                b + (size_t)r0 * nrhs + c0[(size_t)c], (size_t)nrhs * sizeof(double),
-                                (size_t)w * sizeof(double), (size_t)(r1 - r0), cudaMemcpyHostToDevice, sh));
-        HCK(cudaEventRecord(sb[(size_t)c].fwd_wait[(size_t)k], sh));
-      }
-      HCK(cudaEventRecord(eh[(size_t)c], sh));
       solve_sweep(F, vb[(size_t)c], w, s, &sb[(size_t)c]);
     } else {
-      HCK(cudaMemcpy2DAsync(vb[(size_t)c], (size_t)w * sizeof(double), b + c0[(size_t)c],
-                            (size_t)nrhs * sizeof(double), (size_t)w * sizeof(double), (size_t)N,
-                            cudaMemcpyHostToDevice, sh));
-      HCK(cudaEventRecord(eh[(size_t)c], sh));
       HCK(cudaStreamWaitEvent(s, eh[(size_t)c], 0));
       solve_sweep(F, vb[(size_t)c], w, s);
     }
@@ -4892,6 +4970,7 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
   pinned_xfer().d2h_columns(x, nrhs, vb, c0, N, es, sd);
   for (int c = 0; c < nch; ++c) HCK(cudaFreeAsync(vb[(size_t)c], sd));
   HCK(cudaStreamSynchronize(sd));
+  for (cudaEvent_t e : band_events) cudaEventDestroy(e);
   for (int c = 0; c < nch; ++c) {
     cudaEventDestroy(eh[(size_t)c]);
     cudaEventDestroy(es[(size_t)c]);
@@ -4902,16 +4981,40 @@ void solve_pipelined(const hifde_factor_t* F, const double* b, double* x, int nr
   cudaStreamDestroy(sd);
 }
 
+// Joins an options.async_factor factorization; its status (and message).
+int async_done(const hifde_factor_t* f) {
+  std::lock_guard<std::mutex> lk(f->async_m);
+  if (f->worker.joinable()) f->worker.join();
+  f->async_pending.store(0);
+  if (f->async_status != HIFDE_OK) g_err = f->async_err;
+  return f->async_status;
+}
+
 void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, bool dev, cudaStream_t s) {
   const int64_t N = F->n;
   const size_t bytes = (size_t)N * nrhs * sizeof(double);
   std::unique_lock<std::mutex> klk(F->klog_m, std::defer_lock);
-  if (F->klog.on) {
-    klk.lock();
-    F->klog.clear(1);
-  }
   const bool disjoint = (const char*)x >= (const char*)b + bytes || (const char*)x + bytes <= (const char*)b;
-  if (!dev && !F->part && nrhs >= 16 && bytes >= ((size_t)64 << 20) && disjoint && PinnedXfer::page_locked(b)) {
+  const bool pipe_ok = !dev && nrhs >= 16 && bytes >= ((size_t)64 << 20) && disjoint && PinnedXfer::page_locked(b);
+  auto wait_factor = [&]() {  // an options.async_factor factorization (never sharded)
+    if (const int st = async_done(F)) throw Fail{st, F->async_err};
+  };
+  auto klog_begin = [&]() {
+    if (F->klog.on) {
+      klk.lock();
+      F->klog.clear(1);
+    }
+  };
+  if (pipe_ok && F->async_pending.load()) {  // uploads first, then wait for the factor
+    solve_pipelined(F, b, x, nrhs, s, [&]() {
+      wait_factor();
+      klog_begin();
+    });
+    return;
+  }
+  wait_factor();
+  klog_begin();
+  if (pipe_ok && !F->part) {
     solve_pipelined(F, b, x, nrhs, s);
     return;
   }
@@ -5195,6 +5298,54 @@ const char* hifde_last_error(void) { return g_err.c_str(); }
 
 int64_t hifde_last_launch_count(void) { return g_launches; }
 
+// The factorization proper (the calling thread's device is opt.device).
+static int factor_run(hifde_factor_t* F, const GridDesc& g, const hifde_options_t& o, const int64_t* indptr,
+                      const int32_t* indices, const double* vals, int64_t n, int nlevels) {
+  const hifde_options_t* opt = &o;
+  try {
+    std::lock_guard<std::mutex> lock(g_host_mutex);
+    HTRACE("locked");
+    Factorizer fz;
+    HTRACE("factorizer constructed");
+    fz.g = g;
+    fz.opt = *opt;
+    if (opt->variant == HIFDE_VARIANT_MF) {
+      fz.opt.variant = HIFDE_VARIANT_HIFDE;
+      fz.opt.skip_levels = nlevels;  // factor_mf == factor_hifde(skip_levels=L)
+      fz.opt.eps = 0.0;
+    }
+    if (fz.opt.exact_max_batches <= 0) fz.opt.exact_max_batches = 64;
+    fz.F = F;
+    fz.F_ = F;
+    fz.s = F->stream;
+    F->klog.on = opt->kernel_log != 0;
+    // int32 offsets from the caller: widened here on the host threads into
+    // a cached buffer (its pages stay mapped across factorizations)
+    const int64_t* ip64 = indptr;
+    if (opt->indptr_int32) {
+      if (opt->input_on_device) throw Fail{HIFDE_BADARG, "indptr_int32 needs host arrays"};
+      const int32_t* ip32 = reinterpret_cast<const int32_t*>(indptr);
+      int64_t* w = (int64_t*)host_cache().wide_ip.get((size_t)(n + 1) * sizeof(int64_t));
+      if (!w) throw Fail{HIFDE_CUDA, "page-locked host allocation failed"};
+      const int nth = n > (1 << 20) ? PinnedXfer::copy_threads() : 1;
+#pragma omp parallel for num_threads(nth) schedule(static)
+      for (int64_t i = 0; i <= n; ++i) w[i] = ip32[i];
+      ip64 = w;
+    }
+    const int64_t nnz = opt->input_on_device ? 0 : ip64[n];
+    const char* sample = getenv("HIFDE_SAMPLE");  // host sampling profile (diagnostics)
+    if (sample) host_sampler_start();
+    fz.run(ip64, indices, vals, nnz);
+    if (sample) host_sampler_stop(sample);
+  } catch (const Fail& f) {
+    return fail_to_status(f);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HIFDE_INTERNAL;
+  }
+  return HIFDE_OK;
+}
+
 int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* vals, int64_t n,
                  int dim, int n_grid, int m_leaf, int nlevels, const hifde_options_t* opt,
                  hifde_factor_t** out) {
@@ -5247,48 +5398,45 @@ int hifde_factor(const int64_t* indptr, const int32_t* indices, const double* va
       F->own_stream = true;
     }
     HTRACE("stream ready");
-    std::lock_guard<std::mutex> lock(g_host_mutex);
-    HTRACE("locked");
-    Factorizer fz;
-    HTRACE("factorizer constructed");
-    fz.g = g;
-    fz.opt = *opt;
-    if (opt->variant == HIFDE_VARIANT_MF) {
-      fz.opt.variant = HIFDE_VARIANT_HIFDE;
-      fz.opt.skip_levels = nlevels;  // factor_mf == factor_hifde(skip_levels=L)
-      fz.opt.eps = 0.0;
-    }
-    if (fz.opt.exact_max_batches <= 0) fz.opt.exact_max_batches = 64;
-    fz.F = F.get();
-    fz.F_ = F.get();
-    fz.s = F->stream;
-    F->klog.on = opt->kernel_log != 0;
-    // int32 offsets from the caller: widened here on the host threads into
-    // a cached buffer (its pages stay mapped across factorizations)
-    const int64_t* ip64 = indptr;
-    if (opt->indptr_int32) {
-      if (opt->input_on_device) throw Fail{HIFDE_BADARG, "indptr_int32 needs host arrays"};
-      const int32_t* ip32 = reinterpret_cast<const int32_t*>(indptr);
-      int64_t* w = (int64_t*)host_cache().wide_ip.get((size_t)(n + 1) * sizeof(int64_t));
-      if (!w) throw Fail{HIFDE_CUDA, "page-locked host allocation failed"};
-      const int nth = n > (1 << 20) ? PinnedXfer::copy_threads() : 1;
-#pragma omp parallel for num_threads(nth) schedule(static)
-      for (int64_t i = 0; i <= n; ++i) w[i] = ip32[i];
-      ip64 = w;
-    }
-    const int64_t nnz = opt->input_on_device ? 0 : ip64[n];
-    const char* sample = getenv("HIFDE_SAMPLE");  // host sampling profile (diagnostics)
-    if (sample) host_sampler_start();
-    fz.run(ip64, indices, vals, nnz);
-    if (sample) host_sampler_stop(sample);
   } catch (const Fail& f) {
     return fail_to_status(f);
   } catch (const std::exception& e) {
     g_err = e.what();
     return HIFDE_INTERNAL;
   }
+  // options.async_factor (one GPU): the factorization on a library thread;
+  // the handle goes back at once, async_done() joins
+  if (opt->async_factor && !(opt->comm && opt->comm->P > 1)) {
+    hifde_factor_t* Fp = F.get();
+    const hifde_options_t o = *opt;
+    Fp->inputs_issued.store(0);
+    Fp->async_pending.store(1);
+    Fp->worker = std::thread([=]() {
+      g_err.clear();
+      g_launches = 0;
+      int st = HIFDE_OK;
+      if (cudaSetDevice(o.device) != cudaSuccess) {
+        st = HIFDE_CUDA;
+        g_err = "cudaSetDevice failed";
+      } else {
+        st = factor_run(Fp, g, o, indptr, indices, vals, n, nlevels);
+      }
+      Fp->async_status = st;
+      Fp->async_err = g_err;
+      Fp->inputs_issued.store(1);
+    });
+    *out = F.release();
+    return HIFDE_OK;
+  }
+  const int st = factor_run(F.get(), g, *opt, indptr, indices, vals, n, nlevels);
+  if (st != HIFDE_OK) return st;
   *out = F.release();
   return HIFDE_OK;
+}
+
+int hifde_wait(const hifde_factor_t* f) {
+  if (!f) { g_err = "null argument"; return HIFDE_BADARG; }
+  return async_done(f);
 }
 
 int hifde_import(int64_t n, int dim, double eps, int nlevels, const double* tags, const int32_t* kinds,
@@ -5365,7 +5513,7 @@ int hifde_solve(const hifde_factor_t* f, const double* b, double* x, int64_t n, 
   try {
     HCK(cudaSetDevice(f->device));
     cudaStream_t s = stream ? (cudaStream_t)stream : f->stream;
-    do_solve(f, b, x, nrhs, device_ptrs != 0, s);
+    do_solve(f, b, x, nrhs, device_ptrs != 0, s);  // (waits for an asynchronous factorization itself)
   } catch (const Fail& e) {
     return fail_to_status(e);
   } catch (const std::exception& e) {
@@ -5380,6 +5528,7 @@ int hifde_apply(const hifde_factor_t* f, const double* x, double* y, int64_t n, 
   g_err.clear();
   g_launches = 0;
   if (!f || !x || !y) { g_err = "null argument"; return HIFDE_BADARG; }
+  if (const int st = async_done(f)) return st;
   if (n != f->n || nrhs < 1) { g_err = "vector shape mismatch"; return HIFDE_BADARG; }
   try {
     HCK(cudaSetDevice(f->device));
@@ -5399,6 +5548,8 @@ int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* ind
               int* iters, double* residual, int* converged) {
   g_err.clear();
   g_launches = 0;
+  if (f)
+    if (const int st = async_done(f)) return st;
   if (!f || !indptr || !indices || !vals || !b || !x || !iters || !residual || !converged) {
     g_err = "null argument";
     return HIFDE_BADARG;
@@ -5423,6 +5574,8 @@ int hifde_pcg(const hifde_factor_t* f, const int64_t* indptr, const int32_t* ind
 int hifde_level_records(const hifde_factor_t* f, int level, hifde_record_t* out, int64_t cap,
                         int64_t* count) {
   g_err.clear();
+  if (f)
+    if (const int st = async_done(f)) return st;
   if (!f || !count || level < 0 || level >= (int)f->levels.size()) { g_err = "bad level"; return HIFDE_BADARG; }
   auto& L = const_cast<hifde::LevelRec&>(f->levels[(size_t)level]);
   if (L.d_xrec && L.xrec.empty() && L.nxrec > 0) {  // device-symbolic level: copy its export view once
@@ -5446,6 +5599,7 @@ int hifde_level_records(const hifde_factor_t* f, int level, hifde_record_t* out,
 int hifde_copy_arenas(const hifde_factor_t* f, double* fac, int64_t fac_len, int32_t* idx, int64_t idx_len) {
   g_err.clear();
   if (!f) { g_err = "null factor"; return HIFDE_BADARG; }
+  if (const int st = async_done(f)) return st;
   if ((fac && fac_len != (int64_t)f->fac.n) || (idx && idx_len != (int64_t)f->idx.n)) {
     g_err = "arena length mismatch";
     return HIFDE_BADARG;
@@ -5472,6 +5626,8 @@ int hifde_power_norm(const hifde_factor_t* f, const int64_t* indptr, const int32
                      int* converged, int* iters) {
   g_err.clear();
   g_launches = 0;
+  if (f)
+    if (const int st = async_done(f)) return st;
   if (!f || !indptr || !indices || !vals || !x0 || !value || !converged || !iters || n != f->n || kind < 0 ||
       kind > 2 || max_iter < 1) {
     g_err = "bad power-iteration arguments";
@@ -5491,6 +5647,7 @@ int hifde_power_norm(const hifde_factor_t* f, const int64_t* indptr, const int32
 
 int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
   if (!f || !info) return HIFDE_BADARG;
+  if (const int st = async_done(f)) return st;
   std::memset(info, 0, sizeof *info);
   info->n = f->n;
   info->dim = f->dim;
@@ -5512,7 +5669,9 @@ int hifde_get_info(const hifde_factor_t* f, hifde_info_t* info) {
 }
 
 int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info) {
-  if (!f || !info || level < 0 || level >= (int)f->levels.size()) return HIFDE_BADARG;
+  if (!f || !info) return HIFDE_BADARG;
+  if (const int st = async_done(f)) return st;
+  if (level < 0 || level >= (int)f->levels.size()) return HIFDE_BADARG;
   const auto& L = f->levels[(size_t)level];
   info->tag = L.tag;
   info->kind = L.kind;
@@ -5532,6 +5691,7 @@ int hifde_get_level(const hifde_factor_t* f, int level, hifde_level_info_t* info
 int hifde_kernel_stats(const hifde_factor_t* f, int phase, hifde_kernel_stat_t* out, int64_t cap, int64_t* count) {
   g_err.clear();
   if (!f || !count || phase < 0 || phase > 1) { g_err = "bad arguments"; return HIFDE_BADARG; }
+  if (const int st = async_done(f)) return st;
   try {
     HCK(cudaSetDevice(f->device));
     std::lock_guard<std::mutex> lk(f->klog_m);

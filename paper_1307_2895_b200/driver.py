@@ -75,36 +75,72 @@ class GeneralizedLDL:
     algorithmic FLOP/byte counts.
     """
 
-    def __init__(self, handle: int, lib, spd: bool):
+    def __init__(self, handle: int, lib, spd: bool, pending=None):
         self._h = C.c_void_p(handle)
         self._lib = lib
+        self.spd = spd
+        self._info = None
+        # wait=False factorization still running on the library's thread:
+        # (n, dim, eps, input arrays kept alive); everything else is read
+        # from the finished factor on first use (wait())
+        self._pending = pending
+        if pending is None:
+            self._load()
+        else:
+            self.n, self.dim, self.eps = int(pending[0]), int(pending[1]), float(pending[2])
+
+    def wait(self) -> "GeneralizedLDL":
+        """Blocks until a ``wait=False`` factorization is complete and raises
+        what it raised (the reference's exceptions)."""
+        if self._info is None:
+            self._load()
+        return self
+
+    def _load(self):
+        lib = self._lib
+        code = lib.hifde_wait(self._h)
+        self._pending = None
+        if code:
+            _raise(lib, code)
         info = L.Info()
         lib.hifde_get_info(self._h, C.byref(info))
         self.n = int(info.n)
         self.dim = int(info.dim)
-        self.spd = spd
         self.eps = float(info.eps)
-        self.device_bytes = int(info.device_bytes)
-        self.level_info = []
+        self._device_bytes = int(info.device_bytes)
+        self._level_info = []
         for i in range(info.nlevels + 1):
             li = L.LevelInfo()
             lib.hifde_get_level(self._h, i, C.byref(li))
-            self.level_info.append({k: getattr(li, k) for k, _ in L.LevelInfo._fields_})
-        levels = self.level_info[:-1]
+            self._level_info.append({k: getattr(li, k) for k, _ in L.LevelInfo._fields_})
+        levels = self._level_info[:-1]
         trace = [(-1.0, self.n)] + [(d["tag"], int(d["active_after"])) for d in levels]
-        self.metrics = {
+        self._metrics = {
             "s_top": int(info.s_top),
             "active_trace": trace,
             "level_seconds": [(d["tag"], d["seconds"]) for d in levels],
             "m_f_bytes": int(info.m_f_bytes),
             "t_f_seconds": float(info.t_f_seconds),
             "skeleton_counts": [(d["tag"], int(d["nskel"])) for d in levels if d["kind"] == 1],
-            "factor_gflop": sum(d["gflop"] for d in self.level_info),
-            "factor_gbytes": sum(d["gbytes"] for d in self.level_info),
+            "factor_gflop": sum(d["gflop"] for d in self._level_info),
+            "factor_gbytes": sum(d["gbytes"] for d in self._level_info),
             "launches": int(lib.hifde_last_launch_count()),
             "nranks": int(info.nranks),
             "xfer_bytes": int(info.xfer_bytes),
         }
+        self._info = info
+
+    @property
+    def metrics(self) -> dict:
+        return self.wait()._metrics
+
+    @property
+    def level_info(self) -> list:
+        return self.wait()._level_info
+
+    @property
+    def device_bytes(self) -> int:
+        return self.wait()._device_bytes
 
     @property
     def handle(self) -> C.c_void_p:
@@ -145,6 +181,7 @@ class GeneralizedLDL:
         out = self._out(arr)
         if arr.size:
             code = self._lib.hifde_solve(self._h, arr.ctypes.data, out.ctypes.data, self.n, nrhs, 0, None)
+            self._pending = None  # (the solve has waited for a wait=False factorization)
             if code:
                 _raise(self._lib, code)
         return out
@@ -273,7 +310,7 @@ def pinned_csr(a) -> sp.csr_matrix:
 def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, verify: bool,
             order: str = "auto", exact_max_batches: int = 64, device: Optional[int] = None,
             stream: Optional[int] = None, comm=None, kernel_log: bool = False,
-            symbolic: str = "auto") -> GeneralizedLDL:
+            symbolic: str = "auto", wait: bool = True) -> GeneralizedLDL:
     lib = L.load()
     if not spd:
         raise NotImplementedError("indefinite (Bunch-Kaufman) mode is outside the GPU hot path")
@@ -300,12 +337,20 @@ def _factor(a, grid, eps: float, variant: int, spd: bool, skip_levels: int, veri
     opt.kernel_log = int(bool(kernel_log))
     opt.symbolic = L.SYMBOLIC[symbolic]  # "host": the host level analysis throughout (A/B tests)
     opt.indptr_int32 = int(ip32)
+    # wait=False: the call returns while the factorization runs on a library
+    # thread (one GPU); the first use of the factor waits for it and raises
+    # what it raised.  apply_inverse of a page-locked host block uploads the
+    # right-hand sides meanwhile.
+    pending = not wait and comm is None
+    opt.async_factor = int(pending)
     h = C.c_void_p()
     code = lib.hifde_factor(indptr.ctypes.data, indices.ctypes.data, data.ctypes.data, csr.shape[0],
                             int(grid.dim), int(grid.n), int(grid.m), int(grid.nlevels),
                             C.byref(opt), C.byref(h))
     if code:
         _raise(lib, code)
+    if pending:  # the input arrays must outlive the factorization
+        return GeneralizedLDL(h.value, lib, spd, pending=(csr.shape[0], grid.dim, eps, indptr, indices, data, csr))
     return GeneralizedLDL(h.value, lib, spd)
 
 

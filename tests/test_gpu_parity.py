@@ -683,3 +683,47 @@ def test_device_resident_csr_factor_bit_identical(dim, n, m, eps, variant, symbo
         assert np.array_equal(f_dev.apply_inverse(b), x_host)
         f_dev.close()
     f_host.close()
+
+
+def test_wait_false_factor_overlaps_and_matches():
+    """factor_hifde(..., wait=False) returns while the factorization runs on
+    a library thread; apply_inverse of a page-locked host block queues its
+    uploads at once and waits for the factor before the sweep.  Factor,
+    metrics and solutions are those of the blocking call, bit for bit; a
+    failing factorization raises the reference's exception at first use; a
+    pending factor can be closed without being waited for."""
+    import torch
+    g = H.build_grid(2, 512, 8)
+    a = H.assemble(g, H.gaussian_contrast_field(g, seed=2))
+    f0 = H.factor_hifde(a, g, 1e-6)
+    b = np.random.default_rng(3).standard_normal((g.ndof, 32))       # 67 MB: the pipelined host solve
+    bp = torch.from_numpy(b).pin_memory()
+    x0 = f0.apply_inverse(bp.numpy())
+    for _ in range(3):
+        f1 = H.factor_hifde(a, g, 1e-6, wait=False)
+        x1 = f1.apply_inverse(bp.numpy())                            # uploads first, then waits
+        assert np.array_equal(x0, x1)
+        assert f1.metrics["skeleton_counts"] == f0.metrics["skeleton_counts"]
+        assert f1.metrics["m_f_bytes"] == f0.metrics["m_f_bytes"]
+        del x1
+        f1.close()
+    f2 = H.factor_hifde(a, g, 1e-6, wait=False)
+    assert np.array_equal(f2.apply_inverse(b[:, :3]), f0.apply_inverse(b[:, :3]))  # plain path: waits first
+    f2.close()
+    f3 = H.factor_hifde(a, g, 1e-6, wait=False)
+    assert f3.wait().metrics["s_top"] == f0.metrics["s_top"]
+    f3.close()
+    H.factor_hifde(a, g, 1e-6, wait=False).close()                   # never waited for
+    gs = H.build_grid(2, 4, 2)
+    fld = H.constant_field(gs)
+    fld.b[0, 0] = -1e4
+    bad = H.assemble(gs, fld)
+    fb = H.factor_mf(bad, gs, wait=False)
+    with pytest.raises(H.IndefiniteBlockError):
+        fb.apply_inverse(np.ones(gs.ndof))
+    fb.close()
+    fb = H.factor_mf(bad, gs, wait=False)
+    with pytest.raises(H.IndefiniteBlockError):
+        fb.wait()
+    fb.close()
+    f0.close()

@@ -8,13 +8,14 @@ dev = torch.device("cuda", 0)
 torch.cuda.set_device(0)
 stream = torch.cuda.Stream(device=dev)
 r = bench.Runner(3, dev, 0, stream, None, 1, 0)
-nogc = len(sys.argv) > 1 and sys.argv[1] == "nogc"
+nogc = "nogc" in sys.argv[1:]
+wait = "async" not in sys.argv[1:]  # async: factor_hifde(..., wait=False)
 if nogc:
     gc.disable()
 for i in range(12):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    fe = r.fac(r.a_pin, r.g, r.eps, stream=stream.cuda_stream, device=0)
+    fe = r.fac(r.a_pin, r.g, r.eps, stream=stream.cuda_stream, device=0, wait=wait, kernel_log=bool(os.environ.get("HIFDE_PROFILE")))
     t1 = time.perf_counter()
     x = fe.apply_inverse(r.b_pin.numpy())
     t2 = time.perf_counter()
