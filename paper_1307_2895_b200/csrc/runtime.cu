@@ -4505,12 +4505,14 @@ void solve_sweep(const hifde_factor_t* F, double* v, int nrhs, cudaStream_t s, c
   // fine elimination levels: the single-load-phase kernels
   constexpr int small_max_rhs = 64, small_max_n = 96;
   constexpr size_t small_max_smem = kSmemCapBytes;  // (200 KB kept config 3 level 3, 208 KB, on the streaming kernels: 2x slower)
+  // (HIFDE_NO_SOLVE_SMALL: the general record kernels instead -- the tests' A/B of the two)
+  static const bool no_small = getenv("HIFDE_NO_SOLVE_SMALL") != nullptr;
   auto small_path = [&](const LevelRec& L) {
-    return L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+    return !no_small && L.kind == 0 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
            L.max_nq <= 2 * small_max_n && solve_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   auto small_skel = [&](const LevelRec& L) {
-    return L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
+    return !no_small && L.kind == 1 && nrhs >= 2 && nrhs <= small_max_rhs && L.max_nc <= small_max_n &&
            L.max_nq <= 2 * small_max_n && solve_skel_small_smem(L.max_nc, L.max_nq, nrhs) <= small_max_smem;
   };
   const int32_t* idx = F->idx.p;
