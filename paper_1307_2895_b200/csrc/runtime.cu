@@ -5007,17 +5007,31 @@ void do_solve(const hifde_factor_t* F, const double* b, double* x, int nrhs, boo
       F->klog.clear(1);
     }
   };
+  auto solve_timeline = [&]() {  // HIFDE_PROFILE: the solve's logged launches on the factorization's clock
+    if (!getenv("HIFDE_PROFILE") || !F->klog.on || F->klog.v.empty()) return;
+    cudaDeviceSynchronize();
+    const cudaEvent_t t0e = F->klog.v.front().e0;
+    for (const auto& E : F->klog.v) {
+      if (E.phase != 1) continue;
+      float a = 0.f, c = 0.f;
+      cudaEventElapsedTime(&a, t0e, E.e0);
+      cudaEventElapsedTime(&c, t0e, E.e1);
+      fprintf(stderr, "[hifde] tl1 %8.3f %8.3f %7.3f  %-24s tag %.3f\n", a, c, c - a, E.name.c_str(), E.tag);
+    }
+  };
   if (pipe_ok && F->async_pending.load()) {  // uploads first, then wait for the factor
     solve_pipelined(F, b, x, nrhs, s, [&]() {
       wait_factor();
       klog_begin();
     });
+    solve_timeline();
     return;
   }
   wait_factor();
   klog_begin();
   if (pipe_ok && !F->part) {
     solve_pipelined(F, b, x, nrhs, s);
+    solve_timeline();
     return;
   }
   double* v = nullptr;
