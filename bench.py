@@ -466,8 +466,8 @@ def run_gpu(args, world, rank, local):
             dist.barrier()
         # e2e: the public calls with wait=False on one GPU (upload of the
         # right-hand sides under the factorization); the blocking calls beside it
-        t_e2e_block = R.e2e(max(1, min(args.steps, 5)), dist, wait=True)
-        t_e2e = R.e2e(max(1, min(args.steps, 5)), dist, wait=False) if world == 1 else t_e2e_block
+        t_e2e_block = R.e2e(max(1, min(args.steps, 10)), dist, wait=True)
+        t_e2e = R.e2e(max(1, min(args.steps, 10)), dist, wait=False) if world == 1 else t_e2e_block
         if world > 1:
             R.e2e_steps_ms = R.e2e_blocking_steps_ms
         extra = None
@@ -506,7 +506,7 @@ def run_gpu(args, world, rank, local):
                         "RHS in page-locked memory (pinned_csr / pin_memory, outside the timed region); wait=False "
                         "lets apply_inverse upload the right-hand sides while the factorization runs on the "
                         "library's thread (one GPU; results identical); blocking_value: the same two calls with "
-                        f"the default wait=True; mean of {max(1, min(args.steps, 5))} steps after one warm-up",
+                        f"the default wait=True; mean of {max(1, min(args.steps, 10))} steps after one warm-up",
                 "steps_ms": R.e2e_steps_ms,
                 "blocking_value": N / t_e2e_block, "blocking_steps_ms": R.e2e_blocking_steps_ms,
                 "resid": getattr(R, "e2e_resid", None)},

@@ -12,7 +12,7 @@ nogc = "nogc" in sys.argv[1:]
 wait = "async" not in sys.argv[1:]  # async: factor_hifde(..., wait=False)
 if nogc:
     gc.disable()
-for i in range(12):
+for i in range(int(os.environ.get("E2E_STEPS", "12"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     fe = r.fac(r.a_pin, r.g, r.eps, stream=stream.cuda_stream, device=0, wait=wait, kernel_log=bool(os.environ.get("HIFDE_PROFILE")))
