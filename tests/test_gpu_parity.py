@@ -714,6 +714,15 @@ def test_wait_false_factor_overlaps_and_matches():
     assert f3.wait().metrics["s_top"] == f0.metrics["s_top"]
     f3.close()
     H.factor_hifde(a, g, 1e-6, wait=False).close()                   # never waited for
+    g3 = H.build_grid(3, 32, 4)                                       # hifde3x: hand-over to the host analysis
+    a3 = H.assemble(g3, H.gaussian_contrast_field(g3, seed=1))
+    b3 = np.random.default_rng(4).standard_normal((g3.ndof, 4))
+    f3 = H.factor_hifde3x(a3, g3, 1e-3)
+    f3a = H.factor_hifde3x(a3, g3, 1e-3, wait=False)
+    assert np.array_equal(f3a.apply_inverse(b3), f3.apply_inverse(b3))
+    assert f3a.metrics["skeleton_counts"] == f3.metrics["skeleton_counts"]
+    f3a.close()
+    f3.close()
     gs = H.build_grid(2, 4, 2)
     fld = H.constant_field(gs)
     fld.b[0, 0] = -1e4
