@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu --set full captures of several kernels of one config-3 factor + solve:
-#   tools/ncu_multi.sh TAG "name:regex[:skip]" ...
+#   [CFG=5] tools/ncu_multi.sh TAG "name:regex[:skip]" ...
 tag=$1; shift
 mkdir -p gpurun_out
 for spec in "$@"; do
@@ -8,5 +8,5 @@ for spec in "$@"; do
   [ "$rest" != "$kre" ] && skip=${rest#*:}
   timeout 600 /usr/local/cuda/bin/ncu --set full --import-source on --clock-control none \
     -k "regex:$kre" --launch-skip "$skip" --launch-count 1 -f -o "gpurun_out/${tag}_${name}" \
-    python tools/one_step.py 3 > "gpurun_out/${tag}_${name}.log" 2>&1
+    python tools/one_step.py "${CFG:-3}" > "gpurun_out/${tag}_${name}.log" 2>&1
 done
